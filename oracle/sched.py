@@ -1,0 +1,245 @@
+"""Tail-batching round schedule.  TEST INFRASTRUCTURE
+ONLY (see oracle/__init__.py).  Integer-only; compared bit-exactly.
+
+Paper: a short round "launches more than P0 prompts but retains only the
+first P0 that finish"; prompts aborted during the
+speculative short round go to a FIFO long-prompt queue and "once the queue
+reaches size P0" they run in a long round "where speculative execution is
+disabled", "capped at the same maximum".
+SPEC: plan_round / on_prompt_accepted / run_long_round.
+
+Readings: time is the logical decode step (Z1); a prompt
+completes when all G responses finished (Z2); reaching the cap without EOS
+aborts the response in a short round and truncates-and-retains it in a long
+round (Z3); a round with fewer than `target` completable prompts ends when
+no sequence is live (Z4); deferred prompts are re-rolled from scratch in the
+long round, trace attempt 1 (Z5); the queue is FIFO and deferrals enter in
+submission order (Z7); n_submit = ceil(eta * P0) (Z8).
+
+Sequence s = (prompt i, response j) has slot i*G + j; its trace length
+L[i][j] >= 1 counts the EOS token (Z16); token 1 is sampled from the prefill
+logits; e_s = min(L_s, cap).
+"""
+from dataclasses import dataclass, field
+from fractions import Fraction
+from collections import deque
+import math
+import numpy as np
+
+SHORT, LONG = 0, 1
+FINISHED, CAPPED, ABORTED = 1, 2, 3
+
+
+@dataclass
+class Round:
+    kind: int
+    t_end: int
+    accepted: list            # prompt indices, acceptance order
+    deferred: list            # prompt indices, submission order
+    underfilled: bool
+    outcome: np.ndarray       # [n, G] FINISHED / CAPPED / ABORTED
+    retained_len: np.ndarray  # [n, G] length of retained responses, 0 if dropped
+    steps: list = field(default_factory=list)   # per-step records (optional)
+
+
+def _e(L, cap):
+    return np.minimum(np.asarray(L, np.int64), cap)
+
+
+def closed_form(L, cap, target, kind, with_steps=False):
+    """The schedule written out directly from the definition.
+
+    SHORT: T_i = max_j L_ij if every L_ij <= cap else inf; pi = prompts sorted
+    by (T_i, i); A = first min(target, #finite) of pi; t_end = T_pi[target-1]
+    if #finite >= target else max_s e_s.  LONG: every prompt accepted, in
+    (max_j e_ij, i) order; t_end = max e."""
+    L = np.asarray(L, np.int64)
+    n, G = L.shape
+    e = _e(L, cap)
+    if kind == SHORT:
+        ok = np.all(L <= cap, axis=1)
+        T = np.where(ok, L.max(axis=1), np.iinfo(np.int64).max)
+    else:
+        T = e.max(axis=1)
+    order = sorted(range(n), key=lambda i: (T[i], i))
+    n_fin = int(np.sum(T < np.iinfo(np.int64).max))
+    if kind == LONG:
+        target = n
+    n_acc = min(target, n_fin)
+    accepted = order[:n_acc]
+    underfilled = n_fin < target
+    t_end = int(T[order[target - 1]]) if not underfilled else int(e.max())
+    deferred = sorted(set(range(n)) - set(accepted))
+    outcome = np.where(L <= cap, FINISHED, CAPPED)
+    outcome = np.where(e > t_end, ABORTED, outcome)
+    retained = np.zeros_like(L)
+    for i in accepted:
+        retained[i] = e[i]
+    r = Round(kind, t_end, accepted, deferred, bool(underfilled), outcome.astype(np.int32), retained)
+    if with_steps:
+        r.steps = closed_form_steps(L, cap, target, kind, t_end, T, order)
+    return r
+
+
+def closed_form_steps(L, cap, target, kind, t_end, T, order):
+    """Per-step records for t = 1..t_end: live slots decoded at step t
+    (e_s >= t, stable slot order), slots finishing at t, c_i(t), accepted(t),
+    done(t)."""
+    L = np.asarray(L, np.int64)
+    n, G = L.shape
+    e = _e(L, cap).reshape(-1)
+    fin_ok = (L.reshape(-1) <= cap) | (kind == LONG)
+    rank = {p: k for k, p in enumerate(order)}
+    if kind == LONG:
+        target = n
+    steps = []
+    for t in range(1, t_end + 1):
+        live = np.nonzero(e >= t)[0].astype(np.int32)
+        ending = np.nonzero(e == t)[0].astype(np.int32)
+        c = np.sum(((e <= t) & fin_ok).reshape(n, G), axis=1).astype(np.int32)
+        acc = min(target, sum(1 for p in range(n) if T[p] <= t and rank[p] < target))
+        steps.append(dict(t=t, live=live, ending=ending, counts=c, accepted=acc,
+                          done=int(acc == target or t == int(e.max()))))
+    return steps
+
+
+def step_loop(L, cap, target, kind, with_steps=False):
+    """Literal step-by-step simulation of the round (the brute-force pin of
+    `closed_form`): every live sequence emits token t; it ends on EOS (t == L)
+    or at the cap; completed prompts are admitted in index order until
+    `target` are accepted or nothing is live."""
+    L = np.asarray(L, np.int64)
+    n, G = L.shape
+    if kind == LONG:
+        target = n
+    live = list(range(n * G))
+    cnt = [0] * n
+    accepted, steps = [], []
+    outcome = np.zeros((n, G), np.int32)
+    t = 0
+    while True:
+        t += 1
+        decoded = list(live)
+        ending, completed = [], []
+        for s in decoded:
+            i, j = divmod(s, G)
+            if t == L[i, j]:                       # token t is EOS
+                outcome[i, j] = FINISHED
+                ending.append(s)
+                cnt[i] += 1
+                if cnt[i] == G:
+                    completed.append(i)
+            elif t == cap:                         # length cap reached
+                outcome[i, j] = CAPPED
+                ending.append(s)
+                if kind == LONG:
+                    cnt[i] += 1
+                    if cnt[i] == G:
+                        completed.append(i)
+        for i in sorted(completed):
+            if len(accepted) < target:
+                accepted.append(i)
+        live = [s for s in decoded if s not in set(ending)]
+        done = len(accepted) == target or not live
+        if with_steps:
+            steps.append(dict(t=t, live=np.array(decoded, np.int32), ending=np.array(ending, np.int32),
+                              counts=np.array(cnt, np.int32), accepted=len(accepted), done=int(done)))
+        if done:
+            break
+    for s in live:
+        outcome[s // G, s % G] = ABORTED
+    deferred = [i for i in range(n) if i not in accepted]
+    retained = np.zeros((n, G), np.int64)
+    for i in accepted:
+        retained[i] = np.minimum(L[i], cap)
+    r = Round(kind, t, accepted, deferred, len(accepted) < target, outcome, retained, steps)
+    return r
+
+
+# ---------------------------------------------------------------- DP (C3)
+
+def partition(n, world):
+    """Contiguous ranges of global prompt indices per rank (first n % world
+    ranks get one more)."""
+    base, extra = divmod(n, world)
+    out, lo = [], 0
+    for r in range(world):
+        hi = lo + base + (1 if r < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def dp_protocol(L, cap, target, kind, world):
+    """The per-step DP cutoff exchange: each rank counts
+    k_r(t), the prompts of its range completing at step t; after an
+    all-gather rank r admits min(k_r, max(0, target - acc - sum_{r'<r} k_r'))
+    of them, lowest index first.  Returns (t_end, accepted in acceptance
+    order, per-rank live counts per step)."""
+    L = np.asarray(L, np.int64)
+    n, G = L.shape
+    if kind == LONG:
+        target = n
+    e = _e(L, cap)
+    fin_ok = (L <= cap) | (kind == LONG)
+    parts = partition(n, world)
+    acc, accepted, t = 0, [], 0
+    emax = int(e.max())
+    live_counts = []
+    while True:
+        t += 1
+        ks, comp = [], []
+        for lo, hi in parts:
+            c = [i for i in range(lo, hi) if np.all(fin_ok[i]) and int(e[i].max()) == t]
+            comp.append(c)
+            ks.append(len(c))
+        live_counts.append([int(np.sum(e[lo:hi] >= t)) for lo, hi in parts])
+        before = acc
+        for r in range(world):
+            take = min(ks[r], max(0, target - before - sum(ks[:r])))
+            accepted.extend(comp[r][:take])
+            acc += take
+        if acc == target or t >= emax:
+            return t, accepted, live_counts
+
+
+# ---------------------------------------------------------------- planner
+
+def n_launch(P0, eta):
+    """ceil(eta * P0) in exact rational arithmetic."""
+    return math.ceil(Fraction(eta).limit_denominator(1000) * P0)
+
+
+def plan_round(queue_len, P0, eta, tail_batching=True):
+    """LONG over the first P0 queued prompts when |Q| >= P0, else a
+    SHORT round launching ceil(eta*P0) fresh prompts with target P0;
+    BASELINE (plain synchronous rollout) when tail batching is off.
+    Returns (kind_name, n_prompts, target)."""
+    if not tail_batching:
+        return ("baseline", P0, P0)
+    if queue_len >= P0:
+        return ("long", P0, P0)
+    return ("short", n_launch(P0, eta), P0)
+
+
+def simulate(trace, n_rounds, P0, eta, G, short_cap, long_cap, tail_batching=True, n_launch_override=None):
+    """Run `n_rounds` RL steps.  trace [n_prompts_total, 2, G] (attempt 0:
+    first submission, attempt 1: long-round re-roll).  Returns a list of
+    dicts {kind, ids, round: Round, queue_after}."""
+    queue, nxt, out = deque(), 0, []
+    for _ in range(n_rounds):
+        kind, n, target = plan_round(len(queue), P0, eta, tail_batching)
+        if kind == "short" and n_launch_override:
+            n = n_launch_override
+        if kind == "long":
+            ids = [queue.popleft() for _ in range(P0)]
+            r = closed_form(trace[ids, 1, :G], long_cap, target, LONG)
+        elif kind == "baseline":
+            ids = list(range(nxt, nxt + n)); nxt += n
+            r = closed_form(trace[ids, 0, :G], long_cap, n, LONG)
+        else:
+            ids = list(range(nxt, nxt + n)); nxt += n
+            r = closed_form(trace[ids, 0, :G], short_cap, target, SHORT)
+            queue.extend(ids[i] for i in r.deferred)
+        out.append(dict(kind=kind, ids=ids, round=r, queue_after=list(queue)))
+    return out

@@ -1,0 +1,154 @@
+"""Pins of oracle/sched.py: brute force (the literal step loop) against the
+closed form on every tiny trace, SPEC worked examples, special
+cases, invariants and DP-split invariance."""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import sched as X
+from synth.gen import length_trace
+
+
+def _cmp(a, b):
+    assert a.t_end == b.t_end
+    assert a.accepted == b.accepted
+    assert a.deferred == b.deferred
+    assert a.underfilled == b.underfilled
+    assert np.array_equal(a.outcome, b.outcome)
+    assert np.array_equal(a.retained_len, b.retained_len)
+
+
+def test_brute_force_equals_closed_form_all_tiny_traces():
+    """3 prompts x G=2 x lengths 1..4 (4^6 traces), every target and cap."""
+    n, G = 3, 2
+    for flat in itertools.product(range(1, 5), repeat=n * G):
+        L = np.array(flat).reshape(n, G)
+        for cap in range(1, 5):
+            _cmp(X.step_loop(L, cap, n, X.LONG), X.closed_form(L, cap, n, X.LONG))
+            for target in range(1, n + 1):
+                _cmp(X.step_loop(L, cap, target, X.SHORT), X.closed_form(L, cap, target, X.SHORT))
+
+
+def test_per_step_records_match():
+    rng = np.random.default_rng(5)
+    for _ in range(30):
+        L = rng.integers(1, 40, size=(6, 4))
+        for kind, target in ((X.SHORT, 4), (X.LONG, 6)):
+            a = X.step_loop(L, 30, target, kind, with_steps=True)
+            b = X.closed_form(L, 30, target, kind, with_steps=True)
+            assert len(a.steps) == len(b.steps) == a.t_end
+            for sa, sb in zip(a.steps, b.steps):
+                assert np.array_equal(sa["live"], sb["live"])
+                assert np.array_equal(np.sort(sa["ending"]), sb["ending"])
+                assert np.array_equal(sa["counts"], sb["counts"])
+                assert sa["accepted"] == sb["accepted"] and sa["done"] == sb["done"]
+
+
+def test_spec_plan_round_examples():
+    assert X.plan_round(0, 128, 1.25) == ("short", 160, 128)
+    assert X.n_launch(8, 1.25) == 10                                   # S:277 responses
+    assert X.plan_round(128, 128, 1.25) == ("long", 128, 128)
+    assert X.plan_round(0, 128, 1.25, tail_batching=False) == ("baseline", 128, 128)
+    assert X.n_launch(25, 1.25) == 32
+
+
+def test_spec_acceptance_defers_32_of_160():
+    rng = np.random.default_rng(0)
+    L = rng.integers(1, 1000, size=(160, 8))
+    r = X.closed_form(L, 100000, 128, X.SHORT)
+    assert len(r.accepted) == 128 and len(r.deferred) == 32
+
+
+def test_uniform_lengths_accept_lowest_indices():
+    L = np.full((10, 3), 7)
+    r = X.closed_form(L, 100, 8, X.SHORT)
+    assert r.accepted == list(range(8)) and r.deferred == [8, 9]       # S:296 (ties -> index)
+    assert r.t_end == 7
+
+
+def test_eta_one_no_deferrals():
+    rng = np.random.default_rng(1)
+    L = rng.integers(1, 50, size=(12, 4))
+    r = X.closed_form(L, 100, 12, X.SHORT)
+    assert r.deferred == [] and r.t_end == L.max()
+
+
+def test_target_all_is_plain_sync_rollout():
+    rng = np.random.default_rng(2)
+    L = rng.integers(1, 50, size=(8, 4))
+    r = X.closed_form(L, 10_000, 8, X.SHORT)
+    assert r.t_end == L.max()
+
+
+def test_G1_reduces_to_order_statistic():
+    L = np.array([[9], [3], [7], [3], [12]])
+    r = X.closed_form(L, 100, 3, X.SHORT)
+    assert r.accepted == [1, 3, 2] and r.t_end == 7
+
+
+def test_underfilled_round():
+    L = np.array([[5, 200], [300, 3], [4, 4]])
+    r = X.closed_form(L, 100, 2, X.SHORT)
+    assert r.underfilled and r.accepted == [2] and r.t_end == 100
+
+
+def test_long_round_truncates_and_retains():
+    L = np.array([[5, 700], [10, 20]])
+    r = X.closed_form(L, 512, 2, X.LONG)
+    assert r.accepted == [1, 0] and r.t_end == 512
+    assert r.retained_len.tolist() == [[5, 512], [10, 20]]
+    assert r.outcome[0, 1] == X.CAPPED
+
+
+def test_no_short_response_exceeds_cap_and_retained_count_exact():
+    tr = length_trace(400, 8, 5.0, 0.6, 0.85, 4000, 9)
+    for res in X.simulate(tr, 10, 25, 1.25, 8, 600, 4000):
+        r = res["round"]
+        if res["kind"] == "short":
+            assert r.retained_len.max() <= 600
+            if not r.underfilled:
+                assert (r.retained_len > 0).sum() == 25 * 8
+        assert np.all(r.retained_len[r.outcome == X.ABORTED] == 0)
+
+
+def test_periodicity_four_short_one_long():
+    """P:572-574 / S:685: with 32 deferrals per short round (P0=128, eta=1.25)
+    a long round follows every four short rounds."""
+    tr = length_trace(160 * 20, 8, 6.0, 0.6, 0.85, 16384, 2)
+    out = X.simulate(tr, 20, 128, 1.25, 8, 8192, 8192)
+    kinds = "".join(o["kind"][0].upper() for o in out)
+    assert all(len(o["round"].deferred) == 32 for o in out if o["kind"] == "short")
+    assert kinds == "SSSSL" * 4
+
+
+def test_coverage_no_starvation_and_no_resubmission():
+    tr = length_trace(2000, 4, 4.0, 0.6, 0.85, 2000, 11)
+    out = X.simulate(tr, 40, 16, 1.25, 4, 256, 2000)
+    seen_short, trained = set(), []
+    for o in out:
+        if o["kind"] == "short":
+            assert not (set(o["ids"]) & seen_short)                      # never resubmitted
+            seen_short |= set(o["ids"])
+        r = o["round"]
+        trained += [o["ids"][i] for i in r.accepted]
+    queue = set(out[-1]["queue_after"])
+    # every submitted prompt is either trained once or still queued
+    assert sorted(trained + sorted(queue)) == sorted(seen_short)
+    assert len(set(trained)) == len(trained)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_dp_protocol_matches_single_rank(world):
+    rng = np.random.default_rng(world)
+    for _ in range(20):
+        n = int(rng.integers(world, 40))
+        L = rng.integers(1, 60, size=(n, 4))
+        target = int(rng.integers(1, n + 1))
+        ref = X.closed_form(L, 50, target, X.SHORT)
+        t_end, acc, _ = X.dp_protocol(L, 50, target, X.SHORT, world)
+        assert t_end == ref.t_end and acc == ref.accepted
+
+
+def test_partition_contiguous():
+    assert X.partition(10, 4) == [(0, 3), (3, 6), (6, 8), (8, 10)]
