@@ -1,0 +1,212 @@
+/*
+ * rollpacker.h -- C ABI of the B200-native tail-batching rollout path
+ * (RollPacker, arXiv 2509.21009).  Library: librollpacker.so (sm_100a).
+ *
+ * The path is the rollout stage of synchronous GRPO-style RL under tail
+ * batching:
+ *   - a SHORT round launches more prompts than it keeps ("launches more than
+ *     P0 prompts but retains only the first P0 that finish"),
+ *     decodes G responses per prompt under a per-round length cap, and stops
+ *     once `target` prompts have all G responses finished;
+ *   - prompts not accepted are deferred to a FIFO long-prompt queue ("added to
+ *     a long-prompt queue");
+ *   - a LONG round decodes queued prompts with speculation disabled, every
+ *     response retained and truncated at the cap ("capped at the same
+ *     maximum").
+ * Paper notation: P0 = target prompts, R0 = G responses per prompt, eta =
+ * over-provisioning (n_prompts = ceil(eta * P0)).
+ *
+ * Conventions
+ *   - Every call returns 0 (RP_OK) or a negative RP_E* code; rp_last_error()
+ *     gives a one-line reason.  No C++ exception crosses the ABI.
+ *   - Device memory (weights, KV pool, workspace) is allocated by the caller
+ *     (PyTorch) and BORROWED for the lifetime of the context.  Host arrays
+ *     passed to calls are copied before the call returns (except where noted).
+ *   - A context is bound to one CUDA device and one stream; it is
+ *     thread-compatible, not thread-safe (one context per rank / thread).
+ *   - Data-parallel short rounds (world > 1): every rank submits the SAME
+ *     full prompt list; rank r decodes the contiguous slice of prompt indices
+ *     partition(n, world)[r] and the per-step acceptance cutoff is exchanged
+ *     with an NCCL all-gather.  Membership (which prompts are
+ *     accepted / deferred) is identical for every world size.
+ */
+#ifndef ROLLPACKER_H
+#define ROLLPACKER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ error codes */
+#define RP_OK 0
+#define RP_EINVAL -1     /* bad argument (the message names the field)          */
+#define RP_EBUSY -2      /* a round is active: submit while not collected        */
+#define RP_ESTATE -3     /* wrong state: step/collect without an active round    */
+#define RP_ENOMEM_KV -4  /* KV page pool exhausted (no preemption, reading Z17)  */
+#define RP_ECUDA -5      /* CUDA runtime / driver error                          */
+#define RP_ENCCL -6      /* NCCL error                                           */
+#define RP_ENOSPC -7     /* caller buffer too small / capacity exceeded          */
+
+/* ----------------------------------------------------------- round flags */
+#define RP_SHORT 0       /* speculative short round: stop at `target` accepted   */
+#define RP_LONG 1        /* long round: target must equal n_prompts, no aborts   */
+#define RP_TRACE 4       /* trace mode: EOS masked before and forced at L (Z15)  */
+
+/* ------------------------------------------------- finish codes (rp_response) */
+#define RP_FINISH_EOS 1  /* ended with EOS (natural or trace-forced)             */
+#define RP_FINISH_CAP 2  /* truncated at the cap (long rounds only)              */
+
+/* Qwen2-shaped decoder ("Qwen2.5 family").  Weights are
+ * the random-init formula of DESIGN.md reading Z12, generated on device from
+ * weight_seed by rp_init_model.  Constraints: head_dim in {64, 128};
+ * d_model, n_heads*head_dim and d_ff multiples of 128; vocab multiple of 128;
+ * n_heads % n_kv_heads == 0 and n_heads / n_kv_heads <= 8. */
+typedef struct {
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab, eos_id;
+  int32_t qkv_bias;          /* 1 = q/k/v projections carry a bias (Qwen2)     */
+  float rope_theta, rms_eps;
+  uint64_t weight_seed;
+} rp_model_desc;
+
+typedef struct {
+  void* weights;             /* device, >= rp_query_sizes().weights_bytes      */
+  size_t weights_bytes;
+  void* kv_pool;             /* device; n_pages = kv_pool_bytes / page_bytes   */
+  size_t kv_pool_bytes;
+  void* workspace;           /* device, >= rp_query_sizes().workspace_bytes    */
+  size_t workspace_bytes;
+  void* stream;              /* cudaStream_t all work is issued on (NULL = 0)  */
+  int32_t rank, world;       /* data-parallel rank / size (world 1 = no NCCL)  */
+  int32_t max_seqs;          /* max sequences (n_prompts_local * G) per round  */
+  int32_t max_prompts;       /* max prompts per round on this rank             */
+  int32_t max_prompt_len;    /* max tokens of one prompt                       */
+  int32_t max_prompt_tokens; /* max total prompt tokens per round on this rank */
+  int32_t max_cap;           /* max length cap of any round                    */
+  uint64_t sample_seed;      /* Philox key of the sampler (reading Z10)        */
+  float temperature;         /* T of the Gumbel-max sampler (reading Z9: 1.0)  */
+  int32_t graph_steps;       /* decode steps per captured CUDA graph (0 = no graphs) */
+  const void* nccl_id;       /* 128-byte ncclUniqueId when world > 1, else NULL */
+} rp_runtime_desc;
+
+typedef struct {
+  size_t weights_bytes, workspace_bytes, page_bytes;
+} rp_sizes;
+
+/* One prompt of a round.  `tokens` (len ids in [0, vocab), none == eos) and
+ * `trace_lens` (G response lengths >= 1, trace mode only, else NULL) are host
+ * pointers, copied by rp_submit_round.  prompt_id is the caller's global id:
+ * it seeds the sampler stream uid = prompt_id * G + j (reading Z10). */
+typedef struct {
+  int32_t prompt_id;
+  int32_t len;
+  const int32_t* tokens;
+  const int32_t* trace_lens;
+} rp_prompt;
+
+typedef struct {
+  int64_t round_id;
+  int32_t kind;              /* RP_SHORT / RP_LONG                             */
+  int32_t t;                 /* decode steps completed (t_end when done)      */
+  int32_t n_live;            /* sequences still decoding on this rank          */
+  int32_t accepted;          /* accepted prompts (global under DP)             */
+  int32_t accepted_local;    /* accepted prompts decoded on this rank          */
+  int32_t done;              /* 1 once the round reached target or ran dry     */
+  int32_t underfilled;       /* done with accepted < target (reading Z4)       */
+  int32_t n_prompts_local;
+  int64_t decoded_tokens;    /* tokens decoded on this rank this round (incl. aborted) */
+} rp_status;
+
+typedef struct {
+  int32_t prompt_id;         /* global prompt id                               */
+  int32_t j;                 /* response index 0..G-1                          */
+  int32_t len;               /* tokens, including the EOS (reading Z16)        */
+  int32_t finish;            /* RP_FINISH_EOS / RP_FINISH_CAP                  */
+  int64_t tok_off;           /* offset of the tokens in the collect token buffer */
+} rp_response;
+
+/* Size query: bytes the caller must provide for weights and workspace, and the
+ * size of one KV page (64 tokens x all layers x KV heads x {K,V} x head_dim
+ * bf16).  Pure host computation. */
+int rp_query_sizes(const rp_model_desc* md, const rp_runtime_desc* rd, rp_sizes* out);
+
+/* Create a context: validates the descriptors, generates the weights into
+ * rd->weights on rd->stream (formula Z12), builds TMA descriptors, and
+ * creates the NCCL communicator when world > 1.  *out receives the context. */
+int rp_init_model(const rp_model_desc* md, const rp_runtime_desc* rd, void** out);
+
+/* Start a round.  prompts: the FULL
+ * prompt list of the round (every rank passes the same list); NULL pops
+ * n_prompts entries from this context's long-prompt queue (single rank).
+ * G: responses per prompt (R0).  cap: length cap of every response (>= 1).
+ * target: prompts to accept (P0), 1 <= target <= n_prompts; RP_LONG requires
+ * target == n_prompts.  flags: RP_SHORT|RP_LONG [|RP_TRACE].  round_id seeds
+ * the sampler counter (reading Z5: re-rolls draw fresh noise).  Runs the
+ * prefill and decode step 1 (the token sampled from the prefill logits).
+ * Errors: RP_EINVAL, RP_EBUSY (round active), RP_ENOMEM_KV, RP_ENOSPC. */
+int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n_prompts, int32_t G, int32_t cap, int32_t target,
+                    int32_t flags, int64_t round_id);
+
+/* Run up to max_steps decode steps (or until the round is done) and report
+ * the status.  Each step: embed -> L x (RMSNorm, QKV, RoPE+KV append,
+ * attention, O, RMSNorm, gate||up+SwiGLU, down) -> LM head -> sampler ->
+ * round control, all on device (captured in CUDA graphs of graph_steps
+ * steps).  Errors: RP_ESTATE (no round), RP_ENOMEM_KV, RP_ECUDA, RP_ENCCL. */
+int rp_step(void* ctx, int32_t max_steps, rp_status* st);
+
+/* Collect a finished round.  Fills out[0..n) with the accepted responses of
+ * the prompts decoded on this rank, in acceptance order (prompt-major, j
+ * minor), and their tokens into tok_buf (host, int32).  Pass out == NULL to
+ * query *n_out and *n_tok only (the round stays collectable).  A successful
+ * collect with out != NULL closes the round: every unaccepted prompt of this
+ * rank's slice is appended, in submission order, to the long-prompt queue
+ * (SHORT rounds), and all KV pages return to the pool.
+ * Errors: RP_ESTATE (round not done), RP_ENOSPC (buffers too small). */
+int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, int64_t tok_cap, int32_t* n_out,
+               int64_t* n_tok);
+
+/* Snapshot of the long-prompt queue (global prompt ids, oldest first); no
+ * drain.  ids_out may be NULL to query *n_out. */
+int rp_long_queue(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out);
+
+/* Destroy a context (does not free caller-owned device memory). */
+void rp_free(void* ctx);
+
+/* Last error message of the context (or of the last failed rp_init_model
+ * when ctx is NULL).  Valid until the next call on the context. */
+const char* rp_last_error(const void* ctx);
+
+/* Kernel launches issued by this context since creation (evidence for the
+ * bench's gpu_launches; graph launches count their kernel nodes). */
+int64_t rp_launch_count(const void* ctx);
+
+/* ---------------------------------------------------------------- test-only */
+/* Teacher-forced logits of one token sequence (host tokens[n], n <=
+ * max_prompt_tokens and <= max_prompt_len) through the prefill path: writes
+ * n x vocab fp32 to logits_out (host).  Requires no active round. */
+int rp_debug_logits(void* ctx, const int32_t* tokens, int32_t n, float* logits_out);
+
+/* Enable (steps > 0) or disable the per-step schedule trace of the next
+ * round: for every decode step t, the list of sequences decoded at t (slot =
+ * local_prompt * G + j, stable order), the accepted count and done flag. */
+int rp_debug_trace_enable(void* ctx, int32_t steps);
+/* Copy the trace out: buf[t][0] = n decoded, buf[t][1] = accepted | done << 30,
+ * buf[t][2 .. 2 + n) = slots.  Row stride = 2 + max_seqs. */
+int rp_debug_trace_get(void* ctx, int32_t* buf, int32_t steps);
+
+/* Logits of the most recent decode step (rows in the live order of that step)
+ * and the slots of those rows; requires graph_steps <= 1. */
+int rp_debug_last_logits(void* ctx, float* logits_out, int32_t* slots_out, int32_t max_rows, int32_t* n_rows);
+
+/* Run the tcgen05 GEMM alone on device pointers: Y[n][m] = sum_k W[m][k] X[n][k]
+ * (W bf16 [M,K], X bf16 [N,K] with N <= rows_cap rows allocated, Y fp32 [N,M]);
+ * splits = split-K factor (0 = automatic). */
+int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, float* Y, int32_t M, int32_t N,
+                  int32_t K, int32_t splits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROLLPACKER_H */

@@ -1,0 +1,95 @@
+// Shared device helpers of the CUDA path (sm_100a).  Shares nothing with
+// oracle/: the Philox round, the weight formula and the Gumbel mapping are
+// re-implemented here from DESIGN.md §3 (Z10, Z12).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace rp {
+
+constexpr int kPage = 64;          // tokens per KV page (DESIGN.md §5 D1)
+constexpr int kAttnChunk = 512;    // tokens per decode-attention split
+
+// ---------------------------------------------------------------- Philox4x32-10
+struct U4 { uint32_t x, y, z, w; };
+
+__host__ __device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(a, b);
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+
+__host__ __device__ __forceinline__ U4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                              uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    uint32_t hi0 = mulhi32(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    uint32_t hi1 = mulhi32(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  return U4{c0, c1, c2, c3};
+}
+
+__host__ __device__ __forceinline__ uint32_t u4_word(const U4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+// u = ((x >> 9) + 0.5) * 2^-23, exact in fp32, strictly inside (0, 1).
+__device__ __forceinline__ float u01(uint32_t x) {
+  return (__uint2float_rn(x >> 9) + 0.5f) * 1.1920928955078125e-07f;
+}
+
+// Orderable encoding of a float for packed (value, index) argmax with
+// atomicMax on uint64: larger value wins, then lower index.
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ unsigned long long pack_arg(float v, uint32_t idx) {
+  return ((unsigned long long)f2ord(v) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
+}
+__host__ __device__ __forceinline__ uint32_t unpack_idx(unsigned long long p) {
+  return 0xFFFFFFFFu - (uint32_t)(p & 0xFFFFFFFFull);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide exclusive scan of one int per thread (blockDim.x <= 1024).
+// Returns the exclusive prefix; *total receives the block sum.
+__device__ __forceinline__ int block_exscan(int v, int* total, int* smem /*>=33 ints*/) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int w = lane < nw ? smem[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) smem[lane] = w;      // inclusive per-warp totals
+  }
+  __syncthreads();
+  int base = wid ? smem[wid - 1] : 0;
+  int tot = smem[nw - 1];
+  __syncthreads();
+  *total = tot;
+  return base + x - v;
+}
+
+}  // namespace rp

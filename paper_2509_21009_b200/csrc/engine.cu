@@ -1,0 +1,919 @@
+// Host engine behind the C ABI (include/rollpacker.h): weight layout, TMA
+// descriptors, workspace carving, the round state machine (submit -> prefill
+// -> device-resident decode steps in CUDA graphs -> collect), the long-prompt
+// FIFO and the DP cutoff exchange over NCCL.  Every arithmetic step of the
+// path runs in the kernels of this directory; the host only plans, launches
+// and copies.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "../../include/rollpacker.h"
+#include "common.cuh"
+#include "gemm.h"
+#include "kernels.h"
+
+using namespace rp;
+
+namespace {
+
+constexpr int kSMs = 148;
+constexpr size_t kAlign = 1024;
+
+size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
+
+struct Carver {
+  uint8_t* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base((uint8_t*)b) {}
+  template <class T>
+  T* take(size_t count) {
+    off = align_up(off);
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+struct LayerW {
+  __nv_bfloat16 *wqkv, *wo, *wgu, *wd;
+  float *bqkv, *ln1, *ln2;
+  GemmPlan p_qkv, p_o, p_gu, p_down;
+};
+
+struct QueuedPrompt {
+  int32_t id;
+  std::vector<int32_t> tokens;
+  std::vector<int32_t> trace;  // lengths of the long-round attempt (may be empty)
+};
+
+struct Sizes {
+  int S, P, maxp, Tcap, max_items_dec, max_items_pre, pt_rows;
+  size_t part_floats, apart_floats;
+};
+
+}  // namespace
+
+struct RpCtx {
+  rp_model_desc md{};
+  rp_runtime_desc rd{};
+  ModelDims m{};
+  cudaStream_t st = nullptr;
+  std::string err;
+  Sizes z{};
+  int n_pages = 0;
+  long long launches = 0;
+
+  // weights
+  std::vector<LayerW> layers;
+  __nv_bfloat16 *emb = nullptr, *lm = nullptr;
+  float* lnf = nullptr;
+  GemmPlan p_lm{};
+  int s_qkv = 1, s_o = 1, s_gu = 1, s_down = 1, s_lm = 1;
+
+  // activations / workspace
+  float* x = nullptr;
+  __nv_bfloat16 *h = nullptr, *q = nullptr, *att = nullptr, *mid = nullptr;
+  float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
+  int* gctr = nullptr;
+  double* inv_freq = nullptr;
+  AttnItem *items_pre = nullptr;
+  int *pre_tok = nullptr, *pre_pos = nullptr, *pre_pt = nullptr, *pre_last = nullptr, *fork_jobs = nullptr;
+  int *col_meta = nullptr, *col_tok = nullptr;
+  int* identity_pages = nullptr;
+  RoundDev R{};
+  CtlBlock* h_ctl = nullptr;   // pinned mirror
+
+  // graphs
+  cudaGraphExec_t gexec = nullptr;
+  int graph_nodes = 0;
+  bool graph_dirty = true;
+  bool own_stream = false;
+
+  // NCCL
+  ncclComm_t comm = nullptr;
+
+  // round state (host)
+  bool active = false, collected = true;
+  int kind = 0, trace = 0, G = 0, cap = 0, target = 0, n_glob = 0, lo = 0, n_loc = 0;
+  int64_t round_id = 0;
+  std::vector<QueuedPrompt> round_prompts;  // this rank's slice
+  std::deque<QueuedPrompt> fifo;
+  int trace_steps = 0;
+  int* trace_dev = nullptr;
+  bool step_logits_valid = false;
+
+  int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    err = buf;
+    return code;
+  }
+};
+
+static std::string g_init_err;
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return c->fail(RP_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+#define CKN(call)                                                                             \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess) return c->fail(RP_ENCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+// ------------------------------------------------------------------ sizing
+static Sizes compute_sizes(const rp_model_desc* md, const rp_runtime_desc* rd) {
+  Sizes z{};
+  z.S = rd->max_seqs;
+  z.P = rd->max_prompts;
+  z.maxp = (rd->max_prompt_len + rd->max_cap + kPage - 1) / kPage + 1;
+  z.Tcap = std::max(rd->max_seqs, rd->max_prompt_tokens);
+  z.pt_rows = z.S + z.P;
+  const int max_ctx = rd->max_prompt_len + rd->max_cap + 1;
+  z.max_items_dec = z.S * ((max_ctx + kAttnChunk - 1) / kAttnChunk);
+  z.max_items_pre = rd->max_prompt_tokens * ((rd->max_prompt_len + kAttnChunk - 1) / kAttnChunk) + z.P;
+  // split-K partials: worst GEMM at the decode sizes
+  const int d = md->d_model, qkvw = (md->n_heads + 2 * md->n_kv_heads) * md->head_dim, F = md->d_ff;
+  const int hid = md->n_heads * md->head_dim;
+  const int shapes[5][2] = {{qkvw, d}, {d, hid}, {2 * F, d}, {d, F}, {md->vocab, d}};
+  size_t mx = 0;
+  const int nch = (z.S + 255) / 256;
+  for (auto& s : shapes) {
+    const int sp = gemm_pick_splits(s[0], s[1], kSMs);
+    if (sp > 1) mx = std::max(mx, (size_t)(s[0] / 128) * nch * sp * 256 * 128);
+  }
+  // rp_debug_gemm may request up to 16 splits of an arbitrary shape: keep >= 4M floats
+  z.part_floats = std::max(mx, (size_t)1 << 22);
+  z.apart_floats = (size_t)std::max(z.max_items_dec, z.max_items_pre) * md->n_kv_heads * 16 * (md->head_dim + 2);
+  return z;
+}
+
+struct WeightLayout {
+  size_t total;
+  std::vector<size_t> off;  // per layer: wqkv, bqkv, wo, wgu, wd, ln1, ln2 (7 entries); then emb, lm, lnf
+};
+
+static WeightLayout weight_layout(const rp_model_desc* md) {
+  WeightLayout w;
+  const size_t d = md->d_model, hd = md->head_dim, H = md->n_heads, KV = md->n_kv_heads, F = md->d_ff,
+               V = md->vocab;
+  const size_t qkvw = (H + 2 * KV) * hd;
+  size_t off = 0;
+  auto put = [&](size_t bytes) {
+    off = align_up(off);
+    w.off.push_back(off);
+    off += bytes;
+  };
+  for (int l = 0; l < md->n_layers; ++l) {
+    put(qkvw * d * 2);
+    put(qkvw * 4);
+    put(d * H * hd * 2);
+    put(2 * F * d * 2);
+    put(d * F * 2);
+    put(d * 4);
+    put(d * 4);
+  }
+  put(V * d * 2);
+  put(V * d * 2);
+  put(d * 4);
+  w.total = align_up(off);
+  return w;
+}
+
+static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd, RpCtx* c /*nullable*/) {
+  const Sizes z = compute_sizes(md, rd);
+  const size_t d = md->d_model, hd = md->head_dim, H = md->n_heads, KV = md->n_kv_heads, F = md->d_ff,
+               V = md->vocab;
+  Carver cv(c ? rd->workspace : nullptr);
+  auto x = cv.take<float>((size_t)z.Tcap * d);
+  auto h = cv.take<__nv_bfloat16>((size_t)z.Tcap * d);
+  auto qkv = cv.take<float>((size_t)z.Tcap * (H + 2 * KV) * hd);
+  auto q = cv.take<__nv_bfloat16>((size_t)z.Tcap * H * hd);
+  auto att = cv.take<__nv_bfloat16>((size_t)z.Tcap * H * hd);
+  auto mid = cv.take<__nv_bfloat16>((size_t)z.Tcap * F);
+  auto logits = cv.take<float>((size_t)std::max(z.S, std::max(z.P, rd->max_prompt_len)) * V);
+  auto gpart = cv.take<float>(z.part_floats);
+  auto gctr = cv.take<int>(1 << 16);
+  auto apart = cv.take<float>(z.apart_floats);
+  auto invf = cv.take<double>(hd / 2);
+  auto items_dec = cv.take<AttnItem>(z.max_items_dec);
+  auto items_pre = cv.take<AttnItem>(z.max_items_pre);
+  auto pre_tok = cv.take<int>(rd->max_prompt_tokens);
+  auto pre_pos = cv.take<int>(rd->max_prompt_tokens);
+  auto pre_pt = cv.take<int>(rd->max_prompt_tokens);
+  auto pre_last = cv.take<int>(std::max(z.P, rd->max_prompt_len));
+  auto fork_jobs = cv.take<int>((size_t)3 * z.S);
+  auto col_meta = cv.take<int>((size_t)5 * z.S + 1);
+  auto col_tok = cv.take<int>((size_t)z.S * rd->max_cap);
+  // round state
+  auto slot_prompt = cv.take<int>(z.S);
+  auto slot_j = cv.take<int>(z.S);
+  auto kv_len = cv.take<int>(z.S);
+  auto gen = cv.take<int>(z.S);
+  auto trace_L = cv.take<int>(z.S);
+  auto status = cv.take<int>(z.S);
+  auto own0 = cv.take<int>(z.S);
+  auto tok_out = cv.take<int>((size_t)z.S * rd->max_cap);
+  auto page_table = cv.take<int>((size_t)z.pt_rows * z.maxp);
+  auto p_cnt = cv.take<int>(z.P);
+  auto p_state = cv.take<int>(z.P);
+  auto p_gid = cv.take<int>(z.P);
+  auto comp_list = cv.take<int>(z.P);
+  auto accept_order = cv.take<int>(z.P);
+  auto live = cv.take<int>(z.S);
+  auto live_next = cv.take<int>(z.S);
+  auto tok_in = cv.take<int>(z.S);
+  auto row_pos = cv.take<int>(z.S);
+  auto row_pt = cv.take<int>(z.S);
+  auto best = cv.take<unsigned long long>(std::max(z.S, 1));
+  auto ks_local = cv.take<int>(4);
+  auto ks = cv.take<int>((size_t)3 * std::max(1, rd->world));
+  auto ctl = cv.take<CtlBlock>(1);
+  const size_t page_bytes = (size_t)md->n_layers * KV * 2 * kPage * hd * 2;
+  const size_t max_pages = rd->kv_pool_bytes / page_bytes;
+  auto free_stack = cv.take<int>(max_pages + 1);
+  auto ident = cv.take<int>(max_pages + 1);
+  if (c) {
+    c->x = x; c->h = h; c->qkv = qkv; c->q = q; c->att = att; c->mid = mid; c->logits = logits;
+    c->gpart = gpart; c->gctr = gctr; c->apart = apart; c->inv_freq = invf;
+    c->items_pre = items_pre; c->pre_tok = pre_tok; c->pre_pos = pre_pos; c->pre_pt = pre_pt;
+    c->pre_last = pre_last; c->fork_jobs = fork_jobs; c->col_meta = col_meta; c->col_tok = col_tok;
+    c->identity_pages = ident;
+    RoundDev& R = c->R;
+    R.S = z.S; R.P = z.P; R.maxp = z.maxp; R.kv_heads = (int)KV; R.eos = md->eos_id;
+    R.world = rd->world; R.rank = rd->rank;
+    R.slot_prompt = slot_prompt; R.slot_j = slot_j; R.kv_len = kv_len; R.gen = gen; R.trace_L = trace_L;
+    R.status = status; R.own0 = own0; R.tok_out = tok_out; R.page_table = page_table; R.p_cnt = p_cnt;
+    R.p_state = p_state; R.p_gid = p_gid; R.comp_list = comp_list; R.accept_order = accept_order;
+    R.live = live; R.live_next = live_next; R.tok_in = tok_in; R.row_pos = row_pos; R.row_pt = row_pt;
+    R.best = best; R.items = items_dec; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
+    R.ctl = ctl; R.cap = rd->max_cap;
+  }
+  return align_up(cv.off);
+}
+
+static int validate(const rp_model_desc* md, const rp_runtime_desc* rd, std::string& e) {
+  auto bad = [&](const char* f) { e = std::string("invalid field: ") + f; return RP_EINVAL; };
+  if (!md || !rd) return bad("desc (null)");
+  if (md->n_layers < 1) return bad("n_layers");
+  if (md->head_dim != 64 && md->head_dim != 128) return bad("head_dim (64 or 128)");
+  if (md->d_model % 128) return bad("d_model (multiple of 128)");
+  if ((md->n_heads * md->head_dim) % 128) return bad("n_heads*head_dim (multiple of 128)");
+  if (md->d_ff % 64) return bad("d_ff (multiple of 64)");
+  if (md->vocab % 128) return bad("vocab (multiple of 128)");
+  if (md->n_kv_heads < 1 || md->n_heads % md->n_kv_heads) return bad("n_kv_heads");
+  if (md->n_heads / md->n_kv_heads > 8) return bad("n_heads/n_kv_heads (<= 8)");
+  if (((md->n_heads + 2 * md->n_kv_heads) * md->head_dim) % 128) return bad("qkv width (multiple of 128)");
+  if (md->eos_id < 0 || md->eos_id >= md->vocab) return bad("eos_id");
+  if (rd->world < 1 || rd->rank < 0 || rd->rank >= rd->world) return bad("rank/world");
+  if (rd->world > 1 && !rd->nccl_id) return bad("nccl_id (world > 1)");
+  if (rd->max_seqs < 1 || rd->max_seqs > 1 << 16) return bad("max_seqs");
+  if (rd->max_prompts < 1 || rd->max_prompts > rd->max_seqs) return bad("max_prompts");
+  if (rd->max_prompt_len < 1 || rd->max_prompt_tokens < rd->max_prompt_len) return bad("max_prompt_len/tokens");
+  if (rd->max_cap < 1) return bad("max_cap");
+  if (rd->temperature <= 0.f) return bad("temperature");
+  return RP_OK;
+}
+
+// ------------------------------------------------------------------ model forward
+static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, int n_host, int splits, int epi,
+                 void* out, int ldo, const float* bias) {
+  GemmArgs a{};
+  a.M = M; a.K = K; a.n_dev = n_dev; a.n_host = n_host; a.splits = splits; a.epi = epi; a.out = out; a.ldo = ldo;
+  a.bias = bias; a.partial = c->gpart; a.counters = c->gctr;
+  gemm_launch(p, a, kSMs, c->st);
+  c->launches++;
+}
+
+// Transformer body over `n` rows (n_dev on device or n_host): decode (one token
+// per live sequence) or prefill (all prompt tokens).
+static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_host, const int* row_pos,
+                           const int* row_pt, const AttnItem* items, const int* n_items_dev, int n_items_host,
+                           bool decode) {
+  const ModelDims& m = c->m;
+  const int qkvw = (m.H + 2 * m.KV) * m.hd;
+  const int sp_qkv = decode ? c->s_qkv : 1, sp_o = decode ? c->s_o : 1, sp_gu = decode ? c->s_gu : 1,
+            sp_down = decode ? c->s_down : 1;
+  launch_embed(tok, n_dev, n_host, c->emb, c->x, m.d, c->st); c->launches++;
+  for (int l = 0; l < m.L; ++l) {
+    LayerW& w = c->layers[l];
+    launch_rmsnorm(c->x, nullptr, n_dev, n_host, w.ln1, c->h, m.d, m.eps, c->st); c->launches++;
+    gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_F32, c->qkv, qkvw, w.bqkv);
+    launch_rope_append(c->qkv, n_dev, n_host, row_pos, row_pt, c->R.page_table, c->R.maxp, c->q,
+                       c->rd.kv_pool, m, l, c->inv_freq, c->st); c->launches++;
+    launch_attention(c->q, c->rd.kv_pool, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
+                     c->apart, m, l, c->st); c->launches++;
+    launch_attn_merge(items, n_items_dev, n_items_host, c->apart, c->att, m, c->st); c->launches++;
+    gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, EPI_RESID, c->x, m.d, nullptr);
+    launch_rmsnorm(c->x, nullptr, n_dev, n_host, w.ln2, c->h, m.d, m.eps, c->st); c->launches++;
+    gemm(c, w.p_gu, 2 * m.F, m.d, n_dev, n_host, sp_gu, EPI_SWIGLU, c->mid, m.F, nullptr);
+    gemm(c, w.p_down, m.d, m.F, n_dev, n_host, sp_down, EPI_RESID, c->x, m.d, nullptr);
+  }
+}
+
+static void decode_step(RpCtx* c) {
+  RoundDev& R = c->R;
+  const int* n_dev = &R.ctl->n_live;
+  forward_layers(c, R.tok_in, n_dev, 0, R.row_pos, R.row_pt, R.items, &R.ctl->n_items, 0, true);
+  launch_rmsnorm(c->x, nullptr, n_dev, 0, c->lnf, c->h, c->m.d, c->m.eps, c->st); c->launches++;
+  gemm(c, c->p_lm, c->m.V, c->m.d, n_dev, 0, c->s_lm, EPI_F32, c->logits, c->m.V, nullptr);
+  launch_sampler(c->logits, c->m.V, 1, R, c->rd.sample_seed, 1.0f / c->rd.temperature, (uint32_t)c->round_id,
+                 c->st); c->launches++;
+  if (c->rd.world == 1) {
+    launch_ctl(R, 1, 0, c->st); c->launches++;
+  } else {
+    launch_ctl(R, 1, 1, c->st); c->launches++;
+    ncclAllGather(R.ks_local, R.ks, 3, ncclInt32, c->comm, c->st);
+    launch_ctl(R, 1, 2, c->st); c->launches++;
+  }
+}
+
+// (Re)capture graph_steps decode steps.  Kernel parameters (the RoundDev
+// scalars: cap, G, target, kind, trace, round id) are baked into the graph, so
+// it is rebuilt once per round, before its first decode step.
+static int ensure_graph(RpCtx* c) {
+  if (c->rd.graph_steps <= 0 || !c->graph_dirty) return RP_OK;
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+  const long long before = c->launches;
+  for (int i = 0; i < c->rd.graph_steps; ++i) decode_step(c);
+  cudaError_t e = cudaStreamEndCapture(c->st, &g);
+  if (e != cudaSuccess) return c->fail(RP_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  c->graph_nodes = (int)(c->launches - before);
+  c->launches = before;
+  CK(cudaGraphInstantiate(&c->gexec, g, 0));
+  CK(cudaGraphDestroy(g));
+  c->graph_dirty = false;
+  return RP_OK;
+}
+
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+int rp_query_sizes(const rp_model_desc* md, const rp_runtime_desc* rd, rp_sizes* out) {
+  std::string e;
+  int r = validate(md, rd, e);
+  if (r) { g_init_err = e; return r; }
+  if (!out) { g_init_err = "invalid field: out"; return RP_EINVAL; }
+  out->weights_bytes = weight_layout(md).total;
+  out->workspace_bytes = workspace_bytes(md, rd, nullptr);
+  out->page_bytes = (size_t)md->n_layers * md->n_kv_heads * 2 * kPage * md->head_dim * 2;
+  return RP_OK;
+}
+
+static int init_impl(RpCtx* c) {
+  const rp_model_desc* md = &c->md;
+  const rp_runtime_desc* rd = &c->rd;
+  c->st = (cudaStream_t)rd->stream;
+  if (!c->st) {   // graphs cannot be captured on the legacy stream: own one
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  ModelDims& m = c->m;
+  m.L = md->n_layers; m.d = md->d_model; m.H = md->n_heads; m.KV = md->n_kv_heads; m.hd = md->head_dim;
+  m.F = md->d_ff; m.V = md->vocab; m.eos = md->eos_id; m.eps = md->rms_eps;
+  m.page_bytes = (size_t)m.L * m.KV * 2 * kPage * m.hd * 2;
+  c->z = compute_sizes(md, rd);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  int sms = 0, cc_major = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (cc_major != 10) return c->fail(RP_ECUDA, "device is not sm_100 (compute capability %d.x)", cc_major);
+  const WeightLayout wl = weight_layout(md);
+  if (rd->weights_bytes < wl.total) return c->fail(RP_ENOSPC, "weights buffer too small: %zu < %zu", rd->weights_bytes, wl.total);
+  const size_t ws = workspace_bytes(md, rd, nullptr);
+  if (rd->workspace_bytes < ws) return c->fail(RP_ENOSPC, "workspace too small: %zu < %zu", rd->workspace_bytes, ws);
+  c->n_pages = (int)(rd->kv_pool_bytes / m.page_bytes);
+  if (c->n_pages < 2) return c->fail(RP_ENOSPC, "kv pool holds %d pages", c->n_pages);
+  workspace_bytes(md, rd, c);
+  if (gemm_init_attrs()) return c->fail(RP_ECUDA, "gemm smem attribute");
+  if (attn_init_attrs()) return c->fail(RP_ECUDA, "attention smem attribute");
+
+  // ---- weights (formula Z12), layout per layer
+  uint8_t* wb = (uint8_t*)rd->weights;
+  const size_t d = m.d, hd = m.hd, H = m.H, KV = m.KV, F = m.F, V = m.V;
+  const uint64_t seed = md->weight_seed;
+  c->layers.resize(m.L);
+  size_t k = 0;
+  std::vector<float> ones(std::max(d, (size_t)1), 1.0f);
+  for (int l = 0; l < m.L; ++l) {
+    LayerW& w = c->layers[l];
+    w.wqkv = (__nv_bfloat16*)(wb + wl.off[k++]);
+    w.bqkv = (float*)(wb + wl.off[k++]);
+    w.wo = (__nv_bfloat16*)(wb + wl.off[k++]);
+    w.wgu = (__nv_bfloat16*)(wb + wl.off[k++]);
+    w.wd = (__nv_bfloat16*)(wb + wl.off[k++]);
+    w.ln1 = (float*)(wb + wl.off[k++]);
+    w.ln2 = (float*)(wb + wl.off[k++]);
+    const uint32_t base = 0x100u * (uint32_t)(l + 1);
+    launch_init_weights(w.wqkv, (long long)H * hd * d, base + 0, seed, 0, (int)d, 0, c->st);
+    launch_init_weights(w.wqkv + H * hd * d, (long long)KV * hd * d, base + 1, seed, 0, (int)d, 0, c->st);
+    launch_init_weights(w.wqkv + (H + KV) * hd * d, (long long)KV * hd * d, base + 2, seed, 0, (int)d, 0, c->st);
+    if (md->qkv_bias) {
+      launch_init_weights(w.bqkv, (long long)H * hd, base + 3, seed, 1, 1, 0, c->st);
+      launch_init_weights(w.bqkv + H * hd, (long long)KV * hd, base + 4, seed, 1, 1, 0, c->st);
+      launch_init_weights(w.bqkv + (H + KV) * hd, (long long)KV * hd, base + 5, seed, 1, 1, 0, c->st);
+    } else {
+      CK(cudaMemsetAsync(w.bqkv, 0, (H + 2 * KV) * hd * 4, c->st));
+    }
+    launch_init_weights(w.wo, (long long)d * H * hd, base + 6, seed, 0, (int)(H * hd), 0, c->st);
+    launch_init_weights(w.wgu, (long long)F * d, base + 7, seed, 2, (int)d, 0, c->st);
+    launch_init_weights(w.wgu, (long long)F * d, base + 8, seed, 2, (int)d, 1, c->st);
+    launch_init_weights(w.wd, (long long)d * F, base + 9, seed, 0, (int)F, 0, c->st);
+    CK(cudaMemcpyAsync(w.ln1, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(w.ln2, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
+  }
+  c->emb = (__nv_bfloat16*)(wb + wl.off[k++]);
+  c->lm = (__nv_bfloat16*)(wb + wl.off[k++]);
+  c->lnf = (float*)(wb + wl.off[k++]);
+  launch_init_weights(c->emb, (long long)V * d, 0x10000000u, seed, 0, (int)d, 0, c->st);
+  launch_init_weights(c->lm, (long long)V * d, 0x10000001u, seed, 0, (int)d, 0, c->st);
+  CK(cudaMemcpyAsync(c->lnf, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaGetLastError());
+
+  // ---- RoPE frequencies theta^(-2i/hd) in fp64
+  std::vector<double> invf(hd / 2);
+  for (size_t i = 0; i < hd / 2; ++i) invf[i] = std::pow((double)md->rope_theta, -2.0 * (double)i / (double)hd);
+  CK(cudaMemcpyAsync(c->inv_freq, invf.data(), invf.size() * 8, cudaMemcpyHostToDevice, c->st));
+
+  // ---- TMA descriptors
+  const int Tcap = c->z.Tcap;
+  const int qkvw = (int)((H + 2 * KV) * hd);
+  for (auto& w : c->layers) {
+    if (make_tmap_bf16(&w.p_qkv.tmA, w.wqkv, qkvw, (int)d, 128) || make_tmap_bf16(&w.p_qkv.tmB, c->h, Tcap, (int)d, 32) ||
+        make_tmap_bf16(&w.p_o.tmA, w.wo, (int)d, (int)(H * hd), 128) ||
+        make_tmap_bf16(&w.p_o.tmB, c->att, Tcap, (int)(H * hd), 32) ||
+        make_tmap_bf16(&w.p_gu.tmA, w.wgu, (int)(2 * F), (int)d, 128) ||
+        make_tmap_bf16(&w.p_gu.tmB, c->h, Tcap, (int)d, 32) ||
+        make_tmap_bf16(&w.p_down.tmA, w.wd, (int)d, (int)F, 128) ||
+        make_tmap_bf16(&w.p_down.tmB, c->mid, Tcap, (int)F, 32))
+      return c->fail(RP_ECUDA, "cuTensorMapEncodeTiled failed");
+  }
+  if (make_tmap_bf16(&c->p_lm.tmA, c->lm, (int)V, (int)d, 128) || make_tmap_bf16(&c->p_lm.tmB, c->h, Tcap, (int)d, 32))
+    return c->fail(RP_ECUDA, "cuTensorMapEncodeTiled failed (lm head)");
+  c->s_qkv = gemm_pick_splits(qkvw, (int)d, kSMs);
+  c->s_o = gemm_pick_splits((int)d, (int)(H * hd), kSMs);
+  c->s_gu = gemm_pick_splits((int)(2 * F), (int)d, kSMs);
+  c->s_down = gemm_pick_splits((int)d, (int)F, kSMs);
+  c->s_lm = gemm_pick_splits((int)V, (int)d, kSMs);
+  CK(cudaMemsetAsync(c->gctr, 0, (1 << 16) * sizeof(int), c->st));
+
+  // ---- identity free list (page ids 0..n_pages-1)
+  {
+    std::vector<int> idp(c->n_pages);
+    for (int i = 0; i < c->n_pages; ++i) idp[i] = i;
+    CK(cudaMemcpyAsync(c->identity_pages, idp.data(), idp.size() * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
+  CK(cudaMallocHost(&c->h_ctl, sizeof(CtlBlock)));
+  memset(c->h_ctl, 0, sizeof(CtlBlock));
+  c->h_ctl->done = 1;
+  CK(cudaMemcpyAsync(c->R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
+
+  // ---- NCCL
+  if (rd->world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, rd->nccl_id, sizeof id);
+    CKN(ncclCommInitRank(&c->comm, rd->world, id, rd->rank));
+  }
+
+  c->graph_dirty = true;
+  CK(cudaStreamSynchronize(c->st));
+  return RP_OK;
+}
+
+int rp_init_model(const rp_model_desc* md, const rp_runtime_desc* rd, void** out) {
+  std::string e;
+  int r = validate(md, rd, e);
+  if (r) { g_init_err = e; return r; }
+  if (!out) { g_init_err = "invalid field: out"; return RP_EINVAL; }
+  RpCtx* c = new RpCtx();
+  c->md = *md;
+  c->rd = *rd;
+  r = init_impl(c);
+  if (r) {
+    g_init_err = c->err;
+    rp_free(c);
+    *out = nullptr;
+    return r;
+  }
+  *out = c;
+  return RP_OK;
+}
+
+void rp_free(void* ctx) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return;
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->h_ctl) cudaFreeHost(c->h_ctl);
+  if (c->trace_dev) cudaFree(c->trace_dev);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->own_stream) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+const char* rp_last_error(const void* ctx) {
+  return ctx ? ((const RpCtx*)ctx)->err.c_str() : g_init_err.c_str();
+}
+
+int64_t rp_launch_count(const void* ctx) { return ctx ? ((const RpCtx*)ctx)->launches : 0; }
+
+// Prefill attention work list: query blocks of floor(16/g) tokens x key splits.
+static int build_prefill_items(RpCtx* c, const std::vector<int>& plen, const std::vector<int>& poff,
+                               std::vector<AttnItem>& items) {
+  const int g = c->m.H / c->m.KV, tpb = 16 / g;
+  items.clear();
+  for (size_t p = 0; p < plen.size(); ++p) {
+    for (int b0 = 0; b0 < plen[p]; b0 += tpb) {
+      const int nq = std::min(tpb, plen[p] - b0);
+      const int hi = b0 + nq;  // keys [0, hi)
+      const int ns = (hi + kAttnChunk - 1) / kAttnChunk;
+      const int item0 = (int)items.size();
+      for (int s = 0; s < ns; ++s) {
+        AttnItem I;
+        I.q_row0 = poff[p] + b0; I.n_qtok = nq; I.pos0 = b0; I.pt_row = c->z.S + (int)p;
+        I.kv_lo = s * kAttnChunk; I.kv_hi = std::min(hi, (s + 1) * kAttnChunk);
+        I.nsplit = ns; I.item0 = item0;
+        items.push_back(I);
+      }
+    }
+  }
+  return (int)items.size() <= c->z.max_items_pre ? 0 : -1;
+}
+
+// Allocate prompt pages (host mirror of the LIFO free list: ids top-1, top-2, ...)
+// and run the prefill forward of `plen` prompts whose tokens are concatenated in
+// `toks`.  Writes KV into pages of page-table rows S + p; leaves the final-norm
+// hidden state of the rows listed in `out_rows` in h[0..).
+static int prefill(RpCtx* c, const std::vector<int>& toks, const std::vector<int>& plen, int& top,
+                   std::vector<std::vector<int>>& prompt_pages, const std::vector<int>& out_rows) {
+  const int maxp = c->z.maxp, S = c->z.S;
+  const int T = (int)toks.size();
+  std::vector<int> poff(plen.size()), pos(T), pt(T);
+  int o = 0;
+  prompt_pages.assign(plen.size(), {});
+  std::vector<int> ptab((size_t)plen.size() * maxp, 0);
+  for (size_t p = 0; p < plen.size(); ++p) {
+    poff[p] = o;
+    const int np = (plen[p] + kPage - 1) / kPage;
+    if (np > maxp) return c->fail(RP_EINVAL, "prompt %zu longer than max_prompt_len", p);
+    for (int k = 0; k < np; ++k) {
+      if (top <= 0) return c->fail(RP_ENOMEM_KV, "KV pool exhausted during prefill");
+      const int page = --top;
+      prompt_pages[p].push_back(page);
+      ptab[p * maxp + k] = page;
+    }
+    for (int i = 0; i < plen[p]; ++i) { pos[o + i] = i; pt[o + i] = S + (int)p; }
+    o += plen[p];
+  }
+  std::vector<AttnItem> items;
+  if (build_prefill_items(c, plen, poff, items)) return c->fail(RP_ENOSPC, "prefill attention items exceed capacity");
+  CK(cudaMemcpyAsync(c->R.page_table + (size_t)S * maxp, ptab.data(), ptab.size() * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->pre_tok, toks.data(), T * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->pre_pos, pos.data(), T * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->pre_pt, pt.data(), T * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->items_pre, items.data(), items.size() * sizeof(AttnItem), cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->pre_last, out_rows.data(), out_rows.size() * 4, cudaMemcpyHostToDevice, c->st));
+  forward_layers(c, c->pre_tok, nullptr, T, c->pre_pos, c->pre_pt, c->items_pre, nullptr, (int)items.size(), false);
+  launch_rmsnorm(c->x, c->pre_last, nullptr, (int)out_rows.size(), c->lnf, c->h, c->m.d, c->m.eps, c->st);
+  c->launches++;
+  gemm(c, c->p_lm, c->m.V, c->m.d, nullptr, (int)out_rows.size(), 1, EPI_F32, c->logits, c->m.V, nullptr);
+  CK(cudaGetLastError());
+  return RP_OK;
+}
+
+int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, int32_t cap, int32_t target,
+                    int32_t flags, int64_t round_id) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (c->active) return c->fail(RP_EBUSY, "a round is active (collect it first)");
+  const int kind = flags & RP_LONG ? 1 : 0;
+  const int trace = flags & RP_TRACE ? 1 : 0;
+  if (G < 1) return c->fail(RP_EINVAL, "invalid field: G (>= 1)");
+  if (n < 1) return c->fail(RP_EINVAL, "invalid field: n_prompts (>= 1)");
+  if (cap < 1 || cap > c->rd.max_cap) return c->fail(RP_EINVAL, "invalid field: cap (1..max_cap)");
+  if (target < 1 || target > n) return c->fail(RP_EINVAL, "invalid field: target (1..n_prompts)");
+  if (kind == 1 && target != n) return c->fail(RP_EINVAL, "invalid field: target (RP_LONG needs target == n_prompts)");
+  // the full list (this rank's slice is decoded)
+  std::vector<QueuedPrompt> all;
+  if (!prompts) {
+    if (c->rd.world > 1) return c->fail(RP_EINVAL, "invalid field: prompts (NULL queue pop needs world == 1)");
+    if ((int)c->fifo.size() < n) return c->fail(RP_EINVAL, "invalid field: n_prompts (queue holds %zu)", c->fifo.size());
+    for (int i = 0; i < n; ++i) { all.push_back(c->fifo.front()); c->fifo.pop_front(); }
+  } else {
+    all.resize(n);
+    for (int i = 0; i < n; ++i) {
+      const rp_prompt& p = prompts[i];
+      if (p.len < 1 || !p.tokens) return c->fail(RP_EINVAL, "invalid field: prompts[%d].len/tokens", i);
+      if (p.len > c->rd.max_prompt_len) return c->fail(RP_EINVAL, "invalid field: prompts[%d].len > max_prompt_len", i);
+      all[i].id = p.prompt_id;
+      all[i].tokens.assign(p.tokens, p.tokens + p.len);
+      for (int t : all[i].tokens)
+        if (t < 0 || t >= c->m.V || t == c->m.eos) return c->fail(RP_EINVAL, "invalid field: prompts[%d].tokens", i);
+      if (trace) {
+        if (!p.trace_lens) return c->fail(RP_EINVAL, "invalid field: prompts[%d].trace_lens (RP_TRACE)", i);
+        all[i].trace.assign(p.trace_lens, p.trace_lens + G);
+        for (int L : all[i].trace)
+          if (L < 1) return c->fail(RP_EINVAL, "invalid field: prompts[%d].trace_lens (>= 1)", i);
+      }
+    }
+  }
+  if (trace)
+    for (auto& p : all)
+      if ((int)p.trace.size() != G) return c->fail(RP_EINVAL, "invalid field: trace_lens (queued prompt lacks a trace)");
+  // contiguous slice of this rank
+  const int W = c->rd.world, r = c->rd.rank;
+  const int base = n / W, extra = n % W;
+  const int lo = r * base + std::min(r, extra);
+  const int n_loc = base + (r < extra ? 1 : 0);
+  if (n_loc > c->z.P) return c->fail(RP_ENOSPC, "prompts on this rank %d > max_prompts %d", n_loc, c->z.P);
+  if (n_loc * G > c->z.S) return c->fail(RP_ENOSPC, "sequences on this rank %d > max_seqs %d", n_loc * G, c->z.S);
+  long long T = 0;
+  for (int i = 0; i < n_loc; ++i) T += (long long)all[lo + i].tokens.size();
+  if (T > c->rd.max_prompt_tokens) return c->fail(RP_ENOSPC, "prompt tokens %lld > max_prompt_tokens", T);
+
+  c->kind = kind; c->trace = trace; c->G = G; c->cap = cap; c->target = target; c->n_glob = n;
+  c->lo = lo; c->n_loc = n_loc; c->round_id = round_id;
+  c->round_prompts.assign(all.begin() + lo, all.begin() + lo + n_loc);
+  RoundDev& R = c->R;
+  R.cap = cap; R.G = G; R.target = target; R.kind = kind; R.trace = trace; R.n_prompts = n_loc;
+  R.trace_buf = c->trace_dev; R.trace_steps = c->trace_steps;
+
+  // ---- host plan: prompt pages, sibling page tables, fork jobs
+  const int S = c->z.S, maxp = c->z.maxp;
+  int top = c->n_pages;
+  std::vector<int> toks, plen(n_loc), last(n_loc);
+  for (int p = 0; p < n_loc; ++p) {
+    const auto& tk = c->round_prompts[p].tokens;
+    plen[p] = (int)tk.size();
+    toks.insert(toks.end(), tk.begin(), tk.end());
+    last[p] = (int)toks.size() - 1;
+  }
+  std::vector<std::vector<int>> ppages;
+  if (n_loc > 0) {
+    int rc = prefill(c, toks, plen, top, ppages, last);
+    if (rc) return rc;
+  }
+  const int nS = n_loc * G;
+  std::vector<int> slot_prompt(nS), slot_j(nS), kv_len(nS), zeros(std::max(nS, n_loc), 0), trL(nS, 0), own0(nS),
+      live(nS), gid(n_loc), ptab((size_t)std::max(nS, 1) * maxp, 0), jobs;
+  for (int p = 0; p < n_loc; ++p) {
+    gid[p] = c->round_prompts[p].id;
+    for (int j = 0; j < G; ++j) {
+      const int s = p * G + j;
+      slot_prompt[s] = p; slot_j[s] = j; kv_len[s] = plen[p]; live[s] = s;
+      trL[s] = trace ? c->round_prompts[p].trace[j] : 0;
+      const int full = plen[p] / kPage;
+      for (int k = 0; k < full; ++k) ptab[(size_t)s * maxp + k] = ppages[p][k];
+      own0[s] = full;
+      if (plen[p] % kPage) {
+        if (top <= 0) return c->fail(RP_ENOMEM_KV, "KV pool exhausted forking prompt pages");
+        const int pg = --top;
+        ptab[(size_t)s * maxp + full] = pg;
+        jobs.push_back(ppages[p][full]); jobs.push_back(pg); jobs.push_back(plen[p] % kPage);
+      }
+    }
+  }
+  auto up = [&](int* dst, const std::vector<int>& v, size_t count) {
+    return cudaMemcpyAsync(dst, v.data(), count * 4, cudaMemcpyHostToDevice, c->st);
+  };
+  if (nS > 0) {
+    CK(up(R.slot_prompt, slot_prompt, nS)); CK(up(R.slot_j, slot_j, nS)); CK(up(R.kv_len, kv_len, nS));
+    CK(up(R.gen, zeros, nS)); CK(up(R.status, zeros, nS)); CK(up(R.trace_L, trL, nS)); CK(up(R.own0, own0, nS));
+    CK(up(R.live, live, nS)); CK(up(R.page_table, ptab, (size_t)nS * maxp));
+    CK(cudaMemsetAsync(R.best, 0, (size_t)nS * 8, c->st));
+  }
+  if (n_loc > 0) {
+    CK(up(R.p_gid, gid, n_loc)); CK(up(R.p_cnt, zeros, n_loc)); CK(up(R.p_state, zeros, n_loc));
+  }
+  if (!jobs.empty()) {
+    CK(up(c->fork_jobs, jobs, jobs.size()));
+    launch_kv_fork(c->fork_jobs, (int)jobs.size() / 3, c->rd.kv_pool, c->m, c->st);
+    c->launches++;
+  }
+  CK(cudaMemcpyAsync(R.free_stack, c->identity_pages, (size_t)c->n_pages * 4, cudaMemcpyDeviceToDevice, c->st));
+  CtlBlock cb{};
+  cb.n_live = nS; cb.t = 1; cb.free_top = top;
+  *c->h_ctl = cb;
+  CK(cudaMemcpyAsync(R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
+  if (c->trace_dev) CK(cudaMemsetAsync(c->trace_dev, 0, (size_t)c->trace_steps * (2 + S) * 4, c->st));
+  // ---- step 1: token 1 of every sibling from its prompt's prefill logits
+  launch_sampler(c->logits, c->m.V, G, R, c->rd.sample_seed, 1.0f / c->rd.temperature, (uint32_t)round_id, c->st);
+  c->launches++;
+  if (c->rd.world == 1) {
+    launch_ctl(R, 0, 0, c->st); c->launches++;
+  } else {
+    launch_ctl(R, 0, 1, c->st); c->launches++;
+    CKN(ncclAllGather(R.ks_local, R.ks, 3, ncclInt32, c->comm, c->st));
+    launch_ctl(R, 0, 2, c->st); c->launches++;
+  }
+  CK(cudaGetLastError());
+  c->active = true;
+  c->collected = false;
+  c->step_logits_valid = false;
+  c->graph_dirty = true;
+  return RP_OK;
+}
+
+static int read_ctl(RpCtx* c) {
+  CK(cudaMemcpyAsync(c->h_ctl, c->R.ctl, sizeof(CtlBlock), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return RP_OK;
+}
+
+static void fill_status(RpCtx* c, rp_status* st) {
+  if (!st) return;
+  const CtlBlock& b = *c->h_ctl;
+  st->round_id = c->round_id; st->kind = c->kind;
+  st->t = b.done ? b.t_end : b.t - 1;
+  st->n_live = b.done ? 0 : b.n_live;
+  st->accepted = b.acc; st->accepted_local = b.acc_local; st->done = b.done; st->underfilled = b.underfilled;
+  st->n_prompts_local = c->n_loc; st->decoded_tokens = b.decoded;
+}
+
+int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (!c->active) return c->fail(RP_ESTATE, "no active round");
+  int rc = read_ctl(c);
+  if (rc) return rc;
+  int steps = 0;
+  if (!c->h_ctl->done && max_steps > 0 && (rc = ensure_graph(c))) return rc;
+  while (!c->h_ctl->done && steps < max_steps) {
+    if (c->gexec) {
+      CK(cudaGraphLaunch(c->gexec, c->st));
+      c->launches += c->graph_nodes;
+      steps += c->rd.graph_steps;
+    } else {
+      decode_step(c);
+      CK(cudaGetLastError());
+      steps += 1;
+      c->step_logits_valid = true;
+    }
+    if ((rc = read_ctl(c))) return rc;
+  }
+  fill_status(c, st);
+  if (c->h_ctl->err == 1) return c->fail(RP_ENOMEM_KV, "KV page pool exhausted (no preemption; reading Z17)");
+  if (c->h_ctl->err == 2) return c->fail(RP_ENOSPC, "page table overflow (max_prompt_len + max_cap)");
+  return RP_OK;
+}
+
+int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, int64_t tok_cap, int32_t* n_out,
+               int64_t* n_tok) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (!c->active) return c->fail(RP_ESTATE, "no active round");
+  int rc = read_ctl(c);
+  if (rc) return rc;
+  if (!c->h_ctl->done) return c->fail(RP_ESTATE, "round not done");
+  const int acc = c->h_ctl->acc_local, G = c->G, nr = acc * G;
+  launch_collect_pack(c->R, c->col_meta, c->col_tok, c->st);
+  c->launches += 2;
+  std::vector<int> meta((size_t)4 * nr + nr + 1);
+  CK(cudaMemcpyAsync(meta.data(), c->col_meta, (size_t)4 * nr * 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(meta.data() + 4 * nr, c->col_meta + 4 * c->z.S, (size_t)(nr + 1) * 4,
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  const int64_t total = meta[4 * nr + nr];
+  if (n_out) *n_out = nr;
+  if (n_tok) *n_tok = total;
+  if (!out) return RP_OK;
+  if (max_out < nr || tok_cap < total || !tok_buf) return c->fail(RP_ENOSPC, "collect buffers too small");
+  if (total > 0) CK(cudaMemcpyAsync(tok_buf, c->col_tok, total * 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  std::vector<char> accepted(c->n_loc, 0);
+  for (int r = 0; r < nr; ++r) {
+    const int p = meta[4 * r];
+    accepted[p] = 1;
+    out[r].prompt_id = c->round_prompts[p].id;
+    out[r].j = meta[4 * r + 1];
+    out[r].len = meta[4 * r + 2];
+    out[r].finish = meta[4 * r + 3] == ST_CAPPED ? RP_FINISH_CAP : RP_FINISH_EOS;
+    out[r].tok_off = meta[4 * nr + r];
+  }
+  if (c->kind == 0)
+    for (int p = 0; p < c->n_loc; ++p)
+      if (!accepted[p]) {
+        QueuedPrompt q = c->round_prompts[p];
+        c->fifo.push_back(q);
+      }
+  c->active = false;
+  c->collected = true;
+  return RP_OK;
+}
+
+int rp_long_queue(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (n_out) *n_out = (int)c->fifo.size();
+  if (!ids_out) return RP_OK;
+  if (max < (int)c->fifo.size()) return c->fail(RP_ENOSPC, "ids_out too small");
+  int i = 0;
+  for (auto& q : c->fifo) ids_out[i++] = q.id;
+  return RP_OK;
+}
+
+int rp_debug_logits(void* ctx, const int32_t* tokens, int32_t n, float* logits_out) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (c->active) return c->fail(RP_EBUSY, "a round is active");
+  if (n < 1 || n > c->rd.max_prompt_len || n > c->rd.max_prompt_tokens) return c->fail(RP_EINVAL, "invalid field: n");
+  for (int i = 0; i < n; ++i)
+    if (tokens[i] < 0 || tokens[i] >= c->m.V) return c->fail(RP_EINVAL, "invalid field: tokens[%d]", i);
+  std::vector<int> toks(tokens, tokens + n), plen{n}, rows(n);
+  for (int i = 0; i < n; ++i) rows[i] = i;
+  int top = c->n_pages;
+  std::vector<std::vector<int>> pp;
+  int rc = prefill(c, toks, plen, top, pp, rows);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(logits_out, c->logits, (size_t)n * c->m.V * 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return RP_OK;
+}
+
+int rp_debug_trace_enable(void* ctx, int32_t steps) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (c->active) return c->fail(RP_EBUSY, "a round is active");
+  if (c->trace_dev) { cudaFree(c->trace_dev); c->trace_dev = nullptr; }
+  c->trace_steps = 0;
+  if (steps > 0) {
+    CK(cudaMalloc(&c->trace_dev, (size_t)steps * (2 + c->z.S) * 4));
+    c->trace_steps = steps;
+  }
+  c->R.trace_buf = c->trace_dev; c->R.trace_steps = c->trace_steps;
+  c->graph_dirty = true;
+  return RP_OK;
+}
+
+int rp_debug_trace_get(void* ctx, int32_t* buf, int32_t steps) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (!c->trace_dev) return c->fail(RP_ESTATE, "trace not enabled");
+  const int s = std::min(steps, c->trace_steps);
+  CK(cudaMemcpyAsync(buf, c->trace_dev, (size_t)s * (2 + c->z.S) * 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return RP_OK;
+}
+
+int rp_debug_last_logits(void* ctx, float* logits_out, int32_t* slots_out, int32_t max_rows, int32_t* n_rows) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (!c->step_logits_valid) return c->fail(RP_ESTATE, "no eager decode step ran (graph_steps must be 0)");
+  // rows of the last step were the live list before compaction: trace row t-1 holds it
+  if (!c->trace_dev) return c->fail(RP_ESTATE, "needs rp_debug_trace_enable");
+  int rc = read_ctl(c);
+  if (rc) return rc;
+  const int t = c->h_ctl->done ? c->h_ctl->t_end : c->h_ctl->t - 1;
+  if (t < 1 || t > c->trace_steps) return c->fail(RP_ESTATE, "step outside the trace");
+  std::vector<int> row(2 + c->z.S);
+  CK(cudaMemcpyAsync(row.data(), c->trace_dev + (size_t)(t - 1) * (2 + c->z.S), row.size() * 4,
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  const int n = row[0];
+  if (n > max_rows) return c->fail(RP_ENOSPC, "max_rows too small");
+  *n_rows = n;
+  memcpy(slots_out, row.data() + 2, n * 4);
+  CK(cudaMemcpyAsync(logits_out, c->logits, (size_t)n * c->m.V * 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return RP_OK;
+}
+
+int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, float* Y, int32_t M, int32_t N,
+                  int32_t K, int32_t splits) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (M % 128 || K % 64 || M <= 0 || K <= 0 || N < 0 || N > rows_cap) return c->fail(RP_EINVAL, "invalid GEMM shape");
+  if (splits <= 0) splits = gemm_pick_splits(M, K, kSMs);
+  splits = std::min(splits, K / 64);
+  const size_t need = (size_t)(M / 128) * ((N + 255) / 256) * splits * 256 * 128;
+  if (splits > 1 && need > c->z.part_floats) return c->fail(RP_ENOSPC, "split-K workspace too small");
+  if ((M / 128) * ((N + 255) / 256) > (1 << 16)) return c->fail(RP_ENOSPC, "too many tiles");
+  GemmPlan p;
+  if (make_tmap_bf16(&p.tmA, W, M, K, 128) || make_tmap_bf16(&p.tmB, X, rows_cap, K, 32))
+    return c->fail(RP_ECUDA, "tensor map");
+  gemm(c, p, M, K, nullptr, N, splits, EPI_F32, Y, M, nullptr);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->st));
+  return RP_OK;
+}
+
+}  // extern "C"

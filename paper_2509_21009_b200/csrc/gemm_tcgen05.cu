@@ -1,0 +1,395 @@
+// Swap-AB decode/prefill GEMM on the 5th-generation tensor cores (sm_100a).
+//
+//   D[m, n] = sum_k W[m, k] * X[n, k]      (W: weights [M, K] bf16, K-major;
+//                                           X: activations [N, K] bf16, K-major)
+//
+// Weights fill the UMMA M=128 tile; the live batch (or prompt tokens) is the
+// UMMA N dimension, read at run time from device memory so the same launch is
+// valid for every live count inside a captured CUDA graph.  Operands are
+// staged by TMA (SWIZZLE_128B, 64-element K blocks) into a 4-stage
+// shared-memory ring; one elected thread issues tcgen05.mma into a
+// double-buffered TMEM accumulator (2 x 256 fp32 columns); four epilogue warps
+// read TMEM with tcgen05.ld and apply the fused epilogue.
+//
+// Work = m_tiles x n_chunks(256) x splits.  Split-K (fixed per weight shape,
+// independent of N, so results are batch invariant) writes fp32 partials; the
+// last CTA of a tile (atomic ticket) sums them in split order (deterministic)
+// and runs the epilogue.
+//
+// Epilogues (DESIGN.md §5 K1/K2): F32 (+bias) for QKV and logits, RESID
+// (fp32 residual +=) for O/down, SWIGLU (tile rows 0-63 gate, 64-127 up of the
+// same 64 features, weights interleaved at init) for gate||up, BF16 store.
+#include <cuda.h>
+#include <cstdint>
+#include "common.cuh"
+#include "gemm.h"
+
+namespace rp {
+
+constexpr int BM = 128, BK = 64, BN = 256, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;         // 16 KB
+constexpr int B_BYTES = BN * BK * 2;         // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int XCH_BYTES = 64 * 33 * 4;       // swiglu exchange
+constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + XCH_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int GEMM_THREADS = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups of
+// 128 B rows -> stride byte offset 1024; version 1 (sm_100); layout type 2.
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                    // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;          // SBO
+  d |= (uint64_t)1 << 46;                    // version
+  d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, M=128.
+__device__ __forceinline__ uint32_t make_idesc(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                          uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+#define TMEM_LD32(taddr, r)                                                                                   \
+  asm volatile(                                                                                               \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"        \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                              \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),      \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),             \
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),           \
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),           \
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                                  \
+      : "r"(taddr));                                                                                          \
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory")
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
+
+struct Item { int tile, chunk, split; };
+__device__ __forceinline__ Item decode_item(int it, int m_tiles, int splits) {
+  Item r;
+  r.split = it % splits;
+  int q = it / splits;
+  r.tile = q % m_tiles;
+  r.chunk = q / m_tiles;
+  return r;
+}
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    GemmArgs a) {
+  const int N = a.n_dev ? *a.n_dev : a.n_host;
+  if (N <= 0) return;
+  const int m_tiles = a.M / BM;
+  const int n_chunks = (N + BN - 1) / BN;
+  const int n_items = m_tiles * n_chunks * a.splits;
+  if ((int)blockIdx.x >= n_items) return;
+  const int kb_total = a.K / BK;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  float* xch = (float*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES + XCH_BYTES);
+  // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]; then tmem slot, ticket
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+  int* ticket = (int*)(tmem_slot + 1);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+  const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(full0 + 8 * i, 1); mbar_init(empty0 + 8 * i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(tfull0 + 8 * i, 1); mbar_init(tempty0 + 8 * i, 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+      int stage = 0; uint32_t phase = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        Item I = decode_item(it, m_tiles, a.splits);
+        const int kb0 = (int)((long)I.split * kb_total / a.splits), kb1 = (int)((long)(I.split + 1) * kb_total / a.splits);
+        const int n0 = I.chunk * BN, nc = min(BN, N - n0);
+        const int nbox = (nc + 31) >> 5;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const uint32_t fb = full0 + 8 * stage;
+          mbar_expect_tx(fb, A_BYTES + nbox * 32 * BK * 2);
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          tma_load_2d(sa, &tmA, fb, kb * BK, I.tile * BM, pol_w);
+          for (int b = 0; b < nbox; ++b)
+            tma_load_2d(sa + A_BYTES + b * 32 * BK * 2, &tmB, fb, kb * BK, n0 + 32 * b, pol_x);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer (single thread) =====
+      int stage = 0; uint32_t phase = 0; int local = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+        Item I = decode_item(it, m_tiles, a.splits);
+        const int kb0 = (int)((long)I.split * kb_total / a.splits), kb1 = (int)((long)(I.split + 1) * kb_total / a.splits);
+        const int nc = min(BN, N - I.chunk * BN);
+        const int nmma = (nc + 15) & ~15;
+        const uint32_t idesc = make_idesc(nmma);
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(full0 + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint64_t da = make_sdesc(sa), db = make_sdesc(sa + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)   // +32 B along K per UMMA_K=16 step
+            umma_bf16(tmem_d, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          umma_commit(empty0 + 8 * stage);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(tfull0 + 8 * acc);
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue warpgroup =====
+    const int q = warp - 4;                 // TMEM lane quarter
+    const int et = threadIdx.x - 128;       // 0..127
+    int local = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+      Item I = decode_item(it, m_tiles, a.splits);
+      const int n0 = I.chunk * BN, nc = min(BN, N - n0);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(tfull0 + 8 * acc, acc_phase);
+      tc_fence_after();
+      const int row = 32 * q + lane;        // row within the tile
+      const int m = I.tile * BM + row;
+      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(32 * q) << 16);
+      const bool split = a.splits > 1;
+      if (split) {
+        // fp32 partials: part[((tile*n_chunks+chunk)*splits+split)][col][row]
+        float* part = a.partial + ((size_t)((I.chunk * m_tiles + I.tile) * a.splits + I.split)) * BN * BM;
+        for (int c0 = 0; c0 < nc; c0 += 32) {
+          uint32_t r[32];
+          TMEM_LD32(tbase + c0, r);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < nc) part[(c0 + j) * BM + row] = __uint_as_float(r[j]);
+        }
+      }
+      bool last = true;
+      if (split) {
+        tc_fence_before();
+        mbar_arrive(tempty0 + 8 * acc);     // TMEM stage free for the next item
+        __threadfence();
+        named_bar(1, 128);
+        if (et == 0) {
+          int* ctr = a.counters + I.chunk * m_tiles + I.tile;
+          int old = atomicAdd(ctr, 1);
+          *ticket = (old == a.splits - 1);
+          if (old == a.splits - 1) *ctr = 0;
+        }
+        named_bar(1, 128);
+        last = *ticket != 0;
+        __threadfence();
+      }
+      if (!last) continue;
+      // ---- epilogue proper over columns of this chunk
+      const float bias = a.bias ? a.bias[m] : 0.f;
+      for (int c0 = 0; c0 < nc; c0 += 32) {
+        float v[32];
+        if (split) {
+          const float* part0 = a.partial + ((size_t)((I.chunk * m_tiles + I.tile) * a.splits)) * BN * BM;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          for (int s = 0; s < a.splits; ++s) {
+            const float* p = part0 + (size_t)s * BN * BM;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < nc) v[j] += __ldcg(p + (c0 + j) * BM + row);
+          }
+        } else {
+          uint32_t r[32];
+          TMEM_LD32(tbase + c0, r);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        }
+        if (a.epi == EPI_SWIGLU) {
+          // rows 64..127 (quarters 2,3) hold `up`, rows 0..63 hold `gate`
+          named_bar(2, 128);
+          if (q >= 2) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) xch[(row - 64) * 33 + j] = v[j];
+          }
+          named_bar(2, 128);
+          if (q < 2) {
+            const int f = I.tile * 64 + row;
+            __nv_bfloat16* o = (__nv_bfloat16*)a.out;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int n = n0 + c0 + j;
+              if (c0 + j < nc) o[(size_t)n * a.ldo + f] = __float2bfloat16(silu_f(v[j]) * xch[row * 33 + j]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int n = n0 + c0 + j;
+            if (c0 + j >= nc) break;
+            const size_t o = (size_t)n * a.ldo + m;
+            if (a.epi == EPI_F32) ((float*)a.out)[o] = v[j] + bias;
+            else if (a.epi == EPI_RESID) ((float*)a.out)[o] += v[j];
+            else ((__nv_bfloat16*)a.out)[o] = __float2bfloat16(v[j] + bias);
+          }
+        }
+      }
+      if (!split) {
+        tc_fence_before();
+        mbar_arrive(tempty0 + 8 * acc);     // all TMEM reads of this item done
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled)p;
+  }
+  return fn;
+}
+
+int make_tmap_bf16(CUtensorMap* map, const void* base, int rows, int cols, int box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return -1;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+int gemm_smem_bytes() { return GEMM_SMEM; }
+
+int gemm_init_attrs() {
+  return cudaFuncSetAttribute(gemm_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
+                 cudaSuccess
+             ? 0
+             : -1;
+}
+
+int gemm_pick_splits(int M, int K, int n_sms) {
+  // Fill the SMs for a single 256-column chunk: minimise the critical path
+  // ceil(items / n_sms) * ceil(kb / splits) (+ a small per-split cost).
+  const int tiles = M / BM, kb = K / BK;
+  int best = 1;
+  double best_cost = 1e30;
+  for (int s = 1; s <= 16 && s <= kb; ++s) {
+    const int items = tiles * s;
+    const double waves = (double)((items + n_sms - 1) / n_sms);
+    const double cost = waves * ((kb + s - 1) / s + 4) + (s > 1 ? 2.0 : 0.0);
+    if (cost < best_cost - 1e-9) { best_cost = cost; best = s; }
+  }
+  return best;
+}
+
+void gemm_launch(const GemmPlan& p, const GemmArgs& a, int grid, cudaStream_t st) {
+  gemm_tcgen05_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(p.tmA, p.tmB, a);
+}
+
+}  // namespace rp

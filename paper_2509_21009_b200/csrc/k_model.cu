@@ -1,0 +1,177 @@
+// Model-side elementwise kernels: weight formula (Z12), embedding
+// gather, RMSNorm, RoPE + paged-KV append, prompt-page fork (K6-K8).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rp {
+
+// ------------------------------------------------------------- weight formula
+// mode 0: bf16 out[i]; mode 1: fp32 out[i] (biases, exact widening of the bf16
+// value); mode 2: gate/up rows interleaved in 64-row blocks of a [2F, d]
+// tensor (`up` selects the second half of each 128-row block).
+__global__ void init_weights_kernel(void* out, long long n, uint32_t tid, uint32_t k0, uint32_t k1, int mode,
+                                    int in_features, int up) {
+  const float a = 0.034641016151377546f;   // fl32(0.02 * sqrt(3))
+  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b * 4 < n;
+       b += (long long)gridDim.x * blockDim.x) {
+    U4 x = philox((uint32_t)b, tid, 0u, 0x57454947u, k0, k1);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      long long i = b * 4 + w;
+      if (i >= n) break;
+      float u2m1 = __fsub_rn(__fmul_rn(__fadd_rn(__uint2float_rn(u4_word(x, w) >> 9), 0.5f), 2.384185791015625e-07f),
+                             1.0f);
+      __nv_bfloat16 v = __float2bfloat16_rn(__fmul_rn(a, u2m1));
+      if (mode == 1) {
+        ((float*)out)[i] = __bfloat162float(v);
+      } else if (mode == 2) {
+        long long r = i / in_features, c = i % in_features;
+        long long pr = (r / 64) * 128 + (r % 64) + (up ? 64 : 0);
+        ((__nv_bfloat16*)out)[pr * in_features + c] = v;
+      } else {
+        ((__nv_bfloat16*)out)[i] = v;
+      }
+    }
+  }
+}
+
+void launch_init_weights(void* out, long long n, uint32_t tid, uint64_t seed, int mode, int in_features, int up,
+                         cudaStream_t st) {
+  long long blocks = (n + 4 * 256 - 1) / (4 * 256);
+  int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
+  init_weights_kernel<<<grid, 256, 0, st>>>(out, n, tid, (uint32_t)seed, (uint32_t)(seed >> 32), mode,
+                                            in_features, up);
+}
+
+// ------------------------------------------------------------------ embedding
+__global__ void embed_kernel(const int* tok, const int* n_dev, int n_host, const __nv_bfloat16* emb, float* x,
+                             int d) {
+  const int n = n_dev ? *n_dev : n_host;
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const __nv_bfloat162* e = (const __nv_bfloat162*)(emb + (size_t)tok[r] * d);
+    float2* o = (float2*)(x + (size_t)r * d);
+    for (int c = threadIdx.x; c < d / 2; c += blockDim.x) o[c] = __bfloat1622float2(e[c]);
+  }
+}
+
+void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb, float* x, int d, cudaStream_t st) {
+  embed_kernel<<<148 * 4, 256, 0, st>>>(tok, n_dev, n_host, (const __nv_bfloat16*)emb, x, d);
+}
+
+// -------------------------------------------------------------------- RMSNorm
+// h[r] = bf16( x[src] / sqrt(mean(x[src]^2) + eps) * gamma ),  src = gather ? gather[r] : r
+__global__ void rmsnorm_kernel(const float* x, const int* gather, const int* n_dev, int n_host, const float* gamma,
+                               __nv_bfloat16* h, int d, float eps) {
+  __shared__ float red[32];
+  const int n = n_dev ? *n_dev : n_host;
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const int src = gather ? gather[r] : r;
+    const float4* xr = (const float4*)(x + (size_t)src * d);
+    float ss = 0.f;
+    for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+      float4 v = xr[c];
+      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+      v = warp_sum(v);
+      if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
+    __syncthreads();
+    __nv_bfloat162* hr = (__nv_bfloat162*)(h + (size_t)r * d);
+    const float4* g4 = (const float4*)gamma;
+    for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+      float4 v = xr[c], g = g4[c];
+      hr[2 * c] = __floats2bfloat162_rn(v.x * inv * g.x, v.y * inv * g.y);
+      hr[2 * c + 1] = __floats2bfloat162_rn(v.z * inv * g.z, v.w * inv * g.w);
+    }
+  }
+}
+
+void launch_rmsnorm(const float* x, const int* gather, const int* n_dev, int n_host, const float* gamma, void* h,
+                    int d, float eps, cudaStream_t st) {
+  rmsnorm_kernel<<<148 * 4, 256, 0, st>>>(x, gather, n_dev, n_host, gamma, (__nv_bfloat16*)h, d, eps);
+}
+
+// -------------------------------------------------------- RoPE + KV append
+// qkv row r (fp32, bias already added): [q heads | k heads | v heads] x hd.
+// Rotate-half RoPE at position row_pos[r] (angle in fp64, then fp32 sincos
+// of the reduced angle), q -> q_out[r][H][hd] bf16, k/v -> KV page.
+__global__ void rope_append_kernel(const float* qkv, const int* n_dev, int n_host, const int* row_pos,
+                                   const int* row_pt, const int* page_table, int maxp, __nv_bfloat16* q_out,
+                                   uint8_t* kv_pool, ModelDims m, int layer, const double* inv_freq) {
+  extern __shared__ float cs[];   // [hd/2] cos, [hd/2] sin
+  const int n = n_dev ? *n_dev : n_host;
+  const int half = m.hd / 2, W = (m.H + 2 * m.KV) * m.hd;
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const int pos = row_pos[r];
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
+      double ang = (double)pos * inv_freq[i];
+      ang = ang - 6.283185307179586 * floor(ang / 6.283185307179586);
+      float s, c;
+      sincosf((float)ang, &s, &c);
+      cs[i] = c; cs[half + i] = s;
+    }
+    __syncthreads();
+    const float* row = qkv + (size_t)r * W;
+    const int page = page_table[(size_t)row_pt[r] * maxp + pos / kPage];
+    const int prow = pos % kPage;
+    uint8_t* pbase = kv_pool + (size_t)page * m.page_bytes;
+    // q and k: rotated pairs
+    for (int e = threadIdx.x; e < (m.H + m.KV) * half; e += blockDim.x) {
+      const int head = e / half, i = e % half;
+      const float* src = row + head * m.hd;
+      const float x1 = src[i], x2 = src[i + half], c = cs[i], s = cs[half + i];
+      const float o1 = x1 * c - x2 * s, o2 = x2 * c + x1 * s;
+      if (head < m.H) {
+        __nv_bfloat16* dst = q_out + ((size_t)r * m.H + head) * m.hd;
+        dst[i] = __float2bfloat16(o1); dst[i + half] = __float2bfloat16(o2);
+      } else {
+        const int kh = head - m.H;
+        __nv_bfloat16* dst = (__nv_bfloat16*)(pbase + ((size_t)((layer * m.KV + kh) * 2 + 0) * kPage + prow) * m.hd * 2);
+        dst[i] = __float2bfloat16(o1); dst[i + half] = __float2bfloat16(o2);
+      }
+    }
+    for (int e = threadIdx.x; e < m.KV * m.hd; e += blockDim.x) {
+      const int kh = e / m.hd, i = e % m.hd;
+      __nv_bfloat16* dst = (__nv_bfloat16*)(pbase + ((size_t)((layer * m.KV + kh) * 2 + 1) * kPage + prow) * m.hd * 2);
+      dst[i] = __float2bfloat16(row[(m.H + m.KV) * m.hd + e]);
+    }
+    __syncthreads();
+  }
+}
+
+void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const int* row_pos, const int* row_pt,
+                        const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
+                        const double* inv_freq, cudaStream_t st) {
+  rope_append_kernel<<<148 * 4, 256, m.hd * sizeof(float), st>>>(qkv, n_dev, n_host, row_pos, row_pt, page_table,
+                                                                 maxp, (__nv_bfloat16*)q_out, (uint8_t*)kv_pool, m,
+                                                                 layer, inv_freq);
+}
+
+// ------------------------------------------------------------- prompt fork
+// Copy the first `rows` tokens of every (layer, kv head, K|V) block of page
+// src into page dst (the G siblings' private copy of a partial prompt page).
+__global__ void kv_fork_kernel(const int* jobs, int n, uint8_t* pool, ModelDims m) {
+  const int blocks = m.L * m.KV * 2;
+  for (int j = blockIdx.x; j < n * blocks; j += gridDim.x) {
+    const int job = j / blocks, blk = j % blocks;
+    const int src = jobs[3 * job], dst = jobs[3 * job + 1], rows = jobs[3 * job + 2];
+    const int4* s = (const int4*)(pool + (size_t)src * m.page_bytes + (size_t)blk * kPage * m.hd * 2);
+    int4* d = (int4*)(pool + (size_t)dst * m.page_bytes + (size_t)blk * kPage * m.hd * 2);
+    const int n16 = rows * m.hd * 2 / 16;
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) d[i] = s[i];
+  }
+}
+
+void launch_kv_fork(const int* jobs, int n, void* kv_pool, const ModelDims& m, cudaStream_t st) {
+  if (n <= 0) return;
+  kv_fork_kernel<<<148 * 4, 256, 0, st>>>(jobs, n, (uint8_t*)kv_pool, m);
+}
+
+}  // namespace rp

@@ -1,0 +1,301 @@
+// Sampling and round control on the device (K9-K11).
+//
+// sampler: token = argmax_v (logit_v / T + g_v), g_v = -ln(-ln u_v) with
+//   u_v from word v&3 of Philox4x32-10(ctr=(v>>2, t, uid, round_id),
+//   key=seed) (readings Z9-Z11); trace mode masks EOS before the trace
+//   length L and forces it at t = L.  Per-row argmax is a packed
+//   (orderable value, ~index) atomicMax, so the result is independent of the
+//   order CTAs finish in.
+// ctl: one CTA per step.  Finish detection (EOS / cap), per-prompt finished
+//   counters, race-to-completion acceptance in (step, prompt index) order
+//   (P:116-119), round_done, stable prefix-sum compaction of the
+//   live list, KV page free/alloc from a LIFO free list, and the next step's
+//   attention work list.  No host synchronisation inside a step.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rp {
+
+// ------------------------------------------------------------------ sampler
+constexpr int SAMP_CHUNK = 4096;   // vocab entries per work unit
+
+__global__ void __launch_bounds__(256) sampler_kernel(const float* __restrict__ logits, int V, int row_div, RoundDev R,
+                                                       uint32_t k0, uint32_t k1, float inv_temp, uint32_t round_id) {
+  const int n = R.ctl->n_live;
+  const int t = R.ctl->t;
+  const int chunks = (V + SAMP_CHUNK - 1) / SAMP_CHUNK;
+  __shared__ unsigned long long red[8];
+  for (int u = blockIdx.x; u < n * chunks; u += gridDim.x) {
+    const int i = u / chunks, ch = u % chunks;
+    const int s = R.live[i];
+    const int L = R.trace ? R.trace_L[s] : 0x7FFFFFFF;
+    if (R.trace && t == L) {                       // forced EOS at the trace length
+      if (ch == 0 && threadIdx.x == 0) atomicMax(&R.best[i], pack_arg(INFINITY, (uint32_t)R.eos));
+      continue;
+    }
+    const uint32_t uid = (uint32_t)(R.p_gid[R.slot_prompt[s]] * R.G + R.slot_j[s]);
+    const float* lr = logits + (size_t)(i / row_div) * V;
+    unsigned long long best = 0ull;
+    const int v_end = min(V, (ch + 1) * SAMP_CHUNK);
+    for (int b = ch * (SAMP_CHUNK / 4) + threadIdx.x; 4 * b < v_end; b += blockDim.x) {
+      const float4 z4 = *(const float4*)(lr + 4 * b);
+      const U4 x = philox((uint32_t)b, (uint32_t)t, uid, round_id, k0, k1);
+      const float zl[4] = {z4.x, z4.y, z4.z, z4.w};
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const int v = 4 * b + w;
+        const float uu = u01(u4_word(x, w));
+        float z = zl[w] * inv_temp - logf(-logf(uu));
+        if (R.trace && v == R.eos) z = -INFINITY;   // t < L here
+        const unsigned long long p = pack_arg(z, (uint32_t)v);
+        best = p > best ? p : best;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+      best = y > best ? y : best;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long b2 = red[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) b2 = red[w] > b2 ? red[w] : b2;
+      atomicMax(&R.best[i], b2);
+    }
+    __syncthreads();
+  }
+}
+
+void launch_sampler(const float* logits, int V, int row_div, const RoundDev& R, uint64_t seed, float inv_temp,
+                    uint32_t round_id, cudaStream_t st) {
+  sampler_kernel<<<148 * 4, 256, 0, st>>>(logits, V, row_div, R, (uint32_t)seed, (uint32_t)(seed >> 32), inv_temp,
+                                          round_id);
+}
+
+// --------------------------------------------------------------------- ctl
+constexpr int CTL_THREADS = 1024;
+
+// Phase A (everything that does not depend on the other ranks): finish
+// detection, prompts completed at step t (index order), page frees of ended
+// sequences, and the counts exchanged between DP ranks: {k, rows still live,
+// error}.
+__device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
+  __shared__ int s_k, s_top, s_keep, s_need, s_err;
+  CtlBlock* C = R.ctl;
+  const int n = C->n_live;
+  const int t = C->t;
+  const int tid = threadIdx.x;
+  if (R.trace_buf && t <= R.trace_steps) {
+    int* tb = R.trace_buf + (size_t)(t - 1) * (2 + R.S);
+    for (int i = tid; i < n; i += CTL_THREADS) tb[2 + i] = R.live[i];
+    if (tid == 0) tb[0] = n;
+  }
+  for (int i = tid; i < n; i += CTL_THREADS) {
+    const int s = R.live[i];
+    const int tok = (int)unpack_idx(R.best[i]);
+    R.tok_out[(size_t)s * R.cap + t - 1] = tok;
+    R.gen[s] = t;
+    if (appended) R.kv_len[s] += 1;
+    const bool fin = tok == R.eos;
+    const bool capped = !fin && t >= R.cap;
+    R.status[s] = fin ? ST_FINISHED : capped ? ST_CAPPED : ST_LIVE;
+    if (fin || (capped && R.kind == 1)) atomicAdd(&R.p_cnt[R.slot_prompt[s]], 1);
+  }
+  if (tid == 0) { s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; }
+  __syncthreads();
+  // prompts completing at step t, in prompt-index order
+  for (int base = 0; base < R.n_prompts; base += CTL_THREADS) {
+    const int p = base + tid;
+    int flag = 0;
+    if (p < R.n_prompts && R.p_state[p] == PS_RUNNING && R.p_cnt[p] == R.G) flag = 1;
+    int tot;
+    const int off = block_exscan(flag, &tot, scan_sm);
+    if (flag) { R.p_state[p] = PS_COMPLETE; R.comp_list[s_k + off] = p; }
+    __syncthreads();
+    if (tid == 0) s_k += tot;
+    __syncthreads();
+  }
+  // free the private pages of sequences that ended; count survivors and the
+  // pages they need for the next append
+  for (int base = 0; base < n; base += CTL_THREADS) {
+    const int i = base + tid;
+    int cnt = 0, s = -1, keep = 0, need = 0;
+    if (i < n) {
+      s = R.live[i];
+      if (R.status[s] != ST_LIVE) {
+        const int used = (R.kv_len[s] + kPage - 1) / kPage;
+        cnt = max(0, used - R.own0[s]);
+      } else {
+        keep = 1;
+        if (R.kv_len[s] % kPage == 0) {
+          need = 1;
+          if (R.kv_len[s] / kPage >= R.maxp) atomicExch(&s_err, 2);
+        }
+      }
+    }
+    int tot, tk, tn;
+    const int off = block_exscan(cnt, &tot, scan_sm);
+    block_exscan(keep, &tk, scan_sm);
+    block_exscan(need, &tn, scan_sm);
+    for (int c = 0; c < cnt; ++c)
+      R.free_stack[s_top + off + c] = R.page_table[(size_t)s * R.maxp + R.own0[s] + c];
+    __syncthreads();
+    if (tid == 0) { s_top += tot; s_keep += tk; s_need += tn; }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (s_need > s_top && !s_err) s_err = 1;
+    C->free_top = s_top;
+    C->k_step = s_k;
+    C->n_next = s_keep;
+    C->need_pages = s_need;
+    R.ks_local[0] = s_k; R.ks_local[1] = s_keep; R.ks_local[2] = s_err;
+    if (R.world == 1) { R.ks[0] = s_k; R.ks[1] = s_keep; R.ks[2] = s_err; }
+  }
+}
+
+// Phase B: the DP cutoff (S:289-297 under sharding): rank r admits
+// min(k_r, max(0, target - acc - sum_{r'<r} k_r')) of its completed prompts,
+// lowest index first; then stable compaction, page allocation, next-step
+// inputs and attention items, and the (globally identical) done decision.
+__device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
+  __shared__ int s_take, s_acc_new, s_next_global, s_err;
+  CtlBlock* C = R.ctl;
+  const int n = C->n_live;
+  const int t = C->t;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    const int acc = C->acc;
+    int take = 0, total = 0, nextg = 0, err = 0;
+    for (int r = 0; r < R.world; ++r) {
+      const int kr = R.ks[3 * r];
+      const int tr = min(kr, max(0, R.target - acc - total));
+      if (r == R.rank) take = tr;
+      total += tr;
+      nextg += R.ks[3 * r + 1];
+      err = max(err, R.ks[3 * r + 2]);
+    }
+    s_take = take; s_acc_new = acc + total; s_next_global = nextg; s_err = err;
+  }
+  __syncthreads();
+  for (int r = tid; r < s_take; r += CTL_THREADS) {
+    const int p = R.comp_list[r];
+    R.p_state[p] = PS_ACCEPTED;
+    R.accept_order[C->acc_local + r] = p;
+  }
+  const int top = C->free_top;
+  int kept = 0, alloc = 0, items = 0;
+  if (!s_err) {
+    for (int base = 0; base < n; base += CTL_THREADS) {
+      const int i = base + tid;
+      int keep = 0, need = 0, ns = 0, s = -1;
+      if (i < n) {
+        s = R.live[i];
+        keep = R.status[s] == ST_LIVE;
+        if (keep) {
+          need = (R.kv_len[s] % kPage) == 0;
+          ns = (R.kv_len[s] + 1 + kAttnChunk - 1) / kAttnChunk;
+        }
+      }
+      int tk, ta, ti;
+      const int ok = block_exscan(keep, &tk, scan_sm);
+      const int oa = block_exscan(need, &ta, scan_sm);
+      const int oi = block_exscan(ns, &ti, scan_sm);
+      if (keep) {
+        const int pos = kept + ok;
+        const int kv = R.kv_len[s];
+        R.live_next[pos] = s;
+        R.tok_in[pos] = R.tok_out[(size_t)s * R.cap + t - 1];
+        R.row_pos[pos] = kv;
+        R.row_pt[pos] = s;
+        if (need) R.page_table[(size_t)s * R.maxp + kv / kPage] = R.free_stack[top - 1 - (alloc + oa)];
+        const int it0 = items + oi;
+        for (int sp = 0; sp < ns; ++sp) {
+          AttnItem I;
+          I.q_row0 = pos; I.n_qtok = 1; I.pos0 = kv; I.pt_row = s;
+          I.kv_lo = sp * kAttnChunk; I.kv_hi = min(kv + 1, (sp + 1) * kAttnChunk);
+          I.nsplit = ns; I.item0 = it0;
+          R.items[it0 + sp] = I;
+        }
+      }
+      kept += tk; alloc += ta; items += ti;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += CTL_THREADS) R.best[i] = 0ull;
+  for (int i = tid; i < kept; i += CTL_THREADS) R.live[i] = R.live_next[i];
+  if (tid == 0) {
+    C->acc = s_acc_new;
+    C->acc_local += s_take;
+    C->decoded += n;
+    C->free_top = top - alloc;
+    C->n_items = items;
+    const bool done = s_acc_new >= R.target || s_next_global == 0 || s_err;
+    if (R.trace_buf && t <= R.trace_steps) {
+      int* tb = R.trace_buf + (size_t)(t - 1) * (2 + R.S);
+      tb[1] = s_acc_new | (done ? (1 << 30) : 0);
+    }
+    if (s_err) C->err = s_err;
+    if (done) {
+      C->done = 1; C->t_end = t; C->n_final = kept; C->n_live = 0;
+      C->underfilled = s_acc_new < R.target;
+    } else {
+      C->n_live = kept; C->t = t + 1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(CTL_THREADS) ctl_kernel(RoundDev R, int appended, int mode) {
+  __shared__ int scan_sm[40];
+  if (R.ctl->done) return;
+  if (mode != 2) ctl_phase_a(R, appended, scan_sm);
+  if (mode == 0) { __threadfence_block(); __syncthreads(); }
+  if (mode != 1) ctl_phase_b(R, scan_sm);
+}
+
+void launch_ctl(const RoundDev& R, int appended, int mode, cudaStream_t st) {
+  ctl_kernel<<<1, CTL_THREADS, 0, st>>>(R, appended, mode);
+}
+
+// ------------------------------------------------------------ collect pack
+// Pack the accepted prompts' responses, in acceptance order, j = 0..G-1:
+// meta[r] = {prompt (local index), j, len, status}; tokens contiguous.
+__global__ void collect_offsets_kernel(RoundDev R, int* meta, int* offs) {
+  __shared__ int scan_sm[40];
+  const int acc = R.ctl->acc_local;
+  const int nr = acc * R.G;
+  int base_off = 0;
+  for (int base = 0; base < nr; base += blockDim.x) {
+    const int r = base + threadIdx.x;
+    int len = 0;
+    if (r < nr) {
+      const int p = R.accept_order[r / R.G], j = r % R.G, s = p * R.G + j;
+      len = R.gen[s];
+      meta[4 * r] = p; meta[4 * r + 1] = j; meta[4 * r + 2] = len; meta[4 * r + 3] = R.status[s];
+    }
+    int tot;
+    const int off = block_exscan(len, &tot, scan_sm);
+    if (r < nr) offs[r] = base_off + off;
+    base_off += tot;
+  }
+  if (threadIdx.x == 0) offs[nr] = base_off;
+}
+
+__global__ void collect_copy_kernel(RoundDev R, const int* offs, int* tokens) {
+  const int nr = R.ctl->acc_local * R.G;
+  for (int r = blockIdx.x; r < nr; r += gridDim.x) {
+    const int p = R.accept_order[r / R.G], j = r % R.G, s = p * R.G + j;
+    const int len = R.gen[s];
+    for (int k = threadIdx.x; k < len; k += blockDim.x) tokens[offs[r] + k] = R.tok_out[(size_t)s * R.cap + k];
+  }
+}
+
+void launch_collect_pack(const RoundDev& R, int* meta, int* tokens, cudaStream_t st) {
+  // offs lives right after meta: meta has 4*S ints, offs S+1
+  int* offs = meta + 4 * R.S;
+  collect_offsets_kernel<<<1, 1024, 0, st>>>(R, meta, offs);
+  collect_copy_kernel<<<148, 256, 0, st>>>(R, offs, tokens);
+}
+
+}  // namespace rp

@@ -1,0 +1,89 @@
+// Device data structures and launchers of the non-GEMM kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rp {
+
+enum SeqStatus { ST_LIVE = 0, ST_FINISHED = 1, ST_CAPPED = 2, ST_ABORTED = 3 };
+enum PromptState { PS_RUNNING = 0, PS_ACCEPTED = 1, PS_COMPLETE = 2 };
+
+// One unit of attention work: a block of query tokens (decode: 1 token; the
+// g query heads of a KV head form the MMA rows) against a key range.
+struct AttnItem {
+  int q_row0;   // first query row in q/attn_out
+  int n_qtok;   // query tokens in the block
+  int pos0;     // position of the first query token (token k may see keys <= pos0+k)
+  int pt_row;   // page-table row
+  int kv_lo, kv_hi;  // key range [lo, hi) of this split (lo multiple of kPage)
+  int nsplit;   // splits of this query block (1 -> write output directly)
+  int item0;    // index of the block's first item (partials of split s at item0+s)
+};
+
+struct CtlBlock {
+  int n_live;       // rows decoded by the next step on this rank (0 => idle)
+  int t;            // step index the next decode step produces
+  int acc;          // accepted prompts (global under DP)
+  int acc_local;    // accepted prompts of this rank's slice
+  int done;         // round finished (identical on every rank)
+  int err;          // 1 = KV pool exhausted, 2 = page table overflow (any rank)
+  int n_final;      // live rows at the end (aborted in short rounds)
+  int t_end;        // last decoded step
+  int underfilled;
+  int k_step;       // prompts of this rank completed at the last step
+  int n_next;       // rows of this rank still live after the last step
+  int n_items;      // attention items of the next step
+  int free_top;     // KV free-list top
+  int need_pages;   // pages the next step allocates
+  long long decoded;  // tokens decoded this round on this rank
+};
+
+struct RoundDev {
+  int S, P, maxp, cap, G, target, kind /*0 short 1 long*/, trace, eos, n_prompts, kv_heads;
+  int world, rank;
+  int* slot_prompt; int* slot_j; int* kv_len; int* gen; int* trace_L; int* status; int* own0;
+  int* tok_out;       // [S][cap]
+  int* page_table;    // [(S + P)][maxp]
+  int* p_cnt; int* p_state; int* p_gid; int* comp_list; int* accept_order;
+  int* live; int* live_next;
+  int* tok_in; int* row_pos; int* row_pt;
+  unsigned long long* best;
+  AttnItem* items;
+  int* free_stack;
+  int* ks_local;      // [3]: prompts completed at this step, rows still live, error
+  int* ks;            // [3 * world] all-gathered ks_local (== ks_local when world == 1)
+  CtlBlock* ctl;
+  int* trace_buf; int trace_steps;   // debug: [steps][2 + S] (n, acc|done<<30, live...)
+};
+
+struct ModelDims {
+  int L, d, H, KV, hd, F, V, eos;
+  float eps;
+  size_t page_bytes;       // one page: [L][KV][2][kPage][hd] bf16
+};
+
+// weights
+void launch_init_weights(void* out, long long n, uint32_t tid, uint64_t seed, int mode, int in_features,
+                         int up, cudaStream_t st);
+// forward pieces (n = n_dev ? *n_dev : n_host)
+void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb, float* x, int d, cudaStream_t st);
+void launch_rmsnorm(const float* x, const int* gather, const int* n_dev, int n_host, const float* gamma,
+                    void* h, int d, float eps, cudaStream_t st);
+void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const int* row_pos, const int* row_pt,
+                        const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
+                        const double* inv_freq, cudaStream_t st);
+void launch_attention(const void* q, const void* kv_pool, const int* page_table, int maxp, const AttnItem* items,
+                      const int* n_items_dev, int n_items_host, void* out, float* partial, const ModelDims& m,
+                      int layer, cudaStream_t st);
+void launch_attn_merge(const AttnItem* items, const int* n_items_dev, int n_items_host, const float* partial,
+                       void* out, const ModelDims& m, cudaStream_t st);
+void launch_kv_fork(const int* jobs /*[n][3] src,dst,rows*/, int n, void* kv_pool, const ModelDims& m,
+                    cudaStream_t st);
+void launch_sampler(const float* logits, int V, int row_div, const RoundDev& R, uint64_t seed, float inv_temp,
+                    uint32_t round_id, cudaStream_t st);
+void launch_ctl(const RoundDev& R, int appended, int mode /*0 all, 1 phase A, 2 phase B*/, cudaStream_t st);
+void launch_collect_pack(const RoundDev& R, int* meta /*[acc*G][4]*/, int* tokens, cudaStream_t st);
+int attn_smem_bytes(int hd);
+int attn_init_attrs();
+
+}  // namespace rp

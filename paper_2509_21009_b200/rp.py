@@ -1,0 +1,291 @@
+"""Thin ctypes binding of librollpacker.so (include/rollpacker.h).
+
+Argument marshalling only: every step of the path runs in the library's CUDA
+kernels.  PyTorch provides device memory (weights, KV pool, workspace) and
+the stream.  There is no CPU fallback: if the library is missing, importing
+this module raises.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librollpacker.so")
+
+RP_OK, RP_EINVAL, RP_EBUSY, RP_ESTATE, RP_ENOMEM_KV, RP_ECUDA, RP_ENCCL, RP_ENOSPC = 0, -1, -2, -3, -4, -5, -6, -7
+RP_SHORT, RP_LONG, RP_TRACE = 0, 1, 4
+RP_FINISH_EOS, RP_FINISH_CAP = 1, 2
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [("n_layers", ctypes.c_int32), ("d_model", ctypes.c_int32), ("n_heads", ctypes.c_int32),
+                ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("d_ff", ctypes.c_int32),
+                ("vocab", ctypes.c_int32), ("eos_id", ctypes.c_int32), ("qkv_bias", ctypes.c_int32),
+                ("rope_theta", ctypes.c_float), ("rms_eps", ctypes.c_float), ("weight_seed", ctypes.c_uint64)]
+
+
+class RuntimeDesc(ctypes.Structure):
+    _fields_ = [("weights", ctypes.c_void_p), ("weights_bytes", ctypes.c_size_t),
+                ("kv_pool", ctypes.c_void_p), ("kv_pool_bytes", ctypes.c_size_t),
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+                ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("max_seqs", ctypes.c_int32), ("max_prompts", ctypes.c_int32), ("max_prompt_len", ctypes.c_int32),
+                ("max_prompt_tokens", ctypes.c_int32), ("max_cap", ctypes.c_int32),
+                ("sample_seed", ctypes.c_uint64), ("temperature", ctypes.c_float), ("graph_steps", ctypes.c_int32),
+                ("nccl_id", ctypes.c_void_p)]
+
+
+class Sizes(ctypes.Structure):
+    _fields_ = [("weights_bytes", ctypes.c_size_t), ("workspace_bytes", ctypes.c_size_t),
+                ("page_bytes", ctypes.c_size_t)]
+
+
+class Prompt(ctypes.Structure):
+    _fields_ = [("prompt_id", ctypes.c_int32), ("len", ctypes.c_int32),
+                ("tokens", ctypes.POINTER(ctypes.c_int32)), ("trace_lens", ctypes.POINTER(ctypes.c_int32))]
+
+
+class Status(ctypes.Structure):
+    _fields_ = [("round_id", ctypes.c_int64), ("kind", ctypes.c_int32), ("t", ctypes.c_int32),
+                ("n_live", ctypes.c_int32), ("accepted", ctypes.c_int32), ("accepted_local", ctypes.c_int32),
+                ("done", ctypes.c_int32), ("underfilled", ctypes.c_int32), ("n_prompts_local", ctypes.c_int32),
+                ("decoded_tokens", ctypes.c_int64)]
+
+
+class Response(ctypes.Structure):
+    _fields_ = [("prompt_id", ctypes.c_int32), ("j", ctypes.c_int32), ("len", ctypes.c_int32),
+                ("finish", ctypes.c_int32), ("tok_off", ctypes.c_int64)]
+
+
+EXPORTS = ["rp_query_sizes", "rp_init_model", "rp_submit_round", "rp_step", "rp_collect", "rp_long_queue",
+           "rp_free", "rp_last_error", "rp_launch_count", "rp_debug_logits", "rp_debug_trace_enable",
+           "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm"]
+
+
+def load_library(path=LIB_PATH):
+    if not os.path.exists(path):
+        raise ImportError("librollpacker.so not built (run __graft_entry__.build()); no CPU fallback exists")
+    lib = ctypes.CDLL(path)
+    P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    lib.rp_query_sizes.argtypes = [ctypes.POINTER(ModelDesc), ctypes.POINTER(RuntimeDesc), ctypes.POINTER(Sizes)]
+    lib.rp_init_model.argtypes = [ctypes.POINTER(ModelDesc), ctypes.POINTER(RuntimeDesc), ctypes.POINTER(P)]
+    lib.rp_submit_round.argtypes = [P, ctypes.POINTER(Prompt), I32, I32, I32, I32, I32, I64]
+    lib.rp_step.argtypes = [P, I32, ctypes.POINTER(Status)]
+    lib.rp_collect.argtypes = [P, ctypes.POINTER(Response), I32, ctypes.POINTER(I32), I64, ctypes.POINTER(I32),
+                               ctypes.POINTER(I64)]
+    lib.rp_long_queue.argtypes = [P, ctypes.POINTER(I32), I32, ctypes.POINTER(I32)]
+    lib.rp_free.argtypes = [P]
+    lib.rp_free.restype = None
+    lib.rp_last_error.argtypes = [P]
+    lib.rp_last_error.restype = ctypes.c_char_p
+    lib.rp_launch_count.argtypes = [P]
+    lib.rp_launch_count.restype = I64
+    lib.rp_debug_logits.argtypes = [P, ctypes.POINTER(I32), I32, ctypes.POINTER(ctypes.c_float)]
+    lib.rp_debug_trace_enable.argtypes = [P, I32]
+    lib.rp_debug_trace_get.argtypes = [P, ctypes.POINTER(I32), I32]
+    lib.rp_debug_last_logits.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(I32), I32,
+                                         ctypes.POINTER(I32)]
+    lib.rp_debug_gemm.argtypes = [P, P, P, I32, P, I32, I32, I32, I32]
+    for name in EXPORTS:
+        if name not in ("rp_free", "rp_last_error", "rp_launch_count"):
+            getattr(lib, name).restype = I32
+    return lib
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = load_library()
+    return _lib
+
+
+class RPError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("rollpacker error %d: %s" % (code, msg))
+        self.code = code
+
+
+def _i32p(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def model_desc(cfg, weight_seed=0):
+    return ModelDesc(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"],
+                     cfg["d_ff"], cfg["vocab"], cfg["eos_id"], cfg.get("qkv_bias", 1), cfg["rope_theta"],
+                     cfg["rms_eps"], weight_seed)
+
+
+class Engine:
+    """One rollout context on the current CUDA device.
+
+    cfg: model shape dict (synth.configs).  Device buffers are torch tensors
+    owned by this object and borrowed by the library."""
+
+    def __init__(self, cfg, max_seqs, max_prompts, max_prompt_len, max_prompt_tokens, max_cap, kv_pool_bytes=None,
+                 kv_fraction=0.85, weight_seed=0, sample_seed=3, temperature=1.0, graph_steps=16, rank=0, world=1,
+                 nccl_id=None, stream=None):
+        import torch
+        self.torch = torch
+        self.L = lib()
+        self.cfg = dict(cfg)
+        self.md = model_desc(cfg, weight_seed)
+        self.stream = stream if stream is not None else torch.cuda.Stream()
+        self._nccl_id = None
+        if nccl_id is not None:
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        rd = RuntimeDesc()
+        rd.rank, rd.world = rank, world
+        rd.max_seqs, rd.max_prompts, rd.max_prompt_len = max_seqs, max_prompts, max_prompt_len
+        rd.max_prompt_tokens, rd.max_cap = max_prompt_tokens, max_cap
+        rd.sample_seed, rd.temperature, rd.graph_steps = sample_seed, temperature, graph_steps
+        rd.stream = self.stream.cuda_stream
+        rd.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None
+        sz = Sizes()
+        rd.kv_pool_bytes = 1 << 30
+        self._check(self.L.rp_query_sizes(ctypes.byref(self.md), ctypes.byref(rd), ctypes.byref(sz)), None)
+        self.sizes = sz
+        dev = torch.cuda.current_device()
+        self.weights = torch.empty(sz.weights_bytes, dtype=torch.uint8, device=dev)
+        if kv_pool_bytes is None:
+            free, _ = torch.cuda.mem_get_info(dev)
+            kv_pool_bytes = int((free - sz.workspace_bytes * 1.2) * kv_fraction)
+        kv_pool_bytes = max(int(kv_pool_bytes) // sz.page_bytes, 2) * sz.page_bytes
+        rd.kv_pool_bytes = kv_pool_bytes
+        self._check(self.L.rp_query_sizes(ctypes.byref(self.md), ctypes.byref(rd), ctypes.byref(sz)), None)
+        self.sizes = sz
+        self.workspace = torch.empty(sz.workspace_bytes, dtype=torch.uint8, device=dev)
+        self.kv_pool = torch.empty(kv_pool_bytes, dtype=torch.uint8, device=dev)
+        rd.weights, rd.weights_bytes = self.weights.data_ptr(), sz.weights_bytes
+        rd.workspace, rd.workspace_bytes = self.workspace.data_ptr(), sz.workspace_bytes
+        rd.kv_pool, rd.kv_pool_bytes = self.kv_pool.data_ptr(), kv_pool_bytes
+        self.rd = rd
+        self.n_pages = kv_pool_bytes // sz.page_bytes
+        self.max_seqs, self.max_cap = max_seqs, max_cap
+        h = ctypes.c_void_p()
+        torch.cuda.synchronize()
+        self._check(self.L.rp_init_model(ctypes.byref(self.md), ctypes.byref(rd), ctypes.byref(h)), None)
+        self.h = h
+
+    # ------------------------------------------------------------------ utils
+    def _check(self, rc, h="self"):
+        if rc != RP_OK:
+            hh = self.h if h == "self" else None
+            msg = self.L.rp_last_error(hh)
+            raise RPError(rc, msg.decode() if msg else "")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.rp_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launch_count(self):
+        return int(self.L.rp_launch_count(self.h))
+
+    # --------------------------------------------------------------- the ABI
+    def submit(self, prompts, G, cap, target, long_round=False, trace=None, round_id=0):
+        """prompts: list of dicts {prompt_id, tokens} (None -> pop the queue);
+        trace: None or int array [n, G] of response lengths (trace mode)."""
+        flags = (RP_LONG if long_round else RP_SHORT) | (RP_TRACE if trace is not None else 0)
+        if prompts is None:
+            n = target
+            rc = self.L.rp_submit_round(self.h, None, n, G, cap, target, flags, round_id)
+            self._check(rc)
+            return
+        n = len(prompts)
+        arr = (Prompt * n)()
+        self._keep = []
+        for i, p in enumerate(prompts):
+            toks = np.ascontiguousarray(p["tokens"], dtype=np.int32)
+            self._keep.append(toks)
+            arr[i].prompt_id = int(p["prompt_id"])
+            arr[i].len = len(toks)
+            arr[i].tokens = _i32p(toks)
+            if trace is not None:
+                tl = np.ascontiguousarray(trace[i], dtype=np.int32)
+                self._keep.append(tl)
+                arr[i].trace_lens = _i32p(tl)
+        self._check(self.L.rp_submit_round(self.h, arr, n, G, cap, target, flags, round_id))
+
+    def step(self, max_steps=1 << 30):
+        st = Status()
+        self._check(self.L.rp_step(self.h, max_steps, ctypes.byref(st)))
+        return st
+
+    def run(self):
+        st = self.step()
+        while not st.done:
+            st = self.step()
+        return st
+
+    def collect(self):
+        n, nt = ctypes.c_int32(), ctypes.c_int64()
+        self._check(self.L.rp_collect(self.h, None, 0, None, 0, ctypes.byref(n), ctypes.byref(nt)))
+        out = (Response * max(1, n.value))()
+        toks = np.zeros(max(1, nt.value), dtype=np.int32)
+        self._check(self.L.rp_collect(self.h, out, n.value, _i32p(toks), nt.value, ctypes.byref(n), ctypes.byref(nt)))
+        res = []
+        for i in range(n.value):
+            r = out[i]
+            res.append(dict(prompt_id=r.prompt_id, j=r.j, len=r.len, finish=r.finish,
+                            tokens=toks[r.tok_off:r.tok_off + r.len].copy()))
+        return res
+
+    def long_queue(self):
+        n = ctypes.c_int32()
+        self._check(self.L.rp_long_queue(self.h, None, 0, ctypes.byref(n)))
+        ids = np.zeros(max(1, n.value), dtype=np.int32)
+        self._check(self.L.rp_long_queue(self.h, _i32p(ids), n.value, ctypes.byref(n)))
+        return ids[:n.value].tolist()
+
+    # ------------------------------------------------------------ test-only
+    def debug_logits(self, tokens):
+        toks = np.ascontiguousarray(tokens, dtype=np.int32)
+        out = np.zeros((len(toks), self.cfg["vocab"]), dtype=np.float32)
+        self._check(self.L.rp_debug_logits(self.h, _i32p(toks), len(toks),
+                                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+        return out
+
+    def debug_trace_enable(self, steps):
+        self._check(self.L.rp_debug_trace_enable(self.h, steps))
+        self._trace_steps = steps
+
+    def debug_trace(self, steps=None):
+        steps = steps or self._trace_steps
+        buf = np.zeros((steps, 2 + self.max_seqs), dtype=np.int32)
+        self._check(self.L.rp_debug_trace_get(self.h, _i32p(buf), steps))
+        out = []
+        for t in range(steps):
+            n = int(buf[t, 0])
+            if n == 0:
+                break
+            out.append(dict(t=t + 1, live=buf[t, 2:2 + n].copy(), accepted=int(buf[t, 1] & ((1 << 30) - 1)),
+                            done=int(buf[t, 1] >> 30)))
+        return out
+
+    def debug_last_logits(self):
+        out = np.zeros((self.max_seqs, self.cfg["vocab"]), dtype=np.float32)
+        slots = np.zeros(self.max_seqs, dtype=np.int32)
+        n = ctypes.c_int32()
+        self._check(self.L.rp_debug_last_logits(self.h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                                _i32p(slots), self.max_seqs, ctypes.byref(n)))
+        return out[:n.value], slots[:n.value]
+
+    def debug_gemm(self, W, X, N, splits=0):
+        """W: torch bf16 [M, K] cuda, X: torch bf16 [rows_cap, K] cuda -> Y fp32 [N, M]."""
+        torch = self.torch
+        M, K = W.shape
+        Y = torch.zeros((max(N, 1), M), dtype=torch.float32, device=W.device)
+        torch.cuda.synchronize()
+        self._check(self.L.rp_debug_gemm(self.h, W.data_ptr(), X.data_ptr(), X.shape[0], Y.data_ptr(), M, N, K,
+                                         splits))
+        return Y[:N]

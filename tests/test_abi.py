@@ -1,0 +1,77 @@
+"""CPU checks of the boundary: librollpacker.so loads and exports every symbol
+include/rollpacker.h declares; the size query is pure host logic; the binding
+refuses to run without the library (no CPU fallback)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "rollpacker.h")
+
+
+def declared_symbols():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rp_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2509_21009_b200 import rp
+    return rp.load_library()
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ("rp_init_model", "rp_submit_round", "rp_step", "rp_collect", "rp_long_queue"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+
+
+def test_binding_lists_every_export():
+    from paper_2509_21009_b200 import rp
+    assert sorted(rp.EXPORTS) == declared_symbols()
+
+
+def test_query_sizes_and_validation(lib):
+    from paper_2509_21009_b200 import rp
+    from synth.configs import model_config
+    cfg = model_config("qwen2.5-7b")
+    md = rp.model_desc(cfg)
+    rd = rp.RuntimeDesc()
+    rd.world, rd.rank = 1, 0
+    rd.max_seqs, rd.max_prompts, rd.max_prompt_len, rd.max_prompt_tokens, rd.max_cap = 256, 32, 768, 24576, 8192
+    rd.temperature = 1.0
+    rd.kv_pool_bytes = 1 << 30
+    sz = rp.Sizes()
+    assert lib.rp_query_sizes(ctypes.byref(md), ctypes.byref(rd), ctypes.byref(sz)) == 0
+    # weights: 28 layers of Qwen2.5-7B + embed + lm head, bf16 (+ fp32 biases/norms)
+    n_params = 28 * (3584 * 4608 + 3584 * 3584 + 2 * 18944 * 3584 + 3584 * 18944) + 2 * 152064 * 3584
+    assert n_params * 2 <= sz.weights_bytes < n_params * 2 * 1.01
+    assert sz.page_bytes == 28 * 4 * 2 * 64 * 128 * 2
+    bad = rp.model_desc(dict(cfg, head_dim=96))
+    assert lib.rp_query_sizes(ctypes.byref(bad), ctypes.byref(rd), ctypes.byref(sz)) == rp.RP_EINVAL
+    assert b"head_dim" in lib.rp_last_error(None)
+
+
+def test_no_cpu_fallback(tmp_path):
+    from paper_2509_21009_b200 import rp
+    with pytest.raises(ImportError):
+        rp.load_library(str(tmp_path / "missing.so"))
+
+
+def test_sass_uses_tcgen05_and_tma(lib):
+    import subprocess
+    so = os.path.join(ROOT, "paper_2509_21009_b200", "librollpacker.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in out or "UTCQMMA" in out      # tcgen05.mma
+    assert "UTMALDG" in out                           # TMA tensor loads
+    assert "LDTM" in out                              # tcgen05.ld

@@ -1,0 +1,253 @@
+"""GPU parity of the CUDA path (through the C ABI) against the oracle.
+
+Bars (BASELINE.json north_star): schedules / compaction / membership
+bit-exact given a recorded length trace; teacher-forced logits within
+max-abs 2e-2; sampled tokens equal to the oracle's Gumbel argmax wherever the
+oracle's top-2 perturbed gap exceeds 1e-2."""
+import numpy as np
+import pytest
+
+from oracle import decoder, sampler, sched, weights
+from synth import configs, gen
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_TOL = 2e-2
+GAP = 1e-2
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    t.cuda.set_device(0)
+    return t
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return configs.model_config("tiny")
+
+
+@pytest.fixture(scope="module")
+def oracle_w(tiny):
+    return weights.Weights(tiny, configs.WEIGHT_SEED)
+
+
+def make_engine(cfg, graph_steps=4, max_seqs=64, max_prompts=16, max_prompt_len=128, max_prompt_tokens=1024,
+                max_cap=512, kv_pool_bytes=64 << 20, **kw):
+    from paper_2509_21009_b200 import rp
+    return rp.Engine(cfg, max_seqs=max_seqs, max_prompts=max_prompts, max_prompt_len=max_prompt_len,
+                     max_prompt_tokens=max_prompt_tokens, max_cap=max_cap, kv_pool_bytes=kv_pool_bytes,
+                     graph_steps=graph_steps, **kw)
+
+
+# ------------------------------------------------------------------ GEMM
+@pytest.mark.parametrize("M,K", [(128, 64), (512, 256), (256, 1024), (4608, 3584), (2048, 256)])
+@pytest.mark.parametrize("N", [1, 7, 16, 100, 256, 300, 513])
+def test_gemm_tcgen05_vs_fp32(torch, tiny, M, K, N):
+    eng = _shared_engine(tiny)
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + K * 3 + N)
+    W = (torch.randn(M, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    X = (torch.randn(max(N, 1) + 40, K, device="cuda", generator=g)).to(torch.bfloat16)
+    ref = X[:N].float() @ W.float().T
+    for splits in (1, 3):
+        Y = eng.debug_gemm(W, X, N, splits=splits)
+        torch.cuda.synchronize()
+        err = (Y - ref).abs().max().item() if N else 0.0
+        assert err <= 1e-3 * max(1.0, ref.abs().max().item()), (splits, err)
+
+
+_ENG = {}
+
+
+def _shared_engine(cfg):
+    if "tiny" not in _ENG:
+        _ENG["tiny"] = make_engine(cfg)
+    return _ENG["tiny"]
+
+
+# ------------------------------------------------------ teacher-forced logits
+@pytest.mark.parametrize("n", [1, 2, 17, 63, 64, 65, 128])
+def test_teacher_forced_logits(tiny, oracle_w, n):
+    eng = _shared_engine(tiny)
+    rng = np.random.default_rng(n)
+    toks = rng.integers(0, tiny["eos_id"], size=n).astype(np.int32)
+    got = eng.debug_logits(toks)
+    want = decoder.logits(oracle_w, toks)
+    err = np.max(np.abs(got - want))
+    assert err <= LOGIT_TOL, err
+
+
+# ----------------------------------------------------------- schedules
+def _trace(n, G, seed, l_max=600, mu0=3.4):
+    return gen.length_trace(n, G, mu0, 0.6, 0.85, l_max, seed)
+
+
+def _check_round_trace(eng, L, cap, target, kind):
+    ref = sched.closed_form(L, cap, target, kind, with_steps=True)
+    got = eng.debug_trace(ref.t_end + 2)
+    assert len(got) == ref.t_end
+    for a, b in zip(got, ref.steps):
+        assert np.array_equal(a["live"], b["live"]), a["t"]
+        assert a["accepted"] == b["accepted"], a["t"]
+        assert a["done"] == b["done"], a["t"]
+    return ref
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("graph_steps", [0, 4])
+def test_short_round_schedule_bit_exact(tiny, seed, graph_steps):
+    eng = make_engine(tiny, graph_steps=graph_steps)
+    R = configs.ROUNDS["C1-tiny"]
+    n, G = 12, 4
+    ps = gen.prompts(n, 0, tiny["eos_id"], (1, 100), 10 + seed)
+    L = _trace(n, G, seed)[:, 0, :]
+    cap, target = R["short_cap"], 9
+    eng.debug_trace_enable(700)
+    eng.submit(ps, G, cap, target, trace=L, round_id=seed)
+    st = eng.run()
+    ref = _check_round_trace(eng, L, cap, target, sched.SHORT)
+    assert st.t == ref.t_end and st.accepted == len(ref.accepted) and bool(st.underfilled) == ref.underfilled
+    res = eng.collect()
+    acc = list(dict.fromkeys(r["prompt_id"] for r in res))
+    assert acc == [ps[i]["prompt_id"] for i in ref.accepted]
+    for r in res:
+        i = r["prompt_id"] - ps[0]["prompt_id"]
+        assert r["len"] == L[i, r["j"]] and r["tokens"][-1] == tiny["eos_id"]
+        assert np.all(r["tokens"][:-1] != tiny["eos_id"])
+    assert eng.long_queue() == [ps[i]["prompt_id"] for i in ref.deferred]
+    # long round over the queue: every response retained, truncated at the cap
+    q = eng.long_queue()
+    L2 = _trace(n, G, seed)[:, 1, :][[i - ps[0]["prompt_id"] for i in q]]
+    eng.debug_trace_enable(700)
+    eng.submit([ps[i - ps[0]["prompt_id"]] for i in q], G, 200, len(q), long_round=True, trace=L2, round_id=100 + seed)
+    st = eng.run()
+    ref2 = _check_round_trace(eng, L2, 200, len(q), sched.LONG)
+    res2 = eng.collect()
+    assert len(res2) == len(q) * G
+    for r in res2:
+        k = q.index(r["prompt_id"])
+        assert r["len"] == min(L2[k, r["j"]], 200)
+    eng.close()
+
+
+def test_underfilled_and_edge_rounds(tiny):
+    eng = make_engine(tiny, graph_steps=3)
+    ps = gen.prompts(3, 0, tiny["eos_id"], (64, 64), 5)          # page-aligned prompts
+    L = np.array([[5, 200], [300, 3], [4, 4]])
+    eng.debug_trace_enable(200)
+    eng.submit(ps, 2, 100, 2, trace=L)
+    st = eng.run()
+    ref = _check_round_trace(eng, L, 100, 2, sched.SHORT)
+    assert st.underfilled == 1 and ref.underfilled
+    eng.collect()
+    # all lengths 1: done at step 1 (the prefill step)
+    L1 = np.ones((3, 2), np.int32)
+    eng.submit(ps, 2, 100, 3, trace=L1)
+    st = eng.run()
+    assert st.done and st.t == 1 and st.accepted == 3
+    res = eng.collect()
+    assert all(r["len"] == 1 and r["tokens"][0] == tiny["eos_id"] for r in res)
+    eng.close()
+
+
+# ------------------------------------------------------------- sampling
+def _check_sampled(cfg, w, res, prompts_by_id, G, round_id, seed, trace=None):
+    checked = mism = 0
+    for r in res:
+        p = prompts_by_id[r["prompt_id"]]
+        seq = np.concatenate([p, r["tokens"]])
+        lg = decoder.logits(w, seq[:-1], rows=np.arange(len(p) - 1, len(seq) - 1))
+        uid = r["prompt_id"] * G + r["j"]
+        L = None if trace is None else trace[r["prompt_id"]][r["j"]]
+        for t in range(1, r["len"] + 1):
+            tok, gap = sampler.sample(lg[t - 1], t, uid, round_id, seed, eos_id=cfg["eos_id"], trace_len=L)
+            checked += 1
+            if tok != r["tokens"][t - 1]:
+                assert gap <= GAP, (r["prompt_id"], r["j"], t, tok, r["tokens"][t - 1], gap)
+                mism += 1
+    return checked, mism
+
+
+def test_sampled_tokens_trace_mode(tiny, oracle_w):
+    eng = make_engine(tiny, graph_steps=4)
+    n, G = 6, 3
+    ps = gen.prompts(n, 0, tiny["eos_id"], (5, 40), 21)
+    L = np.minimum(_trace(n, G, 7)[:, 0, :], 40)
+    eng.submit(ps, G, 128, n, long_round=True, trace=L, round_id=5)
+    eng.run()
+    res = eng.collect()
+    by_id = {p["prompt_id"]: p["tokens"] for p in ps}
+    tr = {p["prompt_id"]: L[i] for i, p in enumerate(ps)}
+    checked, mism = _check_sampled(tiny, oracle_w, res, by_id, G, 5, 3, trace=tr)
+    assert checked > 100 and mism <= checked // 50
+    eng.close()
+
+
+def test_sampled_tokens_natural_eos(tiny, oracle_w):
+    """Natural mode: EOS is sampled, never forced; responses end at EOS or the
+    cap.  Every token is checked against the oracle's argmax (gap rule)."""
+    eng = make_engine(tiny, graph_steps=2)
+    n, G = 4, 2
+    ps = gen.prompts(n, 0, tiny["eos_id"], (5, 30), 31)
+    eng.submit(ps, G, 48, n, long_round=True, round_id=9)
+    eng.run()
+    res = eng.collect()
+    assert len(res) == n * G
+    by_id = {p["prompt_id"]: p["tokens"] for p in ps}
+    checked, mism = _check_sampled(tiny, oracle_w, res, by_id, G, 9, 3)
+    assert checked >= n * G and mism <= max(1, checked // 50)
+    eng.close()
+
+
+def test_decode_step_logits(tiny, oracle_w):
+    """Logits of eager decode steps (paged decode attention, split-K GEMMs)
+    against the oracle teacher-forced on the GPU's own history."""
+    eng = make_engine(tiny, graph_steps=0)
+    n, G = 3, 2
+    ps = gen.prompts(n, 0, tiny["eos_id"], (60, 70), 41)           # crosses a page boundary
+    L = np.full((n, G), 30, np.int32)
+    eng.debug_trace_enable(64)
+    eng.submit(ps, G, 64, n, long_round=True, trace=L, round_id=1)
+    hist = {}
+    worst = 0.0
+    for step in range(8):
+        st = eng.step(1)
+        lg, slots = eng.debug_last_logits()
+        # tokens generated so far come from the trace of decoded lists + collect later;
+        # rebuild them from the final collect instead: store logits now
+        hist[st.t] = (lg.copy(), slots.copy())
+    eng.run()
+    res = eng.collect()
+    toks = {(r["prompt_id"] - ps[0]["prompt_id"], r["j"]): r["tokens"] for r in res}
+    for t, (lg, slots) in hist.items():
+        for row, s in enumerate(slots):
+            p, j = divmod(int(s), G)
+            seq = np.concatenate([ps[p]["tokens"], toks[(p, j)][:t - 1]])
+            want = decoder.logits(oracle_w, seq, rows=[len(seq) - 1])[0]
+            worst = max(worst, float(np.max(np.abs(lg[row] - want))))
+    assert worst <= LOGIT_TOL, worst
+    eng.close()
+
+
+def test_invalid_arguments(tiny):
+    from paper_2509_21009_b200 import rp
+    eng = make_engine(tiny, graph_steps=0)
+    ps = gen.prompts(2, 0, tiny["eos_id"], (4, 8), 1)
+    with pytest.raises(rp.RPError) as e:
+        eng.submit(ps, 0, 10, 1)
+    assert e.value.code == rp.RP_EINVAL
+    with pytest.raises(rp.RPError):
+        eng.submit(ps, 2, 10, 3)
+    with pytest.raises(rp.RPError):
+        eng.submit(ps, 2, 10, 1, long_round=True)
+    with pytest.raises(rp.RPError) as e:
+        eng.step()
+    assert e.value.code == rp.RP_ESTATE
+    eng.submit(ps, 2, 10, 1)
+    with pytest.raises(rp.RPError) as e:
+        eng.submit(ps, 2, 10, 1)
+    assert e.value.code == rp.RP_EBUSY
+    eng.run()
+    eng.collect()
+    eng.close()
