@@ -1,0 +1,420 @@
+"""Rollout benchmark: tail-batching RL steps on B200 through the C ABI.
+
+One "step" = one RL step = one rollout round (SHORT or LONG, chosen by the
+tail-batching planner, P:529-538 / S:271-279): submit -> prefill -> decode
+steps on device -> collect.  Workload (N=1): BASELINE.json configs[1], the
+Qwen2.5-7B-shaped random-init bf16 model, 32 prompts x G=8 per GPU (the
+per-GPU share of "256 prompts x G=8 on DP=8"), short cap 8192, target
+floor(n/1.25) (reading Z8), long rounds of P0 = target prompts from the FIFO;
+synthetic prompts and a long-tail length trace.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the oracle (plain
+CPU fp64 decoder + integer scheduler) on a bounded sample of the same
+workload on the host cores instead.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import configs, gen  # noqa: E402
+
+ETA_NUM, ETA_DEN = 5, 4          # eta = 1.25
+METRIC = "rollout decoded tokens/s (whole job), plus s/RL-step short vs long"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2-7b", choices=list(configs.ROUNDS))
+    ap.add_argument("--graph-steps", type=int, default=16)
+    ap.add_argument("--profile-steps", type=int, default=24)
+    ap.add_argument("--max-rounds-steps", type=int, default=0, help="debug: cap decode steps per round (invalid)")
+    ap.add_argument("--out", default="")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ workload
+class Workload:
+    """Deterministic prompt stream + length trace + the tail-batching planner
+    state (global FIFO of deferred prompt ids)."""
+
+    def __init__(self, cfg_name, world):
+        self.R = configs.ROUNDS[cfg_name]
+        self.model = configs.model_config(self.R["model"])
+        self.world = world
+        self.n_submit = self.R["n_submit"] * world                       # weak scaling
+        self.P0 = self.n_submit * ETA_DEN // ETA_NUM                      # floor(n / eta)
+        self.G = self.R["G"]
+        self.total = self.n_submit * 64
+        self.prompts = gen.prompts(self.total, 0, self.model["eos_id"], self.R["prompt_len"], configs.PROMPT_SEED)
+        tp = self.R["trace"]
+        self.trace = gen.length_trace(self.total, self.G, tp["mu0"], tp["sigma_p"], tp["sigma_r"], tp["l_max"],
+                                      configs.TRACE_SEED)
+        self.queue = []
+        self.next_fresh = 0
+
+    def plan(self):
+        if len(self.queue) >= self.P0:
+            ids = self.queue[:self.P0]
+            return "long", ids, self.P0, self.R["long_cap"], self.trace[ids, 1, :]
+        ids = list(range(self.next_fresh, self.next_fresh + self.n_submit))
+        return "short", ids, self.P0, self.R["short_cap"], self.trace[ids, 0, :]
+
+    def commit(self, kind, ids, accepted_ids):
+        if kind == "long":
+            self.queue = self.queue[len(ids):]
+        else:
+            self.next_fresh += len(ids)
+            acc = set(accepted_ids)
+            self.queue += [i for i in ids if i not in acc]
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    def __init__(self, idx):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", "clocks_%d.csv" % os.getpid())
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(idx), "--query-gpu=" + q, "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for k, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(k)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2509_21009_b200 import rp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    W = Workload(a.config, world)
+    cfg, G = W.model, W.G
+    # per-rank capacities
+    n_loc = math.ceil(W.n_submit / world)
+    lo, hi = W.R["prompt_len"]
+    nccl_id = None
+    if world > 1:
+        obj = [rp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    eng = rp.Engine(cfg, max_seqs=n_loc * G, max_prompts=n_loc, max_prompt_len=hi, max_prompt_tokens=n_loc * hi,
+                    max_cap=max(W.R["short_cap"], W.R["long_cap"]), graph_steps=a.graph_steps, rank=rank,
+                    world=world, nccl_id=nccl_id, sample_seed=configs.SAMPLE_SEED)
+    st_ev = eng.stream
+
+    def allgather_ids(ids):
+        if world == 1:
+            return list(ids)
+        out = [None] * world
+        dist.all_gather_object(out, list(ids))
+        return [i for part in out for i in part]
+
+    def one_round(round_no, profile=0):
+        kind, ids, target, cap, L = W.plan()
+        plist = [W.prompts[i] for i in ids]
+        h2d = sum(len(p["tokens"]) for p in plist) * 4 + L.size * 4
+        eng.submit(plist, G, cap, target if kind == "short" else len(ids), long_round=(kind == "long"), trace=L,
+                   round_id=round_no)
+        if profile:
+            eng.debug_profile_arm(profile)
+        st = eng.run()
+        res = eng.collect()
+        acc_local = list(dict.fromkeys(r["prompt_id"] for r in res))
+        acc = allgather_ids(acc_local)
+        W.commit(kind, ids, acc)
+        d2h = sum(r["len"] for r in res) * 4 + len(res) * 24
+        retained = sum(r["len"] for r in res)
+        return dict(kind=kind, t_end=st.t, decoded=st.decoded_tokens, retained=retained, h2d=h2d, d2h=d2h,
+                    accepted=st.accepted, underfilled=st.underfilled)
+
+    # ---- warm-up (the first warm-up round is profiled per kernel class)
+    prof = None
+    for r in range(a.warmup):
+        one_round(r, profile=a.profile_steps if r == 0 else 0)
+        if r == 0 and a.profile_steps:
+            prof = eng.debug_profile_read()
+    # ---- timed region
+    clk = Clocks(local) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = eng.launch_count()
+    w0 = time.perf_counter()
+    e0.record(st_ev)
+    rounds = []
+    round_ms = []
+    for r in range(a.steps):
+        rs, re_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tr0 = time.perf_counter()
+        rs.record(st_ev)
+        info = one_round(a.warmup + r)
+        re_.record(st_ev)
+        re_.synchronize()
+        info["wall_s"] = time.perf_counter() - tr0
+        info["dev_s"] = rs.elapsed_time(re_) / 1e3
+        rounds.append(info)
+    e1.record(st_ev)
+    torch.cuda.synchronize()
+    w1 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop() if clk else None
+    dev_s = e0.elapsed_time(e1) / 1e3
+    wall_s = w1 - w0
+    launches = eng.launch_count() - launches0
+    # ---- reductions over ranks
+    t = torch.tensor([dev_s, wall_s], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([sum(x["decoded"] for x in rounds), sum(x["retained"] for x in rounds),
+                        sum(x["h2d"] for x in rounds), sum(x["d2h"] for x in rounds), launches],
+                       dtype=torch.float64, device="cuda")
+    per_round = torch.tensor([x["dev_s"] for x in rounds], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        dist.all_reduce(per_round, op=dist.ReduceOp.MAX)
+    dev_s, wall_s = t.tolist()
+    decoded, retained, h2d, d2h, launches_all = tot.tolist()
+    per_round = per_round.tolist()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    short = [s for s, x in zip(per_round, rounds) if x["kind"] == "short"]
+    long_ = [s for s, x in zip(per_round, rounds) if x["kind"] == "long"]
+    value = decoded / dev_s
+    line = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": round(1e3 * dev_s / a.steps, 2),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (random-init Qwen2.5-7B-shaped weights, seeded prompts, lognormal length trace)",
+        "config": {"workload": "BASELINE configs[1]: Qwen2.5-7B-shaped, %d prompts x G=%d per GPU, short cap %d, "
+                               "target floor(n/1.25), tail batching (eta=1.25), trace mode" % (
+                                   W.R["n_submit"], G, W.R["short_cap"]),
+                   "global_prompts_per_short_round": W.n_submit, "P0": W.P0, "G": G,
+                   "short_cap": W.R["short_cap"], "long_cap": W.R["long_cap"],
+                   "parallelism": "dp%d" % world, "l2": "inputs larger than L2 (15 GB weights streamed per step)",
+                   "graph_steps": a.graph_steps},
+        "per_gpu_tokens_per_s": round(value / world, 1),
+        "retained_tokens_per_s": round(retained / dev_s, 1),
+        "speculation_waste": round(decoded / max(1.0, retained), 3),
+        "s_per_rl_step": {"short_mean": round(statistics.mean(short), 3) if short else None,
+                          "long_mean": round(statistics.mean(long_), 3) if long_ else None,
+                          "all_mean": round(dev_s / a.steps, 3)},
+        "rounds": [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in x.items()} for x in rounds],
+        "e2e": {"value": round(decoded / wall_s, 1), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(h2d / a.steps), "d2h_bytes_per_step": int(d2h / a.steps)},
+        "gpu_launches": int(launches_all),
+        "clocks": clocks,
+    }
+    if prof is not None:
+        line["roofline"], line["kernel_profile"] = roofline(prof, cfg)
+    if world == 1:
+        line["cpu_baseline"] = cpu_baseline(W, quick=True)
+    print(json.dumps(line))
+    if a.out:
+        with open(a.out, "w") as f:
+            f.write(json.dumps(line) + "\n")
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def roofline(prof, cfg):
+    """Dominant kernel class of the profiled decode steps and its roofline.
+    Algorithmic bytes per launch:
+      GEMM (weight stream) = M*K*2 + N*K*2 + N*M*out_bytes (+ N*M*4 read for residual epilogues)
+      attention = sum over rows of ctx * KV * hd * 2 (K,V) * 2 B + q/out rows."""
+    hbm, tf_burst, tf_sus, src = load_peaks()
+    d, H, KV, hd, F, V, L = (cfg[k] for k in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ff", "vocab",
+                                              "n_layers"))
+    steps = max(1, prof["steps"])
+    B = prof["rows"] / steps                          # mean live rows per profiled step
+    ctx = prof["ctx"] / steps                         # mean sum of contexts per step
+    ms, cnt = prof["ms"], prof["launches"]
+    qkvw = (H + 2 * KV) * hd
+    gemm_bytes = {
+        "gemm_qkv": qkvw * d * 2 + B * d * 2 + B * qkvw * 4,
+        "gemm_o": d * H * hd * 2 + B * H * hd * 2 + 2 * B * d * 4,
+        "gemm_gu": 2 * F * d * 2 + B * d * 2 + B * F * 2,
+        "gemm_down": d * F * 2 + B * F * 2 + 2 * B * d * 4,
+        "gemm_lm": V * d * 2 + B * d * 2 + B * V * 4,
+    }
+    gemm_flops = {"gemm_qkv": 2 * B * qkvw * d, "gemm_o": 2 * B * d * H * hd, "gemm_gu": 2 * B * 2 * F * d,
+                  "gemm_down": 2 * B * d * F, "gemm_lm": 2 * B * V * d}
+    attn_bytes = ctx * KV * hd * 2 * 2 + B * H * hd * 2 * 2
+    total = sum(ms.values())
+    dom = max(ms, key=lambda k: ms[k])
+    per_launch_ms = ms[dom] / max(1, cnt[dom])
+    detail = {k: {"ms_per_step": round(ms[k] / steps, 4), "share": round(ms[k] / total, 4),
+                  "launches_per_step": round(cnt[k] / steps, 2)} for k in ms if cnt[k]}
+    for k in gemm_bytes:
+        if cnt.get(k):
+            t = ms[k] / cnt[k] / 1e3
+            detail[k]["hbm_gbs"] = round(gemm_bytes[k] / t / 1e9, 1)
+            detail[k]["tflops"] = round(gemm_flops[k] / t / 1e12, 1)
+    if cnt.get("attention"):
+        t = ms["attention"] / cnt["attention"] / 1e3
+        detail["attention"]["hbm_gbs"] = round(attn_bytes / t / 1e9, 1)
+    if dom == "attention":
+        ach = attn_bytes / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4)}
+    elif dom in gemm_bytes:
+        t = per_launch_ms / 1e3
+        fl = gemm_flops[dom] / t / 1e12
+        by = gemm_bytes[dom] / t / 1e9
+        if gemm_flops[dom] / gemm_bytes[dom] * 1e-3 > tf_sus / hbm:   # above the ridge: tensor bound
+            roof = {"bound": "tensor", "achieved": round(fl, 1), "peak": tf_sus, "unit": "TFLOP/s",
+                    "frac": round(fl / tf_sus, 4)}
+        else:
+            roof = {"bound": "hbm", "achieved": round(by, 1), "peak": hbm, "unit": "GB/s", "frac": round(by / hbm, 4)}
+    else:
+        roof = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None}
+    roof.update({"kernel": dom, "traffic": None, "peak_source": src, "share_of_step": round(ms[dom] / total, 4),
+                 "mean_live_rows": round(B, 1), "mean_ctx_per_row": round(ctx / max(B, 1), 1),
+                 "measured": "CUDA events around each launch of %d eager decode steps (first warm-up round)" % steps})
+    return roof, detail
+
+
+# ------------------------------------------------------------------ oracle (CPU)
+def oracle_sample(W, n_tok=4, prompt_len=32):
+    """The oracle as it stands, on a bounded sample of the same workload: a
+    Qwen2.5-7B-shaped decoder truncated to ONE layer at full width + the full
+    LM head; prefill one prompt, then decode n_tok tokens one at a time.
+    Returns seconds per decoded token extrapolated to the full depth
+    (t_layer * n_layers + t_lm), and the scheduler oracle's us/round."""
+    from oracle import decoder, weights, sched
+    cfg1 = dict(W.model, n_layers=1)
+    w = weights.Weights(cfg1, configs.WEIGHT_SEED, use_c=True)
+    w.layer(0); w.lm_head()
+    dec = decoder.KVDecoder(w)
+    toks = W.prompts[0]["tokens"][:prompt_len]
+    dec.step(toks)
+    t_tot = 0.0
+    tok = int(toks[-1])
+    for _ in range(n_tok):
+        t0 = time.perf_counter()
+        dec.step([tok])
+        t_tot += time.perf_counter() - t0
+    # split the per-step time into layer and LM-head parts
+    h = np.zeros((1, cfg1["d_model"]))
+    t0 = time.perf_counter()
+    for _ in range(n_tok):
+        h @ np.asarray(w.lm_head(), np.float64).T
+    t_lm = (time.perf_counter() - t0) / n_tok
+    t_layer = max(t_tot / n_tok - t_lm, 1e-9)
+    per_tok = t_layer * W.model["n_layers"] + t_lm
+    # scheduler oracle on this round's trace
+    kind, ids, target, cap, L = W.plan()
+    t0 = time.perf_counter()
+    sched.closed_form(L, cap, target, sched.SHORT if kind == "short" else sched.LONG)
+    us_round = (time.perf_counter() - t0) * 1e6
+    return per_tok, us_round, t_layer, t_lm
+
+
+def cpu_baseline(W, quick=True):
+    per_tok, us_round, t_layer, t_lm = oracle_sample(W, n_tok=3 if quick else 6)
+    cores = os.cpu_count()
+    return {"value": round(1.0 / per_tok, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": "fp64 NumPy oracle, Qwen2.5-7B-shaped: 1 layer at full width + LM head, 1 sequence, "
+                      "3 decode steps after a 32-token prefill; per-token time extrapolated to 28 layers "
+                      "(t_layer=%.3fs, t_lm=%.3fs); scheduler oracle %.0f us/round" % (t_layer, t_lm, us_round)}
+
+
+def run_reference(a):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    W = Workload(a.config, 1)
+    for _ in range(a.warmup):
+        oracle_sample(W, n_tok=1)
+    t0 = time.perf_counter()
+    per = []
+    for _ in range(a.steps):
+        per_tok, _, _, _ = oracle_sample(W, n_tok=2)
+        per.append(per_tok)
+    wall = time.perf_counter() - t0
+    value = 1.0 / statistics.mean(per)
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 * wall / a.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "BASELINE configs[1] (bounded oracle sample)"},
+            "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": "per step: 1-layer full-width Qwen2.5-7B-shaped fp64 oracle + LM head, "
+                                       "2 decode steps, extrapolated to 28 layers"},
+            "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -171,6 +171,10 @@ int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, i
  * drain.  ids_out may be NULL to query *n_out. */
 int rp_long_queue(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out);
 
+/* Fill out[128] with a fresh ncclUniqueId (rank 0 of a DP group creates it
+ * and broadcasts it, e.g. with torch.distributed, before rp_init_model). */
+int rp_nccl_unique_id(void* out);
+
 /* Destroy a context (does not free caller-owned device memory). */
 void rp_free(void* ctx);
 
@@ -199,6 +203,29 @@ int rp_debug_trace_get(void* ctx, int32_t* buf, int32_t steps);
 /* Logits of the most recent decode step (rows in the live order of that step)
  * and the slots of those rows; requires graph_steps <= 1. */
 int rp_debug_last_logits(void* ctx, float* logits_out, int32_t* slots_out, int32_t max_rows, int32_t* n_rows);
+
+/* Kernel classes of rp_debug_profile. */
+#define RP_PROF_EMBED 0
+#define RP_PROF_RMSNORM 1
+#define RP_PROF_GEMM_QKV 2
+#define RP_PROF_ROPE 3
+#define RP_PROF_ATTN 4
+#define RP_PROF_MERGE 5
+#define RP_PROF_GEMM_O 6
+#define RP_PROF_GEMM_GU 7
+#define RP_PROF_GEMM_DOWN 8
+#define RP_PROF_GEMM_LM 9
+#define RP_PROF_SAMPLER 10
+#define RP_PROF_CTL 11
+#define RP_PROF_NCCL 12
+#define RP_PROF_N 13
+/* Per-kernel-class timing.  steps > 0 arms profiling: the next `steps` decode
+ * steps run eagerly (no graph) with every launch bracketed by CUDA events on
+ * the context's stream.  steps == 0 reads the totals: ms_out[RP_PROF_N]
+ * (summed milliseconds), counts_out[RP_PROF_N] (launches),
+ * rows_ctx_steps[3] = {sum of live rows, sum of attention context tokens,
+ * profiled steps}.  Any pointer may be NULL. */
+int rp_debug_profile(void* ctx, int32_t steps, double* ms_out, int64_t* counts_out, int64_t* rows_ctx_steps);
 
 /* Run the tcgen05 GEMM alone on device pointers: Y[n][m] = sum_k W[m][k] X[n][k]
  * (W bf16 [M,K], X bf16 [N,K] with N <= rows_cap rows allocated, Y fp32 [N,M]);

@@ -19,9 +19,37 @@ Tensor ids (DESIGN.md §3 Z12 table):
     embed 0x10000000, lm_head 0x10000001,
     layer l: 0x100*(l+1) + {q:0, k:1, v:2, bq:3, bk:4, bv:5, o:6, gate:7, up:8, down:9}
 """
+import ctypes
+import os
+
 import numpy as np
 
 from .philox import stream_words, philox4x32
+
+_CLIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "c", "liboracle_weights.so")
+
+
+def build_c():
+    """Compile oracle/c/weights.c (gcc -O2 -fopenmp; -ffp-contract=off keeps
+    the single fp32 rounding of the formula)."""
+    import subprocess
+    src = os.path.join(os.path.dirname(_CLIB), "weights.c")
+    if os.path.exists(_CLIB) and os.path.getmtime(_CLIB) >= os.path.getmtime(src):
+        return _CLIB
+    subprocess.run(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-shared", "-fPIC", src, "-o", _CLIB],
+                   check=True)
+    return _CLIB
+
+
+def tensor_c(seed, tid, shape):
+    """Same values as `tensor`, from the plain-C generator (large tensors)."""
+    build_c()
+    lib = ctypes.CDLL(_CLIB)
+    n = int(np.prod(shape))
+    out = np.empty(n, np.float32)
+    lib.oracle_weights(out.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(0), ctypes.c_int64(n),
+                       ctypes.c_uint32(tid), ctypes.c_uint64(seed))
+    return out.reshape(shape)
 
 WEIGHT_TAG = 0x57454947          # 'WEIG'
 A_SCALE = np.float32(0.02 * np.sqrt(3.0))
@@ -70,12 +98,12 @@ class Weights:
     """Lazily generated weights of a model config (dict with the keys of
     synth.configs).  Caches tensors as float32 (= the bf16 values)."""
 
-    def __init__(self, cfg, seed):
-        self.cfg, self.seed, self._c = cfg, seed, {}
+    def __init__(self, cfg, seed, use_c=False):
+        self.cfg, self.seed, self._c, self.use_c = cfg, seed, {}, use_c
 
     def _get(self, key, tid, shape):
         if key not in self._c:
-            self._c[key] = tensor(self.seed, tid, shape)
+            self._c[key] = (tensor_c if self.use_c else tensor)(self.seed, tid, shape)
         return self._c[key]
 
     def layer(self, l):

@@ -112,6 +112,15 @@ struct RpCtx {
   int* trace_dev = nullptr;
   bool step_logits_valid = false;
 
+  // per-kernel-class profiling of eager decode steps (rp_debug_profile)
+  int prof_steps_left = 0;
+  bool capturing = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_cls;
+  double prof_ms[RP_PROF_N] = {0};
+  long long prof_cnt[RP_PROF_N] = {0};
+  long long prof_rows = 0, prof_ctx = 0, prof_step_count = 0;
+
   int fail(int code, const char* fmt, ...) {
     char buf[512];
     va_list ap;
@@ -157,8 +166,8 @@ static Sizes compute_sizes(const rp_model_desc* md, const rp_runtime_desc* rd) {
     const int sp = gemm_pick_splits(s[0], s[1], kSMs);
     if (sp > 1) mx = std::max(mx, (size_t)(s[0] / 128) * nch * sp * 256 * 128);
   }
-  // rp_debug_gemm may request up to 16 splits of an arbitrary shape: keep >= 4M floats
-  z.part_floats = std::max(mx, (size_t)1 << 22);
+  // rp_debug_gemm may request splits of an arbitrary shape: keep >= 16M floats
+  z.part_floats = std::max(mx, (size_t)1 << 24);
   z.apart_floats = (size_t)std::max(z.max_items_dec, z.max_items_pre) * md->n_kv_heads * 16 * (md->head_dim + 2);
   return z;
 }
@@ -291,6 +300,23 @@ static int validate(const rp_model_desc* md, const rp_runtime_desc* rd, std::str
 }
 
 // ------------------------------------------------------------------ model forward
+// Profiling brackets: when an eager decode step is profiled, every launch is
+// bracketed by CUDA events on the launching stream.
+struct ProfScope {
+  RpCtx* c; int cls; bool on;
+  ProfScope(RpCtx* c_, int cls_) : c(c_), cls(cls_), on(c_->prof_steps_left > 0 && !c_->capturing) {
+    if (on) {
+      cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, c->st);
+      c->ev.push_back(e); c->ev_cls.push_back(-1);
+    }
+  }
+  ~ProfScope() {
+    if (on) {
+      cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, c->st);
+      c->ev.push_back(e); c->ev_cls.push_back(cls);
+    }
+  }
+};
 static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, int n_host, int splits, int epi,
                  void* out, int ldo, const float* bias) {
   GemmArgs a{};
@@ -309,20 +335,29 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
   const int qkvw = (m.H + 2 * m.KV) * m.hd;
   const int sp_qkv = decode ? c->s_qkv : 1, sp_o = decode ? c->s_o : 1, sp_gu = decode ? c->s_gu : 1,
             sp_down = decode ? c->s_down : 1;
-  launch_embed(tok, n_dev, n_host, c->emb, c->x, m.d, c->st); c->launches++;
+  { ProfScope ps(c, RP_PROF_EMBED); launch_embed(tok, n_dev, n_host, c->emb, c->x, m.d, c->st); c->launches++; }
   for (int l = 0; l < m.L; ++l) {
     LayerW& w = c->layers[l];
-    launch_rmsnorm(c->x, nullptr, n_dev, n_host, w.ln1, c->h, m.d, m.eps, c->st); c->launches++;
-    gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_F32, c->qkv, qkvw, w.bqkv);
-    launch_rope_append(c->qkv, n_dev, n_host, row_pos, row_pt, c->R.page_table, c->R.maxp, c->q,
-                       c->rd.kv_pool, m, l, c->inv_freq, c->st); c->launches++;
-    launch_attention(c->q, c->rd.kv_pool, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
-                     c->apart, m, l, c->st); c->launches++;
-    launch_attn_merge(items, n_items_dev, n_items_host, c->apart, c->att, m, c->st); c->launches++;
-    gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, EPI_RESID, c->x, m.d, nullptr);
-    launch_rmsnorm(c->x, nullptr, n_dev, n_host, w.ln2, c->h, m.d, m.eps, c->st); c->launches++;
-    gemm(c, w.p_gu, 2 * m.F, m.d, n_dev, n_host, sp_gu, EPI_SWIGLU, c->mid, m.F, nullptr);
-    gemm(c, w.p_down, m.d, m.F, n_dev, n_host, sp_down, EPI_RESID, c->x, m.d, nullptr);
+    { ProfScope ps(c, RP_PROF_RMSNORM);
+      launch_rmsnorm(c->x, nullptr, n_dev, n_host, w.ln1, c->h, m.d, m.eps, c->st); c->launches++; }
+    { ProfScope ps(c, RP_PROF_GEMM_QKV);
+      gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_F32, c->qkv, qkvw, w.bqkv); }
+    { ProfScope ps(c, RP_PROF_ROPE);
+      launch_rope_append(c->qkv, n_dev, n_host, row_pos, row_pt, c->R.page_table, c->R.maxp, c->q,
+                         c->rd.kv_pool, m, l, c->inv_freq, c->st); c->launches++; }
+    { ProfScope ps(c, RP_PROF_ATTN);
+      launch_attention(c->q, c->rd.kv_pool, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
+                       c->apart, m, l, c->st); c->launches++; }
+    { ProfScope ps(c, RP_PROF_MERGE);
+      launch_attn_merge(items, n_items_dev, n_items_host, c->apart, c->att, m, c->st); c->launches++; }
+    { ProfScope ps(c, RP_PROF_GEMM_O);
+      gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, EPI_RESID, c->x, m.d, nullptr); }
+    { ProfScope ps(c, RP_PROF_RMSNORM);
+      launch_rmsnorm(c->x, nullptr, n_dev, n_host, w.ln2, c->h, m.d, m.eps, c->st); c->launches++; }
+    { ProfScope ps(c, RP_PROF_GEMM_GU);
+      gemm(c, w.p_gu, 2 * m.F, m.d, n_dev, n_host, sp_gu, EPI_SWIGLU, c->mid, m.F, nullptr); }
+    { ProfScope ps(c, RP_PROF_GEMM_DOWN);
+      gemm(c, w.p_down, m.d, m.F, n_dev, n_host, sp_down, EPI_RESID, c->x, m.d, nullptr); }
   }
 }
 
@@ -330,16 +365,20 @@ static void decode_step(RpCtx* c) {
   RoundDev& R = c->R;
   const int* n_dev = &R.ctl->n_live;
   forward_layers(c, R.tok_in, n_dev, 0, R.row_pos, R.row_pt, R.items, &R.ctl->n_items, 0, true);
-  launch_rmsnorm(c->x, nullptr, n_dev, 0, c->lnf, c->h, c->m.d, c->m.eps, c->st); c->launches++;
-  gemm(c, c->p_lm, c->m.V, c->m.d, n_dev, 0, c->s_lm, EPI_F32, c->logits, c->m.V, nullptr);
-  launch_sampler(c->logits, c->m.V, 1, R, c->rd.sample_seed, 1.0f / c->rd.temperature, (uint32_t)c->round_id,
-                 c->st); c->launches++;
+  { ProfScope ps(c, RP_PROF_RMSNORM);
+    launch_rmsnorm(c->x, nullptr, n_dev, 0, c->lnf, c->h, c->m.d, c->m.eps, c->st); c->launches++; }
+  { ProfScope ps(c, RP_PROF_GEMM_LM);
+    gemm(c, c->p_lm, c->m.V, c->m.d, n_dev, 0, c->s_lm, EPI_F32, c->logits, c->m.V, nullptr); }
+  { ProfScope ps(c, RP_PROF_SAMPLER);
+    launch_sampler(c->logits, c->m.V, 1, R, c->rd.sample_seed, 1.0f / c->rd.temperature, (uint32_t)c->round_id,
+                   c->st); c->launches++; }
   if (c->rd.world == 1) {
+    ProfScope ps(c, RP_PROF_CTL);
     launch_ctl(R, 1, 0, c->st); c->launches++;
   } else {
-    launch_ctl(R, 1, 1, c->st); c->launches++;
-    ncclAllGather(R.ks_local, R.ks, 3, ncclInt32, c->comm, c->st);
-    launch_ctl(R, 1, 2, c->st); c->launches++;
+    { ProfScope ps(c, RP_PROF_CTL); launch_ctl(R, 1, 1, c->st); c->launches++; }
+    { ProfScope ps(c, RP_PROF_NCCL); ncclAllGather(R.ks_local, R.ks, 3, ncclInt32, c->comm, c->st); }
+    { ProfScope ps(c, RP_PROF_CTL); launch_ctl(R, 1, 2, c->st); c->launches++; }
   }
 }
 
@@ -352,7 +391,9 @@ static int ensure_graph(RpCtx* c) {
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
   const long long before = c->launches;
+  c->capturing = true;
   for (int i = 0; i < c->rd.graph_steps; ++i) decode_step(c);
+  c->capturing = false;
   cudaError_t e = cudaStreamEndCapture(c->st, &g);
   if (e != cudaSuccess) return c->fail(RP_ECUDA, "graph capture: %s", cudaGetErrorString(e));
   c->graph_nodes = (int)(c->launches - before);
@@ -516,6 +557,14 @@ int rp_init_model(const rp_model_desc* md, const rp_runtime_desc* rd, void** out
     return r;
   }
   *out = c;
+  return RP_OK;
+}
+
+int rp_nccl_unique_id(void* out) {
+  if (!out) return RP_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) { g_init_err = "ncclGetUniqueId failed"; return RP_ENCCL; }
+  memcpy(out, &id, sizeof id);
   return RP_OK;
 }
 
@@ -758,7 +807,24 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
   int steps = 0;
   if (!c->h_ctl->done && max_steps > 0 && (rc = ensure_graph(c))) return rc;
   while (!c->h_ctl->done && steps < max_steps) {
-    if (c->gexec) {
+    if (c->prof_steps_left > 0) {
+      const int rows = c->h_ctl->n_live;
+      const long long ctx = c->h_ctl->ctx_sum;
+      decode_step(c);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(c->st));
+      for (size_t i = 0; i + 1 < c->ev.size(); i += 2) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
+        c->prof_ms[c->ev_cls[i + 1]] += ms;
+        c->prof_cnt[c->ev_cls[i + 1]] += 1;
+      }
+      for (auto e : c->ev) cudaEventDestroy(e);
+      c->ev.clear(); c->ev_cls.clear();
+      c->prof_rows += rows; c->prof_ctx += ctx; c->prof_step_count += 1;
+      c->prof_steps_left -= 1;
+      steps += 1;
+    } else if (c->gexec) {
       CK(cudaGraphLaunch(c->gexec, c->st));
       c->launches += c->graph_nodes;
       steps += c->rd.graph_steps;
@@ -894,6 +960,23 @@ int rp_debug_last_logits(void* ctx, float* logits_out, int32_t* slots_out, int32
   memcpy(slots_out, row.data() + 2, n * 4);
   CK(cudaMemcpyAsync(logits_out, c->logits, (size_t)n * c->m.V * 4, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  return RP_OK;
+}
+
+int rp_debug_profile(void* ctx, int32_t steps, double* ms_out, int64_t* counts_out, int64_t* rows_ctx_steps) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (steps > 0) {   // arm: the next `steps` decode steps run eagerly, bracketed by events
+    c->prof_steps_left = steps;
+    for (int i = 0; i < RP_PROF_N; ++i) { c->prof_ms[i] = 0; c->prof_cnt[i] = 0; }
+    c->prof_rows = c->prof_ctx = c->prof_step_count = 0;
+    return RP_OK;
+  }
+  for (int i = 0; i < RP_PROF_N; ++i) {
+    if (ms_out) ms_out[i] = c->prof_ms[i];
+    if (counts_out) counts_out[i] = c->prof_cnt[i];
+  }
+  if (rows_ctx_steps) { rows_ctx_steps[0] = c->prof_rows; rows_ctx_steps[1] = c->prof_ctx; rows_ctx_steps[2] = c->prof_step_count; }
   return RP_OK;
 }
 

@@ -186,6 +186,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
   }
   const int top = C->free_top;
   int kept = 0, alloc = 0, items = 0;
+  long long ctx_sum = 0;
   if (!s_err) {
     for (int base = 0; base < n; base += CTL_THREADS) {
       const int i = base + tid;
@@ -198,10 +199,12 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
           ns = (R.kv_len[s] + 1 + kAttnChunk - 1) / kAttnChunk;
         }
       }
-      int tk, ta, ti;
+      int tk, ta, ti, tc;
       const int ok = block_exscan(keep, &tk, scan_sm);
       const int oa = block_exscan(need, &ta, scan_sm);
       const int oi = block_exscan(ns, &ti, scan_sm);
+      block_exscan(keep ? R.kv_len[s] + 1 : 0, &tc, scan_sm);
+      ctx_sum += tc;
       if (keep) {
         const int pos = kept + ok;
         const int kv = R.kv_len[s];
@@ -231,6 +234,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     C->decoded += n;
     C->free_top = top - alloc;
     C->n_items = items;
+    C->ctx_sum = ctx_sum;
     const bool done = s_acc_new >= R.target || s_next_global == 0 || s_err;
     if (R.trace_buf && t <= R.trace_steps) {
       int* tb = R.trace_buf + (size_t)(t - 1) * (2 + R.S);

@@ -36,6 +36,7 @@ struct CtlBlock {
   int free_top;     // KV free-list top
   int need_pages;   // pages the next step allocates
   long long decoded;  // tokens decoded this round on this rank
+  long long ctx_sum;  // sum over next-step rows of the attention context (kv_len + 1)
 };
 
 struct RoundDev {

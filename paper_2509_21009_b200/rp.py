@@ -60,7 +60,7 @@ class Response(ctypes.Structure):
 
 EXPORTS = ["rp_query_sizes", "rp_init_model", "rp_submit_round", "rp_step", "rp_collect", "rp_long_queue",
            "rp_free", "rp_last_error", "rp_launch_count", "rp_debug_logits", "rp_debug_trace_enable",
-           "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm"]
+           "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm", "rp_debug_profile", "rp_nccl_unique_id"]
 
 
 def load_library(path=LIB_PATH):
@@ -87,6 +87,9 @@ def load_library(path=LIB_PATH):
     lib.rp_debug_last_logits.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(I32), I32,
                                          ctypes.POINTER(I32)]
     lib.rp_debug_gemm.argtypes = [P, P, P, I32, P, I32, I32, I32, I32]
+    lib.rp_debug_profile.argtypes = [P, I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64),
+                                     ctypes.POINTER(I64)]
+    lib.rp_nccl_unique_id.argtypes = [P]
     for name in EXPORTS:
         if name not in ("rp_free", "rp_last_error", "rp_launch_count"):
             getattr(lib, name).restype = I32
@@ -101,6 +104,14 @@ def lib():
     if _lib is None:
         _lib = load_library()
     return _lib
+
+
+def nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    rc = lib().rp_nccl_unique_id(buf)
+    if rc != RP_OK:
+        raise RuntimeError("rp_nccl_unique_id failed: %d" % rc)
+    return buf.raw
 
 
 class RPError(RuntimeError):
@@ -279,6 +290,22 @@ class Engine:
         self._check(self.L.rp_debug_last_logits(self.h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
                                                 _i32p(slots), self.max_seqs, ctypes.byref(n)))
         return out[:n.value], slots[:n.value]
+
+    PROF_NAMES = ["embed", "rmsnorm", "gemm_qkv", "rope_append", "attention", "attn_merge", "gemm_o", "gemm_gu",
+                  "gemm_down", "gemm_lm", "sampler", "ctl", "nccl"]
+
+    def debug_profile_arm(self, steps):
+        self._check(self.L.rp_debug_profile(self.h, steps, None, None, None))
+
+    def debug_profile_read(self):
+        n = len(self.PROF_NAMES)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        rcs = (ctypes.c_int64 * 3)()
+        self._check(self.L.rp_debug_profile(self.h, 0, ms, cnt, rcs))
+        return dict(ms={k: ms[i] for i, k in enumerate(self.PROF_NAMES)},
+                    launches={k: int(cnt[i]) for i, k in enumerate(self.PROF_NAMES)},
+                    rows=int(rcs[0]), ctx=int(rcs[1]), steps=int(rcs[2]))
 
     def debug_gemm(self, W, X, N, splits=0):
         """W: torch bf16 [M, K] cuda, X: torch bf16 [rows_cap, K] cuda -> Y fp32 [N, M]."""

@@ -59,3 +59,10 @@ def test_first_element_by_hand():
     want = W.bf16_rne(np.array([w32], np.float32))[0]
     got = W.tensor(0, 0x100, (1, 1))[0, 0]
     assert got == want
+
+
+def test_c_generator_equals_numpy():
+    """oracle/c/weights.c (used for 7B-shaped baselines) equals the NumPy
+    formula element for element."""
+    for tid, shape, seed in [(W.TID_EMBED, (37, 64), 0), (W.layer_tid(3, "down"), (256, 129), 12345678901)]:
+        assert np.array_equal(W.tensor_c(seed, tid, shape), W.tensor(seed, tid, shape))
