@@ -229,9 +229,11 @@ int rp_debug_profile(void* ctx, int32_t steps, double* ms_out, int64_t* counts_o
 
 /* Run the tcgen05 GEMM alone on device pointers: Y[n][m] = sum_k W[m][k] X[n][k]
  * (W bf16 [M,K], X bf16 [N,K] with N <= rows_cap rows allocated, Y fp32 [N,M]);
- * splits = split-K factor (0 = automatic). */
+ * splits = split-K factor (0 = automatic).  Runs once to warm up, then `iters`
+ * back-to-back launches timed with CUDA events; *ms_out (may be NULL) gets the
+ * mean milliseconds per launch. */
 int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, float* Y, int32_t M, int32_t N,
-                  int32_t K, int32_t splits);
+                  int32_t K, int32_t splits, int32_t iters, float* ms_out);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,7 @@ namespace rp {
 
 constexpr int kPage = 64;          // tokens per KV page (DESIGN.md §5 D1)
 constexpr int kAttnChunk = 512;    // tokens per decode-attention split
+constexpr int kAttnFillUnits = 2 * 148;  // (row, kv head) units that fill the GPU without splits
 
 // ---------------------------------------------------------------- Philox4x32-10
 struct U4 { uint32_t x, y, z, w; };

@@ -499,16 +499,13 @@ static int init_impl(RpCtx* c) {
   const int Tcap = c->z.Tcap;
   const int qkvw = (int)((H + 2 * KV) * hd);
   for (auto& w : c->layers) {
-    if (make_tmap_bf16(&w.p_qkv.tmA, w.wqkv, qkvw, (int)d, 128) || make_tmap_bf16(&w.p_qkv.tmB, c->h, Tcap, (int)d, 32) ||
-        make_tmap_bf16(&w.p_o.tmA, w.wo, (int)d, (int)(H * hd), 128) ||
-        make_tmap_bf16(&w.p_o.tmB, c->att, Tcap, (int)(H * hd), 32) ||
-        make_tmap_bf16(&w.p_gu.tmA, w.wgu, (int)(2 * F), (int)d, 128) ||
-        make_tmap_bf16(&w.p_gu.tmB, c->h, Tcap, (int)d, 32) ||
-        make_tmap_bf16(&w.p_down.tmA, w.wd, (int)d, (int)F, 128) ||
-        make_tmap_bf16(&w.p_down.tmB, c->mid, Tcap, (int)F, 32))
+    if (make_plan(&w.p_qkv, w.wqkv, qkvw, (int)d, c->h, Tcap) ||
+        make_plan(&w.p_o, w.wo, (int)d, (int)(H * hd), c->att, Tcap) ||
+        make_plan(&w.p_gu, w.wgu, (int)(2 * F), (int)d, c->h, Tcap) ||
+        make_plan(&w.p_down, w.wd, (int)d, (int)F, c->mid, Tcap))
       return c->fail(RP_ECUDA, "cuTensorMapEncodeTiled failed");
   }
-  if (make_tmap_bf16(&c->p_lm.tmA, c->lm, (int)V, (int)d, 128) || make_tmap_bf16(&c->p_lm.tmB, c->h, Tcap, (int)d, 32))
+  if (make_plan(&c->p_lm, c->lm, (int)V, (int)d, c->h, Tcap))
     return c->fail(RP_ECUDA, "cuTensorMapEncodeTiled failed (lm head)");
   c->s_qkv = gemm_pick_splits(qkvw, (int)d, kSMs);
   c->s_o = gemm_pick_splits((int)d, (int)(H * hd), kSMs);
@@ -981,7 +978,7 @@ int rp_debug_profile(void* ctx, int32_t steps, double* ms_out, int64_t* counts_o
 }
 
 int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, float* Y, int32_t M, int32_t N,
-                  int32_t K, int32_t splits) {
+                  int32_t K, int32_t splits, int32_t iters, float* ms_out) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
   if (M % 128 || K % 64 || M <= 0 || K <= 0 || N < 0 || N > rows_cap) return c->fail(RP_EINVAL, "invalid GEMM shape");
@@ -991,11 +988,22 @@ int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, flo
   if (splits > 1 && need > c->z.part_floats) return c->fail(RP_ENOSPC, "split-K workspace too small");
   if ((M / 128) * ((N + 255) / 256) > (1 << 16)) return c->fail(RP_ENOSPC, "too many tiles");
   GemmPlan p;
-  if (make_tmap_bf16(&p.tmA, W, M, K, 128) || make_tmap_bf16(&p.tmB, X, rows_cap, K, 32))
-    return c->fail(RP_ECUDA, "tensor map");
-  gemm(c, p, M, K, nullptr, N, splits, EPI_F32, Y, M, nullptr);
+  if (make_plan(&p, W, M, K, X, rows_cap)) return c->fail(RP_ECUDA, "tensor map");
+  iters = std::max(iters, 1);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  gemm(c, p, M, K, nullptr, N, splits, EPI_F32, Y, M, nullptr);   // warm
+  CK(cudaEventRecord(e0, c->st));
+  for (int i = 0; i < iters; ++i) gemm(c, p, M, K, nullptr, N, splits, EPI_F32, Y, M, nullptr);
+  CK(cudaEventRecord(e1, c->st));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  if (ms_out) *ms_out = ms / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   return RP_OK;
 }
 

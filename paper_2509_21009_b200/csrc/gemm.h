@@ -22,7 +22,7 @@ struct GemmArgs {
 
 struct GemmPlan {
   CUtensorMap tmA;        // weights [M, K], box 64 x 128
-  CUtensorMap tmB;        // activations [rows_cap, K], box 64 x 32
+  CUtensorMap tmB16, tmB64, tmB256;   // activations [rows_cap, K], boxes of 16 / 64 / 256 rows
 };
 
 int make_tmap_bf16(CUtensorMap* map, const void* base, int rows, int cols, int box_rows);
@@ -30,5 +30,6 @@ int gemm_init_attrs();
 int gemm_smem_bytes();
 int gemm_pick_splits(int M, int K, int n_sms);
 void gemm_launch(const GemmPlan& p, const GemmArgs& a, int grid, cudaStream_t st);
+int make_plan(GemmPlan* p, const void* W, int M, int K, const void* X, int rows_cap);
 
 }  // namespace rp

@@ -136,7 +136,8 @@ __device__ __forceinline__ Item decode_item(int it, int m_tiles, int splits) {
 }
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB16,
+                    const __grid_constant__ CUtensorMap tmB64, const __grid_constant__ CUtensorMap tmB256,
                     GemmArgs a) {
   const int N = a.n_dev ? *a.n_dev : a.n_host;
   if (N <= 0) return;
@@ -169,7 +170,9 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   }
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB16) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB64) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB256) : "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -185,15 +188,24 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         Item I = decode_item(it, m_tiles, a.splits);
         const int kb0 = (int)((long)I.split * kb_total / a.splits), kb1 = (int)((long)(I.split + 1) * kb_total / a.splits);
         const int n0 = I.chunk * BN, nc = min(BN, N - n0);
-        const int nbox = (nc + 31) >> 5;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        // X boxes: one 256-row box for wide chunks, else a few 64- or 16-row boxes
+        const CUtensorMap* tb = nc > 192 ? &tmB256 : nc > 48 ? &tmB64 : &tmB16;
+        const int brow = nc > 192 ? 256 : nc > 48 ? 64 : 16;
+        const int nbox = (nc + brow - 1) / brow;
+        const int cnt = kb1 - kb0;
+        // rotate the K order per tile so the CTAs do not all request the same
+        // activation tile at the same time (an L2 hot spot); the accumulation
+        // order stays fixed per tile (deterministic, batch invariant)
+        const int rot = (I.tile * 7 + I.chunk * 3) % cnt;
+        for (int j = 0; j < cnt; ++j) {
+          const int kb = kb0 + (j + rot) % cnt;
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
-          mbar_expect_tx(fb, A_BYTES + nbox * 32 * BK * 2);
+          mbar_expect_tx(fb, A_BYTES + nbox * brow * BK * 2);
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           tma_load_2d(sa, &tmA, fb, kb * BK, I.tile * BM, pol_w);
           for (int b = 0; b < nbox; ++b)
-            tma_load_2d(sa + A_BYTES + b * 32 * BK * 2, &tmB, fb, kb * BK, n0 + 32 * b, pol_x);
+            tma_load_2d(sa + A_BYTES + b * brow * BK * 2, tb, fb, kb * BK, n0 + brow * b, pol_x);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -271,19 +283,80 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         __threadfence();
       }
       if (!last) continue;
-      // ---- epilogue proper over columns of this chunk
+      if (split && a.epi != EPI_SWIGLU) {
+        // ---- in-order split-K reduction by the last CTA of the tile.  Threads
+        // are remapped to 4 consecutive rows (float4) x columns so every load
+        // is 16 B and 8 independent loads per split are in flight per thread;
+        // the fixed split order keeps the sum deterministic.
+        const float* __restrict__ pb = a.partial + ((size_t)((I.chunk * m_tiles + I.tile) * a.splits)) * BN * BM;
+        const int r4 = (et & 31) * 4;              // rows r4..r4+3 of the tile
+        const int m4 = I.tile * BM + r4;
+        for (int cb = (et >> 5); cb < nc; cb += 4 * 8) {
+          float4 acc[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int s = 0; s < a.splits; ++s) {
+            float4 t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int col = cb + 4 * u;
+              t[u] = col < nc ? __ldcg((const float4*)(pb + (size_t)s * BN * BM + (size_t)col * BM + r4))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              acc[u].x += t[u].x; acc[u].y += t[u].y; acc[u].z += t[u].z; acc[u].w += t[u].w;
+            }
+          }
+          float4 old[8];
+          if (a.epi == EPI_RESID) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int col = cb + 4 * u;
+              if (col < nc) old[u] = *(const float4*)((float*)a.out + (size_t)(n0 + col) * a.ldo + m4);
+            }
+          }
+          float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (a.bias) bb = *(const float4*)(a.bias + m4);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int col = cb + 4 * u;
+            if (col >= nc) continue;
+            const size_t o = (size_t)(n0 + col) * a.ldo + m4;
+            float4 v = acc[u];
+            if (a.epi == EPI_RESID) {
+              v.x += old[u].x; v.y += old[u].y; v.z += old[u].z; v.w += old[u].w;
+              *(float4*)((float*)a.out + o) = v;
+            } else if (a.epi == EPI_F32) {
+              v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
+              *(float4*)((float*)a.out + o) = v;
+            } else {
+              __nv_bfloat162* ob = (__nv_bfloat162*)((__nv_bfloat16*)a.out + o);
+              ob[0] = __floats2bfloat162_rn(v.x + bb.x, v.y + bb.y);
+              ob[1] = __floats2bfloat162_rn(v.z + bb.z, v.w + bb.w);
+            }
+          }
+        }
+        continue;
+      }
+      // ---- epilogue proper over columns of this chunk.  All global loads of
+      // a 32-column chunk are issued before any store (memory-level
+      // parallelism; the compiler cannot hoist loads across stores to `out`).
       const float bias = a.bias ? a.bias[m] : 0.f;
+      const float* __restrict__ part0 =
+          a.partial + ((size_t)((I.chunk * m_tiles + I.tile) * a.splits)) * BN * BM;
       for (int c0 = 0; c0 < nc; c0 += 32) {
         float v[32];
         if (split) {
-          const float* part0 = a.partial + ((size_t)((I.chunk * m_tiles + I.tile) * a.splits)) * BN * BM;
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = 0.f;
           for (int s = 0; s < a.splits; ++s) {
-            const float* p = part0 + (size_t)s * BN * BM;
+            const float* __restrict__ p = part0 + (size_t)s * BN * BM + (size_t)c0 * BM + row;
+            float u[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c0 + j < nc) v[j] += __ldcg(p + (c0 + j) * BM + row);
+            for (int j = 0; j < 32; ++j) u[j] = (c0 + j < nc) ? __ldcg(p + j * BM) : 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += u[j];
           }
         } else {
           uint32_t r[32];
@@ -301,23 +374,29 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           named_bar(2, 128);
           if (q < 2) {
             const int f = I.tile * 64 + row;
-            __nv_bfloat16* o = (__nv_bfloat16*)a.out;
+            __nv_bfloat16* __restrict__ o = (__nv_bfloat16*)a.out + (size_t)(n0 + c0) * a.ldo + f;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int n = n0 + c0 + j;
-              if (c0 + j < nc) o[(size_t)n * a.ldo + f] = __float2bfloat16(silu_f(v[j]) * xch[row * 33 + j]);
-            }
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < nc) o[(size_t)j * a.ldo] = __float2bfloat16(silu_f(v[j]) * xch[row * 33 + j]);
           }
+        } else if (a.epi == EPI_RESID) {
+          float* __restrict__ o = (float*)a.out + (size_t)(n0 + c0) * a.ldo + m;
+          float old[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) old[j] = (c0 + j < nc) ? o[(size_t)j * a.ldo] : 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < nc) o[(size_t)j * a.ldo] = old[j] + v[j];
+        } else if (a.epi == EPI_F32) {
+          float* __restrict__ o = (float*)a.out + (size_t)(n0 + c0) * a.ldo + m;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < nc) o[(size_t)j * a.ldo] = v[j] + bias;
         } else {
+          __nv_bfloat16* __restrict__ o = (__nv_bfloat16*)a.out + (size_t)(n0 + c0) * a.ldo + m;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int n = n0 + c0 + j;
-            if (c0 + j >= nc) break;
-            const size_t o = (size_t)n * a.ldo + m;
-            if (a.epi == EPI_F32) ((float*)a.out)[o] = v[j] + bias;
-            else if (a.epi == EPI_RESID) ((float*)a.out)[o] += v[j];
-            else ((__nv_bfloat16*)a.out)[o] = __float2bfloat16(v[j] + bias);
-          }
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < nc) o[(size_t)j * a.ldo] = __float2bfloat16(v[j] + bias);
         }
       }
       if (!split) {
@@ -389,7 +468,15 @@ int gemm_pick_splits(int M, int K, int n_sms) {
 }
 
 void gemm_launch(const GemmPlan& p, const GemmArgs& a, int grid, cudaStream_t st) {
-  gemm_tcgen05_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(p.tmA, p.tmB, a);
+  gemm_tcgen05_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(p.tmA, p.tmB16, p.tmB64, p.tmB256, a);
+}
+
+int make_plan(GemmPlan* p, const void* W, int M, int K, const void* X, int rows_cap) {
+  if (make_tmap_bf16(&p->tmA, W, M, K, 128)) return -1;
+  if (make_tmap_bf16(&p->tmB16, X, rows_cap, K, 16)) return -1;
+  if (make_tmap_bf16(&p->tmB64, X, rows_cap, K, 64)) return -1;
+  if (make_tmap_bf16(&p->tmB256, X, rows_cap, K, 256)) return -1;
+  return 0;
 }
 
 }  // namespace rp

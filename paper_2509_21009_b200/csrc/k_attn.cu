@@ -252,19 +252,21 @@ __global__ void attn_merge_kernel(const AttnItem* __restrict__ items, const int*
                                   const float* __restrict__ partial, __nv_bfloat16* __restrict__ out, ModelDims m) {
   const int n_items = n_items_dev ? *n_items_dev : n_items_host;
   const int g = m.H / m.KV;
+  const int kvh = blockIdx.y;
   for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
     const AttnItem I = items[it];
     if (I.nsplit == 1 || it != I.item0) continue;
     const int nrows = I.n_qtok * g;
-    for (int e = threadIdx.x; e < m.KV * nrows * HD; e += blockDim.x) {
-      const int kvh = e / (nrows * HD), rem = e % (nrows * HD), r = rem / HD, c = rem % HD;
+    const float* __restrict__ p0 = partial + ((size_t)I.item0 * m.KV + kvh) * (16 * (HD + 2));
+    const size_t sstride = (size_t)m.KV * 16 * (HD + 2);
+    for (int e = threadIdx.x; e < nrows * HD; e += blockDim.x) {
+      const int r = e / HD, c = e % HD;
       float M = -INFINITY;
-      for (int s = 0; s < I.nsplit; ++s)
-        M = fmaxf(M, partial[((size_t)(I.item0 + s) * m.KV + kvh) * (16 * (HD + 2)) + r]);
+      for (int s = 0; s < I.nsplit; ++s) M = fmaxf(M, p0[s * sstride + r]);
       const float Mb = M == -INFINITY ? 0.f : M;
       float L = 0.f, O = 0.f;
       for (int s = 0; s < I.nsplit; ++s) {
-        const float* pp = partial + ((size_t)(I.item0 + s) * m.KV + kvh) * (16 * (HD + 2));
+        const float* pp = p0 + s * sstride;
         const float f = exp2f(pp[r] - Mb);
         L += pp[16 + r] * f;
         O += pp[32 + r * HD + c] * f;
@@ -302,12 +304,11 @@ void launch_attention(const void* q, const void* kv_pool, const int* page_table,
 
 void launch_attn_merge(const AttnItem* items, const int* n_items_dev, int n_items_host, const float* partial,
                        void* out, const ModelDims& m, cudaStream_t st) {
+  dim3 grid((4 * 148 + m.KV - 1) / m.KV, m.KV);
   if (m.hd == 128)
-    attn_merge_kernel<128><<<148 * 2, 256, 0, st>>>(items, n_items_dev, n_items_host, partial,
-                                                     (__nv_bfloat16*)out, m);
+    attn_merge_kernel<128><<<grid, 128, 0, st>>>(items, n_items_dev, n_items_host, partial, (__nv_bfloat16*)out, m);
   else
-    attn_merge_kernel<64><<<148 * 2, 256, 0, st>>>(items, n_items_dev, n_items_host, partial,
-                                                    (__nv_bfloat16*)out, m);
+    attn_merge_kernel<64><<<grid, 128, 0, st>>>(items, n_items_dev, n_items_host, partial, (__nv_bfloat16*)out, m);
 }
 
 }  // namespace rp

@@ -185,6 +185,9 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     R.accept_order[C->acc_local + r] = p;
   }
   const int top = C->free_top;
+  // Split-KV only when the (row, KV head) units alone cannot fill the GPU:
+  // splits add partial traffic and a merge, and are pure overhead otherwise.
+  const int chunk = (C->n_next * R.kv_heads >= kAttnFillUnits) ? (1 << 30) : kAttnChunk;
   int kept = 0, alloc = 0, items = 0;
   long long ctx_sum = 0;
   if (!s_err) {
@@ -196,7 +199,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
         keep = R.status[s] == ST_LIVE;
         if (keep) {
           need = (R.kv_len[s] % kPage) == 0;
-          ns = (R.kv_len[s] + 1 + kAttnChunk - 1) / kAttnChunk;
+          ns = (R.kv_len[s] + chunk) / chunk;
         }
       }
       int tk, ta, ti, tc;
@@ -217,7 +220,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
         for (int sp = 0; sp < ns; ++sp) {
           AttnItem I;
           I.q_row0 = pos; I.n_qtok = 1; I.pos0 = kv; I.pt_row = s;
-          I.kv_lo = sp * kAttnChunk; I.kv_hi = min(kv + 1, (sp + 1) * kAttnChunk);
+          I.kv_lo = sp * chunk; I.kv_hi = min(kv + 1, (sp + 1) * chunk);
           I.nsplit = ns; I.item0 = it0;
           R.items[it0 + sp] = I;
         }

@@ -86,7 +86,7 @@ def load_library(path=LIB_PATH):
     lib.rp_debug_trace_get.argtypes = [P, ctypes.POINTER(I32), I32]
     lib.rp_debug_last_logits.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(I32), I32,
                                          ctypes.POINTER(I32)]
-    lib.rp_debug_gemm.argtypes = [P, P, P, I32, P, I32, I32, I32, I32]
+    lib.rp_debug_gemm.argtypes = [P, P, P, I32, P, I32, I32, I32, I32, I32, ctypes.POINTER(ctypes.c_float)]
     lib.rp_debug_profile.argtypes = [P, I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64),
                                      ctypes.POINTER(I64)]
     lib.rp_nccl_unique_id.argtypes = [P]
@@ -307,12 +307,14 @@ class Engine:
                     launches={k: int(cnt[i]) for i, k in enumerate(self.PROF_NAMES)},
                     rows=int(rcs[0]), ctx=int(rcs[1]), steps=int(rcs[2]))
 
-    def debug_gemm(self, W, X, N, splits=0):
-        """W: torch bf16 [M, K] cuda, X: torch bf16 [rows_cap, K] cuda -> Y fp32 [N, M]."""
+    def debug_gemm(self, W, X, N, splits=0, iters=1, timed=False):
+        """W: torch bf16 [M, K] cuda, X: torch bf16 [rows_cap, K] cuda -> Y fp32 [N, M]
+        (and the mean ms per launch when timed)."""
         torch = self.torch
         M, K = W.shape
         Y = torch.zeros((max(N, 1), M), dtype=torch.float32, device=W.device)
         torch.cuda.synchronize()
+        ms = ctypes.c_float()
         self._check(self.L.rp_debug_gemm(self.h, W.data_ptr(), X.data_ptr(), X.shape[0], Y.data_ptr(), M, N, K,
-                                         splits))
-        return Y[:N]
+                                         splits, iters, ctypes.byref(ms)))
+        return (Y[:N], ms.value) if timed else Y[:N]
