@@ -63,23 +63,23 @@ class Workload:
         tp = self.R["trace"]
         self.trace = gen.length_trace(self.total, self.G, tp["mu0"], tp["sigma_p"], tp["sigma_r"], tp["l_max"],
                                       configs.TRACE_SEED)
-        self.queue = []
+        from paper_2509_21009_b200.dp import GlobalQueue
+        self.queue = GlobalQueue()
         self.next_fresh = 0
 
     def plan(self):
         if len(self.queue) >= self.P0:
-            ids = self.queue[:self.P0]
+            ids = self.queue.ids[:self.P0]
             return "long", ids, self.P0, self.R["long_cap"], self.trace[ids, 1, :]
         ids = list(range(self.next_fresh, self.next_fresh + self.n_submit))
         return "short", ids, self.P0, self.R["short_cap"], self.trace[ids, 0, :]
 
     def commit(self, kind, ids, accepted_ids):
         if kind == "long":
-            self.queue = self.queue[len(ids):]
+            self.queue.pop(len(ids))
         else:
             self.next_fresh += len(ids)
-            acc = set(accepted_ids)
-            self.queue += [i for i in ids if i not in acc]
+            self.queue.defer(ids, accepted_ids)
 
 
 # ------------------------------------------------------------------ clocks
@@ -147,12 +147,7 @@ def run_ours(a):
                     world=world, nccl_id=nccl_id, sample_seed=configs.SAMPLE_SEED)
     st_ev = eng.stream
 
-    def allgather_ids(ids):
-        if world == 1:
-            return list(ids)
-        out = [None] * world
-        dist.all_gather_object(out, list(ids))
-        return [i for part in out for i in part]
+    from paper_2509_21009_b200.dp import all_gather_ids as allgather_ids
 
     def one_round(round_no, profile=0):
         kind, ids, target, cap, L = W.plan()

@@ -92,6 +92,7 @@ struct RpCtx {
   int* identity_pages = nullptr;
   RoundDev R{};
   CtlBlock* h_ctl = nullptr;   // pinned mirror
+  CUtensorMap kv_map{};        // the KV pool as [token rows, head_dim] for TMA
 
   // graphs
   cudaGraphExec_t gexec = nullptr;
@@ -346,7 +347,7 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
       launch_rope_append(c->qkv, n_dev, n_host, row_pos, row_pt, c->R.page_table, c->R.maxp, c->q,
                          c->rd.kv_pool, m, l, c->inv_freq, c->st); c->launches++; }
     { ProfScope ps(c, RP_PROF_ATTN);
-      launch_attention(c->q, c->rd.kv_pool, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
+      launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
                        c->apart, m, l, c->st); c->launches++; }
     { ProfScope ps(c, RP_PROF_MERGE);
       launch_attn_merge(items, n_items_dev, n_items_host, c->apart, c->att, m, c->st); c->launches++; }
@@ -444,6 +445,11 @@ static int init_impl(RpCtx* c) {
   if (rd->workspace_bytes < ws) return c->fail(RP_ENOSPC, "workspace too small: %zu < %zu", rd->workspace_bytes, ws);
   c->n_pages = (int)(rd->kv_pool_bytes / m.page_bytes);
   if (c->n_pages < 2) return c->fail(RP_ENOSPC, "kv pool holds %d pages", c->n_pages);
+  if (make_kv_map(&c->kv_map, rd->kv_pool, (size_t)c->n_pages, m))
+    return c->fail(RP_ECUDA, "KV tensor map (pool too large for 2^31 token rows?)");
+  // stale rows of a page are masked in attention but multiplied by P = 0:
+  // they must be finite, so the pool starts zeroed (all later writes are finite)
+  CK(cudaMemsetAsync(rd->kv_pool, 0, (size_t)c->n_pages * m.page_bytes, c->st));
   workspace_bytes(md, rd, c);
   if (gemm_init_attrs()) return c->fail(RP_ECUDA, "gemm smem attribute");
   if (attn_init_attrs()) return c->fail(RP_ECUDA, "attention smem attribute");

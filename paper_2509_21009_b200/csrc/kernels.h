@@ -1,6 +1,7 @@
 // Device data structures and launchers of the non-GEMM kernels.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace rp {
@@ -73,9 +74,10 @@ void launch_rmsnorm(const float* x, const int* gather, const int* n_dev, int n_h
 void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const int* row_pos, const int* row_pt,
                         const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
                         const double* inv_freq, cudaStream_t st);
-void launch_attention(const void* q, const void* kv_pool, const int* page_table, int maxp, const AttnItem* items,
-                      const int* n_items_dev, int n_items_host, void* out, float* partial, const ModelDims& m,
-                      int layer, cudaStream_t st);
+int make_kv_map(CUtensorMap* map, const void* pool, size_t n_pages, const ModelDims& m);
+void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_table, int maxp,
+                      const AttnItem* items, const int* n_items_dev, int n_items_host, void* out, float* partial,
+                      const ModelDims& m, int layer, cudaStream_t st);
 void launch_attn_merge(const AttnItem* items, const int* n_items_dev, int n_items_host, const float* partial,
                        void* out, const ModelDims& m, cudaStream_t st);
 void launch_kv_fork(const int* jobs /*[n][3] src,dst,rows*/, int n, void* kv_pool, const ModelDims& m,
