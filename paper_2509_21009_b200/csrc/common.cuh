@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cstdio>
 
 namespace rp {
 
@@ -56,6 +57,29 @@ __device__ __forceinline__ unsigned long long pack_arg(float v, uint32_t idx) {
 }
 __host__ __device__ __forceinline__ uint32_t unpack_idx(unsigned long long p) {
   return 0xFFFFFFFFu - (uint32_t)(p & 0xFFFFFFFFull);
+}
+
+// mbarrier wait with a watchdog: a wait that polls ~2^28 times (seconds) is
+// a deadlock -- report it and trap instead of hanging the GPU.  (try_wait
+// suspends the thread for a bounded time per poll, so 2^22 polls >> any
+// legitimate wait in these kernels.)
+__device__ __forceinline__ void mbar_wait_wd(uint32_t bar, uint32_t phase, int tag, long long d0 = 0, long long d1 = 0) {
+  uint32_t ok = 0;
+  uint32_t spins = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase)
+        : "memory");
+    if (!ok && ++spins == (1u << 23)) __trap();
+    if (!ok && spins == (1u << 22)) {
+      printf("rollpacker watchdog: mbarrier wait stuck (tag %d, block %d,%d, thread %d, phase %u, %lld %lld)\n",
+             tag, blockIdx.x, blockIdx.y, threadIdx.x, phase, d0, d1);
+    }
+  } while (!ok);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

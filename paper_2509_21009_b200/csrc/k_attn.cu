@@ -2,10 +2,10 @@
 //
 // The KV pool is addressed by TMA as a 2-D tensor of token rows x head_dim
 // (bf16): page p, layer l, KV head h, K|V is the 64-row block starting at row
-// (((p*L + l)*KV + h)*2 + kv)*64.  One CTA = 1 producer warp + 4 consumer
+// (((p*L + l)*KV + h)*2 + kv)*64.  One CTA = 1 producer warp + 3 consumer
 // warps.  The producer streams whole pages (K and V, SWIZZLE_128B boxes of 64
-// columns) into a 5-stage mbarrier ring; consumer warp w owns pages w, w+4,
-// ... of the current work item.  Work item = (query block, KV head, key
+// columns) into a 6-stage mbarrier ring; consumer warp w (of 3) owns the
+// pages with global index = w mod 3 and therefore always the same 2 stages.  Work item = (query block, KV head, key
 // split): the 16 MMA rows are the (query token, query head) pairs served by
 // one KV head -- decode: 1 token x g heads (g = H/KV <= 8); prefill:
 // floor(16/g) tokens x g heads with per-row causal limits.  S = Q K^T and
@@ -14,7 +14,7 @@
 // log2 domain; the warps merge in shared memory; multi-split blocks write
 // (m, l, O) partials that attn_merge combines in split order.
 // Decode attention moves g FLOP per KV byte, far below the ridge point: the
-// design goal is bytes in flight (5 x 32 KB per SM) and few instructions per
+// design goal is bytes in flight (6 x 32 KB per SM) and few instructions per
 // byte (one TMA per 8 KB box, 128 MMAs per 64-token page per warp).
 #include <cuda.h>
 #include "common.cuh"
@@ -22,9 +22,13 @@
 
 namespace rp {
 
-constexpr int AT_CWARPS = 4;                  // consumer warps
+constexpr int AT_CWARPS = 3;                  // consumer warps
 constexpr int AT_THREADS = (AT_CWARPS + 1) * 32;
-constexpr int AT_STAGES = 5;
+constexpr int AT_STAGES = 6;                  // multiple of AT_CWARPS: stage s is always consumed by
+                                              // warp s % AT_CWARPS, so every warp waits on each of its
+                                              // stages' uses in order (mbarrier parity only tells
+                                              // adjacent phases apart)
+static_assert(AT_STAGES % AT_CWARPS == 0, "stage ownership");
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -47,18 +51,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 __device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t phase) {
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(phase)
-        : "memory");
-  } while (!ok);
 }
 __device__ __forceinline__ void bar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -132,7 +124,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
             const long long gp = gpage + j0 + jj;
             const int st = (int)(gp % AT_STAGES);
             const uint32_t ph = (uint32_t)((gp / AT_STAGES) & 1);
-            bar_wait(empty0 + 8 * st, ph ^ 1);
+            mbar_wait_wd(empty0 + 8 * st, ph ^ 1, 100 + st, gp, (long long)it * 1000 + npg);
             const uint32_t fb = full0 + 8 * st;
             bar_expect_tx(fb, C::STAGE_BYTES);
             const int row_k = (((page * m.L + layer) * m.KV + kvh) * 2 + 0) * row_stride_blk;
@@ -180,10 +172,10 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
     for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
     float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
 
-    for (int j = warp; j < npg; j += AT_CWARPS) {
-      const long long gp = gpage + j;
+    for (int j = (int)((warp - gpage % AT_CWARPS + AT_CWARPS) % AT_CWARPS); j < npg; j += AT_CWARPS) {
+      const long long gp = gpage + j;   // gp % AT_CWARPS == warp
       const int st = (int)(gp % AT_STAGES);
-      bar_wait(full0 + 8 * st, (uint32_t)((gp / AT_STAGES) & 1));
+      mbar_wait_wd(full0 + 8 * st, (uint32_t)((gp / AT_STAGES) & 1), 200 + st, gp, (long long)it * 1000 + npg);
       const uint32_t kt = sbase + st * C::STAGE_BYTES, vt = kt + C::TILE_BYTES;
       const int tok0 = (p_lo + j) * kPage;
       // ---- S = Q K^T (16 x 64)

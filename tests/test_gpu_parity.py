@@ -251,3 +251,30 @@ def test_invalid_arguments(tiny):
     eng.run()
     eng.collect()
     eng.close()
+
+
+def test_decode_long_context_split_kv(tiny, oracle_w):
+    """Contexts of ~650 tokens: 11 KV pages per work item and 512-token
+    key splits (kv_lo > 0) merged by attn_merge; logits of the decode step vs
+    the oracle teacher-forced on the GPU's own history."""
+    eng = make_engine(tiny, graph_steps=0, max_cap=640)
+    n, G = 2, 3
+    ps = gen.prompts(n, 0, tiny["eos_id"], (100, 110), 77)
+    L = np.full((n, G), 600, np.int32)
+    eng.debug_trace_enable(700)
+    eng.submit(ps, G, 640, n, long_round=True, trace=L, round_id=3)
+    eng.step(540)
+    lg, slots = eng.debug_last_logits()
+    st = eng.step(1)
+    t_lg = st.t - 1
+    eng.run()
+    res = eng.collect()
+    toks = {(r["prompt_id"] - ps[0]["prompt_id"], r["j"]): r["tokens"] for r in res}
+    worst = 0.0
+    for row, s in enumerate(slots):
+        p, j = divmod(int(s), G)
+        seq = np.concatenate([ps[p]["tokens"], toks[(p, j)][:t_lg - 1]])
+        want = decoder.logits(oracle_w, seq, rows=[len(seq) - 1])[0]
+        worst = max(worst, float(np.max(np.abs(lg[row] - want))))
+    assert len(seq) > 600 and worst <= LOGIT_TOL, (len(seq), worst)
+    eng.close()

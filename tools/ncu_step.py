@@ -14,6 +14,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--skip", type=int, default=0, help="decode steps to run (graphs) before the eager ones")
     ap.add_argument("--config", default="C2-7b")
+    ap.add_argument("--graph-steps", type=int, default=0)
+    ap.add_argument("--kv-fraction", type=float, default=0.5)
     a = ap.parse_args()
     import torch
     from paper_2509_21009_b200 import rp
@@ -21,15 +23,21 @@ def main():
     W = bench.Workload(a.config, 1)
     lo, hi = W.R["prompt_len"]
     eng = rp.Engine(W.model, max_seqs=W.n_submit * W.G, max_prompts=W.n_submit, max_prompt_len=hi,
-                    max_prompt_tokens=W.n_submit * hi, max_cap=W.R["short_cap"], graph_steps=0,
-                    kv_fraction=0.5)
+                    max_prompt_tokens=W.n_submit * hi, max_cap=W.R["short_cap"], graph_steps=a.graph_steps,
+                    kv_fraction=a.kv_fraction)
     kind, ids, target, cap, L = W.plan()
     eng.submit([W.prompts[i] for i in ids], W.G, cap, target, trace=L, round_id=0)
     if a.skip:
-        eng.step(a.skip)
+        done = 0
+        while done < a.skip:
+            st = eng.step(100)
+            done += 100
+            print("t=%d live=%d done=%d" % (st.t, st.n_live, st.done), flush=True)
+            if st.done:
+                break
     st = eng.step(a.steps)
     torch.cuda.synchronize()
-    print("ok t=%d live=%d" % (st.t, st.n_live))
+    print("ok t=%d live=%d" % (st.t, st.n_live), flush=True)
     eng.close()
 
 
