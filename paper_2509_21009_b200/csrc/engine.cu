@@ -85,6 +85,7 @@ struct RpCtx {
   __nv_bfloat16 *h = nullptr, *q = nullptr, *att = nullptr, *mid = nullptr;
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
   int* gctr = nullptr;
+  int* atickets = nullptr;
   double* inv_freq = nullptr;
   AttnItem *items_pre = nullptr;
   int *pre_tok = nullptr, *pre_pos = nullptr, *pre_pt = nullptr, *pre_last = nullptr, *fork_jobs = nullptr;
@@ -220,6 +221,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto gpart = cv.take<float>(z.part_floats);
   auto gctr = cv.take<int>(1 << 16);
   auto apart = cv.take<float>(z.apart_floats);
+  auto atick = cv.take<int>((size_t)std::max(z.max_items_dec, z.max_items_pre) * KV);
   auto invf = cv.take<double>(hd / 2);
   auto items_dec = cv.take<AttnItem>(z.max_items_dec);
   auto items_pre = cv.take<AttnItem>(z.max_items_pre);
@@ -260,7 +262,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto ident = cv.take<int>(max_pages + 1);
   if (c) {
     c->x = x; c->h = h; c->qkv = qkv; c->q = q; c->att = att; c->mid = mid; c->logits = logits;
-    c->gpart = gpart; c->gctr = gctr; c->apart = apart; c->inv_freq = invf;
+    c->gpart = gpart; c->gctr = gctr; c->apart = apart; c->atickets = atick; c->inv_freq = invf;
     c->items_pre = items_pre; c->pre_tok = pre_tok; c->pre_pos = pre_pos; c->pre_pt = pre_pt;
     c->pre_last = pre_last; c->fork_jobs = fork_jobs; c->col_meta = col_meta; c->col_tok = col_tok;
     c->identity_pages = ident;
@@ -348,9 +350,7 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
                          c->rd.kv_pool, m, l, c->inv_freq, c->st); c->launches++; }
     { ProfScope ps(c, RP_PROF_ATTN);
       launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
-                       c->apart, m, l, c->st); c->launches++; }
-    { ProfScope ps(c, RP_PROF_MERGE);
-      launch_attn_merge(items, n_items_dev, n_items_host, c->apart, c->att, m, c->st); c->launches++; }
+                       c->apart, c->atickets, m, l, c->st); c->launches++; }
     { ProfScope ps(c, RP_PROF_GEMM_O);
       gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, EPI_RESID, c->x, m.d, nullptr); }
     { ProfScope ps(c, RP_PROF_RMSNORM);
@@ -519,6 +519,8 @@ static int init_impl(RpCtx* c) {
   c->s_down = gemm_pick_splits((int)d, (int)F, kSMs);
   c->s_lm = gemm_pick_splits((int)V, (int)d, kSMs);
   CK(cudaMemsetAsync(c->gctr, 0, (1 << 16) * sizeof(int), c->st));
+  CK(cudaMemsetAsync(c->atickets, 0, (size_t)std::max(c->z.max_items_dec, c->z.max_items_pre) * KV * sizeof(int),
+                     c->st));
 
   // ---- identity free list (page ids 0..n_pages-1)
   {

@@ -12,7 +12,8 @@
 // O += P V run on mma.sync m16n8k16 (bf16, fp32 accumulate; a 16-row MMA is
 // the natural shape for g <= 8 query rows) with an online softmax in the
 // log2 domain; the warps merge in shared memory; multi-split blocks write
-// (m, l, O) partials that attn_merge combines in split order.
+// (m, l, O) partials and the last split to finish (atomic ticket) combines
+// them in split order.
 // Decode attention moves g FLOP per KV byte, far below the ridge point: the
 // design goal is bytes in flight (6 x 32 KB per SM) and few instructions per
 // byte (one TMA per 8 KB box, 128 MMAs per 64-token page per warp).
@@ -85,7 +86,8 @@ template <int HD>
 __global__ void __launch_bounds__(AT_THREADS, 1)
 attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __restrict__ q,
             const int* __restrict__ page_table, int maxp, const AttnItem* __restrict__ items, const int* n_items_dev,
-            int n_items_host, __nv_bfloat16* __restrict__ out, float* __restrict__ partial, ModelDims m, int layer) {
+            int n_items_host, __nv_bfloat16* __restrict__ out, float* __restrict__ partial, int* __restrict__ tickets,
+            ModelDims m, int layer) {
   using C = AttnCfg<HD>;
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
@@ -96,7 +98,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
   const uint32_t empty0 = full0 + 8 * AT_STAGES;
 
   const int n_items = n_items_dev ? *n_items_dev : n_items_host;
-  const int kvh = blockIdx.y;
+  const int n_units = n_items * m.KV;            // flat (item, KV head) work units
   const int g = m.H / m.KV;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -111,7 +113,8 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
     // ===================== producer warp =====================
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&kv_map) : "memory");
     long long gpage = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int it = u / m.KV, kvh = u % m.KV;
       const AttnItem I = items[it];
       const int p_lo = I.kv_lo / kPage, npg = (I.kv_hi + kPage - 1) / kPage - p_lo;
       const int* ptab = page_table + (size_t)I.pt_row * maxp + p_lo;
@@ -146,7 +149,8 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
   const float scale = 1.4426950408889634f * rsqrtf((float)HD);
   const int ra = lane >> 2, rb = ra + 8;
   long long gpage = 0;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const int it = u / m.KV, kvh = u % m.KV;
     const AttnItem I = items[it];
     const int nrows = I.n_qtok * g;
     const int p_lo = I.kv_lo / kPage, npg = (I.kv_hi + kPage - 1) / kPage - p_lo;
@@ -285,38 +289,67 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
         if (c == 0) { pp[r] = M; pp[16 + r] = L; }
       }
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(AT_CWARPS * 32) : "memory");
-  }
-}
-
-// Combine the splits of multi-split query blocks in split order.
-template <int HD>
-__global__ void attn_merge_kernel(const AttnItem* __restrict__ items, const int* n_items_dev, int n_items_host,
-                                  const float* __restrict__ partial, __nv_bfloat16* __restrict__ out, ModelDims m) {
-  const int n_items = n_items_dev ? *n_items_dev : n_items_host;
-  const int g = m.H / m.KV;
-  const int kvh = blockIdx.y;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const AttnItem I = items[it];
-    if (I.nsplit == 1 || it != I.item0) continue;
-    const int nrows = I.n_qtok * g;
-    const float* __restrict__ p0 = partial + ((size_t)I.item0 * m.KV + kvh) * (16 * (HD + 2));
-    const size_t sstride = (size_t)m.KV * 16 * (HD + 2);
-    for (int e = threadIdx.x; e < nrows * HD; e += blockDim.x) {
-      const int r = e / HD, c = e % HD;
-      float M = -INFINITY;
-      for (int s = 0; s < I.nsplit; ++s) M = fmaxf(M, p0[s * sstride + r]);
-      const float Mb = M == -INFINITY ? 0.f : M;
-      float L = 0.f, O = 0.f;
-      for (int s = 0; s < I.nsplit; ++s) {
-        const float* pp = p0 + s * sstride;
-        const float f = exp2f(pp[r] - Mb);
-        L += pp[16 + r] * f;
-        O += pp[32 + r * HD + c] * f;
+    if (I.nsplit > 1) {
+      // the last split of this query block to finish merges all splits, in
+      // split order (deterministic); the ticket resets itself
+      __shared__ int s_last;
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"r"(AT_CWARPS * 32) : "memory");
+      if (threadIdx.x == 0) {
+        int* tk = tickets + (size_t)I.item0 * m.KV + kvh;
+        const int old = atomicAdd(tk, 1);
+        s_last = old == I.nsplit - 1;
+        if (s_last) *tk = 0;
       }
-      const int tok = I.q_row0 + r / g, head = kvh * g + r % g;
-      out[((size_t)tok * m.H + head) * HD + c] = __float2bfloat16(L > 0.f ? O / L : 0.f);
+      asm volatile("bar.sync 1, %0;" ::"r"(AT_CWARPS * 32) : "memory");
+      if (s_last) {
+        __threadfence();
+        // per-row split weights w[r][s] = 2^(m_s - M) / L into smem (reuses the
+        // merge buffer), then O = sum_s w[r][s] * O_s with float4 loads of all
+        // splits in flight; fixed split order -> deterministic
+        const float* __restrict__ p0 = partial + ((size_t)I.item0 * m.KV + kvh) * (16 * (HD + 2));
+        const size_t sstride = (size_t)m.KV * 16 * (HD + 2);
+        float* wsm = mrg;                                  // [16][nsplit]
+        const int ns = I.nsplit;
+        if (threadIdx.x < nrows) {
+          const int r = threadIdx.x;
+          float M = -INFINITY;
+          for (int sp = 0; sp < ns; ++sp) M = fmaxf(M, __ldcg(p0 + sp * sstride + r));
+          const float Mb = M == -INFINITY ? 0.f : M;
+          float L = 0.f;
+          for (int sp = 0; sp < ns; ++sp) {
+            const float f = exp2f(__ldcg(p0 + sp * sstride + r) - Mb);
+            wsm[r * ns + sp] = f;
+            L += __ldcg(p0 + sp * sstride + 16 + r) * f;
+          }
+          const float inv = L > 0.f ? 1.f / L : 0.f;
+          for (int sp = 0; sp < ns; ++sp) wsm[r * ns + sp] *= inv;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(AT_CWARPS * 32) : "memory");
+        for (int e = threadIdx.x; e < nrows * (HD / 4); e += AT_CWARPS * 32) {
+          const int r = e / (HD / 4), c4 = (e % (HD / 4)) * 4;
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int s0 = 0; s0 < ns; s0 += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              v[u] = s0 + u < ns ? __ldcg((const float4*)(p0 + (s0 + u) * sstride + 32 + r * HD + c4))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              if (s0 + u >= ns) break;
+              const float w = wsm[r * ns + s0 + u];
+              acc.x += w * v[u].x; acc.y += w * v[u].y; acc.z += w * v[u].z; acc.w += w * v[u].w;
+            }
+          }
+          const int tok = I.q_row0 + r / g, head = kvh * g + r % g;
+          __nv_bfloat162* o2 = (__nv_bfloat162*)(out + ((size_t)tok * m.H + head) * HD + c4);
+          o2[0] = __floats2bfloat162_rn(acc.x, acc.y);
+          o2[1] = __floats2bfloat162_rn(acc.z, acc.w);
+        }
+      }
     }
+    asm volatile("bar.sync 1, %0;" ::"r"(AT_CWARPS * 32) : "memory");
   }
 }
 
@@ -356,26 +389,16 @@ int make_kv_map(CUtensorMap* map, const void* pool, size_t n_pages, const ModelD
 
 void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_table, int maxp,
                       const AttnItem* items, const int* n_items_dev, int n_items_host, void* out, float* partial,
-                      const ModelDims& m, int layer, cudaStream_t st) {
-  const int gx = (148 + m.KV - 1) / m.KV;
-  dim3 grid(gx < 1 ? 1 : gx, m.KV);
+                      int* tickets, const ModelDims& m, int layer, cudaStream_t st) {
+  const int grid = 148;   // one wave, persistent over the flat (item, KV head) units
   if (m.hd == 128)
     attn_kernel<128><<<grid, AT_THREADS, AttnCfg<128>::SMEM, st>>>(kv_map, (const __nv_bfloat16*)q, page_table, maxp,
                                                                    items, n_items_dev, n_items_host,
-                                                                   (__nv_bfloat16*)out, partial, m, layer);
+                                                                   (__nv_bfloat16*)out, partial, tickets, m, layer);
   else
     attn_kernel<64><<<grid, AT_THREADS, AttnCfg<64>::SMEM, st>>>(kv_map, (const __nv_bfloat16*)q, page_table, maxp,
                                                                  items, n_items_dev, n_items_host,
-                                                                 (__nv_bfloat16*)out, partial, m, layer);
-}
-
-void launch_attn_merge(const AttnItem* items, const int* n_items_dev, int n_items_host, const float* partial,
-                       void* out, const ModelDims& m, cudaStream_t st) {
-  dim3 grid((4 * 148 + m.KV - 1) / m.KV, m.KV);
-  if (m.hd == 128)
-    attn_merge_kernel<128><<<grid, 128, 0, st>>>(items, n_items_dev, n_items_host, partial, (__nv_bfloat16*)out, m);
-  else
-    attn_merge_kernel<64><<<grid, 128, 0, st>>>(items, n_items_dev, n_items_host, partial, (__nv_bfloat16*)out, m);
+                                                                 (__nv_bfloat16*)out, partial, tickets, m, layer);
 }
 
 }  // namespace rp

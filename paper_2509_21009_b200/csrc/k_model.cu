@@ -43,6 +43,13 @@ void launch_init_weights(void* out, long long n, uint32_t tid, uint64_t seed, in
                                             in_features, up);
 }
 
+// Row kernels: one wave of 148 CTAs for device-side (decode) row counts; up
+// to 8 CTAs per SM for large host-known (prefill) row counts.
+static inline int row_grid(const int* n_dev, int n_host) {
+  if (n_dev) return 148;
+  return n_host < 148 ? (n_host > 0 ? n_host : 1) : (n_host < 148 * 8 ? n_host : 148 * 8);
+}
+
 // ------------------------------------------------------------------ embedding
 __global__ void embed_kernel(const int* tok, const int* n_dev, int n_host, const __nv_bfloat16* emb, float* x,
                              int d) {
@@ -55,7 +62,7 @@ __global__ void embed_kernel(const int* tok, const int* n_dev, int n_host, const
 }
 
 void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb, float* x, int d, cudaStream_t st) {
-  embed_kernel<<<148 * 4, 256, 0, st>>>(tok, n_dev, n_host, (const __nv_bfloat16*)emb, x, d);
+  embed_kernel<<<row_grid(n_dev, n_host), 256, 0, st>>>(tok, n_dev, n_host, (const __nv_bfloat16*)emb, x, d);
 }
 
 // -------------------------------------------------------------------- RMSNorm
@@ -95,7 +102,7 @@ __global__ void rmsnorm_kernel(const float* x, const int* gather, const int* n_d
 
 void launch_rmsnorm(const float* x, const int* gather, const int* n_dev, int n_host, const float* gamma, void* h,
                     int d, float eps, cudaStream_t st) {
-  rmsnorm_kernel<<<148 * 4, 256, 0, st>>>(x, gather, n_dev, n_host, gamma, (__nv_bfloat16*)h, d, eps);
+  rmsnorm_kernel<<<row_grid(n_dev, n_host), 256, 0, st>>>(x, gather, n_dev, n_host, gamma, (__nv_bfloat16*)h, d, eps);
 }
 
 // -------------------------------------------------------- RoPE + KV append
@@ -149,7 +156,7 @@ __global__ void rope_append_kernel(const float* qkv, const int* n_dev, int n_hos
 void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const int* row_pos, const int* row_pt,
                         const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
                         const double* inv_freq, cudaStream_t st) {
-  rope_append_kernel<<<148 * 4, 256, m.hd * sizeof(float), st>>>(qkv, n_dev, n_host, row_pos, row_pt, page_table,
+  rope_append_kernel<<<row_grid(n_dev, n_host), 256, m.hd * sizeof(float), st>>>(qkv, n_dev, n_host, row_pos, row_pt, page_table,
                                                                  maxp, (__nv_bfloat16*)q_out, (uint8_t*)kv_pool, m,
                                                                  layer, inv_freq);
 }

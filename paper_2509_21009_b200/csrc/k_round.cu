@@ -82,6 +82,7 @@ constexpr int CTL_THREADS = 1024;
 // error}.
 __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
   __shared__ int s_k, s_top, s_keep, s_need, s_err;
+  __shared__ long long s_ctx;
   CtlBlock* C = R.ctl;
   const int n = C->n_live;
   const int t = C->t;
@@ -102,7 +103,7 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     R.status[s] = fin ? ST_FINISHED : capped ? ST_CAPPED : ST_LIVE;
     if (fin || (capped && R.kind == 1)) atomicAdd(&R.p_cnt[R.slot_prompt[s]], 1);
   }
-  if (tid == 0) { s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; }
+  if (tid == 0) { s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; s_ctx = 0; }
   __syncthreads();
   // prompts completing at step t, in prompt-index order
   for (int base = 0; base < R.n_prompts; base += CTL_THREADS) {
@@ -134,14 +135,15 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
         }
       }
     }
-    int tot, tk, tn;
+    int tot, tk, tn, tc;
     const int off = block_exscan(cnt, &tot, scan_sm);
     block_exscan(keep, &tk, scan_sm);
     block_exscan(need, &tn, scan_sm);
+    block_exscan(keep ? R.kv_len[s] + 1 : 0, &tc, scan_sm);
     for (int c = 0; c < cnt; ++c)
       R.free_stack[s_top + off + c] = R.page_table[(size_t)s * R.maxp + R.own0[s] + c];
     __syncthreads();
-    if (tid == 0) { s_top += tot; s_keep += tk; s_need += tn; }
+    if (tid == 0) { s_top += tot; s_keep += tk; s_need += tn; s_ctx += tc; }
     __syncthreads();
   }
   if (tid == 0) {
@@ -150,6 +152,7 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     C->k_step = s_k;
     C->n_next = s_keep;
     C->need_pages = s_need;
+    C->ctx_sum = s_ctx;
     R.ks_local[0] = s_k; R.ks_local[1] = s_keep; R.ks_local[2] = s_err;
     if (R.world == 1) { R.ks[0] = s_k; R.ks[1] = s_keep; R.ks[2] = s_err; }
   }
@@ -185,11 +188,12 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     R.accept_order[C->acc_local + r] = p;
   }
   const int top = C->free_top;
-  // Split-KV only when the (row, KV head) units alone cannot fill the GPU:
-  // splits add partial traffic and a merge, and are pure overhead otherwise.
-  const int chunk = (C->n_next * R.kv_heads >= kAttnFillUnits) ? (1 << 30) : kAttnChunk;
+  // Key-split size: about the step's total context x KV heads / 148 (one
+  // wave of work units), never below 512 tokens; short rows stay unsplit,
+  // long rows are split so no unit dominates the wave.
+  const long long per = (C->ctx_sum * R.kv_heads + 147) / 148;
+  const int chunk = (int)min((long long)(1 << 30), max((long long)kAttnChunk, (per + kPage - 1) / kPage * kPage));
   int kept = 0, alloc = 0, items = 0;
-  long long ctx_sum = 0;
   if (!s_err) {
     for (int base = 0; base < n; base += CTL_THREADS) {
       const int i = base + tid;
@@ -202,12 +206,10 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
           ns = (R.kv_len[s] + chunk) / chunk;
         }
       }
-      int tk, ta, ti, tc;
+      int tk, ta, ti;
       const int ok = block_exscan(keep, &tk, scan_sm);
       const int oa = block_exscan(need, &ta, scan_sm);
       const int oi = block_exscan(ns, &ti, scan_sm);
-      block_exscan(keep ? R.kv_len[s] + 1 : 0, &tc, scan_sm);
-      ctx_sum += tc;
       if (keep) {
         const int pos = kept + ok;
         const int kv = R.kv_len[s];
@@ -237,7 +239,6 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     C->decoded += n;
     C->free_top = top - alloc;
     C->n_items = items;
-    C->ctx_sum = ctx_sum;
     const bool done = s_acc_new >= R.target || s_next_global == 0 || s_err;
     if (R.trace_buf && t <= R.trace_steps) {
       int* tb = R.trace_buf + (size_t)(t - 1) * (2 + R.S);

@@ -77,9 +77,8 @@ void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const in
 int make_kv_map(CUtensorMap* map, const void* pool, size_t n_pages, const ModelDims& m);
 void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_table, int maxp,
                       const AttnItem* items, const int* n_items_dev, int n_items_host, void* out, float* partial,
-                      const ModelDims& m, int layer, cudaStream_t st);
-void launch_attn_merge(const AttnItem* items, const int* n_items_dev, int n_items_host, const float* partial,
-                       void* out, const ModelDims& m, cudaStream_t st);
+                      int* tickets /* [items x KV], zero, self-resetting */, const ModelDims& m, int layer,
+                      cudaStream_t st);
 void launch_kv_fork(const int* jobs /*[n][3] src,dst,rows*/, int n, void* kv_pool, const ModelDims& m,
                     cudaStream_t st);
 void launch_sampler(const float* logits, int V, int row_div, const RoundDev& R, uint64_t seed, float inv_temp,
