@@ -131,7 +131,11 @@ def run_ours(a):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # torch.distributed is host plumbing only (NCCL id broadcast, membership,
+        # timing reductions); the data-path exchange is the library's own NCCL
+        # communicator inside the CUDA graph (a second NCCL group in the same
+        # process deadlocked at init on this image)
+        dist.init_process_group("gloo")
     W = Workload(a.config, world)
     cfg, G = W.model, W.G
     # per-rank capacities
@@ -204,11 +208,11 @@ def run_ours(a):
     wall_s = w1 - w0
     launches = eng.launch_count() - launches0
     # ---- reductions over ranks
-    t = torch.tensor([dev_s, wall_s], dtype=torch.float64, device="cuda")
+    t = torch.tensor([dev_s, wall_s], dtype=torch.float64)
     tot = torch.tensor([sum(x["decoded"] for x in rounds), sum(x["retained"] for x in rounds),
                         sum(x["h2d"] for x in rounds), sum(x["d2h"] for x in rounds), launches],
-                       dtype=torch.float64, device="cuda")
-    per_round = torch.tensor([x["dev_s"] for x in rounds], dtype=torch.float64, device="cuda")
+                       dtype=torch.float64)
+    per_round = torch.tensor([x["dev_s"] for x in rounds], dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
@@ -404,6 +408,8 @@ def run_reference(a):
 
 
 def main():
+    # NCCL's banner/debug log goes to stderr: stdout carries exactly one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     a = parse()
     if a.impl == "reference":
         run_reference(a)
