@@ -88,7 +88,16 @@ typedef struct {
   uint64_t sample_seed;      /* Philox key of the sampler (reading Z10)        */
   float temperature;         /* T of the Gumbel-max sampler (reading Z9: 1.0)  */
   int32_t graph_steps;       /* decode steps per captured CUDA graph (0 = no graphs) */
-  const void* nccl_id;       /* 128-byte ncclUniqueId when world > 1, else NULL */
+  const void* nccl_id;       /* 128-byte ncclUniqueId of the DP group (world > 1) or of
+                                the TP group (tp > 1), else NULL */
+  int32_t tp;                /* tensor-parallel size of this context (0/1 = none).  With
+                                tp > 1 (world must be 1) the context holds only its shard:
+                                heads, KV heads, d_ff and vocab / tp (column-parallel QKV,
+                                gate||up and LM head, row-parallel O and down with an fp32
+                                NCCL all-reduce after each; vocab-sharded sampling with a
+                                MAX all-reduce of the packed argmax).  Every TP rank submits
+                                the same prompts and keeps identical round state. */
+  int32_t tp_rank;           /* rank inside the TP group */
 } rp_runtime_desc;
 
 typedef struct {
@@ -189,7 +198,8 @@ int64_t rp_launch_count(const void* ctx);
 /* ---------------------------------------------------------------- test-only */
 /* Teacher-forced logits of one token sequence (host tokens[n], n <=
  * max_prompt_tokens and <= max_prompt_len) through the prefill path: writes
- * n x vocab fp32 to logits_out (host).  Requires no active round. */
+ * n x vocab fp32 to logits_out (host); under TP, n x (vocab / tp) of this
+ * rank's vocab shard.  Requires no active round. */
 int rp_debug_logits(void* ctx, const int32_t* tokens, int32_t n, float* logits_out);
 
 /* Enable (steps > 0) or disable the per-step schedule trace of the next

@@ -82,6 +82,7 @@ struct RpCtx {
 
   // activations / workspace
   float* x = nullptr;
+  float* ar = nullptr;          // TP: all-reduced partial of a row-parallel GEMM
   __nv_bfloat16 *h = nullptr, *q = nullptr, *att = nullptr, *mid = nullptr;
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
   int* gctr = nullptr;
@@ -96,9 +97,12 @@ struct RpCtx {
   CUtensorMap kv_map{};        // the KV pool as [token rows, head_dim] for TMA
 
   // graphs
+  struct Graph { int bucket; cudaGraphExec_t exec; int nodes; };
+  std::vector<Graph> graphs;    // per live-row bucket, valid for the current round
   cudaGraphExec_t gexec = nullptr;
   int graph_nodes = 0;
   bool graph_dirty = true;
+  int tp = 1;
   bool own_stream = false;
 
   // NCCL
@@ -148,6 +152,20 @@ static std::string g_init_err;
   } while (0)
 
 // ------------------------------------------------------------------ sizing
+static int tp_of(const rp_runtime_desc* rd) { return rd->tp > 1 ? rd->tp : 1; }
+
+// Dimensions of this rank's shard: heads, KV heads, d_ff and vocab are split
+// over the TP group (column-parallel QKV / gate||up / LM head, row-parallel
+// O / down); d_model, layers and the embedding stay whole.
+static ModelDims local_dims(const rp_model_desc* md, const rp_runtime_desc* rd) {
+  const int T = tp_of(rd), r = T > 1 ? rd->tp_rank : 0;
+  ModelDims m{};
+  m.L = md->n_layers; m.d = md->d_model; m.hd = md->head_dim; m.eos = md->eos_id; m.eps = md->rms_eps;
+  m.H = md->n_heads / T; m.KV = md->n_kv_heads / T; m.F = md->d_ff / T; m.V = md->vocab / T; m.v0 = r * m.V;
+  m.page_bytes = (size_t)m.L * m.KV * 2 * kPage * m.hd * 2;
+  return m;
+}
+
 static Sizes compute_sizes(const rp_model_desc* md, const rp_runtime_desc* rd) {
   Sizes z{};
   z.S = rd->max_seqs;
@@ -159,9 +177,10 @@ static Sizes compute_sizes(const rp_model_desc* md, const rp_runtime_desc* rd) {
   z.max_items_dec = z.S * ((max_ctx + kAttnChunk - 1) / kAttnChunk);
   z.max_items_pre = rd->max_prompt_tokens * ((rd->max_prompt_len + kAttnChunk - 1) / kAttnChunk) + z.P;
   // split-K partials: worst GEMM at the decode sizes
-  const int d = md->d_model, qkvw = (md->n_heads + 2 * md->n_kv_heads) * md->head_dim, F = md->d_ff;
-  const int hid = md->n_heads * md->head_dim;
-  const int shapes[5][2] = {{qkvw, d}, {d, hid}, {2 * F, d}, {d, F}, {md->vocab, d}};
+  const ModelDims lm = local_dims(md, rd);
+  const int d = lm.d, qkvw = (lm.H + 2 * lm.KV) * lm.hd, F = lm.F;
+  const int hid = lm.H * lm.hd;
+  const int shapes[5][2] = {{qkvw, d}, {d, hid}, {2 * F, d}, {d, F}, {lm.V, d}};
   size_t mx = 0;
   const int nch = (z.S + 255) / 256;
   for (auto& s : shapes) {
@@ -170,7 +189,7 @@ static Sizes compute_sizes(const rp_model_desc* md, const rp_runtime_desc* rd) {
   }
   // rp_debug_gemm may request splits of an arbitrary shape: keep >= 16M floats
   z.part_floats = std::max(mx, (size_t)1 << 24);
-  z.apart_floats = (size_t)std::max(z.max_items_dec, z.max_items_pre) * md->n_kv_heads * 16 * (md->head_dim + 2);
+  z.apart_floats = (size_t)std::max(z.max_items_dec, z.max_items_pre) * lm.KV * 16 * (lm.hd + 2);
   return z;
 }
 
@@ -179,10 +198,10 @@ struct WeightLayout {
   std::vector<size_t> off;  // per layer: wqkv, bqkv, wo, wgu, wd, ln1, ln2 (7 entries); then emb, lm, lnf
 };
 
-static WeightLayout weight_layout(const rp_model_desc* md) {
+static WeightLayout weight_layout(const rp_model_desc* md, const rp_runtime_desc* rd) {
   WeightLayout w;
-  const size_t d = md->d_model, hd = md->head_dim, H = md->n_heads, KV = md->n_kv_heads, F = md->d_ff,
-               V = md->vocab;
+  const ModelDims lm = local_dims(md, rd);
+  const size_t d = lm.d, hd = lm.hd, H = lm.H, KV = lm.KV, F = lm.F, V = lm.V, Vfull = md->vocab;
   const size_t qkvw = (H + 2 * KV) * hd;
   size_t off = 0;
   auto put = [&](size_t bytes) {
@@ -199,8 +218,8 @@ static WeightLayout weight_layout(const rp_model_desc* md) {
     put(d * 4);
     put(d * 4);
   }
-  put(V * d * 2);
-  put(V * d * 2);
+  put(Vfull * d * 2);   // embedding (whole on every rank)
+  put(V * d * 2);       // LM head shard
   put(d * 4);
   w.total = align_up(off);
   return w;
@@ -208,10 +227,11 @@ static WeightLayout weight_layout(const rp_model_desc* md) {
 
 static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd, RpCtx* c /*nullable*/) {
   const Sizes z = compute_sizes(md, rd);
-  const size_t d = md->d_model, hd = md->head_dim, H = md->n_heads, KV = md->n_kv_heads, F = md->d_ff,
-               V = md->vocab;
+  const ModelDims lm = local_dims(md, rd);
+  const size_t d = lm.d, hd = lm.hd, H = lm.H, KV = lm.KV, F = lm.F, V = lm.V;
   Carver cv(c ? rd->workspace : nullptr);
   auto x = cv.take<float>((size_t)z.Tcap * d);
+  auto ar = cv.take<float>(tp_of(rd) > 1 ? (size_t)z.Tcap * d : 1);
   auto h = cv.take<__nv_bfloat16>((size_t)z.Tcap * d);
   auto qkv = cv.take<float>((size_t)z.Tcap * (H + 2 * KV) * hd);
   auto q = cv.take<__nv_bfloat16>((size_t)z.Tcap * H * hd);
@@ -256,12 +276,12 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto ks_local = cv.take<int>(4);
   auto ks = cv.take<int>((size_t)3 * std::max(1, rd->world));
   auto ctl = cv.take<CtlBlock>(1);
-  const size_t page_bytes = (size_t)md->n_layers * KV * 2 * kPage * hd * 2;
+  const size_t page_bytes = lm.page_bytes;
   const size_t max_pages = rd->kv_pool_bytes / page_bytes;
   auto free_stack = cv.take<int>(max_pages + 1);
   auto ident = cv.take<int>(max_pages + 1);
   if (c) {
-    c->x = x; c->h = h; c->qkv = qkv; c->q = q; c->att = att; c->mid = mid; c->logits = logits;
+    c->x = x; c->ar = ar; c->h = h; c->qkv = qkv; c->q = q; c->att = att; c->mid = mid; c->logits = logits;
     c->gpart = gpart; c->gctr = gctr; c->apart = apart; c->atickets = atick; c->inv_freq = invf;
     c->items_pre = items_pre; c->pre_tok = pre_tok; c->pre_pos = pre_pos; c->pre_pt = pre_pt;
     c->pre_last = pre_last; c->fork_jobs = fork_jobs; c->col_meta = col_meta; c->col_tok = col_tok;
@@ -292,8 +312,20 @@ static int validate(const rp_model_desc* md, const rp_runtime_desc* rd, std::str
   if (md->n_heads / md->n_kv_heads > 8) return bad("n_heads/n_kv_heads (<= 8)");
   if (((md->n_heads + 2 * md->n_kv_heads) * md->head_dim) % 128) return bad("qkv width (multiple of 128)");
   if (md->eos_id < 0 || md->eos_id >= md->vocab) return bad("eos_id");
+  if (rd->tp > 1) {
+    const int T = rd->tp;
+    if (rd->world != 1) return bad("tp (tensor parallelism needs world == 1 for this context)");
+    if (rd->tp_rank < 0 || rd->tp_rank >= T) return bad("tp_rank");
+    if (!rd->nccl_id) return bad("nccl_id (tp > 1)");
+    if (md->n_kv_heads % T || md->n_heads % T) return bad("tp (must divide n_heads and n_kv_heads)");
+    if ((md->d_ff / T) % 64 || md->d_ff % T) return bad("tp (d_ff / tp multiple of 64)");
+    if (md->vocab % T || (md->vocab / T) % 128) return bad("tp (vocab / tp multiple of 128)");
+    if (((md->n_heads + 2 * md->n_kv_heads) / T * md->head_dim) % 128) return bad("tp (local qkv width)");
+    if ((md->n_heads / T * md->head_dim) % 64) return bad("tp (local attention width)");
+  }
   if (rd->world < 1 || rd->rank < 0 || rd->rank >= rd->world) return bad("rank/world");
   if (rd->world > 1 && !rd->nccl_id) return bad("nccl_id (world > 1)");
+  if (rd->tp < 0 || rd->tp > 8) return bad("tp (1..8)");
   if (rd->max_seqs < 1 || rd->max_seqs > 1 << 16) return bad("max_seqs");
   if (rd->max_prompts < 1 || rd->max_prompts > rd->max_seqs) return bad("max_prompts");
   if (rd->max_prompt_len < 1 || rd->max_prompt_tokens < rd->max_prompt_len) return bad("max_prompt_len/tokens");
@@ -329,12 +361,24 @@ static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, in
   c->launches++;
 }
 
+// TP all-reduce (sum) of the row-parallel partial in c->ar over `rows` rows
+// (a host count: the graph bucket at decode, the prompt tokens at prefill).
+static void tp_allreduce_rows(RpCtx* c, int rows) {
+  ProfScope ps(c, RP_PROF_NCCL);
+  ncclAllReduce(c->ar, c->ar, (size_t)rows * c->m.d, ncclFloat32, ncclSum, c->comm, c->st);
+}
+
 // Transformer body over `n` rows (n_dev on device or n_host): decode (one token
-// per live sequence) or prefill (all prompt tokens).
+// per live sequence) or prefill (all prompt tokens).  Under tensor
+// parallelism the O and down GEMMs write their partial sums to c->ar, which
+// is all-reduced and added to the residual stream by the next RMSNorm
+// (`*pending` tells the caller the final norm still owes that add).
 static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_host, const int* row_pos,
                            const int* row_pt, const AttnItem* items, const int* n_items_dev, int n_items_host,
-                           bool decode) {
+                           bool decode, int ar_rows, bool* pending) {
   const ModelDims& m = c->m;
+  const bool tp = c->tp > 1;
+  const float* delta = nullptr;
   const int qkvw = (m.H + 2 * m.KV) * m.hd;
   const int sp_qkv = decode ? c->s_qkv : 1, sp_o = decode ? c->s_o : 1, sp_gu = decode ? c->s_gu : 1,
             sp_down = decode ? c->s_down : 1;
@@ -342,7 +386,7 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
   for (int l = 0; l < m.L; ++l) {
     LayerW& w = c->layers[l];
     { ProfScope ps(c, RP_PROF_RMSNORM);
-      launch_rmsnorm(c->x, nullptr, n_dev, n_host, w.ln1, c->h, m.d, m.eps, c->st); c->launches++; }
+      launch_rmsnorm(c->x, delta, nullptr, n_dev, n_host, w.ln1, c->h, m.d, m.eps, c->st); c->launches++; }
     { ProfScope ps(c, RP_PROF_GEMM_QKV);
       gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_F32, c->qkv, qkvw, w.bqkv); }
     { ProfScope ps(c, RP_PROF_ROPE);
@@ -352,27 +396,50 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
       launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
                        c->apart, c->atickets, m, l, c->st); c->launches++; }
     { ProfScope ps(c, RP_PROF_GEMM_O);
-      gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, EPI_RESID, c->x, m.d, nullptr); }
+      gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
+           nullptr); }
+    if (tp) tp_allreduce_rows(c, ar_rows);
     { ProfScope ps(c, RP_PROF_RMSNORM);
-      launch_rmsnorm(c->x, nullptr, n_dev, n_host, w.ln2, c->h, m.d, m.eps, c->st); c->launches++; }
+      launch_rmsnorm(c->x, tp ? c->ar : nullptr, nullptr, n_dev, n_host, w.ln2, c->h, m.d, m.eps, c->st);
+      c->launches++; }
     { ProfScope ps(c, RP_PROF_GEMM_GU);
       gemm(c, w.p_gu, 2 * m.F, m.d, n_dev, n_host, sp_gu, EPI_SWIGLU, c->mid, m.F, nullptr); }
     { ProfScope ps(c, RP_PROF_GEMM_DOWN);
-      gemm(c, w.p_down, m.d, m.F, n_dev, n_host, sp_down, EPI_RESID, c->x, m.d, nullptr); }
+      gemm(c, w.p_down, m.d, m.F, n_dev, n_host, sp_down, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
+           nullptr); }
+    if (tp) {
+      tp_allreduce_rows(c, ar_rows);
+      delta = c->ar;
+    }
+  }
+  *pending = tp;
+}
+
+// LM head over this rank's vocab shard + sampling; under TP the packed
+// per-row argmax is MAX-all-reduced (exact: the order of maxima is irrelevant).
+static void lm_head_sample(RpCtx* c, const int* n_dev, int n_host, const int* gather, int rows_out, int row_div,
+                           int best_rows, bool pending, int splits) {
+  RoundDev& R = c->R;
+  { ProfScope ps(c, RP_PROF_RMSNORM);
+    launch_rmsnorm(c->x, pending ? c->ar : nullptr, gather, n_dev, n_host, c->lnf, c->h, c->m.d, c->m.eps, c->st);
+    c->launches++; }
+  { ProfScope ps(c, RP_PROF_GEMM_LM);
+    gemm(c, c->p_lm, c->m.V, c->m.d, n_dev, rows_out, splits, EPI_F32, c->logits, c->m.V, nullptr); }
+  { ProfScope ps(c, RP_PROF_SAMPLER);
+    launch_sampler(c->logits, c->m.V, c->m.v0, row_div, R, c->rd.sample_seed, 1.0f / c->rd.temperature,
+                   (uint32_t)c->round_id, c->st); c->launches++; }
+  if (c->tp > 1) {
+    ProfScope ps(c, RP_PROF_NCCL);
+    ncclAllReduce(R.best, R.best, (size_t)best_rows, ncclUint64, ncclMax, c->comm, c->st);
   }
 }
 
-static void decode_step(RpCtx* c) {
+static void decode_step(RpCtx* c, int bucket) {
   RoundDev& R = c->R;
   const int* n_dev = &R.ctl->n_live;
-  forward_layers(c, R.tok_in, n_dev, 0, R.row_pos, R.row_pt, R.items, &R.ctl->n_items, 0, true);
-  { ProfScope ps(c, RP_PROF_RMSNORM);
-    launch_rmsnorm(c->x, nullptr, n_dev, 0, c->lnf, c->h, c->m.d, c->m.eps, c->st); c->launches++; }
-  { ProfScope ps(c, RP_PROF_GEMM_LM);
-    gemm(c, c->p_lm, c->m.V, c->m.d, n_dev, 0, c->s_lm, EPI_F32, c->logits, c->m.V, nullptr); }
-  { ProfScope ps(c, RP_PROF_SAMPLER);
-    launch_sampler(c->logits, c->m.V, 1, R, c->rd.sample_seed, 1.0f / c->rd.temperature, (uint32_t)c->round_id,
-                   c->st); c->launches++; }
+  bool pending = false;
+  forward_layers(c, R.tok_in, n_dev, 0, R.row_pos, R.row_pt, R.items, &R.ctl->n_items, 0, true, bucket, &pending);
+  lm_head_sample(c, n_dev, 0, nullptr, 0, 1, bucket, pending, c->s_lm);
   if (c->rd.world == 1) {
     ProfScope ps(c, RP_PROF_CTL);
     launch_ctl(R, 1, 0, c->st); c->launches++;
@@ -386,22 +453,39 @@ static void decode_step(RpCtx* c) {
 // (Re)capture graph_steps decode steps.  Kernel parameters (the RoundDev
 // scalars: cap, G, target, kind, trace, round id) are baked into the graph, so
 // it is rebuilt once per round, before its first decode step.
-static int ensure_graph(RpCtx* c) {
-  if (c->rd.graph_steps <= 0 || !c->graph_dirty) return RP_OK;
-  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+// Live-row bucket of a decode step: the kernels read the live count on the
+// device, but NCCL counts are host values, so under TP the graphs are keyed
+// by a power-of-two bucket >= the live count (the count only shrinks).
+static int bucket_for(const RpCtx* c, int n) {
+  if (c->tp <= 1) return c->z.S;
+  int b = 16;
+  while (b < n) b *= 2;
+  return std::min(b, c->z.S);
+}
+
+static int ensure_graph(RpCtx* c, int bucket) {
+  if (c->graph_dirty) {
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    c->graph_dirty = false;
+  }
+  for (auto& g : c->graphs)
+    if (g.bucket == bucket) { c->gexec = g.exec; c->graph_nodes = g.nodes; return RP_OK; }
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
   const long long before = c->launches;
   c->capturing = true;
-  for (int i = 0; i < c->rd.graph_steps; ++i) decode_step(c);
+  for (int i = 0; i < c->rd.graph_steps; ++i) decode_step(c, bucket);
   c->capturing = false;
   cudaError_t e = cudaStreamEndCapture(c->st, &g);
   if (e != cudaSuccess) return c->fail(RP_ECUDA, "graph capture: %s", cudaGetErrorString(e));
-  c->graph_nodes = (int)(c->launches - before);
+  RpCtx::Graph entry{bucket, nullptr, (int)(c->launches - before)};
   c->launches = before;
-  CK(cudaGraphInstantiate(&c->gexec, g, 0));
+  CK(cudaGraphInstantiate(&entry.exec, g, 0));
   CK(cudaGraphDestroy(g));
-  c->graph_dirty = false;
+  c->graphs.push_back(entry);
+  c->gexec = entry.exec;
+  c->graph_nodes = entry.nodes;
   return RP_OK;
 }
 
@@ -414,9 +498,9 @@ int rp_query_sizes(const rp_model_desc* md, const rp_runtime_desc* rd, rp_sizes*
   int r = validate(md, rd, e);
   if (r) { g_init_err = e; return r; }
   if (!out) { g_init_err = "invalid field: out"; return RP_EINVAL; }
-  out->weights_bytes = weight_layout(md).total;
+  out->weights_bytes = weight_layout(md, rd).total;
   out->workspace_bytes = workspace_bytes(md, rd, nullptr);
-  out->page_bytes = (size_t)md->n_layers * md->n_kv_heads * 2 * kPage * md->head_dim * 2;
+  out->page_bytes = local_dims(md, rd).page_bytes;
   return RP_OK;
 }
 
@@ -429,9 +513,8 @@ static int init_impl(RpCtx* c) {
     c->own_stream = true;
   }
   ModelDims& m = c->m;
-  m.L = md->n_layers; m.d = md->d_model; m.H = md->n_heads; m.KV = md->n_kv_heads; m.hd = md->head_dim;
-  m.F = md->d_ff; m.V = md->vocab; m.eos = md->eos_id; m.eps = md->rms_eps;
-  m.page_bytes = (size_t)m.L * m.KV * 2 * kPage * m.hd * 2;
+  m = local_dims(md, rd);
+  c->tp = tp_of(rd);
   c->z = compute_sizes(md, rd);
   int dev = 0;
   CK(cudaGetDevice(&dev));
@@ -439,7 +522,7 @@ static int init_impl(RpCtx* c) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, dev));
   if (cc_major != 10) return c->fail(RP_ECUDA, "device is not sm_100 (compute capability %d.x)", cc_major);
-  const WeightLayout wl = weight_layout(md);
+  const WeightLayout wl = weight_layout(md, rd);
   if (rd->weights_bytes < wl.total) return c->fail(RP_ENOSPC, "weights buffer too small: %zu < %zu", rd->weights_bytes, wl.total);
   const size_t ws = workspace_bytes(md, rd, nullptr);
   if (rd->workspace_bytes < ws) return c->fail(RP_ENOSPC, "workspace too small: %zu < %zu", rd->workspace_bytes, ws);
@@ -471,28 +554,39 @@ static int init_impl(RpCtx* c) {
     w.ln1 = (float*)(wb + wl.off[k++]);
     w.ln2 = (float*)(wb + wl.off[k++]);
     const uint32_t base = 0x100u * (uint32_t)(l + 1);
-    launch_init_weights(w.wqkv, (long long)H * hd * d, base + 0, seed, 0, (int)d, 0, c->st);
-    launch_init_weights(w.wqkv + H * hd * d, (long long)KV * hd * d, base + 1, seed, 0, (int)d, 0, c->st);
-    launch_init_weights(w.wqkv + (H + KV) * hd * d, (long long)KV * hd * d, base + 2, seed, 0, (int)d, 0, c->st);
+    // this rank's shard = a block of each full tensor (rank r of T: q rows
+    // [r*H*hd, ...), k/v rows [r*KV*hd, ...), o columns [r*H*hd, ...), gate/up
+    // rows [r*F, ...), down columns [r*F, ...); H, KV, F are local here)
+    const int tr = c->tp > 1 ? rd->tp_rank : 0;
+    const size_t Hf = (size_t)md->n_heads, Ff = (size_t)md->d_ff;
+    launch_init_weights(w.wqkv, (long long)(H * hd), (int)d, (long long)tr * H * hd, 0, (int)d, base + 0, seed, 0, 0,
+                        c->st);
+    launch_init_weights(w.wqkv + H * hd * d, (long long)(KV * hd), (int)d, (long long)tr * KV * hd, 0, (int)d,
+                        base + 1, seed, 0, 0, c->st);
+    launch_init_weights(w.wqkv + (H + KV) * hd * d, (long long)(KV * hd), (int)d, (long long)tr * KV * hd, 0, (int)d,
+                        base + 2, seed, 0, 0, c->st);
     if (md->qkv_bias) {
-      launch_init_weights(w.bqkv, (long long)H * hd, base + 3, seed, 1, 1, 0, c->st);
-      launch_init_weights(w.bqkv + H * hd, (long long)KV * hd, base + 4, seed, 1, 1, 0, c->st);
-      launch_init_weights(w.bqkv + (H + KV) * hd, (long long)KV * hd, base + 5, seed, 1, 1, 0, c->st);
+      launch_init_weights(w.bqkv, (long long)(H * hd), 1, (long long)tr * H * hd, 0, 1, base + 3, seed, 1, 0, c->st);
+      launch_init_weights(w.bqkv + H * hd, (long long)(KV * hd), 1, (long long)tr * KV * hd, 0, 1, base + 4, seed, 1,
+                          0, c->st);
+      launch_init_weights(w.bqkv + (H + KV) * hd, (long long)(KV * hd), 1, (long long)tr * KV * hd, 0, 1, base + 5,
+                          seed, 1, 0, c->st);
     } else {
       CK(cudaMemsetAsync(w.bqkv, 0, (H + 2 * KV) * hd * 4, c->st));
     }
-    launch_init_weights(w.wo, (long long)d * H * hd, base + 6, seed, 0, (int)(H * hd), 0, c->st);
-    launch_init_weights(w.wgu, (long long)F * d, base + 7, seed, 2, (int)d, 0, c->st);
-    launch_init_weights(w.wgu, (long long)F * d, base + 8, seed, 2, (int)d, 1, c->st);
-    launch_init_weights(w.wd, (long long)d * F, base + 9, seed, 0, (int)F, 0, c->st);
+    launch_init_weights(w.wo, (long long)d, (int)(H * hd), 0, (int)(tr * H * hd), (int)(Hf * hd), base + 6, seed, 0, 0,
+                        c->st);
+    launch_init_weights(w.wgu, (long long)F, (int)d, (long long)tr * F, 0, (int)d, base + 7, seed, 2, 0, c->st);
+    launch_init_weights(w.wgu, (long long)F, (int)d, (long long)tr * F, 0, (int)d, base + 8, seed, 2, 1, c->st);
+    launch_init_weights(w.wd, (long long)d, (int)F, 0, (int)(tr * F), (int)Ff, base + 9, seed, 0, 0, c->st);
     CK(cudaMemcpyAsync(w.ln1, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(w.ln2, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
   }
   c->emb = (__nv_bfloat16*)(wb + wl.off[k++]);
   c->lm = (__nv_bfloat16*)(wb + wl.off[k++]);
   c->lnf = (float*)(wb + wl.off[k++]);
-  launch_init_weights(c->emb, (long long)V * d, 0x10000000u, seed, 0, (int)d, 0, c->st);
-  launch_init_weights(c->lm, (long long)V * d, 0x10000001u, seed, 0, (int)d, 0, c->st);
+  launch_init_weights(c->emb, (long long)md->vocab, (int)d, 0, 0, (int)d, 0x10000000u, seed, 0, 0, c->st);
+  launch_init_weights(c->lm, (long long)V, (int)d, (long long)m.v0, 0, (int)d, 0x10000001u, seed, 0, 0, c->st);
   CK(cudaMemcpyAsync(c->lnf, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
   CK(cudaGetLastError());
 
@@ -535,10 +629,11 @@ static int init_impl(RpCtx* c) {
   CK(cudaMemcpyAsync(c->R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
 
   // ---- NCCL
-  if (rd->world > 1) {
+  if (rd->world > 1 || c->tp > 1) {   // DP cutoff exchange or TP all-reduces
     ncclUniqueId id;
     memcpy(&id, rd->nccl_id, sizeof id);
-    CKN(ncclCommInitRank(&c->comm, rd->world, id, rd->rank));
+    if (c->tp > 1) CKN(ncclCommInitRank(&c->comm, c->tp, id, rd->tp_rank));
+    else CKN(ncclCommInitRank(&c->comm, rd->world, id, rd->rank));
   }
 
   c->graph_dirty = true;
@@ -576,7 +671,7 @@ int rp_nccl_unique_id(void* out) {
 void rp_free(void* ctx) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return;
-  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->trace_dev) cudaFree(c->trace_dev);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -646,8 +741,11 @@ static int prefill(RpCtx* c, const std::vector<int>& toks, const std::vector<int
   CK(cudaMemcpyAsync(c->pre_pt, pt.data(), T * 4, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->items_pre, items.data(), items.size() * sizeof(AttnItem), cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->pre_last, out_rows.data(), out_rows.size() * 4, cudaMemcpyHostToDevice, c->st));
-  forward_layers(c, c->pre_tok, nullptr, T, c->pre_pos, c->pre_pt, c->items_pre, nullptr, (int)items.size(), false);
-  launch_rmsnorm(c->x, c->pre_last, nullptr, (int)out_rows.size(), c->lnf, c->h, c->m.d, c->m.eps, c->st);
+  bool pending = false;
+  forward_layers(c, c->pre_tok, nullptr, T, c->pre_pos, c->pre_pt, c->items_pre, nullptr, (int)items.size(), false,
+                 T, &pending);
+  launch_rmsnorm(c->x, pending ? c->ar : nullptr, c->pre_last, nullptr, (int)out_rows.size(), c->lnf, c->h, c->m.d,
+                 c->m.eps, c->st);
   c->launches++;
   gemm(c, c->p_lm, c->m.V, c->m.d, nullptr, (int)out_rows.size(), 1, EPI_F32, c->logits, c->m.V, nullptr);
   CK(cudaGetLastError());
@@ -681,7 +779,7 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
       all[i].id = p.prompt_id;
       all[i].tokens.assign(p.tokens, p.tokens + p.len);
       for (int t : all[i].tokens)
-        if (t < 0 || t >= c->m.V || t == c->m.eos) return c->fail(RP_EINVAL, "invalid field: prompts[%d].tokens", i);
+        if (t < 0 || t >= c->md.vocab || t == c->m.eos) return c->fail(RP_EINVAL, "invalid field: prompts[%d].tokens", i);
       if (trace) {
         if (!p.trace_lens) return c->fail(RP_EINVAL, "invalid field: prompts[%d].trace_lens (RP_TRACE)", i);
         all[i].trace.assign(p.trace_lens, p.trace_lens + G);
@@ -770,8 +868,10 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   CK(cudaMemcpyAsync(R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
   if (c->trace_dev) CK(cudaMemsetAsync(c->trace_dev, 0, (size_t)c->trace_steps * (2 + S) * 4, c->st));
   // ---- step 1: token 1 of every sibling from its prompt's prefill logits
-  launch_sampler(c->logits, c->m.V, G, R, c->rd.sample_seed, 1.0f / c->rd.temperature, (uint32_t)round_id, c->st);
+  launch_sampler(c->logits, c->m.V, c->m.v0, G, R, c->rd.sample_seed, 1.0f / c->rd.temperature, (uint32_t)round_id,
+                 c->st);
   c->launches++;
+  if (c->tp > 1 && nS > 0) CKN(ncclAllReduce(R.best, R.best, (size_t)nS, ncclUint64, ncclMax, c->comm, c->st));
   if (c->rd.world == 1) {
     launch_ctl(R, 0, 0, c->st); c->launches++;
   } else {
@@ -810,12 +910,12 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
   int rc = read_ctl(c);
   if (rc) return rc;
   int steps = 0;
-  if (!c->h_ctl->done && max_steps > 0 && (rc = ensure_graph(c))) return rc;
   while (!c->h_ctl->done && steps < max_steps) {
+    const int bucket = bucket_for(c, c->h_ctl->n_live);
     if (c->prof_steps_left > 0) {
       const int rows = c->h_ctl->n_live;
       const long long ctx = c->h_ctl->ctx_sum;
-      decode_step(c);
+      decode_step(c, bucket);
       CK(cudaGetLastError());
       CK(cudaStreamSynchronize(c->st));
       for (size_t i = 0; i + 1 < c->ev.size(); i += 2) {
@@ -829,12 +929,13 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
       c->prof_rows += rows; c->prof_ctx += ctx; c->prof_step_count += 1;
       c->prof_steps_left -= 1;
       steps += 1;
-    } else if (c->gexec) {
+    } else if (c->rd.graph_steps > 0) {
+      if ((rc = ensure_graph(c, bucket))) return rc;
       CK(cudaGraphLaunch(c->gexec, c->st));
       c->launches += c->graph_nodes;
       steps += c->rd.graph_steps;
     } else {
-      decode_step(c);
+      decode_step(c, bucket);
       CK(cudaGetLastError());
       steps += 1;
       c->step_logits_valid = true;
@@ -908,7 +1009,7 @@ int rp_debug_logits(void* ctx, const int32_t* tokens, int32_t n, float* logits_o
   if (c->active) return c->fail(RP_EBUSY, "a round is active");
   if (n < 1 || n > c->rd.max_prompt_len || n > c->rd.max_prompt_tokens) return c->fail(RP_EINVAL, "invalid field: n");
   for (int i = 0; i < n; ++i)
-    if (tokens[i] < 0 || tokens[i] >= c->m.V) return c->fail(RP_EINVAL, "invalid field: tokens[%d]", i);
+    if (tokens[i] < 0 || tokens[i] >= c->md.vocab) return c->fail(RP_EINVAL, "invalid field: tokens[%d]", i);
   std::vector<int> toks(tokens, tokens + n), plen{n}, rows(n);
   for (int i = 0; i < n; ++i) rows[i] = i;
   int top = c->n_pages;

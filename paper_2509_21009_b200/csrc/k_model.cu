@@ -6,41 +6,42 @@
 namespace rp {
 
 // ------------------------------------------------------------- weight formula
-// mode 0: bf16 out[i]; mode 1: fp32 out[i] (biases, exact widening of the bf16
-// value); mode 2: gate/up rows interleaved in 64-row blocks of a [2F, d]
-// tensor (`up` selects the second half of each 128-row block).
-__global__ void init_weights_kernel(void* out, long long n, uint32_t tid, uint32_t k0, uint32_t k1, int mode,
-                                    int in_features, int up) {
+// Generates the [rows, cols] block whose element (r, c) is element
+// (r0 + r, c0 + c) of the logical [*, in_full] tensor `tid` (TP shards are
+// blocks of the full tensor).  mode 0: bf16 out[r][c]; mode 1: fp32 out[r][c]
+// (biases, exact widening of the bf16 value); mode 2: gate/up rows
+// interleaved in 64-row blocks of a [2*rows, cols] tensor (`up` selects the
+// second half of each 128-row block).
+__global__ void init_weights_kernel(void* out, long long rows, int cols, long long r0, int c0, int in_full,
+                                    uint32_t tid, uint32_t k0, uint32_t k1, int mode, int up) {
   const float a = 0.034641016151377546f;   // fl32(0.02 * sqrt(3))
-  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b * 4 < n;
-       b += (long long)gridDim.x * blockDim.x) {
-    U4 x = philox((uint32_t)b, tid, 0u, 0x57454947u, k0, k1);
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      long long i = b * 4 + w;
-      if (i >= n) break;
-      float u2m1 = __fsub_rn(__fmul_rn(__fadd_rn(__uint2float_rn(u4_word(x, w) >> 9), 0.5f), 2.384185791015625e-07f),
-                             1.0f);
-      __nv_bfloat16 v = __float2bfloat16_rn(__fmul_rn(a, u2m1));
-      if (mode == 1) {
-        ((float*)out)[i] = __bfloat162float(v);
-      } else if (mode == 2) {
-        long long r = i / in_features, c = i % in_features;
-        long long pr = (r / 64) * 128 + (r % 64) + (up ? 64 : 0);
-        ((__nv_bfloat16*)out)[pr * in_features + c] = v;
-      } else {
-        ((__nv_bfloat16*)out)[i] = v;
-      }
+  const long long n = rows * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cols, c = e % cols;
+    const long long i = (r0 + r) * in_full + (c0 + c);          // logical index
+    const U4 x = philox((uint32_t)(i >> 2), tid, 0u, 0x57454947u, k0, k1);
+    const float u2m1 =
+        __fsub_rn(__fmul_rn(__fadd_rn(__uint2float_rn(u4_word(x, (int)(i & 3)) >> 9), 0.5f), 2.384185791015625e-07f),
+                  1.0f);
+    const __nv_bfloat16 v = __float2bfloat16_rn(__fmul_rn(a, u2m1));
+    if (mode == 1) {
+      ((float*)out)[e] = __bfloat162float(v);
+    } else if (mode == 2) {
+      const long long pr = (r / 64) * 128 + (r % 64) + (up ? 64 : 0);
+      ((__nv_bfloat16*)out)[pr * cols + c] = v;
+    } else {
+      ((__nv_bfloat16*)out)[e] = v;
     }
   }
 }
 
-void launch_init_weights(void* out, long long n, uint32_t tid, uint64_t seed, int mode, int in_features, int up,
-                         cudaStream_t st) {
-  long long blocks = (n + 4 * 256 - 1) / (4 * 256);
-  int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
-  init_weights_kernel<<<grid, 256, 0, st>>>(out, n, tid, (uint32_t)seed, (uint32_t)(seed >> 32), mode,
-                                            in_features, up);
+void launch_init_weights(void* out, long long rows, int cols, long long r0, int c0, int in_full, uint32_t tid,
+                         uint64_t seed, int mode, int up, cudaStream_t st) {
+  const long long n = rows * cols;
+  long long blocks = (n + 255) / 256;
+  int grid = (int)(blocks < 148 * 64 ? blocks : 148 * 64);
+  init_weights_kernel<<<grid, 256, 0, st>>>(out, rows, cols, r0, c0, in_full, tid, (uint32_t)seed,
+                                            (uint32_t)(seed >> 32), mode, up);
 }
 
 // Row kernels: one wave of 148 CTAs for device-side (decode) row counts; up
@@ -67,17 +68,30 @@ void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb,
 
 // -------------------------------------------------------------------- RMSNorm
 // h[r] = bf16( x[src] / sqrt(mean(x[src]^2) + eps) * gamma ),  src = gather ? gather[r] : r
-__global__ void rmsnorm_kernel(const float* x, const int* gather, const int* n_dev, int n_host, const float* gamma,
-                               __nv_bfloat16* h, int d, float eps) {
+// With `delta` (tensor parallelism): x[r] += delta[r] first (the all-reduced
+// partial of a row-parallel GEMM) and the updated row is written back.
+__global__ void rmsnorm_kernel(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
+                               const float* gamma, __nv_bfloat16* h, int d, float eps) {
   __shared__ float red[32];
   const int n = n_dev ? *n_dev : n_host;
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
     const int src = gather ? gather[r] : r;
-    const float4* xr = (const float4*)(x + (size_t)src * d);
+    float4* xr = (float4*)(x + (size_t)src * d);
     float ss = 0.f;
-    for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
-      float4 v = xr[c];
-      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    if (delta) {
+      const float4* dr = (const float4*)(delta + (size_t)src * d);
+      for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+        float4 v = xr[c];
+        const float4 a = dr[c];
+        v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+        xr[c] = v;
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      }
+    } else {
+      for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+        float4 v = xr[c];
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      }
     }
     ss = warp_sum(ss);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -100,9 +114,10 @@ __global__ void rmsnorm_kernel(const float* x, const int* gather, const int* n_d
   }
 }
 
-void launch_rmsnorm(const float* x, const int* gather, const int* n_dev, int n_host, const float* gamma, void* h,
-                    int d, float eps, cudaStream_t st) {
-  rmsnorm_kernel<<<row_grid(n_dev, n_host), 256, 0, st>>>(x, gather, n_dev, n_host, gamma, (__nv_bfloat16*)h, d, eps);
+void launch_rmsnorm(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
+                    const float* gamma, void* h, int d, float eps, cudaStream_t st) {
+  rmsnorm_kernel<<<row_grid(n_dev, n_host), 256, 0, st>>>(x, delta, gather, n_dev, n_host, gamma, (__nv_bfloat16*)h,
+                                                          d, eps);
 }
 
 // -------------------------------------------------------- RoPE + KV append

@@ -19,8 +19,12 @@ namespace rp {
 // ------------------------------------------------------------------ sampler
 constexpr int SAMP_CHUNK = 4096;   // vocab entries per work unit
 
-__global__ void __launch_bounds__(256) sampler_kernel(const float* __restrict__ logits, int V, int row_div, RoundDev R,
-                                                       uint32_t k0, uint32_t k1, float inv_temp, uint32_t round_id) {
+// Under tensor parallelism `logits` holds the vocab shard [v0, v0 + V): the
+// noise and the packed index use the global vocab id, only the shard owning
+// EOS masks / forces it, and the per-row maxima are then MAX-all-reduced.
+__global__ void __launch_bounds__(256) sampler_kernel(const float* __restrict__ logits, int V, int v0, int row_div,
+                                                       RoundDev R, uint32_t k0, uint32_t k1, float inv_temp,
+                                                       uint32_t round_id) {
   const int n = R.ctl->n_live;
   const int t = R.ctl->t;
   const int chunks = (V + SAMP_CHUNK - 1) / SAMP_CHUNK;
@@ -30,7 +34,8 @@ __global__ void __launch_bounds__(256) sampler_kernel(const float* __restrict__ 
     const int s = R.live[i];
     const int L = R.trace ? R.trace_L[s] : 0x7FFFFFFF;
     if (R.trace && t == L) {                       // forced EOS at the trace length
-      if (ch == 0 && threadIdx.x == 0) atomicMax(&R.best[i], pack_arg(INFINITY, (uint32_t)R.eos));
+      if (ch == 0 && threadIdx.x == 0 && R.eos >= v0 && R.eos < v0 + V)
+        atomicMax(&R.best[i], pack_arg(INFINITY, (uint32_t)R.eos));
       continue;
     }
     const uint32_t uid = (uint32_t)(R.p_gid[R.slot_prompt[s]] * R.G + R.slot_j[s]);
@@ -39,11 +44,11 @@ __global__ void __launch_bounds__(256) sampler_kernel(const float* __restrict__ 
     const int v_end = min(V, (ch + 1) * SAMP_CHUNK);
     for (int b = ch * (SAMP_CHUNK / 4) + threadIdx.x; 4 * b < v_end; b += blockDim.x) {
       const float4 z4 = *(const float4*)(lr + 4 * b);
-      const U4 x = philox((uint32_t)b, (uint32_t)t, uid, round_id, k0, k1);
+      const U4 x = philox((uint32_t)(b + (v0 >> 2)), (uint32_t)t, uid, round_id, k0, k1);
       const float zl[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        const int v = 4 * b + w;
+        const int v = v0 + 4 * b + w;                 // global vocab id
         const float uu = u01(u4_word(x, w));
         float z = zl[w] * inv_temp - logf(-logf(uu));
         if (R.trace && v == R.eos) z = -INFINITY;   // t < L here
@@ -67,10 +72,10 @@ __global__ void __launch_bounds__(256) sampler_kernel(const float* __restrict__ 
   }
 }
 
-void launch_sampler(const float* logits, int V, int row_div, const RoundDev& R, uint64_t seed, float inv_temp,
-                    uint32_t round_id, cudaStream_t st) {
-  sampler_kernel<<<148 * 4, 256, 0, st>>>(logits, V, row_div, R, (uint32_t)seed, (uint32_t)(seed >> 32), inv_temp,
-                                          round_id);
+void launch_sampler(const float* logits, int V, int v0, int row_div, const RoundDev& R, uint64_t seed,
+                    float inv_temp, uint32_t round_id, cudaStream_t st) {
+  sampler_kernel<<<148 * 4, 256, 0, st>>>(logits, V, v0, row_div, R, (uint32_t)seed, (uint32_t)(seed >> 32),
+                                          inv_temp, round_id);
 }
 
 // --------------------------------------------------------------------- ctl

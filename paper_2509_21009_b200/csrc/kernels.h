@@ -58,19 +58,22 @@ struct RoundDev {
   int* trace_buf; int trace_steps;   // debug: [steps][2 + S] (n, acc|done<<30, live...)
 };
 
+// Per-rank model dimensions: under tensor parallelism H, KV, F and V are the
+// local shard sizes (vocab rows [v0, v0 + V) of the LM head live here).
 struct ModelDims {
   int L, d, H, KV, hd, F, V, eos;
+  int v0;                  // first vocab id of this rank's LM-head shard
   float eps;
   size_t page_bytes;       // one page: [L][KV][2][kPage][hd] bf16
 };
 
 // weights
-void launch_init_weights(void* out, long long n, uint32_t tid, uint64_t seed, int mode, int in_features,
-                         int up, cudaStream_t st);
+void launch_init_weights(void* out, long long rows, int cols, long long r0, int c0, int in_full, uint32_t tid,
+                         uint64_t seed, int mode, int up, cudaStream_t st);
 // forward pieces (n = n_dev ? *n_dev : n_host)
 void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb, float* x, int d, cudaStream_t st);
-void launch_rmsnorm(const float* x, const int* gather, const int* n_dev, int n_host, const float* gamma,
-                    void* h, int d, float eps, cudaStream_t st);
+void launch_rmsnorm(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
+                    const float* gamma, void* h, int d, float eps, cudaStream_t st);
 void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const int* row_pos, const int* row_pt,
                         const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
                         const double* inv_freq, cudaStream_t st);
@@ -81,8 +84,8 @@ void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_
                       cudaStream_t st);
 void launch_kv_fork(const int* jobs /*[n][3] src,dst,rows*/, int n, void* kv_pool, const ModelDims& m,
                     cudaStream_t st);
-void launch_sampler(const float* logits, int V, int row_div, const RoundDev& R, uint64_t seed, float inv_temp,
-                    uint32_t round_id, cudaStream_t st);
+void launch_sampler(const float* logits, int V, int v0, int row_div, const RoundDev& R, uint64_t seed,
+                    float inv_temp, uint32_t round_id, cudaStream_t st);
 void launch_ctl(const RoundDev& R, int appended, int mode /*0 all, 1 phase A, 2 phase B*/, cudaStream_t st);
 void launch_collect_pack(const RoundDev& R, int* meta /*[acc*G][4]*/, int* tokens, cudaStream_t st);
 int attn_smem_bytes(int hd);

@@ -33,7 +33,7 @@ class RuntimeDesc(ctypes.Structure):
                 ("max_seqs", ctypes.c_int32), ("max_prompts", ctypes.c_int32), ("max_prompt_len", ctypes.c_int32),
                 ("max_prompt_tokens", ctypes.c_int32), ("max_cap", ctypes.c_int32),
                 ("sample_seed", ctypes.c_uint64), ("temperature", ctypes.c_float), ("graph_steps", ctypes.c_int32),
-                ("nccl_id", ctypes.c_void_p)]
+                ("nccl_id", ctypes.c_void_p), ("tp", ctypes.c_int32), ("tp_rank", ctypes.c_int32)]
 
 
 class Sizes(ctypes.Structure):
@@ -138,7 +138,7 @@ class Engine:
 
     def __init__(self, cfg, max_seqs, max_prompts, max_prompt_len, max_prompt_tokens, max_cap, kv_pool_bytes=None,
                  kv_fraction=0.85, weight_seed=0, sample_seed=3, temperature=1.0, graph_steps=16, rank=0, world=1,
-                 nccl_id=None, stream=None):
+                 nccl_id=None, stream=None, tp=1, tp_rank=0):
         import torch
         self.torch = torch
         self.L = lib()
@@ -150,6 +150,8 @@ class Engine:
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
         rd = RuntimeDesc()
         rd.rank, rd.world = rank, world
+        rd.tp, rd.tp_rank = tp, tp_rank
+        self.tp, self.tp_rank = tp, tp_rank
         rd.max_seqs, rd.max_prompts, rd.max_prompt_len = max_seqs, max_prompts, max_prompt_len
         rd.max_prompt_tokens, rd.max_cap = max_prompt_tokens, max_cap
         rd.sample_seed, rd.temperature, rd.graph_steps = sample_seed, temperature, graph_steps
@@ -260,8 +262,9 @@ class Engine:
 
     # ------------------------------------------------------------ test-only
     def debug_logits(self, tokens):
+        """Teacher-forced logits (under TP: this rank's vocab shard)."""
         toks = np.ascontiguousarray(tokens, dtype=np.int32)
-        out = np.zeros((len(toks), self.cfg["vocab"]), dtype=np.float32)
+        out = np.zeros((len(toks), self.cfg["vocab"] // max(1, self.tp)), dtype=np.float32)
         self._check(self.L.rp_debug_logits(self.h, _i32p(toks), len(toks),
                                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
         return out
@@ -284,7 +287,7 @@ class Engine:
         return out
 
     def debug_last_logits(self):
-        out = np.zeros((self.max_seqs, self.cfg["vocab"]), dtype=np.float32)
+        out = np.zeros((self.max_seqs, self.cfg["vocab"] // max(1, self.tp)), dtype=np.float32)
         slots = np.zeros(self.max_seqs, dtype=np.int32)
         n = ctypes.c_int32()
         self._check(self.L.rp_debug_last_logits(self.h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
