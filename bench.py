@@ -146,30 +146,47 @@ def run_ours(a):
         obj = [rp.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+    # short rounds: data parallel over the N GPUs (prompts sharded by index)
     eng = rp.Engine(cfg, max_seqs=n_loc * G, max_prompts=n_loc, max_prompt_len=hi, max_prompt_tokens=n_loc * hi,
                     max_cap=max(W.R["short_cap"], W.R["long_cap"]), graph_steps=a.graph_steps, rank=rank,
-                    world=world, nccl_id=nccl_id, sample_seed=configs.SAMPLE_SEED)
+                    world=world, nccl_id=nccl_id, sample_seed=configs.SAMPLE_SEED,
+                    kv_fraction=0.85 if world == 1 else 0.45)
     st_ev = eng.stream
+    # long rounds (elastic TP): one TP=N group over the same GPUs,
+    # holding only its weight shard; every rank decodes all P0 queued prompts
+    eng_long = eng
+    if world > 1 and cfg["n_kv_heads"] % world == 0:
+        obj = [rp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        eng_long = rp.Engine(cfg, max_seqs=W.P0 * G, max_prompts=W.P0, max_prompt_len=hi,
+                             max_prompt_tokens=W.P0 * hi, max_cap=W.R["long_cap"], graph_steps=a.graph_steps,
+                             tp=world, tp_rank=rank, nccl_id=obj[0], sample_seed=configs.SAMPLE_SEED,
+                             kv_fraction=0.85, stream=st_ev)
 
     from paper_2509_21009_b200.dp import all_gather_ids as allgather_ids
 
     def one_round(round_no, profile=0):
         kind, ids, target, cap, L = W.plan()
+        e = eng_long if kind == "long" else eng
         plist = [W.prompts[i] for i in ids]
         h2d = sum(len(p["tokens"]) for p in plist) * 4 + L.size * 4
-        eng.submit(plist, G, cap, target if kind == "short" else len(ids), long_round=(kind == "long"), trace=L,
-                   round_id=round_no)
+        e.submit(plist, G, cap, target if kind == "short" else len(ids), long_round=(kind == "long"), trace=L,
+                 round_id=round_no)
         if profile:
-            eng.debug_profile_arm(profile)
-        st = eng.run()
-        res = eng.collect()
+            e.debug_profile_arm(profile)
+        st = e.run()
+        res = e.collect()
         acc_local = list(dict.fromkeys(r["prompt_id"] for r in res))
-        acc = allgather_ids(acc_local)
+        acc = acc_local if (kind == "long" and e is not eng) else allgather_ids(acc_local)
         W.commit(kind, ids, acc)
         d2h = sum(r["len"] for r in res) * 4 + len(res) * 24
         retained = sum(r["len"] for r in res)
-        return dict(kind=kind, t_end=st.t, decoded=st.decoded_tokens, retained=retained, h2d=h2d, d2h=d2h,
-                    accepted=st.accepted, underfilled=st.underfilled)
+        decoded = st.decoded_tokens
+        if e is not eng and rank != 0:
+            # TP ranks decode the same tokens: count them once (on rank 0)
+            decoded, retained, h2d, d2h = 0, 0, 0, 0
+        return dict(kind=kind, t_end=st.t, decoded=decoded, retained=retained, h2d=h2d, d2h=d2h,
+                    accepted=st.accepted, underfilled=st.underfilled, tp=e.tp)
 
     # ---- warm-up (the first warm-up round is profiled per kernel class)
     prof = None
@@ -183,7 +200,7 @@ def run_ours(a):
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = eng.launch_count()
+    launches0 = eng.launch_count() + (eng_long.launch_count() if eng_long is not eng else 0)
     w0 = time.perf_counter()
     e0.record(st_ev)
     rounds = []
@@ -206,7 +223,7 @@ def run_ours(a):
     clocks = clk.stop() if clk else None
     dev_s = e0.elapsed_time(e1) / 1e3
     wall_s = w1 - w0
-    launches = eng.launch_count() - launches0
+    launches = eng.launch_count() + (eng_long.launch_count() if eng_long is not eng else 0) - launches0
     # ---- reductions over ranks
     t = torch.tensor([dev_s, wall_s], dtype=torch.float64)
     tot = torch.tensor([sum(x["decoded"] for x in rounds), sum(x["retained"] for x in rounds),
@@ -220,9 +237,18 @@ def run_ours(a):
     dev_s, wall_s = t.tolist()
     decoded, retained, h2d, d2h, launches_all = tot.tolist()
     per_round = per_round.tolist()
-    if rank != 0:
+    def shutdown():
         if world > 1:
+            dist.barrier()
+        if eng_long is not eng:
+            eng_long.close()
+        eng.close()
+        if world > 1:
+            dist.barrier()
             dist.destroy_process_group()
+
+    if rank != 0:
+        shutdown()
         return
     short = [s for s, x in zip(per_round, rounds) if x["kind"] == "short"]
     long_ = [s for s, x in zip(per_round, rounds) if x["kind"] == "long"]
@@ -245,7 +271,7 @@ def run_ours(a):
                                    W.R["n_submit"], G, W.R["short_cap"]),
                    "global_prompts_per_short_round": W.n_submit, "P0": W.P0, "G": G,
                    "short_cap": W.R["short_cap"], "long_cap": W.R["long_cap"],
-                   "parallelism": "dp%d" % world, "l2": "inputs larger than L2 (15 GB weights streamed per step)",
+                   "parallelism": "short rounds dp%d, long rounds tp%d" % (world, world if eng_long is not eng else 1), "l2": "inputs larger than L2 (15 GB weights streamed per step)",
                    "graph_steps": a.graph_steps},
         "per_gpu_tokens_per_s": round(value / world, 1),
         "retained_tokens_per_s": round(retained / dev_s, 1),
@@ -263,13 +289,11 @@ def run_ours(a):
         line["roofline"], line["kernel_profile"] = roofline(prof, cfg)
     if world == 1:
         line["cpu_baseline"] = cpu_baseline(W, quick=True)
-    print(json.dumps(line))
+    emit(json.dumps(line))
     if a.out:
         with open(a.out, "w") as f:
             f.write(json.dumps(line) + "\n")
-    eng.close()
-    if world > 1:
-        dist.destroy_process_group()
+    shutdown()
 
 
 def load_peaks():
@@ -404,12 +428,23 @@ def run_reference(a):
                              "sample": "per step: 1-layer full-width Qwen2.5-7B-shaped fp64 oracle + LM head, "
                                        "2 decode steps, extrapolated to 28 layers"},
             "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    emit(json.dumps(line))
+
+
+_STDOUT_FD = None
+
+
+def emit(text):
+    """Write the result line to the real stdout (fd 1 is redirected to stderr
+    while the libraries run, so NCCL/CUDA banners cannot pollute it)."""
+    os.write(_STDOUT_FD if _STDOUT_FD is not None else 1, (text + "\n").encode())
 
 
 def main():
-    # NCCL's banner/debug log goes to stderr: stdout carries exactly one JSON line
-    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    global _STDOUT_FD
+    _STDOUT_FD = os.dup(1)
+    sys.stdout.flush()
+    os.dup2(2, 1)
     a = parse()
     if a.impl == "reference":
         run_reference(a)
