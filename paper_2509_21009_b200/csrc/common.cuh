@@ -82,6 +82,15 @@ __device__ __forceinline__ void mbar_wait_wd(uint32_t bar, uint32_t phase, int t
   } while (!ok);
 }
 
+// Programmatic dependent launch (PDL).  Every kernel of the step is launched
+// with programmatic stream serialization: it may start while its predecessor
+// finishes.  Each kernel first waits for the predecessor (griddepcontrol.wait)
+// before touching its outputs, then lets its own successor launch.  Because
+// the trigger comes after the wait, a kernel's pre-wait code can rely on all
+// kernels before its predecessor having completed.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -115,6 +124,22 @@ __device__ __forceinline__ int block_exscan(int v, int* total, int* smem /*>=33 
   __syncthreads();
   *total = tot;
   return base + x - v;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 }  // namespace rp

@@ -26,12 +26,13 @@
 
 namespace rp {
 
-constexpr int BM = 128, BK = 64, BN = 256, STAGES = 4;
+constexpr int BM = 128, BK = 64, BN = 256;
 constexpr int A_BYTES = BM * BK * 2;         // 16 KB
-constexpr int B_BYTES = BN * BK * 2;         // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int B_BYTES = BN * BK * 2;         // 32 KB (widest activation tile)
+constexpr int RING_BYTES = 4 * (A_BYTES + B_BYTES);   // 192 KB of stages
+constexpr int MAX_STAGES = 12;               // ring depth at small N (18 KB stages)
 constexpr int XCH_BYTES = 64 * 33 * 4;       // swiglu exchange
-constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + XCH_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int GEMM_SMEM = RING_BYTES + XCH_BYTES + 1024 /*align*/ + 8 * (2 * MAX_STAGES + 4) + 16;
 constexpr int GEMM_THREADS = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -136,15 +137,24 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   if ((int)blockIdx.x >= n_items) return;
   const int kb_total = a.K / BK;
 
+  // Ring geometry from the widest activation chunk: 16/64/256-row boxes; at
+  // small N the stages shrink and the ring deepens (more weight bytes in
+  // flight per SM for the HBM-bound small-batch regime).
+  const int wmax = min(BN, N);
+  const int brow_max = wmax > 192 ? 256 : wmax > 48 ? 64 : 16;
+  const int b_rows = ((wmax + brow_max - 1) / brow_max) * brow_max;
+  const int STAGE_BYTES = A_BYTES + ((b_rows * BK * 2 + 1023) & ~1023);
+  const int STAGES = min(MAX_STAGES, RING_BYTES / STAGE_BYTES);
+
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  float* xch = (float*)(smem + STAGES * STAGE_BYTES);
-  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES + XCH_BYTES);
-  // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]; then tmem slot, ticket
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+  float* xch = (float*)(smem + RING_BYTES);
+  uint64_t* bars = (uint64_t*)(smem + RING_BYTES + XCH_BYTES);
+  // bars: full[MAX_STAGES], empty[MAX_STAGES], tfull[2], tempty[2]; then tmem slot, ticket
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * MAX_STAGES + 4);
   int* ticket = (int*)(tmem_slot + 1);
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
-  const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + MAX_STAGES);
+  const uint32_t tfull0 = smem_u32(bars + 2 * MAX_STAGES), tempty0 = smem_u32(bars + 2 * MAX_STAGES + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -167,12 +177,15 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (!(warp == 0 && lane == 0)) pdl_wait();   // the producer waits after its weight prefetch
+  pdl_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer =====
       const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
       int stage = 0; uint32_t phase = 0;
+      bool first = true;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         Item I = decode_item(it, m_tiles, a.splits);
         const int kb0 = (int)((long)I.split * kb_total / a.splits), kb1 = (int)((long)(I.split + 1) * kb_total / a.splits);
@@ -186,7 +199,32 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         // activation tile at the same time (an L2 hot spot); the accumulation
         // order stays fixed per tile (deterministic, batch invariant)
         const int rot = (I.tile * 7 + I.chunk * 3) % cnt;
-        for (int j = 0; j < cnt; ++j) {
+        int j0 = 0;
+        if (first) {
+          // Programmatic dependent launch: the weights do not depend on the
+          // previous kernel, so the first ring's worth of weight tiles is
+          // requested before waiting for it; activations only after.
+          first = false;
+          const int npre = min(cnt, STAGES);
+          for (int j = 0; j < npre; ++j) {
+            const int kb = kb0 + (j + rot) % cnt;
+            const uint32_t fb = full0 + 8 * j;
+            mbar_expect_tx(fb, A_BYTES + nbox * brow * BK * 2);
+            tma_load_2d(smem_u32(smem + j * STAGE_BYTES), &tmA, fb, kb * BK, I.tile * BM, pol_w);
+          }
+          pdl_wait();
+          for (int j = 0; j < npre; ++j) {
+            const int kb = kb0 + (j + rot) % cnt;
+            const uint32_t fb = full0 + 8 * j;
+            const uint32_t sa = smem_u32(smem + j * STAGE_BYTES);
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d(sa + A_BYTES + b * brow * BK * 2, tb, fb, kb * BK, n0 + brow * b, pol_x);
+          }
+          j0 = npre;
+          stage = npre % STAGES;
+          phase = npre == STAGES ? 1u : 0u;
+        }
+        for (int j = j0; j < cnt; ++j) {
           const int kb = kb0 + (j + rot) % cnt;
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
@@ -457,7 +495,8 @@ int gemm_pick_splits(int M, int K, int n_sms) {
 }
 
 void gemm_launch(const GemmPlan& p, const GemmArgs& a, int grid, cudaStream_t st) {
-  gemm_tcgen05_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(p.tmA, p.tmB16, p.tmB64, p.tmB256, a);
+  launch_pdl(gemm_tcgen05_kernel, dim3(grid), dim3(GEMM_THREADS), GEMM_SMEM, st, p.tmA, p.tmB16, p.tmB64, p.tmB256,
+             a);
 }
 
 int make_plan(GemmPlan* p, const void* W, int M, int K, const void* X, int rows_cap) {

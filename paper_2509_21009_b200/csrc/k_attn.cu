@@ -97,6 +97,8 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
   const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(bars);
   const uint32_t empty0 = full0 + 8 * AT_STAGES;
 
+  pdl_wait();
+  pdl_launch_dependents();
   const int n_items = n_items_dev ? *n_items_dev : n_items_host;
   const int n_units = n_items * m.KV;            // flat (item, KV head) work units
   const int g = m.H / m.KV;
@@ -392,13 +394,13 @@ void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_
                       int* tickets, const ModelDims& m, int layer, cudaStream_t st) {
   const int grid = 148;   // one wave, persistent over the flat (item, KV head) units
   if (m.hd == 128)
-    attn_kernel<128><<<grid, AT_THREADS, AttnCfg<128>::SMEM, st>>>(kv_map, (const __nv_bfloat16*)q, page_table, maxp,
-                                                                   items, n_items_dev, n_items_host,
-                                                                   (__nv_bfloat16*)out, partial, tickets, m, layer);
+    launch_pdl(attn_kernel<128>, dim3(grid), dim3(AT_THREADS), AttnCfg<128>::SMEM, st, kv_map,
+               (const __nv_bfloat16*)q, page_table, maxp, items, n_items_dev, n_items_host, (__nv_bfloat16*)out,
+               partial, tickets, m, layer);
   else
-    attn_kernel<64><<<grid, AT_THREADS, AttnCfg<64>::SMEM, st>>>(kv_map, (const __nv_bfloat16*)q, page_table, maxp,
-                                                                 items, n_items_dev, n_items_host,
-                                                                 (__nv_bfloat16*)out, partial, tickets, m, layer);
+    launch_pdl(attn_kernel<64>, dim3(grid), dim3(AT_THREADS), AttnCfg<64>::SMEM, st, kv_map,
+               (const __nv_bfloat16*)q, page_table, maxp, items, n_items_dev, n_items_host, (__nv_bfloat16*)out,
+               partial, tickets, m, layer);
 }
 
 }  // namespace rp

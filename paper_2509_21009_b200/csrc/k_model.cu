@@ -54,6 +54,8 @@ static inline int row_grid(const int* n_dev, int n_host) {
 // ------------------------------------------------------------------ embedding
 __global__ void embed_kernel(const int* tok, const int* n_dev, int n_host, const __nv_bfloat16* emb, float* x,
                              int d) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int n = n_dev ? *n_dev : n_host;
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
     const __nv_bfloat162* e = (const __nv_bfloat162*)(emb + (size_t)tok[r] * d);
@@ -63,7 +65,8 @@ __global__ void embed_kernel(const int* tok, const int* n_dev, int n_host, const
 }
 
 void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb, float* x, int d, cudaStream_t st) {
-  embed_kernel<<<row_grid(n_dev, n_host), 256, 0, st>>>(tok, n_dev, n_host, (const __nv_bfloat16*)emb, x, d);
+  launch_pdl(embed_kernel, dim3(row_grid(n_dev, n_host)), dim3(256), 0, st, tok, n_dev, n_host,
+             (const __nv_bfloat16*)emb, x, d);
 }
 
 // -------------------------------------------------------------------- RMSNorm
@@ -73,6 +76,8 @@ void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb,
 __global__ void rmsnorm_kernel(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
                                const float* gamma, __nv_bfloat16* h, int d, float eps) {
   __shared__ float red[32];
+  pdl_wait();
+  pdl_launch_dependents();
   const int n = n_dev ? *n_dev : n_host;
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
     const int src = gather ? gather[r] : r;
@@ -116,8 +121,8 @@ __global__ void rmsnorm_kernel(float* x, const float* delta, const int* gather, 
 
 void launch_rmsnorm(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
                     const float* gamma, void* h, int d, float eps, cudaStream_t st) {
-  rmsnorm_kernel<<<row_grid(n_dev, n_host), 256, 0, st>>>(x, delta, gather, n_dev, n_host, gamma, (__nv_bfloat16*)h,
-                                                          d, eps);
+  launch_pdl(rmsnorm_kernel, dim3(row_grid(n_dev, n_host)), dim3(256), 0, st, x, delta, gather, n_dev, n_host, gamma,
+             (__nv_bfloat16*)h, d, eps);
 }
 
 // -------------------------------------------------------- RoPE + KV append
@@ -128,6 +133,8 @@ __global__ void rope_append_kernel(const float* qkv, const int* n_dev, int n_hos
                                    const int* row_pt, const int* page_table, int maxp, __nv_bfloat16* q_out,
                                    uint8_t* kv_pool, ModelDims m, int layer, const double* inv_freq) {
   extern __shared__ float cs[];   // [hd/2] cos, [hd/2] sin
+  pdl_wait();
+  pdl_launch_dependents();
   const int n = n_dev ? *n_dev : n_host;
   const int half = m.hd / 2, W = (m.H + 2 * m.KV) * m.hd;
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
@@ -171,9 +178,8 @@ __global__ void rope_append_kernel(const float* qkv, const int* n_dev, int n_hos
 void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const int* row_pos, const int* row_pt,
                         const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
                         const double* inv_freq, cudaStream_t st) {
-  rope_append_kernel<<<row_grid(n_dev, n_host), 256, m.hd * sizeof(float), st>>>(qkv, n_dev, n_host, row_pos, row_pt, page_table,
-                                                                 maxp, (__nv_bfloat16*)q_out, (uint8_t*)kv_pool, m,
-                                                                 layer, inv_freq);
+  launch_pdl(rope_append_kernel, dim3(row_grid(n_dev, n_host)), dim3(256), m.hd * sizeof(float), st, qkv, n_dev,
+             n_host, row_pos, row_pt, page_table, maxp, (__nv_bfloat16*)q_out, (uint8_t*)kv_pool, m, layer, inv_freq);
 }
 
 // ------------------------------------------------------------- prompt fork

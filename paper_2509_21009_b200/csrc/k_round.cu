@@ -25,6 +25,8 @@ constexpr int SAMP_CHUNK = 4096;   // vocab entries per work unit
 __global__ void __launch_bounds__(256) sampler_kernel(const float* __restrict__ logits, int V, int v0, int row_div,
                                                        RoundDev R, uint32_t k0, uint32_t k1, float inv_temp,
                                                        uint32_t round_id) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int n = R.ctl->n_live;
   const int t = R.ctl->t;
   const int chunks = (V + SAMP_CHUNK - 1) / SAMP_CHUNK;
@@ -74,8 +76,8 @@ __global__ void __launch_bounds__(256) sampler_kernel(const float* __restrict__ 
 
 void launch_sampler(const float* logits, int V, int v0, int row_div, const RoundDev& R, uint64_t seed,
                     float inv_temp, uint32_t round_id, cudaStream_t st) {
-  sampler_kernel<<<148 * 4, 256, 0, st>>>(logits, V, v0, row_div, R, (uint32_t)seed, (uint32_t)(seed >> 32),
-                                          inv_temp, round_id);
+  launch_pdl(sampler_kernel, dim3(148 * 4), dim3(256), 0, st, logits, V, v0, row_div, R, (uint32_t)seed,
+             (uint32_t)(seed >> 32), inv_temp, round_id);
 }
 
 // --------------------------------------------------------------------- ctl
@@ -193,22 +195,27 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     R.accept_order[C->acc_local + r] = p;
   }
   const int top = C->free_top;
-  // Key-split size: about the step's total context x KV heads / 148 (one
-  // wave of work units), never below 512 tokens; short rows stay unsplit,
-  // long rows are split so no unit dominates the wave.
-  const long long per = (C->ctx_sum * R.kv_heads + 147) / 148;
-  const int chunk = (int)min((long long)(1 << 30), max((long long)kAttnChunk, (per + kPage - 1) / kPage * kPage));
+  // Key splits: the flat (item, KV head) work list should fill one wave of
+  // 148 CTAs with units of about equal size.  Row r gets
+  // ns_r = max(1, floor(ctx_r * U / sum ctx)) splits, U = 148 / KV (so
+  // sum ns_r <= U whenever no row is forced up to 1), each of
+  // ceil(ctx_r / ns_r) tokens rounded up to whole pages.
+  const long long ctx_total = max(1LL, C->ctx_sum);
+  const int U = max(1, 148 / R.kv_heads);
   int kept = 0, alloc = 0, items = 0;
   if (!s_err) {
     for (int base = 0; base < n; base += CTL_THREADS) {
       const int i = base + tid;
-      int keep = 0, need = 0, ns = 0, s = -1;
+      int keep = 0, need = 0, ns = 0, chunk = 0, s = -1;
       if (i < n) {
         s = R.live[i];
         keep = R.status[s] == ST_LIVE;
         if (keep) {
+          const int ctx = R.kv_len[s] + 1;
           need = (R.kv_len[s] % kPage) == 0;
-          ns = (R.kv_len[s] + chunk) / chunk;
+          const int want = (int)max(1LL, (long long)ctx * U / ctx_total);
+          chunk = ((ctx + want - 1) / want + kPage - 1) / kPage * kPage;   // whole pages per split
+          ns = (ctx + chunk - 1) / chunk;
         }
       }
       int tk, ta, ti;
@@ -261,6 +268,8 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
 
 __global__ void __launch_bounds__(CTL_THREADS) ctl_kernel(RoundDev R, int appended, int mode) {
   __shared__ int scan_sm[40];
+  pdl_wait();
+  pdl_launch_dependents();
   if (R.ctl->done) return;
   if (mode != 2) ctl_phase_a(R, appended, scan_sm);
   if (mode == 0) { __threadfence_block(); __syncthreads(); }
@@ -268,7 +277,7 @@ __global__ void __launch_bounds__(CTL_THREADS) ctl_kernel(RoundDev R, int append
 }
 
 void launch_ctl(const RoundDev& R, int appended, int mode, cudaStream_t st) {
-  ctl_kernel<<<1, CTL_THREADS, 0, st>>>(R, appended, mode);
+  launch_pdl(ctl_kernel, dim3(1), dim3(CTL_THREADS), 0, st, R, appended, mode);
 }
 
 // ------------------------------------------------------------ collect pack

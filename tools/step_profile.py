@@ -24,12 +24,20 @@ def main():
             st = eng.step(16)
         if st.done:
             break
+        import time
+        torch.cuda.synchronize()
+        n0, t0 = st.t, time.perf_counter()
+        st = eng.step(64)
+        torch.cuda.synchronize()
+        gms = (time.perf_counter() - t0) * 1e3 / max(1, st.t - n0)
+        if st.done:
+            break
         eng.debug_profile_arm(16)
         st = eng.step(16)
         p = eng.debug_profile_read()
         tot = sum(p["ms"].values())
-        print("B~%d rows/step=%.1f ctx/row=%.0f step_ms=%.3f" % (b, p["rows"] / p["steps"], p["ctx"] / max(1, p["rows"]),
-                                                                tot / p["steps"]))
+        print("B~%d rows/step=%.1f ctx/row=%.0f eager_step_ms=%.3f graph_step_ms=%.3f" % (
+            b, p["rows"] / p["steps"], p["ctx"] / max(1, p["rows"]), tot / p["steps"], gms))
         print("   " + "  ".join("%s=%.3f" % (k, v / p["steps"]) for k, v in p["ms"].items() if v > 0))
     eng.close()
 
