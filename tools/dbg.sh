@@ -1,2 +1,2 @@
-nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv
-for v in a b c a b c; do cp abtest/$v.so paper_2509_21009_b200/librollpacker.so; echo "== $v"; timeout -s KILL 200 python tools/gemm_bench.py lm gu 2>&1 | grep -E "auto" | grep -E "N= 16|N=256"; done
+timeout -s KILL 300 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
+timeout -s KILL 300 python tools/step_profile.py 256 128 32 16 2>&1 | grep -A1 B~

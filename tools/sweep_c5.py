@@ -45,8 +45,8 @@ def main():
         total = n_sub * (a.steps + 2) * 2
         ps = gen.prompts(total, 0, cfg["eos_id"], (256, 768), configs.PROMPT_SEED)
         tr = gen.length_trace(total, G, 6.0, 0.6, SIGMA_R.get(ratio, 0.85), 16384, configs.TRACE_SEED)
-        base = tr[:, 0, :].reshape(-1, 128 * 8)
-        meas = float(np.median([b.max() / np.median(b) for b in base[:max(1, len(base) // 2)]]))
+        big = gen.length_trace(128 * 40, G, 6.0, 0.6, SIGMA_R.get(ratio, 0.85), 16384, 99)[:, 0, :]
+        meas = float(np.median([b.max() / np.median(b) for b in big.reshape(-1, 128 * G)]))
         for mode in ("tail", "sync"):
             queue, nxt, times, toks, kinds = [], 0, [], 0, []
             for step in range(a.steps):
