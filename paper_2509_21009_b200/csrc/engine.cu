@@ -9,6 +9,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -394,7 +396,7 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
                          c->rd.kv_pool, m, l, c->inv_freq, c->st); c->launches++; }
     { ProfScope ps(c, RP_PROF_ATTN);
       launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
-                       c->apart, c->atickets, m, l, c->st); c->launches++; }
+                       c->apart, c->atickets, m, l, decode, c->st); c->launches++; }
     { ProfScope ps(c, RP_PROF_GEMM_O);
       gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
            nullptr); }
@@ -1103,6 +1105,30 @@ int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, flo
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   gemm(c, p, M, K, nullptr, N, splits, EPI_F32, Y, M, nullptr);   // warm
+  if (getenv("RP_GEMM_TIMELINE")) {   // debug: per-CTA phase timeline of one launch, to stderr
+    long long* tl = nullptr;
+    CK(cudaMalloc(&tl, kSMs * 16 * sizeof(long long)));
+    CK(cudaMemsetAsync(tl, 0, kSMs * 16 * sizeof(long long), c->st));
+    GemmArgs a{};
+    a.M = M; a.K = K; a.n_host = N; a.splits = splits; a.epi = EPI_F32; a.out = Y; a.ldo = M;
+    a.partial = c->gpart; a.counters = c->gctr; a.timeline = tl;
+    gemm_launch(p, a, kSMs, c->st);
+    std::vector<long long> h(kSMs * 16);
+    CK(cudaMemcpyAsync(h.data(), tl, h.size() * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    cudaFree(tl);
+    long long t0 = LLONG_MAX, tend = 0;
+    for (int b = 0; b < kSMs; ++b) if (h[b * 16]) t0 = std::min(t0, h[b * 16]);
+    double acc[16] = {0}; int cnt[16] = {0};
+    for (int b = 0; b < kSMs; ++b)
+      for (int k = 0; k < 16; ++k)
+        if (h[b * 16 + k]) { acc[k] += (h[b * 16 + k] - t0) / 1e3; cnt[k]++; tend = std::max(tend, h[b * 16 + k]); }
+    fprintf(stderr, "gemm timeline M=%d N=%d K=%d splits=%d (us from first CTA start, mean over CTAs):", M, N, K, splits);
+    const char* nm[16] = {"start", "setup", "it0_first", "it0_lastmma", "it1_first", "it1_lastmma", "it2_first",
+                          "it2_lastmma", "it0_epi", "it1_epi", "it2_epi", "", "", "", "", ""};
+    for (int k = 0; k < 11; ++k) if (cnt[k]) fprintf(stderr, " %s=%.2f(%d)", nm[k], acc[k] / cnt[k], cnt[k]);
+    fprintf(stderr, " end=%.2f\n", (tend - t0) / 1e3);
+  }
   CK(cudaEventRecord(e0, c->st));
   for (int i = 0; i < iters; ++i) gemm(c, p, M, K, nullptr, N, splits, EPI_F32, Y, M, nullptr);
   CK(cudaEventRecord(e1, c->st));

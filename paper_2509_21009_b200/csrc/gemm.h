@@ -18,6 +18,7 @@ struct GemmArgs {
   const float* bias;      // [M] or nullptr (EPI_F32 / EPI_BF16)
   float* partial;         // split-K partials (splits > 1)
   int* counters;          // split-K tickets, zero-initialised, self-resetting
+  long long* timeline;    // debug: per-CTA %globaltimer stamps [grid][16] (nullptr = off)
 };
 
 struct GemmPlan {

@@ -115,6 +115,15 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
 
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// debug timeline: [0] CTA start, [1] setup done, [2+2i] item i first stage ready,
+// [3+2i] item i last MMA issued (i < 3), [8+i] item i epilogue done (i < 3)
+#define TL(k) do { if (a.timeline) a.timeline[blockIdx.x * 16 + (k)] = gtimer(); } while (0)
+
 struct Item { int tile, chunk, split; };
 __device__ __forceinline__ Item decode_item(int it, int m_tiles, int splits) {
   Item r;
@@ -131,6 +140,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                     GemmArgs a) {
   const int N = a.n_dev ? *a.n_dev : a.n_host;
   if (N <= 0) return;
+  if (threadIdx.x == 0) TL(0);
   const int m_tiles = a.M / BM;
   const int n_chunks = (N + BN - 1) / BN;
   const int n_items = m_tiles * n_chunks * a.splits;
@@ -177,6 +187,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) TL(1);
   if (!(warp == 0 && lane == 0)) pdl_wait();   // the producer waits after its weight prefetch
   pdl_launch_dependents();
 
@@ -254,6 +265,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         const uint32_t tmem_d = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(full0 + 8 * stage, phase);
+          if (kb == kb0 && local < 3) TL(2 + 2 * local);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint64_t da = make_sdesc(sa), db = make_sdesc(sa + A_BYTES);
@@ -264,6 +276,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         umma_commit(tfull0 + 8 * acc);
+        if (local < 3) TL(3 + 2 * local);
       }
     }
   } else if (warp >= 4) {
@@ -430,6 +443,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         tc_fence_before();
         mbar_arrive(tempty0 + 8 * acc);     // all TMEM reads of this item done
       }
+      if (et == 0 && local < 3) TL(8 + local);
     }
   }
   tc_fence_before();

@@ -23,13 +23,9 @@
 
 namespace rp {
 
-constexpr int AT_CWARPS = 3;                  // consumer warps
-constexpr int AT_THREADS = (AT_CWARPS + 1) * 32;
-constexpr int AT_STAGES = 6;                  // multiple of AT_CWARPS: stage s is always consumed by
-                                              // warp s % AT_CWARPS, so every warp waits on each of its
-                                              // stages' uses in order (mbarrier parity only tells
-                                              // adjacent phases apart)
-static_assert(AT_STAGES % AT_CWARPS == 0, "stage ownership");
+constexpr int AT_STAGES = 6;   // 64-token stages.  Stage s is always consumed by warp s % CW (CW divides
+                               // AT_STAGES): mbarrier parity only tells adjacent phases apart, so every
+                               // waiter must consume its stage's uses in order.
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -45,6 +41,11 @@ __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b
       "{%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t movtrans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -67,13 +68,16 @@ __device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, uint
       : "memory");
 }
 
-template <int HD>
+template <int HD, int CW, int NQT>
 struct AttnCfg {
   static constexpr int HALVES = HD / 64;             // 128-byte column halves (TMA boxes) per row
   static constexpr int TILE_BYTES = kPage * HD * 2;  // K (or V) block of one page
   static constexpr int STAGE_BYTES = 2 * TILE_BYTES;
-  static constexpr int MERGE_FLOATS = AT_CWARPS * 16 * (HD + 2);
+  static constexpr int MR = 8 * NQT;                 // query rows per work unit (<= 8: decode, <= 16: prefill)
+  static constexpr int MERGE_FLOATS = CW * MR * (HD + 2);
+  static constexpr int THREADS = (CW + 1) * 32;
   static constexpr int SMEM = AT_STAGES * STAGE_BYTES + MERGE_FLOATS * 4 + 1024 + 256;
+  static_assert(AT_STAGES % CW == 0, "stage ownership");
 };
 
 // byte offset of (row, 16-byte chunk) in a [64][HD] tile stored as HD/64
@@ -82,13 +86,17 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   return (uint32_t)((chunk >> 3) * 8192 + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
 }
 
-template <int HD>
-__global__ void __launch_bounds__(AT_THREADS, 1)
+// S^T = K Q^T: the key tokens are the MMA rows (m16) and the <= 8 query rows
+// of a work unit are the n8 columns, so no MMA lane is padding; P^T reaches
+// the PV MMA through movmatrix.trans; O^T = V^T P^T keeps head_dim on the rows.
+template <int HD, int CW, int NQT>
+__global__ void __launch_bounds__((CW + 1) * 32, 1)
 attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __restrict__ q,
             const int* __restrict__ page_table, int maxp, const AttnItem* __restrict__ items, const int* n_items_dev,
             int n_items_host, __nv_bfloat16* __restrict__ out, float* __restrict__ partial, int* __restrict__ tickets,
             ModelDims m, int layer) {
-  using C = AttnCfg<HD>;
+  using C = AttnCfg<HD, CW, NQT>;
+  constexpr int MR = C::MR;
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
   float* mrg = (float*)(sm + AT_STAGES * C::STAGE_BYTES);
@@ -109,9 +117,8 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
-  const int row_stride_blk = kPage;   // rows per K|V block
 
-  if (warp == AT_CWARPS) {
+  if (warp == CW) {
     // ===================== producer warp =====================
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&kv_map) : "memory");
     long long gpage = 0;
@@ -132,7 +139,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
             mbar_wait_wd(empty0 + 8 * st, ph ^ 1, 100 + st, gp, (long long)it * 1000 + npg);
             const uint32_t fb = full0 + 8 * st;
             bar_expect_tx(fb, C::STAGE_BYTES);
-            const int row_k = (((page * m.L + layer) * m.KV + kvh) * 2 + 0) * row_stride_blk;
+            const int row_k = (((page * m.L + layer) * m.KV + kvh) * 2 + 0) * kPage;
             const uint32_t dst = sbase + st * C::STAGE_BYTES;
 #pragma unroll
             for (int h = 0; h < C::HALVES; ++h) {
@@ -149,138 +156,174 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
 
   // ===================== consumer warps =====================
   const float scale = 1.4426950408889634f * rsqrtf((float)HD);
-  const int ra = lane >> 2, rb = ra + 8;
+  const int tq = lane >> 2, tr = lane & 3;      // fragment row / column-pair coordinates
   long long gpage = 0;
   for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
     const int it = u / m.KV, kvh = u % m.KV;
     const AttnItem I = items[it];
     const int nrows = I.n_qtok * g;
     const int p_lo = I.kv_lo / kPage, npg = (I.kv_hi + kPage - 1) / kPage - p_lo;
-    // ---- Q fragments (A operand 16 x HD), rows r = tok*g + head
-    uint32_t qa[HD / 16][4];
-    {
-      const int c = 2 * (lane & 3);
-      const __nv_bfloat16* q0 = ra < nrows ? q + ((size_t)(I.q_row0 + ra / g) * m.H + kvh * g + ra % g) * HD : nullptr;
-      const __nv_bfloat16* q1 = rb < nrows ? q + ((size_t)(I.q_row0 + rb / g) * m.H + kvh * g + rb % g) * HD : nullptr;
+    // ---- Q^T B fragments: qb[nq][kk] = {Q[row][kk*16 + 2tr..], Q[row][kk*16 + 8 + 2tr..]}, row = nq*8 + tq
+    uint32_t qb[NQT][HD / 16][2];
+#pragma unroll
+    for (int nq = 0; nq < NQT; ++nq) {
+      const int r = nq * 8 + tq;
+      const __nv_bfloat16* qr =
+          r < nrows ? q + ((size_t)(I.q_row0 + r / g) * m.H + kvh * g + r % g) * HD : nullptr;
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
-        qa[kk][0] = q0 ? *(const uint32_t*)(q0 + kk * 16 + c) : 0u;
-        qa[kk][1] = q1 ? *(const uint32_t*)(q1 + kk * 16 + c) : 0u;
-        qa[kk][2] = q0 ? *(const uint32_t*)(q0 + kk * 16 + 8 + c) : 0u;
-        qa[kk][3] = q1 ? *(const uint32_t*)(q1 + kk * 16 + 8 + c) : 0u;
+        qb[nq][kk][0] = qr ? *(const uint32_t*)(qr + kk * 16 + 2 * tr) : 0u;
+        qb[nq][kk][1] = qr ? *(const uint32_t*)(qr + kk * 16 + 8 + 2 * tr) : 0u;
       }
     }
-    const int lim_a = ra < nrows ? I.pos0 + ra / g + 1 : 0;   // keys j < lim visible
-    const int lim_b = rb < nrows ? I.pos0 + rb / g + 1 : 0;
-    const int kv_hi = I.kv_hi;
-    float o[HD / 8][4];
+    // this thread's two query columns per n-tile: rows nq*8 + 2tr + e
+    int lim[NQT][2];
 #pragma unroll
-    for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-    float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+    for (int nq = 0; nq < NQT; ++nq)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = nq * 8 + 2 * tr + e;
+        lim[nq][e] = r < nrows ? I.pos0 + r / g + 1 : 0;   // keys j < lim visible
+      }
+    const int kv_hi = I.kv_hi;
+    float o[HD / 16][NQT][4];                    // O^T: rows = head dim, cols = query rows
+#pragma unroll
+    for (int i = 0; i < HD / 16; ++i)
+#pragma unroll
+      for (int nq = 0; nq < NQT; ++nq) o[i][nq][0] = o[i][nq][1] = o[i][nq][2] = o[i][nq][3] = 0.f;
+    float mrun[NQT][2], lrun[NQT][2];
+#pragma unroll
+    for (int nq = 0; nq < NQT; ++nq) { mrun[nq][0] = mrun[nq][1] = -INFINITY; lrun[nq][0] = lrun[nq][1] = 0.f; }
 
-    for (int j = (int)((warp - gpage % AT_CWARPS + AT_CWARPS) % AT_CWARPS); j < npg; j += AT_CWARPS) {
-      const long long gp = gpage + j;   // gp % AT_CWARPS == warp
+    for (int j = (int)((warp - gpage % CW + CW) % CW); j < npg; j += CW) {
+      const long long gp = gpage + j;   // gp % CW == warp
       const int st = (int)(gp % AT_STAGES);
       mbar_wait_wd(full0 + 8 * st, (uint32_t)((gp / AT_STAGES) & 1), 200 + st, gp, (long long)it * 1000 + npg);
       const uint32_t kt = sbase + st * C::STAGE_BYTES, vt = kt + C::TILE_BYTES;
       const int tok0 = (p_lo + j) * kPage;
-      // ---- S = Q K^T (16 x 64)
-      float s[8][4];
+      // ---- S^T = K Q^T (64 tokens x query rows): 4 token tiles of 16
+      float s[4][NQT][4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nq = 0; nq < NQT; ++nq) s[mt][nq][0] = s[mt][nq][1] = s[mt][nq][2] = s[mt][nq][3] = 0.f;
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
 #pragma unroll
-        for (int n2 = 0; n2 < 4; ++n2) {
-          const int row = n2 * 16 + (lane & 7) + ((lane >> 4) << 3);
-          const int ch = 2 * kk + ((lane >> 3) & 1);
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4(kt + swz(row, ch), b0, b1, b2, b3);
-          mma16816(s[2 * n2], qa[kk], b0, b1);
-          mma16816(s[2 * n2 + 1], qa[kk], b2, b3);
+        for (int mt = 0; mt < 4; ++mt) {
+          const int row = mt * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+          const int ch = 2 * kk + (lane >> 4);
+          uint32_t a[4];
+          ldsm_x4(kt + swz(row, ch), a[0], a[1], a[2], a[3]);
+#pragma unroll
+          for (int nq = 0; nq < NQT; ++nq) mma16816(s[mt][nq], a, qb[nq][kk][0], qb[nq][kk][1]);
         }
       }
-      // ---- mask + online softmax (log2 domain)
-      float mx_a = -INFINITY, mx_b = -INFINITY;
+      // ---- mask + online softmax per query column (log2 domain)
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
+      for (int nq = 0; nq < NQT; ++nq) {
+        float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int jtok = tok0 + mt * 16 + tq + 8 * h;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const bool v = jtok < kv_hi && jtok < lim[nq][e];
+              float& x = s[mt][nq][2 * h + e];
+              x = v ? x * scale : -INFINITY;
+              mx[e] = fmaxf(mx[e], x);
+            }
+          }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int jj = tok0 + nt * 8 + 2 * (lane & 3) + e;
-          const bool va = jj < kv_hi && jj < lim_a, vb = jj < kv_hi && jj < lim_b;
-          s[nt][e] = va ? s[nt][e] * scale : -INFINITY;
-          s[nt][2 + e] = vb ? s[nt][2 + e] * scale : -INFINITY;
-          mx_a = fmaxf(mx_a, s[nt][e]);
-          mx_b = fmaxf(mx_b, s[nt][2 + e]);
+          mx[e] = fmaxf(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], 4));
+          mx[e] = fmaxf(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], 8));
+          mx[e] = fmaxf(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], 16));
+          const float mn = fmaxf(mrun[nq][e], mx[e]);
+          const float base = mn == -INFINITY ? 0.f : mn;
+          const float al = exp2f(mrun[nq][e] - base);
+          mrun[nq][e] = mn;
+          float ps = 0.f;
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              float& x = s[mt][nq][2 * h + e];
+              x = exp2f(x - base);
+              ps += x;
+            }
+          lrun[nq][e] = lrun[nq][e] * al + ps;
+#pragma unroll
+          for (int i = 0; i < HD / 16; ++i) { o[i][nq][e] *= al; o[i][nq][2 + e] *= al; }
         }
-      mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 1));
-      mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 2));
-      mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 1));
-      mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 2));
-      const float mn_a = fmaxf(m_a, mx_a), mn_b = fmaxf(m_b, mx_b);
-      const float base_a = mn_a == -INFINITY ? 0.f : mn_a, base_b = mn_b == -INFINITY ? 0.f : mn_b;
-      const float al_a = exp2f(m_a - base_a), al_b = exp2f(m_b - base_b);
-      m_a = mn_a; m_b = mn_b;
-      float ps_a = 0.f, ps_b = 0.f;
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        s[nt][0] = exp2f(s[nt][0] - base_a); s[nt][1] = exp2f(s[nt][1] - base_a);
-        s[nt][2] = exp2f(s[nt][2] - base_b); s[nt][3] = exp2f(s[nt][3] - base_b);
-        ps_a += s[nt][0] + s[nt][1];
-        ps_b += s[nt][2] + s[nt][3];
       }
-      l_a = l_a * al_a + ps_a;
-      l_b = l_b * al_b + ps_b;
-#pragma unroll
-      for (int i = 0; i < HD / 8; ++i) { o[i][0] *= al_a; o[i][1] *= al_a; o[i][2] *= al_b; o[i][3] *= al_b; }
-      // ---- O += P V: 4 k-steps of 16 tokens
+      // ---- O^T += V^T P^T: 4 k-steps of 16 tokens
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
-        uint32_t pa[4];
-        pa[0] = pack_bf16(s[2 * ks][0], s[2 * ks][1]);
-        pa[1] = pack_bf16(s[2 * ks][2], s[2 * ks][3]);
-        pa[2] = pack_bf16(s[2 * ks + 1][0], s[2 * ks + 1][1]);
-        pa[3] = pack_bf16(s[2 * ks + 1][2], s[2 * ks + 1][3]);
-        const int row = ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+        uint32_t pb[NQT][2];
 #pragma unroll
-        for (int dt = 0; dt < HD / 8; dt += 2) {
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(vt + swz(row, dt + (lane >> 4)), b0, b1, b2, b3);
-          mma16816(o[dt], pa, b0, b1);
-          mma16816(o[dt + 1], pa, b2, b3);
+        for (int nq = 0; nq < NQT; ++nq) {
+          pb[nq][0] = movtrans(pack_bf16(s[ks][nq][0], s[ks][nq][1]));   // tokens 0-7 of the k-step
+          pb[nq][1] = movtrans(pack_bf16(s[ks][nq][2], s[ks][nq][3]));   // tokens 8-15
+        }
+        const int row = ks * 16 + (lane & 7) + ((lane >> 4) << 3);
+#pragma unroll
+        for (int mh = 0; mh < HD / 16; ++mh) {
+          uint32_t a[4];
+          ldsm_x4_t(vt + swz(row, 2 * mh + ((lane >> 3) & 1)), a[0], a[1], a[2], a[3]);
+#pragma unroll
+          for (int nq = 0; nq < NQT; ++nq) mma16816(o[mh][nq], a, pb[nq][0], pb[nq][1]);
         }
       }
       __syncwarp();
       if (lane == 0) bar_arrive(empty0 + 8 * st);   // stage free for the producer
     }
     gpage += npg;
-    // ---- merge the consumer warps' (m, l, O) in shared memory
-    l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
-    l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
-    l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
-    l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
-    float* wm = mrg + warp * 16 * (HD + 2);          // [16] m, [16] l, [16][HD] O
-    if ((lane & 3) == 0) { wm[ra] = m_a; wm[16 + ra] = l_a; wm[rb] = m_b; wm[16 + rb] = l_b; }
+    // ---- merge the consumer warps' (m, l, O) in shared memory: [MR] m, [MR] l, [MR][HD] O
 #pragma unroll
-    for (int i = 0; i < HD / 8; ++i) {
-      const int c = i * 8 + 2 * (lane & 3);
-      *(float2*)(wm + 32 + ra * HD + c) = make_float2(o[i][0], o[i][1]);
-      *(float2*)(wm + 32 + rb * HD + c) = make_float2(o[i][2], o[i][3]);
+    for (int nq = 0; nq < NQT; ++nq)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        lrun[nq][e] += __shfl_xor_sync(0xffffffffu, lrun[nq][e], 4);
+        lrun[nq][e] += __shfl_xor_sync(0xffffffffu, lrun[nq][e], 8);
+        lrun[nq][e] += __shfl_xor_sync(0xffffffffu, lrun[nq][e], 16);
+      }
+    float* wm = mrg + warp * MR * (HD + 2);
+    if (tq == 0) {
+#pragma unroll
+      for (int nq = 0; nq < NQT; ++nq)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          wm[nq * 8 + 2 * tr + e] = mrun[nq][e];
+          wm[MR + nq * 8 + 2 * tr + e] = lrun[nq][e];
+        }
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(AT_CWARPS * 32) : "memory");
-    for (int e = threadIdx.x; e < nrows * HD; e += AT_CWARPS * 32) {
+#pragma unroll
+    for (int mh = 0; mh < HD / 16; ++mh)
+#pragma unroll
+      for (int nq = 0; nq < NQT; ++nq)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = nq * 8 + 2 * tr + e;
+          wm[2 * MR + r * HD + mh * 16 + tq] = o[mh][nq][e];
+          wm[2 * MR + r * HD + mh * 16 + tq + 8] = o[mh][nq][2 + e];
+        }
+    asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
+    for (int e = threadIdx.x; e < nrows * HD; e += CW * 32) {
       const int r = e / HD, c = e % HD;
       float M = -INFINITY;
 #pragma unroll
-      for (int w = 0; w < AT_CWARPS; ++w) M = fmaxf(M, mrg[w * 16 * (HD + 2) + r]);
+      for (int w = 0; w < CW; ++w) M = fmaxf(M, mrg[w * MR * (HD + 2) + r]);
       const float Mb = M == -INFINITY ? 0.f : M;
       float L = 0.f, O = 0.f;
 #pragma unroll
-      for (int w = 0; w < AT_CWARPS; ++w) {
-        const float* ww = mrg + w * 16 * (HD + 2);
+      for (int w = 0; w < CW; ++w) {
+        const float* ww = mrg + w * MR * (HD + 2);
         const float f = exp2f(ww[r] - Mb);
-        L += ww[16 + r] * f;
-        O += ww[32 + r * HD + c] * f;
+        L += ww[MR + r] * f;
+        O += ww[2 * MR + r * HD + c] * f;
       }
       const int tok = I.q_row0 + r / g, head = kvh * g + r % g;
       if (I.nsplit == 1) {
@@ -296,22 +339,19 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
       // split order (deterministic); the ticket resets itself
       __shared__ int s_last;
       __threadfence();
-      asm volatile("bar.sync 1, %0;" ::"r"(AT_CWARPS * 32) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
       if (threadIdx.x == 0) {
         int* tk = tickets + (size_t)I.item0 * m.KV + kvh;
         const int old = atomicAdd(tk, 1);
         s_last = old == I.nsplit - 1;
         if (s_last) *tk = 0;
       }
-      asm volatile("bar.sync 1, %0;" ::"r"(AT_CWARPS * 32) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
       if (s_last) {
         __threadfence();
-        // per-row split weights w[r][s] = 2^(m_s - M) / L into smem (reuses the
-        // merge buffer), then O = sum_s w[r][s] * O_s with float4 loads of all
-        // splits in flight; fixed split order -> deterministic
         const float* __restrict__ p0 = partial + ((size_t)I.item0 * m.KV + kvh) * (16 * (HD + 2));
         const size_t sstride = (size_t)m.KV * 16 * (HD + 2);
-        float* wsm = mrg;                                  // [16][nsplit]
+        float* wsm = mrg;                                  // [16][nsplit] split weights
         const int ns = I.nsplit;
         if (threadIdx.x < nrows) {
           const int r = threadIdx.x;
@@ -327,21 +367,21 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
           const float inv = L > 0.f ? 1.f / L : 0.f;
           for (int sp = 0; sp < ns; ++sp) wsm[r * ns + sp] *= inv;
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(AT_CWARPS * 32) : "memory");
-        for (int e = threadIdx.x; e < nrows * (HD / 4); e += AT_CWARPS * 32) {
+        asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
+        for (int e = threadIdx.x; e < nrows * (HD / 4); e += CW * 32) {
           const int r = e / (HD / 4), c4 = (e % (HD / 4)) * 4;
           float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
           for (int s0 = 0; s0 < ns; s0 += 8) {
             float4 v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-              v[u] = s0 + u < ns ? __ldcg((const float4*)(p0 + (s0 + u) * sstride + 32 + r * HD + c4))
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int u8 = 0; u8 < 8; ++u8)
+              v[u8] = s0 + u8 < ns ? __ldcg((const float4*)(p0 + (s0 + u8) * sstride + 32 + r * HD + c4))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              if (s0 + u >= ns) break;
-              const float w = wsm[r * ns + s0 + u];
-              acc.x += w * v[u].x; acc.y += w * v[u].y; acc.z += w * v[u].z; acc.w += w * v[u].w;
+            for (int u8 = 0; u8 < 8; ++u8) {
+              if (s0 + u8 >= ns) break;
+              const float w = wsm[r * ns + s0 + u8];
+              acc.x += w * v[u8].x; acc.y += w * v[u8].y; acc.z += w * v[u8].z; acc.w += w * v[u8].w;
             }
           }
           const int tok = I.q_row0 + r / g, head = kvh * g + r % g;
@@ -351,18 +391,29 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
         }
       }
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(AT_CWARPS * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
   }
 }
 
-int attn_smem_bytes(int hd) { return hd == 128 ? AttnCfg<128>::SMEM : AttnCfg<64>::SMEM; }
+// decode: <= 8 query rows per unit (1 token x g heads): 6 consumer warps;
+// prefill: <= 16 rows (floor(16/g) tokens x g heads): 3 consumer warps (the
+// 16-row merge buffer leaves room for fewer).
+using AttnDec128 = AttnCfg<128, 6, 1>;
+using AttnPre128 = AttnCfg<128, 3, 2>;
+using AttnDec64 = AttnCfg<64, 6, 1>;
+using AttnPre64 = AttnCfg<64, 3, 2>;
+
+int attn_smem_bytes(int hd) { return hd == 128 ? AttnDec128::SMEM : AttnDec64::SMEM; }
 
 int attn_init_attrs() {
-  cudaError_t e1 = cudaFuncSetAttribute(attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        AttnCfg<128>::SMEM);
-  cudaError_t e2 = cudaFuncSetAttribute(attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        AttnCfg<64>::SMEM);
-  return (e1 == cudaSuccess && e2 == cudaSuccess) ? 0 : -1;
+  cudaError_t e[4] = {
+      cudaFuncSetAttribute(attn_kernel<128, 6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnDec128::SMEM),
+      cudaFuncSetAttribute(attn_kernel<128, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnPre128::SMEM),
+      cudaFuncSetAttribute(attn_kernel<64, 6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnDec64::SMEM),
+      cudaFuncSetAttribute(attn_kernel<64, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnPre64::SMEM)};
+  for (auto x : e)
+    if (x != cudaSuccess) return -1;
+  return 0;
 }
 
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -391,16 +442,25 @@ int make_kv_map(CUtensorMap* map, const void* pool, size_t n_pages, const ModelD
 
 void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_table, int maxp,
                       const AttnItem* items, const int* n_items_dev, int n_items_host, void* out, float* partial,
-                      int* tickets, const ModelDims& m, int layer, cudaStream_t st) {
-  const int grid = 148;   // one wave, persistent over the flat (item, KV head) units
-  if (m.hd == 128)
-    launch_pdl(attn_kernel<128>, dim3(grid), dim3(AT_THREADS), AttnCfg<128>::SMEM, st, kv_map,
-               (const __nv_bfloat16*)q, page_table, maxp, items, n_items_dev, n_items_host, (__nv_bfloat16*)out,
-               partial, tickets, m, layer);
-  else
-    launch_pdl(attn_kernel<64>, dim3(grid), dim3(AT_THREADS), AttnCfg<64>::SMEM, st, kv_map,
-               (const __nv_bfloat16*)q, page_table, maxp, items, n_items_dev, n_items_host, (__nv_bfloat16*)out,
-               partial, tickets, m, layer);
+                      int* tickets, const ModelDims& m, int layer, bool decode, cudaStream_t st) {
+  const dim3 grid(148);   // one wave, persistent over the flat (item, KV head) units
+  const auto* qq = (const __nv_bfloat16*)q;
+  auto* oo = (__nv_bfloat16*)out;
+  if (m.hd == 128) {
+    if (decode)
+      launch_pdl(attn_kernel<128, 6, 1>, grid, dim3(AttnDec128::THREADS), AttnDec128::SMEM, st, kv_map, qq,
+                 page_table, maxp, items, n_items_dev, n_items_host, oo, partial, tickets, m, layer);
+    else
+      launch_pdl(attn_kernel<128, 3, 2>, grid, dim3(AttnPre128::THREADS), AttnPre128::SMEM, st, kv_map, qq,
+                 page_table, maxp, items, n_items_dev, n_items_host, oo, partial, tickets, m, layer);
+  } else {
+    if (decode)
+      launch_pdl(attn_kernel<64, 6, 1>, grid, dim3(AttnDec64::THREADS), AttnDec64::SMEM, st, kv_map, qq, page_table,
+                 maxp, items, n_items_dev, n_items_host, oo, partial, tickets, m, layer);
+    else
+      launch_pdl(attn_kernel<64, 3, 2>, grid, dim3(AttnPre64::THREADS), AttnPre64::SMEM, st, kv_map, qq, page_table,
+                 maxp, items, n_items_dev, n_items_host, oo, partial, tickets, m, layer);
+  }
 }
 
 }  // namespace rp

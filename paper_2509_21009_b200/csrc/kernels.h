@@ -81,7 +81,7 @@ int make_kv_map(CUtensorMap* map, const void* pool, size_t n_pages, const ModelD
 void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_table, int maxp,
                       const AttnItem* items, const int* n_items_dev, int n_items_host, void* out, float* partial,
                       int* tickets /* [items x KV], zero, self-resetting */, const ModelDims& m, int layer,
-                      cudaStream_t st);
+                      bool decode /* <= 8 query rows per unit */, cudaStream_t st);
 void launch_kv_fork(const int* jobs /*[n][3] src,dst,rows*/, int n, void* kv_pool, const ModelDims& m,
                     cudaStream_t st);
 void launch_sampler(const float* logits, int V, int v0, int row_div, const RoundDev& R, uint64_t seed,

@@ -53,7 +53,7 @@ def main():
                 if mode == "sync":
                     ids = list(range(nxt, nxt + P0)); nxt += P0
                     L = tr[ids, 0, :]
-                    kind, target, long_round = "sync", P0, True
+                    kind, target, long_round = "baseline", P0, True
                 elif len(queue) >= P0:
                     ids, queue = queue[:P0], queue[P0:]
                     L = tr[ids, 1, :]
