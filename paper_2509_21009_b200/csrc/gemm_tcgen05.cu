@@ -32,7 +32,9 @@ constexpr int B_BYTES = BN * BK * 2;         // 32 KB (widest activation tile)
 constexpr int RING_BYTES = 4 * (A_BYTES + B_BYTES);   // 192 KB of stages
 constexpr int MAX_STAGES = 12;               // ring depth at small N (18 KB stages)
 constexpr int XCH_BYTES = 64 * 33 * 4;       // swiglu exchange
-constexpr int GEMM_SMEM = RING_BYTES + XCH_BYTES + 1024 /*align*/ + 8 * (2 * MAX_STAGES + 4) + 16;
+constexpr int TS = BM + 4;                   // fp32 row stride of the epilogue staging tile
+constexpr int STG_BYTES = 32 * TS * 4;       // [32 columns][128 rows] fp32 staging for 16-byte stores
+constexpr int GEMM_SMEM = RING_BYTES + XCH_BYTES + STG_BYTES + 1024 /*align*/ + 8 * (2 * MAX_STAGES + 4) + 16;
 constexpr int GEMM_THREADS = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -159,7 +161,8 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   float* xch = (float*)(smem + RING_BYTES);
-  uint64_t* bars = (uint64_t*)(smem + RING_BYTES + XCH_BYTES);
+  float* stg = (float*)(smem + RING_BYTES + XCH_BYTES);
+  uint64_t* bars = (uint64_t*)(smem + RING_BYTES + XCH_BYTES + STG_BYTES);
   // bars: full[MAX_STAGES], empty[MAX_STAGES], tfull[2], tempty[2]; then tmem slot, ticket
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * MAX_STAGES + 4);
   int* ticket = (int*)(tmem_slot + 1);
@@ -404,8 +407,12 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         }
+        // Output goes through a shared-memory transpose so each thread writes
+        // 16-byte vectors of consecutive features (a row-owning thread would
+        // otherwise issue 32 scalar stores per chunk).
         if (a.epi == EPI_SWIGLU) {
           // rows 64..127 (quarters 2,3) hold `up`, rows 0..63 hold `gate`
+          __nv_bfloat16* st2 = (__nv_bfloat16*)stg;           // [32 columns][72] bf16
           named_bar(2, 128);
           if (q >= 2) {
 #pragma unroll
@@ -413,31 +420,42 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           }
           named_bar(2, 128);
           if (q < 2) {
-            const int f = I.tile * 64 + row;
-            __nv_bfloat16* __restrict__ o = (__nv_bfloat16*)a.out + (size_t)(n0 + c0) * a.ldo + f;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c0 + j < nc) o[(size_t)j * a.ldo] = __float2bfloat16(silu_f(v[j]) * xch[row * 33 + j]);
+            for (int j = 0; j < 32; ++j) st2[j * 72 + row] = __float2bfloat16(silu_f(v[j]) * xch[row * 33 + j]);
           }
-        } else if (a.epi == EPI_RESID) {
-          float* __restrict__ o = (float*)a.out + (size_t)(n0 + c0) * a.ldo + m;
-          float old[32];
+          named_bar(2, 128);
+          const int f0 = I.tile * 64;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) old[j] = (c0 + j < nc) ? o[(size_t)j * a.ldo] : 0.f;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < nc) o[(size_t)j * a.ldo] = old[j] + v[j];
-        } else if (a.epi == EPI_F32) {
-          float* __restrict__ o = (float*)a.out + (size_t)(n0 + c0) * a.ldo + m;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < nc) o[(size_t)j * a.ldo] = v[j] + bias;
+          for (int i = 0; i < 2; ++i) {
+            const int idx = et + 128 * i, n = idx >> 3, f8 = (idx & 7) * 8;
+            if (c0 + n < nc)
+              *(uint4*)((__nv_bfloat16*)a.out + (size_t)(n0 + c0 + n) * a.ldo + f0 + f8) = *(const uint4*)(st2 + n * 72 + f8);
+          }
         } else {
-          __nv_bfloat16* __restrict__ o = (__nv_bfloat16*)a.out + (size_t)(n0 + c0) * a.ldo + m;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < nc) o[(size_t)j * a.ldo] = __float2bfloat16(v[j] + bias);
+          for (int j = 0; j < 32; ++j) stg[j * TS + row] = v[j] + bias;
+          named_bar(2, 128);
+          const int mt0 = I.tile * BM;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int idx = et + 128 * i, n = idx >> 5, m4 = (idx & 31) * 4;
+            if (c0 + n >= nc) continue;
+            float4 val = *(const float4*)(stg + n * TS + m4);
+            const size_t o = (size_t)(n0 + c0 + n) * a.ldo + mt0 + m4;
+            if (a.epi == EPI_RESID) {
+              const float4 old = *(const float4*)((float*)a.out + o);
+              val.x += old.x; val.y += old.y; val.z += old.z; val.w += old.w;
+              *(float4*)((float*)a.out + o) = val;
+            } else if (a.epi == EPI_F32) {
+              *(float4*)((float*)a.out + o) = val;
+            } else {
+              __nv_bfloat162* ob = (__nv_bfloat162*)((__nv_bfloat16*)a.out + o);
+              ob[0] = __floats2bfloat162_rn(val.x, val.y);
+              ob[1] = __floats2bfloat162_rn(val.z, val.w);
+            }
+          }
         }
+        named_bar(2, 128);                   // staging reused by the next chunk
       }
       if (!split) {
         tc_fence_before();
