@@ -148,6 +148,9 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int n_items = m_tiles * n_chunks * a.splits;
   if ((int)blockIdx.x >= n_items) return;
   const int kb_total = a.K / BK;
+  // cooperative split-K reduction: grid fits one wave and the chunk is wide
+  // enough that a single CTA reducing the whole tile would be the bottleneck
+  const bool coop = a.splits > 1 && n_items <= (int)gridDim.x && min(BN, N) >= 96;
 
   // Ring geometry from the widest activation chunk: 16/64/256-row boxes; at
   // small N the stages shrink and the ring deepens (more weight bytes in
@@ -299,31 +302,64 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(32 * q) << 16);
       const bool split = a.splits > 1;
       if (split) {
-        // fp32 partials: part[((tile*n_chunks+chunk)*splits+split)][col][row]
+        // fp32 partials: part[((tile*n_chunks+chunk)*splits+split)][col][row],
+        // staged through shared memory so every thread writes float4s
         float* part = a.partial + ((size_t)((I.chunk * m_tiles + I.tile) * a.splits + I.split)) * BN * BM;
         for (int c0 = 0; c0 < nc; c0 += 32) {
           uint32_t r[32];
           TMEM_LD32(tbase + c0, r);
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < nc) part[(c0 + j) * BM + row] = __uint_as_float(r[j]);
+          for (int j = 0; j < 32; ++j) stg[j * TS + row] = __uint_as_float(r[j]);
+          named_bar(2, 128);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int idx = et + 128 * i, n = idx >> 5, m4 = (idx & 31) * 4;
+            if (c0 + n < nc) __stcg((float4*)(part + (size_t)(c0 + n) * BM + m4), *(const float4*)(stg + n * TS + m4));
+          }
+          named_bar(2, 128);
         }
       }
       bool last = true;
+      int col_lo = 0, col_hi = nc;
+      if (split && et == 0 && local == 0) TL(11);   // partials written
       if (split) {
         tc_fence_before();
         mbar_arrive(tempty0 + 8 * acc);     // TMEM stage free for the next item
         __threadfence();
         named_bar(1, 128);
-        if (et == 0) {
-          int* ctr = a.counters + I.chunk * m_tiles + I.tile;
-          int old = atomicAdd(ctr, 1);
-          *ticket = (old == a.splits - 1);
-          if (old == a.splits - 1) *ctr = 0;
+        int* ctr = a.counters + I.chunk * m_tiles + I.tile;
+        if (coop) {
+          // One wave (every CTA of the grid is resident, so waiting on the
+          // other splits cannot deadlock): all split CTAs of the tile wait for
+          // its partials, then each reduces its own 1/splits of the columns
+          // (in split order: deterministic).  The last to finish resets.
+          if (et == 0) {
+            atomicAdd(ctr, 1);
+            uint32_t spins = 0;
+            while (atomicAdd(ctr, 0) < a.splits) {
+              __nanosleep(64);
+              if (++spins == (1u << 24)) {
+                printf("rollpacker watchdog: split-K wait stuck (block %d)\n", blockIdx.x);
+                __trap();
+              }
+            }
+          }
+          named_bar(1, 128);
+          __threadfence();
+          const int per = ((nc + a.splits - 1) / a.splits + 3) & ~3;
+          col_lo = min(nc, I.split * per);
+          col_hi = min(nc, col_lo + per);
+        } else {
+          if (et == 0) {
+            int old = atomicAdd(ctr, 1);
+            *ticket = (old == a.splits - 1);
+            if (old == a.splits - 1) *ctr = 0;
+          }
+          named_bar(1, 128);
+          last = *ticket != 0;
+          __threadfence();
         }
-        named_bar(1, 128);
-        last = *ticket != 0;
-        __threadfence();
+        if (et == 0 && local == 0) TL(12);        // ticket taken
       }
       if (!last) continue;
       if (split && a.epi != EPI_SWIGLU) {
@@ -334,7 +370,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         const float* __restrict__ pb = a.partial + ((size_t)((I.chunk * m_tiles + I.tile) * a.splits)) * BN * BM;
         const int r4 = (et & 31) * 4;              // rows r4..r4+3 of the tile
         const int m4 = I.tile * BM + r4;
-        for (int cb = (et >> 5); cb < nc; cb += 4 * 8) {
+        for (int cb = col_lo + (et >> 5); cb < col_hi; cb += 4 * 8) {
           float4 acc[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -343,8 +379,8 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               const int col = cb + 4 * u;
-              t[u] = col < nc ? __ldcg((const float4*)(pb + (size_t)s * BN * BM + (size_t)col * BM + r4))
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
+              t[u] = col < col_hi ? __ldcg((const float4*)(pb + (size_t)s * BN * BM + (size_t)col * BM + r4))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -356,7 +392,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               const int col = cb + 4 * u;
-              if (col < nc) old[u] = *(const float4*)((float*)a.out + (size_t)(n0 + col) * a.ldo + m4);
+              if (col < col_hi) old[u] = *(const float4*)((float*)a.out + (size_t)(n0 + col) * a.ldo + m4);
             }
           }
           float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -364,7 +400,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int col = cb + 4 * u;
-            if (col >= nc) continue;
+            if (col >= col_hi) continue;
             const size_t o = (size_t)(n0 + col) * a.ldo + m4;
             float4 v = acc[u];
             if (a.epi == EPI_RESID) {
@@ -378,6 +414,17 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               ob[0] = __floats2bfloat162_rn(v.x + bb.x, v.y + bb.y);
               ob[1] = __floats2bfloat162_rn(v.z + bb.z, v.w + bb.w);
             }
+          }
+        }
+        if (et == 0 && local == 0) TL(13);        // reduction + epilogue done
+        if (coop) {
+          // second counter: the last split CTA of the tile to finish resets both
+          __threadfence();
+          named_bar(1, 128);
+          if (et == 0) {
+            int* ctr = a.counters + I.chunk * m_tiles + I.tile;
+            int* done = a.counters + 32768 + I.chunk * m_tiles + I.tile;
+            if (atomicAdd(done, 1) == a.splits - 1) { *done = 0; atomicExch(ctr, 0); }
           }
         }
         continue;
