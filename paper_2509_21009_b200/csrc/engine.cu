@@ -90,6 +90,7 @@ struct RpCtx {
   int* gctr = nullptr;
   int* atickets = nullptr;
   double* inv_freq = nullptr;
+  float2* rope_cs = nullptr;    // [pos][hd/2] (cos, sin) of pos * theta^(-2i/hd), from fp64
   AttnItem *items_pre = nullptr;
   int *pre_tok = nullptr, *pre_pos = nullptr, *pre_pt = nullptr, *pre_last = nullptr, *fork_jobs = nullptr;
   int *col_meta = nullptr, *col_tok = nullptr;
@@ -245,6 +246,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto apart = cv.take<float>(z.apart_floats);
   auto atick = cv.take<int>((size_t)std::max(z.max_items_dec, z.max_items_pre) * KV);
   auto invf = cv.take<double>(hd / 2);
+  auto rope_cs = cv.take<float2>((size_t)(rd->max_prompt_len + rd->max_cap + 2) * (hd / 2));
   auto items_dec = cv.take<AttnItem>(z.max_items_dec);
   auto items_pre = cv.take<AttnItem>(z.max_items_pre);
   auto pre_tok = cv.take<int>(rd->max_prompt_tokens);
@@ -285,6 +287,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   if (c) {
     c->x = x; c->ar = ar; c->h = h; c->qkv = qkv; c->q = q; c->att = att; c->mid = mid; c->logits = logits;
     c->gpart = gpart; c->gctr = gctr; c->apart = apart; c->atickets = atick; c->inv_freq = invf;
+    c->rope_cs = rope_cs;
     c->items_pre = items_pre; c->pre_tok = pre_tok; c->pre_pos = pre_pos; c->pre_pt = pre_pt;
     c->pre_last = pre_last; c->fork_jobs = fork_jobs; c->col_meta = col_meta; c->col_tok = col_tok;
     c->identity_pages = ident;
@@ -355,8 +358,9 @@ struct ProfScope {
   }
 };
 static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, int n_host, int splits, int epi,
-                 void* out, int ldo, const float* bias) {
+                 void* out, int ldo, const float* bias, const RopeArgs* rope = nullptr) {
   GemmArgs a{};
+  if (rope) a.rope = *rope;
   a.M = M; a.K = K; a.n_dev = n_dev; a.n_host = n_host; a.splits = splits; a.epi = epi; a.out = out; a.ldo = ldo;
   a.bias = bias; a.partial = c->gpart; a.counters = c->gctr;
   gemm_launch(p, a, kSMs, c->st);
@@ -389,11 +393,19 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
     LayerW& w = c->layers[l];
     { ProfScope ps(c, RP_PROF_RMSNORM);
       launch_rmsnorm(c->x, delta, nullptr, n_dev, n_host, w.ln1, c->h, m.d, m.eps, c->st); c->launches++; }
-    { ProfScope ps(c, RP_PROF_GEMM_QKV);
-      gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_F32, c->qkv, qkvw, w.bqkv); }
-    { ProfScope ps(c, RP_PROF_ROPE);
-      launch_rope_append(c->qkv, n_dev, n_host, row_pos, row_pt, c->R.page_table, c->R.maxp, c->q,
-                         c->rd.kv_pool, m, l, c->inv_freq, c->st); c->launches++; }
+    if (decode && sp_qkv > 1 && m.hd % 64 == 0) {
+      // RoPE + KV append fused into the split-K reduction of the QKV GEMM
+      ProfScope ps(c, RP_PROF_GEMM_QKV);
+      RopeArgs ra{c->q, (uint8_t*)c->rd.kv_pool, c->R.page_table, row_pos, row_pt, c->rope_cs, m.page_bytes,
+                  c->R.maxp, l, m.H, m.KV, m.hd};
+      gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_QKV_ROPE, c->qkv, qkvw, w.bqkv, &ra);
+    } else {
+      { ProfScope ps(c, RP_PROF_GEMM_QKV);
+        gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_F32, c->qkv, qkvw, w.bqkv); }
+      { ProfScope ps(c, RP_PROF_ROPE);
+        launch_rope_append(c->qkv, n_dev, n_host, row_pos, row_pt, c->R.page_table, c->R.maxp, c->q,
+                           c->rd.kv_pool, m, l, c->inv_freq, c->st); c->launches++; }
+    }
     { ProfScope ps(c, RP_PROF_ATTN);
       launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
                        c->apart, c->atickets, m, l, decode, c->st); c->launches++; }
@@ -596,6 +608,17 @@ static int init_impl(RpCtx* c) {
   std::vector<double> invf(hd / 2);
   for (size_t i = 0; i < hd / 2; ++i) invf[i] = std::pow((double)md->rope_theta, -2.0 * (double)i / (double)hd);
   CK(cudaMemcpyAsync(c->inv_freq, invf.data(), invf.size() * 8, cudaMemcpyHostToDevice, c->st));
+  {
+    const size_t npos = (size_t)rd->max_prompt_len + rd->max_cap + 2;
+    std::vector<float2> cs(npos * (hd / 2));
+    for (size_t p = 0; p < npos; ++p)
+      for (size_t i = 0; i < hd / 2; ++i) {
+        const double ang = std::fmod((double)p * invf[i], 6.283185307179586);
+        cs[p * (hd / 2) + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+      }
+    CK(cudaMemcpyAsync(c->rope_cs, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
 
   // ---- TMA descriptors
   const int Tcap = c->z.Tcap;

@@ -2,10 +2,25 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
 
 namespace rp {
 
-enum GemmEpi { EPI_F32 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_BF16 = 3 };
+enum GemmEpi { EPI_F32 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_BF16 = 3, EPI_QKV_ROPE = 4 };
+
+// Fused QKV epilogue (decode, split-K path): bias, rotate-half RoPE from a
+// per-position cos/sin table, q -> q_out bf16 [n][H][hd], k/v -> KV page.
+struct RopeArgs {
+  __nv_bfloat16* q_out;
+  uint8_t* kv_pool;
+  const int* page_table;
+  const int* row_pos;
+  const int* row_pt;
+  const float2* cs;       // [pos][hd/2] (cos, sin)
+  size_t page_bytes;
+  int maxp, layer, H, KV, hd;
+};
 
 struct GemmArgs {
   int M, K;               // weight rows (multiple of 128), reduction dim (multiple of 64)
@@ -19,6 +34,7 @@ struct GemmArgs {
   float* partial;         // split-K partials (splits > 1)
   int* counters;          // split-K tickets, zero-initialised, self-resetting
   long long* timeline;    // debug: per-CTA %globaltimer stamps [grid][16] (nullptr = off)
+  RopeArgs rope;          // EPI_QKV_ROPE only
 };
 
 struct GemmPlan {

@@ -387,6 +387,56 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               acc[u].x += t[u].x; acc[u].y += t[u].y; acc[u].z += t[u].z; acc[u].w += t[u].w;
             }
           }
+          if (a.epi == EPI_QKV_ROPE) {
+            // rows r4..r4+3 of head-dim index i0 = (m4 % hd); the rotate-half
+            // partner rows (i +- hd/2) live in lane ^ (hd/8) of this warp
+            const RopeArgs& R = a.rope;
+            const int hd = R.hd, half = hd >> 1;
+            const int head = m4 / hd, i0 = m4 % hd;
+            const bool is_q = head < R.H, is_v = head >= R.H + R.KV;
+            const bool lo = i0 < half;
+            const float4 bb = a.bias ? *(const float4*)(a.bias + m4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              float4 v = acc[u];
+              v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
+              float4 p;
+              p.x = __shfl_xor_sync(0xffffffffu, v.x, hd >> 3);
+              p.y = __shfl_xor_sync(0xffffffffu, v.y, hd >> 3);
+              p.z = __shfl_xor_sync(0xffffffffu, v.z, hd >> 3);
+              p.w = __shfl_xor_sync(0xffffffffu, v.w, hd >> 3);
+              const int col = cb + 4 * u;
+              if (col >= col_hi) continue;
+              const int n = n0 + col;
+              const int pos = R.row_pos[n];
+              float4 o = v;
+              if (!is_v) {
+                const float2* cs = R.cs + (size_t)pos * half + (lo ? i0 : i0 - half);
+                const float4 c01 = *(const float4*)cs, c23 = *(const float4*)(cs + 2);   // (c,s) x 4
+                const float sg = lo ? -1.f : 1.f;    // lo: x c - x' s ; hi: x c + x' s
+                o.x = v.x * c01.x + sg * p.x * c01.y;
+                o.y = v.y * c01.z + sg * p.y * c01.w;
+                o.z = v.z * c23.x + sg * p.z * c23.y;
+                o.w = v.w * c23.z + sg * p.w * c23.w;
+              }
+              __nv_bfloat162 o01 = __floats2bfloat162_rn(o.x, o.y), o23 = __floats2bfloat162_rn(o.z, o.w);
+              uint2 packed;
+              packed.x = *(uint32_t*)&o01;
+              packed.y = *(uint32_t*)&o23;
+              __nv_bfloat16* dst;
+              if (is_q) {
+                dst = R.q_out + ((size_t)n * R.H + head) * hd + i0;
+              } else {
+                const int kh = is_v ? head - R.H - R.KV : head - R.H;
+                const int page = R.page_table[(size_t)R.row_pt[n] * R.maxp + pos / kPage];
+                dst = (__nv_bfloat16*)(R.kv_pool + (size_t)page * R.page_bytes +
+                                       ((size_t)((R.layer * R.KV + kh) * 2 + (is_v ? 1 : 0)) * kPage + pos % kPage) *
+                                           hd * 2) + i0;
+              }
+              *(uint2*)dst = packed;
+            }
+            continue;
+          }
           float4 old[8];
           if (a.epi == EPI_RESID) {
 #pragma unroll

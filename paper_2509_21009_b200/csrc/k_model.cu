@@ -1,5 +1,6 @@
 // Model-side elementwise kernels: weight formula (Z12), embedding
 // gather, RMSNorm, RoPE + paged-KV append, prompt-page fork (K6-K8).
+#include <algorithm>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -71,8 +72,9 @@ void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb,
 
 // -------------------------------------------------------------------- RMSNorm
 // h[r] = bf16( x[src] / sqrt(mean(x[src]^2) + eps) * gamma ),  src = gather ? gather[r] : r
-// With `delta` (tensor parallelism): x[r] += delta[r] first (the all-reduced
-// partial of a row-parallel GEMM) and the updated row is written back.
+// One CTA (256 threads) per row.  With `delta` (tensor parallelism):
+// x[r] += delta[r] first (the all-reduced partial of a row-parallel GEMM) and
+// the updated row is written back.
 __global__ void rmsnorm_kernel(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
                                const float* gamma, __nv_bfloat16* h, int d, float eps) {
   __shared__ float red[32];
