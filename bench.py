@@ -304,6 +304,22 @@ def load_peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the newest committed ncu --set full summary (profiles/rNN_ncu_traffic.json,
+    written by tools/make_profiles.py from a capture of the same decode step)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json")))
+    if not files:
+        return None, None
+    d = json.load(open(files[-1]))
+    for tag, ent in d.items():
+        if "256" in tag and kernel in ent["dram_bytes_per_launch"]:
+            return int(ent["dram_bytes_per_launch"][kernel]), "%s [%s] %s" % (
+                os.path.relpath(files[-1], ROOT), tag, ent["shape"])
+    return None, None
+
+
 def roofline(prof, cfg):
     """Dominant kernel class of the profiled decode steps and its roofline.
     Algorithmic bytes per launch:
@@ -354,7 +370,9 @@ def roofline(prof, cfg):
             roof = {"bound": "hbm", "achieved": round(by, 1), "peak": hbm, "unit": "GB/s", "frac": round(by / hbm, 4)}
     else:
         roof = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None}
-    roof.update({"kernel": dom, "traffic": None, "peak_source": src, "share_of_step": round(ms[dom] / total, 4),
+    traffic, traffic_src = ncu_traffic(dom)
+    roof.update({"kernel": dom, "traffic": traffic, "traffic_source": traffic_src, "peak_source": src,
+                 "share_of_step": round(ms[dom] / total, 4),
                  "mean_live_rows": round(B, 1), "mean_ctx_per_row": round(ctx / max(B, 1), 1),
                  "measured": "CUDA events around each launch of %d eager decode steps (first warm-up round)" % steps})
     return roof, detail
