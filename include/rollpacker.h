@@ -149,14 +149,21 @@ int rp_init_model(const rp_model_desc* md, const rp_runtime_desc* rd, void** out
 /* Start a round.  prompts: the FULL
  * prompt list of the round (every rank passes the same list); NULL pops
  * n_prompts entries from this context's long-prompt queue (single rank).
- * G: responses per prompt (R0).  cap: length cap of every response (>= 1).
+ * G: responses launched per prompt.  keep: responses retained per prompt
+ * (R0), 1 <= keep <= G, or 0 for keep = G.  keep < G is response-level
+ * speculation ("each prompt produces more than R0
+ * responses, finishing after the first R0 complete"): a prompt completes at
+ * the step its keep-th response emits EOS (ties at that step go to the lower
+ * j), its other responses are aborted at once, and only the keep finished
+ * ones are collected.  RP_LONG requires keep == G (speculation disabled,
+ * P:124).  cap: length cap of every response (>= 1).
  * target: prompts to accept (P0), 1 <= target <= n_prompts; RP_LONG requires
  * target == n_prompts.  flags: RP_SHORT|RP_LONG [|RP_TRACE].  round_id seeds
  * the sampler counter (reading Z5: re-rolls draw fresh noise).  Runs the
  * prefill and decode step 1 (the token sampled from the prefill logits).
  * Errors: RP_EINVAL, RP_EBUSY (round active), RP_ENOMEM_KV, RP_ENOSPC. */
-int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n_prompts, int32_t G, int32_t cap, int32_t target,
-                    int32_t flags, int64_t round_id);
+int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n_prompts, int32_t G, int32_t keep, int32_t cap,
+                    int32_t target, int32_t flags, int64_t round_id);
 
 /* Run up to max_steps decode steps (or until the round is done) and report
  * the status.  Each step: embed -> L x (RMSNorm, QKV, RoPE+KV append,

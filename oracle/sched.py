@@ -46,20 +46,45 @@ def _e(L, cap):
     return np.minimum(np.asarray(L, np.int64), cap)
 
 
-def closed_form(L, cap, target, kind, with_steps=False):
-    """The schedule written out directly from the definition.
-
-    SHORT: T_i = max_j L_ij if every L_ij <= cap else inf; pi = prompts sorted
-    by (T_i, i); A = first min(target, #finite) of pi; t_end = T_pi[target-1]
-    if #finite >= target else max_s e_s.  LONG: every prompt accepted, in
-    (max_j e_ij, i) order; t_end = max e."""
+def _kept(L, cap, keep):
+    """Response-level speculation: the first `keep` of
+    a prompt's responses to finish (EOS within the cap) are retained; ties at
+    the same step go to the lower response index j.  Returns the boolean mask
+    and T_i = the step of the keep-th finish (inf if fewer finish)."""
     L = np.asarray(L, np.int64)
     n, G = L.shape
+    kept = np.zeros((n, G), bool)
+    T = np.full(n, np.iinfo(np.int64).max)
+    for i in range(n):
+        fin = [(L[i, j], j) for j in range(G) if L[i, j] <= cap]
+        fin.sort()
+        if len(fin) >= keep:
+            for _, j in fin[:keep]:
+                kept[i, j] = True
+            T[i] = fin[keep - 1][0]
+    return kept, T
+
+
+def closed_form(L, cap, target, kind, with_steps=False, keep=None):
+    """The schedule written out directly from the definition.
+
+    SHORT: T_i = the keep-th smallest finished length of prompt i (keep = G:
+    max_j L_ij if every L_ij <= cap), inf if fewer than keep finish within the
+    cap; pi = prompts sorted by (T_i, i); A = first min(target, #finite) of
+    pi; t_end = T_pi[target-1] if #finite >= target else the last step any
+    sequence is live.  With keep < G a prompt's remaining siblings are aborted
+    right after step T_i.  LONG (no speculation, keep = G): every prompt
+    accepted, in (max_j e_ij, i) order; t_end = max e."""
+    L = np.asarray(L, np.int64)
+    n, G = L.shape
+    keep = G if keep is None else keep
     e = _e(L, cap)
     if kind == SHORT:
-        ok = np.all(L <= cap, axis=1)
-        T = np.where(ok, L.max(axis=1), np.iinfo(np.int64).max)
+        kept, T = _kept(L, cap, keep)
+        # a sequence stops at its own end or when its prompt completes
+        e = np.minimum(e, np.minimum(T, np.iinfo(np.int64).max)[:, None])
     else:
+        kept = np.ones((n, G), bool)
         T = e.max(axis=1)
     order = sorted(range(n), key=lambda i: (T[i], i))
     n_fin = int(np.sum(T < np.iinfo(np.int64).max))
@@ -70,24 +95,26 @@ def closed_form(L, cap, target, kind, with_steps=False):
     underfilled = n_fin < target
     t_end = int(T[order[target - 1]]) if not underfilled else int(e.max())
     deferred = sorted(set(range(n)) - set(accepted))
+    e0 = _e(L, cap)
     outcome = np.where(L <= cap, FINISHED, CAPPED)
-    outcome = np.where(e > t_end, ABORTED, outcome)
+    outcome = np.where((e0 > t_end) | ((e0 > e) & (kind == SHORT)), ABORTED, outcome)
     retained = np.zeros_like(L)
     for i in accepted:
-        retained[i] = e[i]
+        retained[i] = np.where(kept[i], e0[i], 0)
     r = Round(kind, t_end, accepted, deferred, bool(underfilled), outcome.astype(np.int32), retained)
     if with_steps:
-        r.steps = closed_form_steps(L, cap, target, kind, t_end, T, order)
+        r.steps = closed_form_steps(L, cap, target, kind, t_end, T, order, e, keep)
     return r
 
 
-def closed_form_steps(L, cap, target, kind, t_end, T, order):
+def closed_form_steps(L, cap, target, kind, t_end, T, order, e_eff=None, keep=None):
     """Per-step records for t = 1..t_end: live slots decoded at step t
     (e_s >= t, stable slot order), slots finishing at t, c_i(t), accepted(t),
     done(t)."""
     L = np.asarray(L, np.int64)
     n, G = L.shape
-    e = _e(L, cap).reshape(-1)
+    e0 = _e(L, cap).reshape(-1)
+    e = (e0 if e_eff is None else np.asarray(e_eff)).reshape(-1)
     fin_ok = (L.reshape(-1) <= cap) | (kind == LONG)
     rank = {p: k for k, p in enumerate(order)}
     if kind == LONG:
@@ -95,21 +122,28 @@ def closed_form_steps(L, cap, target, kind, t_end, T, order):
     steps = []
     for t in range(1, t_end + 1):
         live = np.nonzero(e >= t)[0].astype(np.int32)
-        ending = np.nonzero(e == t)[0].astype(np.int32)
-        c = np.sum(((e <= t) & fin_ok).reshape(n, G), axis=1).astype(np.int32)
+        ending = np.nonzero((e == t) & (e == e0))[0].astype(np.int32)   # EOS or cap, not a sibling abort
+        Lf = np.minimum(np.asarray(L, np.int64).reshape(-1), cap)
+        c = np.sum(((Lf <= t) & (e >= Lf) & fin_ok).reshape(n, G), axis=1)
+        c = np.minimum(c, G if keep is None or kind == LONG else keep).astype(np.int32)
         acc = min(target, sum(1 for p in range(n) if T[p] <= t and rank[p] < target))
         steps.append(dict(t=t, live=live, ending=ending, counts=c, accepted=acc,
                           done=int(acc == target or t == int(e.max()))))
     return steps
 
 
-def step_loop(L, cap, target, kind, with_steps=False):
+def step_loop(L, cap, target, kind, with_steps=False, keep=None):
     """Literal step-by-step simulation of the round (the brute-force pin of
     `closed_form`): every live sequence emits token t; it ends on EOS (t == L)
-    or at the cap; completed prompts are admitted in index order until
-    `target` are accepted or nothing is live."""
+    or at the cap; a prompt completes when `keep` of its responses finished
+    (its other live responses are aborted after that step); completed prompts
+    are admitted in index order until `target` are accepted or nothing is
+    live."""
     L = np.asarray(L, np.int64)
     n, G = L.shape
+    keep = G if (keep is None or kind == LONG) else keep
+    kept = np.zeros((n, G), bool)
+    done_p = [False] * n
     if kind == LONG:
         target = n
     live = list(range(n * G))
@@ -121,25 +155,34 @@ def step_loop(L, cap, target, kind, with_steps=False):
         t += 1
         decoded = list(live)
         ending, completed = [], []
-        for s in decoded:
+        for s in decoded:                          # slot order: lower j first
             i, j = divmod(s, G)
             if t == L[i, j]:                       # token t is EOS
                 outcome[i, j] = FINISHED
                 ending.append(s)
-                cnt[i] += 1
-                if cnt[i] == G:
-                    completed.append(i)
+                if not done_p[i] and cnt[i] < keep:
+                    cnt[i] += 1
+                    kept[i, j] = True
+                    if cnt[i] == keep:
+                        completed.append(i)
             elif t == cap:                         # length cap reached
                 outcome[i, j] = CAPPED
                 ending.append(s)
                 if kind == LONG:
                     cnt[i] += 1
+                    kept[i, j] = True
                     if cnt[i] == G:
                         completed.append(i)
+        for i in completed:
+            done_p[i] = True
         for i in sorted(completed):
             if len(accepted) < target:
                 accepted.append(i)
-        live = [s for s in decoded if s not in set(ending)]
+        # siblings of a prompt that completed at t are aborted after step t
+        aborted_now = [s for s in decoded if s not in set(ending) and done_p[s // G]]
+        for s in aborted_now:
+            outcome[s // G, s % G] = ABORTED
+        live = [s for s in decoded if s not in set(ending) and not done_p[s // G]]
         done = len(accepted) == target or not live
         if with_steps:
             steps.append(dict(t=t, live=np.array(decoded, np.int32), ending=np.array(ending, np.int32),
@@ -151,7 +194,7 @@ def step_loop(L, cap, target, kind, with_steps=False):
     deferred = [i for i in range(n) if i not in accepted]
     retained = np.zeros((n, G), np.int64)
     for i in accepted:
-        retained[i] = np.minimum(L[i], cap)
+        retained[i] = np.where(kept[i], np.minimum(L[i], cap), 0)
     r = Round(kind, t, accepted, deferred, len(accepted) < target, outcome, retained, steps)
     return r
 
@@ -170,7 +213,7 @@ def partition(n, world):
     return out
 
 
-def dp_protocol(L, cap, target, kind, world):
+def dp_protocol(L, cap, target, kind, world, keep=None):
     """The per-step DP cutoff exchange: each rank counts
     k_r(t), the prompts of its range completing at step t; after an
     all-gather rank r admits min(k_r, max(0, target - acc - sum_{r'<r} k_r'))
@@ -181,7 +224,11 @@ def dp_protocol(L, cap, target, kind, world):
     if kind == LONG:
         target = n
     e = _e(L, cap)
-    fin_ok = (L <= cap) | (kind == LONG)
+    if kind == SHORT:
+        _, T = _kept(L, cap, G if keep is None else keep)
+        e = np.minimum(e, T[:, None])
+    else:
+        T = e.max(axis=1)
     parts = partition(n, world)
     acc, accepted, t = 0, [], 0
     emax = int(e.max())
@@ -190,7 +237,7 @@ def dp_protocol(L, cap, target, kind, world):
         t += 1
         ks, comp = [], []
         for lo, hi in parts:
-            c = [i for i in range(lo, hi) if np.all(fin_ok[i]) and int(e[i].max()) == t]
+            c = [i for i in range(lo, hi) if T[i] == t]
             comp.append(c)
             ks.append(len(c))
         live_counts.append([int(np.sum(e[lo:hi] >= t)) for lo, hi in parts])

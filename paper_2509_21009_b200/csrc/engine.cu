@@ -113,7 +113,7 @@ struct RpCtx {
 
   // round state (host)
   bool active = false, collected = true;
-  int kind = 0, trace = 0, G = 0, cap = 0, target = 0, n_glob = 0, lo = 0, n_loc = 0;
+  int kind = 0, trace = 0, G = 0, keep = 0, cap = 0, target = 0, n_glob = 0, lo = 0, n_loc = 0;
   int64_t round_id = 0;
   std::vector<QueuedPrompt> round_prompts;  // this rank's slice
   std::deque<QueuedPrompt> fifo;
@@ -777,14 +777,17 @@ static int prefill(RpCtx* c, const std::vector<int>& toks, const std::vector<int
   return RP_OK;
 }
 
-int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, int32_t cap, int32_t target,
-                    int32_t flags, int64_t round_id) {
+int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, int32_t keep, int32_t cap,
+                    int32_t target, int32_t flags, int64_t round_id) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
   if (c->active) return c->fail(RP_EBUSY, "a round is active (collect it first)");
   const int kind = flags & RP_LONG ? 1 : 0;
   const int trace = flags & RP_TRACE ? 1 : 0;
   if (G < 1) return c->fail(RP_EINVAL, "invalid field: G (>= 1)");
+  if (keep == 0) keep = G;
+  if (keep < 1 || keep > G) return c->fail(RP_EINVAL, "invalid field: keep (1..G, 0 = G)");
+  if (kind == 1 && keep != G) return c->fail(RP_EINVAL, "invalid field: keep (RP_LONG needs keep == G)");
   if (n < 1) return c->fail(RP_EINVAL, "invalid field: n_prompts (>= 1)");
   if (cap < 1 || cap > c->rd.max_cap) return c->fail(RP_EINVAL, "invalid field: cap (1..max_cap)");
   if (target < 1 || target > n) return c->fail(RP_EINVAL, "invalid field: target (1..n_prompts)");
@@ -814,8 +817,10 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
     }
   }
   if (trace)
-    for (auto& p : all)
-      if ((int)p.trace.size() != G) return c->fail(RP_EINVAL, "invalid field: trace_lens (queued prompt lacks a trace)");
+    for (auto& p : all) {
+      if ((int)p.trace.size() < G) return c->fail(RP_EINVAL, "invalid field: trace_lens (queued prompt lacks a trace)");
+      p.trace.resize(G);   // a queued prompt re-runs with the long round's G (= R0)
+    }
   // contiguous slice of this rank
   const int W = c->rd.world, r = c->rd.rank;
   const int base = n / W, extra = n % W;
@@ -827,11 +832,11 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   for (int i = 0; i < n_loc; ++i) T += (long long)all[lo + i].tokens.size();
   if (T > c->rd.max_prompt_tokens) return c->fail(RP_ENOSPC, "prompt tokens %lld > max_prompt_tokens", T);
 
-  c->kind = kind; c->trace = trace; c->G = G; c->cap = cap; c->target = target; c->n_glob = n;
+  c->kind = kind; c->trace = trace; c->G = G; c->keep = keep; c->cap = cap; c->target = target; c->n_glob = n;
   c->lo = lo; c->n_loc = n_loc; c->round_id = round_id;
   c->round_prompts.assign(all.begin() + lo, all.begin() + lo + n_loc);
   RoundDev& R = c->R;
-  R.cap = cap; R.G = G; R.target = target; R.kind = kind; R.trace = trace; R.n_prompts = n_loc;
+  R.cap = cap; R.G = G; R.keep = keep; R.target = target; R.kind = kind; R.trace = trace; R.n_prompts = n_loc;
   R.trace_buf = c->trace_dev; R.trace_steps = c->trace_steps;
 
   // ---- host plan: prompt pages, sibling page tables, fork jobs
@@ -981,7 +986,7 @@ int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, i
   int rc = read_ctl(c);
   if (rc) return rc;
   if (!c->h_ctl->done) return c->fail(RP_ESTATE, "round not done");
-  const int acc = c->h_ctl->acc_local, G = c->G, nr = acc * G;
+  const int acc = c->h_ctl->acc_local, nr = acc * c->keep;
   launch_collect_pack(c->R, c->col_meta, c->col_tok, c->st);
   c->launches += 2;
   std::vector<int> meta((size_t)4 * nr + nr + 1);

@@ -112,14 +112,32 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
   }
   if (tid == 0) { s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; s_ctx = 0; }
   __syncthreads();
-  // prompts completing at step t, in prompt-index order
+  // prompts completing at step t, in prompt-index order.  A prompt completes
+  // when `keep` of its responses have finished ("finishing after
+  // the first R0 complete"; keep == G without response-level speculation).
+  // Of the siblings that finished at step t, the lowest j fill the remaining
+  // keep slots (the rest are ST_DROPPED); siblings still decoding are aborted
+  // at once, so their pages are freed below and they leave the batch.
   for (int base = 0; base < R.n_prompts; base += CTL_THREADS) {
     const int p = base + tid;
     int flag = 0;
-    if (p < R.n_prompts && R.p_state[p] == PS_RUNNING && R.p_cnt[p] == R.G) flag = 1;
+    if (p < R.n_prompts && R.p_state[p] == PS_RUNNING && R.p_cnt[p] >= R.keep) flag = 1;
     int tot;
     const int off = block_exscan(flag, &tot, scan_sm);
-    if (flag) { R.p_state[p] = PS_COMPLETE; R.comp_list[s_k + off] = p; }
+    if (flag) {
+      R.p_state[p] = PS_COMPLETE; R.comp_list[s_k + off] = p;
+      if (R.keep < R.G) {
+        int room = R.keep;
+        for (int j = 0; j < R.G; ++j)
+          if (R.status[p * R.G + j] == ST_FINISHED && R.gen[p * R.G + j] < t) --room;
+        for (int j = 0; j < R.G; ++j) {
+          const int s = p * R.G + j;
+          const int st = R.status[s];
+          if (st == ST_LIVE) R.status[s] = ST_ABORTED;
+          else if (st == ST_FINISHED && R.gen[s] == t) { if (room > 0) --room; else R.status[s] = ST_DROPPED; }
+        }
+      }
+    }
     __syncthreads();
     if (tid == 0) s_k += tot;
     __syncthreads();
@@ -281,18 +299,32 @@ void launch_ctl(const RoundDev& R, int appended, int mode, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------ collect pack
-// Pack the accepted prompts' responses, in acceptance order, j = 0..G-1:
-// meta[r] = {prompt (local index), j, len, status}; tokens contiguous.
+// Pack the retained responses of the accepted prompts, in acceptance order,
+// j ascending: all G in a long round, the `keep` finished ones in a short
+// round.  meta[r] = {prompt (local index), j, len, status}; tokens contiguous.
+__device__ __forceinline__ int retained_slot(const RoundDev& R, int r) {
+  const int p = R.accept_order[r / R.keep];
+  int q = r % R.keep;
+  for (int j = 0; j < R.G; ++j) {
+    const int s = p * R.G + j;
+    if (R.kind == 1 || R.status[s] == ST_FINISHED) {
+      if (q == 0) return s;
+      --q;
+    }
+  }
+  return p * R.G;   // unreachable: an accepted prompt has keep retained responses
+}
+
 __global__ void collect_offsets_kernel(RoundDev R, int* meta, int* offs) {
   __shared__ int scan_sm[40];
   const int acc = R.ctl->acc_local;
-  const int nr = acc * R.G;
+  const int nr = acc * R.keep;
   int base_off = 0;
   for (int base = 0; base < nr; base += blockDim.x) {
     const int r = base + threadIdx.x;
     int len = 0;
     if (r < nr) {
-      const int p = R.accept_order[r / R.G], j = r % R.G, s = p * R.G + j;
+      const int s = retained_slot(R, r), p = R.slot_prompt[s], j = R.slot_j[s];
       len = R.gen[s];
       meta[4 * r] = p; meta[4 * r + 1] = j; meta[4 * r + 2] = len; meta[4 * r + 3] = R.status[s];
     }
@@ -305,9 +337,9 @@ __global__ void collect_offsets_kernel(RoundDev R, int* meta, int* offs) {
 }
 
 __global__ void collect_copy_kernel(RoundDev R, const int* offs, int* tokens) {
-  const int nr = R.ctl->acc_local * R.G;
+  const int nr = R.ctl->acc_local * R.keep;
   for (int r = blockIdx.x; r < nr; r += gridDim.x) {
-    const int p = R.accept_order[r / R.G], j = r % R.G, s = p * R.G + j;
+    const int s = retained_slot(R, r);
     const int len = R.gen[s];
     for (int k = threadIdx.x; k < len; k += blockDim.x) tokens[offs[r] + k] = R.tok_out[(size_t)s * R.cap + k];
   }

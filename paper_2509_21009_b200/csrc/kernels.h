@@ -6,7 +6,9 @@
 
 namespace rp {
 
-enum SeqStatus { ST_LIVE = 0, ST_FINISHED = 1, ST_CAPPED = 2, ST_ABORTED = 3 };
+// ST_DROPPED: finished (EOS) at the step its prompt completed but beyond the
+// first `keep` (response-level speculation, ties to the lower j).
+enum SeqStatus { ST_LIVE = 0, ST_FINISHED = 1, ST_CAPPED = 2, ST_ABORTED = 3, ST_DROPPED = 4 };
 enum PromptState { PS_RUNNING = 0, PS_ACCEPTED = 1, PS_COMPLETE = 2 };
 
 // One unit of attention work: a block of query tokens (decode: 1 token; the
@@ -42,6 +44,7 @@ struct CtlBlock {
 
 struct RoundDev {
   int S, P, maxp, cap, G, target, kind /*0 short 1 long*/, trace, eos, n_prompts, kv_heads;
+  int keep;           // responses retained per prompt (R0 <= G; == G in long rounds)
   int world, rank;
   int* slot_prompt; int* slot_j; int* kv_len; int* gen; int* trace_L; int* status; int* own0;
   int* tok_out;       // [S][cap]
@@ -87,7 +90,7 @@ void launch_kv_fork(const int* jobs /*[n][3] src,dst,rows*/, int n, void* kv_poo
 void launch_sampler(const float* logits, int V, int v0, int row_div, const RoundDev& R, uint64_t seed,
                     float inv_temp, uint32_t round_id, cudaStream_t st);
 void launch_ctl(const RoundDev& R, int appended, int mode /*0 all, 1 phase A, 2 phase B*/, cudaStream_t st);
-void launch_collect_pack(const RoundDev& R, int* meta /*[acc*G][4]*/, int* tokens, cudaStream_t st);
+void launch_collect_pack(const RoundDev& R, int* meta /*[acc*keep][4]*/, int* tokens, cudaStream_t st);
 int attn_smem_bytes(int hd);
 int attn_init_attrs();
 

@@ -70,7 +70,7 @@ def load_library(path=LIB_PATH):
     P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     lib.rp_query_sizes.argtypes = [ctypes.POINTER(ModelDesc), ctypes.POINTER(RuntimeDesc), ctypes.POINTER(Sizes)]
     lib.rp_init_model.argtypes = [ctypes.POINTER(ModelDesc), ctypes.POINTER(RuntimeDesc), ctypes.POINTER(P)]
-    lib.rp_submit_round.argtypes = [P, ctypes.POINTER(Prompt), I32, I32, I32, I32, I32, I64]
+    lib.rp_submit_round.argtypes = [P, ctypes.POINTER(Prompt), I32, I32, I32, I32, I32, I32, I64]
     lib.rp_step.argtypes = [P, I32, ctypes.POINTER(Status)]
     lib.rp_collect.argtypes = [P, ctypes.POINTER(Response), I32, ctypes.POINTER(I32), I64, ctypes.POINTER(I32),
                                ctypes.POINTER(I64)]
@@ -205,13 +205,15 @@ class Engine:
         return int(self.L.rp_launch_count(self.h))
 
     # --------------------------------------------------------------- the ABI
-    def submit(self, prompts, G, cap, target, long_round=False, trace=None, round_id=0):
+    def submit(self, prompts, G, cap, target, long_round=False, trace=None, round_id=0, keep=0):
         """prompts: list of dicts {prompt_id, tokens} (None -> pop the queue);
-        trace: None or int array [n, G] of response lengths (trace mode)."""
+        trace: None or int array [n, G] of response lengths (trace mode);
+        keep: responses retained per prompt (R0 < G: response-level
+        speculation; 0 -> G)."""
         flags = (RP_LONG if long_round else RP_SHORT) | (RP_TRACE if trace is not None else 0)
         if prompts is None:
             n = target
-            rc = self.L.rp_submit_round(self.h, None, n, G, cap, target, flags, round_id)
+            rc = self.L.rp_submit_round(self.h, None, n, G, keep, cap, target, flags, round_id)
             self._check(rc)
             return
         n = len(prompts)
@@ -227,7 +229,7 @@ class Engine:
                 tl = np.ascontiguousarray(trace[i], dtype=np.int32)
                 self._keep.append(tl)
                 arr[i].trace_lens = _i32p(tl)
-        self._check(self.L.rp_submit_round(self.h, arr, n, G, cap, target, flags, round_id))
+        self._check(self.L.rp_submit_round(self.h, arr, n, G, keep, cap, target, flags, round_id))
 
     def step(self, max_steps=1 << 30):
         st = Status()

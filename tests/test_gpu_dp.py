@@ -30,16 +30,18 @@ def main():
                     kv_pool_bytes=64 << 20, graph_steps=4, rank=rank, world=world, nccl_id=obj[0])
     ok = True
     fifo = []
-    for seed in range(3):
+    for seed in range(5):
+        # seeds 3, 4: response-level speculation, G = 5 launched, R0 = 4 kept
+        Gs, keep = (G, None) if seed < 3 else (5, 4)
         ps = gen.prompts(n, 0, cfg["eos_id"], (1, 100), 40 + seed)
-        L = gen.length_trace(n, G, 3.4, 0.6, 0.85, 600, seed)[:, 0, :]
+        L = gen.length_trace(n, Gs, 3.4, 0.6, 0.85, 600, seed)[:, 0, :]
         target = 10
-        eng.submit(ps, G, cap, target, trace=L, round_id=seed)
+        eng.submit(ps, Gs, cap, target, trace=L, round_id=seed, keep=keep or 0)
         st = eng.run()
         res = eng.collect()
         acc_local = list(dict.fromkeys(r["prompt_id"] for r in res))
         acc = dp.all_gather_ids(acc_local)
-        ref = sched.closed_form(L, cap, target, sched.SHORT)
+        ref = sched.closed_form(L, cap, target, sched.SHORT, keep=keep)
         lo, hi = dp.partition(n, world)[rank]
         fifo += [ps[i]["prompt_id"] for i in ref.deferred if lo <= i < hi]   # this rank's deferrals
         good = (st.t == ref.t_end and sorted(acc) == sorted(ps[i]["prompt_id"] for i in ref.accepted)
@@ -48,7 +50,8 @@ def main():
                 and eng.long_queue() == fifo)
         for r in res:
             i = r["prompt_id"] - ps[0]["prompt_id"]
-            good = good and r["len"] == L[i, r["j"]]
+            good = good and r["len"] == L[i, r["j"]] and ref.retained_len[i, r["j"]] == r["len"]
+        good = good and len(res) == sum(int(np.count_nonzero(ref.retained_len[i])) for i in range(lo, hi))
         print("rank %d seed %d t_end %d/%d accepted %d/%d ok=%s" % (rank, seed, st.t, ref.t_end, st.accepted,
                                                                   len(ref.accepted), good), flush=True)
         ok = ok and good

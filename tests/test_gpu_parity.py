@@ -83,8 +83,8 @@ def _trace(n, G, seed, l_max=600, mu0=3.4):
     return gen.length_trace(n, G, mu0, 0.6, 0.85, l_max, seed)
 
 
-def _check_round_trace(eng, L, cap, target, kind):
-    ref = sched.closed_form(L, cap, target, kind, with_steps=True)
+def _check_round_trace(eng, L, cap, target, kind, keep=None):
+    ref = sched.closed_form(L, cap, target, kind, with_steps=True, keep=keep)
     got = eng.debug_trace(ref.t_end + 2)
     assert len(got) == ref.t_end
     for a, b in zip(got, ref.steps):
@@ -128,6 +128,74 @@ def test_short_round_schedule_bit_exact(tiny, seed, graph_steps):
     for r in res2:
         k = q.index(r["prompt_id"])
         assert r["len"] == min(L2[k, r["j"]], 200)
+    eng.close()
+
+
+@pytest.mark.parametrize("seed,graph_steps", [(0, 0), (1, 4), (2, 4)])
+def test_response_speculation_schedule_bit_exact(tiny, seed, graph_steps):
+    """NEXT-1: G = ceil(1.25 R0) = 5 responses
+    launched per prompt, the first R0 = 4 to finish kept, siblings aborted at
+    once.  Per-step live lists, acceptance, the retained set and the queue
+    match the oracle; the long round re-runs R0 responses without
+    speculation."""
+    eng = make_engine(tiny, graph_steps=graph_steps, max_seqs=80)
+    n, G, R0 = 14, 5, 4
+    ps = gen.prompts(n, 0, tiny["eos_id"], (1, 100), 50 + seed)
+    full = _trace(n, G, 60 + seed)
+    L = full[:, 0, :]
+    cap, target = 128, 10
+    eng.debug_trace_enable(700)
+    eng.submit(ps, G, cap, target, trace=L, round_id=seed, keep=R0)
+    st = eng.run()
+    ref = _check_round_trace(eng, L, cap, target, sched.SHORT, keep=R0)
+    assert st.t == ref.t_end and st.accepted == len(ref.accepted) and bool(st.underfilled) == ref.underfilled
+    assert st.decoded_tokens == sum(len(x["live"]) for x in ref.steps)
+    res = eng.collect()
+    assert len(res) == len(ref.accepted) * R0
+    got = [(r["prompt_id"] - ps[0]["prompt_id"], r["j"], r["len"]) for r in res]
+    want = [(i, j, int(ref.retained_len[i, j])) for i in ref.accepted for j in range(G) if ref.retained_len[i, j]]
+    assert got == want
+    for r in res:
+        assert r["tokens"][-1] == tiny["eos_id"] and r["finish"] == 1
+    assert eng.long_queue() == [ps[i]["prompt_id"] for i in ref.deferred]
+    q = eng.long_queue()
+    if len(q) >= 2:
+        L2 = full[:, 1, :R0][[i - ps[0]["prompt_id"] for i in q]]
+        eng.debug_trace_enable(700)
+        eng.submit([ps[i - ps[0]["prompt_id"]] for i in q], R0, cap, len(q), long_round=True, trace=L2,
+                   round_id=100 + seed)
+        eng.run()
+        _check_round_trace(eng, L2, cap, len(q), sched.LONG)
+        assert len(eng.collect()) == len(q) * R0
+    eng.close()
+
+
+def test_response_speculation_ties_and_sampling(tiny, oracle_w):
+    """Hand-worked ties (oracle test_speculation_keeps_first_finishers...):
+    G=4, keep=2; prompt 0 keeps j=1,3 (both end at 3), prompt 1 keeps j=0
+    and j=1 (j=2 ends at the same step 7 and is dropped).  The kept tokens
+    are the oracle's Gumbel argmax with uid = prompt_id * G + j."""
+    eng = make_engine(tiny, graph_steps=2)
+    ps = gen.prompts(2, 0, tiny["eos_id"], (10, 30), 77)
+    L = np.array([[5, 3, 9, 3], [2, 7, 7, 20]])
+    eng.debug_trace_enable(64)
+    eng.submit(ps, 4, 100, 2, trace=L, round_id=4, keep=2)
+    st = eng.run()
+    _check_round_trace(eng, L, 100, 2, sched.SHORT, keep=2)
+    assert st.t == 7
+    res = eng.collect()
+    assert [(r["prompt_id"] - ps[0]["prompt_id"], r["j"], r["len"]) for r in res] == [
+        (0, 1, 3), (0, 3, 3), (1, 0, 2), (1, 1, 7)]
+    by_id = {p["prompt_id"]: p["tokens"] for p in ps}
+    tr = {p["prompt_id"]: L[i] for i, p in enumerate(ps)}
+    checked, mism = _check_sampled(tiny, oracle_w, res, by_id, 4, 4, 3, trace=tr)
+    assert checked == 15 and mism <= 1
+    # keep = G is the non-speculative schedule
+    eng.debug_trace_enable(64)
+    eng.submit(ps, 4, 100, 2, trace=L, round_id=4, keep=4)
+    st = eng.run()
+    _check_round_trace(eng, L, 100, 2, sched.SHORT)
+    assert st.t == 20 and len(eng.collect()) == 8
     eng.close()
 
 
@@ -241,6 +309,10 @@ def test_invalid_arguments(tiny):
         eng.submit(ps, 2, 10, 3)
     with pytest.raises(rp.RPError):
         eng.submit(ps, 2, 10, 1, long_round=True)
+    with pytest.raises(rp.RPError):
+        eng.submit(ps, 2, 10, 1, keep=3)                         # keep > G
+    with pytest.raises(rp.RPError):
+        eng.submit(ps, 2, 10, 2, long_round=True, keep=1)        # no speculation in a long round
     with pytest.raises(rp.RPError) as e:
         eng.step()
     assert e.value.code == rp.RP_ESTATE

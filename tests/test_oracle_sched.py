@@ -30,13 +30,55 @@ def test_brute_force_equals_closed_form_all_tiny_traces():
                 _cmp(X.step_loop(L, cap, target, X.SHORT), X.closed_form(L, cap, target, X.SHORT))
 
 
+def test_brute_force_speculation_all_tiny_traces():
+    """Response-level speculation: 2 prompts x G=3 x
+    lengths 1..4 (4^6 traces), every keep < G, cap and target."""
+    n, G = 2, 3
+    for flat in itertools.product(range(1, 5), repeat=n * G):
+        L = np.array(flat).reshape(n, G)
+        for keep in (1, 2):
+            for cap in (2, 4):
+                for target in (1, 2):
+                    _cmp(X.step_loop(L, cap, target, X.SHORT, keep=keep),
+                         X.closed_form(L, cap, target, X.SHORT, keep=keep))
+
+
+def test_speculation_keeps_first_finishers_and_aborts_siblings():
+    """Hand-worked case: G=4, keep=2.  Prompt 0 lengths (5,3,9,3): the two
+    3s finish first -> T_0 = 3, j=1,3 kept, j=0,2 aborted after step 3.
+    Prompt 1 (2,7,7,20): T_1 = 7, tie at 7 goes to j=1 (lower index), j=2
+    finishes at 7 but is not retained, j=3 aborted."""
+    L = np.array([[5, 3, 9, 3], [2, 7, 7, 20]])
+    r = X.closed_form(L, 100, 2, X.SHORT, keep=2)
+    assert r.accepted == [0, 1] and r.t_end == 7
+    assert r.retained_len.tolist() == [[0, 3, 0, 3], [2, 7, 0, 0]]
+    assert r.outcome.tolist() == [[X.ABORTED, X.FINISHED, X.ABORTED, X.FINISHED],
+                                  [X.FINISHED, X.FINISHED, X.FINISHED, X.ABORTED]]
+    # keep = G reproduces the non-speculative schedule
+    for keep in (None, 4):
+        r = X.closed_form(L, 100, 2, X.SHORT, keep=keep)
+        assert r.accepted == [0, 1] and r.t_end == 20
+
+
+def test_speculation_decodes_fewer_tokens():
+    """With keep < G every prompt completes no later and fewer tokens are
+    decoded than with keep = G on the same trace (monotonicity)."""
+    tr = length_trace(40, 8, 4.0, 0.5, 0.8, 2000, 11)[:, 0, :]
+    full = X.closed_form(tr, 1024, 30, X.SHORT, with_steps=True)
+    spec = X.closed_form(tr, 1024, 30, X.SHORT, with_steps=True, keep=6)
+    assert spec.t_end <= full.t_end
+    assert sum(len(s["live"]) for s in spec.steps) < sum(len(s["live"]) for s in full.steps)
+    assert all(int(np.count_nonzero(spec.retained_len[i])) == 6 for i in spec.accepted)
+
+
 def test_per_step_records_match():
     rng = np.random.default_rng(5)
-    for _ in range(30):
+    for it in range(40):
         L = rng.integers(1, 40, size=(6, 4))
+        keep = None if it % 2 == 0 else 1 + it % 3
         for kind, target in ((X.SHORT, 4), (X.LONG, 6)):
-            a = X.step_loop(L, 30, target, kind, with_steps=True)
-            b = X.closed_form(L, 30, target, kind, with_steps=True)
+            a = X.step_loop(L, 30, target, kind, with_steps=True, keep=keep)
+            b = X.closed_form(L, 30, target, kind, with_steps=True, keep=keep)
             assert len(a.steps) == len(b.steps) == a.t_end
             for sa, sb in zip(a.steps, b.steps):
                 assert np.array_equal(sa["live"], sb["live"])
