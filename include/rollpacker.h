@@ -241,7 +241,7 @@ int rp_debug_last_logits(void* ctx, float* logits_out, int32_t* slots_out, int32
  * the context's stream.  steps == 0 reads the totals: ms_out[RP_PROF_N]
  * (summed milliseconds), counts_out[RP_PROF_N] (launches),
  * rows_ctx_steps[3] = {sum of live rows, sum of attention context tokens,
- * profiled steps}.  Any pointer may be NULL. */
+ * profiled steps}; steps < 0 disarms.  Any pointer may be NULL. */
 int rp_debug_profile(void* ctx, int32_t steps, double* ms_out, int64_t* counts_out, int64_t* rows_ctx_steps);
 
 /* Run the tcgen05 GEMM alone on device pointers: Y[n][m] = sum_k W[m][k] X[n][k]

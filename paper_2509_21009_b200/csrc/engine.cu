@@ -1102,6 +1102,7 @@ int rp_debug_last_logits(void* ctx, float* logits_out, int32_t* slots_out, int32
 int rp_debug_profile(void* ctx, int32_t steps, double* ms_out, int64_t* counts_out, int64_t* rows_ctx_steps) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
+  if (steps < 0) { c->prof_steps_left = 0; return RP_OK; }
   if (steps > 0) {   // arm: the next `steps` decode steps run eagerly, bracketed by events
     c->prof_steps_left = steps;
     for (int i = 0; i < RP_PROF_N; ++i) { c->prof_ms[i] = 0; c->prof_cnt[i] = 0; }
