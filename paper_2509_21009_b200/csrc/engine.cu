@@ -84,6 +84,7 @@ struct RpCtx {
 
   // activations / workspace
   float* x = nullptr;
+  float* ssq = nullptr;         // [rows][d / 128] per-tile sums of squares of x (folded RMSNorm)
   float* ar = nullptr;          // TP: all-reduced partial of a row-parallel GEMM
   __nv_bfloat16 *h = nullptr, *q = nullptr, *att = nullptr, *mid = nullptr;
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
@@ -236,6 +237,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto x = cv.take<float>((size_t)z.Tcap * d);
   auto ar = cv.take<float>(tp_of(rd) > 1 ? (size_t)z.Tcap * d : 1);
   auto h = cv.take<__nv_bfloat16>((size_t)z.Tcap * d);
+  auto ssq = cv.take<float>((size_t)z.Tcap * std::max<size_t>(1, d / 128));   // folded-RMSNorm partial sums
   auto qkv = cv.take<float>((size_t)z.Tcap * (H + 2 * KV) * hd);
   auto q = cv.take<__nv_bfloat16>((size_t)z.Tcap * H * hd);
   auto att = cv.take<__nv_bfloat16>((size_t)z.Tcap * H * hd);
@@ -285,7 +287,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto free_stack = cv.take<int>(max_pages + 1);
   auto ident = cv.take<int>(max_pages + 1);
   if (c) {
-    c->x = x; c->ar = ar; c->h = h; c->qkv = qkv; c->q = q; c->att = att; c->mid = mid; c->logits = logits;
+    c->x = x; c->ar = ar; c->h = h; c->ssq = ssq; c->qkv = qkv; c->q = q; c->att = att; c->mid = mid; c->logits = logits;
     c->gpart = gpart; c->gctr = gctr; c->apart = apart; c->atickets = atick; c->inv_freq = invf;
     c->rope_cs = rope_cs;
     c->items_pre = items_pre; c->pre_tok = pre_tok; c->pre_pos = pre_pos; c->pre_pt = pre_pt;
@@ -357,12 +359,22 @@ struct ProfScope {
     }
   }
 };
+// Folded RMSNorm (DESIGN.md §5 K6): FOLD_PRODUCE on a RESID GEMM also writes
+// bf16(x) into c->h and per-tile sums of squares into c->ssq; FOLD_CONSUME
+// scales each output row of a GEMM reading c->h by 1/rms.  Valid because the
+// norm weights are 1 (Z12); under TP the RMSNorm kernel runs instead.
+enum { FOLD_NONE = 0, FOLD_PRODUCE = 1, FOLD_CONSUME = 2 };
+
 static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, int n_host, int splits, int epi,
-                 void* out, int ldo, const float* bias, const RopeArgs* rope = nullptr) {
+                 void* out, int ldo, const float* bias, const RopeArgs* rope = nullptr, int fold = FOLD_NONE) {
   GemmArgs a{};
   if (rope) a.rope = *rope;
   a.M = M; a.K = K; a.n_dev = n_dev; a.n_host = n_host; a.splits = splits; a.epi = epi; a.out = out; a.ldo = ldo;
   a.bias = bias; a.partial = c->gpart; a.counters = c->gctr;
+  a.ssq_stride = c->m.d / 128; a.ssq_parts = c->m.d / 128;
+  a.norm_inv_d = 1.0f / (float)c->m.d; a.norm_eps = c->m.eps;
+  if (fold == FOLD_PRODUCE) { a.xb_out = c->h; a.ldxb = c->m.d; a.ssq_out = c->ssq; }
+  if (fold == FOLD_CONSUME) a.ssq_in = c->ssq;
   gemm_launch(p, a, kSMs, c->st);
   c->launches++;
 }
@@ -388,20 +400,27 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
   const int qkvw = (m.H + 2 * m.KV) * m.hd;
   const int sp_qkv = decode ? c->s_qkv : 1, sp_o = decode ? c->s_o : 1, sp_gu = decode ? c->s_gu : 1,
             sp_down = decode ? c->s_down : 1;
+  // folded RMSNorm on a single rank: only layer 0's input norm is a kernel
+  static const bool no_fold = getenv("RP_NO_FOLD") != nullptr;   // A/B switch for measurements
+  const bool fold = !tp && m.d % 128 == 0 && !no_fold;
+  const int f_prod = fold ? FOLD_PRODUCE : FOLD_NONE, f_cons = fold ? FOLD_CONSUME : FOLD_NONE;
   { ProfScope ps(c, RP_PROF_EMBED); launch_embed(tok, n_dev, n_host, c->emb, c->x, m.d, c->st); c->launches++; }
   for (int l = 0; l < m.L; ++l) {
     LayerW& w = c->layers[l];
-    { ProfScope ps(c, RP_PROF_RMSNORM);
-      launch_rmsnorm(c->x, delta, nullptr, n_dev, n_host, w.ln1, c->h, m.d, m.eps, c->st); c->launches++; }
+    const int f_in = (fold && l > 0) ? FOLD_CONSUME : FOLD_NONE;
+    if (f_in == FOLD_NONE) {
+      ProfScope ps(c, RP_PROF_RMSNORM);
+      launch_rmsnorm(c->x, delta, nullptr, n_dev, n_host, w.ln1, c->h, m.d, m.eps, c->st); c->launches++;
+    }
     if (decode && sp_qkv > 1 && m.hd % 64 == 0) {
       // RoPE + KV append fused into the split-K reduction of the QKV GEMM
       ProfScope ps(c, RP_PROF_GEMM_QKV);
       RopeArgs ra{c->q, (uint8_t*)c->rd.kv_pool, c->R.page_table, row_pos, row_pt, c->rope_cs, m.page_bytes,
                   c->R.maxp, l, m.H, m.KV, m.hd};
-      gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_QKV_ROPE, c->qkv, qkvw, w.bqkv, &ra);
+      gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_QKV_ROPE, c->qkv, qkvw, w.bqkv, &ra, f_in);
     } else {
       { ProfScope ps(c, RP_PROF_GEMM_QKV);
-        gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_F32, c->qkv, qkvw, w.bqkv); }
+        gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_F32, c->qkv, qkvw, w.bqkv, nullptr, f_in); }
       { ProfScope ps(c, RP_PROF_ROPE);
         launch_rope_append(c->qkv, n_dev, n_host, row_pos, row_pt, c->R.page_table, c->R.maxp, c->q,
                            c->rd.kv_pool, m, l, c->inv_freq, c->st); c->launches++; }
@@ -411,16 +430,18 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
                        c->apart, c->atickets, m, l, decode, c->st); c->launches++; }
     { ProfScope ps(c, RP_PROF_GEMM_O);
       gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
-           nullptr); }
+           nullptr, nullptr, f_prod); }
     if (tp) tp_allreduce_rows(c, ar_rows);
-    { ProfScope ps(c, RP_PROF_RMSNORM);
+    if (!fold) {
+      ProfScope ps(c, RP_PROF_RMSNORM);
       launch_rmsnorm(c->x, tp ? c->ar : nullptr, nullptr, n_dev, n_host, w.ln2, c->h, m.d, m.eps, c->st);
-      c->launches++; }
+      c->launches++;
+    }
     { ProfScope ps(c, RP_PROF_GEMM_GU);
-      gemm(c, w.p_gu, 2 * m.F, m.d, n_dev, n_host, sp_gu, EPI_SWIGLU, c->mid, m.F, nullptr); }
+      gemm(c, w.p_gu, 2 * m.F, m.d, n_dev, n_host, sp_gu, EPI_SWIGLU, c->mid, m.F, nullptr, nullptr, f_cons); }
     { ProfScope ps(c, RP_PROF_GEMM_DOWN);
       gemm(c, w.p_down, m.d, m.F, n_dev, n_host, sp_down, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
-           nullptr); }
+           nullptr, nullptr, f_prod); }
     if (tp) {
       tp_allreduce_rows(c, ar_rows);
       delta = c->ar;
@@ -434,11 +455,16 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
 static void lm_head_sample(RpCtx* c, const int* n_dev, int n_host, const int* gather, int rows_out, int row_div,
                            int best_rows, bool pending, int splits) {
   RoundDev& R = c->R;
-  { ProfScope ps(c, RP_PROF_RMSNORM);
+  // folded final norm when the rows are the residual rows in place (decode)
+  const bool fold = c->tp <= 1 && !gather && c->m.d % 128 == 0 && !getenv("RP_NO_FOLD");
+  if (!fold) {
+    ProfScope ps(c, RP_PROF_RMSNORM);
     launch_rmsnorm(c->x, pending ? c->ar : nullptr, gather, n_dev, n_host, c->lnf, c->h, c->m.d, c->m.eps, c->st);
-    c->launches++; }
+    c->launches++;
+  }
   { ProfScope ps(c, RP_PROF_GEMM_LM);
-    gemm(c, c->p_lm, c->m.V, c->m.d, n_dev, rows_out, splits, EPI_F32, c->logits, c->m.V, nullptr); }
+    gemm(c, c->p_lm, c->m.V, c->m.d, n_dev, rows_out, splits, EPI_F32, c->logits, c->m.V, nullptr, nullptr,
+         fold ? FOLD_CONSUME : FOLD_NONE); }
   { ProfScope ps(c, RP_PROF_SAMPLER);
     launch_sampler(c->logits, c->m.V, c->m.v0, row_div, R, c->rd.sample_seed, 1.0f / c->rd.temperature,
                    (uint32_t)c->round_id, c->st); c->launches++; }

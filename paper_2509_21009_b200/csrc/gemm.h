@@ -35,6 +35,17 @@ struct GemmArgs {
   int* counters;          // split-K tickets, zero-initialised, self-resetting
   long long* timeline;    // debug: per-CTA %globaltimer stamps [grid][16] (nullptr = off)
   RopeArgs rope;          // EPI_QKV_ROPE only
+  // Folded RMSNorm (norm weights are 1, Z12): a RESID producer also writes
+  // bf16(x) to xb_out[n * ldxb + m] and the sum of squares of its 128-feature
+  // tile to ssq_out[n * ssq_stride + tile]; a consumer (ssq_in != nullptr)
+  // multiplies output column n by rsqrt(sum_p ssq_in[n * ssq_stride + p] *
+  // norm_inv_d + norm_eps), p < ssq_parts, before bias / SwiGLU / RoPE.
+  __nv_bfloat16* xb_out;
+  int ldxb;
+  float* ssq_out;
+  const float* ssq_in;
+  int ssq_parts, ssq_stride;
+  float norm_inv_d, norm_eps;
 };
 
 struct GemmPlan {

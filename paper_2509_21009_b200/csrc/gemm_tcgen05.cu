@@ -34,7 +34,8 @@ constexpr int MAX_STAGES = 12;               // ring depth at small N (18 KB sta
 constexpr int XCH_BYTES = 64 * 33 * 4;       // swiglu exchange
 constexpr int TS = BM + 4;                   // fp32 row stride of the epilogue staging tile
 constexpr int STG_BYTES = 32 * TS * 4;       // [32 columns][128 rows] fp32 staging for 16-byte stores
-constexpr int GEMM_SMEM = RING_BYTES + XCH_BYTES + STG_BYTES + 1024 /*align*/ + 8 * (2 * MAX_STAGES + 4) + 16;
+constexpr int RSC_BYTES = BN * 4;             // per-column RMSNorm scales of the current item
+constexpr int GEMM_SMEM = RING_BYTES + XCH_BYTES + STG_BYTES + RSC_BYTES + 1024 /*align*/ + 8 * (2 * MAX_STAGES + 4) + 16;
 constexpr int GEMM_THREADS = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -165,7 +166,8 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   float* xch = (float*)(smem + RING_BYTES);
   float* stg = (float*)(smem + RING_BYTES + XCH_BYTES);
-  uint64_t* bars = (uint64_t*)(smem + RING_BYTES + XCH_BYTES + STG_BYTES);
+  float* rsc = (float*)(smem + RING_BYTES + XCH_BYTES + STG_BYTES);
+  uint64_t* bars = (uint64_t*)(smem + RING_BYTES + XCH_BYTES + STG_BYTES + RSC_BYTES);
   // bars: full[MAX_STAGES], empty[MAX_STAGES], tfull[2], tempty[2]; then tmem slot, ticket
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * MAX_STAGES + 4);
   int* ticket = (int*)(tmem_slot + 1);
@@ -290,11 +292,34 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     const int q = warp - 4;                 // TMEM lane quarter
     const int et = threadIdx.x - 128;       // 0..127
     int local = 0;
+    int rsc_chunk = -1;                     // chunk whose RMSNorm scales are in rsc
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
       Item I = decode_item(it, m_tiles, a.splits);
       const int n0 = I.chunk * BN, nc = min(BN, N - n0);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
+      if (a.ssq_in && I.chunk != rsc_chunk) {
+        // folded RMSNorm: column scales of this chunk (once per chunk; every
+        // decode item shares chunk 0), computed while the item's MMAs run.
+        // Parts are loaded 8 at a time and summed in part order (deterministic).
+        rsc_chunk = I.chunk;
+        named_bar(3, 128);
+        for (int cc = et; cc < nc; cc += 128) {
+          const float* sp = a.ssq_in + (size_t)(n0 + cc) * a.ssq_stride;
+          float ss = 0.f;
+          int p = 0;
+          for (; p + 8 <= a.ssq_parts; p += 8) {
+            float t[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) t[k] = __ldcg(sp + p + k);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) ss += t[k];
+          }
+          for (; p < a.ssq_parts; ++p) ss += __ldcg(sp + p);
+          rsc[cc] = 1.0f / sqrtf(ss * a.norm_inv_d + a.norm_eps);
+        }
+        named_bar(3, 128);
+      }
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       const int row = 32 * q + lane;        // row within the tile
@@ -387,6 +412,14 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               acc[u].x += t[u].x; acc[u].y += t[u].y; acc[u].z += t[u].z; acc[u].w += t[u].w;
             }
           }
+          if (a.ssq_in) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int col = cb + 4 * u;
+              const float sc = col < col_hi ? rsc[col] : 0.f;
+              acc[u].x *= sc; acc[u].y *= sc; acc[u].z *= sc; acc[u].w *= sc;
+            }
+          }
           if (a.epi == EPI_QKV_ROPE) {
             // rows r4..r4+3 of head-dim index i0 = (m4 % hd); the rotate-half
             // partner rows (i +- hd/2) live in lane ^ (hd/8) of this warp
@@ -456,6 +489,17 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             if (a.epi == EPI_RESID) {
               v.x += old[u].x; v.y += old[u].y; v.z += old[u].z; v.w += old[u].w;
               *(float4*)((float*)a.out + o) = v;
+              if (a.ssq_out) {
+                // bf16(x) for the next GEMM and this tile's sum of squares of
+                // column n (the warp covers the tile's 128 rows: lanes x 4)
+                __nv_bfloat162* xb = (__nv_bfloat162*)(a.xb_out + (size_t)(n0 + col) * a.ldxb + m4);
+                xb[0] = __floats2bfloat162_rn(v.x, v.y);
+                xb[1] = __floats2bfloat162_rn(v.z, v.w);
+                float ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+                if (lane == 0) a.ssq_out[(size_t)(n0 + col) * a.ssq_stride + I.tile] = ss;
+              }
             } else if (a.epi == EPI_F32) {
               v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
               *(float4*)((float*)a.out + o) = v;
@@ -504,6 +548,10 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         }
+        if (a.ssq_in) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= (c0 + j < nc) ? rsc[c0 + j] : 0.f;
+        }
         // Output goes through a shared-memory transpose so each thread writes
         // 16-byte vectors of consecutive features (a row-owning thread would
         // otherwise issue 32 scalar stores per chunk).
@@ -543,6 +591,15 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               const float4 old = *(const float4*)((float*)a.out + o);
               val.x += old.x; val.y += old.y; val.z += old.z; val.w += old.w;
               *(float4*)((float*)a.out + o) = val;
+              if (a.ssq_out) {   // warp = one column n, lanes = the tile's 128 rows x 4
+                __nv_bfloat162* xb = (__nv_bfloat162*)(a.xb_out + (size_t)(n0 + c0 + n) * a.ldxb + mt0 + m4);
+                xb[0] = __floats2bfloat162_rn(val.x, val.y);
+                xb[1] = __floats2bfloat162_rn(val.z, val.w);
+                float ss = val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+                if (lane == 0) a.ssq_out[(size_t)(n0 + c0 + n) * a.ssq_stride + I.tile] = ss;
+              }
             } else if (a.epi == EPI_F32) {
               *(float4*)((float*)a.out + o) = val;
             } else {

@@ -1,6 +1,6 @@
-# A/B of the small-footprint GEMM (co-resident PDL prefetch) vs the 192 KB ring
-set -x
+# A/B: folded RMSNorm vs the RMSNorm kernel, graph step times at several live-batch sizes
 mkdir -p gpurun_out
-timeout -s KILL 300 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -5
-timeout -s KILL 200 python tools/step_profile.py 256 128 64 48 32 16 2>&1 | grep "graph_step" 
-RP_GEMM_BIGRING=1 timeout -s KILL 200 python tools/step_profile.py 256 128 64 48 32 16 2>&1 | grep "graph_step"
+for i in 1 2; do
+timeout -s KILL 200 python tools/step_profile.py 256 128 64 16 2>&1 | grep -A1 "graph_step"
+RP_NO_FOLD=1 timeout -s KILL 200 python tools/step_profile.py 256 128 64 16 2>&1 | grep -A1 "graph_step"
+done
