@@ -137,6 +137,45 @@ __device__ __forceinline__ Item decode_item(int it, int m_tiles, int splits) {
   return r;
 }
 
+// ---- split-K reduction helpers: rows r4..r4+3 of columns cb + 4u (u < RU)
+constexpr int RU = 4;
+template <int S>
+__device__ __forceinline__ void reduce_splits(float4 (&acc)[RU], const float* __restrict__ pb, int cb, int col_hi,
+                                              int r4) {
+  float4 t[S][RU];
+#pragma unroll
+  for (int sp = 0; sp < S; ++sp)
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int col = cb + 4 * u;
+      t[sp][u] = col < col_hi ? __ldcg((const float4*)(pb + (size_t)sp * BN * BM + (size_t)col * BM + r4))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+  for (int u = 0; u < RU; ++u) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int sp = 0; sp < S; ++sp) { v.x += t[sp][u].x; v.y += t[sp][u].y; v.z += t[sp][u].z; v.w += t[sp][u].w; }
+    acc[u] = v;
+  }
+}
+__device__ __forceinline__ void reduce_splits_loop(float4 (&acc)[RU], const float* __restrict__ pb, int cb, int col_hi,
+                                                   int r4, int S) {
+#pragma unroll
+  for (int u = 0; u < RU; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int sp = 0; sp < S; ++sp) {
+    float4 t[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int col = cb + 4 * u;
+      t[u] = col < col_hi ? __ldcg((const float4*)(pb + (size_t)sp * BN * BM + (size_t)col * BM + r4))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) { acc[u].x += t[u].x; acc[u].y += t[u].y; acc[u].z += t[u].z; acc[u].w += t[u].w; }
+  }
+}
+
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB16,
                     const __grid_constant__ CUtensorMap tmB64, const __grid_constant__ CUtensorMap tmB256,
@@ -395,26 +434,21 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         const float* __restrict__ pb = a.partial + ((size_t)((I.chunk * m_tiles + I.tile) * a.splits)) * BN * BM;
         const int r4 = (et & 31) * 4;              // rows r4..r4+3 of the tile
         const int m4 = I.tile * BM + r4;
-        for (int cb = col_lo + (et >> 5); cb < col_hi; cb += 4 * 8) {
-          float4 acc[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int s = 0; s < a.splits; ++s) {
-            float4 t[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int col = cb + 4 * u;
-              t[u] = col < col_hi ? __ldcg((const float4*)(pb + (size_t)s * BN * BM + (size_t)col * BM + r4))
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              acc[u].x += t[u].x; acc[u].y += t[u].y; acc[u].z += t[u].z; acc[u].w += t[u].w;
-            }
+        for (int cb = col_lo + (et >> 5); cb < col_hi; cb += 4 * RU) {
+          float4 acc[RU];
+          // every split's partials requested at once (one L2 round trip),
+          // summed in split order (deterministic, bit-identical to a loop)
+          switch (a.splits) {
+            case 2: reduce_splits<2>(acc, pb, cb, col_hi, r4); break;
+            case 3: reduce_splits<3>(acc, pb, cb, col_hi, r4); break;
+            case 4: reduce_splits<4>(acc, pb, cb, col_hi, r4); break;
+            case 5: reduce_splits<5>(acc, pb, cb, col_hi, r4); break;
+            case 6: reduce_splits<6>(acc, pb, cb, col_hi, r4); break;
+            default: reduce_splits_loop(acc, pb, cb, col_hi, r4, a.splits); break;
           }
           if (a.ssq_in) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < RU; ++u) {
               const int col = cb + 4 * u;
               const float sc = col < col_hi ? rsc[col] : 0.f;
               acc[u].x *= sc; acc[u].y *= sc; acc[u].z *= sc; acc[u].w *= sc;
@@ -430,7 +464,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             const bool lo = i0 < half;
             const float4 bb = a.bias ? *(const float4*)(a.bias + m4) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < RU; ++u) {
               float4 v = acc[u];
               v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
               float4 p;
@@ -470,10 +504,10 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             }
             continue;
           }
-          float4 old[8];
+          float4 old[RU];
           if (a.epi == EPI_RESID) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < RU; ++u) {
               const int col = cb + 4 * u;
               if (col < col_hi) old[u] = *(const float4*)((float*)a.out + (size_t)(n0 + col) * a.ldo + m4);
             }
@@ -481,7 +515,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
           if (a.bias) bb = *(const float4*)(a.bias + m4);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < RU; ++u) {
             const int col = cb + 4 * u;
             if (col >= col_hi) continue;
             const size_t o = (size_t)(n0 + col) * a.ldo + m4;
