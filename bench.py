@@ -182,11 +182,13 @@ def run_ours(a):
         d2h = sum(r["len"] for r in res) * 4 + len(res) * 24
         retained = sum(r["len"] for r in res)
         decoded = st.decoded_tokens
+        # algorithmic HBM bytes of this rank's decode steps (step 1 comes from the prefill)
+        hbm = step_bytes(cfg, e.tp, max(0, st.t - 1), st.decoded_tokens, st.kv_tokens_read)
         if e is not eng and rank != 0:
             # TP ranks decode the same tokens: count them once (on rank 0)
             decoded, retained, h2d, d2h = 0, 0, 0, 0
         return dict(kind=kind, t_end=st.t, decoded=decoded, retained=retained, h2d=h2d, d2h=d2h,
-                    accepted=st.accepted, underfilled=st.underfilled, tp=e.tp)
+                    accepted=st.accepted, underfilled=st.underfilled, tp=e.tp, hbm_bytes=hbm)
 
     # ---- warm-up (the first warm-up round is profiled per kernel class)
     prof = None
@@ -227,15 +229,15 @@ def run_ours(a):
     # ---- reductions over ranks
     t = torch.tensor([dev_s, wall_s], dtype=torch.float64)
     tot = torch.tensor([sum(x["decoded"] for x in rounds), sum(x["retained"] for x in rounds),
-                        sum(x["h2d"] for x in rounds), sum(x["d2h"] for x in rounds), launches],
-                       dtype=torch.float64)
+                        sum(x["h2d"] for x in rounds), sum(x["d2h"] for x in rounds), launches,
+                        sum(x["hbm_bytes"] for x in rounds)], dtype=torch.float64)
     per_round = torch.tensor([x["dev_s"] for x in rounds], dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
         dist.all_reduce(per_round, op=dist.ReduceOp.MAX)
     dev_s, wall_s = t.tolist()
-    decoded, retained, h2d, d2h, launches_all = tot.tolist()
+    decoded, retained, h2d, d2h, launches_all, hbm_all = tot.tolist()
     per_round = per_round.tolist()
     def shutdown():
         if world > 1:
@@ -287,6 +289,13 @@ def run_ours(a):
     }
     if prof is not None:
         line["roofline"], line["kernel_profile"] = roofline(prof, cfg)
+    peak_hbm = load_peaks()[0]
+    line["step_roofline"] = {
+        "bound": "hbm", "unit": "GB/s", "achieved": round(hbm_all / dev_s / 1e9, 1), "peak": peak_hbm * world,
+        "frac": round(hbm_all / dev_s / 1e9 / (peak_hbm * world), 4),
+        "bytes_per_decode_step": round(hbm_all / max(1, sum(max(0, x["t_end"] - 1) for x in rounds)), 0),
+        "scope": "whole timed rounds: every decode step streams all weights once, plus the KV context each "
+                 "live row's attention reads and the logits write + sampler read (DESIGN.md section 7)"}
     if world == 1:
         line["cpu_baseline"] = cpu_baseline(W, quick=True)
     emit(json.dumps(line))
@@ -294,6 +303,23 @@ def run_ours(a):
         with open(a.out, "w") as f:
             f.write(json.dumps(line) + "\n")
     shutdown()
+
+
+def weight_bytes(cfg, tp=1):
+    """bf16 weight bytes one rank streams per decode step (all GEMMs + LM head shard)."""
+    d, H, KV, hd, F, V, L = (cfg[k] for k in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ff", "vocab",
+                                              "n_layers"))
+    per_layer = ((H + 2 * KV) * hd * d + d * H * hd + 2 * F * d + d * F) * 2 // tp
+    return L * per_layer + V * d * 2 // tp
+
+
+def step_bytes(cfg, tp, steps, rows, kv_tokens):
+    """Algorithmic HBM bytes of `steps` decode steps over `rows` decoded rows
+    reading `kv_tokens` context tokens (per layer and KV head) in total:
+    weights once per step + K and V of every context token in every layer and
+    local KV head + fp32 logits written by the LM head and read by the sampler."""
+    L, KV, hd, V = cfg["n_layers"], cfg["n_kv_heads"] // tp, cfg["head_dim"], cfg["vocab"] // tp
+    return steps * weight_bytes(cfg, tp) + kv_tokens * L * KV * hd * 2 * 2 + rows * V * 4 * 2
 
 
 def load_peaks():

@@ -126,6 +126,8 @@ typedef struct {
   int32_t underfilled;       /* done with accepted < target (reading Z4)       */
   int32_t n_prompts_local;
   int64_t decoded_tokens;    /* tokens decoded on this rank this round (incl. aborted) */
+  int64_t kv_tokens_read;    /* sum over decode steps and decoded rows of the attention context
+                                (KV tokens read per layer and KV head); measurement only   */
 } rp_status;
 
 typedef struct {

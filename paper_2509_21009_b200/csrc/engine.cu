@@ -957,6 +957,7 @@ static void fill_status(RpCtx* c, rp_status* st) {
   st->n_live = b.done ? 0 : b.n_live;
   st->accepted = b.acc; st->accepted_local = b.acc_local; st->done = b.done; st->underfilled = b.underfilled;
   st->n_prompts_local = c->n_loc; st->decoded_tokens = b.decoded;
+  st->kv_tokens_read = b.kv_read;
 }
 
 int rp_step(void* ctx, int32_t max_steps, rp_status* st) {

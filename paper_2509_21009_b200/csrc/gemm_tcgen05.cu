@@ -389,10 +389,10 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (split) {
         tc_fence_before();
         mbar_arrive(tempty0 + 8 * acc);     // TMEM stage free for the next item
-        __threadfence();
-        named_bar(1, 128);
         int* ctr = a.counters + I.chunk * m_tiles + I.tile;
         if (coop) {
+          __threadfence();
+          named_bar(1, 128);
           // One wave (every CTA of the grid is resident, so waiting on the
           // other splits cannot deadlock): all split CTAs of the tile wait for
           // its partials, then each reduces its own 1/splits of the columns
@@ -413,7 +413,35 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           const int per = ((nc + a.splits - 1) / a.splits + 3) & ~3;
           col_lo = min(nc, I.split * per);
           col_hi = min(nc, col_lo + per);
+        } else if (n_items <= (int)gridDim.x) {
+          // One wave: split S-1 is the tile's designated reducer.  The other
+          // splits publish their partials with a fire-and-forget release add
+          // and leave at once (their SM goes to the next kernel's prefetch);
+          // the reducer acquires the count, resets it and reduces in split
+          // order (the same sums as the ticket path, bit for bit).
+          named_bar(1, 128);
+          if (I.split != a.splits - 1) {
+            if (et == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(ctr) : "memory");
+            last = false;
+          } else {
+            if (et == 0) {
+              uint32_t spins = 0;
+              int v;
+              do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+                if (++spins == (1u << 26)) {
+                  printf("rollpacker watchdog: split-K reducer stuck (block %d)\n", blockIdx.x);
+                  __trap();
+                }
+              } while (v < a.splits - 1);
+              *ctr = 0;
+            }
+            named_bar(1, 128);
+            last = true;
+          }
         } else {
+          __threadfence();
+          named_bar(1, 128);
           if (et == 0) {
             int old = atomicAdd(ctr, 1);
             *ticket = (old == a.splits - 1);

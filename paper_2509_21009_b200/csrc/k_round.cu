@@ -89,7 +89,7 @@ constexpr int CTL_THREADS = 1024;
 // error}.
 __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
   __shared__ int s_k, s_top, s_keep, s_need, s_err;
-  __shared__ long long s_ctx;
+  __shared__ long long s_ctx, s_rd;
   CtlBlock* C = R.ctl;
   const int n = C->n_live;
   const int t = C->t;
@@ -110,7 +110,7 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     R.status[s] = fin ? ST_FINISHED : capped ? ST_CAPPED : ST_LIVE;
     if (fin || (capped && R.kind == 1)) atomicAdd(&R.p_cnt[R.slot_prompt[s]], 1);
   }
-  if (tid == 0) { s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; s_ctx = 0; }
+  if (tid == 0) { s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; s_ctx = 0; s_rd = 0; }
   __syncthreads();
   // prompts completing at step t, in prompt-index order.  A prompt completes
   // when `keep` of its responses have finished ("finishing after
@@ -160,7 +160,9 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
         }
       }
     }
-    int tot, tk, tn, tc;
+    int tot, tk, tn, tc, trd;
+    // KV tokens the attention of this step read for row i: its context incl. the appended token
+    block_exscan(i < n && appended ? R.kv_len[s] : 0, &trd, scan_sm);
     const int off = block_exscan(cnt, &tot, scan_sm);
     block_exscan(keep, &tk, scan_sm);
     block_exscan(need, &tn, scan_sm);
@@ -168,7 +170,7 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     for (int c = 0; c < cnt; ++c)
       R.free_stack[s_top + off + c] = R.page_table[(size_t)s * R.maxp + R.own0[s] + c];
     __syncthreads();
-    if (tid == 0) { s_top += tot; s_keep += tk; s_need += tn; s_ctx += tc; }
+    if (tid == 0) { s_top += tot; s_keep += tk; s_need += tn; s_ctx += tc; s_rd += trd; }
     __syncthreads();
   }
   if (tid == 0) {
@@ -178,6 +180,7 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     C->n_next = s_keep;
     C->need_pages = s_need;
     C->ctx_sum = s_ctx;
+    C->kv_read += s_rd;
     R.ks_local[0] = s_k; R.ks_local[1] = s_keep; R.ks_local[2] = s_err;
     if (R.world == 1) { R.ks[0] = s_k; R.ks[1] = s_keep; R.ks[2] = s_err; }
   }

@@ -40,6 +40,7 @@ struct CtlBlock {
   int need_pages;   // pages the next step allocates
   long long decoded;  // tokens decoded this round on this rank
   long long ctx_sum;  // sum over next-step rows of the attention context (kv_len + 1)
+  long long kv_read;  // sum over decode steps so far of the decoded rows' attention context
 };
 
 struct RoundDev {

@@ -50,7 +50,7 @@ class Status(ctypes.Structure):
     _fields_ = [("round_id", ctypes.c_int64), ("kind", ctypes.c_int32), ("t", ctypes.c_int32),
                 ("n_live", ctypes.c_int32), ("accepted", ctypes.c_int32), ("accepted_local", ctypes.c_int32),
                 ("done", ctypes.c_int32), ("underfilled", ctypes.c_int32), ("n_prompts_local", ctypes.c_int32),
-                ("decoded_tokens", ctypes.c_int64)]
+                ("decoded_tokens", ctypes.c_int64), ("kv_tokens_read", ctypes.c_int64)]
 
 
 class Response(ctypes.Structure):
