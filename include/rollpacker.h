@@ -189,6 +189,22 @@ int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, i
  * drain.  ids_out may be NULL to query *n_out. */
 int rp_long_queue(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out);
 
+/* Tensor-parallel decode over NVLink peer memory.  A
+ * context created with tp > 1 (d a multiple of 128) owns a device block of
+ * receive slots [2][tp][max_seqs][d] fp32 plus arrival counters.
+ * rp_tp_ipc_handle writes its CUDA IPC handle (RP_IPC_HANDLE_BYTES bytes) to
+ * `out`; after every rank of the TP group has gathered all handles (rank
+ * order, e.g. with torch.distributed), rp_tp_ipc_open maps the peers' blocks
+ * and switches decode steps to the peer path: the row-parallel O/down GEMMs
+ * push their fp32 partial tiles into every rank's slot with NVLink stores and
+ * count them with system-scope release adds, and one kernel per norm adds
+ * the partials in rank order and applies the RMSNorm (no NCCL call).  Prefill
+ * and the LM-head argmax keep NCCL.  Errors: RP_ESTATE (no peer block),
+ * RP_EBUSY (round active), RP_ECUDA (IPC mapping failed). */
+#define RP_IPC_HANDLE_BYTES 64
+int rp_tp_ipc_handle(void* ctx, void* out);
+int rp_tp_ipc_open(void* ctx, const void* handles /* tp x RP_IPC_HANDLE_BYTES */);
+
 /* Fill out[128] with a fresh ncclUniqueId (rank 0 of a DP group creates it
  * and broadcasts it, e.g. with torch.distributed, before rp_init_model). */
 int rp_nccl_unique_id(void* out);

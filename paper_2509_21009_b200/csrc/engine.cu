@@ -81,6 +81,16 @@ struct RpCtx {
   float* lnf = nullptr;
   GemmPlan p_lm{};
   int s_qkv = 1, s_o = 1, s_gu = 1, s_down = 1, s_lm = 1;
+  // tensor-parallel peer all-reduce (decode): this rank's IPC-exported block
+  // = recv [2 slots][tp][S][d] fp32 + flags [2][tp] u64, the peers' blocks
+  // mapped through CUDA IPC, per-slot use generations and CTA tickets
+  void* tp_ipc = nullptr;
+  size_t tp_recv_floats = 0;      // floats of one [tp][S][d] slot
+  void* tp_peer_base[8] = {nullptr};
+  bool tp_peer = false;
+  unsigned long long* tp_gen = nullptr;   // [2]
+  int* tp_done = nullptr;                 // [2]
+  bool peer_decode = false;               // the current forward pushes partials (final norm owes a tp_norm)
 
   // activations / workspace
   float* x = nullptr;
@@ -365,9 +375,27 @@ struct ProfScope {
 // norm weights are 1 (Z12); under TP the RMSNorm kernel runs instead.
 enum { FOLD_NONE = 0, FOLD_PRODUCE = 1, FOLD_CONSUME = 2 };
 
+// Tensor-parallel peer push of a row-parallel GEMM's fp32 output: rank q's
+// receive slot `slot` for source rank `src`, inside rank q's IPC block `base`.
+static float* tp_slot(RpCtx* c, void* base, int slot, int src) {
+  return (float*)base + (size_t)slot * c->tp_recv_floats + (size_t)src * (c->tp_recv_floats / c->tp);
+}
+static unsigned long long* tp_flags(RpCtx* c, void* base, int slot) {
+  return (unsigned long long*)((float*)base + 2 * c->tp_recv_floats) + (size_t)slot * c->tp;
+}
+
 static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, int n_host, int splits, int epi,
-                 void* out, int ldo, const float* bias, const RopeArgs* rope = nullptr, int fold = FOLD_NONE) {
+                 void* out, int ldo, const float* bias, const RopeArgs* rope = nullptr, int fold = FOLD_NONE,
+                 int push_slot = -1) {
   GemmArgs a{};
+  if (push_slot >= 0) {
+    const int me = c->rd.tp_rank;
+    a.push_n = c->tp;
+    for (int q = 0; q < c->tp; ++q) {
+      a.push_dst[q] = tp_slot(c, c->tp_peer_base[q], push_slot, me);
+      a.push_flag[q] = tp_flags(c, c->tp_peer_base[q], push_slot) + me;
+    }
+  }
   if (rope) a.rope = *rope;
   a.M = M; a.K = K; a.n_dev = n_dev; a.n_host = n_host; a.splits = splits; a.epi = epi; a.out = out; a.ldo = ldo;
   a.bias = bias; a.partial = c->gpart; a.counters = c->gctr;
@@ -404,11 +432,25 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
   static const bool no_fold = getenv("RP_NO_FOLD") != nullptr;   // A/B switch for measurements
   const bool fold = !tp && m.d % 128 == 0 && !no_fold;
   const int f_prod = fold ? FOLD_PRODUCE : FOLD_NONE, f_cons = fold ? FOLD_CONSUME : FOLD_NONE;
+  // TP decode over NVLink peer memory: the O/down GEMMs push their partials
+  // into every rank (slots 0/1) and tp_norm adds them and normalizes
+  const bool peer = tp && decode && c->tp_peer;
+  c->peer_decode = peer;
+  auto tp_norm = [&](int slot, const float* gamma, int splits) {
+    ProfScope ps(c, RP_PROF_RMSNORM);
+    void* own = c->tp_peer_base[c->rd.tp_rank];
+    launch_tp_norm(c->x, tp_slot(c, own, slot, 0), c->tp, c->tp_recv_floats / c->tp, tp_flags(c, own, slot),
+                   c->tp_gen + slot, c->tp_done + slot, m.d / 128, splits, n_dev, n_host, gamma, c->h, m.d, m.eps,
+                   c->st);
+    c->launches++;
+  };
   { ProfScope ps(c, RP_PROF_EMBED); launch_embed(tok, n_dev, n_host, c->emb, c->x, m.d, c->st); c->launches++; }
   for (int l = 0; l < m.L; ++l) {
     LayerW& w = c->layers[l];
     const int f_in = (fold && l > 0) ? FOLD_CONSUME : FOLD_NONE;
-    if (f_in == FOLD_NONE) {
+    if (peer && l > 0) {
+      tp_norm(1, w.ln1, sp_down);
+    } else if (f_in == FOLD_NONE) {
       ProfScope ps(c, RP_PROF_RMSNORM);
       launch_rmsnorm(c->x, delta, nullptr, n_dev, n_host, w.ln1, c->h, m.d, m.eps, c->st); c->launches++;
     }
@@ -430,9 +472,13 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
                        c->apart, c->atickets, m, l, decode, c->st); c->launches++; }
     { ProfScope ps(c, RP_PROF_GEMM_O);
       gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
-           nullptr, nullptr, f_prod); }
-    if (tp) tp_allreduce_rows(c, ar_rows);
-    if (!fold) {
+           nullptr, nullptr, f_prod, peer ? 0 : -1); }
+    if (peer) {
+      tp_norm(0, w.ln2, sp_o);
+    } else if (tp) {
+      tp_allreduce_rows(c, ar_rows);
+    }
+    if (!fold && !peer) {
       ProfScope ps(c, RP_PROF_RMSNORM);
       launch_rmsnorm(c->x, tp ? c->ar : nullptr, nullptr, n_dev, n_host, w.ln2, c->h, m.d, m.eps, c->st);
       c->launches++;
@@ -441,8 +487,8 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
       gemm(c, w.p_gu, 2 * m.F, m.d, n_dev, n_host, sp_gu, EPI_SWIGLU, c->mid, m.F, nullptr, nullptr, f_cons); }
     { ProfScope ps(c, RP_PROF_GEMM_DOWN);
       gemm(c, w.p_down, m.d, m.F, n_dev, n_host, sp_down, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
-           nullptr, nullptr, f_prod); }
-    if (tp) {
+           nullptr, nullptr, f_prod, peer ? 1 : -1); }
+    if (tp && !peer) {
       tp_allreduce_rows(c, ar_rows);
       delta = c->ar;
     }
@@ -457,7 +503,14 @@ static void lm_head_sample(RpCtx* c, const int* n_dev, int n_host, const int* ga
   RoundDev& R = c->R;
   // folded final norm when the rows are the residual rows in place (decode)
   const bool fold = c->tp <= 1 && !gather && c->m.d % 128 == 0 && !getenv("RP_NO_FOLD");
-  if (!fold) {
+  if (c->peer_decode && !gather) {
+    ProfScope ps(c, RP_PROF_RMSNORM);
+    void* own = c->tp_peer_base[c->rd.tp_rank];
+    launch_tp_norm(c->x, tp_slot(c, own, 1, 0), c->tp, c->tp_recv_floats / c->tp, tp_flags(c, own, 1),
+                   c->tp_gen + 1, c->tp_done + 1, c->m.d / 128, c->s_down, n_dev, n_host, c->lnf, c->h, c->m.d,
+                   c->m.eps, c->st);
+    c->launches++;
+  } else if (!fold) {
     ProfScope ps(c, RP_PROF_RMSNORM);
     launch_rmsnorm(c->x, pending ? c->ar : nullptr, gather, n_dev, n_host, c->lnf, c->h, c->m.d, c->m.eps, c->st);
     c->launches++;
@@ -679,6 +732,17 @@ static int init_impl(RpCtx* c) {
   c->h_ctl->done = 1;
   CK(cudaMemcpyAsync(c->R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
 
+  // ---- TP peer block (exported with CUDA IPC; rp_tp_ipc_open enables it)
+  if (c->tp > 1 && c->tp <= 8 && d % 128 == 0) {
+    c->tp_recv_floats = (size_t)c->tp * c->z.S * d;
+    const size_t bytes = 2 * c->tp_recv_floats * sizeof(float) + 2 * (size_t)c->tp * sizeof(unsigned long long);
+    CK(cudaMalloc(&c->tp_ipc, bytes));
+    CK(cudaMemset(c->tp_ipc, 0, bytes));
+    CK(cudaMalloc(&c->tp_gen, 2 * sizeof(unsigned long long) + 2 * sizeof(int)));
+    CK(cudaMemset(c->tp_gen, 0, 2 * sizeof(unsigned long long) + 2 * sizeof(int)));
+    c->tp_done = (int*)(c->tp_gen + 2);
+  }
+
   // ---- NCCL
   if (rd->world > 1 || c->tp > 1) {   // DP cutoff exchange or TP all-reduces
     ncclUniqueId id;
@@ -726,6 +790,10 @@ void rp_free(void* ctx) {
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->trace_dev) cudaFree(c->trace_dev);
   if (c->comm) ncclCommDestroy(c->comm);
+  for (int q = 0; q < 8; ++q)
+    if (c->tp_peer_base[q] && c->tp_peer_base[q] != c->tp_ipc) cudaIpcCloseMemHandle(c->tp_peer_base[q]);
+  if (c->tp_ipc) cudaFree(c->tp_ipc);
+  if (c->tp_gen) cudaFree(c->tp_gen);
   if (c->own_stream) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -1046,6 +1114,35 @@ int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, i
       }
   c->active = false;
   c->collected = true;
+  return RP_OK;
+}
+
+int rp_tp_ipc_handle(void* ctx, void* out) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c || !out) return RP_EINVAL;
+  if (!c->tp_ipc) return c->fail(RP_ESTATE, "no TP peer block (tp == 1 or d % 128 != 0)");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->tp_ipc));
+  memcpy(out, &h, sizeof h);
+  return RP_OK;
+}
+
+int rp_tp_ipc_open(void* ctx, const void* handles) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c || !handles) return RP_EINVAL;
+  if (!c->tp_ipc) return c->fail(RP_ESTATE, "no TP peer block");
+  if (c->active) return c->fail(RP_EBUSY, "a round is active");
+  for (int q = 0; q < c->tp; ++q) {
+    if (q == c->rd.tp_rank) { c->tp_peer_base[q] = c->tp_ipc; continue; }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char*)handles + (size_t)q * RP_IPC_HANDLE_BYTES, sizeof h);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return c->fail(RP_ECUDA, "cudaIpcOpenMemHandle(rank %d): %s", q, cudaGetErrorString(e));
+    c->tp_peer_base[q] = p;
+  }
+  c->tp_peer = true;
+  c->graph_dirty = true;
   return RP_OK;
 }
 

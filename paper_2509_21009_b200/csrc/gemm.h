@@ -46,6 +46,13 @@ struct GemmArgs {
   const float* ssq_in;
   int ssq_parts, ssq_stride;
   float norm_inv_d, norm_eps;
+  // Tensor-parallel push (decode, row-parallel O/down): an F32 output tile is
+  // written to push_dst[q] (rank q's receive slot for this rank, row stride
+  // ldo; q = 0..push_n-1, local or NVLink peer memory) instead of `out`, then
+  // each finished output unit adds 1 to push_flag[q] (system-scope release).
+  float* push_dst[8];
+  unsigned long long* push_flag[8];
+  int push_n;
 };
 
 struct GemmPlan {

@@ -176,6 +176,17 @@ __device__ __forceinline__ void reduce_splits_loop(float4 (&acc)[RU], const floa
   }
 }
 
+// Tensor-parallel push: this output unit's stores (local and NVLink peer) are
+// released at system scope, then every destination's counter is bumped.
+__device__ __forceinline__ void push_signal(const GemmArgs& a, int et) {
+  if (!a.push_n) return;
+  __threadfence_system();
+  named_bar(1, 128);
+  if (et == 0)
+    for (int q = 0; q < a.push_n; ++q)
+      asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(a.push_flag[q]) : "memory");
+}
+
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB16,
                     const __grid_constant__ CUtensorMap tmB64, const __grid_constant__ CUtensorMap tmB256,
@@ -564,7 +575,11 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               }
             } else if (a.epi == EPI_F32) {
               v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
-              *(float4*)((float*)a.out + o) = v;
+              if (a.push_n) {
+                for (int q = 0; q < a.push_n; ++q) *(float4*)(a.push_dst[q] + o) = v;
+              } else {
+                *(float4*)((float*)a.out + o) = v;
+              }
             } else {
               __nv_bfloat162* ob = (__nv_bfloat162*)((__nv_bfloat16*)a.out + o);
               ob[0] = __floats2bfloat162_rn(v.x + bb.x, v.y + bb.y);
@@ -573,6 +588,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           }
         }
         if (et == 0 && local == 0) TL(13);        // reduction + epilogue done
+        push_signal(a, et);
         if (coop) {
           // second counter: the last split CTA of the tile to finish resets both
           __threadfence();
@@ -663,7 +679,11 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 if (lane == 0) a.ssq_out[(size_t)(n0 + c0 + n) * a.ssq_stride + I.tile] = ss;
               }
             } else if (a.epi == EPI_F32) {
-              *(float4*)((float*)a.out + o) = val;
+              if (a.push_n) {
+                for (int q = 0; q < a.push_n; ++q) *(float4*)(a.push_dst[q] + o) = val;
+              } else {
+                *(float4*)((float*)a.out + o) = val;
+              }
             } else {
               __nv_bfloat162* ob = (__nv_bfloat162*)((__nv_bfloat16*)a.out + o);
               ob[0] = __floats2bfloat162_rn(val.x, val.y);
@@ -677,6 +697,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         tc_fence_before();
         mbar_arrive(tempty0 + 8 * acc);     // all TMEM reads of this item done
       }
+      push_signal(a, et);
       if (et == 0 && local < 3) TL(8 + local);
     }
   }
@@ -735,6 +756,10 @@ int gemm_pick_splits(int M, int K, int n_sms) {
   double best_cost = 1e30;
   for (int s = 1; s <= 16 && s <= kb; ++s) {
     const int items = tiles * s;
+    // split-K only within one wave: a multi-wave split (ticket reduction,
+    // partial traffic, uneven waves) measured slower than no split, e.g.
+    // 13824 x 5120 at N=136: 4 splits 58.6 us vs none 45.0 us
+    if (s > 1 && items > n_sms) break;
     const double waves = (double)((items + n_sms - 1) / n_sms);
     const double cost = waves * ((kb + s - 1) / s + 4) + (s > 1 ? 2.0 : 0.0);
     if (cost < best_cost - 1e-9) { best_cost = cost; best = s; }

@@ -127,6 +127,100 @@ void launch_rmsnorm(float* x, const float* delta, const int* gather, const int* 
              (__nv_bfloat16*)h, d, eps);
 }
 
+// --------------------------------------------------- TP add + RMSNorm (peer)
+// Tensor-parallel decode: the row-parallel GEMM of every rank pushed its fp32
+// partial into recv[src] of this rank (NVLink stores, gemm_tcgen05 push) and
+// counted its finished output units in flags[src].  Wait until every source
+// delivered this use's units, then x[r] += sum_src recv[src][r] in rank order
+// (identical bits on every rank), write x back and h = bf16(x / rms * gamma).
+// gen = output units of this slot consumed so far on this rank (cumulative:
+// the units per use depend on the live count); the last CTA advances it.
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void tp_norm_kernel(float* x, const float* recv, int tp, size_t src_stride,
+                               const unsigned long long* flags, unsigned long long* gen, int* done, int m_tiles,
+                               int splits, const int* n_dev, const float* gamma, __nv_bfloat16* h, int d, float eps) {
+  __shared__ float red[32];
+  __shared__ unsigned long long s_units;
+  pdl_wait();
+  pdl_launch_dependents();
+  const int n = *n_dev;
+  if (n <= 0) return;
+  if (threadIdx.x == 0) {
+    // output units the producer GEMM signals per use (its cooperative
+    // split-K reduction finishes one column slice per split)
+    const int n_chunks = (n + 255) / 256;
+    const bool coop = splits > 1 && m_tiles * n_chunks * splits <= 148 && min(256, n) >= 96;
+    const unsigned long long units = (unsigned long long)m_tiles * n_chunks * (coop ? splits : 1);
+    const unsigned long long target = *(volatile unsigned long long*)gen + units;
+    s_units = units;
+    for (int q = 0; q < tp; ++q) {
+      uint32_t spins = 0;
+      while (ld_acquire_sys_u64(flags + q) < target) {
+        if (++spins == (1u << 28)) {
+          printf("rollpacker watchdog: TP peer partial stuck (rank slot %d, %llu < %llu)\n", q,
+                 ld_acquire_sys_u64(flags + q), target);
+          __trap();
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    float4* xr = (float4*)(x + (size_t)r * d);
+    float ss = 0.f;
+    for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+      float4 s = __ldcg((const float4*)(recv + (size_t)r * d) + c);
+      for (int q = 1; q < tp; ++q) {
+        const float4 a = __ldcg((const float4*)(recv + q * src_stride + (size_t)r * d) + c);
+        s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
+      }
+      float4 v = xr[c];
+      v.x += s.x; v.y += s.y; v.z += s.z; v.w += s.w;
+      xr[c] = v;
+      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+      v = warp_sum(v);
+      if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
+    __syncthreads();
+    __nv_bfloat162* hr = (__nv_bfloat162*)(h + (size_t)r * d);
+    const float4* g4 = (const float4*)gamma;
+    for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+      float4 v = xr[c], g = g4[c];
+      hr[2 * c] = __floats2bfloat162_rn(v.x * inv * g.x, v.y * inv * g.y);
+      hr[2 * c + 1] = __floats2bfloat162_rn(v.z * inv * g.z, v.w * inv * g.w);
+    }
+  }
+  // this use of the slot is consumed once every CTA is past its reads
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
+      *done = 0;
+      *gen += s_units;
+    }
+  }
+}
+
+void launch_tp_norm(float* x, const float* recv, int tp, size_t src_stride, const unsigned long long* flags,
+                    unsigned long long* gen, int* done, int m_tiles, int splits, const int* n_dev, int n_rows_grid,
+                    const float* gamma, void* h, int d, float eps, cudaStream_t st) {
+  launch_pdl(tp_norm_kernel, dim3(row_grid(n_dev, n_rows_grid)), dim3(256), 0, st, x, recv, tp, src_stride, flags, gen,
+             done, m_tiles, splits, n_dev, gamma, (__nv_bfloat16*)h, d, eps);
+}
+
 // -------------------------------------------------------- RoPE + KV append
 // qkv row r (fp32, bias already added): [q heads | k heads | v heads] x hd.
 // Rotate-half RoPE at position row_pos[r] (angle in fp64, then fp32 sincos

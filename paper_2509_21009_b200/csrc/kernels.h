@@ -78,6 +78,10 @@ void launch_init_weights(void* out, long long rows, int cols, long long r0, int 
 void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb, float* x, int d, cudaStream_t st);
 void launch_rmsnorm(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
                     const float* gamma, void* h, int d, float eps, cudaStream_t st);
+void launch_tp_norm(float* x, const float* recv /* [tp][rows][d] slot base */, int tp, size_t src_stride,
+                    const unsigned long long* flags /* [tp] */, unsigned long long* gen, int* done, int m_tiles,
+                    int splits, const int* n_dev, int n_rows_grid, const float* gamma, void* h, int d, float eps,
+                    cudaStream_t st);
 void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const int* row_pos, const int* row_pt,
                         const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
                         const double* inv_freq, cudaStream_t st);

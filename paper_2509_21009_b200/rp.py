@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "librollpacker.so")
 RP_OK, RP_EINVAL, RP_EBUSY, RP_ESTATE, RP_ENOMEM_KV, RP_ECUDA, RP_ENCCL, RP_ENOSPC = 0, -1, -2, -3, -4, -5, -6, -7
 RP_SHORT, RP_LONG, RP_TRACE = 0, 1, 4
 RP_FINISH_EOS, RP_FINISH_CAP = 1, 2
+RP_IPC_HANDLE_BYTES = 64
 
 
 class ModelDesc(ctypes.Structure):
@@ -60,7 +61,8 @@ class Response(ctypes.Structure):
 
 EXPORTS = ["rp_query_sizes", "rp_init_model", "rp_submit_round", "rp_step", "rp_collect", "rp_long_queue",
            "rp_free", "rp_last_error", "rp_launch_count", "rp_debug_logits", "rp_debug_trace_enable",
-           "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm", "rp_debug_profile", "rp_nccl_unique_id"]
+           "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm", "rp_debug_profile", "rp_nccl_unique_id",
+           "rp_tp_ipc_handle", "rp_tp_ipc_open"]
 
 
 def load_library(path=LIB_PATH):
@@ -90,6 +92,8 @@ def load_library(path=LIB_PATH):
     lib.rp_debug_profile.argtypes = [P, I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64),
                                      ctypes.POINTER(I64)]
     lib.rp_nccl_unique_id.argtypes = [P]
+    lib.rp_tp_ipc_handle.argtypes = [P, P]
+    lib.rp_tp_ipc_open.argtypes = [P, P]
     for name in EXPORTS:
         if name not in ("rp_free", "rp_last_error", "rp_launch_count"):
             getattr(lib, name).restype = I32
@@ -138,7 +142,7 @@ class Engine:
 
     def __init__(self, cfg, max_seqs, max_prompts, max_prompt_len, max_prompt_tokens, max_cap, kv_pool_bytes=None,
                  kv_fraction=0.85, weight_seed=0, sample_seed=3, temperature=1.0, graph_steps=16, rank=0, world=1,
-                 nccl_id=None, stream=None, tp=1, tp_rank=0):
+                 nccl_id=None, stream=None, tp=1, tp_rank=0, tp_peer=True):
         import torch
         self.torch = torch
         self.L = lib()
@@ -182,6 +186,25 @@ class Engine:
         torch.cuda.synchronize()
         self._check(self.L.rp_init_model(ctypes.byref(self.md), ctypes.byref(rd), ctypes.byref(h)), None)
         self.h = h
+        self.tp_peer = False
+        if tp > 1 and tp_peer:
+            self._open_tp_peers()
+
+    def _open_tp_peers(self):
+        """TP decode over NVLink peer memory: gather every rank's IPC handle
+        of its receive block over the host process group (which must be the
+        TP group, ranks in TP order) and map the peers."""
+        import torch.distributed as dist
+        if not dist.is_initialized() or dist.get_world_size() != self.tp:
+            return
+        hb = ctypes.create_string_buffer(RP_IPC_HANDLE_BYTES)
+        if self.L.rp_tp_ipc_handle(self.h, hb) != RP_OK:
+            return                                   # shape without a peer block: NCCL all-reduce path
+        allh = [None] * self.tp
+        dist.all_gather_object(allh, hb.raw)
+        joined = ctypes.create_string_buffer(b"".join(allh), RP_IPC_HANDLE_BYTES * self.tp)
+        self._check(self.L.rp_tp_ipc_open(self.h, joined))
+        self.tp_peer = True
 
     # ------------------------------------------------------------------ utils
     def _check(self, rc, h="self"):

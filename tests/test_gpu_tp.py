@@ -26,9 +26,27 @@ def main():
     dist.broadcast_object_list(obj, src=0)
     cfg = configs.model_config("tiny")
     w = weights.Weights(cfg, configs.WEIGHT_SEED)
-    eng = rp.Engine(cfg, max_seqs=64, max_prompts=16, max_prompt_len=128, max_prompt_tokens=1024, max_cap=512,
-                    kv_pool_bytes=64 << 20, graph_steps=4, tp=world, tp_rank=rank, nccl_id=obj[0])
     ok = True
+    # decode all-reduce over NVLink peer memory (default), then the NCCL path
+    for peer in (True, False):
+        ok &= run_checks(rp, gen, sched, decoder, sampler, dist, cfg, w, world, rank, obj[0], peer)
+    flag = torch.tensor([1 if ok else 0])
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    dist.destroy_process_group()
+    if rank == 0:
+        print("TP PARITY", "PASS" if flag.item() == 1 else "FAIL")
+    sys.exit(0 if flag.item() == 1 else 1)
+
+
+def run_checks(rp, gen, sched, decoder, sampler, dist, cfg, w, world, rank, nccl_id, peer):
+    if not peer:
+        obj = [rp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    eng = rp.Engine(cfg, max_seqs=64, max_prompts=16, max_prompt_len=128, max_prompt_tokens=1024, max_cap=512,
+                    kv_pool_bytes=64 << 20, graph_steps=4, tp=world, tp_rank=rank, nccl_id=nccl_id, tp_peer=peer)
+    ok = eng.tp_peer == peer
+    print("rank %d decode all-reduce: %s" % (rank, "NVLink peer push" if eng.tp_peer else "NCCL"), flush=True)
     # 1. teacher-forced logits, gathered over the vocab shards
     toks = gen.prompts(1, 0, cfg["eos_id"], (70, 70), 9)[0]["tokens"]
     part = eng.debug_logits(toks)
@@ -72,12 +90,7 @@ def main():
         rank, sched_ok, same, checked, mism, gap_ok), flush=True)
     ok &= sched_ok and same and gap_ok and len(res) == n * G
     eng.close()
-    flag = torch.tensor([1 if ok else 0])
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-    dist.destroy_process_group()
-    if rank == 0:
-        print("TP PARITY", "PASS" if flag.item() == 1 else "FAIL")
-    sys.exit(0 if flag.item() == 1 else 1)
+    return ok
 
 
 if __name__ == "__main__":

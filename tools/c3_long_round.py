@@ -1,0 +1,116 @@
+"""a Qwen2.5-14B-shaped long round under tensor
+parallelism (row a14, elastic TP).  Run under torchrun on N GPUs (N = 2 or 4):
+
+  python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
+      tools/c3_long_round.py [--p0 32] [--cap 32768] [--out gpurun_out/c3_tp2.json]
+
+Long-prompt queue recipe: the C2 trace generator (mu0 6.0,
+sigma_p 0.6, sigma_r 0.85) with L_max = 32768; the queue holds the first P0
+prompts whose first attempt has a response longer than the short cap (8192)
+-- prompts every short round defers -- and the long round decodes their
+re-rolls (trace attempt 1, reading Z5) with speculation disabled, every
+response retained and truncated at the cap.  Reports
+decoded tokens / device second, ms per decode step and the step count
+(rank 0 prints one JSON line).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--p0", type=int, default=32)
+    ap.add_argument("--cap", type=int, default=32768)
+    ap.add_argument("--short-cap", type=int, default=8192)
+    ap.add_argument("--out", default="")
+    ap.add_argument("--profile-steps", type=int, default=0,
+                    help="after 1000 graph steps, time this many eager steps per kernel class (not timed run)")
+    a = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+    from paper_2509_21009_b200 import rp
+    from synth import configs, gen
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = configs.model_config("qwen2.5-14b")
+    G = 8
+    lo, hi = 256, 768
+    n_pool = 4000
+    tr = gen.length_trace(n_pool, G, 6.0, 0.6, 0.85, 32768, configs.TRACE_SEED)
+    queue = [int(i) for i in np.nonzero(tr[:, 0, :].max(axis=1) > a.short_cap)[0][:a.p0]]
+    ps_all = gen.prompts(n_pool, 0, cfg["eos_id"], (lo, hi), configs.PROMPT_SEED)
+    prompts = [ps_all[i] for i in queue]
+    L = tr[queue, 1, :]
+    nccl_id = None
+    if world > 1:
+        obj = [rp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    eng = rp.Engine(cfg, max_seqs=a.p0 * G, max_prompts=a.p0, max_prompt_len=hi, max_prompt_tokens=a.p0 * hi,
+                    max_cap=a.cap, graph_steps=16, tp=world, tp_rank=rank, nccl_id=nccl_id,
+                    sample_seed=configs.SAMPLE_SEED, kv_fraction=0.85)
+    # warm-up: a short long-round of 2 prompts (graph capture, NCCL setup)
+    eng.submit(prompts[:2], G, 64, 2, long_round=True, trace=np.minimum(L[:2], 64), round_id=999)
+    eng.run()
+    eng.collect()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(eng.stream)
+    eng.submit(prompts, G, a.cap, len(prompts), long_round=True, trace=L, round_id=1)
+    prof = None
+    if a.profile_steps:
+        st = eng.step(1000)
+        eng.debug_profile_arm(a.profile_steps)
+        st = eng.step(a.profile_steps)
+        prof = eng.debug_profile_read()
+        eng.debug_profile_arm(-1)
+    st = eng.run()
+    res = eng.collect()
+    e1.record(eng.stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    dev = e0.elapsed_time(e1) / 1e3
+    t = torch.tensor([dev, wall], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev, wall = t.tolist()
+    ok = (len(res) == len(prompts) * G and
+          all(r["len"] == min(int(L[queue.index(r["prompt_id"])][r["j"]]), a.cap) for r in res))
+    if rank == 0:
+        line = dict(config="C3 qwen2.5-14b-shaped long round", tp=world, p0=len(prompts), G=G, cap=a.cap,
+                    steps=st.t, decoded_tokens=st.decoded_tokens, retained=sum(r["len"] for r in res),
+                    kv_tokens_read=st.kv_tokens_read, dev_s=round(dev, 3), wall_s=round(wall, 3),
+                    tokens_per_s=round(st.decoded_tokens / dev, 1), ms_per_step=round(1e3 * dev / st.t, 3),
+                    lengths_match_trace=bool(ok), max_len=int(min(L.max(), a.cap)),
+                    queue_recipe="first %d prompts with a first-attempt response > %d (trace mu0 6.0, L_max 32768)" % (
+                        len(prompts), a.short_cap))
+        if prof:
+            n = max(1, prof["steps"])
+            line["profile"] = dict(rows=round(prof["rows"] / n, 1), ctx=round(prof["ctx"] / max(1, prof["rows"]), 0),
+                                   ms_per_step={k: round(v / n, 3) for k, v in prof["ms"].items() if v > 0})
+            line["note"] = "profiled run: eager steps inside the round, dev_s not a clean timing"
+        print(json.dumps(line), flush=True)
+        if a.out:
+            json.dump(line, open(a.out, "w"), indent=1)
+    eng.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
