@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--profile-steps", type=int, default=24)
     ap.add_argument("--max-rounds-steps", type=int, default=0, help="debug: cap decode steps per round (invalid)")
     ap.add_argument("--out", default="")
+    ap.add_argument("--long-tp", default="auto", choices=["auto", "1", "n"],
+                    help="long-round tensor parallelism: auto = smallest TP whose worst-case KV fits (planner), "
+                         "1 = data-parallel replicas, n = one TP group over all GPUs")
     return ap.parse_args()
 
 
@@ -146,16 +149,22 @@ def run_ours(a):
         obj = [rp.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+    # Long-round parallelism (elastic TP; the static form of the
+    # planner): the smallest TP size whose worst-case KV --
+    # every sequence of a replica's share at prompt + cap tokens -- fits the
+    # per-GPU pool without preemption.  TP=1 means the N GPUs run data-parallel
+    # replicas of the long round (each decodes its slice of the P0 prompts).
+    long_tp = plan_long_tp(a.long_tp, cfg, W, world)
     # short rounds: data parallel over the N GPUs (prompts sharded by index)
     eng = rp.Engine(cfg, max_seqs=n_loc * G, max_prompts=n_loc, max_prompt_len=hi, max_prompt_tokens=n_loc * hi,
                     max_cap=max(W.R["short_cap"], W.R["long_cap"]), graph_steps=a.graph_steps, rank=rank,
                     world=world, nccl_id=nccl_id, sample_seed=configs.SAMPLE_SEED,
-                    kv_fraction=0.85 if world == 1 else 0.45)
+                    kv_fraction=0.85 if long_tp == 1 else 0.45)
     st_ev = eng.stream
     # long rounds (elastic TP): one TP=N group over the same GPUs,
     # holding only its weight shard; every rank decodes all P0 queued prompts
     eng_long = eng
-    if world > 1 and cfg["n_kv_heads"] % world == 0:
+    if long_tp > 1:
         obj = [rp.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         eng_long = rp.Engine(cfg, max_seqs=W.P0 * G, max_prompts=W.P0, max_prompt_len=hi,
@@ -273,7 +282,9 @@ def run_ours(a):
                                    W.R["n_submit"], G, W.R["short_cap"]),
                    "global_prompts_per_short_round": W.n_submit, "P0": W.P0, "G": G,
                    "short_cap": W.R["short_cap"], "long_cap": W.R["long_cap"],
-                   "parallelism": "short rounds dp%d, long rounds tp%d" % (world, world if eng_long is not eng else 1), "l2": "inputs larger than L2 (15 GB weights streamed per step)",
+                   "parallelism": "short rounds dp%d, long rounds %s" % (
+                       world, ("tp%d" % long_tp) if eng_long is not eng else "dp%d (planner: TP=1 fits the worst-case KV)" % world),
+                   "l2": "inputs larger than L2 (14 GB of weights streamed per decode step)",
                    "graph_steps": a.graph_steps},
         "per_gpu_tokens_per_s": round(value / world, 1),
         "retained_tokens_per_s": round(retained / dev_s, 1),
@@ -303,6 +314,31 @@ def run_ours(a):
         with open(a.out, "w") as f:
             f.write(json.dumps(line) + "\n")
     shutdown()
+
+
+def plan_long_tp(choice, cfg, W, world):
+    """Long-round TP size: 1, the whole group, or (auto) the smallest of
+    {1, world} whose worst-case KV per GPU fits ~80% of the memory left after
+    that TP size's weight shard."""
+    can_tp = world > 1 and cfg["n_kv_heads"] % world == 0
+    if choice == "1" or world == 1:
+        return 1
+    if choice == "n":
+        return world if can_tp else 1
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    hi = W.R["prompt_len"][1]
+    per_tok = cfg["n_layers"] * cfg["n_kv_heads"] * cfg["head_dim"] * 2 * 2
+    for t in ([1, world] if can_tp else [1]):
+        prompts = -(-W.P0 // (world // t))
+        need = prompts * W.G * (hi + W.R["long_cap"]) * per_tok / t
+        # t = 1: one engine holds the full weights; t > 1: the DP engine's full
+        # weights plus the TP shard
+        full = weight_bytes(cfg, 1) + cfg["vocab"] * cfg["d_model"] * 2
+        weights = full if t == 1 else full + weight_bytes(cfg, t)
+        if need <= 0.8 * (free - weights):
+            return t
+    return world if can_tp else 1
 
 
 def weight_bytes(cfg, tp=1):
