@@ -94,6 +94,18 @@ def main():
             lines.append("%-40s %6d launches  %8.1f us mean  share %5.1f%%" % (k[:40], v["launches"], v["mean_us"],
                                                                              100 * v["share"]))
     open(os.path.join(ROOT, "profiles", "%s_ncu_digest.txt" % tag), "w").write("\n".join(lines) + "\n")
+    # per-kernel DRAM traffic per launch (bench.py roofline.traffic): the
+    # captures hold the first six GEMM/attention launches of one decode step
+    order = ["gemm_qkv", "attention", "gemm_o", "gemm_gu", "gemm_down", "gemm_qkv_next_layer"]
+    traffic = {}
+    for label, recs in summary["reports"].items():
+        shape = os.environ.get("SHAPE_" + label, label)
+        traffic["%s_%s" % (tag, label)] = {
+            "shape": shape, "source": "profiles/%s_ncu_summary.json (ncu --set full, one decode step)" % tag,
+            "dram_bytes_per_launch": {k: r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0)
+                                      for k, r in zip(order, recs)},
+            "ncu_duration_us": {k: 1e6 * r.get("gpu__time_duration.sum", 0) for k, r in zip(order, recs)}}
+    json.dump(traffic, open(os.path.join(ROOT, "profiles", "%s_ncu_traffic.json" % tag), "w"), indent=1)
     print("\n".join(lines))
 
 
