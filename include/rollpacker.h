@@ -185,6 +185,19 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st);
 int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, int64_t tok_cap, int32_t* n_out,
                int64_t* n_tok);
 
+/* Streaming collect (completed prompts go to the
+ * reward / trainer stages while the round continues).  Between rp_step calls
+ * of an active round (or after it is done, before rp_collect), fills out[]
+ * with the retained responses of this rank's accepted prompts whose
+ * acceptance index (local, 0-based) is in [first, accepted so far), in the
+ * order rp_collect would return them; *n_accepted receives the accepted
+ * count (pass it as `first` next time).  An accepted prompt's responses are
+ * final, so a streamed response never changes; the round stays active and
+ * rp_collect still returns everything and closes it.  out == NULL queries
+ * sizes.  Errors: RP_ESTATE (no round), RP_EINVAL (first), RP_ENOSPC. */
+int rp_collect_ready(void* ctx, int32_t first, rp_response* out, int32_t max_out, int32_t* tok_buf, int64_t tok_cap,
+                     int32_t* n_out, int64_t* n_tok, int32_t* n_accepted);
+
 /* Snapshot of the long-prompt queue (global prompt ids, oldest first); no
  * drain.  ids_out may be NULL to query *n_out. */
 int rp_long_queue(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out);

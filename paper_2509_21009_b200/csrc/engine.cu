@@ -1073,16 +1073,14 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
   return RP_OK;
 }
 
-int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, int64_t tok_cap, int32_t* n_out,
-               int64_t* n_tok) {
-  RpCtx* c = (RpCtx*)ctx;
-  if (!c) return RP_EINVAL;
-  if (!c->active) return c->fail(RP_ESTATE, "no active round");
-  int rc = read_ctl(c);
-  if (rc) return rc;
-  if (!c->h_ctl->done) return c->fail(RP_ESTATE, "round not done");
-  const int acc = c->h_ctl->acc_local, nr = acc * c->keep;
-  launch_collect_pack(c->R, c->col_meta, c->col_tok, c->st);
+// Pack the responses of this rank's accepted prompts with acceptance index
+// in [first, accepted so far) and copy them to the host (shared by rp_collect
+// and rp_collect_ready).  n_out / n_tok may be queried with out == NULL.
+static int collect_range(RpCtx* c, int first, rp_response* out, int32_t max_out, int32_t* tok_buf, int64_t tok_cap,
+                         int32_t* n_out, int64_t* n_tok, std::vector<char>* accepted) {
+  const int acc = c->h_ctl->acc_local;
+  const int nr = std::max(0, acc - first) * c->keep;
+  launch_collect_pack(c->R, first, c->col_meta, c->col_tok, c->st);
   c->launches += 2;
   std::vector<int> meta((size_t)4 * nr + nr + 1);
   CK(cudaMemcpyAsync(meta.data(), c->col_meta, (size_t)4 * nr * 4, cudaMemcpyDeviceToHost, c->st));
@@ -1096,16 +1094,29 @@ int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, i
   if (max_out < nr || tok_cap < total || !tok_buf) return c->fail(RP_ENOSPC, "collect buffers too small");
   if (total > 0) CK(cudaMemcpyAsync(tok_buf, c->col_tok, total * 4, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  std::vector<char> accepted(c->n_loc, 0);
   for (int r = 0; r < nr; ++r) {
     const int p = meta[4 * r];
-    accepted[p] = 1;
+    if (accepted) (*accepted)[p] = 1;
     out[r].prompt_id = c->round_prompts[p].id;
     out[r].j = meta[4 * r + 1];
     out[r].len = meta[4 * r + 2];
     out[r].finish = meta[4 * r + 3] == ST_CAPPED ? RP_FINISH_CAP : RP_FINISH_EOS;
     out[r].tok_off = meta[4 * nr + r];
   }
+  return RP_OK;
+}
+
+int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, int64_t tok_cap, int32_t* n_out,
+               int64_t* n_tok) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (!c->active) return c->fail(RP_ESTATE, "no active round");
+  int rc = read_ctl(c);
+  if (rc) return rc;
+  if (!c->h_ctl->done) return c->fail(RP_ESTATE, "round not done");
+  std::vector<char> accepted(c->n_loc, 0);
+  if ((rc = collect_range(c, 0, out, max_out, tok_buf, tok_cap, n_out, n_tok, &accepted))) return rc;
+  if (!out) return RP_OK;
   if (c->kind == 0)
     for (int p = 0; p < c->n_loc; ++p)
       if (!accepted[p]) {
@@ -1115,6 +1126,18 @@ int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, i
   c->active = false;
   c->collected = true;
   return RP_OK;
+}
+
+int rp_collect_ready(void* ctx, int32_t first, rp_response* out, int32_t max_out, int32_t* tok_buf, int64_t tok_cap,
+                     int32_t* n_out, int64_t* n_tok, int32_t* n_accepted) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (!c->active) return c->fail(RP_ESTATE, "no active round");
+  int rc = read_ctl(c);
+  if (rc) return rc;
+  if (first < 0 || first > c->h_ctl->acc_local) return c->fail(RP_EINVAL, "invalid field: first");
+  if (n_accepted) *n_accepted = c->h_ctl->acc_local;
+  return collect_range(c, first, out, max_out, tok_buf, tok_cap, n_out, n_tok, nullptr);
 }
 
 int rp_tp_ipc_handle(void* ctx, void* out) {

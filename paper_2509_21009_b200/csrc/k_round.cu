@@ -318,16 +318,16 @@ __device__ __forceinline__ int retained_slot(const RoundDev& R, int r) {
   return p * R.G;   // unreachable: an accepted prompt has keep retained responses
 }
 
-__global__ void collect_offsets_kernel(RoundDev R, int* meta, int* offs) {
+__global__ void collect_offsets_kernel(RoundDev R, int first, int* meta, int* offs) {
   __shared__ int scan_sm[40];
   const int acc = R.ctl->acc_local;
-  const int nr = acc * R.keep;
+  const int nr = max(0, acc - first) * R.keep;
   int base_off = 0;
   for (int base = 0; base < nr; base += blockDim.x) {
     const int r = base + threadIdx.x;
     int len = 0;
     if (r < nr) {
-      const int s = retained_slot(R, r), p = R.slot_prompt[s], j = R.slot_j[s];
+      const int s = retained_slot(R, first * R.keep + r), p = R.slot_prompt[s], j = R.slot_j[s];
       len = R.gen[s];
       meta[4 * r] = p; meta[4 * r + 1] = j; meta[4 * r + 2] = len; meta[4 * r + 3] = R.status[s];
     }
@@ -339,20 +339,20 @@ __global__ void collect_offsets_kernel(RoundDev R, int* meta, int* offs) {
   if (threadIdx.x == 0) offs[nr] = base_off;
 }
 
-__global__ void collect_copy_kernel(RoundDev R, const int* offs, int* tokens) {
-  const int nr = R.ctl->acc_local * R.keep;
+__global__ void collect_copy_kernel(RoundDev R, int first, const int* offs, int* tokens) {
+  const int nr = max(0, R.ctl->acc_local - first) * R.keep;
   for (int r = blockIdx.x; r < nr; r += gridDim.x) {
-    const int s = retained_slot(R, r);
+    const int s = retained_slot(R, first * R.keep + r);
     const int len = R.gen[s];
     for (int k = threadIdx.x; k < len; k += blockDim.x) tokens[offs[r] + k] = R.tok_out[(size_t)s * R.cap + k];
   }
 }
 
-void launch_collect_pack(const RoundDev& R, int* meta, int* tokens, cudaStream_t st) {
+void launch_collect_pack(const RoundDev& R, int first, int* meta, int* tokens, cudaStream_t st) {
   // offs lives right after meta: meta has 4*S ints, offs S+1
   int* offs = meta + 4 * R.S;
-  collect_offsets_kernel<<<1, 1024, 0, st>>>(R, meta, offs);
-  collect_copy_kernel<<<148, 256, 0, st>>>(R, offs, tokens);
+  collect_offsets_kernel<<<1, 1024, 0, st>>>(R, first, meta, offs);
+  collect_copy_kernel<<<148, 256, 0, st>>>(R, first, offs, tokens);
 }
 
 }  // namespace rp

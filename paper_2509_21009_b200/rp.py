@@ -62,7 +62,7 @@ class Response(ctypes.Structure):
 EXPORTS = ["rp_query_sizes", "rp_init_model", "rp_submit_round", "rp_step", "rp_collect", "rp_long_queue",
            "rp_free", "rp_last_error", "rp_launch_count", "rp_debug_logits", "rp_debug_trace_enable",
            "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm", "rp_debug_profile", "rp_nccl_unique_id",
-           "rp_tp_ipc_handle", "rp_tp_ipc_open"]
+           "rp_tp_ipc_handle", "rp_tp_ipc_open", "rp_collect_ready"]
 
 
 def load_library(path=LIB_PATH):
@@ -94,6 +94,8 @@ def load_library(path=LIB_PATH):
     lib.rp_nccl_unique_id.argtypes = [P]
     lib.rp_tp_ipc_handle.argtypes = [P, P]
     lib.rp_tp_ipc_open.argtypes = [P, P]
+    lib.rp_collect_ready.argtypes = [P, I32, ctypes.POINTER(Response), I32, ctypes.POINTER(I32), I64,
+                                     ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I32)]
     for name in EXPORTS:
         if name not in ("rp_free", "rp_last_error", "rp_launch_count"):
             getattr(lib, name).restype = I32
@@ -277,6 +279,21 @@ class Engine:
             res.append(dict(prompt_id=r.prompt_id, j=r.j, len=r.len, finish=r.finish,
                             tokens=toks[r.tok_off:r.tok_off + r.len].copy()))
         return res
+
+    def collect_ready(self, first):
+        """Streaming collect: responses of the prompts accepted with local
+        acceptance index >= first so far (the round stays active).  Returns
+        (responses, accepted count to pass as `first` next time)."""
+        n, nt, na = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32()
+        self._check(self.L.rp_collect_ready(self.h, first, None, 0, None, 0, ctypes.byref(n), ctypes.byref(nt),
+                                            ctypes.byref(na)))
+        out = (Response * max(1, n.value))()
+        toks = np.zeros(max(1, nt.value), dtype=np.int32)
+        self._check(self.L.rp_collect_ready(self.h, first, out, n.value, _i32p(toks), nt.value, ctypes.byref(n),
+                                            ctypes.byref(nt), ctypes.byref(na)))
+        res = [dict(prompt_id=out[i].prompt_id, j=out[i].j, len=out[i].len, finish=out[i].finish,
+                    tokens=toks[out[i].tok_off:out[i].tok_off + out[i].len].copy()) for i in range(n.value)]
+        return res, na.value
 
     def long_queue(self):
         n = ctypes.c_int32()

@@ -199,6 +199,36 @@ def test_response_speculation_ties_and_sampling(tiny, oracle_w):
     eng.close()
 
 
+def test_streaming_collect(tiny):
+    """NEXT-3: responses streamed between rp_step calls are final
+    (identical to the closing collect, same order) and only ever cover prompts
+    accepted by the current step, in the oracle's acceptance order."""
+    eng = make_engine(tiny, graph_steps=0)
+    n, G, R0 = 12, 5, 4
+    ps = gen.prompts(n, 0, tiny["eos_id"], (1, 100), 91)
+    L = _trace(n, G, 92)[:, 0, :]
+    eng.submit(ps, G, 128, 9, trace=L, round_id=3, keep=R0)
+    ref = sched.closed_form(L, 128, 9, sched.SHORT, keep=R0)
+    streamed, first, calls = [], 0, 0
+    while True:
+        st = eng.step(7)
+        got, first_new = eng.collect_ready(first)
+        assert len(got) == (first_new - first) * R0
+        # every streamed prompt completed no later than the current step
+        for r in got:
+            i = r["prompt_id"] - ps[0]["prompt_id"]
+            assert ref.retained_len[i, r["j"]] == r["len"] <= st.t
+        streamed += got
+        first, calls = first_new, calls + 1
+        if st.done:
+            break
+    final = eng.collect()
+    key = lambda rs: [(r["prompt_id"], r["j"], r["len"], r["tokens"].tolist()) for r in rs]
+    assert key(streamed) == key(final) and calls > 3
+    assert list(dict.fromkeys(r["prompt_id"] - ps[0]["prompt_id"] for r in final)) == ref.accepted
+    eng.close()
+
+
 def test_underfilled_and_edge_rounds(tiny):
     eng = make_engine(tiny, graph_steps=3)
     ps = gen.prompts(3, 0, tiny["eos_id"], (64, 64), 5)          # page-aligned prompts

@@ -1,5 +1,5 @@
 """a Qwen2.5-14B-shaped long round under tensor
-parallelism (row a14, elastic TP).  Run under torchrun on N GPUs (N = 2 or 4):
+parallelism (row a14, elastic TP); --model qwen2.5-32b gives the C4 long round.  Run under torchrun on N GPUs (N = 2 or 4):
 
   python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
       tools/c3_long_round.py [--p0 32] [--cap 32768] [--out gpurun_out/c3_tp2.json]
@@ -28,6 +28,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--p0", type=int, default=32)
+    ap.add_argument("--model", default="qwen2.5-14b", help="qwen2.5-14b (C3) or qwen2.5-32b (C4 long round)")
     ap.add_argument("--cap", type=int, default=32768)
     ap.add_argument("--short-cap", type=int, default=8192)
     ap.add_argument("--out", default="")
@@ -43,7 +44,7 @@ def main():
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     if world > 1:
         dist.init_process_group("gloo")
-    cfg = configs.model_config("qwen2.5-14b")
+    cfg = configs.model_config(a.model)
     G = 8
     lo, hi = 256, 768
     n_pool = 4000
@@ -91,7 +92,7 @@ def main():
     ok = (len(res) == len(prompts) * G and
           all(r["len"] == min(int(L[queue.index(r["prompt_id"])][r["j"]]), a.cap) for r in res))
     if rank == 0:
-        line = dict(config="C3 qwen2.5-14b-shaped long round", tp=world, p0=len(prompts), G=G, cap=a.cap,
+        line = dict(config="%s %s-shaped long round" % ("C3" if "14b" in a.model else "C4", a.model), tp=world, p0=len(prompts), G=G, cap=a.cap,
                     steps=st.t, decoded_tokens=st.decoded_tokens, retained=sum(r["len"] for r in res),
                     kv_tokens_read=st.kv_tokens_read, dev_s=round(dev, 3), wall_s=round(wall, 3),
                     tokens_per_s=round(st.decoded_tokens / dev, 1), ms_per_step=round(1e3 * dev / st.t, 3),
