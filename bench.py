@@ -277,15 +277,9 @@ def run_ours(a):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init Qwen2.5-7B-shaped weights, seeded prompts, lognormal length trace)",
-        "config": {"workload": "BASELINE configs[1]: Qwen2.5-7B-shaped, %d prompts x G=%d per GPU, short cap %d, "
-                               "target floor(n/1.25), tail batching (eta=1.25), trace mode" % (
-                                   W.R["n_submit"], G, W.R["short_cap"]),
-                   "global_prompts_per_short_round": W.n_submit, "P0": W.P0, "G": G,
-                   "short_cap": W.R["short_cap"], "long_cap": W.R["long_cap"],
-                   "parallelism": "short rounds dp%d, long rounds %s" % (
-                       world, ("tp%d" % long_tp) if eng_long is not eng else "dp%d (planner: TP=1 fits the worst-case KV)" % world),
-                   "l2": "inputs larger than L2 (14 GB of weights streamed per decode step)",
-                   "graph_steps": a.graph_steps},
+        "config": bench_config(W, "short rounds dp%d, long rounds %s" % (
+            world, ("tp%d" % long_tp) if eng_long is not eng else "dp%d (planner: TP=1 fits the worst-case KV)" % world),
+            a.graph_steps),
         "per_gpu_tokens_per_s": round(value / world, 1),
         "retained_tokens_per_s": round(retained / dev_s, 1),
         "speculation_waste": round(decoded / max(1.0, retained), 3),
@@ -314,6 +308,16 @@ def run_ours(a):
         with open(a.out, "w") as f:
             f.write(json.dumps(line) + "\n")
     shutdown()
+
+
+def bench_config(W, parallelism, graph_steps):
+    """The workload description shared by both arms (BASELINE.json configs[1], per GPU)."""
+    return {"workload": "BASELINE configs[1]: Qwen2.5-7B-shaped, %d prompts x G=%d per GPU, short cap %d, "
+                        "target floor(n/1.25), tail batching (eta=1.25), trace mode" % (
+                            W.R["n_submit"], W.G, W.R["short_cap"]),
+            "global_prompts_per_short_round": W.n_submit, "P0": W.P0, "G": W.G,
+            "short_cap": W.R["short_cap"], "long_cap": W.R["long_cap"], "parallelism": parallelism,
+            "l2": "inputs larger than L2 (14 GB of weights streamed per decode step)", "graph_steps": graph_steps}
 
 
 def plan_long_tp(choice, cfg, W, world):
@@ -503,7 +507,8 @@ def run_reference(a):
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 * wall / a.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "BASELINE configs[1] (bounded oracle sample)"},
+            "data": "synthetic (random-init Qwen2.5-7B-shaped weights, seeded prompts)",
+            "config": bench_config(W, "fp64 NumPy oracle on the host cores, rank 0 only (bounded sample)", 0),
             "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "oracle",
                              "sample": "per step: 1-layer full-width Qwen2.5-7B-shaped fp64 oracle + LM head, "
                                        "2 decode steps, extrapolated to 28 layers"},
