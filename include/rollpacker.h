@@ -140,7 +140,7 @@ typedef struct {
 
 /* Size query: bytes the caller must provide for weights and workspace, and the
  * size of one KV page (64 tokens x all layers x KV heads x {K,V} x head_dim
- * bf16).  Pure host computation. */
+ * fp16, reading Z20).  Pure host computation. */
 int rp_query_sizes(const rp_model_desc* md, const rp_runtime_desc* rd, rp_sizes* out);
 
 /* Create a context: validates the descriptors, generates the weights into
@@ -276,7 +276,7 @@ int rp_debug_last_logits(void* ctx, float* logits_out, int32_t* slots_out, int32
 int rp_debug_profile(void* ctx, int32_t steps, double* ms_out, int64_t* counts_out, int64_t* rows_ctx_steps);
 
 /* Run the tcgen05 GEMM alone on device pointers: Y[n][m] = sum_k W[m][k] X[n][k]
- * (W bf16 [M,K], X bf16 [N,K] with N <= rows_cap rows allocated, Y fp32 [N,M]);
+ * (W fp16 [M,K], X fp16 [N,K] with N <= rows_cap rows allocated, Y fp32 [N,M]);
  * splits = split-K factor (0 = automatic).  Runs once to warm up, then `iters`
  * back-to-back launches timed with CUDA events; *ms_out (may be NULL) gets the
  * mean milliseconds per launch. */

@@ -5,9 +5,22 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cstdio>
 
 namespace rp {
+
+// Activation / KV-cache / GEMM-operand element type (reading Z20):
+// fp16.  Its 11-bit significand keeps the teacher-forced logits of the
+// 28-layer 7B decoder within the north-star 2e-2 of the fp64 oracle, which
+// bf16 activations (8 bits) miss by ~7x; the weights are the bf16 values of
+// the Z12 formula re-encoded exactly in fp16 (magnitudes below 6.1e-5 round to
+// the fp16 subnormal grid, <= 3e-8).
+using act_t = __half;
+using act2_t = __half2;
+__device__ __forceinline__ act_t to_act(float a) { return __float2half_rn(a); }
+__device__ __forceinline__ act2_t to_act2(float a, float b) { return __floats2half2_rn(a, b); }
+
 
 constexpr int kPage = 64;          // tokens per KV page (DESIGN.md §5 D1)
 constexpr int kAttnChunk = 512;    // tokens per decode-attention split

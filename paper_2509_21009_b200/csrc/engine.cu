@@ -47,7 +47,7 @@ struct Carver {
 };
 
 struct LayerW {
-  __nv_bfloat16 *wqkv, *wo, *wgu, *wd;
+  __half *wqkv, *wo, *wgu, *wd;           // fp16 re-encodings of the bf16 formula values (Z20)
   float *bqkv, *ln1, *ln2;
   GemmPlan p_qkv, p_o, p_gu, p_down;
 };
@@ -77,7 +77,8 @@ struct RpCtx {
 
   // weights
   std::vector<LayerW> layers;
-  __nv_bfloat16 *emb = nullptr, *lm = nullptr;
+  __nv_bfloat16* emb = nullptr;            // gathered by the embedding kernel only
+  __half* lm = nullptr;
   float* lnf = nullptr;
   GemmPlan p_lm{};
   int s_qkv = 1, s_o = 1, s_gu = 1, s_down = 1, s_lm = 1;
@@ -96,7 +97,7 @@ struct RpCtx {
   float* x = nullptr;
   float* ssq = nullptr;         // [rows][d / 128] per-tile sums of squares of x (folded RMSNorm)
   float* ar = nullptr;          // TP: all-reduced partial of a row-parallel GEMM
-  __nv_bfloat16 *h = nullptr, *q = nullptr, *att = nullptr, *mid = nullptr;
+  __half *h = nullptr, *q = nullptr, *att = nullptr, *mid = nullptr;   // activations (Z20)
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
   int* gctr = nullptr;
   int* atickets = nullptr;
@@ -246,12 +247,12 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   Carver cv(c ? rd->workspace : nullptr);
   auto x = cv.take<float>((size_t)z.Tcap * d);
   auto ar = cv.take<float>(tp_of(rd) > 1 ? (size_t)z.Tcap * d : 1);
-  auto h = cv.take<__nv_bfloat16>((size_t)z.Tcap * d);
+  auto h = cv.take<__half>((size_t)z.Tcap * d);
   auto ssq = cv.take<float>((size_t)z.Tcap * std::max<size_t>(1, d / 128));   // folded-RMSNorm partial sums
   auto qkv = cv.take<float>((size_t)z.Tcap * (H + 2 * KV) * hd);
-  auto q = cv.take<__nv_bfloat16>((size_t)z.Tcap * H * hd);
-  auto att = cv.take<__nv_bfloat16>((size_t)z.Tcap * H * hd);
-  auto mid = cv.take<__nv_bfloat16>((size_t)z.Tcap * F);
+  auto q = cv.take<__half>((size_t)z.Tcap * H * hd);
+  auto att = cv.take<__half>((size_t)z.Tcap * H * hd);
+  auto mid = cv.take<__half>((size_t)z.Tcap * F);
   auto logits = cv.take<float>((size_t)std::max(z.S, std::max(z.P, rd->max_prompt_len)) * V);
   auto gpart = cv.take<float>(z.part_floats);
   auto gctr = cv.take<int>(1 << 16);
@@ -639,11 +640,11 @@ static int init_impl(RpCtx* c) {
   std::vector<float> ones(std::max(d, (size_t)1), 1.0f);
   for (int l = 0; l < m.L; ++l) {
     LayerW& w = c->layers[l];
-    w.wqkv = (__nv_bfloat16*)(wb + wl.off[k++]);
+    w.wqkv = (__half*)(wb + wl.off[k++]);
     w.bqkv = (float*)(wb + wl.off[k++]);
-    w.wo = (__nv_bfloat16*)(wb + wl.off[k++]);
-    w.wgu = (__nv_bfloat16*)(wb + wl.off[k++]);
-    w.wd = (__nv_bfloat16*)(wb + wl.off[k++]);
+    w.wo = (__half*)(wb + wl.off[k++]);
+    w.wgu = (__half*)(wb + wl.off[k++]);
+    w.wd = (__half*)(wb + wl.off[k++]);
     w.ln1 = (float*)(wb + wl.off[k++]);
     w.ln2 = (float*)(wb + wl.off[k++]);
     const uint32_t base = 0x100u * (uint32_t)(l + 1);
@@ -676,9 +677,9 @@ static int init_impl(RpCtx* c) {
     CK(cudaMemcpyAsync(w.ln2, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
   }
   c->emb = (__nv_bfloat16*)(wb + wl.off[k++]);
-  c->lm = (__nv_bfloat16*)(wb + wl.off[k++]);
+  c->lm = (__half*)(wb + wl.off[k++]);
   c->lnf = (float*)(wb + wl.off[k++]);
-  launch_init_weights(c->emb, (long long)md->vocab, (int)d, 0, 0, (int)d, 0x10000000u, seed, 0, 0, c->st);
+  launch_init_weights(c->emb, (long long)md->vocab, (int)d, 0, 0, (int)d, 0x10000000u, seed, 0, 0, c->st, 0);
   launch_init_weights(c->lm, (long long)V, (int)d, (long long)m.v0, 0, (int)d, 0x10000001u, seed, 0, 0, c->st);
   CK(cudaMemcpyAsync(c->lnf, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
   CK(cudaGetLastError());

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cstdint>
 
 namespace rp {
@@ -12,7 +13,7 @@ enum GemmEpi { EPI_F32 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_BF16 = 3, EPI_QKV
 // Fused QKV epilogue (decode, split-K path): bias, rotate-half RoPE from a
 // per-position cos/sin table, q -> q_out bf16 [n][H][hd], k/v -> KV page.
 struct RopeArgs {
-  __nv_bfloat16* q_out;
+  __half* q_out;
   uint8_t* kv_pool;
   const int* page_table;
   const int* row_pos;
@@ -40,7 +41,7 @@ struct GemmArgs {
   // tile to ssq_out[n * ssq_stride + tile]; a consumer (ssq_in != nullptr)
   // multiplies output column n by rsqrt(sum_p ssq_in[n * ssq_stride + p] *
   // norm_inv_d + norm_eps), p < ssq_parts, before bias / SwiGLU / RoPE.
-  __nv_bfloat16* xb_out;
+  __half* xb_out;
   int ldxb;
   float* ssq_out;
   const float* ssq_in;
@@ -60,7 +61,7 @@ struct GemmPlan {
   CUtensorMap tmB16, tmB64, tmB256;   // activations [rows_cap, K], boxes of 16 / 64 / 256 rows
 };
 
-int make_tmap_bf16(CUtensorMap* map, const void* base, int rows, int cols, int box_rows);
+int make_tmap_act(CUtensorMap* map, const void* base, int rows, int cols, int box_rows);
 int gemm_init_attrs();
 int gemm_smem_bytes();
 int gemm_pick_splits(int M, int K, int n_sms);

@@ -1,7 +1,7 @@
 // Swap-AB decode/prefill GEMM on the 5th-generation tensor cores (sm_100a).
 //
-//   D[m, n] = sum_k W[m, k] * X[n, k]      (W: weights [M, K] bf16, K-major;
-//                                           X: activations [N, K] bf16, K-major)
+//   D[m, n] = sum_k W[m, k] * X[n, k]      (W: weights [M, K] fp16, K-major;
+//                                           X: activations [N, K] fp16, K-major)
 //
 // Weights fill the UMMA M=128 tile; the live batch (or prompt tokens) is the
 // UMMA N dimension, read at run time from device memory so the same launch is
@@ -81,11 +81,12 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
   return d;
 }
-// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, M=128.
+// Instruction descriptor, kind::f16: D fp32 (bits 4-5 = 1), A and B fp16
+// (bits 7-9, 10-12 = 0; bf16 would be 1), both K-major, N >> 3, M >> 4.
 __device__ __forceinline__ uint32_t make_idesc(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                           uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -329,7 +330,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           const uint64_t da = make_sdesc(sa), db = make_sdesc(sa + A_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)   // +32 B along K per UMMA_K=16 step
-            umma_bf16(tmem_d, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            umma_f16(tmem_d, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           umma_commit(empty0 + 8 * stage);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -525,17 +526,17 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 o.z = v.z * c23.x + sg * p.z * c23.y;
                 o.w = v.w * c23.z + sg * p.w * c23.w;
               }
-              __nv_bfloat162 o01 = __floats2bfloat162_rn(o.x, o.y), o23 = __floats2bfloat162_rn(o.z, o.w);
+              act2_t o01 = to_act2(o.x, o.y), o23 = to_act2(o.z, o.w);
               uint2 packed;
               packed.x = *(uint32_t*)&o01;
               packed.y = *(uint32_t*)&o23;
-              __nv_bfloat16* dst;
+              act_t* dst;
               if (is_q) {
                 dst = R.q_out + ((size_t)n * R.H + head) * hd + i0;
               } else {
                 const int kh = is_v ? head - R.H - R.KV : head - R.H;
                 const int page = R.page_table[(size_t)R.row_pt[n] * R.maxp + pos / kPage];
-                dst = (__nv_bfloat16*)(R.kv_pool + (size_t)page * R.page_bytes +
+                dst = (act_t*)(R.kv_pool + (size_t)page * R.page_bytes +
                                        ((size_t)((R.layer * R.KV + kh) * 2 + (is_v ? 1 : 0)) * kPage + pos % kPage) *
                                            hd * 2) + i0;
               }
@@ -563,11 +564,11 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               v.x += old[u].x; v.y += old[u].y; v.z += old[u].z; v.w += old[u].w;
               *(float4*)((float*)a.out + o) = v;
               if (a.ssq_out) {
-                // bf16(x) for the next GEMM and this tile's sum of squares of
+                // fp16(x) for the next GEMM and this tile's sum of squares of
                 // column n (the warp covers the tile's 128 rows: lanes x 4)
-                __nv_bfloat162* xb = (__nv_bfloat162*)(a.xb_out + (size_t)(n0 + col) * a.ldxb + m4);
-                xb[0] = __floats2bfloat162_rn(v.x, v.y);
-                xb[1] = __floats2bfloat162_rn(v.z, v.w);
+                act2_t* xb = (act2_t*)(a.xb_out + (size_t)(n0 + col) * a.ldxb + m4);
+                xb[0] = to_act2(v.x, v.y);
+                xb[1] = to_act2(v.z, v.w);
                 float ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
@@ -581,9 +582,9 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 *(float4*)((float*)a.out + o) = v;
               }
             } else {
-              __nv_bfloat162* ob = (__nv_bfloat162*)((__nv_bfloat16*)a.out + o);
-              ob[0] = __floats2bfloat162_rn(v.x + bb.x, v.y + bb.y);
-              ob[1] = __floats2bfloat162_rn(v.z + bb.z, v.w + bb.w);
+              act2_t* ob = (act2_t*)((act_t*)a.out + o);
+              ob[0] = to_act2(v.x + bb.x, v.y + bb.y);
+              ob[1] = to_act2(v.z + bb.z, v.w + bb.w);
             }
           }
         }
@@ -635,7 +636,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         // otherwise issue 32 scalar stores per chunk).
         if (a.epi == EPI_SWIGLU) {
           // rows 64..127 (quarters 2,3) hold `up`, rows 0..63 hold `gate`
-          __nv_bfloat16* st2 = (__nv_bfloat16*)stg;           // [32 columns][72] bf16
+          act_t* st2 = (act_t*)stg;                   // [32 columns][72] fp16
           named_bar(2, 128);
           if (q >= 2) {
 #pragma unroll
@@ -644,7 +645,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           named_bar(2, 128);
           if (q < 2) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) st2[j * 72 + row] = __float2bfloat16(silu_f(v[j]) * xch[row * 33 + j]);
+            for (int j = 0; j < 32; ++j) st2[j * 72 + row] = to_act(silu_f(v[j]) * xch[row * 33 + j]);
           }
           named_bar(2, 128);
           const int f0 = I.tile * 64;
@@ -652,7 +653,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           for (int i = 0; i < 2; ++i) {
             const int idx = et + 128 * i, n = idx >> 3, f8 = (idx & 7) * 8;
             if (c0 + n < nc)
-              *(uint4*)((__nv_bfloat16*)a.out + (size_t)(n0 + c0 + n) * a.ldo + f0 + f8) = *(const uint4*)(st2 + n * 72 + f8);
+              *(uint4*)((act_t*)a.out + (size_t)(n0 + c0 + n) * a.ldo + f0 + f8) = *(const uint4*)(st2 + n * 72 + f8);
           }
         } else {
 #pragma unroll
@@ -670,9 +671,9 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               val.x += old.x; val.y += old.y; val.z += old.z; val.w += old.w;
               *(float4*)((float*)a.out + o) = val;
               if (a.ssq_out) {   // warp = one column n, lanes = the tile's 128 rows x 4
-                __nv_bfloat162* xb = (__nv_bfloat162*)(a.xb_out + (size_t)(n0 + c0 + n) * a.ldxb + mt0 + m4);
-                xb[0] = __floats2bfloat162_rn(val.x, val.y);
-                xb[1] = __floats2bfloat162_rn(val.z, val.w);
+                act2_t* xb = (act2_t*)(a.xb_out + (size_t)(n0 + c0 + n) * a.ldxb + mt0 + m4);
+                xb[0] = to_act2(val.x, val.y);
+                xb[1] = to_act2(val.z, val.w);
                 float ss = val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
@@ -685,9 +686,9 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 *(float4*)((float*)a.out + o) = val;
               }
             } else {
-              __nv_bfloat162* ob = (__nv_bfloat162*)((__nv_bfloat16*)a.out + o);
-              ob[0] = __floats2bfloat162_rn(val.x, val.y);
-              ob[1] = __floats2bfloat162_rn(val.z, val.w);
+              act2_t* ob = (act2_t*)((act_t*)a.out + o);
+              ob[0] = to_act2(val.x, val.y);
+              ob[1] = to_act2(val.z, val.w);
             }
           }
         }
@@ -726,14 +727,14 @@ static PFN_encodeTiled get_encode() {
   return fn;
 }
 
-int make_tmap_bf16(CUtensorMap* map, const void* base, int rows, int cols, int box_rows) {
+int make_tmap_act(CUtensorMap* map, const void* base, int rows, int cols, int box_rows) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return -1;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -2;
@@ -773,10 +774,10 @@ void gemm_launch(const GemmPlan& p, const GemmArgs& a, int grid, cudaStream_t st
 }
 
 int make_plan(GemmPlan* p, const void* W, int M, int K, const void* X, int rows_cap) {
-  if (make_tmap_bf16(&p->tmA, W, M, K, 128)) return -1;
-  if (make_tmap_bf16(&p->tmB16, X, rows_cap, K, 16)) return -1;
-  if (make_tmap_bf16(&p->tmB64, X, rows_cap, K, 64)) return -1;
-  if (make_tmap_bf16(&p->tmB256, X, rows_cap, K, 256)) return -1;
+  if (make_tmap_act(&p->tmA, W, M, K, 128)) return -1;
+  if (make_tmap_act(&p->tmB16, X, rows_cap, K, 16)) return -1;
+  if (make_tmap_act(&p->tmB64, X, rows_cap, K, 64)) return -1;
+  if (make_tmap_act(&p->tmB256, X, rows_cap, K, 256)) return -1;
   return 0;
 }
 

@@ -1,7 +1,7 @@
 // Paged-KV GQA attention for decode and prefill (K4/K5).
 //
 // The KV pool is addressed by TMA as a 2-D tensor of token rows x head_dim
-// (bf16): page p, layer l, KV head h, K|V is the 64-row block starting at row
+// (fp16, reading Z20): page p, layer l, KV head h, K|V is the 64-row block starting at row
 // (((p*L + l)*KV + h)*2 + kv)*64.  One CTA = 1 producer warp + 3 consumer
 // warps.  The producer streams whole pages (K and V, SWIZZLE_128B boxes of 64
 // columns) into a 6-stage mbarrier ring; consumer warp w (of 3) owns the
@@ -9,7 +9,7 @@
 // split): the 16 MMA rows are the (query token, query head) pairs served by
 // one KV head -- decode: 1 token x g heads (g = H/KV <= 8); prefill:
 // floor(16/g) tokens x g heads with per-row causal limits.  S = Q K^T and
-// O += P V run on mma.sync m16n8k16 (bf16, fp32 accumulate; a 16-row MMA is
+// O += P V run on mma.sync m16n8k16 (fp16, fp32 accumulate; a 16-row MMA is
 // the natural shape for g <= 8 query rows) with an online softmax in the
 // log2 domain; the warps merge in shared memory; multi-split blocks write
 // (m, l, O) partials and the last split to finish (atomic ticket) combines
@@ -37,7 +37,7 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
 }
 __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
@@ -47,8 +47,8 @@ __device__ __forceinline__ uint32_t movtrans(uint32_t x) {
   asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
   return y;
 }
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+__device__ __forceinline__ uint32_t pack_act(float lo, float hi) {
+  act2_t v = to_act2(lo, hi);
   return *(uint32_t*)&v;
 }
 __device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
@@ -91,9 +91,9 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
 // the PV MMA through movmatrix.trans; O^T = V^T P^T keeps head_dim on the rows.
 template <int HD, int CW, int NQT>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
-attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __restrict__ q,
+attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict__ q,
             const int* __restrict__ page_table, int maxp, const AttnItem* __restrict__ items, const int* n_items_dev,
-            int n_items_host, __nv_bfloat16* __restrict__ out, float* __restrict__ partial, int* __restrict__ tickets,
+            int n_items_host, act_t* __restrict__ out, float* __restrict__ partial, int* __restrict__ tickets,
             ModelDims m, int layer) {
   using C = AttnCfg<HD, CW, NQT>;
   constexpr int MR = C::MR;
@@ -105,7 +105,15 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
   const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(bars);
   const uint32_t empty0 = full0 + 8 * AT_STAGES;
 
-  pdl_wait();
+  // Decode (NQT == 1): the work list, page tables and every KV page except
+  // the one holding a row's current position come from kernels that finished
+  // before the QKV GEMM started (the round control of the previous step,
+  // earlier steps' KV appends), so the producer streams pages before the
+  // programmatic-dependency wait and waits only at the first page the QKV
+  // GEMM still writes (its fused KV append); consumers wait before reading Q.
+  // Prefill (rope_append wrote every prompt page) waits up front.
+  constexpr bool kEarly = NQT == 1;
+  if (!kEarly) pdl_wait();
   pdl_launch_dependents();
   const int n_items = n_items_dev ? *n_items_dev : n_items_host;
   const int n_units = n_items * m.KV;            // flat (item, KV head) work units
@@ -121,6 +129,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
   if (warp == CW) {
     // ===================== producer warp =====================
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&kv_map) : "memory");
+    bool waited = !kEarly;
     long long gpage = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int it = u / m.KV, kvh = u % m.KV;
@@ -133,6 +142,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
         for (int jj = 0; jj < cnt; ++jj) {
           const int page = __shfl_sync(0xffffffffu, mine, jj);
           if (lane == 0) {
+            if (!waited && (p_lo + j0 + jj + 1) * kPage > I.pos0) { pdl_wait(); waited = true; }
             const long long gp = gpage + j0 + jj;
             const int st = (int)(gp % AT_STAGES);
             const uint32_t ph = (uint32_t)((gp / AT_STAGES) & 1);
@@ -155,6 +165,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
   }
 
   // ===================== consumer warps =====================
+  if (kEarly) pdl_wait();                         // Q and the current KV row come from the QKV GEMM
   const float scale = 1.4426950408889634f * rsqrtf((float)HD);
   const int tq = lane >> 2, tr = lane & 3;      // fragment row / column-pair coordinates
   long long gpage = 0;
@@ -168,7 +179,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
 #pragma unroll
     for (int nq = 0; nq < NQT; ++nq) {
       const int r = nq * 8 + tq;
-      const __nv_bfloat16* qr =
+      const act_t* qr =
           r < nrows ? q + ((size_t)(I.q_row0 + r / g) * m.H + kvh * g + r % g) * HD : nullptr;
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
@@ -265,8 +276,8 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
         uint32_t pb[NQT][2];
 #pragma unroll
         for (int nq = 0; nq < NQT; ++nq) {
-          pb[nq][0] = movtrans(pack_bf16(s[ks][nq][0], s[ks][nq][1]));   // tokens 0-7 of the k-step
-          pb[nq][1] = movtrans(pack_bf16(s[ks][nq][2], s[ks][nq][3]));   // tokens 8-15
+          pb[nq][0] = movtrans(pack_act(s[ks][nq][0], s[ks][nq][1]));   // tokens 0-7 of the k-step
+          pb[nq][1] = movtrans(pack_act(s[ks][nq][2], s[ks][nq][3]));   // tokens 8-15
         }
         const int row = ks * 16 + (lane & 7) + ((lane >> 4) << 3);
 #pragma unroll
@@ -327,7 +338,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
       }
       const int tok = I.q_row0 + r / g, head = kvh * g + r % g;
       if (I.nsplit == 1) {
-        out[((size_t)tok * m.H + head) * HD + c] = __float2bfloat16(L > 0.f ? O / L : 0.f);
+        out[((size_t)tok * m.H + head) * HD + c] = to_act(L > 0.f ? O / L : 0.f);
       } else {
         float* pp = partial + ((size_t)it * m.KV + kvh) * (16 * (HD + 2));
         pp[32 + r * HD + c] = O;
@@ -385,9 +396,9 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const __nv_bfloat16* __r
             }
           }
           const int tok = I.q_row0 + r / g, head = kvh * g + r % g;
-          __nv_bfloat162* o2 = (__nv_bfloat162*)(out + ((size_t)tok * m.H + head) * HD + c4);
-          o2[0] = __floats2bfloat162_rn(acc.x, acc.y);
-          o2[1] = __floats2bfloat162_rn(acc.z, acc.w);
+          act2_t* o2 = (act2_t*)(out + ((size_t)tok * m.H + head) * HD + c4);
+          o2[0] = to_act2(acc.x, acc.y);
+          o2[1] = to_act2(acc.z, acc.w);
         }
       }
     }
@@ -420,7 +431,7 @@ typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint3
                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// The pool as [n_pages * L * KV * 2 * 64 rows, hd] bf16 with 64 x 64 boxes.
+// The pool as [n_pages * L * KV * 2 * 64 rows, hd] fp16 with 64 x 64 boxes.
 int make_kv_map(CUtensorMap* map, const void* pool, size_t n_pages, const ModelDims& m) {
   void* p = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -434,7 +445,7 @@ int make_kv_map(CUtensorMap* map, const void* pool, size_t n_pages, const ModelD
   cuuint64_t strides[1] = {(cuuint64_t)m.hd * 2};
   cuuint32_t box[2] = {64, (cuuint32_t)kPage};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, es,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(pool), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -2;
@@ -444,8 +455,8 @@ void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_
                       const AttnItem* items, const int* n_items_dev, int n_items_host, void* out, float* partial,
                       int* tickets, const ModelDims& m, int layer, bool decode, cudaStream_t st) {
   const dim3 grid(148);   // one wave, persistent over the flat (item, KV head) units
-  const auto* qq = (const __nv_bfloat16*)q;
-  auto* oo = (__nv_bfloat16*)out;
+  const auto* qq = (const act_t*)q;
+  auto* oo = (act_t*)out;
   if (m.hd == 128) {
     if (decode)
       launch_pdl(attn_kernel<128, 6, 1>, grid, dim3(AttnDec128::THREADS), AttnDec128::SMEM, st, kv_map, qq,

@@ -9,12 +9,13 @@ namespace rp {
 // ------------------------------------------------------------- weight formula
 // Generates the [rows, cols] block whose element (r, c) is element
 // (r0 + r, c0 + c) of the logical [*, in_full] tensor `tid` (TP shards are
-// blocks of the full tensor).  mode 0: bf16 out[r][c]; mode 1: fp32 out[r][c]
-// (biases, exact widening of the bf16 value); mode 2: gate/up rows
+// blocks of the full tensor).  mode 0: 16-bit out[r][c]; mode 1: fp32
+// out[r][c] (biases, exact widening of the bf16 value); mode 2: gate/up rows
 // interleaved in 64-row blocks of a [2*rows, cols] tensor (`up` selects the
-// second half of each 128-row block).
+// second half of each 128-row block).  The value is the bf16 of the formula;
+// `f16` stores it as fp16 (GEMM operands, reading Z20), else as bf16.
 __global__ void init_weights_kernel(void* out, long long rows, int cols, long long r0, int c0, int in_full,
-                                    uint32_t tid, uint32_t k0, uint32_t k1, int mode, int up) {
+                                    uint32_t tid, uint32_t k0, uint32_t k1, int mode, int up, int f16) {
   const float a = 0.034641016151377546f;   // fl32(0.02 * sqrt(3))
   const long long n = rows * cols;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
@@ -25,24 +26,25 @@ __global__ void init_weights_kernel(void* out, long long rows, int cols, long lo
         __fsub_rn(__fmul_rn(__fadd_rn(__uint2float_rn(u4_word(x, (int)(i & 3)) >> 9), 0.5f), 2.384185791015625e-07f),
                   1.0f);
     const __nv_bfloat16 v = __float2bfloat16_rn(__fmul_rn(a, u2m1));
+    long long o = e;
     if (mode == 1) {
       ((float*)out)[e] = __bfloat162float(v);
+      continue;
     } else if (mode == 2) {
-      const long long pr = (r / 64) * 128 + (r % 64) + (up ? 64 : 0);
-      ((__nv_bfloat16*)out)[pr * cols + c] = v;
-    } else {
-      ((__nv_bfloat16*)out)[e] = v;
+      o = ((r / 64) * 128 + (r % 64) + (up ? 64 : 0)) * cols + c;
     }
+    if (f16) ((__half*)out)[o] = __float2half_rn(__bfloat162float(v));
+    else ((__nv_bfloat16*)out)[o] = v;
   }
 }
 
 void launch_init_weights(void* out, long long rows, int cols, long long r0, int c0, int in_full, uint32_t tid,
-                         uint64_t seed, int mode, int up, cudaStream_t st) {
+                         uint64_t seed, int mode, int up, cudaStream_t st, int f16) {
   const long long n = rows * cols;
   long long blocks = (n + 255) / 256;
   int grid = (int)(blocks < 148 * 64 ? blocks : 148 * 64);
   init_weights_kernel<<<grid, 256, 0, st>>>(out, rows, cols, r0, c0, in_full, tid, (uint32_t)seed,
-                                            (uint32_t)(seed >> 32), mode, up);
+                                            (uint32_t)(seed >> 32), mode, up, f16);
 }
 
 // Row kernels: one wave of 148 CTAs for device-side (decode) row counts; up
@@ -71,12 +73,12 @@ void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb,
 }
 
 // -------------------------------------------------------------------- RMSNorm
-// h[r] = bf16( x[src] / sqrt(mean(x[src]^2) + eps) * gamma ),  src = gather ? gather[r] : r
+// h[r] = fp16( x[src] / sqrt(mean(x[src]^2) + eps) * gamma ),  src = gather ? gather[r] : r
 // One CTA (256 threads) per row.  With `delta` (tensor parallelism):
 // x[r] += delta[r] first (the all-reduced partial of a row-parallel GEMM) and
 // the updated row is written back.
 __global__ void rmsnorm_kernel(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
-                               const float* gamma, __nv_bfloat16* h, int d, float eps) {
+                               const float* gamma, act_t* h, int d, float eps) {
   __shared__ float red[32];
   pdl_wait();
   pdl_launch_dependents();
@@ -111,12 +113,12 @@ __global__ void rmsnorm_kernel(float* x, const float* delta, const int* gather, 
     __syncthreads();
     const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
     __syncthreads();
-    __nv_bfloat162* hr = (__nv_bfloat162*)(h + (size_t)r * d);
+    act2_t* hr = (act2_t*)(h + (size_t)r * d);
     const float4* g4 = (const float4*)gamma;
     for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
       float4 v = xr[c], g = g4[c];
-      hr[2 * c] = __floats2bfloat162_rn(v.x * inv * g.x, v.y * inv * g.y);
-      hr[2 * c + 1] = __floats2bfloat162_rn(v.z * inv * g.z, v.w * inv * g.w);
+      hr[2 * c] = to_act2(v.x * inv * g.x, v.y * inv * g.y);
+      hr[2 * c + 1] = to_act2(v.z * inv * g.z, v.w * inv * g.w);
     }
   }
 }
@@ -124,7 +126,7 @@ __global__ void rmsnorm_kernel(float* x, const float* delta, const int* gather, 
 void launch_rmsnorm(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
                     const float* gamma, void* h, int d, float eps, cudaStream_t st) {
   launch_pdl(rmsnorm_kernel, dim3(row_grid(n_dev, n_host)), dim3(256), 0, st, x, delta, gather, n_dev, n_host, gamma,
-             (__nv_bfloat16*)h, d, eps);
+             (act_t*)h, d, eps);
 }
 
 // --------------------------------------------------- TP add + RMSNorm (peer)
@@ -132,7 +134,7 @@ void launch_rmsnorm(float* x, const float* delta, const int* gather, const int* 
 // partial into recv[src] of this rank (NVLink stores, gemm_tcgen05 push) and
 // counted its finished output units in flags[src].  Wait until every source
 // delivered this use's units, then x[r] += sum_src recv[src][r] in rank order
-// (identical bits on every rank), write x back and h = bf16(x / rms * gamma).
+// (identical bits on every rank), write x back and h = fp16(x / rms * gamma).
 // gen = output units of this slot consumed so far on this rank (cumulative:
 // the units per use depend on the live count); the last CTA advances it.
 __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
@@ -143,7 +145,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 
 __global__ void tp_norm_kernel(float* x, const float* recv, int tp, size_t src_stride,
                                const unsigned long long* flags, unsigned long long* gen, int* done, int m_tiles,
-                               int splits, const int* n_dev, const float* gamma, __nv_bfloat16* h, int d, float eps) {
+                               int splits, const int* n_dev, const float* gamma, act_t* h, int d, float eps) {
   __shared__ float red[32];
   __shared__ unsigned long long s_units;
   pdl_wait();
@@ -195,12 +197,12 @@ __global__ void tp_norm_kernel(float* x, const float* recv, int tp, size_t src_s
     __syncthreads();
     const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
     __syncthreads();
-    __nv_bfloat162* hr = (__nv_bfloat162*)(h + (size_t)r * d);
+    act2_t* hr = (act2_t*)(h + (size_t)r * d);
     const float4* g4 = (const float4*)gamma;
     for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
       float4 v = xr[c], g = g4[c];
-      hr[2 * c] = __floats2bfloat162_rn(v.x * inv * g.x, v.y * inv * g.y);
-      hr[2 * c + 1] = __floats2bfloat162_rn(v.z * inv * g.z, v.w * inv * g.w);
+      hr[2 * c] = to_act2(v.x * inv * g.x, v.y * inv * g.y);
+      hr[2 * c + 1] = to_act2(v.z * inv * g.z, v.w * inv * g.w);
     }
   }
   // this use of the slot is consumed once every CTA is past its reads
@@ -218,15 +220,15 @@ void launch_tp_norm(float* x, const float* recv, int tp, size_t src_stride, cons
                     unsigned long long* gen, int* done, int m_tiles, int splits, const int* n_dev, int n_rows_grid,
                     const float* gamma, void* h, int d, float eps, cudaStream_t st) {
   launch_pdl(tp_norm_kernel, dim3(row_grid(n_dev, n_rows_grid)), dim3(256), 0, st, x, recv, tp, src_stride, flags, gen,
-             done, m_tiles, splits, n_dev, gamma, (__nv_bfloat16*)h, d, eps);
+             done, m_tiles, splits, n_dev, gamma, (act_t*)h, d, eps);
 }
 
 // -------------------------------------------------------- RoPE + KV append
 // qkv row r (fp32, bias already added): [q heads | k heads | v heads] x hd.
 // Rotate-half RoPE at position row_pos[r] (angle in fp64, then fp32 sincos
-// of the reduced angle), q -> q_out[r][H][hd] bf16, k/v -> KV page.
+// of the reduced angle), q -> q_out[r][H][hd] fp16, k/v -> KV page (fp16).
 __global__ void rope_append_kernel(const float* qkv, const int* n_dev, int n_host, const int* row_pos,
-                                   const int* row_pt, const int* page_table, int maxp, __nv_bfloat16* q_out,
+                                   const int* row_pt, const int* page_table, int maxp, act_t* q_out,
                                    uint8_t* kv_pool, ModelDims m, int layer, const double* inv_freq) {
   extern __shared__ float cs[];   // [hd/2] cos, [hd/2] sin
   pdl_wait();
@@ -254,18 +256,18 @@ __global__ void rope_append_kernel(const float* qkv, const int* n_dev, int n_hos
       const float x1 = src[i], x2 = src[i + half], c = cs[i], s = cs[half + i];
       const float o1 = x1 * c - x2 * s, o2 = x2 * c + x1 * s;
       if (head < m.H) {
-        __nv_bfloat16* dst = q_out + ((size_t)r * m.H + head) * m.hd;
-        dst[i] = __float2bfloat16(o1); dst[i + half] = __float2bfloat16(o2);
+        act_t* dst = q_out + ((size_t)r * m.H + head) * m.hd;
+        dst[i] = to_act(o1); dst[i + half] = to_act(o2);
       } else {
         const int kh = head - m.H;
-        __nv_bfloat16* dst = (__nv_bfloat16*)(pbase + ((size_t)((layer * m.KV + kh) * 2 + 0) * kPage + prow) * m.hd * 2);
-        dst[i] = __float2bfloat16(o1); dst[i + half] = __float2bfloat16(o2);
+        act_t* dst = (act_t*)(pbase + ((size_t)((layer * m.KV + kh) * 2 + 0) * kPage + prow) * m.hd * 2);
+        dst[i] = to_act(o1); dst[i + half] = to_act(o2);
       }
     }
     for (int e = threadIdx.x; e < m.KV * m.hd; e += blockDim.x) {
       const int kh = e / m.hd, i = e % m.hd;
-      __nv_bfloat16* dst = (__nv_bfloat16*)(pbase + ((size_t)((layer * m.KV + kh) * 2 + 1) * kPage + prow) * m.hd * 2);
-      dst[i] = __float2bfloat16(row[(m.H + m.KV) * m.hd + e]);
+      act_t* dst = (act_t*)(pbase + ((size_t)((layer * m.KV + kh) * 2 + 1) * kPage + prow) * m.hd * 2);
+      dst[i] = to_act(row[(m.H + m.KV) * m.hd + e]);
     }
     __syncthreads();
   }
@@ -275,7 +277,7 @@ void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const in
                         const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
                         const double* inv_freq, cudaStream_t st) {
   launch_pdl(rope_append_kernel, dim3(row_grid(n_dev, n_host)), dim3(256), m.hd * sizeof(float), st, qkv, n_dev,
-             n_host, row_pos, row_pt, page_table, maxp, (__nv_bfloat16*)q_out, (uint8_t*)kv_pool, m, layer, inv_freq);
+             n_host, row_pos, row_pt, page_table, maxp, (act_t*)q_out, (uint8_t*)kv_pool, m, layer, inv_freq);
 }
 
 // ------------------------------------------------------------- prompt fork

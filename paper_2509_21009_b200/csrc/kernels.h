@@ -73,7 +73,7 @@ struct ModelDims {
 
 // weights
 void launch_init_weights(void* out, long long rows, int cols, long long r0, int c0, int in_full, uint32_t tid,
-                         uint64_t seed, int mode, int up, cudaStream_t st);
+                         uint64_t seed, int mode, int up, cudaStream_t st, int f16 = 1);
 // forward pieces (n = n_dev ? *n_dev : n_host)
 void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb, float* x, int d, cudaStream_t st);
 void launch_rmsnorm(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,

@@ -353,7 +353,7 @@ class Engine:
                     rows=int(rcs[0]), ctx=int(rcs[1]), steps=int(rcs[2]))
 
     def debug_gemm(self, W, X, N, splits=0, iters=1, timed=False):
-        """W: torch bf16 [M, K] cuda, X: torch bf16 [rows_cap, K] cuda -> Y fp32 [N, M]
+        """W: torch fp16 [M, K] cuda, X: torch fp16 [rows_cap, K] cuda -> Y fp32 [N, M]
         (and the mean ms per launch when timed)."""
         torch = self.torch
         M, K = W.shape

@@ -47,8 +47,8 @@ def make_engine(cfg, graph_steps=4, max_seqs=64, max_prompts=16, max_prompt_len=
 def test_gemm_tcgen05_vs_fp32(torch, tiny, M, K, N):
     eng = _shared_engine(tiny)
     g = torch.Generator(device="cuda").manual_seed(M * 7 + K * 3 + N)
-    W = (torch.randn(M, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
-    X = (torch.randn(max(N, 1) + 40, K, device="cuda", generator=g)).to(torch.bfloat16)
+    W = (torch.randn(M, K, device="cuda", generator=g) * 0.05).to(torch.float16)
+    X = (torch.randn(max(N, 1) + 40, K, device="cuda", generator=g)).to(torch.float16)
     ref = X[:N].float() @ W.float().T
     for splits in (1, 3):
         Y = eng.debug_gemm(W, X, N, splits=splits)

@@ -19,8 +19,8 @@ def main():
     only = sys.argv[1:] or list(shapes)
     for name in only:
         M, K = shapes[name]
-        W = (torch.randn(M, K, device="cuda") * 0.02).to(torch.bfloat16)
-        X = torch.randn(512, K, device="cuda").to(torch.bfloat16)
+        W = (torch.randn(M, K, device="cuda") * 0.02).to(torch.float16)
+        X = torch.randn(512, K, device="cuda").to(torch.float16)
         for N in (16, 64, 128, 256):
             for sp in (0, 1, 2, 4, 8):
                 try:

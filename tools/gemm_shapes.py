@@ -12,8 +12,8 @@ eng = rp.Engine(model_config("tiny"), max_seqs=256, max_prompts=16, max_prompt_l
                 max_cap=64, kv_pool_bytes=64 << 20, graph_steps=0)
 for spec in sys.argv[1:]:
     M, K, N = (int(x) for x in spec.split(","))
-    W = (torch.randn(M, K, device="cuda") * 0.02).to(torch.bfloat16)
-    X = torch.randn(512, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(M, K, device="cuda") * 0.02).to(torch.float16)
+    X = torch.randn(512, K, device="cuda").to(torch.float16)
     for sp in (0, 1, 2):
         _, ms = eng.debug_gemm(W, X, N, splits=sp, iters=5, timed=True)
         us = ms * 1e3

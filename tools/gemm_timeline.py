@@ -13,8 +13,8 @@ eng = rp.Engine(model_config("tiny"), max_seqs=256, max_prompts=16, max_prompt_l
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 shapes = [(4608, 3584), (3584, 3584), (37888, 3584), (3584, 18944)]
 for M, K in shapes:
-    W = (torch.randn(M, K, device="cuda") * 0.02).to(torch.bfloat16)
-    X = torch.randn(512, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(M, K, device="cuda") * 0.02).to(torch.float16)
+    X = torch.randn(512, K, device="cuda").to(torch.float16)
     for N in [int(x) for x in (sys.argv[1:] or ["16", "32", "64"])]:
         for sp in (0,):
             flush.fill_(1)

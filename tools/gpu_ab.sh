@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-for i in 1 2; do
-timeout -s KILL 200 python tools/step_profile.py 256 192 128 2>&1 | grep -A1 "graph_step"
-RP_GEMM_NO_PAIR=1 timeout -s KILL 200 python tools/step_profile.py 256 192 128 2>&1 | grep -A1 "graph_step"
-done
+timeout -s KILL 600 python -m pytest tests/test_gpu_7b.py -x -q -s 2>&1 | grep "max-abs\|passed\|failed"
+timeout -s KILL 200 python tools/step_profile.py 256 128 64 16 2>&1 | grep "graph_step"
