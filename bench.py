@@ -275,7 +275,7 @@ def run_ours(a):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "bf16",
+        "dtype": "fp16",
         "data": "synthetic (random-init Qwen2.5-7B-shaped weights, seeded prompts, lognormal length trace)",
         "config": bench_config(W, "short rounds dp%d, long rounds %s" % (
             world, ("tp%d" % long_tp) if eng_long is not eng else "dp%d (planner: TP=1 fits the worst-case KV)" % world),
@@ -437,7 +437,9 @@ def roofline(prof, cfg):
     else:
         roof = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None}
     traffic, traffic_src = ncu_traffic(dom)
-    roof.update({"kernel": dom, "traffic": traffic, "traffic_source": traffic_src, "peak_source": src,
+    roof.update({"kernel": dom, "traffic": traffic, "traffic_source": traffic_src,
+                 "peak_source": src + (" (cuBLAS bf16 dense; fp16 runs at the same tensor rate)"
+                                       if roof.get("unit") == "TFLOP/s" else ""),
                  "share_of_step": round(ms[dom] / total, 4),
                  "mean_live_rows": round(B, 1), "mean_ctx_per_row": round(ctx / max(B, 1), 1),
                  "measured": "CUDA events around each launch of %d eager decode steps (first warm-up round)" % steps})
