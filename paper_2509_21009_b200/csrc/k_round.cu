@@ -222,7 +222,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
   // sum ns_r <= U whenever no row is forced up to 1), each of
   // ceil(ctx_r / ns_r) tokens rounded up to whole pages.
   const long long ctx_total = max(1LL, C->ctx_sum);
-  const int U = max(1, 148 / R.kv_heads);
+  const int U = R.attn_units > 0 ? R.attn_units : max(1, 148 / R.kv_heads);
   int kept = 0, alloc = 0, items = 0;
   if (!s_err) {
     for (int base = 0; base < n; base += CTL_THREADS) {

@@ -46,6 +46,7 @@ struct CtlBlock {
 struct RoundDev {
   int S, P, maxp, cap, G, target, kind /*0 short 1 long*/, trace, eos, n_prompts, kv_heads;
   int keep;           // responses retained per prompt (R0 <= G; == G in long rounds)
+  int attn_units;     // decode-attention split budget per KV head (0: 148 / KV)
   int world, rank;
   int* slot_prompt; int* slot_j; int* kv_len; int* gen; int* trace_L; int* status; int* own0;
   int* tok_out;       // [S][cap]

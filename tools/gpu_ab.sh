@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout -s KILL 600 python -m pytest tests/test_gpu_7b.py -x -q -s 2>&1 | grep "max-abs\|passed\|failed"
-timeout -s KILL 200 python tools/step_profile.py 256 128 64 16 2>&1 | grep "graph_step"
+for U in 0 18 9 74; do echo "U=$U"; RP_ATTN_UNITS=$U timeout -s KILL 200 python tools/step_profile.py 256 64 16 2>&1 | grep -A1 "graph_step" | grep -o "graph_step_ms=[0-9.]*\|attention=[0-9.]*"; done
