@@ -92,6 +92,7 @@ struct RpCtx {
   unsigned long long* tp_gen = nullptr;   // [2]
   int* tp_done = nullptr;                 // [2]
   bool peer_decode = false;               // the current forward pushes partials (final norm owes a tp_norm)
+  long long* attn_tl = nullptr;           // debug (RP_ATTN_TIMELINE): last attention launch's CTA marks
 
   // activations / workspace
   float* x = nullptr;
@@ -734,6 +735,12 @@ static int init_impl(RpCtx* c) {
   c->h_ctl->done = 1;
   CK(cudaMemcpyAsync(c->R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
 
+  if (getenv("RP_ATTN_TIMELINE")) {
+    CK(cudaMalloc(&c->attn_tl, (size_t)kSMs * 8 * sizeof(long long)));
+    CK(cudaMemset(c->attn_tl, 0, (size_t)kSMs * 8 * sizeof(long long)));
+    attn_set_timeline(c->attn_tl);
+  }
+
   // ---- TP peer block (exported with CUDA IPC; rp_tp_ipc_open enables it)
   if (c->tp > 1 && c->tp <= 8 && d % 128 == 0) {
     c->tp_recv_floats = (size_t)c->tp * c->z.S * d;
@@ -796,6 +803,7 @@ void rp_free(void* ctx) {
     if (c->tp_peer_base[q] && c->tp_peer_base[q] != c->tp_ipc) cudaIpcCloseMemHandle(c->tp_peer_base[q]);
   if (c->tp_ipc) cudaFree(c->tp_ipc);
   if (c->tp_gen) cudaFree(c->tp_gen);
+  if (c->attn_tl) { attn_set_timeline(nullptr); cudaFree(c->attn_tl); }
   if (c->own_stream) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -1070,6 +1078,24 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
     if ((rc = read_ctl(c))) return rc;
   }
   fill_status(c, st);
+  if (c->attn_tl) {   // debug: marks of the last attention launch, us from the earliest CTA start
+    std::vector<long long> h((size_t)kSMs * 8);
+    CK(cudaMemcpy(h.data(), c->attn_tl, h.size() * 8, cudaMemcpyDeviceToHost));
+    long long t0 = LLONG_MAX;
+    for (int b = 0; b < kSMs; ++b) if (h[(size_t)b * 8]) t0 = std::min(t0, h[(size_t)b * 8]);
+    const char* nm[7] = {"start", "depwait", "page0", "lastpage", "written", "merged", "end"};
+    fprintf(stderr, "attn timeline (n_live %d):", c->h_ctl->n_live);
+    for (int k = 0; k < 7; ++k) {
+      double sum = 0, mx = -1e30; int n = 0;
+      for (int b = 0; b < kSMs; ++b) {
+        const long long v = h[(size_t)b * 8 + k];
+        if (v && v >= t0) { const double u = (v - t0) / 1e3; sum += u; mx = std::max(mx, u); ++n; }
+      }
+      if (n) fprintf(stderr, " %s=%.2f/%.2f(%d)", nm[k], sum / n, mx, n);
+    }
+    fprintf(stderr, "\n");
+    CK(cudaMemset(c->attn_tl, 0, h.size() * 8));
+  }
   if (c->h_ctl->err == 1) return c->fail(RP_ENOMEM_KV, "KV page pool exhausted (no preemption; reading Z17)");
   if (c->h_ctl->err == 2) return c->fail(RP_ENOSPC, "page table overflow (max_prompt_len + max_cap)");
   return RP_OK;

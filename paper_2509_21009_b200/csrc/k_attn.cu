@@ -68,6 +68,18 @@ __device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, uint
       : "memory");
 }
 
+// debug timeline (RP_ATTN_TIMELINE): per CTA, %globaltimer marks of its first
+// unit -- [0] start, [1] producer past the dependency wait, [2] first page
+// ready (consumer warp 0), [3] last page consumed, [4] output / partial
+// written, [5] split merge done, [6] end
+__device__ long long* g_attn_tl = nullptr;
+__device__ __forceinline__ long long attn_gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define ATL(k) do { if (g_attn_tl) g_attn_tl[blockIdx.x * 8 + (k)] = attn_gtimer(); } while (0)
+
 template <int HD, int CW, int NQT>
 struct AttnCfg {
   static constexpr int HALVES = HD / 64;             // 128-byte column halves (TMA boxes) per row
@@ -113,6 +125,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
   // GEMM still writes (its fused KV append); consumers wait before reading Q.
   // Prefill (rope_append wrote every prompt page) waits up front.
   constexpr bool kEarly = NQT == 1;
+  if (threadIdx.x == 0) ATL(0);
   if (!kEarly) pdl_wait();
   pdl_launch_dependents();
   const int n_items = n_items_dev ? *n_items_dev : n_items_host;
@@ -142,7 +155,11 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
         for (int jj = 0; jj < cnt; ++jj) {
           const int page = __shfl_sync(0xffffffffu, mine, jj);
           if (lane == 0) {
-            if (!waited && (p_lo + j0 + jj + 1) * kPage > I.pos0) { pdl_wait(); waited = true; }
+            if (!waited && (p_lo + j0 + jj + 1) * kPage > I.pos0) {
+              pdl_wait();
+              waited = true;
+              if (u == (int)blockIdx.x) ATL(1);
+            }
             const long long gp = gpage + j0 + jj;
             const int st = (int)(gp % AT_STAGES);
             const uint32_t ph = (uint32_t)((gp / AT_STAGES) & 1);
@@ -210,6 +227,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
       const long long gp = gpage + j;   // gp % CW == warp
       const int st = (int)(gp % AT_STAGES);
       mbar_wait_wd(full0 + 8 * st, (uint32_t)((gp / AT_STAGES) & 1), 200 + st, gp, (long long)it * 1000 + npg);
+      if (threadIdx.x == 0 && j == 0 && u == (int)blockIdx.x) ATL(2);
       const uint32_t kt = sbase + st * C::STAGE_BYTES, vt = kt + C::TILE_BYTES;
       const int tok0 = (p_lo + j) * kPage;
       // ---- S^T = K Q^T (64 tokens x query rows): 4 token tiles of 16
@@ -292,6 +310,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
       if (lane == 0) bar_arrive(empty0 + 8 * st);   // stage free for the producer
     }
     gpage += npg;
+    if (threadIdx.x == 0 && u == (int)blockIdx.x) ATL(3);
     // ---- merge the consumer warps' (m, l, O) in shared memory: [MR] m, [MR] l, [MR][HD] O
 #pragma unroll
     for (int nq = 0; nq < NQT; ++nq)
@@ -345,6 +364,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
         if (c == 0) { pp[r] = M; pp[16 + r] = L; }
       }
     }
+    if (threadIdx.x == 0 && u == (int)blockIdx.x) ATL(4);
     if (I.nsplit > 1) {
       // the last split of this query block to finish merges all splits, in
       // split order (deterministic); the ticket resets itself
@@ -402,8 +422,10 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
         }
       }
     }
+    if (threadIdx.x == 0 && u == (int)blockIdx.x) ATL(5);
     asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
   }
+  if (threadIdx.x == 0) ATL(6);
 }
 
 // decode: <= 8 query rows per unit (1 token x g heads): 6 consumer warps;
@@ -413,6 +435,8 @@ using AttnDec128 = AttnCfg<128, 6, 1>;
 using AttnPre128 = AttnCfg<128, 3, 2>;
 using AttnDec64 = AttnCfg<64, 6, 1>;
 using AttnPre64 = AttnCfg<64, 3, 2>;
+
+void attn_set_timeline(long long* p) { cudaMemcpyToSymbol(g_attn_tl, &p, sizeof p); }
 
 int attn_smem_bytes(int hd) { return hd == 128 ? AttnDec128::SMEM : AttnDec64::SMEM; }
 

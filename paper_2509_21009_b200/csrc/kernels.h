@@ -99,6 +99,7 @@ void launch_ctl(const RoundDev& R, int appended, int mode /*0 all, 1 phase A, 2 
 // responses of the accepted prompts with acceptance index >= first (local)
 void launch_collect_pack(const RoundDev& R, int first, int* meta /*[acc*keep][4]*/, int* tokens, cudaStream_t st);
 int attn_smem_bytes(int hd);
+void attn_set_timeline(long long* p /* [148][8] or nullptr */);
 int attn_init_attrs();
 
 }  // namespace rp
