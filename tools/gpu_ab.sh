@@ -1,2 +1,6 @@
 mkdir -p gpurun_out
-for U in 0 18 9 74; do echo "U=$U"; RP_ATTN_UNITS=$U timeout -s KILL 200 python tools/step_profile.py 256 64 16 2>&1 | grep -A1 "graph_step" | grep -o "graph_step_ms=[0-9.]*\|attention=[0-9.]*"; done
+timeout -s KILL 300 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
+for i in 1 2; do
+timeout -s KILL 200 python tools/step_profile.py 256 192 128 16 2>&1 | grep -A1 "graph_step" | grep -o "B~[0-9]*\|graph_step_ms=[0-9.]*\|gemm_gu=[0-9.]*\|gemm_qkv=[0-9.]*\|rmsnorm=[0-9.]*" | paste -sd' '
+RP_NO_FOLD=1 timeout -s KILL 200 python tools/step_profile.py 256 192 128 16 2>&1 | grep -A1 "graph_step" | grep -o "B~[0-9]*\|graph_step_ms=[0-9.]*\|gemm_gu=[0-9.]*\|gemm_qkv=[0-9.]*\|rmsnorm=[0-9.]*" | paste -sd' '
+done
