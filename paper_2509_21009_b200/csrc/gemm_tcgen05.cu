@@ -21,6 +21,7 @@
 // same 64 features, weights interleaved at init) for gate||up, BF16 store.
 #include <cuda.h>
 #include <cstdint>
+#include <cstdlib>
 #include "common.cuh"
 #include "gemm.h"
 
@@ -83,8 +84,8 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
 }
 // Instruction descriptor, kind::f16: D fp32 (bits 4-5 = 1), A and B fp16
 // (bits 7-9, 10-12 = 0; bf16 would be 1), both K-major, N >> 3, M >> 4.
-__device__ __forceinline__ uint32_t make_idesc(int n) {
-  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+__device__ __forceinline__ uint32_t make_idesc(int n, int m = BM) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                           uint32_t accum) {
@@ -94,6 +95,49 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t 
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(accum));
 }
+// CTA-pair (cta_group::2) forms: the leader issues the M=256 MMA over both
+// CTAs' shared memory (each holds its 128 weight rows and half of the
+// activation rows) into both CTAs' TMEM; commits multicast to both CTAs.
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                              uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(bar)
+      : "memory");
+}
+// shared::cluster address of the same shared-memory offset in cluster CTA 0
+__device__ __forceinline__ uint32_t leader_addr(uint32_t a) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(leader_bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
@@ -188,6 +232,13 @@ __device__ __forceinline__ void push_signal(const GemmArgs& a, int et) {
       asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(a.push_flag[q]) : "memory");
 }
 
+// CG = 1: one CTA per 128-row weight tile.  CG = 2 (no split-K, launched as
+// clusters of 2): a CTA pair per 256-row tile -- each CTA loads its 128
+// weight rows and half of the activation rows, the leader issues
+// tcgen05.mma.cta_group::2 (M = 256) and each CTA's TMEM holds its 128 output
+// rows, so a stage carries half the activation bytes per SM and the ring runs
+// deeper (the wide-batch regime is bound by ring bytes per FLOP).
+template <int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB16,
                     const __grid_constant__ CUtensorMap tmB64, const __grid_constant__ CUtensorMap tmB256,
@@ -195,19 +246,24 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int N = a.n_dev ? *a.n_dev : a.n_host;
   if (N <= 0) return;
   if (threadIdx.x == 0) TL(0);
-  const int m_tiles = a.M / BM;
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0u;
+  const int cta_id = CG == 2 ? (int)blockIdx.x / 2 : (int)blockIdx.x;   // work-unit owner (the pair)
+  const int n_ctas = CG == 2 ? (int)gridDim.x / 2 : (int)gridDim.x;
+  const bool leader = crank == 0;
+  const int m_tiles = a.M / (BM * CG);
   const int n_chunks = (N + BN - 1) / BN;
   const int n_items = m_tiles * n_chunks * a.splits;
-  if ((int)blockIdx.x >= n_items) return;
+  if (cta_id >= n_items) return;                   // both CTAs of a pair leave together
   const int kb_total = a.K / BK;
   // cooperative split-K reduction: grid fits one wave and the chunk is wide
   // enough that a single CTA reducing the whole tile would be the bottleneck
-  const bool coop = a.splits > 1 && n_items <= (int)gridDim.x && min(BN, N) >= 96;
+  const bool coop = a.splits > 1 && n_items <= n_ctas && min(BN, N) >= 96;
 
   // Ring geometry from the widest activation chunk: 16/64/256-row boxes; at
   // small N the stages shrink and the ring deepens (more weight bytes in
   // flight per SM for the HBM-bound small-batch regime).
-  const int wmax = min(BN, N);
+  // (pair: each CTA holds half of the 16-padded chunk, at most 128 rows)
+  const int wmax = CG == 2 ? ((min(BN, N) + 15) & ~15) / 2 : min(BN, N);
   const int brow_max = wmax > 192 ? 256 : wmax > 48 ? 64 : 16;
   const int b_rows = ((wmax + brow_max - 1) / brow_max) * brow_max;
   const int STAGE_BYTES = A_BYTES + ((b_rows * BK * 2 + 1023) & ~1023);
@@ -228,13 +284,19 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) { mbar_init(full0 + 8 * i, 1); mbar_init(empty0 + 8 * i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(tfull0 + 8 * i, 1); mbar_init(tempty0 + 8 * i, 128); }
+    // tempty: 128 epilogue threads (single CTA) or one elected arrival per CTA (pair, leader's barrier)
+    for (int i = 0; i < 2; ++i) { mbar_init(tfull0 + 8 * i, 1); mbar_init(tempty0 + 8 * i, CG == 2 ? 2 : 128); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -244,6 +306,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync_all();                 // the peer's barriers exist before any remote use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) TL(1);
@@ -256,14 +319,23 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
       int stage = 0; uint32_t phase = 0;
       bool first = true;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      for (int it = cta_id; it < n_items; it += n_ctas) {
         Item I = decode_item(it, m_tiles, a.splits);
         const int kb0 = (int)((long)I.split * kb_total / a.splits), kb1 = (int)((long)(I.split + 1) * kb_total / a.splits);
-        const int n0 = I.chunk * BN, nc = min(BN, N - n0);
+        const int wrow = (I.tile * CG + (int)crank) * BM;   // this CTA's 128 weight rows
+        int n0 = I.chunk * BN, nc = min(BN, N - n0);
+        if (CG == 2) {                        // this CTA's half of the 16-padded chunk
+          const int half = ((nc + 15) & ~15) / 2;
+          n0 += (int)crank * half;
+          nc = half;
+        }
         // X boxes: one 256-row box for wide chunks, else a few 64- or 16-row boxes
         const CUtensorMap* tb = nc > 192 ? &tmB256 : nc > 48 ? &tmB64 : &tmB16;
         const int brow = nc > 192 ? 256 : nc > 48 ? 64 : 16;
         const int nbox = (nc + brow - 1) / brow;
+        // pair: the leader arms its full barrier with both CTAs' bytes; every
+        // TMA of the pair completes on the leader's barrier
+        const uint32_t stage_tx = (uint32_t)CG * (A_BYTES + nbox * brow * BK * 2);
         const int cnt = kb1 - kb0;
         // rotate the K order per tile so the CTAs do not all request the same
         // activation tile at the same time (an L2 hot spot); the accumulation
@@ -279,16 +351,19 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           for (int j = 0; j < npre; ++j) {
             const int kb = kb0 + (j + rot) % cnt;
             const uint32_t fb = full0 + 8 * j;
-            mbar_expect_tx(fb, A_BYTES + nbox * brow * BK * 2);
-            tma_load_2d(smem_u32(smem + j * STAGE_BYTES), &tmA, fb, kb * BK, I.tile * BM, pol_w);
+            if (leader) mbar_expect_tx(fb, stage_tx);
+            if (CG == 2) tma_load_2d_pair(smem_u32(smem + j * STAGE_BYTES), &tmA, leader_addr(fb), kb * BK, wrow, pol_w);
+            else tma_load_2d(smem_u32(smem + j * STAGE_BYTES), &tmA, fb, kb * BK, wrow, pol_w);
           }
           pdl_wait();
           for (int j = 0; j < npre; ++j) {
             const int kb = kb0 + (j + rot) % cnt;
             const uint32_t fb = full0 + 8 * j;
             const uint32_t sa = smem_u32(smem + j * STAGE_BYTES);
-            for (int b = 0; b < nbox; ++b)
-              tma_load_2d(sa + A_BYTES + b * brow * BK * 2, tb, fb, kb * BK, n0 + brow * b, pol_x);
+            for (int b = 0; b < nbox; ++b) {
+              if (CG == 2) tma_load_2d_pair(sa + A_BYTES + b * brow * BK * 2, tb, leader_addr(fb), kb * BK, n0 + brow * b, pol_x);
+              else tma_load_2d(sa + A_BYTES + b * brow * BK * 2, tb, fb, kb * BK, n0 + brow * b, pol_x);
+            }
           }
           j0 = npre;
           stage = npre % STAGES;
@@ -298,25 +373,32 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           const int kb = kb0 + (j + rot) % cnt;
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
-          mbar_expect_tx(fb, A_BYTES + nbox * brow * BK * 2);
+          if (leader) mbar_expect_tx(fb, stage_tx);
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-          tma_load_2d(sa, &tmA, fb, kb * BK, I.tile * BM, pol_w);
-          for (int b = 0; b < nbox; ++b)
-            tma_load_2d(sa + A_BYTES + b * brow * BK * 2, tb, fb, kb * BK, n0 + brow * b, pol_x);
+          if (CG == 2) {
+            const uint32_t lb = leader_addr(fb);
+            tma_load_2d_pair(sa, &tmA, lb, kb * BK, wrow, pol_w);
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d_pair(sa + A_BYTES + b * brow * BK * 2, tb, lb, kb * BK, n0 + brow * b, pol_x);
+          } else {
+            tma_load_2d(sa, &tmA, fb, kb * BK, wrow, pol_w);
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d(sa + A_BYTES + b * brow * BK * 2, tb, fb, kb * BK, n0 + brow * b, pol_x);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer (single thread) =====
+    if (lane == 0 && leader) {
+      // ===== MMA issuer (single thread; the pair's leader for CG = 2) =====
       int stage = 0; uint32_t phase = 0; int local = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+      for (int it = cta_id; it < n_items; it += n_ctas, ++local) {
         Item I = decode_item(it, m_tiles, a.splits);
         const int kb0 = (int)((long)I.split * kb_total / a.splits), kb1 = (int)((long)(I.split + 1) * kb_total / a.splits);
         const int nc = min(BN, N - I.chunk * BN);
         const int nmma = (nc + 15) & ~15;
-        const uint32_t idesc = make_idesc(nmma);
+        const uint32_t idesc = make_idesc(nmma, BM * CG);
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
@@ -329,12 +411,16 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint64_t da = make_sdesc(sa), db = make_sdesc(sa + A_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)   // +32 B along K per UMMA_K=16 step
-            umma_f16(tmem_d, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          umma_commit(empty0 + 8 * stage);
+          for (int k = 0; k < BK / 16; ++k) {  // +32 B along K per UMMA_K=16 step
+            if (CG == 2) umma_f16_pair(tmem_d, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            else umma_f16(tmem_d, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          if (CG == 2) umma_commit_pair(empty0 + 8 * stage);
+          else umma_commit(empty0 + 8 * stage);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(tfull0 + 8 * acc);
+        if (CG == 2) umma_commit_pair(tfull0 + 8 * acc);
+        else umma_commit(tfull0 + 8 * acc);
         if (local < 3) TL(3 + 2 * local);
       }
     }
@@ -344,8 +430,9 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     const int et = threadIdx.x - 128;       // 0..127
     int local = 0;
     int rsc_chunk = -1;                     // chunk whose RMSNorm scales are in rsc
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+    for (int it = cta_id; it < n_items; it += n_ctas, ++local) {
       Item I = decode_item(it, m_tiles, a.splits);
+      if (CG == 2) I.tile = I.tile * 2 + (int)crank;   // this CTA's 128-row tile (the pair has no split-K)
       const int n0 = I.chunk * BN, nc = min(BN, N - n0);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
@@ -696,7 +783,12 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       }
       if (!split) {
         tc_fence_before();
-        mbar_arrive(tempty0 + 8 * acc);     // all TMEM reads of this item done
+        if (CG == 2) {                       // one arrival per CTA on the leader's barrier
+          named_bar(1, 128);
+          if (et == 0) mbar_arrive_remote(leader_addr(tempty0 + 8 * acc));
+        } else {
+          mbar_arrive(tempty0 + 8 * acc);   // all TMEM reads of this item done
+        }
       }
       push_signal(a, et);
       if (et == 0 && local < 3) TL(8 + local);
@@ -704,9 +796,11 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync_all();                 // the leader's MMAs into this CTA's TMEM are done
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    if (CG == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
   }
 }
 
@@ -743,10 +837,12 @@ int make_tmap_act(CUtensorMap* map, const void* base, int rows, int cols, int bo
 int gemm_smem_bytes() { return GEMM_SMEM; }
 
 int gemm_init_attrs() {
-  return cudaFuncSetAttribute(gemm_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
-                 cudaSuccess
-             ? 0
-             : -1;
+  const bool ok =
+      cudaFuncSetAttribute(gemm_tcgen05_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
+          cudaSuccess &&
+      cudaFuncSetAttribute(gemm_tcgen05_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
+          cudaSuccess;
+  return ok ? 0 : -1;
 }
 
 int gemm_pick_splits(int M, int K, int n_sms) {
@@ -768,9 +864,31 @@ int gemm_pick_splits(int M, int K, int n_sms) {
   return best;
 }
 
+// With RP_GEMM_PAIR=1, unsplit GEMMs whose weight rows pair up run as CTA
+// pairs (clusters of 2, one per TPC).  Off by default: parity-green, but on
+// the 7B decode step it is ~1% faster above 128 live rows and 2.5-6% slower
+// at 16-64 rows, where the rollout spends most steps
+// (profiles/r01_gemm_chain_experiment.txt).
 void gemm_launch(const GemmPlan& p, const GemmArgs& a, int grid, cudaStream_t st) {
-  launch_pdl(gemm_tcgen05_kernel, dim3(grid), dim3(GEMM_THREADS), GEMM_SMEM, st, p.tmA, p.tmB16, p.tmB64, p.tmB256,
-             a);
+  static const bool pair = getenv("RP_GEMM_PAIR") != nullptr;
+  if (pair && a.splits == 1 && a.M % (2 * BM) == 0 && !a.timeline && grid % 2 == 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = GEMM_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<2>, p.tmA, p.tmB16, p.tmB64, p.tmB256, a);
+    return;
+  }
+  launch_pdl(gemm_tcgen05_kernel<1>, dim3(grid), dim3(GEMM_THREADS), GEMM_SMEM, st, p.tmA, p.tmB16, p.tmB64,
+             p.tmB256, a);
 }
 
 int make_plan(GemmPlan* p, const void* W, int M, int K, const void* X, int rows_cap) {
