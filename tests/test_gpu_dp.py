@@ -56,6 +56,33 @@ def main():
                                                                   len(ref.accepted), good), flush=True)
         ok = ok and good
     eng.close()
+    # full size, in the launch configuration bench.py times at N GPUs: the
+    # first short round of the C2-7b workload (32 prompts x G=8 per GPU,
+    # graphs of 16 steps, data-parallel over the world) against the
+    # single-rank oracle schedule
+    import bench
+    W = bench.Workload("C2-7b", world)
+    lo, hi = W.R["prompt_len"]
+    n_loc = -(-W.n_submit // world)
+    obj = [rp.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    eng = rp.Engine(W.model, max_seqs=n_loc * W.G, max_prompts=n_loc, max_prompt_len=hi,
+                    max_prompt_tokens=n_loc * hi, max_cap=W.R["short_cap"], graph_steps=16, rank=rank,
+                    world=world, nccl_id=obj[0], kv_fraction=0.85)
+    kind, ids, target, cap, L = W.plan()
+    eng.submit([W.prompts[i] for i in ids], W.G, cap, target, trace=L, round_id=0)
+    st = eng.run()
+    res = eng.collect()
+    ref = sched.closed_form(L, cap, target, sched.SHORT)
+    acc = dp.all_gather_ids(list(dict.fromkeys(r["prompt_id"] for r in res)))
+    lo_r, hi_r = dp.partition(len(ids), world)[rank]
+    good = (st.t == ref.t_end and sorted(acc) == sorted(ids[i] for i in ref.accepted) and
+            all(lo_r <= ids.index(r["prompt_id"]) < hi_r and r["len"] == L[ids.index(r["prompt_id"]), r["j"]]
+                for r in res))
+    print("rank %d full-size 7B short round: t_end %d/%d accepted %d/%d ok=%s" % (
+        rank, st.t, ref.t_end, st.accepted, len(ref.accepted), good), flush=True)
+    ok = ok and good
+    eng.close()
     flag = torch.tensor([1 if ok else 0])
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     dist.destroy_process_group()
