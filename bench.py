@@ -193,11 +193,12 @@ def run_ours(a):
         decoded = st.decoded_tokens
         # algorithmic HBM bytes of this rank's decode steps (step 1 comes from the prefill)
         hbm = step_bytes(cfg, e.tp, max(0, st.t - 1), st.decoded_tokens, st.kv_tokens_read)
+        t_roof = round_t_roof(cfg, e.tp, e.rows_histogram(), st.decoded_tokens, st.kv_tokens_read)
         if e is not eng and rank != 0:
             # TP ranks decode the same tokens: count them once (on rank 0)
             decoded, retained, h2d, d2h = 0, 0, 0, 0
         return dict(kind=kind, t_end=st.t, decoded=decoded, retained=retained, h2d=h2d, d2h=d2h,
-                    accepted=st.accepted, underfilled=st.underfilled, tp=e.tp, hbm_bytes=hbm)
+                    accepted=st.accepted, underfilled=st.underfilled, tp=e.tp, hbm_bytes=hbm, t_roof_s=t_roof)
 
     # ---- warm-up (the first warm-up round is profiled per kernel class)
     prof = None
@@ -240,11 +241,13 @@ def run_ours(a):
     tot = torch.tensor([sum(x["decoded"] for x in rounds), sum(x["retained"] for x in rounds),
                         sum(x["h2d"] for x in rounds), sum(x["d2h"] for x in rounds), launches,
                         sum(x["hbm_bytes"] for x in rounds)], dtype=torch.float64)
+    t_roof_all = torch.tensor([sum(x["t_roof_s"] for x in rounds)], dtype=torch.float64)
     per_round = torch.tensor([x["dev_s"] for x in rounds], dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
         dist.all_reduce(per_round, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t_roof_all, op=dist.ReduceOp.MAX)
     dev_s, wall_s = t.tolist()
     decoded, retained, h2d, d2h, launches_all, hbm_all = tot.tolist()
     per_round = per_round.tolist()
@@ -295,6 +298,12 @@ def run_ours(a):
     if prof is not None:
         line["roofline"], line["kernel_profile"] = roofline(prof, cfg)
     peak_hbm = load_peaks()[0]
+    line["round_roofline"] = {
+        "t_roof_s": round(t_roof_all.item(), 3), "t_measured_s": round(dev_s, 3),
+        "frac": round(t_roof_all.item() / dev_s, 4),
+        "formula": "sum over decode steps t of max(W/BW, 2 P B_t / peak_tensor) + KV_t/BW + logits_t/BW "
+                   "(SURVEY section 8(d)); B_t from the device histogram of live rows per step, "
+                   "BW and peak_tensor (sustained) from MEASURED_PEAKS.json; max over ranks"}
     line["step_roofline"] = {
         "bound": "hbm", "unit": "GB/s", "achieved": round(hbm_all / dev_s / 1e9, 1), "peak": peak_hbm * world,
         "frac": round(hbm_all / dev_s / 1e9 / (peak_hbm * world), 4),
@@ -360,6 +369,22 @@ def step_bytes(cfg, tp, steps, rows, kv_tokens):
     local KV head + fp32 logits written by the LM head and read by the sampler."""
     L, KV, hd, V = cfg["n_layers"], cfg["n_kv_heads"] // tp, cfg["head_dim"], cfg["vocab"] // tp
     return steps * weight_bytes(cfg, tp) + kv_tokens * L * KV * hd * 2 * 2 + rows * V * 4 * 2
+
+
+def round_t_roof(cfg, tp, hist, rows, kv_tokens):
+    """Roofline time of one round's decode steps on one rank:
+    every step streams the weight shard or runs its GEMM FLOPs at the tensor
+    peak, whichever is longer, plus the KV reads and the logits traffic."""
+    bw, _, tf_sus, _ = load_peaks()
+    w = weight_bytes(cfg, tp)
+    p = w / 2                                           # parameters streamed per step (16-bit)
+    L, KV, hd, V = cfg["n_layers"], cfg["n_kv_heads"] // tp, cfg["head_dim"], cfg["vocab"] // tp
+    t = 0.0
+    for r, steps in enumerate(hist):
+        if steps:
+            t += steps * max(w / (bw * 1e9), 2.0 * p * r / (tf_sus * 1e12))
+    t += kv_tokens * L * KV * hd * 2 * 2 / (bw * 1e9) + rows * V * 4 * 2 / (bw * 1e9)
+    return t
 
 
 def load_peaks():

@@ -94,7 +94,8 @@ typedef struct {
                                 tp > 1 (world must be 1) the context holds only its shard:
                                 heads, KV heads, d_ff and vocab / tp (column-parallel QKV,
                                 gate||up and LM head, row-parallel O and down with an fp32
-                                NCCL all-reduce after each; vocab-sharded sampling with a
+                                all-reduce after each -- NCCL, or at decode the NVLink peer
+                                push of rp_tp_ipc_open; vocab-sharded sampling with a
                                 MAX all-reduce of the packed argmax).  Every TP rank submits
                                 the same prompts and keeps identical round state. */
   int32_t tp_rank;           /* rank inside the TP group */
@@ -197,6 +198,11 @@ int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, i
  * sizes.  Errors: RP_ESTATE (no round), RP_EINVAL (first), RP_ENOSPC. */
 int rp_collect_ready(void* ctx, int32_t first, rp_response* out, int32_t max_out, int32_t* tok_buf, int64_t tok_cap,
                      int32_t* n_out, int64_t* n_tok, int32_t* n_accepted);
+
+/* Measurement: out[r] = decode steps of the current (or last) round on this
+ * rank that decoded r live rows, r = 0..n-1 (rows above max_seqs read 0).
+ * Lets the caller compute the per-round roofline of SURVEY §8(d). */
+int rp_round_rows_histogram(void* ctx, int64_t* out, int32_t n);
 
 /* Snapshot of the long-prompt queue (global prompt ids, oldest first); no
  * drain.  ids_out may be NULL to query *n_out. */

@@ -262,6 +262,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto invf = cv.take<double>(hd / 2);
   auto rope_cs = cv.take<float2>((size_t)(rd->max_prompt_len + rd->max_cap + 2) * (hd / 2));
   auto items_dec = cv.take<AttnItem>(z.max_items_dec);
+  auto rows_hist = cv.take<unsigned long long>((size_t)z.S + 1);
   auto items_pre = cv.take<AttnItem>(z.max_items_pre);
   auto pre_tok = cv.take<int>(rd->max_prompt_tokens);
   auto pre_pos = cv.take<int>(rd->max_prompt_tokens);
@@ -313,7 +314,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
     R.status = status; R.own0 = own0; R.tok_out = tok_out; R.page_table = page_table; R.p_cnt = p_cnt;
     R.p_state = p_state; R.p_gid = p_gid; R.comp_list = comp_list; R.accept_order = accept_order;
     R.live = live; R.live_next = live_next; R.tok_in = tok_in; R.row_pos = row_pos; R.row_pt = row_pt;
-    R.best = best; R.items = items_dec; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
+    R.best = best; R.items = items_dec; R.rows_hist = rows_hist; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
     R.ctl = ctl; R.cap = rd->max_cap;
   }
   return align_up(cv.off);
@@ -996,6 +997,7 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
     c->launches++;
   }
   CK(cudaMemcpyAsync(R.free_stack, c->identity_pages, (size_t)c->n_pages * 4, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemsetAsync(R.rows_hist, 0, ((size_t)c->z.S + 1) * sizeof(unsigned long long), c->st));
   CtlBlock cb{};
   cb.n_live = nS; cb.t = 1; cb.free_top = top;
   *c->h_ctl = cb;
@@ -1194,6 +1196,17 @@ int rp_tp_ipc_open(void* ctx, const void* handles) {
   }
   c->tp_peer = true;
   c->graph_dirty = true;
+  return RP_OK;
+}
+
+int rp_round_rows_histogram(void* ctx, int64_t* out, int32_t n) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c || !out || n < 1) return RP_EINVAL;
+  const int m = std::min(n, c->z.S + 1);
+  std::vector<unsigned long long> h(m);
+  CK(cudaMemcpyAsync(h.data(), c->R.rows_hist, (size_t)m * 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  for (int i = 0; i < n; ++i) out[i] = i < m ? (int64_t)h[i] : 0;
   return RP_OK;
 }
 

@@ -110,7 +110,10 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     R.status[s] = fin ? ST_FINISHED : capped ? ST_CAPPED : ST_LIVE;
     if (fin || (capped && R.kind == 1)) atomicAdd(&R.p_cnt[R.slot_prompt[s]], 1);
   }
-  if (tid == 0) { s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; s_ctx = 0; s_rd = 0; }
+  if (tid == 0) {
+    s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; s_ctx = 0; s_rd = 0;
+    if (appended && R.rows_hist) R.rows_hist[n] += 1;   // one decode step over n rows
+  }
   __syncthreads();
   // prompts completing at step t, in prompt-index order.  A prompt completes
   // when `keep` of its responses have finished ("finishing after

@@ -56,6 +56,7 @@ struct RoundDev {
   int* tok_in; int* row_pos; int* row_pt;
   unsigned long long* best;
   AttnItem* items;
+  unsigned long long* rows_hist;  // [S + 1] decode steps of this round by live rows (measurement)
   int* free_stack;
   int* ks_local;      // [3]: prompts completed at this step, rows still live, error
   int* ks;            // [3 * world] all-gathered ks_local (== ks_local when world == 1)

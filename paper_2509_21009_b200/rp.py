@@ -62,7 +62,7 @@ class Response(ctypes.Structure):
 EXPORTS = ["rp_query_sizes", "rp_init_model", "rp_submit_round", "rp_step", "rp_collect", "rp_long_queue",
            "rp_free", "rp_last_error", "rp_launch_count", "rp_debug_logits", "rp_debug_trace_enable",
            "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm", "rp_debug_profile", "rp_nccl_unique_id",
-           "rp_tp_ipc_handle", "rp_tp_ipc_open", "rp_collect_ready"]
+           "rp_tp_ipc_handle", "rp_tp_ipc_open", "rp_collect_ready", "rp_round_rows_histogram"]
 
 
 def load_library(path=LIB_PATH):
@@ -94,6 +94,7 @@ def load_library(path=LIB_PATH):
     lib.rp_nccl_unique_id.argtypes = [P]
     lib.rp_tp_ipc_handle.argtypes = [P, P]
     lib.rp_tp_ipc_open.argtypes = [P, P]
+    lib.rp_round_rows_histogram.argtypes = [P, ctypes.POINTER(I64), I32]
     lib.rp_collect_ready.argtypes = [P, I32, ctypes.POINTER(Response), I32, ctypes.POINTER(I32), I64,
                                      ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I32)]
     for name in EXPORTS:
@@ -294,6 +295,13 @@ class Engine:
         res = [dict(prompt_id=out[i].prompt_id, j=out[i].j, len=out[i].len, finish=out[i].finish,
                     tokens=toks[out[i].tok_off:out[i].tok_off + out[i].len].copy()) for i in range(n.value)]
         return res, na.value
+
+    def rows_histogram(self):
+        """Decode steps of the current/last round by live-row count (index = rows)."""
+        out = np.zeros(self.max_seqs + 1, dtype=np.int64)
+        self._check(self.L.rp_round_rows_histogram(self.h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                                   len(out)))
+        return out
 
     def long_queue(self):
         n = ctypes.c_int32()

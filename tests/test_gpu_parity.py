@@ -108,6 +108,11 @@ def test_short_round_schedule_bit_exact(tiny, seed, graph_steps):
     st = eng.run()
     ref = _check_round_trace(eng, L, cap, target, sched.SHORT)
     assert st.t == ref.t_end and st.accepted == len(ref.accepted) and bool(st.underfilled) == ref.underfilled
+    # device histogram of live rows per decode step (bench round_roofline) = the oracle's live counts
+    # of steps 2..t_end (step 1 samples from the prefill logits)
+    hist = eng.rows_histogram()
+    want = np.bincount([len(x["live"]) for x in ref.steps[1:]], minlength=len(hist))
+    assert np.array_equal(hist, want[:len(hist)])
     res = eng.collect()
     acc = list(dict.fromkeys(r["prompt_id"] for r in res))
     assert acc == [ps[i]["prompt_id"] for i in ref.accepted]
