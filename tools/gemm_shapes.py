@@ -1,5 +1,5 @@
-"""Time single GEMM launches (rp_debug_gemm, L2 flushed before the timed
-loop) at given shapes: python tools/gemm_shapes.py M,K,N [M,K,N ...]"""
+"""Time single GEMM launches (rp_debug_gemm) at given shapes and split-K
+factors: python tools/gemm_shapes.py M,K,N [M,K,N ...] [--splits 0,1,2]"""
 import os
 import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -10,11 +10,17 @@ from synth.configs import model_config
 torch.cuda.set_device(0)
 eng = rp.Engine(model_config("tiny"), max_seqs=256, max_prompts=16, max_prompt_len=64, max_prompt_tokens=512,
                 max_cap=64, kv_pool_bytes=64 << 20, graph_steps=0)
-for spec in sys.argv[1:]:
+args = sys.argv[1:]
+splits = [0, 1, 2]
+if "--splits" in args:
+    i = args.index("--splits")
+    splits = [int(x) for x in args[i + 1].split(",")]
+    args = args[:i] + args[i + 2:]
+for spec in args:
     M, K, N = (int(x) for x in spec.split(","))
     W = (torch.randn(M, K, device="cuda") * 0.02).to(torch.float16)
     X = torch.randn(512, K, device="cuda").to(torch.float16)
-    for sp in (0, 1, 2):
+    for sp in splits:
         _, ms = eng.debug_gemm(W, X, N, splits=sp, iters=5, timed=True)
         us = ms * 1e3
         print("M=%d K=%d N=%d splits=%s: %.1f us  %.2f TB/s  %.0f TFLOP/s" % (
