@@ -187,9 +187,10 @@ def test_dp_protocol_matches_single_rank(world):
         n = int(rng.integers(world, 40))
         L = rng.integers(1, 60, size=(n, 4))
         target = int(rng.integers(1, n + 1))
-        ref = X.closed_form(L, 50, target, X.SHORT)
-        t_end, acc, _ = X.dp_protocol(L, 50, target, X.SHORT, world)
-        assert t_end == ref.t_end and acc == ref.accepted
+        for keep in (None, 3, 1):               # also under response-level speculation (keep < G)
+            ref = X.closed_form(L, 50, target, X.SHORT, keep=keep)
+            t_end, acc, _ = X.dp_protocol(L, 50, target, X.SHORT, world, keep=keep)
+            assert t_end == ref.t_end and acc == ref.accepted
 
 
 def test_partition_contiguous():
