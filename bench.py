@@ -446,7 +446,9 @@ def roofline(prof, cfg):
             detail[k]["tflops"] = round(gemm_flops[k] / t / 1e12, 1)
     if cnt.get("attention"):
         t = ms["attention"] / cnt["attention"] / 1e3
-        detail["attention"]["hbm_gbs"] = round(attn_bytes / t / 1e9, 1)
+        # bytes of every row's full context: the prompt pages the G siblings share are re-read
+        # (mostly from L2), so this is an effective rate; the DRAM traffic is in profiles/ (ncu)
+        detail["attention"]["context_gbs"] = round(attn_bytes / t / 1e9, 1)
     if dom == "attention":
         ach = attn_bytes / (per_launch_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4)}
