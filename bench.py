@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--profile-steps", type=int, default=24)
     ap.add_argument("--max-rounds-steps", type=int, default=0, help="debug: cap decode steps per round (invalid)")
     ap.add_argument("--out", default="")
+    ap.add_argument("--schedule", default="tail", choices=["tail", "sync"],
+                    help="tail batching (default) or the plain synchronous rollout baseline on the same stream")
     ap.add_argument("--long-tp", default="auto", choices=["auto", "1", "n"],
                     help="long-round tensor parallelism: auto = smallest TP whose worst-case KV fits (planner), "
                          "1 = data-parallel replicas, n = one TP group over all GPUs")
@@ -54,7 +56,7 @@ class Workload:
     """Deterministic prompt stream + length trace + the tail-batching planner
     state (global FIFO of deferred prompt ids)."""
 
-    def __init__(self, cfg_name, world):
+    def __init__(self, cfg_name, world, schedule="tail"):
         self.R = configs.ROUNDS[cfg_name]
         self.model = configs.model_config(self.R["model"])
         self.world = world
@@ -69,8 +71,14 @@ class Workload:
         from paper_2509_21009_b200.dp import GlobalQueue
         self.queue = GlobalQueue()
         self.next_fresh = 0
+        # "tail": the planner of S:271-279; "sync": plain synchronous rollout (the
+        # veRL baseline): every RL step decodes P0 fresh prompts to completion
+        self.schedule = schedule
 
     def plan(self):
+        if self.schedule == "sync":
+            ids = list(range(self.next_fresh, self.next_fresh + self.P0))
+            return "long", ids, self.P0, self.R["long_cap"], self.trace[ids, 0, :]
         if len(self.queue) >= self.P0:
             ids = self.queue.ids[:self.P0]
             return "long", ids, self.P0, self.R["long_cap"], self.trace[ids, 1, :]
@@ -78,6 +86,9 @@ class Workload:
         return "short", ids, self.P0, self.R["short_cap"], self.trace[ids, 0, :]
 
     def commit(self, kind, ids, accepted_ids):
+        if self.schedule == "sync":
+            self.next_fresh += len(ids)
+            return
         if kind == "long":
             self.queue.pop(len(ids))
         else:
@@ -139,7 +150,7 @@ def run_ours(a):
         # communicator inside the CUDA graph (a second NCCL group in the same
         # process deadlocked at init on this image)
         dist.init_process_group("gloo")
-    W = Workload(a.config, world)
+    W = Workload(a.config, world, a.schedule)
     cfg, G = W.model, W.G
     # per-rank capacities
     n_loc = math.ceil(W.n_submit / world)
@@ -321,9 +332,11 @@ def run_ours(a):
 
 def bench_config(W, parallelism, graph_steps):
     """The workload description shared by both arms (BASELINE.json configs[1], per GPU)."""
+    sched = ("tail batching (eta=1.25)" if W.schedule == "tail" else
+             "plain synchronous rollout baseline: P0 fresh prompts per RL step decoded to completion")
     return {"workload": "BASELINE configs[1]: Qwen2.5-7B-shaped, %d prompts x G=%d per GPU, short cap %d, "
-                        "target floor(n/1.25), tail batching (eta=1.25), trace mode" % (
-                            W.R["n_submit"], W.G, W.R["short_cap"]),
+                        "target floor(n/1.25), %s, trace mode" % (W.R["n_submit"], W.G, W.R["short_cap"], sched),
+            "schedule": W.schedule,
             "global_prompts_per_short_round": W.n_submit, "P0": W.P0, "G": W.G,
             "short_cap": W.R["short_cap"], "long_cap": W.R["long_cap"], "parallelism": parallelism,
             "l2": "inputs larger than L2 (14 GB of weights streamed per decode step)", "graph_steps": graph_steps}
