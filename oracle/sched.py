@@ -199,6 +199,168 @@ def step_loop(L, cap, target, kind, with_steps=False, keep=None):
     return r
 
 
+# ------------------------------------------- continuous issuance (NEXT-4)
+#
+# P:1386 (DAPO integration): "we set a maximum number of active requests for
+# each LLM instance and continuously issue new requests ... other unfinished
+# prompts are retained in the queue".  Readings (Z21): a request is
+# a prompt with its G responses; a prompt is active from its issue step tau
+# until none of its responses is live; after each step the lowest-index
+# unissued prompts are issued while fewer than `max_active` are active; a
+# prompt issued at tau emits its k-th token at step tau + k - 1 (tau = 1 for
+# the first min(max_active, n)); acceptance, the cutoff and the keep rule are
+# those of the plain round; prompts never issued before the round ends are
+# returned unissued (neither accepted nor deferred).
+
+UNISSUED = 0
+
+
+@dataclass
+class IssueRound(Round):
+    issue_step: np.ndarray = None   # [n] tau_i, 0 if never issued
+    unissued: list = field(default_factory=list)
+
+
+def issue_step_loop(L, cap, target, kind, max_active, with_steps=False, keep=None):
+    """Literal step loop of a round with continuous issuance: each step every
+    live response emits its next token; endings, completions, acceptance and
+    sibling aborts as in `step_loop`; then prompts are issued in index order
+    while fewer than `max_active` prompts have a live response."""
+    L = np.asarray(L, np.int64)
+    n, G = L.shape
+    keep = G if (keep is None or kind == LONG) else keep
+    if kind == LONG:
+        target = n
+    tau = np.zeros(n, np.int64)
+    kept = np.zeros((n, G), bool)
+    done_p = [False] * n
+    cnt = [0] * n
+    outcome = np.zeros((n, G), np.int32)
+    nxt = min(max_active, n)
+    tau[:nxt] = 1
+    live = list(range(nxt * G))
+    accepted, steps = [], []
+    t = 0
+    while True:
+        t += 1
+        decoded = list(live)
+        ending, completed = [], []
+        for s in decoded:
+            i, j = divmod(s, G)
+            k = t - tau[i] + 1                     # local token index
+            if k == L[i, j]:
+                outcome[i, j] = FINISHED
+                ending.append(s)
+                if not done_p[i] and cnt[i] < keep:
+                    cnt[i] += 1
+                    kept[i, j] = True
+                    if cnt[i] == keep:
+                        completed.append(i)
+            elif k == cap:
+                outcome[i, j] = CAPPED
+                ending.append(s)
+                if kind == LONG:
+                    cnt[i] += 1
+                    kept[i, j] = True
+                    if cnt[i] == G:
+                        completed.append(i)
+        for i in completed:
+            done_p[i] = True
+        for i in sorted(completed):
+            if len(accepted) < target:
+                accepted.append(i)
+        for s in decoded:
+            if s not in ending and done_p[s // G]:
+                outcome[s // G, s % G] = ABORTED
+        live = [s for s in decoded if s not in set(ending) and not done_p[s // G]]
+        active = len(set(s // G for s in live))
+        done = len(accepted) == target
+        while not done and active < max_active and nxt < n:      # issue after step t
+            tau[nxt] = t + 1
+            live.extend(range(nxt * G, nxt * G + G))
+            nxt += 1
+            active += 1
+        done = done or not live
+        if with_steps:
+            steps.append(dict(t=t, live=np.array(decoded, np.int32), ending=np.array(ending, np.int32),
+                              counts=np.array(cnt, np.int32), accepted=len(accepted), done=int(done)))
+        if done:
+            break
+    for s in live:
+        if tau[s // G] <= t:
+            outcome[s // G, s % G] = ABORTED
+    unissued = [i for i in range(n) if tau[i] == 0 or tau[i] > t]
+    tau[unissued] = 0
+    deferred = [i for i in range(n) if i not in accepted and i not in unissued]
+    retained = np.zeros((n, G), np.int64)
+    for i in accepted:
+        retained[i] = np.where(kept[i], np.minimum(L[i], cap), 0)
+    return IssueRound(kind, t, accepted, deferred, len(accepted) < target, outcome, retained, steps,
+                      issue_step=tau, unissued=unissued)
+
+
+def issue_closed_form(L, cap, target, kind, max_active, keep=None, with_steps=False):
+    """The same round from its definition as list scheduling: prompt i is
+    active for d_i steps (T_i if it completes, else its longest response,
+    e = min(L, cap)), independent of when it is issued; prompts take the
+    earliest-freed of `max_active` slots in index order (tau_i = 1 + the
+    step the slot freed); prompt i completes at C_i = tau_i + T_i - 1; the
+    first `target` by (C_i, i) are accepted and t_end is the target-th
+    completion (else the last active step); prompts with tau_i > t_end are
+    unissued."""
+    import heapq
+    L = np.asarray(L, np.int64)
+    n, G = L.shape
+    keep = G if (keep is None or kind == LONG) else keep
+    INF = np.iinfo(np.int64).max
+    e0 = _e(L, cap)
+    if kind == SHORT:
+        kept, T = _kept(L, cap, keep)
+        e = np.minimum(e0, T[:, None])
+    else:
+        kept = np.ones((n, G), bool)
+        T = e0.max(axis=1)
+        e = e0
+        target = n
+    d = e.max(axis=1)                                   # steps a prompt stays active
+    tau = np.zeros(n, np.int64)
+    slots = []
+    for i in range(n):
+        if i < max_active:
+            tau[i] = 1
+        else:
+            tau[i] = heapq.heappop(slots) + 1
+        heapq.heappush(slots, int(tau[i] + d[i] - 1))
+    C = np.where(T < INF, tau + np.where(T < INF, T, 0) - 1, INF)
+    order = sorted(range(n), key=lambda i: (C[i], i))
+    n_fin = int(np.sum(C < INF))
+    n_acc = min(target, n_fin)
+    accepted = order[:n_acc]
+    underfilled = n_fin < target
+    t_end = int(C[order[target - 1]]) if not underfilled else int(np.max(tau + d - 1))
+    unissued = [i for i in range(n) if tau[i] > t_end]
+    deferred = [i for i in range(n) if i not in set(accepted) and i not in set(unissued)]
+    end_abs = tau[:, None] + e - 1                      # last step each response decodes
+    outcome = np.where(L <= cap, FINISHED, CAPPED)
+    outcome = np.where((tau[:, None] + e0 - 1 > t_end) | ((e0 > e) & (kind == SHORT)), ABORTED, outcome)
+    outcome[unissued] = UNISSUED
+    retained = np.zeros_like(L)
+    for i in accepted:
+        retained[i] = np.where(kept[i], e0[i], 0)
+    tau_out = tau.copy()
+    tau_out[unissued] = 0
+    r = IssueRound(kind, t_end, accepted, deferred, bool(underfilled), outcome.astype(np.int32), retained,
+                   issue_step=tau_out, unissued=unissued)
+    if with_steps:
+        tflat, endf = np.repeat(tau, G), end_abs.reshape(-1)
+        for t in range(1, t_end + 1):
+            live = np.nonzero((tflat <= t) & (endf >= t))[0].astype(np.int32)
+            acc = sum(1 for p in order[:n_acc] if C[p] <= t)
+            r.steps.append(dict(t=t, live=live, accepted=acc,
+                                done=int(acc == target or t == t_end)))
+    return r
+
+
 # ---------------------------------------------------------------- DP (C3)
 
 def partition(n, world):

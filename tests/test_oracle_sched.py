@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from oracle import sched as X
+from oracle import sched
 from synth.gen import length_trace
 
 
@@ -195,3 +196,93 @@ def test_dp_protocol_matches_single_rank(world):
 
 def test_partition_contiguous():
     assert X.partition(10, 4) == [(0, 3), (3, 6), (6, 8), (8, 10)]
+
+
+# ---------------------------------------------------------------- NEXT-4 continuous issuance
+
+def _issue_equal(a, b, steps=True):
+    assert a.t_end == b.t_end and a.accepted == b.accepted and a.deferred == b.deferred
+    assert a.unissued == b.unissued and a.underfilled == b.underfilled
+    assert np.array_equal(a.issue_step, b.issue_step)
+    assert np.array_equal(a.outcome, b.outcome) and np.array_equal(a.retained_len, b.retained_len)
+    if steps:
+        assert len(a.steps) == len(b.steps)
+        for x, y in zip(a.steps, b.steps):
+            assert np.array_equal(x["live"], y["live"]) and x["accepted"] == y["accepted"] and x["done"] == y["done"]
+
+
+def test_issue_hand_worked():
+    # G = 1, at most 2 active, lengths 3 1 2 4, target 3.  Steps 1: {0, 1}; 1 ends -> 2 issued at 2;
+    # step 3: 0 and 2 end, 3 accepted -> done; prompt 3 (tau would be 4) is never issued.
+    L = np.array([[3], [1], [2], [4]])
+    for r in (sched.issue_step_loop(L, 8, 3, sched.SHORT, 2, with_steps=True),
+              sched.issue_closed_form(L, 8, 3, sched.SHORT, 2, with_steps=True)):
+        assert r.t_end == 3 and r.accepted == [1, 0, 2] and r.deferred == [] and r.unissued == [3]
+        assert list(r.issue_step) == [1, 1, 2, 0]
+        assert [list(s["live"]) for s in r.steps] == [[0, 1], [0, 2], [0, 2]]
+    # a prompt that can never complete (capped response) holds its slot until its last response ends
+    L = np.array([[9, 1], [1, 1], [2, 2]])
+    r = sched.issue_step_loop(L, 4, 2, sched.SHORT, 1)
+    # prompt 0 holds the only slot for 4 steps (capped at 4), 1 runs at step 5, 2 at 6-7
+    assert list(r.issue_step) == [1, 5, 6] and r.accepted == [1, 2] and r.t_end == 7 and r.deferred == [0]
+
+
+def test_issue_reduces_to_plain_round():
+    """max_active >= n issues everything at step 1: the plain round."""
+    rng = np.random.default_rng(11)
+    for _ in range(300):
+        n, G = int(rng.integers(1, 8)), int(rng.integers(1, 4))
+        L = rng.integers(1, 10, (n, G))
+        cap = int(rng.integers(1, 10))
+        kind = int(rng.integers(0, 2))
+        target = int(rng.integers(1, n + 1)) if kind == sched.SHORT else n
+        keep = int(rng.integers(1, G + 1)) if kind == sched.SHORT else None
+        a = sched.issue_step_loop(L, cap, target, kind, n + int(rng.integers(0, 3)), keep=keep)
+        b = sched.closed_form(L, cap, target, kind, keep=keep)
+        assert a.t_end == b.t_end and a.accepted == b.accepted and a.deferred == b.deferred and a.unissued == []
+        assert np.array_equal(a.outcome, b.outcome) and np.array_equal(a.retained_len, b.retained_len)
+
+
+def test_issue_step_loop_vs_list_scheduling_exhaustive():
+    """Two formulations -- the literal step loop and list scheduling of the
+    prompts' (issue-independent) active durations -- agree on every n <= 3,
+    G <= 2 trace of lengths 1..3 for every cap, max_active, target and keep."""
+    import itertools
+    for G in (1, 2):
+        for n in (1, 2, 3):
+            for Ls in itertools.product(range(1, 4), repeat=n * G):
+                L = np.array(Ls).reshape(n, G)
+                for cap in (1, 2, 3):
+                    for A in range(1, n + 1):
+                        for kind in (sched.SHORT, sched.LONG):
+                            for target in (range(1, n + 1) if kind == sched.SHORT else [n]):
+                                for keep in (range(1, G + 1) if kind == sched.SHORT else [None]):
+                                    _issue_equal(sched.issue_step_loop(L, cap, target, kind, A, True, keep),
+                                                 sched.issue_closed_form(L, cap, target, kind, A, keep, True))
+
+
+def test_issue_invariants_random():
+    rng = np.random.default_rng(12)
+    for _ in range(400):
+        n, G = int(rng.integers(1, 10)), int(rng.integers(1, 5))
+        L = rng.integers(1, 14, (n, G))
+        cap = int(rng.integers(1, 14))
+        A = int(rng.integers(1, n + 1))
+        target = int(rng.integers(1, n + 1))
+        keep = int(rng.integers(1, G + 1))
+        r = sched.issue_step_loop(L, cap, target, sched.SHORT, A, True, keep)
+        _issue_equal(r, sched.issue_closed_form(L, cap, target, sched.SHORT, A, keep, True))
+        tau = r.issue_step
+        issued = [i for i in range(n) if tau[i] > 0]
+        assert issued == list(range(len(issued)))                          # index order
+        assert r.unissued == list(range(len(issued), n))
+        assert sorted(r.accepted + r.deferred + r.unissued) == list(range(n))
+        for s in r.steps:
+            active = set(int(x) // G for x in s["live"])
+            assert len(active) <= A
+            # work conserving: a free slot is never left idle while prompts wait
+            waiting = [i for i in range(n) if tau[i] == 0 or tau[i] > s["t"]]
+            if len(active) < A and waiting and s["t"] < r.t_end:
+                assert all(tau[i] == 0 or tau[i] > s["t"] for i in waiting)
+                nxt = s["t"] + 1
+                assert any(tau[i] == nxt for i in range(n)) or not waiting or r.t_end == s["t"]
