@@ -204,6 +204,29 @@ int rp_collect_ready(void* ctx, int32_t first, rp_response* out, int32_t max_out
  * Lets the caller compute the per-round roofline of SURVEY §8(d). */
 int rp_round_rows_histogram(void* ctx, int64_t* out, int32_t n);
 
+/* Continuous issuance (DAPO integration:
+ * "set a maximum number of active requests for each LLM instance and
+ * continuously issue new requests"; readings Z21).  Applies to the rounds
+ * submitted after the call; max_active = 0 (the default) turns it off.  With
+ * max_active = A > 0 at most A of this rank's prompts have a live response at
+ * any step: the first min(A, n_local) start at step 1, and after every step
+ * the lowest-index unissued prompts are issued while fewer than A are active
+ * (a prompt stays active until none of its responses is live).  A prompt
+ * issued after step t decodes its last prompt token at step t + 1 and emits
+ * its k-th token at step t + k (the sampler counter is the response's token
+ * index k, so its tokens do not depend on when it was issued); its other
+ * plen - 1 tokens are prefilled at submit, so every prompt of such a round
+ * needs len >= 2 beyond the first A.  Acceptance, the cutoff, keep and the
+ * cap are unchanged.  Prompts never issued when the round ends are neither
+ * accepted nor deferred: rp_round_unissued lists them.  Errors: RP_EINVAL
+ * (max_active < 0), RP_EBUSY (a round is active). */
+int rp_round_issue_cap(void* ctx, int32_t max_active);
+
+/* Global ids of this rank's prompts the finished round never issued
+ * (continuous issuance; in submission order).  ids_out may be NULL to query
+ * *n_out.  Errors: RP_ESTATE (round not done), RP_ENOSPC (max too small). */
+int rp_round_unissued(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out);
+
 /* Snapshot of the long-prompt queue (global prompt ids, oldest first); no
  * drain.  ids_out may be NULL to query *n_out. */
 int rp_long_queue(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out);

@@ -127,6 +127,8 @@ struct RpCtx {
   // round state (host)
   bool active = false, collected = true;
   int kind = 0, trace = 0, G = 0, keep = 0, cap = 0, target = 0, n_glob = 0, lo = 0, n_loc = 0;
+  int issue_cap = 0;       // rp_round_issue_cap: applies to the next submitted rounds
+  int max_active = 0;      // of the current round (0 = every prompt issued at submit)
   int64_t round_id = 0;
   std::vector<QueuedPrompt> round_prompts;  // this rank's slice
   std::deque<QueuedPrompt> fifo;
@@ -279,6 +281,9 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto trace_L = cv.take<int>(z.S);
   auto status = cv.take<int>(z.S);
   auto own0 = cv.take<int>(z.S);
+  auto t0 = cv.take<int>(z.S);
+  auto p_last_tok = cv.take<int>(z.P);
+  auto p_stamp = cv.take<int>(z.P);
   auto tok_out = cv.take<int>((size_t)z.S * rd->max_cap);
   auto page_table = cv.take<int>((size_t)z.pt_rows * z.maxp);
   auto p_cnt = cv.take<int>(z.P);
@@ -311,7 +316,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
     R.world = rd->world; R.rank = rd->rank;
     R.attn_units = getenv("RP_ATTN_UNITS") ? atoi(getenv("RP_ATTN_UNITS")) : 0;   // measurement override
     R.slot_prompt = slot_prompt; R.slot_j = slot_j; R.kv_len = kv_len; R.gen = gen; R.trace_L = trace_L;
-    R.status = status; R.own0 = own0; R.tok_out = tok_out; R.page_table = page_table; R.p_cnt = p_cnt;
+    R.status = status; R.own0 = own0; R.t0 = t0; R.p_last_tok = p_last_tok; R.p_stamp = p_stamp; R.tok_out = tok_out; R.page_table = page_table; R.p_cnt = p_cnt;
     R.p_state = p_state; R.p_gid = p_gid; R.comp_list = comp_list; R.accept_order = accept_order;
     R.live = live; R.live_next = live_next; R.tok_in = tok_in; R.row_pos = row_pos; R.row_pt = row_pt;
     R.best = best; R.items = items_dec; R.rows_hist = rows_hist; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
@@ -937,22 +942,34 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   for (int i = 0; i < n_loc; ++i) T += (long long)all[lo + i].tokens.size();
   if (T > c->rd.max_prompt_tokens) return c->fail(RP_ENOSPC, "prompt tokens %lld > max_prompt_tokens", T);
 
+  // continuous issuance: the first min(A, n_loc) prompts start at step 1, the
+  // others are prefilled without their last token, which they decode as their
+  // first step once issued (oracle sched.issue_step_loop)
+  const int A = c->issue_cap > 0 ? std::min(c->issue_cap, n_loc) : 0;
+  if (A > 0)
+    for (int i = A; i < n_loc; ++i)
+      if (all[lo + i].tokens.size() < 2)
+        return c->fail(RP_EINVAL, "invalid field: prompts[%d].len (continuous issuance needs >= 2)", lo + i);
   c->kind = kind; c->trace = trace; c->G = G; c->keep = keep; c->cap = cap; c->target = target; c->n_glob = n;
+  c->max_active = A;
   c->lo = lo; c->n_loc = n_loc; c->round_id = round_id;
   c->round_prompts.assign(all.begin() + lo, all.begin() + lo + n_loc);
   RoundDev& R = c->R;
   R.cap = cap; R.G = G; R.keep = keep; R.target = target; R.kind = kind; R.trace = trace; R.n_prompts = n_loc;
+  R.max_active = A;
+  const int n_first = A > 0 ? A : n_loc;   // prompts live at step 1
   R.trace_buf = c->trace_dev; R.trace_steps = c->trace_steps;
 
   // ---- host plan: prompt pages, sibling page tables, fork jobs
   const int S = c->z.S, maxp = c->z.maxp;
   int top = c->n_pages;
-  std::vector<int> toks, plen(n_loc), last(n_loc);
+  std::vector<int> toks, plen(n_loc), last(n_first), last_tok(n_loc);
   for (int p = 0; p < n_loc; ++p) {
     const auto& tk = c->round_prompts[p].tokens;
-    plen[p] = (int)tk.size();
-    toks.insert(toks.end(), tk.begin(), tk.end());
-    last[p] = (int)toks.size() - 1;
+    plen[p] = (int)tk.size() - (p >= n_first ? 1 : 0);
+    last_tok[p] = tk.back();
+    toks.insert(toks.end(), tk.begin(), tk.begin() + plen[p]);
+    if (p < n_first) last[p] = (int)toks.size() - 1;
   }
   std::vector<std::vector<int>> ppages;
   if (n_loc > 0) {
@@ -961,12 +978,13 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   }
   const int nS = n_loc * G;
   std::vector<int> slot_prompt(nS), slot_j(nS), kv_len(nS), zeros(std::max(nS, n_loc), 0), trL(nS, 0), own0(nS),
-      live(nS), gid(n_loc), ptab((size_t)std::max(nS, 1) * maxp, 0), jobs;
+      live(n_first * G), gid(n_loc), ptab((size_t)std::max(nS, 1) * maxp, 0), jobs;
   for (int p = 0; p < n_loc; ++p) {
     gid[p] = c->round_prompts[p].id;
     for (int j = 0; j < G; ++j) {
       const int s = p * G + j;
-      slot_prompt[s] = p; slot_j[s] = j; kv_len[s] = plen[p]; live[s] = s;
+      slot_prompt[s] = p; slot_j[s] = j; kv_len[s] = plen[p];
+      if (p < n_first) live[s] = s;
       trL[s] = trace ? c->round_prompts[p].trace[j] : 0;
       const int full = plen[p] / kPage;
       for (int k = 0; k < full; ++k) ptab[(size_t)s * maxp + k] = ppages[p][k];
@@ -985,11 +1003,12 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   if (nS > 0) {
     CK(up(R.slot_prompt, slot_prompt, nS)); CK(up(R.slot_j, slot_j, nS)); CK(up(R.kv_len, kv_len, nS));
     CK(up(R.gen, zeros, nS)); CK(up(R.status, zeros, nS)); CK(up(R.trace_L, trL, nS)); CK(up(R.own0, own0, nS));
-    CK(up(R.live, live, nS)); CK(up(R.page_table, ptab, (size_t)nS * maxp));
+    CK(up(R.live, live, (size_t)n_first * G)); CK(up(R.page_table, ptab, (size_t)nS * maxp)); CK(up(R.t0, zeros, nS));
     CK(cudaMemsetAsync(R.best, 0, (size_t)nS * 8, c->st));
   }
   if (n_loc > 0) {
     CK(up(R.p_gid, gid, n_loc)); CK(up(R.p_cnt, zeros, n_loc)); CK(up(R.p_state, zeros, n_loc));
+    CK(up(R.p_last_tok, last_tok, n_loc)); CK(up(R.p_stamp, zeros, n_loc));
   }
   if (!jobs.empty()) {
     CK(up(c->fork_jobs, jobs, jobs.size()));
@@ -999,7 +1018,7 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   CK(cudaMemcpyAsync(R.free_stack, c->identity_pages, (size_t)c->n_pages * 4, cudaMemcpyDeviceToDevice, c->st));
   CK(cudaMemsetAsync(R.rows_hist, 0, ((size_t)c->z.S + 1) * sizeof(unsigned long long), c->st));
   CtlBlock cb{};
-  cb.n_live = nS; cb.t = 1; cb.free_top = top;
+  cb.n_live = n_first * G; cb.t = 1; cb.free_top = top; cb.n_issued = n_first;
   *c->h_ctl = cb;
   CK(cudaMemcpyAsync(R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
   if (c->trace_dev) CK(cudaMemsetAsync(c->trace_dev, 0, (size_t)c->trace_steps * (2 + S) * 4, c->st));
@@ -1007,7 +1026,8 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   launch_sampler(c->logits, c->m.V, c->m.v0, G, R, c->rd.sample_seed, 1.0f / c->rd.temperature, (uint32_t)round_id,
                  c->st);
   c->launches++;
-  if (c->tp > 1 && nS > 0) CKN(ncclAllReduce(R.best, R.best, (size_t)nS, ncclUint64, ncclMax, c->comm, c->st));
+  if (c->tp > 1 && nS > 0)
+    CKN(ncclAllReduce(R.best, R.best, (size_t)n_first * G, ncclUint64, ncclMax, c->comm, c->st));
   if (c->rd.world == 1) {
     launch_ctl(R, 0, 0, c->st); c->launches++;
   } else {
@@ -1048,7 +1068,10 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
   if (rc) return rc;
   int steps = 0;
   while (!c->h_ctl->done && steps < max_steps) {
-    const int bucket = bucket_for(c, c->h_ctl->n_live);
+    // rows can grow inside a graph of graph_steps steps when prompts are issued
+    const int grow = c->max_active ? std::min(c->max_active * c->G, c->h_ctl->n_live +
+                                              (c->n_loc - c->h_ctl->n_issued) * c->G) : 0;
+    const int bucket = bucket_for(c, std::max(c->h_ctl->n_live, grow));
     if (c->prof_steps_left > 0) {
       const int rows = c->h_ctl->n_live;
       const long long ctx = c->h_ctl->ctx_sum;
@@ -1149,7 +1172,7 @@ int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, i
   if (!out) return RP_OK;
   if (c->kind == 0)
     for (int p = 0; p < c->n_loc; ++p)
-      if (!accepted[p]) {
+      if (!accepted[p] && p < c->h_ctl->n_issued) {
         QueuedPrompt q = c->round_prompts[p];
         c->fifo.push_back(q);
       }
@@ -1207,6 +1230,32 @@ int rp_round_rows_histogram(void* ctx, int64_t* out, int32_t n) {
   CK(cudaMemcpyAsync(h.data(), c->R.rows_hist, (size_t)m * 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   for (int i = 0; i < n; ++i) out[i] = i < m ? (int64_t)h[i] : 0;
+  return RP_OK;
+}
+
+int rp_round_issue_cap(void* ctx, int32_t max_active) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (max_active < 0) return c->fail(RP_EINVAL, "invalid field: max_active (>= 0)");
+  if (c->active) return c->fail(RP_EBUSY, "a round is active (collect it first)");
+  c->issue_cap = max_active;
+  return RP_OK;
+}
+
+int rp_round_unissued(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (c->active) {
+    int rc = read_ctl(c);
+    if (rc) return rc;
+    if (!c->h_ctl->done) return c->fail(RP_ESTATE, "round not done");
+  }
+  const int n_is = c->round_prompts.empty() ? 0 : std::min(c->h_ctl->n_issued, c->n_loc);
+  const int n = c->n_loc - n_is;
+  if (n_out) *n_out = n;
+  if (!ids_out) return RP_OK;
+  if (max < n) return c->fail(RP_ENOSPC, "ids_out too small");
+  for (int i = 0; i < n; ++i) ids_out[i] = c->round_prompts[n_is + i].id;
   return RP_OK;
 }
 

@@ -34,8 +34,9 @@ __global__ void __launch_bounds__(256) sampler_kernel(const float* __restrict__ 
   for (int u = blockIdx.x; u < n * chunks; u += gridDim.x) {
     const int i = u / chunks, ch = u % chunks;
     const int s = R.live[i];
+    const int tl = t - R.t0[s];                    // this response's token index
     const int L = R.trace ? R.trace_L[s] : 0x7FFFFFFF;
-    if (R.trace && t == L) {                       // forced EOS at the trace length
+    if (R.trace && tl == L) {                       // forced EOS at the trace length
       if (ch == 0 && threadIdx.x == 0 && R.eos >= v0 && R.eos < v0 + V)
         atomicMax(&R.best[i], pack_arg(INFINITY, (uint32_t)R.eos));
       continue;
@@ -46,14 +47,14 @@ __global__ void __launch_bounds__(256) sampler_kernel(const float* __restrict__ 
     const int v_end = min(V, (ch + 1) * SAMP_CHUNK);
     for (int b = ch * (SAMP_CHUNK / 4) + threadIdx.x; 4 * b < v_end; b += blockDim.x) {
       const float4 z4 = *(const float4*)(lr + 4 * b);
-      const U4 x = philox((uint32_t)(b + (v0 >> 2)), (uint32_t)t, uid, round_id, k0, k1);
+      const U4 x = philox((uint32_t)(b + (v0 >> 2)), (uint32_t)tl, uid, round_id, k0, k1);
       const float zl[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         const int v = v0 + 4 * b + w;                 // global vocab id
         const float uu = u01(u4_word(x, w));
         float z = zl[w] * inv_temp - logf(-logf(uu));
-        if (R.trace && v == R.eos) z = -INFINITY;   // t < L here
+        if (R.trace && v == R.eos) z = -INFINITY;   // tl < L here
         const unsigned long long p = pack_arg(z, (uint32_t)v);
         best = p > best ? p : best;
       }
@@ -101,12 +102,13 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
   }
   for (int i = tid; i < n; i += CTL_THREADS) {
     const int s = R.live[i];
+    const int tl = t - R.t0[s];
     const int tok = (int)unpack_idx(R.best[i]);
-    R.tok_out[(size_t)s * R.cap + t - 1] = tok;
-    R.gen[s] = t;
+    R.tok_out[(size_t)s * R.cap + tl - 1] = tok;
+    R.gen[s] = tl;
     if (appended) R.kv_len[s] += 1;
     const bool fin = tok == R.eos;
-    const bool capped = !fin && t >= R.cap;
+    const bool capped = !fin && tl >= R.cap;
     R.status[s] = fin ? ST_FINISHED : capped ? ST_CAPPED : ST_LIVE;
     if (fin || (capped && R.kind == 1)) atomicAdd(&R.p_cnt[R.slot_prompt[s]], 1);
   }
@@ -130,14 +132,15 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     if (flag) {
       R.p_state[p] = PS_COMPLETE; R.comp_list[s_k + off] = p;
       if (R.keep < R.G) {
+        const int tl = t - R.t0[p * R.G];
         int room = R.keep;
         for (int j = 0; j < R.G; ++j)
-          if (R.status[p * R.G + j] == ST_FINISHED && R.gen[p * R.G + j] < t) --room;
+          if (R.status[p * R.G + j] == ST_FINISHED && R.gen[p * R.G + j] < tl) --room;
         for (int j = 0; j < R.G; ++j) {
           const int s = p * R.G + j;
           const int st = R.status[s];
           if (st == ST_LIVE) R.status[s] = ST_ABORTED;
-          else if (st == ST_FINISHED && R.gen[s] == t) { if (room > 0) --room; else R.status[s] = ST_DROPPED; }
+          else if (st == ST_FINISHED && R.gen[s] == tl) { if (room > 0) --room; else R.status[s] = ST_DROPPED; }
         }
       }
     }
@@ -157,6 +160,7 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
         cnt = max(0, used - R.own0[s]);
       } else {
         keep = 1;
+        if (R.max_active) R.p_stamp[R.slot_prompt[s]] = t;
         if (R.kv_len[s] % kPage == 0) {
           need = 1;
           if (R.kv_len[s] / kPage >= R.maxp) atomicExch(&s_err, 2);
@@ -176,7 +180,43 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     if (tid == 0) { s_top += tot; s_keep += tk; s_need += tn; s_ctx += tc; s_rd += trd; }
     __syncthreads();
   }
+  // Continuous issuance (NEXT-4; oracle sched.issue_step_loop): after
+  // step t the lowest-index unissued prompts of this rank are issued while
+  // fewer than max_active prompts have a live response.  An issued prompt's G
+  // sequences decode its last prompt token at step t + 1 (their KV holds the
+  // other plen - 1 tokens since submit), producing token 1 there.
+  int issue_n = 0;
+  if (R.max_active) {
+    __syncthreads();
+    const int n_is = C->n_issued;
+    int active = 0;
+    for (int base = 0; base < n_is; base += CTL_THREADS) {
+      int tot;
+      block_exscan(base + tid < n_is && R.p_stamp[base + tid] == t ? 1 : 0, &tot, scan_sm);
+      active += tot;
+    }
+    issue_n = max(0, min(R.max_active - active, R.n_prompts - n_is));
+    for (int base = 0; base < issue_n * R.G; base += CTL_THREADS) {
+      const int r = base + tid;
+      int need = 0, ctx = 0;
+      if (r < issue_n * R.G) {
+        const int s = n_is * R.G + r;
+        ctx = R.kv_len[s] + 1;
+        if (R.kv_len[s] % kPage == 0) {
+          need = 1;
+          if (R.kv_len[s] / kPage >= R.maxp) atomicExch(&s_err, 2);
+        }
+      }
+      int tn, tc;
+      block_exscan(need, &tn, scan_sm);
+      block_exscan(ctx, &tc, scan_sm);
+      if (tid == 0) { s_need += tn; s_ctx += tc; }
+      __syncthreads();
+    }
+  }
   if (tid == 0) {
+    s_keep += issue_n * R.G;
+    C->issue_n = issue_n;
     if (s_need > s_top && !s_err) s_err = 1;
     C->free_top = s_top;
     C->k_step = s_k;
@@ -227,13 +267,17 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
   const long long ctx_total = max(1LL, C->ctx_sum);
   const int U = R.attn_units > 0 ? R.attn_units : max(1, 148 / R.kv_heads);
   int kept = 0, alloc = 0, items = 0;
+  // rows n .. n + nis - 1 are the sequences issued after this step (none once
+  // the target is reached: the round ends here)
+  const int n_is0 = C->n_issued;
+  const int nis = s_acc_new >= R.target ? 0 : C->issue_n * R.G;
   if (!s_err) {
-    for (int base = 0; base < n; base += CTL_THREADS) {
+    for (int base = 0; base < n + nis; base += CTL_THREADS) {
       const int i = base + tid;
       int keep = 0, need = 0, ns = 0, chunk = 0, s = -1;
-      if (i < n) {
-        s = R.live[i];
-        keep = R.status[s] == ST_LIVE;
+      if (i < n + nis) {
+        s = i < n ? R.live[i] : n_is0 * R.G + (i - n);
+        keep = i >= n || R.status[s] == ST_LIVE;
         if (keep) {
           const int ctx = R.kv_len[s] + 1;
           need = (R.kv_len[s] % kPage) == 0;
@@ -250,7 +294,12 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
         const int pos = kept + ok;
         const int kv = R.kv_len[s];
         R.live_next[pos] = s;
-        R.tok_in[pos] = R.tok_out[(size_t)s * R.cap + t - 1];
+        if (i < n) {
+          R.tok_in[pos] = R.tok_out[(size_t)s * R.cap + (t - R.t0[s]) - 1];
+        } else {
+          R.tok_in[pos] = R.p_last_tok[R.slot_prompt[s]];
+          R.t0[s] = t;
+        }
         R.row_pos[pos] = kv;
         R.row_pt[pos] = s;
         if (need) R.page_table[(size_t)s * R.maxp + kv / kPage] = R.free_stack[top - 1 - (alloc + oa)];
@@ -275,6 +324,8 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     C->decoded += n;
     C->free_top = top - alloc;
     C->n_items = items;
+    C->n_issued = n_is0 + nis / R.G;
+    C->issue_n = 0;
     const bool done = s_acc_new >= R.target || s_next_global == 0 || s_err;
     if (R.trace_buf && t <= R.trace_steps) {
       int* tb = R.trace_buf + (size_t)(t - 1) * (2 + R.S);

@@ -41,14 +41,20 @@ struct CtlBlock {
   long long decoded;  // tokens decoded this round on this rank
   long long ctx_sum;  // sum over next-step rows of the attention context (kv_len + 1)
   long long kv_read;  // sum over decode steps so far of the decoded rows' attention context
+  int n_issued;     // continuous issuance: prompts of this rank issued so far (committed)
+  int issue_n;      // prompts phase A issues after this step (committed by phase B unless done)
 };
 
 struct RoundDev {
   int S, P, maxp, cap, G, target, kind /*0 short 1 long*/, trace, eos, n_prompts, kv_heads;
   int keep;           // responses retained per prompt (R0 <= G; == G in long rounds)
+  int max_active;     // continuous issuance (NEXT-4): max prompts with a live response; 0 = off
   int attn_units;     // decode-attention split budget per KV head (0: 148 / KV)
   int world, rank;
   int* slot_prompt; int* slot_j; int* kv_len; int* gen; int* trace_L; int* status; int* own0;
+  int* t0;            // [S] step before the sequence's first token: local token index = t - t0 (0 unless issued late)
+  int* p_last_tok;    // [P] last prompt token (a late-issued prompt decodes it as its first step)
+  int* p_stamp;       // [P] last step the prompt had a live response (active-prompt count)
   int* tok_out;       // [S][cap]
   int* page_table;    // [(S + P)][maxp]
   int* p_cnt; int* p_state; int* p_gid; int* comp_list; int* accept_order;

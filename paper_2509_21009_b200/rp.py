@@ -62,7 +62,8 @@ class Response(ctypes.Structure):
 EXPORTS = ["rp_query_sizes", "rp_init_model", "rp_submit_round", "rp_step", "rp_collect", "rp_long_queue",
            "rp_free", "rp_last_error", "rp_launch_count", "rp_debug_logits", "rp_debug_trace_enable",
            "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm", "rp_debug_profile", "rp_nccl_unique_id",
-           "rp_tp_ipc_handle", "rp_tp_ipc_open", "rp_collect_ready", "rp_round_rows_histogram"]
+           "rp_tp_ipc_handle", "rp_tp_ipc_open", "rp_collect_ready", "rp_round_rows_histogram",
+           "rp_round_issue_cap", "rp_round_unissued"]
 
 
 def load_library(path=LIB_PATH):
@@ -95,6 +96,8 @@ def load_library(path=LIB_PATH):
     lib.rp_tp_ipc_handle.argtypes = [P, P]
     lib.rp_tp_ipc_open.argtypes = [P, P]
     lib.rp_round_rows_histogram.argtypes = [P, ctypes.POINTER(I64), I32]
+    lib.rp_round_issue_cap.argtypes = [P, I32]
+    lib.rp_round_unissued.argtypes = [P, ctypes.POINTER(I32), I32, ctypes.POINTER(I32)]
     lib.rp_collect_ready.argtypes = [P, I32, ctypes.POINTER(Response), I32, ctypes.POINTER(I32), I64,
                                      ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I32)]
     for name in EXPORTS:
@@ -302,6 +305,19 @@ class Engine:
         self._check(self.L.rp_round_rows_histogram(self.h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                                    len(out)))
         return out
+
+    def issue_cap(self, max_active):
+        """Continuous issuance for the next rounds (NEXT-4): at most
+        `max_active` prompts of this rank active; 0 turns it off."""
+        self._check(self.L.rp_round_issue_cap(self.h, int(max_active)))
+
+    def unissued(self):
+        """Global ids of this rank's prompts the finished round never issued."""
+        n = ctypes.c_int32()
+        self._check(self.L.rp_round_unissued(self.h, None, 0, ctypes.byref(n)))
+        ids = np.zeros(max(1, n.value), dtype=np.int32)
+        self._check(self.L.rp_round_unissued(self.h, _i32p(ids), n.value, ctypes.byref(n)))
+        return ids[:n.value].tolist()
 
     def long_queue(self):
         n = ctypes.c_int32()

@@ -204,6 +204,82 @@ def test_response_speculation_ties_and_sampling(tiny, oracle_w):
     eng.close()
 
 
+def _check_issue_trace(eng, L, cap, target, kind, A, keep=None):
+    ref = sched.issue_step_loop(L, cap, target, kind, A, with_steps=True, keep=keep)
+    got = eng.debug_trace(ref.t_end + 2)
+    assert len(got) == ref.t_end
+    for a, b in zip(got, ref.steps):
+        assert np.array_equal(a["live"], b["live"]), a["t"]
+        assert a["accepted"] == b["accepted"] and a["done"] == b["done"], a["t"]
+    return ref
+
+
+@pytest.mark.parametrize("seed,graph_steps,A,keep", [(0, 0, 3, None), (1, 4, 5, None), (2, 4, 4, 3),
+                                                     (3, 0, 1, None), (4, 4, 12, None)])
+def test_continuous_issuance_schedule_bit_exact(tiny, seed, graph_steps, A, keep):
+    """NEXT-4: at most A prompts active, new ones issued after every
+    step in index order.  Per-step live lists (incl. the rows issued into the
+    batch), acceptance, the retained set, the queue and the unissued prompts
+    match the oracle's step loop; A >= n is the plain round."""
+    eng = make_engine(tiny, graph_steps=graph_steps)
+    n, G = 12, 4
+    ps = gen.prompts(n, 0, tiny["eos_id"], (2, 100), 90 + seed)
+    L = _trace(n, G, 70 + seed, l_max=120)[:, 0, :]
+    cap, target = 96, 8
+    eng.issue_cap(A)
+    eng.debug_trace_enable(900)
+    eng.submit(ps, G, cap, target, trace=L, round_id=seed, keep=keep or 0)
+    st = eng.run()
+    ref = _check_issue_trace(eng, L, cap, target, sched.SHORT, A, keep=keep)
+    assert st.t == ref.t_end and st.accepted == len(ref.accepted) and bool(st.underfilled) == ref.underfilled
+    assert st.decoded_tokens == sum(len(x["live"]) for x in ref.steps)
+    hist = eng.rows_histogram()
+    want = np.bincount([len(x["live"]) for x in ref.steps[1:]], minlength=len(hist))
+    assert np.array_equal(hist, want[:len(hist)])
+    res = eng.collect()
+    got = [(r["prompt_id"] - ps[0]["prompt_id"], r["j"], r["len"]) for r in res]
+    want = [(i, j, int(ref.retained_len[i, j])) for i in ref.accepted for j in range(G) if ref.retained_len[i, j]]
+    assert got == want
+    for r in res:
+        assert r["tokens"][-1] == tiny["eos_id"] and np.all(r["tokens"][:-1] != tiny["eos_id"])
+    assert eng.long_queue() == [ps[i]["prompt_id"] for i in ref.deferred]
+    assert eng.unissued() == [ps[i]["prompt_id"] for i in ref.unissued]
+    if A >= n:
+        assert ref.unissued == [] and ref.t_end == sched.closed_form(L, cap, target, sched.SHORT, keep=keep).t_end
+    # issuance off again: the plain schedule
+    eng.issue_cap(0)
+    eng.debug_trace_enable(900)
+    eng.submit(ps, G, cap, target, trace=L, round_id=seed, keep=keep or 0)
+    eng.run()
+    _check_round_trace(eng, L, cap, target, sched.SHORT, keep=keep)
+    eng.collect()
+    eng.close()
+
+
+def test_continuous_issuance_sampling_and_long_round(tiny, oracle_w):
+    """Late-issued prompts decode their last prompt token as their first step;
+    their tokens are still the oracle's Gumbel argmax at token index k (the
+    counter does not depend on the issue step).  Long round, A = 2 of 6."""
+    eng = make_engine(tiny, graph_steps=4)
+    n, G = 6, 3
+    ps = gen.prompts(n, 0, tiny["eos_id"], (2, 70), 23)
+    ps[3]["tokens"] = np.repeat(ps[3]["tokens"][:1], 65)   # 64 prefilled tokens: the first step opens a page
+    L = np.minimum(_trace(n, G, 9)[:, 0, :], 30)
+    eng.issue_cap(2)
+    eng.debug_trace_enable(400)
+    eng.submit(ps, G, 24, n, long_round=True, trace=L, round_id=6)
+    st = eng.run()
+    ref = _check_issue_trace(eng, L, 24, n, sched.LONG, 2)
+    assert st.t == ref.t_end and eng.unissued() == []
+    res = eng.collect()
+    assert len(res) == n * G
+    by_id = {p["prompt_id"]: np.asarray(p["tokens"]) for p in ps}
+    tr = {p["prompt_id"]: L[i] for i, p in enumerate(ps)}
+    checked, mism = _check_sampled(tiny, oracle_w, res, by_id, G, 6, 3, trace=tr)
+    assert checked > 100 and mism <= checked // 50
+    eng.close()
+
+
 def test_streaming_collect(tiny):
     """NEXT-3: responses streamed between rp_step calls are final
     (identical to the closing collect, same order) and only ever cover prompts
