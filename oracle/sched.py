@@ -299,15 +299,10 @@ def issue_step_loop(L, cap, target, kind, max_active, with_steps=False, keep=Non
                       issue_step=tau, unissued=unissued)
 
 
-def issue_closed_form(L, cap, target, kind, max_active, keep=None, with_steps=False):
-    """The same round from its definition as list scheduling: prompt i is
-    active for d_i steps (T_i if it completes, else its longest response,
-    e = min(L, cap)), independent of when it is issued; prompts take the
-    earliest-freed of `max_active` slots in index order (tau_i = 1 + the
-    step the slot freed); prompt i completes at C_i = tau_i + T_i - 1; the
-    first `target` by (C_i, i) are accepted and t_end is the target-th
-    completion (else the last active step); prompts with tau_i > t_end are
-    unissued."""
+def _issue_schedule(L, cap, kind, max_active, keep=None):
+    """List scheduling of one instance's prompts: returns tau (issue step),
+    C (completion step, inf if the prompt cannot complete), d (steps active),
+    e0 = min(L, cap), e (steps each response decodes) and the keep mask."""
     import heapq
     L = np.asarray(L, np.int64)
     n, G = L.shape
@@ -321,7 +316,6 @@ def issue_closed_form(L, cap, target, kind, max_active, keep=None, with_steps=Fa
         kept = np.ones((n, G), bool)
         T = e0.max(axis=1)
         e = e0
-        target = n
     d = e.max(axis=1)                                   # steps a prompt stays active
     tau = np.zeros(n, np.int64)
     slots = []
@@ -332,6 +326,60 @@ def issue_closed_form(L, cap, target, kind, max_active, keep=None, with_steps=Fa
             tau[i] = heapq.heappop(slots) + 1
         heapq.heappush(slots, int(tau[i] + d[i] - 1))
     C = np.where(T < INF, tau + np.where(T < INF, T, 0) - 1, INF)
+    return tau, C, d, e0, e, kept
+
+
+def issue_dp_protocol(L, cap, target, kind, world, max_active, keep=None):
+    """Continuous issuance under DP: each rank issues its own contiguous
+    slice with its own cap of `max_active` ("for each LLM instance"),
+    and the per-step cutoff exchange of `dp_protocol` admits completions
+    globally.  Returns (t_end, accepted in acceptance order, deferred,
+    unissued), prompt indices."""
+    L = np.asarray(L, np.int64)
+    n, G = L.shape
+    if kind == LONG:
+        target = n
+    INF = np.iinfo(np.int64).max
+    parts = partition(n, world)
+    tau, C, last = np.zeros(n, np.int64), np.full(n, INF), 0
+    for lo, hi in parts:
+        if hi > lo:
+            ta, Ca, d, _, _, _ = _issue_schedule(L[lo:hi], cap, kind, max_active, keep)
+            tau[lo:hi], C[lo:hi] = ta, Ca
+            last = max(last, int(np.max(ta + d - 1)))
+    acc, accepted, t = 0, [], 0
+    while True:
+        t += 1
+        before = acc
+        total = 0
+        for lo, hi in parts:
+            comp = [i for i in range(lo, hi) if C[i] == t]
+            take = min(len(comp), max(0, target - before - total))
+            accepted.extend(comp[:take])
+            total += take
+        acc += total
+        if acc == target or t >= last:
+            break
+    unissued = [i for i in range(n) if tau[i] > t]
+    deferred = [i for i in range(n) if i not in set(accepted) and i not in set(unissued)]
+    return t, accepted, deferred, unissued
+
+
+def issue_closed_form(L, cap, target, kind, max_active, keep=None, with_steps=False):
+    """The same round from its definition as list scheduling: prompt i is
+    active for d_i steps (T_i if it completes, else its longest response,
+    e = min(L, cap)), independent of when it is issued; prompts take the
+    earliest-freed of `max_active` slots in index order (tau_i = 1 + the
+    step the slot freed); prompt i completes at C_i = tau_i + T_i - 1; the
+    first `target` by (C_i, i) are accepted and t_end is the target-th
+    completion (else the last active step); prompts with tau_i > t_end are
+    unissued."""
+    L = np.asarray(L, np.int64)
+    n, G = L.shape
+    INF = np.iinfo(np.int64).max
+    if kind == LONG:
+        target = n
+    tau, C, d, e0, e, kept = _issue_schedule(L, cap, kind, max_active, keep)
     order = sorted(range(n), key=lambda i: (C[i], i))
     n_fin = int(np.sum(C < INF))
     n_acc = min(target, n_fin)

@@ -55,6 +55,28 @@ def main():
         print("rank %d seed %d t_end %d/%d accepted %d/%d ok=%s" % (rank, seed, st.t, ref.t_end, st.accepted,
                                                                   len(ref.accepted), good), flush=True)
         ok = ok and good
+    # continuous issuance (NEXT-4): at most 3 prompts active per rank, issued
+    # rank-locally; the cutoff exchange is unchanged
+    for seed in (5, 6):
+        ps = gen.prompts(n, 0, cfg["eos_id"], (2, 100), 40 + seed)
+        L = gen.length_trace(n, G, 3.4, 0.6, 0.85, 300, seed)[:, 0, :]
+        eng.issue_cap(3)
+        eng.submit(ps, G, cap, 7, trace=L, round_id=seed)
+        st = eng.run()
+        res = eng.collect()
+        acc = dp.all_gather_ids(list(dict.fromkeys(r["prompt_id"] for r in res)))
+        t_end, r_acc, r_def, r_un = sched.issue_dp_protocol(L, cap, 7, sched.SHORT, world, 3)
+        lo, hi = dp.partition(n, world)[rank]
+        fifo += [ps[i]["prompt_id"] for i in r_def if lo <= i < hi]
+        good = (st.t == t_end and sorted(acc) == sorted(ps[i]["prompt_id"] for i in r_acc)
+                and eng.long_queue() == fifo
+                and eng.unissued() == [ps[i]["prompt_id"] for i in r_un if lo <= i < hi])
+        for r in res:
+            good = good and r["len"] == L[r["prompt_id"] - ps[0]["prompt_id"], r["j"]]
+        print("rank %d issue seed %d t_end %d/%d accepted %d unissued %d ok=%s" % (
+            rank, seed, st.t, t_end, len(acc), len(r_un), good), flush=True)
+        ok = ok and good
+    eng.issue_cap(0)
     eng.close()
     # full size, in the launch configuration bench.py times at N GPUs: the
     # first short round of the C2-7b workload (32 prompts x G=8 per GPU,

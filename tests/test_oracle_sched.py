@@ -286,3 +286,23 @@ def test_issue_invariants_random():
                 assert all(tau[i] == 0 or tau[i] > s["t"] for i in waiting)
                 nxt = s["t"] + 1
                 assert any(tau[i] == nxt for i in range(n)) or not waiting or r.t_end == s["t"]
+
+
+def test_issue_dp_protocol_single_rank_and_plain():
+    """world = 1 is the single-instance round; max_active >= slice size is
+    the plain dp_protocol."""
+    rng = np.random.default_rng(13)
+    for _ in range(300):
+        n, G = int(rng.integers(1, 12)), int(rng.integers(1, 4))
+        L = rng.integers(1, 12, (n, G))
+        cap = int(rng.integers(1, 12))
+        target = int(rng.integers(1, n + 1))
+        keep = int(rng.integers(1, G + 1))
+        A = int(rng.integers(1, n + 1))
+        r = sched.issue_step_loop(L, cap, target, sched.SHORT, A, keep=keep)
+        t, acc, dfr, un = sched.issue_dp_protocol(L, cap, target, sched.SHORT, 1, A, keep=keep)
+        assert (t, acc, dfr, un) == (r.t_end, r.accepted, r.deferred, r.unissued)
+        world = int(rng.integers(1, 4))
+        t2, acc2, _ = sched.dp_protocol(L, cap, target, sched.SHORT, world, keep=keep)
+        t3, acc3, _, un3 = sched.issue_dp_protocol(L, cap, target, sched.SHORT, world, n, keep=keep)
+        assert (t2, acc2) == (t3, acc3) and un3 == []
