@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--profile-steps", type=int, default=24)
     ap.add_argument("--max-rounds-steps", type=int, default=0, help="debug: cap decode steps per round (invalid)")
     ap.add_argument("--out", default="")
-    ap.add_argument("--schedule", default="tail", choices=["tail", "sync"],
+    ap.add_argument("--issue-cap", type=int, default=0,
+                    help="--schedule issue: max active prompts per GPU (0 = ceil(P0 / n_gpus))")
+    ap.add_argument("--schedule", default="tail", choices=["tail", "sync", "issue"],
                     help="tail batching (default) or the plain synchronous rollout baseline on the same stream")
     ap.add_argument("--long-tp", default="auto", choices=["auto", "1", "n"],
                     help="long-round tensor parallelism: auto = smallest TP whose worst-case KV fits (planner), "
@@ -74,6 +76,9 @@ class Workload:
         # "tail": the planner of S:271-279; "sync": plain synchronous rollout (the
         # veRL baseline): every RL step decodes P0 fresh prompts to completion
         self.schedule = schedule
+        # "issue": tail batching with continuous issuance in the short rounds
+        # (NEXT-4); prompts a round never issued return to the stream
+        self.returned = []
 
     def plan(self):
         if self.schedule == "sync":
@@ -82,18 +87,20 @@ class Workload:
         if len(self.queue) >= self.P0:
             ids = self.queue.ids[:self.P0]
             return "long", ids, self.P0, self.R["long_cap"], self.trace[ids, 1, :]
-        ids = list(range(self.next_fresh, self.next_fresh + self.n_submit))
+        ids = self.returned + list(range(self.next_fresh, self.next_fresh + self.n_submit - len(self.returned)))
         return "short", ids, self.P0, self.R["short_cap"], self.trace[ids, 0, :]
 
-    def commit(self, kind, ids, accepted_ids):
+    def commit(self, kind, ids, accepted_ids, unissued=()):
         if self.schedule == "sync":
             self.next_fresh += len(ids)
             return
         if kind == "long":
             self.queue.pop(len(ids))
         else:
-            self.next_fresh += len(ids)
-            self.queue.defer(ids, accepted_ids)
+            self.next_fresh = max(self.next_fresh, max(ids) + 1)
+            un = set(unissued)
+            self.returned = [i for i in ids if i in un]
+            self.queue.defer([i for i in ids if i not in un], accepted_ids)
 
 
 # ------------------------------------------------------------------ clocks
@@ -184,12 +191,16 @@ def run_ours(a):
                              kv_fraction=0.85, stream=st_ev)
 
     from paper_2509_21009_b200.dp import all_gather_ids as allgather_ids
+    issue_cap = a.issue_cap or -(-W.P0 // world)
+    W.issue_cap = issue_cap if W.schedule == "issue" else None
 
     def one_round(round_no, profile=0):
         kind, ids, target, cap, L = W.plan()
         e = eng_long if kind == "long" else eng
         plist = [W.prompts[i] for i in ids]
         h2d = sum(len(p["tokens"]) for p in plist) * 4 + L.size * 4
+        if W.schedule == "issue":
+            e.issue_cap(issue_cap if kind == "short" else 0)
         e.submit(plist, G, cap, target if kind == "short" else len(ids), long_round=(kind == "long"), trace=L,
                  round_id=round_no)
         if profile:
@@ -198,7 +209,8 @@ def run_ours(a):
         res = e.collect()
         acc_local = list(dict.fromkeys(r["prompt_id"] for r in res))
         acc = acc_local if (kind == "long" and e is not eng) else allgather_ids(acc_local)
-        W.commit(kind, ids, acc)
+        un = allgather_ids(e.unissued()) if (W.schedule == "issue" and kind == "short") else []
+        W.commit(kind, ids, acc, un)
         d2h = sum(r["len"] for r in res) * 4 + len(res) * 24
         retained = sum(r["len"] for r in res)
         decoded = st.decoded_tokens
@@ -208,7 +220,7 @@ def run_ours(a):
         if e is not eng and rank != 0:
             # TP ranks decode the same tokens: count them once (on rank 0)
             decoded, retained, h2d, d2h = 0, 0, 0, 0
-        return dict(kind=kind, t_end=st.t, decoded=decoded, retained=retained, h2d=h2d, d2h=d2h,
+        return dict(kind=kind, t_end=st.t, unissued=len(un), decoded=decoded, retained=retained, h2d=h2d, d2h=d2h,
                     accepted=st.accepted, underfilled=st.underfilled, tp=e.tp, hbm_bytes=hbm, t_roof_s=t_roof)
 
     # ---- warm-up (the first warm-up round is profiled per kernel class)
@@ -332,8 +344,10 @@ def run_ours(a):
 
 def bench_config(W, parallelism, graph_steps):
     """The workload description shared by both arms (BASELINE.json configs[1], per GPU)."""
-    sched = ("tail batching (eta=1.25)" if W.schedule == "tail" else
-             "plain synchronous rollout baseline: P0 fresh prompts per RL step decoded to completion")
+    sched = {"tail": "tail batching (eta=1.25)",
+             "sync": "plain synchronous rollout baseline: P0 fresh prompts per RL step decoded to completion",
+             "issue": "tail batching (eta=1.25) with continuous issuance in the short rounds, at most %s prompts "
+                      "active per GPU (NEXT-4)" % getattr(W, "issue_cap", None)}[W.schedule]
     return {"workload": "BASELINE configs[1]: Qwen2.5-7B-shaped, %d prompts x G=%d per GPU, short cap %d, "
                         "target floor(n/1.25), %s, trace mode" % (W.R["n_submit"], W.G, W.R["short_cap"], sched),
             "schedule": W.schedule,
