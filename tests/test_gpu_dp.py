@@ -55,17 +55,17 @@ def main():
         print("rank %d seed %d t_end %d/%d accepted %d/%d ok=%s" % (rank, seed, st.t, ref.t_end, st.accepted,
                                                                   len(ref.accepted), good), flush=True)
         ok = ok and good
-    # continuous issuance (NEXT-4): at most 3 prompts active per rank, issued
+    # continuous issuance (NEXT-4): at most A prompts active per rank, issued
     # rank-locally; the cutoff exchange is unchanged
-    for seed in (5, 6):
+    for seed, A, tg in ((5, 3, 7), (6, 2, 5), (7, 2, 4)):
         ps = gen.prompts(n, 0, cfg["eos_id"], (2, 100), 40 + seed)
         L = gen.length_trace(n, G, 3.4, 0.6, 0.85, 300, seed)[:, 0, :]
-        eng.issue_cap(3)
-        eng.submit(ps, G, cap, 7, trace=L, round_id=seed)
+        eng.issue_cap(A)
+        eng.submit(ps, G, cap, tg, trace=L, round_id=seed)
         st = eng.run()
         res = eng.collect()
         acc = dp.all_gather_ids(list(dict.fromkeys(r["prompt_id"] for r in res)))
-        t_end, r_acc, r_def, r_un = sched.issue_dp_protocol(L, cap, 7, sched.SHORT, world, 3)
+        t_end, r_acc, r_def, r_un = sched.issue_dp_protocol(L, cap, tg, sched.SHORT, world, A)
         lo, hi = dp.partition(n, world)[rank]
         fifo += [ps[i]["prompt_id"] for i in r_def if lo <= i < hi]
         good = (st.t == t_end and sorted(acc) == sorted(ps[i]["prompt_id"] for i in r_acc)
