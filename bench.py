@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--profile-steps", type=int, default=24)
     ap.add_argument("--max-rounds-steps", type=int, default=0, help="debug: cap decode steps per round (invalid)")
     ap.add_argument("--out", default="")
+    ap.add_argument("--stream-collect", type=int, default=0,
+                    help="NEXT-3: rp_collect_ready every K decode steps during the round (0 = off)")
     ap.add_argument("--issue-cap", type=int, default=0,
                     help="--schedule issue: max active prompts per GPU (0 = ceil(P0 / n_gpus))")
     ap.add_argument("--schedule", default="tail", choices=["tail", "sync", "issue"],
@@ -205,13 +207,24 @@ def run_ours(a):
                  round_id=round_no)
         if profile:
             e.debug_profile_arm(profile)
-        st = e.run()
+        streamed = 0
+        if a.stream_collect > 0:
+            # NEXT-3: stream the accepted prompts' responses every `stream_collect`
+            # decode steps while the round runs (a reward stage would consume them)
+            first = 0
+            st = e.step(a.stream_collect)
+            while not st.done:
+                got, first = e.collect_ready(first)      # final: accepted before the round ended
+                streamed += sum(r["len"] for r in got)
+                st = e.step(a.stream_collect)
+        else:
+            st = e.run()
         res = e.collect()
         acc_local = list(dict.fromkeys(r["prompt_id"] for r in res))
         acc = acc_local if (kind == "long" and e is not eng) else allgather_ids(acc_local)
         un = allgather_ids(e.unissued()) if (W.schedule == "issue" and kind == "short") else []
         W.commit(kind, ids, acc, un)
-        d2h = sum(r["len"] for r in res) * 4 + len(res) * 24
+        d2h = (sum(r["len"] for r in res) + streamed) * 4 + len(res) * 24
         retained = sum(r["len"] for r in res)
         decoded = st.decoded_tokens
         # algorithmic HBM bytes of this rank's decode steps (step 1 comes from the prefill)
@@ -220,7 +233,7 @@ def run_ours(a):
         if e is not eng and rank != 0:
             # TP ranks decode the same tokens: count them once (on rank 0)
             decoded, retained, h2d, d2h = 0, 0, 0, 0
-        return dict(kind=kind, t_end=st.t, unissued=len(un), decoded=decoded, retained=retained, h2d=h2d, d2h=d2h,
+        return dict(kind=kind, t_end=st.t, unissued=len(un), streamed=streamed, decoded=decoded, retained=retained, h2d=h2d, d2h=d2h,
                     accepted=st.accepted, underfilled=st.underfilled, tp=e.tp, hbm_bytes=hbm, t_roof_s=t_roof)
 
     # ---- warm-up (the first warm-up round is profiled per kernel class)
@@ -318,6 +331,9 @@ def run_ours(a):
         "gpu_launches": int(launches_all),
         "clocks": clocks,
     }
+    if a.stream_collect:
+        line["config"]["stream_collect_steps"] = a.stream_collect
+        line["streamed_fraction"] = round(sum(x["streamed"] for x in rounds) / max(1, sum(x["retained"] for x in rounds)), 4)
     if prof is not None:
         line["roofline"], line["kernel_profile"] = roofline(prof, cfg)
     peak_hbm = load_peaks()[0]
