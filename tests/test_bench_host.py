@@ -1,0 +1,68 @@
+"""Host logic of bench.py (no GPU): the workload stream and planner state for
+the three schedules, checked against the oracle's round outcomes."""
+import numpy as np
+
+import bench
+from oracle import sched
+
+
+def _run(W, n_rounds, A=None):
+    """Drive the workload with oracle rounds (what the engines return)."""
+    kinds = []
+    for _ in range(n_rounds):
+        kind, ids, target, cap, L = W.plan()
+        kinds.append(kind)
+        if kind == "long":
+            r = sched.closed_form(L, cap, len(ids), sched.LONG)
+            W.commit(kind, ids, [ids[i] for i in r.accepted])
+        elif A:
+            r = sched.issue_step_loop(L, cap, target, sched.SHORT, A)
+            W.commit(kind, ids, [ids[i] for i in r.accepted], [ids[i] for i in r.unissued])
+        else:
+            r = sched.closed_form(L, cap, target, sched.SHORT)
+            W.commit(kind, ids, [ids[i] for i in r.accepted])
+    return kinds
+
+
+def test_tail_schedule_matches_oracle_simulate():
+    W = bench.Workload("C1-tiny", 1)
+    kinds = _run(W, 6)
+    ref = sched.simulate(W.trace, 6, W.P0, 1.25, W.G, W.R["short_cap"], W.R["long_cap"],
+                         n_launch_override=W.n_submit)
+    assert kinds == [x["kind"] for x in ref]
+    assert W.queue.ids == ref[-1]["queue_after"]
+
+
+def test_sync_schedule_takes_fresh_prompts():
+    W = bench.Workload("C1-tiny", 2, "sync")
+    seen = []
+    for _ in range(3):
+        kind, ids, target, cap, L = W.plan()
+        assert kind == "long" and target == W.P0 and cap == W.R["long_cap"]
+        assert np.array_equal(L, W.trace[ids, 0, :])
+        seen += ids
+        W.commit(kind, ids, ids)
+    assert seen == list(range(3 * W.P0)) and len(W.queue) == 0
+
+
+def test_issue_schedule_returns_unissued_prompts():
+    W = bench.Workload("C1-tiny", 1, "issue")
+    A = 2
+    stream = []
+    for _ in range(8):
+        kind, ids, target, cap, L = W.plan()
+        if kind == "short":
+            stream.append(list(ids))
+            r = sched.issue_step_loop(L, cap, target, sched.SHORT, A)
+            un = [ids[i] for i in r.unissued]
+            W.commit(kind, ids, [ids[i] for i in r.accepted], un)
+            assert W.returned == un
+            nxt, _, _, _, _ = W.plan()
+            if nxt == "short":
+                assert W.plan()[1][:len(un)] == un            # back at the front of the stream
+        else:
+            r = sched.closed_form(L, cap, len(ids), sched.LONG)
+            W.commit(kind, ids, [ids[i] for i in r.accepted])
+    # every fresh id enters a short round in order, none skipped
+    firsts = sorted(set(i for s in stream for i in s))
+    assert firsts == list(range(len(firsts)))
