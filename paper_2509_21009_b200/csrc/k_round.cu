@@ -1,7 +1,8 @@
 // Sampling and round control on the device (K9-K11).
 //
 // sampler: token = argmax_v (logit_v / T + g_v), g_v = -ln(-ln u_v) with
-//   u_v from word v&3 of Philox4x32-10(ctr=(v>>2, t, uid, round_id),
+//   u_v from word v&3 of Philox4x32-10(ctr=(v>>2, t, uid, round_id), t the
+//   response's token index (the step minus its issue offset t0),
 //   key=seed) (readings Z9-Z11); trace mode masks EOS before the trace
 //   length L and forces it at t = L.  Per-row argmax is a packed
 //   (orderable value, ~index) atomicMax, so the result is independent of the
