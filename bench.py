@@ -49,9 +49,10 @@ def parse():
                     help="--schedule issue: max active prompts per GPU (0 = ceil(P0 / n_gpus))")
     ap.add_argument("--schedule", default="tail", choices=["tail", "sync", "issue"],
                     help="tail batching (default) or the plain synchronous rollout baseline on the same stream")
-    ap.add_argument("--long-tp", default="auto", choices=["auto", "1", "n"],
+    ap.add_argument("--long-tp", default="auto", choices=["auto", "1", "n", "profile"],
                     help="long-round tensor parallelism: auto = smallest TP whose worst-case KV fits (planner), "
-                         "1 = data-parallel replicas, n = one TP group over all GPUs")
+                         "1 = data-parallel replicas, n = one TP group over all GPUs, profile = fastest "
+                         "fitting size by the offline profile (tools/profile_grid.py)")
     return ap.parse_args()
 
 
@@ -174,7 +175,8 @@ def run_ours(a):
     # every sequence of a replica's share at prompt + cap tokens -- fits the
     # per-GPU pool without preemption.  TP=1 means the N GPUs run data-parallel
     # replicas of the long round (each decodes its slice of the P0 prompts).
-    long_tp = plan_long_tp(a.long_tp, cfg, W, world)
+    grid = json.load(open(TP_GRID)) if (a.long_tp == "profile" and os.path.exists(TP_GRID)) else None
+    long_tp = plan_long_tp(a.long_tp, cfg, W, world, grid)
     # short rounds: data parallel over the N GPUs (prompts sharded by index)
     eng = rp.Engine(cfg, max_seqs=n_loc * G, max_prompts=n_loc, max_prompt_len=hi, max_prompt_tokens=n_loc * hi,
                     max_cap=max(W.R["short_cap"], W.R["long_cap"]), graph_steps=a.graph_steps, rank=rank,
@@ -372,10 +374,26 @@ def bench_config(W, parallelism, graph_steps):
             "l2": "inputs larger than L2 (14 GB of weights streamed per decode step)", "graph_steps": graph_steps}
 
 
-def plan_long_tp(choice, cfg, W, world):
-    """Long-round TP size: 1, the whole group, or (auto) the smallest of
-    {1, world} whose worst-case KV per GPU fits ~80% of the memory left after
-    that TP size's weight shard."""
+TP_GRID = os.path.join(ROOT, "profiles", "r01_tp_grid_7b.json")
+
+
+def grid_step_ms(grid, tp, B, ctx):
+    """Decode-step ms of the offline profile (tools/profile_grid.py) at the
+    grid point nearest to (B, ctx) in log space, or None."""
+    pts = [p for p in grid["points"] if p["tp"] == tp]
+    if not pts:
+        return None
+    p = min(pts, key=lambda p: abs(math.log(p["B"] / B)) + abs(math.log(p["ctx"] / ctx)))
+    return p["ms_per_step"]
+
+
+def plan_long_tp(choice, cfg, W, world, grid=None):
+    """Long-round TP size: 1, the whole group, (auto) the smallest of {1,
+    world} whose worst-case KV per GPU fits ~80% of the memory left after
+    that TP size's weight shard, or (profile, A8/A9) among the sizes that fit,
+    the one the offline profile predicts fastest per decode step for the
+    long round's rows per replica at a representative context (mean prompt +
+    a quarter of the long cap)."""
     can_tp = world > 1 and cfg["n_kv_heads"] % world == 0
     if choice == "1" or world == 1:
         return 1
@@ -385,6 +403,7 @@ def plan_long_tp(choice, cfg, W, world):
     free, _ = torch.cuda.mem_get_info()
     hi = W.R["prompt_len"][1]
     per_tok = cfg["n_layers"] * cfg["n_kv_heads"] * cfg["head_dim"] * 2 * 2
+    fits = []
     for t in ([1, world] if can_tp else [1]):
         prompts = -(-W.P0 // (world // t))
         need = prompts * W.G * (hi + W.R["long_cap"]) * per_tok / t
@@ -393,8 +412,16 @@ def plan_long_tp(choice, cfg, W, world):
         full = weight_bytes(cfg, 1) + cfg["vocab"] * cfg["d_model"] * 2
         weights = full if t == 1 else full + weight_bytes(cfg, t)
         if need <= 0.8 * (free - weights):
-            return t
-    return world if can_tp else 1
+            fits.append(t)
+    if not fits:
+        return world if can_tp else 1
+    if choice == "profile" and grid is not None:
+        ctx = sum(W.R["prompt_len"]) / 2 + W.R["long_cap"] / 4
+        pred = {t: grid_step_ms(grid, t, -(-W.P0 // (world // t)) * W.G, ctx) for t in fits}
+        pred = {t: v for t, v in pred.items() if v is not None}
+        if pred:
+            return min(pred, key=pred.get)
+    return fits[0]
 
 
 def weight_bytes(cfg, tp=1):

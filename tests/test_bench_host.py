@@ -66,3 +66,12 @@ def test_issue_schedule_returns_unissued_prompts():
     # every fresh id enters a short round in order, none skipped
     firsts = sorted(set(i for s in stream for i in s))
     assert firsts == list(range(len(firsts)))
+
+
+def test_grid_nearest_point():
+    grid = {"points": [dict(tp=1, B=8, ctx=1024, ms_per_step=3.0), dict(tp=1, B=256, ctx=1024, ms_per_step=8.0),
+                       dict(tp=2, B=256, ctx=4096, ms_per_step=5.0)]}
+    assert bench.grid_step_ms(grid, 1, 200, 2000) == 8.0
+    assert bench.grid_step_ms(grid, 1, 10, 900) == 3.0
+    assert bench.grid_step_ms(grid, 2, 8, 100) == 5.0
+    assert bench.grid_step_ms(grid, 4, 8, 100) is None
