@@ -378,13 +378,20 @@ TP_GRID = os.path.join(ROOT, "profiles", "r01_tp_grid_7b.json")
 
 
 def grid_step_ms(grid, tp, B, ctx):
-    """Decode-step ms of the offline profile (tools/profile_grid.py) at the
-    grid point nearest to (B, ctx) in log space, or None."""
+    """Decode-step ms of the offline profile (tools/profile_grid.py) for TP
+    size tp: the grid context nearest to ctx (log space), then linear in B
+    between the bracketing grid batches (extrapolated past the ends), or
+    None when the profile has no point of this TP size."""
     pts = [p for p in grid["points"] if p["tp"] == tp]
     if not pts:
         return None
-    p = min(pts, key=lambda p: abs(math.log(p["B"] / B)) + abs(math.log(p["ctx"] / ctx)))
-    return p["ms_per_step"]
+    c = min({p["ctx"] for p in pts}, key=lambda c: abs(math.log(c / ctx)))
+    row = sorted((p["B"], p["ms_per_step"]) for p in pts if p["ctx"] == c)
+    if len(row) == 1:
+        return row[0][1]
+    k = next((i for i in range(1, len(row)) if row[i][0] >= B), len(row) - 1)
+    (b0, m0), (b1, m1) = row[k - 1], row[k]
+    return max(m0 + (m1 - m0) * (B - b0) / (b1 - b0), 0.0)
 
 
 def plan_long_tp(choice, cfg, W, world, grid=None):

@@ -68,10 +68,12 @@ def test_issue_schedule_returns_unissued_prompts():
     assert firsts == list(range(len(firsts)))
 
 
-def test_grid_nearest_point():
+def test_grid_interpolation():
     grid = {"points": [dict(tp=1, B=8, ctx=1024, ms_per_step=3.0), dict(tp=1, B=256, ctx=1024, ms_per_step=8.0),
-                       dict(tp=2, B=256, ctx=4096, ms_per_step=5.0)]}
-    assert bench.grid_step_ms(grid, 1, 200, 2000) == 8.0
-    assert bench.grid_step_ms(grid, 1, 10, 900) == 3.0
+                       dict(tp=1, B=8, ctx=4096, ms_per_step=4.0), dict(tp=2, B=256, ctx=4096, ms_per_step=5.0)]}
+    assert bench.grid_step_ms(grid, 1, 256, 2000) == 8.0                 # nearest context 1024 (log space)
+    assert abs(bench.grid_step_ms(grid, 1, 132, 1024) - 5.5) < 1e-9      # linear in B
+    assert abs(bench.grid_step_ms(grid, 1, 504, 1024) - 13.0) < 1e-9     # extrapolated past the last batch
+    assert bench.grid_step_ms(grid, 1, 8, 8192) == 4.0                    # single point of that context
     assert bench.grid_step_ms(grid, 2, 8, 100) == 5.0
     assert bench.grid_step_ms(grid, 4, 8, 100) is None
