@@ -319,7 +319,8 @@ def run_ours(a):
         "dtype": "fp16",
         "data": "synthetic (random-init Qwen2.5-7B-shaped weights, seeded prompts, lognormal length trace)",
         "config": bench_config(W, "short rounds dp%d, long rounds %s" % (
-            world, ("tp%d" % long_tp) if eng_long is not eng else "dp%d (planner: TP=1 fits the worst-case KV)" % world),
+            world, ("tp%d" % long_tp) if eng_long is not eng else ("dp%d (planner: TP=1 fits the worst-case KV)" % world if a.long_tp != "profile" else
+                 "dp%d (planner: profile predicts DP replicas fastest among the fitting TP sizes)" % world)),
             a.graph_steps),
         "per_gpu_tokens_per_s": round(value / world, 1),
         "retained_tokens_per_s": round(retained / dev_s, 1),

@@ -315,6 +315,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
     R.S = z.S; R.P = z.P; R.maxp = z.maxp; R.kv_heads = (int)KV; R.eos = md->eos_id;
     R.world = rd->world; R.rank = rd->rank;
     R.attn_units = getenv("RP_ATTN_UNITS") ? atoi(getenv("RP_ATTN_UNITS")) : 0;   // measurement override
+    R.attn_waves = getenv("RP_ATTN_WAVES") ? atoi(getenv("RP_ATTN_WAVES")) : 1;   // A/B switch
     R.slot_prompt = slot_prompt; R.slot_j = slot_j; R.kv_len = kv_len; R.gen = gen; R.trace_L = trace_L;
     R.status = status; R.own0 = own0; R.t0 = t0; R.p_last_tok = p_last_tok; R.p_stamp = p_stamp; R.tok_out = tok_out; R.page_table = page_table; R.p_cnt = p_cnt;
     R.p_state = p_state; R.p_gid = p_gid; R.comp_list = comp_list; R.accept_order = accept_order;

@@ -266,12 +266,34 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
   // sum ns_r <= U whenever no row is forced up to 1), each of
   // ceil(ctx_r / ns_r) tokens rounded up to whole pages.
   const long long ctx_total = max(1LL, C->ctx_sum);
-  const int U = R.attn_units > 0 ? R.attn_units : max(1, 148 / R.kv_heads);
-  int kept = 0, alloc = 0, items = 0;
   // rows n .. n + nis - 1 are the sequences issued after this step (none once
   // the target is reached: the round ends here)
   const int n_is0 = C->n_issued;
   const int nis = s_acc_new >= R.target ? 0 : C->issue_n * R.G;
+  // Full waves: with more rows than one wave's units per head, budget k waves
+  // (k = ceil(rows / U1)) so the flat list fills whole waves instead of
+  // leaving a partial one; the splits left over by the floors go one each to
+  // the first rows, so every wave is full (R.attn_waves; 0 = the plain floor).
+  const int U1 = R.attn_units > 0 ? R.attn_units : max(1, 148 / R.kv_heads);
+  int U = U1, left = 0;
+  if (R.attn_waves && !s_err) {
+    const int rows = C->n_next;
+    U = U1 * max(1, (rows + U1 - 1) / U1);
+    int sum = 0;
+    for (int base = 0; base < n + nis; base += CTL_THREADS) {
+      const int i = base + tid;
+      int b = 0;
+      if (i < n + nis) {
+        const int s = i < n ? R.live[i] : n_is0 * R.G + (i - n);
+        if (i >= n || R.status[s] == ST_LIVE) b = (int)((long long)(R.kv_len[s] + 1) * U / ctx_total);
+      }
+      int tot;
+      block_exscan(b, &tot, scan_sm);
+      sum += tot;
+    }
+    left = max(0, U - sum);
+  }
+  int kept = 0, alloc = 0, items = 0;
   if (!s_err) {
     for (int base = 0; base < n + nis; base += CTL_THREADS) {
       const int i = base + tid;
@@ -289,6 +311,12 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
       }
       int tk, ta, ti;
       const int ok = block_exscan(keep, &tk, scan_sm);
+      if (keep && R.attn_waves) {           // re-derive this row's splits with the leftover share
+        const int ctx = R.kv_len[s] + 1;
+        const int want = max(1, (int)((long long)ctx * U / ctx_total) + (kept + ok < left ? 1 : 0));
+        chunk = ((ctx + want - 1) / want + kPage - 1) / kPage * kPage;
+        ns = (ctx + chunk - 1) / chunk;
+      }
       const int oa = block_exscan(need, &ta, scan_sm);
       const int oi = block_exscan(ns, &ti, scan_sm);
       if (keep) {

@@ -50,6 +50,7 @@ struct RoundDev {
   int keep;           // responses retained per prompt (R0 <= G; == G in long rounds)
   int max_active;     // continuous issuance (NEXT-4): max prompts with a live response; 0 = off
   int attn_units;     // decode-attention split budget per KV head (0: 148 / KV)
+  int attn_waves;     // 1: budget whole waves of attention units (k-wave fill), 0: one-wave floor
   int world, rank;
   int* slot_prompt; int* slot_j; int* kv_len; int* gen; int* trace_L; int* status; int* own0;
   int* t0;            // [S] step before the sequence's first token: local token index = t - t0 (0 unless issued late)
