@@ -270,15 +270,18 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
   // the target is reached: the round ends here)
   const int n_is0 = C->n_issued;
   const int nis = s_acc_new >= R.target ? 0 : C->issue_n * R.G;
-  // Full waves: with more rows than one wave's units per head, budget k waves
-  // (k = ceil(rows / U1)) so the flat list fills whole waves instead of
-  // leaving a partial one; the splits left over by the floors go one each to
-  // the first rows, so every wave is full (R.attn_waves; 0 = the plain floor).
+  // Full waves: with k = ceil(rows / U1) in {2, 3} (between one and three
+  // waves' worth of rows per head) budget k whole waves so the flat list
+  // does not end in a partial wave; the splits left over by the floors go one
+  // each to the first rows.  Measured (profiles/r01_attn_waves_ab.txt): -3% step
+  // time at 40-48 rows, neutral at 56 and 83, but +2-6% at k >= 4 (more,
+  // smaller units cost more merges than the balance saves), so k >= 4 and
+  // k = 1 keep the plain floor.  R.attn_waves = 0 disables it (A/B).
   const int U1 = R.attn_units > 0 ? R.attn_units : max(1, 148 / R.kv_heads);
   int U = U1, left = 0;
-  if (R.attn_waves && !s_err) {
-    const int rows = C->n_next;
-    U = U1 * max(1, (rows + U1 - 1) / U1);
+  const int kw = (C->n_next + U1 - 1) / U1;
+  if (R.attn_waves && !s_err && kw >= 2 && kw <= 3) {
+    U = U1 * kw;
     int sum = 0;
     for (int base = 0; base < n + nis; base += CTL_THREADS) {
       const int i = base + tid;
@@ -311,7 +314,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
       }
       int tk, ta, ti;
       const int ok = block_exscan(keep, &tk, scan_sm);
-      if (keep && R.attn_waves) {           // re-derive this row's splits with the leftover share
+      if (keep && U != U1) {                // re-derive this row's splits with the leftover share
         const int ctx = R.kv_len[s] + 1;
         const int want = max(1, (int)((long long)ctx * U / ctx_total) + (kept + ok < left ? 1 : 0));
         chunk = ((ctx + want - 1) / want + kPage - 1) / kPage * kPage;
