@@ -28,6 +28,7 @@ struct GemmArgs {
   const int* n_dev;       // live N read on device (nullptr -> n_host)
   int n_host;
   int splits;             // split-K factor (1 = direct epilogue)
+  int coop_min;           // cooperative split-K reduction from this chunk width up (set by gemm_launch)
   int epi;                // GemmEpi
   void* out;              // out[n * ldo + m] (SWIGLU: out[n * ldo + feature])
   int ldo;
@@ -63,6 +64,9 @@ struct GemmPlan {
 
 int make_tmap_act(CUtensorMap* map, const void* base, int rows, int cols, int box_rows);
 int gemm_init_attrs();
+// chunk width from which a one-wave split-K GEMM reduces cooperatively (RP_COOP_MIN overrides;
+// tp_norm must use the same value to count the producer's signals)
+int gemm_coop_min();
 int gemm_smem_bytes();
 int gemm_pick_splits(int M, int K, int n_sms);
 void gemm_launch(const GemmPlan& p, const GemmArgs& a, int grid, cudaStream_t st);

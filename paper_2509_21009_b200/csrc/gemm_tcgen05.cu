@@ -257,7 +257,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int kb_total = a.K / BK;
   // cooperative split-K reduction: grid fits one wave and the chunk is wide
   // enough that a single CTA reducing the whole tile would be the bottleneck
-  const bool coop = a.splits > 1 && n_items <= n_ctas && min(BN, N) >= 96;
+  const bool coop = a.splits > 1 && n_items <= n_ctas && min(BN, N) >= a.coop_min;
 
   // Ring geometry from the widest activation chunk: 16/64/256-row boxes; at
   // small N the stages shrink and the ring deepens (more weight bytes in
@@ -869,8 +869,15 @@ int gemm_pick_splits(int M, int K, int n_sms) {
 // the 7B decode step it is ~1% faster above 128 live rows and 2.5-6% slower
 // at 16-64 rows, where the rollout spends most steps
 // (profiles/r01_gemm_chain_experiment.txt).
-void gemm_launch(const GemmPlan& p, const GemmArgs& a, int grid, cudaStream_t st) {
+int gemm_coop_min() {
+  static const int v = getenv("RP_COOP_MIN") ? atoi(getenv("RP_COOP_MIN")) : 96;
+  return v;
+}
+
+void gemm_launch(const GemmPlan& p, const GemmArgs& a0, int grid, cudaStream_t st) {
   static const bool pair = getenv("RP_GEMM_PAIR") != nullptr;
+  GemmArgs a = a0;
+  a.coop_min = gemm_coop_min();
   if (pair && a.splits == 1 && a.M % (2 * BM) == 0 && !a.timeline && grid % 2 == 0) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include "common.cuh"
 #include "kernels.h"
+#include "gemm.h"
 
 namespace rp {
 
@@ -145,7 +146,8 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 
 __global__ void tp_norm_kernel(float* x, const float* recv, int tp, size_t src_stride,
                                const unsigned long long* flags, unsigned long long* gen, int* done, int m_tiles,
-                               int splits, const int* n_dev, const float* gamma, act_t* h, int d, float eps) {
+                               int splits, int coop_min, const int* n_dev, const float* gamma, act_t* h, int d,
+                               float eps) {
   __shared__ float red[32];
   __shared__ unsigned long long s_units;
   pdl_wait();
@@ -156,7 +158,7 @@ __global__ void tp_norm_kernel(float* x, const float* recv, int tp, size_t src_s
     // output units the producer GEMM signals per use (its cooperative
     // split-K reduction finishes one column slice per split)
     const int n_chunks = (n + 255) / 256;
-    const bool coop = splits > 1 && m_tiles * n_chunks * splits <= 148 && min(256, n) >= 96;
+    const bool coop = splits > 1 && m_tiles * n_chunks * splits <= 148 && min(256, n) >= coop_min;
     const unsigned long long units = (unsigned long long)m_tiles * n_chunks * (coop ? splits : 1);
     const unsigned long long target = *(volatile unsigned long long*)gen + units;
     s_units = units;
@@ -220,7 +222,7 @@ void launch_tp_norm(float* x, const float* recv, int tp, size_t src_stride, cons
                     unsigned long long* gen, int* done, int m_tiles, int splits, const int* n_dev, int n_rows_grid,
                     const float* gamma, void* h, int d, float eps, cudaStream_t st) {
   launch_pdl(tp_norm_kernel, dim3(row_grid(n_dev, n_rows_grid)), dim3(256), 0, st, x, recv, tp, src_stride, flags, gen,
-             done, m_tiles, splits, n_dev, gamma, (act_t*)h, d, eps);
+             done, m_tiles, splits, gemm_coop_min(), n_dev, gamma, (act_t*)h, d, eps);
 }
 
 // -------------------------------------------------------- RoPE + KV append
