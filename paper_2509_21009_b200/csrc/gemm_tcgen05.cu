@@ -864,16 +864,20 @@ int gemm_pick_splits(int M, int K, int n_sms) {
   return best;
 }
 
+// Cooperative split-K from 24-wide chunks up: on the 7B decode step 9-11%
+// faster at 56-100 live rows than the earlier 96, 5.5% at 40-48 rows, 3% at
+// 32 rows, neutral at 128; never cooperative is 16% slower at ~114 rows
+// (profiles/r01_coop_min_ab.txt).
+int gemm_coop_min() {
+  static const int v = getenv("RP_COOP_MIN") ? atoi(getenv("RP_COOP_MIN")) : 24;
+  return v;
+}
+
 // With RP_GEMM_PAIR=1, unsplit GEMMs whose weight rows pair up run as CTA
 // pairs (clusters of 2, one per TPC).  Off by default: parity-green, but on
 // the 7B decode step it is ~1% faster above 128 live rows and 2.5-6% slower
 // at 16-64 rows, where the rollout spends most steps
 // (profiles/r01_gemm_chain_experiment.txt).
-int gemm_coop_min() {
-  static const int v = getenv("RP_COOP_MIN") ? atoi(getenv("RP_COOP_MIN")) : 96;
-  return v;
-}
-
 void gemm_launch(const GemmPlan& p, const GemmArgs& a0, int grid, cudaStream_t st) {
   static const bool pair = getenv("RP_GEMM_PAIR") != nullptr;
   GemmArgs a = a0;
