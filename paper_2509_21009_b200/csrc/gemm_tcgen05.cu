@@ -864,12 +864,13 @@ int gemm_pick_splits(int M, int K, int n_sms) {
   return best;
 }
 
-// Cooperative split-K from 24-wide chunks up: on the 7B decode step 9-11%
+// Cooperative split-K from 16-wide chunks up: on the 7B decode step 9-11%
 // faster at 56-100 live rows than the earlier 96, 5.5% at 40-48 rows, 3% at
-// 32 rows, neutral at 128; never cooperative is 16% slower at ~114 rows
+// 32 rows, 2% at 20-24 rows, neutral at 128 and at 12-16; never cooperative
+// is 16% slower at ~114 rows; 8 is 1% slower at 12 rows
 // (profiles/r01_coop_min_ab.txt).
 int gemm_coop_min() {
-  static const int v = getenv("RP_COOP_MIN") ? atoi(getenv("RP_COOP_MIN")) : 24;
+  static const int v = getenv("RP_COOP_MIN") ? atoi(getenv("RP_COOP_MIN")) : 16;
   return v;
 }
 
