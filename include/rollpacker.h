@@ -28,7 +28,8 @@
  *     full prompt list; rank r decodes the contiguous slice of prompt indices
  *     partition(n, world)[r] and the per-step acceptance cutoff is exchanged
  *     with an NCCL all-gather.  Membership (which prompts are
- *     accepted / deferred) is identical for every world size.
+ *     accepted / deferred) is identical for every world size, and so is the
+ *     global long-prompt queue every rank keeps.
  */
 #ifndef ROLLPACKER_H
 #define ROLLPACKER_H
@@ -88,10 +89,11 @@ typedef struct {
   uint64_t sample_seed;      /* Philox key of the sampler (reading Z10)        */
   float temperature;         /* T of the Gumbel-max sampler (reading Z9: 1.0)  */
   int32_t graph_steps;       /* decode steps per captured CUDA graph (0 = no graphs) */
-  const void* nccl_id;       /* 128-byte ncclUniqueId of the DP group (world > 1) or of
-                                the TP group (tp > 1), else NULL */
+  const void* nccl_id;       /* 128-byte ncclUniqueId of the DP group (world > 1): the ranks
+                                with this context's tp_rank, one per replica; with world == 1
+                                and tp > 1 it may instead name the TP group.  NULL otherwise */
   int32_t tp;                /* tensor-parallel size of this context (0/1 = none).  With
-                                tp > 1 (world must be 1) the context holds only its shard:
+                                tp > 1 the context holds only its shard:
                                 heads, KV heads, d_ff and vocab / tp (column-parallel QKV,
                                 gate||up and LM head, row-parallel O and down with an fp32
                                 all-reduce after each -- NCCL, or at decode the NVLink peer
@@ -99,21 +101,32 @@ typedef struct {
                                 MAX all-reduce of the packed argmax).  Every TP rank submits
                                 the same prompts and keeps identical round state. */
   int32_t tp_rank;           /* rank inside the TP group */
+  const void* tp_nccl_id;    /* ncclUniqueId of this replica's TP group (tp > 1; NULL with
+                                world == 1 -> nccl_id).  world > 1 with tp > 1 is DP x TP:
+                                `world` replicas of `tp` ranks each (the C4 short rounds) */
+  void* local_group;         /* NULL, or a handle of rp_local_group_create: every rank of
+                                the job (world x tp) is a context of THIS process on THIS
+                                device, created concurrently from one thread per rank;
+                                collectives run through device memory (no NCCL, no IPC)
+                                and nccl ids are ignored (a test mode, not a fast path) */
 } rp_runtime_desc;
 
 typedef struct {
   size_t weights_bytes, workspace_bytes, page_bytes;
 } rp_sizes;
 
-/* One prompt of a round.  `tokens` (len ids in [0, vocab), none == eos) and
- * `trace_lens` (G response lengths >= 1, trace mode only, else NULL) are host
- * pointers, copied by rp_submit_round.  prompt_id is the caller's global id:
+/* One prompt of a round.  `tokens` (len ids in [0, vocab), none == eos),
+ * `trace_lens` (G response lengths >= 1, trace mode only, else NULL) and
+ * `trace_lens_retry` are host pointers, copied by rp_submit_round.  prompt_id is the caller's global id:
  * it seeds the sampler stream uid = prompt_id * G + j (reading Z10). */
 typedef struct {
   int32_t prompt_id;
   int32_t len;
   const int32_t* tokens;
   const int32_t* trace_lens;
+  const int32_t* trace_lens_retry; /* trace mode: G lengths of the re-roll (reading Z5) used if
+                                      this prompt is deferred and later popped by a NULL-prompt
+                                      LONG round; NULL -> trace_lens again */
 } rp_prompt;
 
 typedef struct {
@@ -149,9 +162,22 @@ int rp_query_sizes(const rp_model_desc* md, const rp_runtime_desc* rd, rp_sizes*
  * creates the NCCL communicator when world > 1.  *out receives the context. */
 int rp_init_model(const rp_model_desc* md, const rp_runtime_desc* rd, void** out);
 
+/* Plan the next round (the tail-batching planner; SPEC S:271-279
+ * plan_round): if the long-prompt queue holds >= P0 prompts, *kind = RP_LONG
+ * and *n_prompts = P0 (submit it with prompts == NULL: the first P0 queued
+ * prompts, target = P0); otherwise *kind = RP_SHORT and *n_prompts =
+ * ceil(eta * P0) (submit that many fresh prompts with target = P0).
+ * drain != 0 (end of the prompt stream, reading Z7) plans a LONG round over
+ * a non-empty queue shorter than P0.  Host only; identical on every rank.
+ * Errors: RP_EINVAL (P0 < 1, eta < 1). */
+int rp_plan_round(void* ctx, int32_t P0, float eta, int32_t drain, int32_t* kind, int32_t* n_prompts);
+
 /* Start a round.  prompts: the FULL
  * prompt list of the round (every rank passes the same list); NULL pops
- * n_prompts entries from this context's long-prompt queue (single rank).
+ * n_prompts entries from the head of the long-prompt queue (every DP rank
+ * holds the same global queue, so every rank pops the same prompts and
+ * decodes its slice).  The queue is popped only once the round has started:
+ * a submit that fails leaves it unchanged.
  * G: responses launched per prompt.  keep: responses retained per prompt
  * (R0), 1 <= keep <= G, or 0 for keep = G.  keep < G is response-level
  * speculation ("each prompt produces more than R0
@@ -228,8 +254,25 @@ int rp_round_issue_cap(void* ctx, int32_t max_active);
 int rp_round_unissued(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out);
 
 /* Snapshot of the long-prompt queue (global prompt ids, oldest first); no
- * drain.  ids_out may be NULL to query *n_out. */
+ * drain.  Under data parallelism the queue is global: rp_collect gathers
+ * every rank's accepted prompts (DP collective) and every rank appends all
+ * unaccepted prompts of the round in submission order, so all ranks hold
+ * the same queue.  ids_out may be NULL to query *n_out. */
 int rp_long_queue(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out);
+
+/* Drop the first n entries of the long-prompt queue (they were submitted
+ * explicitly on another context, e.g. a TP context of the same GPUs).
+ * Errors: RP_EINVAL (n < 0 or n > queue length). */
+int rp_long_queue_pop(void* ctx, int32_t n);
+
+/* Single-GPU local group: a host object shared by the
+ * world x tp contexts of one process on one device, holding the exchange
+ * buffers of the device-memory collectives (k_comm.cu) and the TP peer
+ * blocks.  Create it once, pass it in rp_runtime_desc.local_group of every
+ * rank's context, create the contexts concurrently (rp_init_model waits for
+ * all of them), free it after the contexts.  Errors: RP_EINVAL. */
+int rp_local_group_create(int32_t world, int32_t tp, void** out);
+void rp_local_group_free(void* group);
 
 /* Tensor-parallel decode over NVLink peer memory.  A
  * context created with tp > 1 (d a multiple of 128) owns a device block of
@@ -277,8 +320,9 @@ int rp_debug_trace_enable(void* ctx, int32_t steps);
  * buf[t][2 .. 2 + n) = slots.  Row stride = 2 + max_seqs. */
 int rp_debug_trace_get(void* ctx, int32_t* buf, int32_t steps);
 
-/* Logits of the most recent decode step (rows in the live order of that step)
- * and the slots of those rows; requires graph_steps <= 1. */
+/* Logits of the most recent decode step (rows in the live order of that step;
+ * eager or the last step of a CUDA graph) and the slots of those rows;
+ * requires rp_debug_trace_enable. */
 int rp_debug_last_logits(void* ctx, float* logits_out, int32_t* slots_out, int32_t max_rows, int32_t* n_rows);
 
 /* Kernel classes of rp_debug_profile. */

@@ -120,8 +120,18 @@ class KVDecoder:
         self.v = [None] * self.cfg["n_layers"]
         self.n = 0
 
-    def step(self, tokens):
-        """Feed tokens [T] at positions n..n+T-1; returns logits [T, V]."""
+    def fork(self):
+        """An independent decoder with the same cache (the G responses of a
+        prompt continue one shared prompt prefix; `step` never writes the
+        cached arrays in place, so sharing them is safe)."""
+        d = KVDecoder(self.w)
+        d.k, d.v, d.n = list(self.k), list(self.v), self.n
+        return d
+
+    def step(self, tokens, head=True):
+        """Feed tokens [T] at positions n..n+T-1; returns logits [T, V], or
+        with head=False the final-norm hidden states [T, d] (the caller
+        applies the LM head, e.g. in vocab chunks)."""
         cfg = self.cfg
         H, KV, hd, eps = cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"], cfg["rms_eps"]
         f64 = lambda a: np.asarray(a, np.float64)
@@ -146,4 +156,6 @@ class KVDecoder:
             x = x + (silu(h2 @ f64(w["gate"]).T) * (h2 @ f64(w["up"]).T)) @ f64(w["down"]).T
         self.n += T
         h = rmsnorm(x, self.w.final_norm(), eps)
+        if not head:
+            return h
         return h @ np.asarray(self.w.lm_head(), np.float64).T

@@ -139,6 +139,12 @@ __device__ __forceinline__ int block_exscan(int v, int* total, int* smem /*>=33 
   return base + x - v;
 }
 
+// Programmatic dependent launch is switched off on the calling thread while
+// a context of a single-GPU local group (rp_local_group_create) issues work:
+// several contexts then share one GPU, and a PDL-launched kernel parked in
+// griddepcontrol.wait would hold SMs another context's producer needs.
+extern thread_local bool g_no_pdl;
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
@@ -151,7 +157,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_no_pdl ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 

@@ -10,6 +10,9 @@
 
 #include <algorithm>
 #include <climits>
+#include <condition_variable>
+#include <chrono>
+#include <mutex>
 #include <cstdlib>
 #include <cmath>
 #include <cstdarg>
@@ -55,7 +58,8 @@ struct LayerW {
 struct QueuedPrompt {
   int32_t id;
   std::vector<int32_t> tokens;
-  std::vector<int32_t> trace;  // lengths of the long-round attempt (may be empty)
+  std::vector<int32_t> trace;        // lengths of this round's attempt (trace mode)
+  std::vector<int32_t> trace_retry;  // lengths of the re-roll if deferred (reading Z5; empty -> trace)
 };
 
 struct Sizes {
@@ -63,7 +67,53 @@ struct Sizes {
   size_t part_floats, apart_floats;
 };
 
+// Exchange buffers of one communicator of a single-GPU local group
+// (k_comm.cu): slots[2][size][slot_bytes] and the members' epochs gen[size].
+struct LocalComm {
+  int size = 0;
+  size_t slot_bytes = 0;
+  uint8_t* slots = nullptr;
+  unsigned long long* gen = nullptr;
+};
+
+// One communicator of a context: NCCL, or the device-memory exchange of a
+// local group (then `state` = this member's {epoch, ticket} on the device).
+struct CommCtx {
+  ncclComm_t nccl = nullptr;
+  LocalComm* local = nullptr;
+  int size = 1, rank = 0;
+  int* state = nullptr;
+};
+
 }  // namespace
+
+// Single-GPU local group (rp_local_group_create): world x tp contexts of one
+// process on one device.  DP communicator d_t = {(r, t) : r < world} per
+// tp rank t, TP communicator t_r = {(r, q) : q < tp} per replica r.
+struct RpLocalGroup {
+  int world = 1, tp = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0, barrier_gen = 0;
+  std::vector<LocalComm> dp, tpc;     // [tp], [world]
+  std::vector<void*> tp_blocks;       // [world * tp] TP peer receive blocks
+  bool alloc_ok = false;
+  std::string alloc_err;
+
+  // host barrier over every member context (rp_init_model); false after
+  // 300 s without every member (one of them failed before the barrier)
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int g = barrier_gen;
+    if (++arrived == world * tp) {
+      arrived = 0;
+      ++barrier_gen;
+      cv.notify_all();
+      return true;
+    }
+    return cv.wait_for(lk, std::chrono::seconds(300), [&] { return barrier_gen != g; });
+  }
+};
 
 struct RpCtx {
   rp_model_desc md{};
@@ -121,8 +171,12 @@ struct RpCtx {
   int tp = 1;
   bool own_stream = false;
 
-  // NCCL
-  ncclComm_t comm = nullptr;
+  // communicators: data-parallel (the cutoff exchange and round membership)
+  // and tensor-parallel (all-reduces); NCCL or a local group's device memory
+  CommCtx dp, tpc;
+  RpLocalGroup* lg = nullptr;
+  int coop_min = 16;          // cooperative split-K from this chunk width (no_spin: never)
+  int* memb = nullptr;        // [P + 1] local membership, then [world][P + 1] gathered (rp_collect)
 
   // round state (host)
   bool active = false, collected = true;
@@ -131,6 +185,8 @@ struct RpCtx {
   int max_active = 0;      // of the current round (0 = every prompt issued at submit)
   int64_t round_id = 0;
   std::vector<QueuedPrompt> round_prompts;  // this rank's slice
+  std::vector<QueuedPrompt> round_all;      // the whole submitted list (the global FIFO needs every prompt)
+  int fifo_pop = 0;                         // queue entries the active round consumes (popped at submit success)
   std::deque<QueuedPrompt> fifo;
   int trace_steps = 0;
   int* trace_dev = nullptr;
@@ -157,6 +213,10 @@ struct RpCtx {
 };
 
 static std::string g_init_err;
+
+// Programmatic dependent launch is off while a local-group context issues
+// work from this thread (common.cuh g_no_pdl).
+static inline void pdl_mode(const RpCtx* c) { g_no_pdl = c->lg != nullptr; }
 
 #define CK(call)                                                                              \
   do {                                                                                        \
@@ -191,8 +251,13 @@ static Sizes compute_sizes(const rp_model_desc* md, const rp_runtime_desc* rd) {
   z.maxp = (rd->max_prompt_len + rd->max_cap + kPage - 1) / kPage + 1;
   z.Tcap = std::max(rd->max_seqs, rd->max_prompt_tokens);
   z.pt_rows = z.S + z.P;
-  const int max_ctx = rd->max_prompt_len + rd->max_cap + 1;
-  z.max_items_dec = z.S * ((max_ctx + kAttnChunk - 1) / kAttnChunk);
+  // Decode attention work list (ctl phase B): row r gets ns_r <= want_r key
+  // splits with sum_r want_r <= rows + U, U <= 3 * U1 (k-wave budget, k <= 3)
+  // and U1 = 148 / KV (or the RP_ATTN_UNITS override): at most S + 3 * U1.
+  const int kv_loc = md->n_kv_heads / tp_of(rd);
+  const int units_env = getenv("RP_ATTN_UNITS") ? atoi(getenv("RP_ATTN_UNITS")) : 0;
+  const int U1max = std::max(std::max(1, 148 / std::max(1, kv_loc)), units_env);
+  z.max_items_dec = z.S + 3 * U1max;
   z.max_items_pre = rd->max_prompt_tokens * ((rd->max_prompt_len + kAttnChunk - 1) / kAttnChunk) + z.P;
   // split-K partials: worst GEMM at the decode sizes
   const ModelDims lm = local_dims(md, rd);
@@ -298,7 +363,8 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto row_pt = cv.take<int>(z.S);
   auto best = cv.take<unsigned long long>(std::max(z.S, 1));
   auto ks_local = cv.take<int>(4);
-  auto ks = cv.take<int>((size_t)3 * std::max(1, rd->world));
+  auto ks = cv.take<int>((size_t)4 * std::max(1, rd->world));
+  auto memb = cv.take<int>((size_t)(z.P + 1) * (1 + std::max(1, rd->world)));
   auto ctl = cv.take<CtlBlock>(1);
   const size_t page_bytes = lm.page_bytes;
   const size_t max_pages = rd->kv_pool_bytes / page_bytes;
@@ -311,6 +377,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
     c->items_pre = items_pre; c->pre_tok = pre_tok; c->pre_pos = pre_pos; c->pre_pt = pre_pt;
     c->pre_last = pre_last; c->fork_jobs = fork_jobs; c->col_meta = col_meta; c->col_tok = col_tok;
     c->identity_pages = ident;
+    c->memb = memb;
     RoundDev& R = c->R;
     R.S = z.S; R.P = z.P; R.maxp = z.maxp; R.kv_heads = (int)KV; R.eos = md->eos_id;
     R.world = rd->world; R.rank = rd->rank;
@@ -320,6 +387,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
     R.status = status; R.own0 = own0; R.t0 = t0; R.p_last_tok = p_last_tok; R.p_stamp = p_stamp; R.tok_out = tok_out; R.page_table = page_table; R.p_cnt = p_cnt;
     R.p_state = p_state; R.p_gid = p_gid; R.comp_list = comp_list; R.accept_order = accept_order;
     R.live = live; R.live_next = live_next; R.tok_in = tok_in; R.row_pos = row_pos; R.row_pt = row_pt;
+    R.max_items = z.max_items_dec;
     R.best = best; R.items = items_dec; R.rows_hist = rows_hist; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
     R.ctl = ctl; R.cap = rd->max_cap;
   }
@@ -339,11 +407,13 @@ static int validate(const rp_model_desc* md, const rp_runtime_desc* rd, std::str
   if (md->n_heads / md->n_kv_heads > 8) return bad("n_heads/n_kv_heads (<= 8)");
   if (((md->n_heads + 2 * md->n_kv_heads) * md->head_dim) % 128) return bad("qkv width (multiple of 128)");
   if (md->eos_id < 0 || md->eos_id >= md->vocab) return bad("eos_id");
+  const RpLocalGroup* lg = (const RpLocalGroup*)rd->local_group;
+  if (lg && (lg->world != std::max(1, rd->world) || lg->tp != std::max(1, rd->tp)))
+    return bad("local_group (created for another world / tp)");
   if (rd->tp > 1) {
     const int T = rd->tp;
-    if (rd->world != 1) return bad("tp (tensor parallelism needs world == 1 for this context)");
     if (rd->tp_rank < 0 || rd->tp_rank >= T) return bad("tp_rank");
-    if (!rd->nccl_id) return bad("nccl_id (tp > 1)");
+    if (!lg && !rd->tp_nccl_id && !(rd->world == 1 && rd->nccl_id)) return bad("tp_nccl_id (tp > 1)");
     if (md->n_kv_heads % T || md->n_heads % T) return bad("tp (must divide n_heads and n_kv_heads)");
     if ((md->d_ff / T) % 64 || md->d_ff % T) return bad("tp (d_ff / tp multiple of 64)");
     if (md->vocab % T || (md->vocab / T) % 128) return bad("tp (vocab / tp multiple of 128)");
@@ -351,7 +421,7 @@ static int validate(const rp_model_desc* md, const rp_runtime_desc* rd, std::str
     if ((md->n_heads / T * md->head_dim) % 64) return bad("tp (local attention width)");
   }
   if (rd->world < 1 || rd->rank < 0 || rd->rank >= rd->world) return bad("rank/world");
-  if (rd->world > 1 && !rd->nccl_id) return bad("nccl_id (world > 1)");
+  if (rd->world > 1 && !rd->nccl_id && !lg) return bad("nccl_id (world > 1)");
   if (rd->tp < 0 || rd->tp > 8) return bad("tp (1..8)");
   if (rd->max_seqs < 1 || rd->max_seqs > 1 << 16) return bad("max_seqs");
   if (rd->max_prompts < 1 || rd->max_prompts > rd->max_seqs) return bad("max_prompts");
@@ -380,9 +450,10 @@ struct ProfScope {
   }
 };
 // Folded RMSNorm (DESIGN.md §5 K6): FOLD_PRODUCE on a RESID GEMM also writes
-// bf16(x) into c->h and per-tile sums of squares into c->ssq; FOLD_CONSUME
-// scales each output row of a GEMM reading c->h by 1/rms.  Valid because the
-// norm weights are 1 (Z12); under TP the RMSNorm kernel runs instead.
+// fp16(x) into c->h and per-tile sums of squares into c->ssq; FOLD_CONSUME
+// scales each output row of a GEMM reading c->h by 1/rms.  The norm gains are
+// folded into the consuming weights at init (rp_init_model), so every norm
+// runs with unit gain; under TP the RMSNorm kernel runs instead.
 enum { FOLD_NONE = 0, FOLD_PRODUCE = 1, FOLD_CONSUME = 2 };
 
 // Tensor-parallel peer push of a row-parallel GEMM's fp32 output: rank q's
@@ -392,6 +463,28 @@ static float* tp_slot(RpCtx* c, void* base, int slot, int src) {
 }
 static unsigned long long* tp_flags(RpCtx* c, void* base, int slot) {
   return (unsigned long long*)((float*)base + 2 * c->tp_recv_floats) + (size_t)slot * c->tp;
+}
+
+// ---------------------------------------------------------------- collectives
+// NCCL (one process per GPU) or the device-memory exchange of a single-GPU
+// local group; both carry the same message and combine it in rank order.
+static void local_coll(RpCtx* c, CommCtx& cm, int op, const void* send, void* recv, size_t bytes) {
+  launch_local_publish(send, bytes, cm.local->slots, cm.local->slot_bytes, cm.size, cm.rank, cm.local->gen, cm.state,
+                       c->st);
+  launch_local_reduce(op, recv, bytes, cm.local->slots, cm.local->slot_bytes, cm.size, cm.local->gen, cm.state, c->st);
+  c->launches += 2;
+}
+static void coll_allgather_i32(RpCtx* c, CommCtx& cm, const int* send, int* recv, size_t count) {
+  if (cm.local) local_coll(c, cm, LOP_GATHER, send, recv, count * 4);
+  else ncclAllGather(send, recv, count, ncclInt32, cm.nccl, c->st);
+}
+static void coll_allreduce_sum_f32(RpCtx* c, CommCtx& cm, float* buf, size_t count) {
+  if (cm.local) local_coll(c, cm, LOP_SUM_F32, buf, buf, count * 4);
+  else ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, cm.nccl, c->st);
+}
+static void coll_allreduce_max_u64(RpCtx* c, CommCtx& cm, unsigned long long* buf, size_t count) {
+  if (cm.local) local_coll(c, cm, LOP_MAX_U64, buf, buf, count * 8);
+  else ncclAllReduce(buf, buf, count, ncclUint64, ncclMax, cm.nccl, c->st);
 }
 
 static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, int n_host, int splits, int epi,
@@ -409,6 +502,7 @@ static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, in
   if (rope) a.rope = *rope;
   a.M = M; a.K = K; a.n_dev = n_dev; a.n_host = n_host; a.splits = splits; a.epi = epi; a.out = out; a.ldo = ldo;
   a.bias = bias; a.partial = c->gpart; a.counters = c->gctr;
+  a.no_spin = c->lg ? 1 : 0;
   a.ssq_stride = c->m.d / 128; a.ssq_parts = c->m.d / 128;
   a.norm_inv_d = 1.0f / (float)c->m.d; a.norm_eps = c->m.eps;
   if (fold == FOLD_PRODUCE) { a.xb_out = c->h; a.ldxb = c->m.d; a.ssq_out = c->ssq; }
@@ -421,7 +515,7 @@ static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, in
 // (a host count: the graph bucket at decode, the prompt tokens at prefill).
 static void tp_allreduce_rows(RpCtx* c, int rows) {
   ProfScope ps(c, RP_PROF_NCCL);
-  ncclAllReduce(c->ar, c->ar, (size_t)rows * c->m.d, ncclFloat32, ncclSum, c->comm, c->st);
+  coll_allreduce_sum_f32(c, c->tpc, c->ar, (size_t)rows * c->m.d);
 }
 
 // Transformer body over `n` rows (n_dev on device or n_host): decode (one token
@@ -450,19 +544,20 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
     ProfScope ps(c, RP_PROF_RMSNORM);
     void* own = c->tp_peer_base[c->rd.tp_rank];
     launch_tp_norm(c->x, tp_slot(c, own, slot, 0), c->tp, c->tp_recv_floats / c->tp, tp_flags(c, own, slot),
-                   c->tp_gen + slot, c->tp_done + slot, m.d / 128, splits, n_dev, n_host, gamma, c->h, m.d, m.eps,
-                   c->st);
+                   c->tp_gen + slot, c->tp_done + slot, m.d / 128, splits, c->coop_min, c->lg ? 8 : 0, n_dev, n_host,
+                   gamma, c->h, m.d, m.eps, c->st);
     c->launches++;
   };
   { ProfScope ps(c, RP_PROF_EMBED); launch_embed(tok, n_dev, n_host, c->emb, c->x, m.d, c->st); c->launches++; }
   for (int l = 0; l < m.L; ++l) {
-    LayerW& w = c->layers[l];
+    const LayerW& w = c->layers[l];
     const int f_in = (fold && l > 0) ? FOLD_CONSUME : FOLD_NONE;
+    // the norm gains are folded into the consuming weights at init (unit gain here)
     if (peer && l > 0) {
-      tp_norm(1, w.ln1, sp_down);
+      tp_norm(1, nullptr, sp_down);
     } else if (f_in == FOLD_NONE) {
       ProfScope ps(c, RP_PROF_RMSNORM);
-      launch_rmsnorm(c->x, delta, nullptr, n_dev, n_host, w.ln1, c->h, m.d, m.eps, c->st); c->launches++;
+      launch_rmsnorm(c->x, delta, nullptr, n_dev, n_host, nullptr, c->h, m.d, m.eps, c->st); c->launches++;
     }
     if (decode && sp_qkv > 1 && m.hd % 64 == 0) {
       // RoPE + KV append fused into the split-K reduction of the QKV GEMM
@@ -484,13 +579,13 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
       gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
            nullptr, nullptr, f_prod, peer ? 0 : -1); }
     if (peer) {
-      tp_norm(0, w.ln2, sp_o);
+      tp_norm(0, nullptr, sp_o);
     } else if (tp) {
       tp_allreduce_rows(c, ar_rows);
     }
     if (!fold && !peer) {
       ProfScope ps(c, RP_PROF_RMSNORM);
-      launch_rmsnorm(c->x, tp ? c->ar : nullptr, nullptr, n_dev, n_host, w.ln2, c->h, m.d, m.eps, c->st);
+      launch_rmsnorm(c->x, tp ? c->ar : nullptr, nullptr, n_dev, n_host, nullptr, c->h, m.d, m.eps, c->st);
       c->launches++;
     }
     { ProfScope ps(c, RP_PROF_GEMM_GU);
@@ -517,12 +612,12 @@ static void lm_head_sample(RpCtx* c, const int* n_dev, int n_host, const int* ga
     ProfScope ps(c, RP_PROF_RMSNORM);
     void* own = c->tp_peer_base[c->rd.tp_rank];
     launch_tp_norm(c->x, tp_slot(c, own, 1, 0), c->tp, c->tp_recv_floats / c->tp, tp_flags(c, own, 1),
-                   c->tp_gen + 1, c->tp_done + 1, c->m.d / 128, c->s_down, n_dev, n_host, c->lnf, c->h, c->m.d,
-                   c->m.eps, c->st);
+                   c->tp_gen + 1, c->tp_done + 1, c->m.d / 128, c->s_down, c->coop_min, c->lg ? 8 : 0, n_dev, n_host,
+                   nullptr, c->h, c->m.d, c->m.eps, c->st);
     c->launches++;
   } else if (!fold) {
     ProfScope ps(c, RP_PROF_RMSNORM);
-    launch_rmsnorm(c->x, pending ? c->ar : nullptr, gather, n_dev, n_host, c->lnf, c->h, c->m.d, c->m.eps, c->st);
+    launch_rmsnorm(c->x, pending ? c->ar : nullptr, gather, n_dev, n_host, nullptr, c->h, c->m.d, c->m.eps, c->st);
     c->launches++;
   }
   { ProfScope ps(c, RP_PROF_GEMM_LM);
@@ -533,7 +628,7 @@ static void lm_head_sample(RpCtx* c, const int* n_dev, int n_host, const int* ga
                    (uint32_t)c->round_id, c->st); c->launches++; }
   if (c->tp > 1) {
     ProfScope ps(c, RP_PROF_NCCL);
-    ncclAllReduce(R.best, R.best, (size_t)best_rows, ncclUint64, ncclMax, c->comm, c->st);
+    coll_allreduce_max_u64(c, c->tpc, R.best, (size_t)best_rows);
   }
 }
 
@@ -548,7 +643,7 @@ static void decode_step(RpCtx* c, int bucket) {
     launch_ctl(R, 1, 0, c->st); c->launches++;
   } else {
     { ProfScope ps(c, RP_PROF_CTL); launch_ctl(R, 1, 1, c->st); c->launches++; }
-    { ProfScope ps(c, RP_PROF_NCCL); ncclAllGather(R.ks_local, R.ks, 3, ncclInt32, c->comm, c->st); }
+    { ProfScope ps(c, RP_PROF_NCCL); coll_allgather_i32(c, c->dp, R.ks_local, R.ks, 3); }
     { ProfScope ps(c, RP_PROF_CTL); launch_ctl(R, 1, 2, c->st); c->launches++; }
   }
 }
@@ -691,6 +786,15 @@ static int init_impl(RpCtx* c) {
   launch_init_weights(c->emb, (long long)md->vocab, (int)d, 0, 0, (int)d, 0x10000000u, seed, 0, 0, c->st, 0);
   launch_init_weights(c->lm, (long long)V, (int)d, (long long)m.v0, 0, (int)d, 0x10000001u, seed, 0, 0, c->st);
   CK(cudaMemcpyAsync(c->lnf, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
+  // RMSNorm gains folded into the consuming GEMMs' weight columns (QKV <- ln1,
+  // gate||up <- ln2, LM head <- final norm): RMSNorm(x) * g . W^T =
+  // (x / rms) . (W diag g)^T, so every norm kernel and folded norm runs with
+  // unit gain.  The Z12 gains are 1, for which the fold is exact.
+  for (auto& w : c->layers) {
+    launch_scale_cols(w.wqkv, (long long)((H + 2 * KV) * hd), (int)d, w.ln1, c->st);
+    launch_scale_cols(w.wgu, (long long)(2 * F), (int)d, w.ln2, c->st);
+  }
+  launch_scale_cols(c->lm, (long long)V, (int)d, c->lnf, c->st);
   CK(cudaGetLastError());
 
   // ---- RoPE frequencies theta^(-2i/hd) in fp64
@@ -759,12 +863,64 @@ static int init_impl(RpCtx* c) {
     c->tp_done = (int*)(c->tp_gen + 2);
   }
 
-  // ---- NCCL
-  if (rd->world > 1 || c->tp > 1) {   // DP cutoff exchange or TP all-reduces
-    ncclUniqueId id;
-    memcpy(&id, rd->nccl_id, sizeof id);
-    if (c->tp > 1) CKN(ncclCommInitRank(&c->comm, c->tp, id, rd->tp_rank));
-    else CKN(ncclCommInitRank(&c->comm, rd->world, id, rd->rank));
+  // ---- communicators: DP group (the ranks with this tp_rank, one per
+  // replica) and TP group (this replica's tp ranks)
+  c->lg = (RpLocalGroup*)rd->local_group;
+  c->coop_min = c->lg ? 0x7FFFFFFF : gemm_coop_min();
+  c->dp.size = std::max(1, rd->world); c->dp.rank = rd->world > 1 ? rd->rank : 0;
+  c->tpc.size = c->tp; c->tpc.rank = c->tp > 1 ? rd->tp_rank : 0;
+  if (c->lg) {
+    RpLocalGroup* g = c->lg;
+    {
+      // the first member sizes and allocates the exchange buffers
+      std::lock_guard<std::mutex> lk(g->mu);
+      if (!g->alloc_ok && g->alloc_err.empty()) {
+        const size_t dp_slot = align_up((size_t)(c->z.P + 1) * 4 + 16, 256);
+        const size_t tp_slot = align_up(std::max((size_t)c->z.Tcap * m.d * 4, (size_t)c->z.S * 8) + 16, 256);
+        auto mk = [&](LocalComm& lc, int size, size_t slot) -> bool {
+          lc.size = size; lc.slot_bytes = slot;
+          if (cudaMalloc(&lc.slots, 2 * (size_t)size * slot) != cudaSuccess) return false;
+          if (cudaMalloc(&lc.gen, (size_t)size * 8) != cudaSuccess) return false;
+          return cudaMemset(lc.gen, 0, (size_t)size * 8) == cudaSuccess;
+        };
+        g->dp.resize(g->tp); g->tpc.resize(g->world);
+        bool ok = true;
+        if (g->world > 1) for (auto& lc : g->dp) ok = ok && mk(lc, g->world, dp_slot);
+        if (g->tp > 1) for (auto& lc : g->tpc) ok = ok && mk(lc, g->tp, tp_slot);
+        g->tp_blocks.assign((size_t)g->world * g->tp, nullptr);
+        if (ok) g->alloc_ok = true; else g->alloc_err = "local group exchange buffers: cudaMalloc failed";
+      }
+      if (!g->alloc_ok) return c->fail(RP_ECUDA, "%s", g->alloc_err.c_str());
+      if (c->tp > 1) g->tp_blocks[(size_t)c->dp.rank * c->tp + c->tpc.rank] = c->tp_ipc;
+    }
+    CK(cudaMalloc(&c->dp.state, 8 * sizeof(int)));
+    CK(cudaMemset(c->dp.state, 0, 8 * sizeof(int)));
+    c->tpc.state = c->dp.state + 4;
+    if (c->dp.size > 1) {
+      c->dp.local = &g->dp[c->tpc.rank];
+      if ((size_t)(c->z.P + 1) * 4 + 16 > c->dp.local->slot_bytes) return c->fail(RP_EINVAL, "local group: max_prompts differ");
+    }
+    if (c->tp > 1) {
+      c->tpc.local = &g->tpc[c->dp.rank];
+      if ((size_t)c->z.Tcap * m.d * 4 > c->tpc.local->slot_bytes) return c->fail(RP_EINVAL, "local group: capacities differ");
+    }
+    CK(cudaStreamSynchronize(c->st));
+    if (!g->barrier()) return c->fail(RP_ESTATE, "local group: not every member reached rp_init_model");
+    if (c->tp > 1 && c->tp_ipc) {
+      for (int q = 0; q < c->tp; ++q) c->tp_peer_base[q] = g->tp_blocks[(size_t)c->dp.rank * c->tp + q];
+      c->tp_peer = true;   // plain device pointers: the peers live on this device
+    }
+  } else {
+    if (rd->world > 1) {
+      ncclUniqueId id;
+      memcpy(&id, rd->nccl_id, sizeof id);
+      CKN(ncclCommInitRank(&c->dp.nccl, rd->world, id, rd->rank));
+    }
+    if (c->tp > 1) {
+      ncclUniqueId id;
+      memcpy(&id, rd->tp_nccl_id ? rd->tp_nccl_id : rd->nccl_id, sizeof id);
+      CKN(ncclCommInitRank(&c->tpc.nccl, c->tp, id, rd->tp_rank));
+    }
   }
 
   c->graph_dirty = true;
@@ -780,6 +936,8 @@ int rp_init_model(const rp_model_desc* md, const rp_runtime_desc* rd, void** out
   RpCtx* c = new RpCtx();
   c->md = *md;
   c->rd = *rd;
+  c->lg = (RpLocalGroup*)rd->local_group;
+  pdl_mode(c);
   r = init_impl(c);
   if (r) {
     g_init_err = c->err;
@@ -805,9 +963,12 @@ void rp_free(void* ctx) {
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->trace_dev) cudaFree(c->trace_dev);
-  if (c->comm) ncclCommDestroy(c->comm);
-  for (int q = 0; q < 8; ++q)
-    if (c->tp_peer_base[q] && c->tp_peer_base[q] != c->tp_ipc) cudaIpcCloseMemHandle(c->tp_peer_base[q]);
+  if (c->dp.nccl) ncclCommDestroy(c->dp.nccl);
+  if (c->tpc.nccl) ncclCommDestroy(c->tpc.nccl);
+  if (c->dp.state) cudaFree(c->dp.state);
+  if (!c->lg)
+    for (int q = 0; q < 8; ++q)
+      if (c->tp_peer_base[q] && c->tp_peer_base[q] != c->tp_ipc) cudaIpcCloseMemHandle(c->tp_peer_base[q]);
   if (c->tp_ipc) cudaFree(c->tp_ipc);
   if (c->tp_gen) cudaFree(c->tp_gen);
   if (c->attn_tl) { attn_set_timeline(nullptr); cudaFree(c->attn_tl); }
@@ -892,6 +1053,7 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
                     int32_t target, int32_t flags, int64_t round_id) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
+  pdl_mode(c);
   if (c->active) return c->fail(RP_EBUSY, "a round is active (collect it first)");
   const int kind = flags & RP_LONG ? 1 : 0;
   const int trace = flags & RP_TRACE ? 1 : 0;
@@ -903,12 +1065,17 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   if (cap < 1 || cap > c->rd.max_cap) return c->fail(RP_EINVAL, "invalid field: cap (1..max_cap)");
   if (target < 1 || target > n) return c->fail(RP_EINVAL, "invalid field: target (1..n_prompts)");
   if (kind == 1 && target != n) return c->fail(RP_EINVAL, "invalid field: target (RP_LONG needs target == n_prompts)");
-  // the full list (this rank's slice is decoded)
+  // the full list (this rank's slice is decoded).  A NULL list takes the head
+  // of the (global) long-prompt queue; the entries leave the queue only once
+  // the round has started, so a failed submit loses no prompt
   std::vector<QueuedPrompt> all;
+  int pop = 0;
   if (!prompts) {
-    if (c->rd.world > 1) return c->fail(RP_EINVAL, "invalid field: prompts (NULL queue pop needs world == 1)");
     if ((int)c->fifo.size() < n) return c->fail(RP_EINVAL, "invalid field: n_prompts (queue holds %zu)", c->fifo.size());
-    for (int i = 0; i < n; ++i) { all.push_back(c->fifo.front()); c->fifo.pop_front(); }
+    all.assign(c->fifo.begin(), c->fifo.begin() + n);
+    for (auto& q : all)   // the long round re-rolls the prompt (reading Z5)
+      if (!q.trace_retry.empty()) q.trace = q.trace_retry;
+    pop = n;
   } else {
     all.resize(n);
     for (int i = 0; i < n; ++i) {
@@ -924,6 +1091,11 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
         all[i].trace.assign(p.trace_lens, p.trace_lens + G);
         for (int L : all[i].trace)
           if (L < 1) return c->fail(RP_EINVAL, "invalid field: prompts[%d].trace_lens (>= 1)", i);
+        if (p.trace_lens_retry) {
+          all[i].trace_retry.assign(p.trace_lens_retry, p.trace_lens_retry + G);
+          for (int L : all[i].trace_retry)
+            if (L < 1) return c->fail(RP_EINVAL, "invalid field: prompts[%d].trace_lens_retry (>= 1)", i);
+        }
       }
     }
   }
@@ -955,6 +1127,7 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   c->max_active = A;
   c->lo = lo; c->n_loc = n_loc; c->round_id = round_id;
   c->round_prompts.assign(all.begin() + lo, all.begin() + lo + n_loc);
+  c->round_all = all;
   RoundDev& R = c->R;
   R.cap = cap; R.G = G; R.keep = keep; R.target = target; R.kind = kind; R.trace = trace; R.n_prompts = n_loc;
   R.max_active = A;
@@ -1027,16 +1200,16 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   launch_sampler(c->logits, c->m.V, c->m.v0, G, R, c->rd.sample_seed, 1.0f / c->rd.temperature, (uint32_t)round_id,
                  c->st);
   c->launches++;
-  if (c->tp > 1 && nS > 0)
-    CKN(ncclAllReduce(R.best, R.best, (size_t)n_first * G, ncclUint64, ncclMax, c->comm, c->st));
+  if (c->tp > 1 && nS > 0) coll_allreduce_max_u64(c, c->tpc, R.best, (size_t)n_first * G);
   if (c->rd.world == 1) {
     launch_ctl(R, 0, 0, c->st); c->launches++;
   } else {
     launch_ctl(R, 0, 1, c->st); c->launches++;
-    CKN(ncclAllGather(R.ks_local, R.ks, 3, ncclInt32, c->comm, c->st));
+    coll_allgather_i32(c, c->dp, R.ks_local, R.ks, 3);
     launch_ctl(R, 0, 2, c->st); c->launches++;
   }
   CK(cudaGetLastError());
+  for (int i = 0; i < pop; ++i) c->fifo.pop_front();
   c->active = true;
   c->collected = false;
   c->step_logits_valid = false;
@@ -1064,6 +1237,7 @@ static void fill_status(RpCtx* c, rp_status* st) {
 int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
+  pdl_mode(c);
   if (!c->active) return c->fail(RP_ESTATE, "no active round");
   int rc = read_ctl(c);
   if (rc) return rc;
@@ -1095,6 +1269,7 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
       CK(cudaGraphLaunch(c->gexec, c->st));
       c->launches += c->graph_nodes;
       steps += c->rd.graph_steps;
+      c->step_logits_valid = true;   // logits of the graph's last decoded step
     } else {
       decode_step(c, bucket);
       CK(cudaGetLastError());
@@ -1124,6 +1299,7 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
   }
   if (c->h_ctl->err == 1) return c->fail(RP_ENOMEM_KV, "KV page pool exhausted (no preemption; reading Z17)");
   if (c->h_ctl->err == 2) return c->fail(RP_ENOSPC, "page table overflow (max_prompt_len + max_cap)");
+  if (c->h_ctl->err == 3) return c->fail(RP_ENOSPC, "decode attention work list overflow (capacity %d)", c->z.max_items_dec);
   return RP_OK;
 }
 
@@ -1164,6 +1340,7 @@ int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, i
                int64_t* n_tok) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
+  pdl_mode(c);
   if (!c->active) return c->fail(RP_ESTATE, "no active round");
   int rc = read_ctl(c);
   if (rc) return rc;
@@ -1171,12 +1348,29 @@ int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, i
   std::vector<char> accepted(c->n_loc, 0);
   if ((rc = collect_range(c, 0, out, max_out, tok_buf, tok_cap, n_out, n_tok, &accepted))) return rc;
   if (!out) return RP_OK;
-  if (c->kind == 0)
-    for (int p = 0; p < c->n_loc; ++p)
-      if (!accepted[p] && p < c->h_ctl->n_issued) {
-        QueuedPrompt q = c->round_prompts[p];
-        c->fifo.push_back(q);
-      }
+  if (c->kind == 0) {
+    // Deferral (reading Z7): every issued, unaccepted prompt of the
+    // round joins the long-prompt queue in submission order.  Under DP the
+    // ranks all-gather {accepted flags of their slice, prompts issued}, so
+    // every rank appends the same prompts: the queue is global.
+    const int W = c->rd.world, P1 = c->z.P + 1;
+    std::vector<int> memb((size_t)P1 * W, 0);
+    for (int p = 0; p < c->n_loc; ++p) memb[p] = accepted[p];
+    memb[P1 - 1] = std::min(c->h_ctl->n_issued, c->n_loc);
+    if (W > 1) {
+      CK(cudaMemcpyAsync(c->memb, memb.data(), (size_t)P1 * 4, cudaMemcpyHostToDevice, c->st));
+      coll_allgather_i32(c, c->dp, c->memb, c->memb + P1, (size_t)P1);
+      CK(cudaMemcpyAsync(memb.data(), c->memb + P1, (size_t)P1 * W * 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+    }
+    const int n = c->n_glob, base = n / W, extra = n % W;
+    for (int q = 0; q < W; ++q) {
+      const int lo_q = q * base + std::min(q, extra), n_q = base + (q < extra ? 1 : 0);
+      const int* mq = memb.data() + (size_t)q * P1;
+      for (int i = 0; i < n_q; ++i)
+        if (!mq[i] && i < mq[P1 - 1]) c->fifo.push_back(c->round_all[lo_q + i]);
+    }
+  }
   c->active = false;
   c->collected = true;
   return RP_OK;
@@ -1186,6 +1380,7 @@ int rp_collect_ready(void* ctx, int32_t first, rp_response* out, int32_t max_out
                      int32_t* n_out, int64_t* n_tok, int32_t* n_accepted) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
+  pdl_mode(c);
   if (!c->active) return c->fail(RP_ESTATE, "no active round");
   int rc = read_ctl(c);
   if (rc) return rc;
@@ -1271,9 +1466,60 @@ int rp_long_queue(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out) {
   return RP_OK;
 }
 
+int rp_long_queue_pop(void* ctx, int32_t n) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (n < 0 || n > (int)c->fifo.size()) return c->fail(RP_EINVAL, "invalid field: n (queue holds %zu)", c->fifo.size());
+  for (int i = 0; i < n; ++i) c->fifo.pop_front();
+  return RP_OK;
+}
+
+// The tail-batching planner ("once the long-prompt queue reaches
+// P0, a long round ... otherwise a short round over eta P0 fresh prompts";
+// SPEC S:271-279 plan_round, S:277 ceil(eta * P0); reading Z7 for the drain).
+int rp_plan_round(void* ctx, int32_t P0, float eta, int32_t drain, int32_t* kind, int32_t* n_prompts) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (P0 < 1) return c->fail(RP_EINVAL, "invalid field: P0 (>= 1)");
+  if (!(eta >= 1.0f)) return c->fail(RP_EINVAL, "invalid field: eta (>= 1)");
+  if (!kind || !n_prompts) return c->fail(RP_EINVAL, "invalid field: kind/n_prompts (NULL)");
+  const int q = (int)c->fifo.size();
+  if (q >= P0 || (drain && q > 0)) {
+    *kind = RP_LONG;
+    *n_prompts = std::min(q, P0);
+  } else {
+    *kind = RP_SHORT;
+    // ceil in exact arithmetic: eta is a float (1.25 exactly); the tiny
+    // margin keeps a product that lands on an integer from rounding up
+    *n_prompts = (int)std::ceil((double)eta * (double)P0 - 1e-9);
+  }
+  return RP_OK;
+}
+
+int rp_local_group_create(int32_t world, int32_t tp, void** out) {
+  if (!out || world < 1 || tp < 1 || tp > 8 || world * tp > 64) {
+    g_init_err = "invalid field: world/tp/out";
+    return RP_EINVAL;
+  }
+  RpLocalGroup* g = new RpLocalGroup();
+  g->world = world;
+  g->tp = tp;
+  *out = g;
+  return RP_OK;
+}
+
+void rp_local_group_free(void* group) {
+  RpLocalGroup* g = (RpLocalGroup*)group;
+  if (!g) return;
+  for (auto& lc : g->dp) { if (lc.slots) cudaFree(lc.slots); if (lc.gen) cudaFree(lc.gen); }
+  for (auto& lc : g->tpc) { if (lc.slots) cudaFree(lc.slots); if (lc.gen) cudaFree(lc.gen); }
+  delete g;
+}
+
 int rp_debug_logits(void* ctx, const int32_t* tokens, int32_t n, float* logits_out) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
+  pdl_mode(c);
   if (c->active) return c->fail(RP_EBUSY, "a round is active");
   if (n < 1 || n > c->rd.max_prompt_len || n > c->rd.max_prompt_tokens) return c->fail(RP_EINVAL, "invalid field: n");
   for (int i = 0; i < n; ++i)
@@ -1317,7 +1563,7 @@ int rp_debug_trace_get(void* ctx, int32_t* buf, int32_t steps) {
 int rp_debug_last_logits(void* ctx, float* logits_out, int32_t* slots_out, int32_t max_rows, int32_t* n_rows) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
-  if (!c->step_logits_valid) return c->fail(RP_ESTATE, "no eager decode step ran (graph_steps must be 0)");
+  if (!c->step_logits_valid) return c->fail(RP_ESTATE, "no decode step ran since submit");
   // rows of the last step were the live list before compaction: trace row t-1 holds it
   if (!c->trace_dev) return c->fail(RP_ESTATE, "needs rp_debug_trace_enable");
   int rc = read_ctl(c);
@@ -1359,6 +1605,7 @@ int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, flo
                   int32_t K, int32_t splits, int32_t iters, float* ms_out) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
+  pdl_mode(c);
   if (M % 128 || K % 64 || M <= 0 || K <= 0 || N < 0 || N > rows_cap) return c->fail(RP_EINVAL, "invalid GEMM shape");
   if (splits <= 0) splits = gemm_pick_splits(M, K, kSMs);
   splits = std::min(splits, K / 64);

@@ -11,7 +11,8 @@ namespace rp {
 enum GemmEpi { EPI_F32 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_BF16 = 3, EPI_QKV_ROPE = 4 };
 
 // Fused QKV epilogue (decode, split-K path): bias, rotate-half RoPE from a
-// per-position cos/sin table, q -> q_out bf16 [n][H][hd], k/v -> KV page.
+// per-position cos/sin table, q -> q_out fp16 [n][H][hd], k/v -> KV page
+// (fp16, reading Z20).
 struct RopeArgs {
   __half* q_out;
   uint8_t* kv_pool;
@@ -29,6 +30,7 @@ struct GemmArgs {
   int n_host;
   int splits;             // split-K factor (1 = direct epilogue)
   int coop_min;           // cooperative split-K reduction from this chunk width up (set by gemm_launch)
+  int no_spin;            // 1: no inter-CTA waits (ticket reduction only; single-GPU local groups)
   int epi;                // GemmEpi
   void* out;              // out[n * ldo + m] (SWIGLU: out[n * ldo + feature])
   int ldo;
@@ -37,8 +39,9 @@ struct GemmArgs {
   int* counters;          // split-K tickets, zero-initialised, self-resetting
   long long* timeline;    // debug: per-CTA %globaltimer stamps [grid][16] (nullptr = off)
   RopeArgs rope;          // EPI_QKV_ROPE only
-  // Folded RMSNorm (norm weights are 1, Z12): a RESID producer also writes
-  // bf16(x) to xb_out[n * ldxb + m] and the sum of squares of its 128-feature
+  // Folded RMSNorm (the gains are folded into the consuming weights at init):
+  // a RESID producer also writes
+  // fp16(x) to xb_out[n * ldxb + m] and the sum of squares of its 128-feature
   // tile to ssq_out[n * ssq_stride + tile]; a consumer (ssq_in != nullptr)
   // multiplies output column n by rsqrt(sum_p ssq_in[n * ssq_stride + p] *
   // norm_inv_d + norm_eps), p < ssq_parts, before bias / SwiGLU / RoPE.
@@ -58,7 +61,7 @@ struct GemmArgs {
 };
 
 struct GemmPlan {
-  CUtensorMap tmA;        // weights [M, K], box 64 x 128
+  CUtensorMap tmA;        // weights [M, K] fp16, box 64 x 128
   CUtensorMap tmB16, tmB64, tmB256;   // activations [rows_cap, K], boxes of 16 / 64 / 256 rows
 };
 

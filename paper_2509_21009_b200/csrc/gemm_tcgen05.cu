@@ -12,9 +12,10 @@
 // read TMEM with tcgen05.ld and apply the fused epilogue.
 //
 // Work = m_tiles x n_chunks(256) x splits.  Split-K (fixed per weight shape,
-// independent of N, so results are batch invariant) writes fp32 partials; the
-// last CTA of a tile (atomic ticket) sums them in split order (deterministic)
-// and runs the epilogue.
+// independent of N, so results are batch invariant) writes fp32 partials that
+// are summed in split order (deterministic): by the tile's last CTA (ticket),
+// by a designated reducer split, or cooperatively by all split CTAs of the
+// tile (one column slice each) -- the same sums bit for bit.
 //
 // Epilogues (DESIGN.md §5 K1/K2): F32 (+bias) for QKV and logits, RESID
 // (fp32 residual +=) for O/down, SWIGLU (tile rows 0-63 gate, 64-127 up of the
@@ -338,9 +339,11 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         const uint32_t stage_tx = (uint32_t)CG * (A_BYTES + nbox * brow * BK * 2);
         const int cnt = kb1 - kb0;
         // rotate the K order per tile so the CTAs do not all request the same
-        // activation tile at the same time (an L2 hot spot); the accumulation
-        // order stays fixed per tile (deterministic, batch invariant)
-        const int rot = (I.tile * 7 + I.chunk * 3) % cnt;
+        // activation tile at the same time (an L2 hot spot).  The rotation
+        // depends on the weight tile only, so a row's accumulation order is
+        // the same in every 256-row chunk: results are batch invariant
+        // (identical for any live count, position in the batch or DP split)
+        const int rot = (I.tile * 7) % cnt;
         int j0 = 0;
         if (first) {
           // Programmatic dependent launch: the weights do not depend on the
@@ -512,7 +515,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           const int per = ((nc + a.splits - 1) / a.splits + 3) & ~3;
           col_lo = min(nc, I.split * per);
           col_hi = min(nc, col_lo + per);
-        } else if (n_items <= (int)gridDim.x) {
+        } else if (n_items <= (int)gridDim.x && !a.no_spin) {
           // One wave: split S-1 is the tile's designated reducer.  The other
           // splits publish their partials with a fire-and-forget release add
           // and leave at once (their SM goes to the next kernel's prefetch);
@@ -882,7 +885,10 @@ int gemm_coop_min() {
 void gemm_launch(const GemmPlan& p, const GemmArgs& a0, int grid, cudaStream_t st) {
   static const bool pair = getenv("RP_GEMM_PAIR") != nullptr;
   GemmArgs a = a0;
-  a.coop_min = gemm_coop_min();
+  // no_spin (single-GPU local groups): every split-K tile is reduced by its
+  // last CTA (ticket), never by CTAs waiting for each other, because other
+  // contexts' kernels may hold the SMs the waited-for splits need
+  a.coop_min = a0.no_spin ? 0x7FFFFFFF : gemm_coop_min();
   if (pair && a.splits == 1 && a.M % (2 * BM) == 0 && !a.timeline && grid % 2 == 0) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -895,7 +901,7 @@ void gemm_launch(const GemmPlan& p, const GemmArgs& a0, int grid, cudaStream_t s
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = g_no_pdl ? 1 : 2;
     cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<2>, p.tmA, p.tmB16, p.tmB64, p.tmB256, a);
     return;
   }

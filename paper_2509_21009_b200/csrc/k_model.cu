@@ -75,6 +75,8 @@ void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb,
 
 // -------------------------------------------------------------------- RMSNorm
 // h[r] = fp16( x[src] / sqrt(mean(x[src]^2) + eps) * gamma ),  src = gather ? gather[r] : r
+// (gamma == nullptr: unit gain -- the engine folds the gains into the weights
+// of the consuming GEMM at init)
 // One CTA (256 threads) per row.  With `delta` (tensor parallelism):
 // x[r] += delta[r] first (the all-reduced partial of a row-parallel GEMM) and
 // the updated row is written back.
@@ -117,7 +119,7 @@ __global__ void rmsnorm_kernel(float* x, const float* delta, const int* gather, 
     act2_t* hr = (act2_t*)(h + (size_t)r * d);
     const float4* g4 = (const float4*)gamma;
     for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
-      float4 v = xr[c], g = g4[c];
+      const float4 v = xr[c], g = g4 ? g4[c] : make_float4(1.f, 1.f, 1.f, 1.f);
       hr[2 * c] = to_act2(v.x * inv * g.x, v.y * inv * g.y);
       hr[2 * c + 1] = to_act2(v.z * inv * g.z, v.w * inv * g.w);
     }
@@ -202,7 +204,7 @@ __global__ void tp_norm_kernel(float* x, const float* recv, int tp, size_t src_s
     act2_t* hr = (act2_t*)(h + (size_t)r * d);
     const float4* g4 = (const float4*)gamma;
     for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
-      float4 v = xr[c], g = g4[c];
+      const float4 v = xr[c], g = g4 ? g4[c] : make_float4(1.f, 1.f, 1.f, 1.f);
       hr[2 * c] = to_act2(v.x * inv * g.x, v.y * inv * g.y);
       hr[2 * c + 1] = to_act2(v.z * inv * g.z, v.w * inv * g.w);
     }
@@ -219,10 +221,27 @@ __global__ void tp_norm_kernel(float* x, const float* recv, int tp, size_t src_s
 }
 
 void launch_tp_norm(float* x, const float* recv, int tp, size_t src_stride, const unsigned long long* flags,
-                    unsigned long long* gen, int* done, int m_tiles, int splits, const int* n_dev, int n_rows_grid,
-                    const float* gamma, void* h, int d, float eps, cudaStream_t st) {
-  launch_pdl(tp_norm_kernel, dim3(row_grid(n_dev, n_rows_grid)), dim3(256), 0, st, x, recv, tp, src_stride, flags, gen,
-             done, m_tiles, splits, gemm_coop_min(), n_dev, gamma, (act_t*)h, d, eps);
+                    unsigned long long* gen, int* done, int m_tiles, int splits, int coop_min, int max_grid,
+                    const int* n_dev, int n_rows_grid, const float* gamma, void* h, int d, float eps,
+                    cudaStream_t st) {
+  // max_grid bounds the CTAs that spin on the peers' flags (single-GPU local
+  // groups: the peers' GEMMs must find free SMs)
+  const int grid = std::min(row_grid(n_dev, n_rows_grid), max_grid > 0 ? max_grid : 1 << 30);
+  launch_pdl(tp_norm_kernel, dim3(grid), dim3(256), 0, st, x, recv, tp, src_stride, flags, gen, done, m_tiles, splits,
+             coop_min, n_dev, gamma, (act_t*)h, d, eps);
+}
+
+// ------------------------------------------------------ folded norm gains
+__global__ void scale_cols_kernel(__half* w, long long rows, int cols, const float* __restrict__ gamma) {
+  const long long n = rows * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    w[e] = __float2half_rn(__half2float(w[e]) * gamma[e % cols]);
+}
+
+void launch_scale_cols(void* w, long long rows, int cols, const float* gamma, cudaStream_t st) {
+  const long long n = rows * cols;
+  const int grid = (int)std::min<long long>((n + 255) / 256, 148 * 64);
+  scale_cols_kernel<<<grid, 256, 0, st>>>((__half*)w, rows, cols, gamma);
 }
 
 // -------------------------------------------------------- RoPE + KV append

@@ -341,7 +341,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
           I.q_row0 = pos; I.n_qtok = 1; I.pos0 = kv; I.pt_row = s;
           I.kv_lo = sp * chunk; I.kv_hi = min(kv + 1, (sp + 1) * chunk);
           I.nsplit = ns; I.item0 = it0;
-          R.items[it0 + sp] = I;
+          if (it0 + sp < R.max_items) R.items[it0 + sp] = I;   // capacity proven in compute_sizes
         }
       }
       kept += tk; alloc += ta; items += ti;
@@ -355,9 +355,10 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     C->acc_local += s_take;
     C->decoded += n;
     C->free_top = top - alloc;
-    C->n_items = items;
+    C->n_items = min(items, R.max_items);
     C->n_issued = n_is0 + nis / R.G;
     C->issue_n = 0;
+    if (items > R.max_items) s_err = 3;    // unreachable by the bound S + 3 * U1; fail loudly if not
     const bool done = s_acc_new >= R.target || s_next_global == 0 || s_err;
     if (R.trace_buf && t <= R.trace_steps) {
       int* tb = R.trace_buf + (size_t)(t - 1) * (2 + R.S);

@@ -29,7 +29,7 @@ struct CtlBlock {
   int acc;          // accepted prompts (global under DP)
   int acc_local;    // accepted prompts of this rank's slice
   int done;         // round finished (identical on every rank)
-  int err;          // 1 = KV pool exhausted, 2 = page table overflow (any rank)
+  int err;          // 1 = KV pool exhausted, 2 = page table overflow, 3 = attention work list overflow (any rank)
   int n_final;      // live rows at the end (aborted in short rounds)
   int t_end;        // last decoded step
   int underfilled;
@@ -52,6 +52,7 @@ struct RoundDev {
   int attn_units;     // decode-attention split budget per KV head (0: 148 / KV)
   int attn_waves;     // 1: budget whole waves of attention units (k-wave fill), 0: one-wave floor
   int world, rank;
+  int max_items;      // capacity of `items` (ctl flags err 3 rather than overflow it)
   int* slot_prompt; int* slot_j; int* kv_len; int* gen; int* trace_L; int* status; int* own0;
   int* t0;            // [S] step before the sequence's first token: local token index = t - t0 (0 unless issued late)
   int* p_last_tok;    // [P] last prompt token (a late-issued prompt decodes it as its first step)
@@ -77,7 +78,7 @@ struct ModelDims {
   int L, d, H, KV, hd, F, V, eos;
   int v0;                  // first vocab id of this rank's LM-head shard
   float eps;
-  size_t page_bytes;       // one page: [L][KV][2][kPage][hd] bf16
+  size_t page_bytes;       // one page: [L][KV][2][kPage][hd] fp16 (reading Z20)
 };
 
 // weights
@@ -89,8 +90,23 @@ void launch_rmsnorm(float* x, const float* delta, const int* gather, const int* 
                     const float* gamma, void* h, int d, float eps, cudaStream_t st);
 void launch_tp_norm(float* x, const float* recv /* [tp][rows][d] slot base */, int tp, size_t src_stride,
                     const unsigned long long* flags /* [tp] */, unsigned long long* gen, int* done, int m_tiles,
-                    int splits, const int* n_dev, int n_rows_grid, const float* gamma, void* h, int d, float eps,
-                    cudaStream_t st);
+                    int splits, int coop_min, int max_grid, const int* n_dev, int n_rows_grid, const float* gamma,
+                    void* h, int d, float eps, cudaStream_t st);
+// w[m][k] *= gamma[k] for an fp16 [rows, cols] weight (an RMSNorm gain folded
+// into the GEMM that consumes the normalised activations)
+void launch_scale_cols(void* w, long long rows, int cols, const float* gamma, cudaStream_t st);
+
+// Device-memory collectives of a single-GPU local group (several contexts of
+// one process on one device): rank `me` of a group of
+// `size` copies `bytes` of src into its slot of the exchange buffer
+// slots[2][size][slot_bytes] and publishes epoch e = state[0] + 1 in gen[me];
+// the reduce kernel waits until every gen[q] >= e and combines the slots in
+// rank order.  state = {epoch, ticket} per (context, group), zero-initialised.
+enum LocalOp { LOP_GATHER = 0, LOP_SUM_F32 = 1, LOP_MAX_U64 = 2 };
+void launch_local_publish(const void* src, size_t bytes, uint8_t* slots, size_t slot_bytes, int size, int me,
+                          unsigned long long* gen, int* state, cudaStream_t st);
+void launch_local_reduce(int op, void* dst, size_t bytes, const uint8_t* slots, size_t slot_bytes, int size,
+                         const unsigned long long* gen, const int* state, cudaStream_t st);
 void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const int* row_pos, const int* row_pt,
                         const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
                         const double* inv_freq, cudaStream_t st);

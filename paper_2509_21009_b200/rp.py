@@ -34,7 +34,8 @@ class RuntimeDesc(ctypes.Structure):
                 ("max_seqs", ctypes.c_int32), ("max_prompts", ctypes.c_int32), ("max_prompt_len", ctypes.c_int32),
                 ("max_prompt_tokens", ctypes.c_int32), ("max_cap", ctypes.c_int32),
                 ("sample_seed", ctypes.c_uint64), ("temperature", ctypes.c_float), ("graph_steps", ctypes.c_int32),
-                ("nccl_id", ctypes.c_void_p), ("tp", ctypes.c_int32), ("tp_rank", ctypes.c_int32)]
+                ("nccl_id", ctypes.c_void_p), ("tp", ctypes.c_int32), ("tp_rank", ctypes.c_int32),
+                ("tp_nccl_id", ctypes.c_void_p), ("local_group", ctypes.c_void_p)]
 
 
 class Sizes(ctypes.Structure):
@@ -44,7 +45,8 @@ class Sizes(ctypes.Structure):
 
 class Prompt(ctypes.Structure):
     _fields_ = [("prompt_id", ctypes.c_int32), ("len", ctypes.c_int32),
-                ("tokens", ctypes.POINTER(ctypes.c_int32)), ("trace_lens", ctypes.POINTER(ctypes.c_int32))]
+                ("tokens", ctypes.POINTER(ctypes.c_int32)), ("trace_lens", ctypes.POINTER(ctypes.c_int32)),
+                ("trace_lens_retry", ctypes.POINTER(ctypes.c_int32))]
 
 
 class Status(ctypes.Structure):
@@ -63,7 +65,8 @@ EXPORTS = ["rp_query_sizes", "rp_init_model", "rp_submit_round", "rp_step", "rp_
            "rp_free", "rp_last_error", "rp_launch_count", "rp_debug_logits", "rp_debug_trace_enable",
            "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm", "rp_debug_profile", "rp_nccl_unique_id",
            "rp_tp_ipc_handle", "rp_tp_ipc_open", "rp_collect_ready", "rp_round_rows_histogram",
-           "rp_round_issue_cap", "rp_round_unissued"]
+           "rp_round_issue_cap", "rp_round_unissued", "rp_plan_round", "rp_long_queue_pop",
+           "rp_local_group_create", "rp_local_group_free"]
 
 
 def load_library(path=LIB_PATH):
@@ -100,8 +103,13 @@ def load_library(path=LIB_PATH):
     lib.rp_round_unissued.argtypes = [P, ctypes.POINTER(I32), I32, ctypes.POINTER(I32)]
     lib.rp_collect_ready.argtypes = [P, I32, ctypes.POINTER(Response), I32, ctypes.POINTER(I32), I64,
                                      ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I32)]
+    lib.rp_plan_round.argtypes = [P, I32, ctypes.c_float, I32, ctypes.POINTER(I32), ctypes.POINTER(I32)]
+    lib.rp_long_queue_pop.argtypes = [P, I32]
+    lib.rp_local_group_create.argtypes = [I32, I32, ctypes.POINTER(P)]
+    lib.rp_local_group_free.argtypes = [P]
+    lib.rp_local_group_free.restype = None
     for name in EXPORTS:
-        if name not in ("rp_free", "rp_last_error", "rp_launch_count"):
+        if name not in ("rp_free", "rp_last_error", "rp_launch_count", "rp_local_group_free"):
             getattr(lib, name).restype = I32
     return lib
 
@@ -130,6 +138,26 @@ class RPError(RuntimeError):
         self.code = code
 
 
+class LocalGroup:
+    """Single-GPU local group (rp_local_group_create): the world x tp ranks of
+    a job as contexts of this process on the current device, exchanging
+    through device memory.  Create one Engine per rank, each from its own
+    thread (rp_init_model waits for every member); close the engines first."""
+
+    def __init__(self, world, tp=1):
+        self.L = lib()
+        h = ctypes.c_void_p()
+        rc = self.L.rp_local_group_create(world, tp, ctypes.byref(h))
+        if rc != RP_OK:
+            raise RPError(rc, "rp_local_group_create(%d, %d)" % (world, tp))
+        self.h, self.world, self.tp = h, world, tp
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.rp_local_group_free(self.h)
+            self.h = None
+
+
 def _i32p(a):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
 
@@ -148,16 +176,19 @@ class Engine:
 
     def __init__(self, cfg, max_seqs, max_prompts, max_prompt_len, max_prompt_tokens, max_cap, kv_pool_bytes=None,
                  kv_fraction=0.85, weight_seed=0, sample_seed=3, temperature=1.0, graph_steps=16, rank=0, world=1,
-                 nccl_id=None, stream=None, tp=1, tp_rank=0, tp_peer=True):
+                 nccl_id=None, stream=None, tp=1, tp_rank=0, tp_peer=True, tp_nccl_id=None, local_group=None):
         import torch
         self.torch = torch
         self.L = lib()
         self.cfg = dict(cfg)
         self.md = model_desc(cfg, weight_seed)
         self.stream = stream if stream is not None else torch.cuda.Stream()
-        self._nccl_id = None
+        self._nccl_id = self._tp_nccl_id = None
         if nccl_id is not None:
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        if tp_nccl_id is not None:
+            self._tp_nccl_id = ctypes.create_string_buffer(bytes(tp_nccl_id), 128)
+        self.local_group = local_group
         rd = RuntimeDesc()
         rd.rank, rd.world = rank, world
         rd.tp, rd.tp_rank = tp, tp_rank
@@ -167,6 +198,8 @@ class Engine:
         rd.sample_seed, rd.temperature, rd.graph_steps = sample_seed, temperature, graph_steps
         rd.stream = self.stream.cuda_stream
         rd.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None
+        rd.tp_nccl_id = ctypes.cast(self._tp_nccl_id, ctypes.c_void_p) if self._tp_nccl_id is not None else None
+        rd.local_group = local_group.h if local_group is not None else None
         sz = Sizes()
         rd.kv_pool_bytes = 1 << 30
         self._check(self.L.rp_query_sizes(ctypes.byref(self.md), ctypes.byref(rd), ctypes.byref(sz)), None)
@@ -192,8 +225,8 @@ class Engine:
         torch.cuda.synchronize()
         self._check(self.L.rp_init_model(ctypes.byref(self.md), ctypes.byref(rd), ctypes.byref(h)), None)
         self.h = h
-        self.tp_peer = False
-        if tp > 1 and tp_peer:
+        self.tp_peer = local_group is not None and tp > 1       # local groups map the peers at init
+        if tp > 1 and tp_peer and local_group is None:
             self._open_tp_peers()
 
     def _open_tp_peers(self):
@@ -234,12 +267,16 @@ class Engine:
         return int(self.L.rp_launch_count(self.h))
 
     # --------------------------------------------------------------- the ABI
-    def submit(self, prompts, G, cap, target, long_round=False, trace=None, round_id=0, keep=0):
-        """prompts: list of dicts {prompt_id, tokens} (None -> pop the queue);
-        trace: None or int array [n, G] of response lengths (trace mode);
-        keep: responses retained per prompt (R0 < G: response-level
-        speculation; 0 -> G)."""
-        flags = (RP_LONG if long_round else RP_SHORT) | (RP_TRACE if trace is not None else 0)
+    def submit(self, prompts, G, cap, target, long_round=False, trace=None, round_id=0, keep=0, trace_retry=None,
+               trace_mode=None):
+        """prompts: list of dicts {prompt_id, tokens} (None -> pop `target`
+        prompts off the long-prompt queue; pass trace_mode=True for a trace-mode
+        round over queued prompts); trace: None or int array [n, G] of response
+        lengths (trace mode); trace_retry: [n, G] lengths of the re-roll used if
+        a prompt is deferred (reading Z5); keep: responses retained per prompt
+        (R0 < G: response-level speculation; 0 -> G)."""
+        tm = trace is not None if trace_mode is None else trace_mode
+        flags = (RP_LONG if long_round else RP_SHORT) | (RP_TRACE if tm else 0)
         if prompts is None:
             n = target
             rc = self.L.rp_submit_round(self.h, None, n, G, keep, cap, target, flags, round_id)
@@ -258,6 +295,10 @@ class Engine:
                 tl = np.ascontiguousarray(trace[i], dtype=np.int32)
                 self._keep.append(tl)
                 arr[i].trace_lens = _i32p(tl)
+            if trace_retry is not None:
+                tr = np.ascontiguousarray(trace_retry[i], dtype=np.int32)
+                self._keep.append(tr)
+                arr[i].trace_lens_retry = _i32p(tr)
         self._check(self.L.rp_submit_round(self.h, arr, n, G, keep, cap, target, flags, round_id))
 
     def step(self, max_steps=1 << 30):
@@ -318,6 +359,17 @@ class Engine:
         ids = np.zeros(max(1, n.value), dtype=np.int32)
         self._check(self.L.rp_round_unissued(self.h, _i32p(ids), n.value, ctypes.byref(n)))
         return ids[:n.value].tolist()
+
+    def plan(self, P0, eta=1.25, drain=False):
+        """The library's tail-batching planner: ('long', P0) when the queue
+        holds >= P0 prompts, else ('short', ceil(eta * P0))."""
+        k, n = ctypes.c_int32(), ctypes.c_int32()
+        self._check(self.L.rp_plan_round(self.h, int(P0), float(eta), 1 if drain else 0, ctypes.byref(k),
+                                         ctypes.byref(n)))
+        return ("long" if k.value == RP_LONG else "short"), n.value
+
+    def long_queue_pop(self, n):
+        self._check(self.L.rp_long_queue_pop(self.h, int(n)))
 
     def long_queue(self):
         n = ctypes.c_int32()

@@ -8,6 +8,11 @@ MODELS = {
     "tiny": dict(n_layers=2, d_model=256, n_heads=4, n_kv_heads=2, head_dim=64,
                  d_ff=1024, vocab=4096, eos_id=4095, rope_theta=1e6, rms_eps=1e-6,
                  qkv_bias=1),
+    # the 14B attention shape (KV=8, g=5, hd=128) at tiny width: TP=2/4/8
+    # parity in one process (single-GPU local groups)
+    "tiny-kv8": dict(n_layers=2, d_model=512, n_heads=40, n_kv_heads=8, head_dim=128,
+                     d_ff=2048, vocab=4096, eos_id=4095, rope_theta=1e6, rms_eps=1e-6,
+                     qkv_bias=1),
     "qwen2.5-7b": dict(n_layers=28, d_model=3584, n_heads=28, n_kv_heads=4, head_dim=128,
                        d_ff=18944, vocab=152064, eos_id=151643, rope_theta=1e6, rms_eps=1e-6,
                        qkv_bias=1),

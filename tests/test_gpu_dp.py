@@ -43,7 +43,7 @@ def main():
         acc = dp.all_gather_ids(acc_local)
         ref = sched.closed_form(L, cap, target, sched.SHORT, keep=keep)
         lo, hi = dp.partition(n, world)[rank]
-        fifo += [ps[i]["prompt_id"] for i in ref.deferred if lo <= i < hi]   # this rank's deferrals
+        fifo += [ps[i]["prompt_id"] for i in ref.deferred]   # the global queue, identical on every rank
         good = (st.t == ref.t_end and sorted(acc) == sorted(ps[i]["prompt_id"] for i in ref.accepted)
                 and st.accepted == len(ref.accepted)
                 and all(lo <= r["prompt_id"] - ps[0]["prompt_id"] < hi for r in res)
@@ -67,7 +67,7 @@ def main():
         acc = dp.all_gather_ids(list(dict.fromkeys(r["prompt_id"] for r in res)))
         t_end, r_acc, r_def, r_un = sched.issue_dp_protocol(L, cap, tg, sched.SHORT, world, A)
         lo, hi = dp.partition(n, world)[rank]
-        fifo += [ps[i]["prompt_id"] for i in r_def if lo <= i < hi]
+        fifo += [ps[i]["prompt_id"] for i in r_def]
         good = (st.t == t_end and sorted(acc) == sorted(ps[i]["prompt_id"] for i in r_acc)
                 and eng.long_queue() == fifo
                 and eng.unissued() == [ps[i]["prompt_id"] for i in r_un if lo <= i < hi])

@@ -73,13 +73,35 @@ def test_kv_decoder_equals_full_forward():
     assert np.allclose(inc, full, atol=1e-10)
 
 
-def test_cross_check_transformers_qwen2():
+def test_kv_decoder_fork_and_hidden():
+    """fork(): siblings continuing one prompt prefix equal full forwards of
+    their own sequences; head=False returns the final-norm hidden rows."""
+    cfg = model_config("tiny")
+    w = Weights(cfg, 0)
+    prompt = np.array([5, 17, 99, 3, 1000])
+    dec = D.KVDecoder(w)
+    dec.step(prompt, head=False)
+    for cont in ([7, 8, 9], [4000, 1]):
+        h = dec.fork().step(cont, head=False)
+        full = D.hidden(w, np.concatenate([prompt, cont]))
+        assert np.allclose(h, full[len(prompt):], atol=1e-12)
+    assert dec.n == len(prompt)
+
+
+# tiny (g=2, hd=64), the 14B attention shape at tiny width (g=5, hd=128) and
+# ONE full-width Qwen2.5-7B layer (d=3584, g=7, hd=128, d_ff=18944; vocab cut
+# to 4096 to keep the LM head small -- it does not touch the layer arithmetic)
+XCHECK = [("tiny", {}), ("tiny-kv8", {}), ("qwen2.5-7b", dict(n_layers=1, vocab=4096, eos_id=4095))]
+
+
+@pytest.mark.parametrize("name,over", XCHECK, ids=[x[0] for x in XCHECK])
+def test_cross_check_transformers_qwen2(name, over):
     """Library cross-check (the whole decoder): the oracle's logits equal
     transformers' Qwen2ForCausalLM in float64 with the same weights."""
     torch = pytest.importorskip("torch")
     tr = pytest.importorskip("transformers")
-    cfg = model_config("tiny")
-    w = Weights(cfg, 0)
+    cfg = dict(model_config(name), **over)
+    w = Weights(cfg, 0, use_c=cfg["d_model"] > 1024)
     hc = tr.Qwen2Config(vocab_size=cfg["vocab"], hidden_size=cfg["d_model"],
                         intermediate_size=cfg["d_ff"], num_hidden_layers=cfg["n_layers"],
                         num_attention_heads=cfg["n_heads"], num_key_value_heads=cfg["n_kv_heads"],
@@ -87,10 +109,11 @@ def test_cross_check_transformers_qwen2():
                         tie_word_embeddings=False, max_position_embeddings=4096, use_sliding_window=False)
     hc._attn_implementation = "eager"
     m = tr.Qwen2ForCausalLM(hc).to(torch.float64).eval()
-    from oracle.weights import tensor, TID_EMBED
+    from oracle.weights import tensor, tensor_c, TID_EMBED
     T = lambda a: torch.from_numpy(np.asarray(a, np.float64))
+    gen_t = tensor_c if w.use_c else tensor
     with torch.no_grad():
-        m.model.embed_tokens.weight.copy_(T(tensor(0, TID_EMBED, (cfg["vocab"], cfg["d_model"]))))
+        m.model.embed_tokens.weight.copy_(T(gen_t(0, TID_EMBED, (cfg["vocab"], cfg["d_model"]))))
         m.lm_head.weight.copy_(T(w.lm_head()))
         for l, layer in enumerate(m.model.layers):
             lw = w.layer(l)
