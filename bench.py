@@ -29,7 +29,8 @@ sys.path.insert(0, ROOT)
 from synth import configs, gen  # noqa: E402
 
 ETA_NUM, ETA_DEN = 5, 4          # eta = 1.25
-METRIC = "rollout decoded tokens/s (whole job), plus s/RL-step short vs long"
+ETA = ETA_NUM / ETA_DEN
+METRIC = "rollout retained tokens/s (whole job), plus s/RL-step short vs long"
 
 
 def parse():
@@ -40,7 +41,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2-7b", choices=list(configs.ROUNDS))
     ap.add_argument("--graph-steps", type=int, default=16)
-    ap.add_argument("--profile-steps", type=int, default=24)
+    ap.add_argument("--profile-steps", type=int, default=1,
+                    help="> 0: profile the first short and the first long warm-up round whole (per-kernel roofline)")
     ap.add_argument("--max-rounds-steps", type=int, default=0, help="debug: cap decode steps per round (invalid)")
     ap.add_argument("--out", default="")
     ap.add_argument("--stream-collect", type=int, default=0,
@@ -58,8 +60,10 @@ def parse():
 
 # ------------------------------------------------------------------ workload
 class Workload:
-    """Deterministic prompt stream + length trace + the tail-batching planner
-    state (global FIFO of deferred prompt ids)."""
+    """Deterministic prompt stream + length trace (the caller's dataset).  The
+    tail-batching planner and the global long-prompt FIFO live in the library
+    (rp_plan_round, rp_long_queue); `plan`/`commit` here are the plain
+    synchronous baseline and the oracle-side bookkeeping of tools/tests."""
 
     def __init__(self, cfg_name, world, schedule="tail"):
         self.R = configs.ROUNDS[cfg_name]
@@ -74,7 +78,7 @@ class Workload:
         self.trace = gen.length_trace(self.total, self.G, tp["mu0"], tp["sigma_p"], tp["sigma_r"], tp["l_max"],
                                       configs.TRACE_SEED)
         from paper_2509_21009_b200.dp import GlobalQueue
-        self.queue = GlobalQueue()
+        self.queue = GlobalQueue()            # oracle-side mirror (tools, tests); the bench uses the library's
         self.next_fresh = 0
         # "tail": the planner of S:271-279; "sync": plain synchronous rollout (the
         # veRL baseline): every RL step decodes P0 fresh prompts to completion
@@ -92,6 +96,14 @@ class Workload:
             return "long", ids, self.P0, self.R["long_cap"], self.trace[ids, 1, :]
         ids = self.returned + list(range(self.next_fresh, self.next_fresh + self.n_submit - len(self.returned)))
         return "short", ids, self.P0, self.R["short_cap"], self.trace[ids, 0, :]
+
+    def fresh(self, n):
+        """The next n prompts of the stream: prompts a continuous-issuance
+        round never issued come back first (NEXT-4)."""
+        ids = self.returned[:n] + list(range(self.next_fresh, self.next_fresh + n - min(n, len(self.returned))))
+        self.returned = self.returned[n:]
+        self.next_fresh = max([self.next_fresh] + [i + 1 for i in ids])
+        return ids
 
     def commit(self, kind, ids, accepted_ids, unissued=()):
         if self.schedule == "sync":
@@ -198,17 +210,42 @@ def run_ours(a):
     issue_cap = a.issue_cap or -(-W.P0 // world)
     W.issue_cap = issue_cap if W.schedule == "issue" else None
 
-    def one_round(round_no, profile=0):
-        kind, ids, target, cap, L = W.plan()
-        e = eng_long if kind == "long" else eng
-        plist = [W.prompts[i] for i in ids]
-        h2d = sum(len(p["tokens"]) for p in plist) * 4 + L.size * 4
-        if W.schedule == "issue":
-            e.issue_cap(issue_cap if kind == "short" else 0)
-        e.submit(plist, G, cap, target if kind == "short" else len(ids), long_round=(kind == "long"), trace=L,
-                 round_id=round_no)
+    def one_round(round_no, profile=False):
+        """One RL step.  Tail batching: the library's planner (rp_plan_round)
+        picks the round; a SHORT round takes ceil(eta * P0) fresh prompts of
+        the stream, a LONG round pops P0 prompts off the library's global
+        queue (submit with prompts == NULL; every DP rank pops the same)."""
+        tr = W.trace
+        if W.schedule == "sync":
+            ids = W.fresh(W.P0)
+            kind, e = "long", eng
+            plist = [W.prompts[i] for i in ids]
+            e.submit(plist, G, W.R["long_cap"], len(ids), long_round=True, trace=tr[ids, 0, :], round_id=round_no)
+        else:
+            kind, n = eng.plan(W.P0, ETA)
+            if kind == "short":
+                e = eng
+                ids = W.fresh(n)
+                plist = [W.prompts[i] for i in ids]
+                if W.schedule == "issue":
+                    e.issue_cap(issue_cap)
+                e.submit(plist, G, W.R["short_cap"], W.P0, trace=tr[ids, 0, :], trace_retry=tr[ids, 1, :],
+                         round_id=round_no)
+            else:
+                ids = eng.long_queue()[:n]
+                plist = [W.prompts[i] for i in ids]
+                if eng_long is eng:
+                    e = eng
+                    if W.schedule == "issue":
+                        e.issue_cap(0)
+                    e.submit(None, G, W.R["long_cap"], n, long_round=True, trace_mode=True, round_id=round_no)
+                else:                       # TP context over the same GPUs: hand the queue head over
+                    e = eng_long
+                    e.submit(plist, G, W.R["long_cap"], n, long_round=True, trace=tr[ids, 1, :], round_id=round_no)
+                    eng.long_queue_pop(n)
+        h2d = sum(len(p["tokens"]) for p in plist) * 4 + len(plist) * G * 4 * (2 if kind == "short" else 1)
         if profile:
-            e.debug_profile_arm(profile)
+            e.debug_profile_arm(1 << 30)        # every decode step of this round, eagerly, events per launch
         streamed = 0
         if a.stream_collect > 0:
             # NEXT-3: stream the accepted prompts' responses every `stream_collect`
@@ -221,29 +258,40 @@ def run_ours(a):
                 st = e.step(a.stream_collect)
         else:
             st = e.run()
+        prof = None
+        hist = e.rows_histogram()
+        if profile:
+            prof = e.debug_profile_read()
+            e.debug_profile_arm(-1)
+            prof.update(kind=kind, hist=hist.tolist(), kv_tokens=st.kv_tokens_read, tp=e.tp)
         res = e.collect()
-        acc_local = list(dict.fromkeys(r["prompt_id"] for r in res))
-        acc = acc_local if (kind == "long" and e is not eng) else allgather_ids(acc_local)
-        un = allgather_ids(e.unissued()) if (W.schedule == "issue" and kind == "short") else []
-        W.commit(kind, ids, acc, un)
+        if W.schedule == "issue" and kind == "short":
+            W.returned = allgather_ids(e.unissued()) + W.returned
         d2h = (sum(r["len"] for r in res) + streamed) * 4 + len(res) * 24
         retained = sum(r["len"] for r in res)
         decoded = st.decoded_tokens
         # algorithmic HBM bytes of this rank's decode steps (step 1 comes from the prefill)
         hbm = step_bytes(cfg, e.tp, max(0, st.t - 1), st.decoded_tokens, st.kv_tokens_read)
-        t_roof = round_t_roof(cfg, e.tp, e.rows_histogram(), st.decoded_tokens, st.kv_tokens_read)
+        t_roof = round_t_roof(cfg, e.tp, hist, st.decoded_tokens, st.kv_tokens_read)
         if e is not eng and rank != 0:
             # TP ranks decode the same tokens: count them once (on rank 0)
             decoded, retained, h2d, d2h = 0, 0, 0, 0
-        return dict(kind=kind, t_end=st.t, unissued=len(un), streamed=streamed, decoded=decoded, retained=retained, h2d=h2d, d2h=d2h,
-                    accepted=st.accepted, underfilled=st.underfilled, tp=e.tp, hbm_bytes=hbm, t_roof_s=t_roof)
+        info = dict(kind=kind, t_end=st.t, streamed=streamed, decoded=decoded, retained=retained, h2d=h2d,
+                    d2h=d2h, accepted=st.accepted, underfilled=st.underfilled, tp=e.tp, hbm_bytes=hbm,
+                    t_roof_s=t_roof)
+        return info, prof
 
-    # ---- warm-up (the first warm-up round is profiled per kernel class)
-    prof = None
+    # ---- warm-up.  The first SHORT and the first LONG warm-up round are
+    # profiled whole (every decode step eager, CUDA events around every launch
+    # on the engine stream): the per-kernel-class roofline covers the same
+    # mix of live-batch sizes and contexts as the timed region.
+    profs = []
     for r in range(a.warmup):
-        one_round(r, profile=a.profile_steps if r == 0 else 0)
-        if r == 0 and a.profile_steps:
-            prof = eng.debug_profile_read()
+        kind_next = "long" if (W.schedule == "sync" or eng.plan(W.P0, ETA)[0] == "long") else "short"
+        want = a.profile_steps > 0 and kind_next not in {p["kind"] for p in profs}
+        _, prof = one_round(r, profile=want)
+        if prof is not None:
+            profs.append(prof)
     # ---- timed region
     clk = Clocks(local) if rank == 0 else None
     if world > 1:
@@ -259,7 +307,7 @@ def run_ours(a):
         rs, re_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tr0 = time.perf_counter()
         rs.record(st_ev)
-        info = one_round(a.warmup + r)
+        info, _ = one_round(a.warmup + r)
         re_.record(st_ev)
         re_.synchronize()
         info["wall_s"] = time.perf_counter() - tr0
@@ -304,7 +352,7 @@ def run_ours(a):
         return
     short = [s for s, x in zip(per_round, rounds) if x["kind"] == "short"]
     long_ = [s for s, x in zip(per_round, rounds) if x["kind"] == "long"]
-    value = decoded / dev_s
+    value = retained / dev_s
     line = {
         "metric": METRIC,
         "value": round(value, 1),
@@ -323,13 +371,14 @@ def run_ours(a):
                  "dp%d (planner: profile predicts DP replicas fastest among the fitting TP sizes)" % world)),
             a.graph_steps),
         "per_gpu_tokens_per_s": round(value / world, 1),
-        "retained_tokens_per_s": round(retained / dev_s, 1),
+        "decoded_tokens_per_s": round(decoded / dev_s, 1),
+        "decoded_per_gpu_tokens_per_s": round(decoded / dev_s / world, 1),
         "speculation_waste": round(decoded / max(1.0, retained), 3),
         "s_per_rl_step": {"short_mean": round(statistics.mean(short), 3) if short else None,
                           "long_mean": round(statistics.mean(long_), 3) if long_ else None,
                           "all_mean": round(dev_s / a.steps, 3)},
         "rounds": [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in x.items()} for x in rounds],
-        "e2e": {"value": round(decoded / wall_s, 1), "unit": "tokens/s",
+        "e2e": {"value": round(retained / wall_s, 1), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(h2d / a.steps), "d2h_bytes_per_step": int(d2h / a.steps)},
         "gpu_launches": int(launches_all),
         "clocks": clocks,
@@ -337,8 +386,8 @@ def run_ours(a):
     if a.stream_collect:
         line["config"]["stream_collect_steps"] = a.stream_collect
         line["streamed_fraction"] = round(sum(x["streamed"] for x in rounds) / max(1, sum(x["retained"] for x in rounds)), 4)
-    if prof is not None:
-        line["roofline"], line["kernel_profile"] = roofline(prof, cfg)
+    if profs:
+        line["roofline"], line["kernel_profile"] = roofline(profs, cfg)
     peak_hbm = load_peaks()[0]
     line["round_roofline"] = {
         "t_roof_s": round(t_roof_all.item(), 3), "t_measured_s": round(dev_s, 3),
@@ -353,7 +402,7 @@ def run_ours(a):
         "scope": "whole timed rounds: every decode step streams all weights once, plus the KV context each "
                  "live row's attention reads and the logits write + sampler read (DESIGN.md section 7)"}
     if world == 1:
-        line["cpu_baseline"] = cpu_baseline(W, quick=True)
+        line["cpu_baseline"] = cpu_baseline(W)
     emit(json.dumps(line))
     if a.out:
         with open(a.out, "w") as f:
@@ -474,126 +523,199 @@ def load_peaks():
 
 
 def ncu_traffic(kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
-    the newest committed ncu --set full summary (profiles/rNN_ncu_traffic.json,
-    written by tools/make_profiles.py from a capture of the same decode step)."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    (and the capture's live batch) from the newest committed ncu --set full
+    summary, profiles/rNN_ncu_traffic.json, written by tools/make_profiles.py
+    from a capture of this bench command's decode steps."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json")))
     if not files:
         return None, None
     d = json.load(open(files[-1]))
+    best = None
     for tag, ent in d.items():
-        if "256" in tag and kernel in ent["dram_bytes_per_launch"]:
-            return int(ent["dram_bytes_per_launch"][kernel]), "%s [%s] %s" % (
-                os.path.relpath(files[-1], ROOT), tag, ent["shape"])
-    return None, None
+        if kernel in ent.get("dram_bytes_per_launch", {}):
+            b = int(ent["dram_bytes_per_launch"][kernel])
+            if best is None or ent.get("rows", 0) < best[2]:      # the smallest captured batch: the common case
+                best = (b, "%s [%s] %s" % (os.path.relpath(files[-1], ROOT), tag, ent.get("shape", "")),
+                        ent.get("rows", 0))
+    return (best[0], best[1]) if best else (None, None)
 
 
-def roofline(prof, cfg):
-    """Dominant kernel class of the profiled decode steps and its roofline.
-    Algorithmic bytes per launch:
-      GEMM (weight stream) = M*K*2 + N*K*2 + N*M*out_bytes (+ N*M*4 read for residual epilogues)
-      attention = sum over rows of ctx * KV * hd * 2 (K,V) * 2 B + q/out rows."""
-    hbm, tf_burst, tf_sus, src = load_peaks()
-    d, H, KV, hd, F, V, L = (cfg[k] for k in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ff", "vocab",
-                                              "n_layers"))
-    steps = max(1, prof["steps"])
-    B = prof["rows"] / steps                          # mean live rows per profiled step
-    ctx = prof["ctx"] / steps                         # mean sum of contexts per step
-    ms, cnt = prof["ms"], prof["launches"]
+def launch_work(cfg, tp, cls, B):
+    """Algorithmic (bytes, FLOPs) of ONE launch of kernel class `cls` at B live
+    rows: a GEMM streams its weights once and reads /
+    writes its activations (M*K*2 + B*K*2 + B*M*out, + B*M*4 for residual
+    read-modify-write), FLOPs 2*B*M*K; the sampler reads the fp32 logits;
+    RMSNorm / embedding read and write one row each.  Attention is counted
+    from the context separately (attn_work)."""
+    d, H, KV, hd, F, V = (cfg[k] for k in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ff", "vocab"))
+    H, KV, F, V = H // tp, KV // tp, F // tp, V // tp
     qkvw = (H + 2 * KV) * hd
-    gemm_bytes = {
-        "gemm_qkv": qkvw * d * 2 + B * d * 2 + B * qkvw * 4,
-        "gemm_o": d * H * hd * 2 + B * H * hd * 2 + 2 * B * d * 4,
-        "gemm_gu": 2 * F * d * 2 + B * d * 2 + B * F * 2,
-        "gemm_down": d * F * 2 + B * F * 2 + 2 * B * d * 4,
-        "gemm_lm": V * d * 2 + B * d * 2 + B * V * 4,
-    }
-    gemm_flops = {"gemm_qkv": 2 * B * qkvw * d, "gemm_o": 2 * B * d * H * hd, "gemm_gu": 2 * B * 2 * F * d,
-                  "gemm_down": 2 * B * d * F, "gemm_lm": 2 * B * V * d}
-    attn_bytes = ctx * KV * hd * 2 * 2 + B * H * hd * 2 * 2
-    total = sum(ms.values())
-    dom = max(ms, key=lambda k: ms[k])
-    per_launch_ms = ms[dom] / max(1, cnt[dom])
-    detail = {k: {"ms_per_step": round(ms[k] / steps, 4), "share": round(ms[k] / total, 4),
-                  "launches_per_step": round(cnt[k] / steps, 2)} for k in ms if cnt[k]}
-    for k in gemm_bytes:
-        if cnt.get(k):
-            t = ms[k] / cnt[k] / 1e3
-            detail[k]["hbm_gbs"] = round(gemm_bytes[k] / t / 1e9, 1)
-            detail[k]["tflops"] = round(gemm_flops[k] / t / 1e12, 1)
-    if cnt.get("attention"):
-        t = ms["attention"] / cnt["attention"] / 1e3
-        # bytes of every row's full context: the prompt pages the G siblings share are re-read
-        # (mostly from L2), so this is an effective rate; the DRAM traffic is in profiles/ (ncu)
-        detail["attention"]["context_gbs"] = round(attn_bytes / t / 1e9, 1)
-    if dom == "attention":
-        ach = attn_bytes / (per_launch_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4)}
-    elif dom in gemm_bytes:
-        t = per_launch_ms / 1e3
-        fl = gemm_flops[dom] / t / 1e12
-        by = gemm_bytes[dom] / t / 1e9
-        if gemm_flops[dom] / gemm_bytes[dom] * 1e-3 > tf_sus / hbm:   # above the ridge: tensor bound
-            roof = {"bound": "tensor", "achieved": round(fl, 1), "peak": tf_sus, "unit": "TFLOP/s",
-                    "frac": round(fl / tf_sus, 4)}
-        else:
-            roof = {"bound": "hbm", "achieved": round(by, 1), "peak": hbm, "unit": "GB/s", "frac": round(by / hbm, 4)}
+    g = {"gemm_qkv": (qkvw, d, 2, 0),          # fused RoPE epilogue: q -> fp16, k/v -> their KV page (fp16)
+         "gemm_o": (d, H * hd, 4, 4), "gemm_gu": (2 * F, d, 1, 0), "gemm_down": (d, F, 4, 4),
+         "gemm_lm": (V, d, 4, 0)}
+    if cls in g:
+        M, K, ob, rd = g[cls]
+        return M * K * 2 + B * K * 2 + B * M * ob + B * M * rd, 2.0 * B * M * K
+    if cls == "sampler":
+        return B * V * 4, 0.0
+    if cls in ("rmsnorm", "embed"):
+        return B * d * 6, 0.0
+    return 0, 0.0
+
+
+LAUNCHES_PER_STEP = {"gemm_qkv": "L", "gemm_o": "L", "gemm_gu": "L", "gemm_down": "L", "attention": "L",
+                     "gemm_lm": 1, "sampler": 1, "embed": 1, "ctl": 1}
+
+
+def roofline(profs, cfg):
+    """Per-kernel-class roofline over whole profiled rounds (the first short
+    and the first long round of the run, every decode step): algorithmic
+    bytes and FLOPs summed over every launch at its live batch (device
+    histogram of rows per step) and the attention context actually read
+    (kv_tokens_read), divided by the class's summed CUDA-event time.  The
+    `roofline` object is the dominant class (largest share of the profiled
+    time): bound = hbm if its launches' byte time exceeds their FLOP time at
+    the peaks, achieved = algorithmic bytes (FLOPs) / time."""
+    hbm, tf_burst, tf_sus, src = load_peaks()
+    L = cfg["n_layers"]
+    tot_ms, tot_cnt, by, fl, t_roof, steps, rows_sum, ctx_sum = {}, {}, {}, {}, {}, 0, 0, 0
+    for p in profs:
+        tp = p.get("tp", 1)
+        hd, KV, H = cfg["head_dim"], cfg["n_kv_heads"] // tp, cfg["n_heads"] // tp
+        hist = p["hist"]
+        steps += sum(hist)
+        rows_sum += sum(B * n for B, n in enumerate(hist))
+        ctx_sum += p["kv_tokens"]
+        for k, v in p["ms"].items():
+            tot_ms[k] = tot_ms.get(k, 0.0) + v
+            tot_cnt[k] = tot_cnt.get(k, 0) + p["launches"][k]
+        for cls in ("gemm_qkv", "gemm_o", "gemm_gu", "gemm_down", "gemm_lm", "sampler", "embed"):
+            nl = L if LAUNCHES_PER_STEP[cls] == "L" else 1
+            for B, n in enumerate(hist):
+                if n:
+                    b, f = launch_work(cfg, tp, cls, B)
+                    by[cls] = by.get(cls, 0) + n * nl * b
+                    fl[cls] = fl.get(cls, 0) + n * nl * f
+                    t_roof[cls] = t_roof.get(cls, 0) + n * nl * max(b / (hbm * 1e9), f / (tf_sus * 1e12))
+        ab = p["kv_tokens"] * L * KV * hd * 2 * 2 + sum(B * n for B, n in enumerate(hist)) * L * H * hd * 2 * 2
+        by["attention"] = by.get("attention", 0) + ab
+        fl["attention"] = fl.get("attention", 0) + 4.0 * p["kv_tokens"] * L * H * hd
+        t_roof["attention"] = t_roof.get("attention", 0) + ab / (hbm * 1e9)
+    total = sum(tot_ms.values())
+    detail = {}
+    for k, v in sorted(tot_ms.items(), key=lambda kv: -kv[1]):
+        if not tot_cnt.get(k):
+            continue
+        dd = {"ms_per_step": round(v / max(1, steps), 4), "share": round(v / total, 4),
+              "launches_per_step": round(tot_cnt[k] / max(1, steps), 2)}
+        if k in by:
+            t = v / 1e3
+            dd["hbm_gbs"] = round(by[k] / t / 1e9, 1)
+            if fl.get(k):
+                dd["tflops"] = round(fl[k] / t / 1e12, 1)
+            dd["roofline_frac"] = round(t_roof[k] / t, 4)
+        detail[k] = dd
+    dom = max(tot_ms, key=lambda k: tot_ms[k])
+    t = tot_ms[dom] / 1e3
+    tensor = fl.get(dom, 0) / (tf_sus * 1e12) > by.get(dom, 0) / (hbm * 1e9)
+    if tensor:
+        ach = fl[dom] / t / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 1), "peak": tf_sus, "unit": "TFLOP/s",
+                "frac": round(ach / tf_sus, 4)}
     else:
-        roof = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None}
+        ach = by.get(dom, 0) / t / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4)}
     traffic, traffic_src = ncu_traffic(dom)
     roof.update({"kernel": dom, "traffic": traffic, "traffic_source": traffic_src,
-                 "peak_source": src + (" (cuBLAS bf16 dense; fp16 runs at the same tensor rate)"
-                                       if roof.get("unit") == "TFLOP/s" else ""),
-                 "share_of_step": round(ms[dom] / total, 4),
-                 "mean_live_rows": round(B, 1), "mean_ctx_per_row": round(ctx / max(B, 1), 1),
-                 "measured": "CUDA events around each launch of %d eager decode steps (first warm-up round)" % steps})
+                 "peak_source": src + (" sustained cuBLAS bf16 dense (fp16 runs at the same tensor rate)"
+                                       if tensor else " HBM copy bandwidth"),
+                 "share_of_profiled_time": round(tot_ms[dom] / total, 4),
+                 "roofline_time_frac": round(t_roof.get(dom, 0) / t, 4),
+                 "launches": tot_cnt[dom], "mean_live_rows": round(rows_sum / max(1, steps), 1),
+                 "mean_ctx_per_row": round(ctx_sum / max(1, rows_sum), 1),
+                 "measured": "CUDA events around every launch of every decode step of whole rounds (%s; %d "
+                             "steps), step enqueued behind a host gate so no host gap is timed" % (
+                                 " + ".join("%s round of %d steps" % (p["kind"], sum(p["hist"])) for p in profs),
+                                 steps)})
     return roof, detail
 
 
 # ------------------------------------------------------------------ oracle (CPU)
-def oracle_sample(W, n_tok=4, prompt_len=32):
-    """The oracle as it stands, on a bounded sample of the same workload: a
-    Qwen2.5-7B-shaped decoder truncated to ONE layer at full width + the full
-    LM head; prefill one prompt, then decode n_tok tokens one at a time.
-    Returns seconds per decoded token extrapolated to the full depth
-    (t_layer * n_layers + t_lm), and the scheduler oracle's us/round."""
-    from oracle import decoder, weights, sched
-    cfg1 = dict(W.model, n_layers=1)
-    w = weights.Weights(cfg1, configs.WEIGHT_SEED, use_c=True)
-    w.layer(0); w.lm_head()
-    dec = decoder.KVDecoder(w)
-    toks = W.prompts[0]["tokens"][:prompt_len]
-    dec.step(toks)
-    t_tot = 0.0
-    tok = int(toks[-1])
-    for _ in range(n_tok):
-        t0 = time.perf_counter()
-        dec.step([tok])
-        t_tot += time.perf_counter() - t0
-    # split the per-step time into layer and LM-head parts
-    h = np.zeros((1, cfg1["d_model"]))
-    t0 = time.perf_counter()
-    for _ in range(n_tok):
-        h @ np.asarray(w.lm_head(), np.float64).T
-    t_lm = (time.perf_counter() - t0) / n_tok
-    t_layer = max(t_tot / n_tok - t_lm, 1e-9)
-    per_tok = t_layer * W.model["n_layers"] + t_lm
-    # scheduler oracle on this round's trace
-    kind, ids, target, cap, L = W.plan()
-    t0 = time.perf_counter()
-    sched.closed_form(L, cap, target, sched.SHORT if kind == "short" else sched.LONG)
-    us_round = (time.perf_counter() - t0) * 1e6
-    return per_tok, us_round, t_layer, t_lm
+class OracleSample:
+    """The oracle as it stands, on the bounded sample of BASELINE.md section 4:
+    B = 8 sequences (one prompt's G = 8 responses) at context ~512, decoded
+    one token at a time with the fp64 KVDecoder, on the Qwen2.5-7B shape cut
+    to ONE full-width layer + the full 152 064-row LM head.  Setup (weight
+    formula, widening to fp64, the shared 512-token prefill) is not timed; a
+    timed step feeds one token to each of the 8 sequences.  Per-token time is
+    extrapolated to the full depth as t_layer * n_layers + t_lm."""
+
+    def __init__(self, W, B=8, ctx=512):
+        from oracle import decoder, weights
+        self.decoder = decoder
+        cfg1 = dict(W.model, n_layers=1)
+        self.L = W.model["n_layers"]
+        w = weights.Weights(cfg1, configs.WEIGHT_SEED, use_c=True)
+        w.layer(0)
+        for k in list(w._c):
+            w._c[k] = np.asarray(w._c[k], np.float64)
+        self.lm = np.asarray(w.lm_head(), np.float64)
+        self.w = w
+        prompt = np.resize(W.prompts[0]["tokens"], ctx)            # ~512 prompt tokens
+        root = decoder.KVDecoder(w)
+        root.step(prompt, head=False)
+        self.decs = [root.fork() for _ in range(B)]
+        self.tok = [int(prompt[-1 - b]) for b in range(B)]
+        self.B, self.ctx = B, ctx
+        self.t_layer = self.t_lm = 0.0
+        self.n = 0
+
+    def step(self):
+        """One decode step of the B sequences; returns seconds per token
+        extrapolated to the full depth."""
+        tl = tm = 0.0
+        for b, d in enumerate(self.decs):
+            t0 = time.perf_counter()
+            h = d.step([self.tok[b]], head=False)
+            t1 = time.perf_counter()
+            z = h @ self.lm.T
+            t2 = time.perf_counter()
+            self.tok[b] = int(np.argmax(z[0]))
+            tl += t1 - t0
+            tm += t2 - t1
+        self.t_layer += tl
+        self.t_lm += tm
+        self.n += self.B
+        return (tl * self.L + tm) / self.B
+
+    def per_token(self):
+        return (self.t_layer * self.L + self.t_lm) / max(1, self.n)
 
 
-def cpu_baseline(W, quick=True):
-    per_tok, us_round, t_layer, t_lm = oracle_sample(W, n_tok=3 if quick else 6)
-    cores = os.cpu_count()
-    return {"value": round(1.0 / per_tok, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
-            "sample": "fp64 NumPy oracle, Qwen2.5-7B-shaped: 1 layer at full width + LM head, 1 sequence, "
-                      "3 decode steps after a 32-token prefill; per-token time extrapolated to 28 layers "
-                      "(t_layer=%.3fs, t_lm=%.3fs); scheduler oracle %.0f us/round" % (t_layer, t_lm, us_round)}
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return {i.get("internal_api", "?"): i.get("num_threads") for i in threadpool_info()}
+    except Exception:
+        return {}
+
+
+def sample_text(o):
+    return ("fp64 NumPy oracle (KVDecoder), Qwen2.5-7B shape cut to 1 full-width layer + the full LM head, "
+            "B=%d sequences (one prompt's G=8 responses forked from a shared %d-token prefill), %d decode "
+            "tokens timed; per-token time extrapolated to %d layers (t_layer=%.3fs, t_lm=%.3fs per token); "
+            "BLAS threads %s" % (o.B, o.ctx, o.n, o.L, o.t_layer / max(1, o.n), o.t_lm / max(1, o.n),
+                                 blas_threads()))
+
+
+def cpu_baseline(W, steps=8):
+    o = OracleSample(W)
+    for _ in range(steps):
+        o.step()
+    return {"value": round(1.0 / o.per_token(), 4), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": sample_text(o)}
 
 
 def run_reference(a):
@@ -602,23 +724,23 @@ def run_reference(a):
     if rank != 0:
         return
     W = Workload(a.config, 1)
+    o = OracleSample(W)
     for _ in range(a.warmup):
-        oracle_sample(W, n_tok=1)
+        o.step()
+    o.t_layer = o.t_lm = 0.0
+    o.n = 0
     t0 = time.perf_counter()
-    per = []
     for _ in range(a.steps):
-        per_tok, _, _, _ = oracle_sample(W, n_tok=2)
-        per.append(per_tok)
+        o.step()
     wall = time.perf_counter() - t0
-    value = 1.0 / statistics.mean(per)
+    value = 1.0 / o.per_token()
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 * wall / a.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (random-init Qwen2.5-7B-shaped weights, seeded prompts)",
             "config": bench_config(W, "fp64 NumPy oracle on the host cores, rank 0 only (bounded sample)", 0),
             "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "oracle",
-                             "sample": "per step: 1-layer full-width Qwen2.5-7B-shaped fp64 oracle + LM head, "
-                                       "2 decode steps, extrapolated to 28 layers"},
+                             "sample": "per step: one decode token for each of the 8 sequences; " + sample_text(o)},
             "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(json.dumps(line))
 

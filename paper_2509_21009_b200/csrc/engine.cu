@@ -177,6 +177,7 @@ struct RpCtx {
   RpLocalGroup* lg = nullptr;
   int coop_min = 16;          // cooperative split-K from this chunk width (no_spin: never)
   int* memb = nullptr;        // [P + 1] local membership, then [world][P + 1] gathered (rp_collect)
+  int* memb_h = nullptr;      // pinned host staging of memb
 
   // round state (host)
   bool active = false, collected = true;
@@ -195,8 +196,10 @@ struct RpCtx {
   // per-kernel-class profiling of eager decode steps (rp_debug_profile)
   int prof_steps_left = 0;
   bool capturing = false;
-  std::vector<cudaEvent_t> ev;
+  std::vector<cudaEvent_t> ev, ev_pool;   // events of the current profiled step (from the pool)
   std::vector<int> ev_cls;
+  volatile int* gate_h = nullptr;         // host-mapped flag that holds a profiled step until it is enqueued
+  int* gate_d = nullptr;
   double prof_ms[RP_PROF_N] = {0};
   long long prof_cnt[RP_PROF_N] = {0};
   long long prof_rows = 0, prof_ctx = 0, prof_step_count = 0;
@@ -217,6 +220,12 @@ static std::string g_init_err;
 // Programmatic dependent launch is off while a local-group context issues
 // work from this thread (common.cuh g_no_pdl).
 static inline void pdl_mode(const RpCtx* c) { g_no_pdl = c->lg != nullptr; }
+
+// Local groups: a pageable-memory copy is staged by the driver in order
+// across the whole CUDA context, so one queued behind this stream's spinning
+// collective would also hold up the other members' copies -- a deadlock.
+// Pageable copies are therefore only issued on an idle stream.
+static inline cudaError_t idle(RpCtx* c) { return c->lg ? cudaStreamSynchronize(c->st) : cudaSuccess; }
 
 #define CK(call)                                                                              \
   do {                                                                                        \
@@ -434,19 +443,23 @@ static int validate(const rp_model_desc* md, const rp_runtime_desc* rd, std::str
 // ------------------------------------------------------------------ model forward
 // Profiling brackets: when an eager decode step is profiled, every launch is
 // bracketed by CUDA events on the launching stream.
+static cudaEvent_t prof_event(RpCtx* c) {
+  if (c->ev.size() == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  cudaEvent_t e = c->ev_pool[c->ev.size()];
+  c->ev.push_back(e);
+  return e;
+}
 struct ProfScope {
   RpCtx* c; int cls; bool on;
   ProfScope(RpCtx* c_, int cls_) : c(c_), cls(cls_), on(c_->prof_steps_left > 0 && !c_->capturing) {
-    if (on) {
-      cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, c->st);
-      c->ev.push_back(e); c->ev_cls.push_back(-1);
-    }
+    if (on) { cudaEventRecord(prof_event(c), c->st); c->ev_cls.push_back(-1); }
   }
   ~ProfScope() {
-    if (on) {
-      cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, c->st);
-      c->ev.push_back(e); c->ev_cls.push_back(cls);
-    }
+    if (on) { cudaEventRecord(prof_event(c), c->st); c->ev_cls.push_back(cls); }
   }
 };
 // Folded RMSNorm (DESIGN.md §5 K6): FOLD_PRODUCE on a RESID GEMM also writes
@@ -842,6 +855,7 @@ static int init_impl(RpCtx* c) {
     CK(cudaStreamSynchronize(c->st));
   }
   CK(cudaMallocHost(&c->h_ctl, sizeof(CtlBlock)));
+  if (rd->world > 1) CK(cudaMallocHost(&c->memb_h, (size_t)(c->z.P + 1) * (rd->world + 1) * 4));
   memset(c->h_ctl, 0, sizeof(CtlBlock));
   c->h_ctl->done = 1;
   CK(cudaMemcpyAsync(c->R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
@@ -961,6 +975,9 @@ void rp_free(void* ctx) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return;
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->gate_h) cudaFreeHost((void*)c->gate_h);
+  if (c->memb_h) cudaFreeHost(c->memb_h);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->trace_dev) cudaFree(c->trace_dev);
   if (c->dp.nccl) ncclCommDestroy(c->dp.nccl);
@@ -1032,6 +1049,7 @@ static int prefill(RpCtx* c, const std::vector<int>& toks, const std::vector<int
   }
   std::vector<AttnItem> items;
   if (build_prefill_items(c, plen, poff, items)) return c->fail(RP_ENOSPC, "prefill attention items exceed capacity");
+  CK(idle(c));
   CK(cudaMemcpyAsync(c->R.page_table + (size_t)S * maxp, ptab.data(), ptab.size() * 4, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->pre_tok, toks.data(), T * 4, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->pre_pos, pos.data(), T * 4, cudaMemcpyHostToDevice, c->st));
@@ -1174,6 +1192,7 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   auto up = [&](int* dst, const std::vector<int>& v, size_t count) {
     return cudaMemcpyAsync(dst, v.data(), count * 4, cudaMemcpyHostToDevice, c->st);
   };
+  CK(idle(c));   // the prefill may end in (TP) collectives
   if (nS > 0) {
     CK(up(R.slot_prompt, slot_prompt, nS)); CK(up(R.slot_j, slot_j, nS)); CK(up(R.kv_len, kv_len, nS));
     CK(up(R.gen, zeros, nS)); CK(up(R.status, zeros, nS)); CK(up(R.trace_L, trL, nS)); CK(up(R.own0, own0, nS));
@@ -1250,7 +1269,20 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
     if (c->prof_steps_left > 0) {
       const int rows = c->h_ctl->n_live;
       const long long ctx = c->h_ctl->ctx_sum;
+      // the step is enqueued behind a gate kernel and released once every
+      // launch is queued, so the kernels run back to back and no event
+      // bracket contains host launch latency
+      if (!c->gate_h) {
+        int* hp = nullptr;
+        CK(cudaHostAlloc(&hp, sizeof(int), cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(&c->gate_d, hp, 0));
+        c->gate_h = hp;
+      }
+      *c->gate_h = 0;
+      launch_host_gate(c->gate_d, c->st);
       decode_step(c, bucket);
+      __sync_synchronize();
+      *c->gate_h = 1;
       CK(cudaGetLastError());
       CK(cudaStreamSynchronize(c->st));
       for (size_t i = 0; i + 1 < c->ev.size(); i += 2) {
@@ -1259,7 +1291,6 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
         c->prof_ms[c->ev_cls[i + 1]] += ms;
         c->prof_cnt[c->ev_cls[i + 1]] += 1;
       }
-      for (auto e : c->ev) cudaEventDestroy(e);
       c->ev.clear(); c->ev_cls.clear();
       c->prof_rows += rows; c->prof_ctx += ctx; c->prof_step_count += 1;
       c->prof_steps_left -= 1;
@@ -1358,10 +1389,13 @@ int rp_collect(void* ctx, rp_response* out, int32_t max_out, int32_t* tok_buf, i
     for (int p = 0; p < c->n_loc; ++p) memb[p] = accepted[p];
     memb[P1 - 1] = std::min(c->h_ctl->n_issued, c->n_loc);
     if (W > 1) {
-      CK(cudaMemcpyAsync(c->memb, memb.data(), (size_t)P1 * 4, cudaMemcpyHostToDevice, c->st));
+      // pinned staging: the copy back is queued behind the collective
+      memcpy(c->memb_h, memb.data(), (size_t)P1 * 4);
+      CK(cudaMemcpyAsync(c->memb, c->memb_h, (size_t)P1 * 4, cudaMemcpyHostToDevice, c->st));
       coll_allgather_i32(c, c->dp, c->memb, c->memb + P1, (size_t)P1);
-      CK(cudaMemcpyAsync(memb.data(), c->memb + P1, (size_t)P1 * W * 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(c->memb_h + P1, c->memb + P1, (size_t)P1 * W * 4, cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
+      memcpy(memb.data(), c->memb_h + P1, (size_t)P1 * W * 4);
     }
     const int n = c->n_glob, base = n / W, extra = n % W;
     for (int q = 0; q < W; ++q) {
@@ -1530,6 +1564,7 @@ int rp_debug_logits(void* ctx, const int32_t* tokens, int32_t n, float* logits_o
   std::vector<std::vector<int>> pp;
   int rc = prefill(c, toks, plen, top, pp, rows);
   if (rc) return rc;
+  CK(idle(c));
   CK(cudaMemcpyAsync(logits_out, c->logits, (size_t)n * c->m.V * 4, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   return RP_OK;

@@ -103,4 +103,17 @@ void launch_local_reduce(int op, void* dst, size_t bytes, const uint8_t* slots, 
   local_reduce_kernel<<<grid, 256, 0, st>>>(op, dst, bytes, slots, slot_bytes, size, gen, state);
 }
 
+__global__ void host_gate_kernel(const volatile int* flag) {
+  uint32_t spins = 0;
+  while (*flag == 0) {
+    __nanosleep(1000);
+    if (++spins == (1u << 24)) {
+      printf("rollpacker watchdog: profiling gate never released\n");
+      __trap();
+    }
+  }
+}
+
+void launch_host_gate(const int* flag, cudaStream_t st) { host_gate_kernel<<<1, 1, 0, st>>>(flag); }
+
 }  // namespace rp

@@ -120,6 +120,8 @@ void launch_kv_fork(const int* jobs /*[n][3] src,dst,rows*/, int n, void* kv_poo
 void launch_sampler(const float* logits, int V, int v0, int row_div, const RoundDev& R, uint64_t seed,
                     float inv_temp, uint32_t round_id, cudaStream_t st);
 void launch_ctl(const RoundDev& R, int appended, int mode /*0 all, 1 phase A, 2 phase B*/, cudaStream_t st);
+// spin until the host-mapped *flag != 0 (profiling: release a fully enqueued step)
+void launch_host_gate(const int* flag, cudaStream_t st);
 // responses of the accepted prompts with acceptance index >= first (local)
 void launch_collect_pack(const RoundDev& R, int first, int* meta /*[acc*keep][4]*/, int* tokens, cudaStream_t st);
 int attn_smem_bytes(int hd);

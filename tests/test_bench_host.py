@@ -77,3 +77,26 @@ def test_grid_interpolation():
     assert bench.grid_step_ms(grid, 1, 8, 8192) == 4.0                    # single point of that context
     assert bench.grid_step_ms(grid, 2, 8, 100) == 5.0
     assert bench.grid_step_ms(grid, 4, 8, 100) is None
+
+
+def test_whole_round_roofline_accounting():
+    """bench.roofline over a synthetic whole-round profile: algorithmic bytes
+    summed over every launch at its live batch; the dominant class is the
+    largest measured time; below the ridge the bound is HBM."""
+    from synth import configs
+    cfg = configs.model_config("qwen2.5-7b")
+    L = cfg["n_layers"]
+    hist = [0] * 257
+    hist[16], hist[256] = 90, 10                     # 100 decode steps
+    gu16, _ = bench.launch_work(cfg, 1, "gemm_gu", 16)
+    gu256, f256 = bench.launch_work(cfg, 1, "gemm_gu", 256)
+    assert gu16 == 2 * cfg["d_ff"] * cfg["d_model"] * 2 + 16 * cfg["d_model"] * 2 + 16 * cfg["d_ff"] * 2
+    assert f256 == 2.0 * 256 * 2 * cfg["d_ff"] * cfg["d_model"]
+    ms = {"gemm_gu": 100.0, "gemm_down": 50.0, "attention": 40.0}
+    prof = dict(kind="short", hist=hist, kv_tokens=1000 * 100, tp=1, ms=ms,
+                launches={"gemm_gu": 100 * L, "gemm_down": 100 * L, "attention": 100 * L}, rows=0, ctx=0, steps=100)
+    roof, detail = bench.roofline([prof], cfg)
+    assert roof["kernel"] == "gemm_gu" and roof["bound"] == "hbm" and roof["unit"] == "GB/s"
+    want = (90 * gu16 + 10 * gu256) * L / 0.1 / 1e9
+    assert abs(roof["achieved"] - want) < 0.1 and abs(roof["frac"] - want / roof["peak"]) < 1e-4
+    assert detail["gemm_gu"]["share"] == round(100 / 190, 4)
