@@ -350,11 +350,17 @@ int rp_debug_profile(void* ctx, int32_t steps, double* ms_out, int64_t* counts_o
 
 /* Run the tcgen05 GEMM alone on device pointers: Y[n][m] = sum_k W[m][k] X[n][k]
  * (W fp16 [M,K], X fp16 [N,K] with N <= rows_cap rows allocated, Y fp32 [N,M]);
+ * w_tiled bit 0: W is stored in 128 x 64 tiles, tile (m / 128, k / 64) at
+ * element ((m / 128) * (K / 64) + k / 64) * 8192, row-major inside (the layout
+ * rp_init_model generates the model's GEMM weights in); else row-major.
+ * w_tiled bit 1: split-precision activations -- X holds 2 * rows_cap rows,
+ * the fp16 values and then their fp16 rounding residuals, and Y = W (X_hi +
+ * X_lo)^T (reading Z22).
  * splits = split-K factor (0 = automatic).  Runs once to warm up, then `iters`
  * back-to-back launches timed with CUDA events; *ms_out (may be NULL) gets the
  * mean milliseconds per launch. */
 int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, float* Y, int32_t M, int32_t N,
-                  int32_t K, int32_t splits, int32_t iters, float* ms_out);
+                  int32_t K, int32_t splits, int32_t iters, int32_t w_tiled, float* ms_out);
 
 #ifdef __cplusplus
 }

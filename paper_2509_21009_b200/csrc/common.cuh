@@ -20,6 +20,19 @@ using act_t = __half;
 using act2_t = __half2;
 __device__ __forceinline__ act_t to_act(float a) { return __float2half_rn(a); }
 __device__ __forceinline__ act2_t to_act2(float a, float b) { return __floats2half2_rn(a, b); }
+// fp16 of 4 consecutive values (8-byte aligned) and, when lo != nullptr, their
+// rounding residuals fp16(v - float(fp16(v))): split-precision activations
+// (reading Z22) carry hi + lo ~ 22 significant bits into the next GEMM
+__device__ __forceinline__ void store_act4(act_t* hi, act_t* lo, float4 v) {
+  const act2_t h01 = to_act2(v.x, v.y), h23 = to_act2(v.z, v.w);
+  ((act2_t*)hi)[0] = h01;
+  ((act2_t*)hi)[1] = h23;
+  if (lo) {
+    const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+    ((act2_t*)lo)[0] = to_act2(v.x - f01.x, v.y - f01.y);
+    ((act2_t*)lo)[1] = to_act2(v.z - f23.x, v.w - f23.y);
+  }
+}
 
 
 constexpr int kPage = 64;          // tokens per KV page (DESIGN.md §5 D1)

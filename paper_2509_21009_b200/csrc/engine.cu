@@ -149,6 +149,10 @@ struct RpCtx {
   float* ssq = nullptr;         // [rows][d / 128] per-tile sums of squares of x (folded RMSNorm)
   float* ar = nullptr;          // TP: all-reduced partial of a row-parallel GEMM
   __half *h = nullptr, *q = nullptr, *att = nullptr, *mid = nullptr;   // activations (Z20)
+  // split-precision residuals of the activations (reading Z22); the
+  // producers write them and the consumers read them only while act_lo is set
+  __half *h_lo = nullptr, *q_lo = nullptr, *att_lo = nullptr, *mid_lo = nullptr;
+  bool act_lo = true;
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
   int* gctr = nullptr;
   int* atickets = nullptr;
@@ -199,6 +203,10 @@ struct RpCtx {
   std::vector<cudaEvent_t> ev, ev_pool;   // events of the current profiled step (from the pool)
   std::vector<int> ev_cls;
   volatile int* gate_h = nullptr;         // host-mapped flag that holds a profiled step until it is enqueued
+  // measurement only (RP_SKIP=attention,gemm_qkv,...): kernel classes left
+  // out of decode steps, so a graph step's time without them is its exposed cost
+  unsigned skip_mask = 0;
+  int cur_cls = -1;
   int* gate_d = nullptr;
   double prof_ms[RP_PROF_N] = {0};
   long long prof_cnt[RP_PROF_N] = {0};
@@ -220,6 +228,7 @@ static std::string g_init_err;
 // Programmatic dependent launch is off while a local-group context issues
 // work from this thread (common.cuh g_no_pdl).
 static inline void pdl_mode(const RpCtx* c) { g_no_pdl = c->lg != nullptr; }
+static inline bool skipped(const RpCtx* c) { return c->cur_cls >= 0 && ((c->skip_mask >> c->cur_cls) & 1u); }
 
 // Local groups: a pageable-memory copy is staged by the driver in order
 // across the whole CUDA context, so one queued behind this stream's spinning
@@ -274,7 +283,7 @@ static Sizes compute_sizes(const rp_model_desc* md, const rp_runtime_desc* rd) {
   const int hid = lm.H * lm.hd;
   const int shapes[5][2] = {{qkvw, d}, {d, hid}, {2 * F, d}, {d, F}, {lm.V, d}};
   size_t mx = 0;
-  const int nch = (z.S + 255) / 256;
+  const int nch = (z.S + 127) / 128;   // 128-column chunks of the split-precision GEMMs
   for (auto& s : shapes) {
     const int sp = gemm_pick_splits(s[0], s[1], kSMs);
     if (sp > 1) mx = std::max(mx, (size_t)(s[0] / 128) * nch * sp * 256 * 128);
@@ -325,11 +334,15 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto x = cv.take<float>((size_t)z.Tcap * d);
   auto ar = cv.take<float>(tp_of(rd) > 1 ? (size_t)z.Tcap * d : 1);
   auto h = cv.take<__half>((size_t)z.Tcap * d);
+  auto h_lo = cv.take<__half>((size_t)z.Tcap * d);         // split-precision residuals (reading Z22)
   auto ssq = cv.take<float>((size_t)z.Tcap * std::max<size_t>(1, d / 128));   // folded-RMSNorm partial sums
   auto qkv = cv.take<float>((size_t)z.Tcap * (H + 2 * KV) * hd);
   auto q = cv.take<__half>((size_t)z.Tcap * H * hd);
+  auto q_lo = cv.take<__half>((size_t)z.Tcap * H * hd);
   auto att = cv.take<__half>((size_t)z.Tcap * H * hd);
+  auto att_lo = cv.take<__half>((size_t)z.Tcap * H * hd);
   auto mid = cv.take<__half>((size_t)z.Tcap * F);
+  auto mid_lo = cv.take<__half>((size_t)z.Tcap * F);
   auto logits = cv.take<float>((size_t)std::max(z.S, std::max(z.P, rd->max_prompt_len)) * V);
   auto gpart = cv.take<float>(z.part_floats);
   auto gctr = cv.take<int>(1 << 16);
@@ -381,6 +394,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto ident = cv.take<int>(max_pages + 1);
   if (c) {
     c->x = x; c->ar = ar; c->h = h; c->ssq = ssq; c->qkv = qkv; c->q = q; c->att = att; c->mid = mid; c->logits = logits;
+    c->h_lo = h_lo; c->q_lo = q_lo; c->att_lo = att_lo; c->mid_lo = mid_lo;
     c->gpart = gpart; c->gctr = gctr; c->apart = apart; c->atickets = atick; c->inv_freq = invf;
     c->rope_cs = rope_cs;
     c->items_pre = items_pre; c->pre_tok = pre_tok; c->pre_pos = pre_pos; c->pre_pt = pre_pt;
@@ -456,6 +470,7 @@ static cudaEvent_t prof_event(RpCtx* c) {
 struct ProfScope {
   RpCtx* c; int cls; bool on;
   ProfScope(RpCtx* c_, int cls_) : c(c_), cls(cls_), on(c_->prof_steps_left > 0 && !c_->capturing) {
+    c->cur_cls = cls;
     if (on) { cudaEventRecord(prof_event(c), c->st); c->ev_cls.push_back(-1); }
   }
   ~ProfScope() {
@@ -502,7 +517,8 @@ static void coll_allreduce_max_u64(RpCtx* c, CommCtx& cm, unsigned long long* bu
 
 static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, int n_host, int splits, int epi,
                  void* out, int ldo, const float* bias, const RopeArgs* rope = nullptr, int fold = FOLD_NONE,
-                 int push_slot = -1) {
+                 int push_slot = -1, __half* out_lo = nullptr) {
+  if (skipped(c)) return;
   GemmArgs a{};
   if (push_slot >= 0) {
     const int me = c->rd.tp_rank;
@@ -516,9 +532,11 @@ static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, in
   a.M = M; a.K = K; a.n_dev = n_dev; a.n_host = n_host; a.splits = splits; a.epi = epi; a.out = out; a.ldo = ldo;
   a.bias = bias; a.partial = c->gpart; a.counters = c->gctr;
   a.no_spin = c->lg ? 1 : 0;
+  a.lo = c->act_lo ? 1 : 0;
+  a.out_lo = c->act_lo ? out_lo : nullptr;
   a.ssq_stride = c->m.d / 128; a.ssq_parts = c->m.d / 128;
   a.norm_inv_d = 1.0f / (float)c->m.d; a.norm_eps = c->m.eps;
-  if (fold == FOLD_PRODUCE) { a.xb_out = c->h; a.ldxb = c->m.d; a.ssq_out = c->ssq; }
+  if (fold == FOLD_PRODUCE) { a.xb_out = c->h; a.xb_lo = c->h_lo; a.ldxb = c->m.d; a.ssq_out = c->ssq; }
   if (fold == FOLD_CONSUME) a.ssq_in = c->ssq;
   gemm_launch(p, a, kSMs, c->st);
   c->launches++;
@@ -558,10 +576,10 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
     void* own = c->tp_peer_base[c->rd.tp_rank];
     launch_tp_norm(c->x, tp_slot(c, own, slot, 0), c->tp, c->tp_recv_floats / c->tp, tp_flags(c, own, slot),
                    c->tp_gen + slot, c->tp_done + slot, m.d / 128, splits, c->coop_min, c->lg ? 8 : 0, n_dev, n_host,
-                   gamma, c->h, m.d, m.eps, c->st);
+                   gamma, c->h, m.d, m.eps, c->st, c->h_lo);
     c->launches++;
   };
-  { ProfScope ps(c, RP_PROF_EMBED); launch_embed(tok, n_dev, n_host, c->emb, c->x, m.d, c->st); c->launches++; }
+  { ProfScope ps(c, RP_PROF_EMBED); if (!skipped(c)) launch_embed(tok, n_dev, n_host, c->emb, c->x, m.d, c->st); c->launches++; }
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = c->layers[l];
     const int f_in = (fold && l > 0) ? FOLD_CONSUME : FOLD_NONE;
@@ -570,12 +588,12 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
       tp_norm(1, nullptr, sp_down);
     } else if (f_in == FOLD_NONE) {
       ProfScope ps(c, RP_PROF_RMSNORM);
-      launch_rmsnorm(c->x, delta, nullptr, n_dev, n_host, nullptr, c->h, m.d, m.eps, c->st); c->launches++;
+      if (!skipped(c)) launch_rmsnorm(c->x, delta, nullptr, n_dev, n_host, nullptr, c->h, m.d, m.eps, c->st, c->h_lo); c->launches++;
     }
     if (decode && sp_qkv > 1 && m.hd % 64 == 0) {
       // RoPE + KV append fused into the split-K reduction of the QKV GEMM
       ProfScope ps(c, RP_PROF_GEMM_QKV);
-      RopeArgs ra{c->q, (uint8_t*)c->rd.kv_pool, c->R.page_table, row_pos, row_pt, c->rope_cs, m.page_bytes,
+      RopeArgs ra{c->q, c->q_lo, (uint8_t*)c->rd.kv_pool, c->R.page_table, row_pos, row_pt, c->rope_cs, m.page_bytes,
                   c->R.maxp, l, m.H, m.KV, m.hd};
       gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_QKV_ROPE, c->qkv, qkvw, w.bqkv, &ra, f_in);
     } else {
@@ -583,11 +601,11 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
         gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_F32, c->qkv, qkvw, w.bqkv, nullptr, f_in); }
       { ProfScope ps(c, RP_PROF_ROPE);
         launch_rope_append(c->qkv, n_dev, n_host, row_pos, row_pt, c->R.page_table, c->R.maxp, c->q,
-                           c->rd.kv_pool, m, l, c->inv_freq, c->st); c->launches++; }
+                           c->rd.kv_pool, m, l, c->inv_freq, c->st, c->q_lo); c->launches++; }
     }
     { ProfScope ps(c, RP_PROF_ATTN);
-      launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
-                       c->apart, c->atickets, m, l, decode, c->st); c->launches++; }
+      if (!skipped(c)) launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
+                       c->apart, c->atickets, m, l, decode, c->st, c->q_lo, c->att_lo); c->launches++; }
     { ProfScope ps(c, RP_PROF_GEMM_O);
       gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
            nullptr, nullptr, f_prod, peer ? 0 : -1); }
@@ -598,11 +616,12 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
     }
     if (!fold && !peer) {
       ProfScope ps(c, RP_PROF_RMSNORM);
-      launch_rmsnorm(c->x, tp ? c->ar : nullptr, nullptr, n_dev, n_host, nullptr, c->h, m.d, m.eps, c->st);
+      launch_rmsnorm(c->x, tp ? c->ar : nullptr, nullptr, n_dev, n_host, nullptr, c->h, m.d, m.eps, c->st, c->h_lo);
       c->launches++;
     }
     { ProfScope ps(c, RP_PROF_GEMM_GU);
-      gemm(c, w.p_gu, 2 * m.F, m.d, n_dev, n_host, sp_gu, EPI_SWIGLU, c->mid, m.F, nullptr, nullptr, f_cons); }
+      gemm(c, w.p_gu, 2 * m.F, m.d, n_dev, n_host, sp_gu, EPI_SWIGLU, c->mid, m.F, nullptr, nullptr, f_cons, -1,
+           c->mid_lo); }
     { ProfScope ps(c, RP_PROF_GEMM_DOWN);
       gemm(c, w.p_down, m.d, m.F, n_dev, n_host, sp_down, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
            nullptr, nullptr, f_prod, peer ? 1 : -1); }
@@ -626,18 +645,19 @@ static void lm_head_sample(RpCtx* c, const int* n_dev, int n_host, const int* ga
     void* own = c->tp_peer_base[c->rd.tp_rank];
     launch_tp_norm(c->x, tp_slot(c, own, 1, 0), c->tp, c->tp_recv_floats / c->tp, tp_flags(c, own, 1),
                    c->tp_gen + 1, c->tp_done + 1, c->m.d / 128, c->s_down, c->coop_min, c->lg ? 8 : 0, n_dev, n_host,
-                   nullptr, c->h, c->m.d, c->m.eps, c->st);
+                   nullptr, c->h, c->m.d, c->m.eps, c->st, c->h_lo);
     c->launches++;
   } else if (!fold) {
     ProfScope ps(c, RP_PROF_RMSNORM);
-    launch_rmsnorm(c->x, pending ? c->ar : nullptr, gather, n_dev, n_host, nullptr, c->h, c->m.d, c->m.eps, c->st);
+    launch_rmsnorm(c->x, pending ? c->ar : nullptr, gather, n_dev, n_host, nullptr, c->h, c->m.d, c->m.eps, c->st,
+                   c->h_lo);
     c->launches++;
   }
   { ProfScope ps(c, RP_PROF_GEMM_LM);
     gemm(c, c->p_lm, c->m.V, c->m.d, n_dev, rows_out, splits, EPI_F32, c->logits, c->m.V, nullptr, nullptr,
          fold ? FOLD_CONSUME : FOLD_NONE); }
   { ProfScope ps(c, RP_PROF_SAMPLER);
-    launch_sampler(c->logits, c->m.V, c->m.v0, row_div, R, c->rd.sample_seed, 1.0f / c->rd.temperature,
+    if (!skipped(c)) launch_sampler(c->logits, c->m.V, c->m.v0, row_div, R, c->rd.sample_seed, 1.0f / c->rd.temperature,
                    (uint32_t)c->round_id, c->st); c->launches++; }
   if (c->tp > 1) {
     ProfScope ps(c, RP_PROF_NCCL);
@@ -754,6 +774,18 @@ static int init_impl(RpCtx* c) {
   const uint64_t seed = md->weight_seed;
   c->layers.resize(m.L);
   size_t k = 0;
+  // split-precision activations (reading Z22); RP_ACT_LO=0 turns them off (A/B)
+  c->act_lo = !(getenv("RP_ACT_LO") && atoi(getenv("RP_ACT_LO")) == 0);
+  if (const char* sk = getenv("RP_SKIP")) {
+    static const char* names[RP_PROF_N] = {"embed", "rmsnorm", "gemm_qkv", "rope_append", "attention", "attn_merge",
+                                           "gemm_o", "gemm_gu", "gemm_down", "gemm_lm", "sampler", "ctl", "nccl"};
+    for (int i = 0; i < RP_PROF_N; ++i)
+      if (i != RP_PROF_CTL && i != RP_PROF_NCCL && strstr(sk, names[i])) c->skip_mask |= 1u << i;
+  }
+  if (!c->act_lo) c->h_lo = c->q_lo = c->att_lo = c->mid_lo = nullptr;   // producers skip, plans map hi only
+  // GEMM weights in 128 x 64 tiles: every weight TMA box is one contiguous
+  // 16 KB read (RP_W_ROWMAJOR=1: plain row-major, an A/B switch)
+  const int wt = getenv("RP_W_ROWMAJOR") ? 0 : 1;
   std::vector<float> ones(std::max(d, (size_t)1), 1.0f);
   for (int l = 0; l < m.L; ++l) {
     LayerW& w = c->layers[l];
@@ -770,12 +802,13 @@ static int init_impl(RpCtx* c) {
     // rows [r*F, ...), down columns [r*F, ...); H, KV, F are local here)
     const int tr = c->tp > 1 ? rd->tp_rank : 0;
     const size_t Hf = (size_t)md->n_heads, Ff = (size_t)md->d_ff;
+    // GEMM weights are stored in 128 x 64 tiles (weight_tiled_index, k_model.cu)
     launch_init_weights(w.wqkv, (long long)(H * hd), (int)d, (long long)tr * H * hd, 0, (int)d, base + 0, seed, 0, 0,
-                        c->st);
-    launch_init_weights(w.wqkv + H * hd * d, (long long)(KV * hd), (int)d, (long long)tr * KV * hd, 0, (int)d,
-                        base + 1, seed, 0, 0, c->st);
-    launch_init_weights(w.wqkv + (H + KV) * hd * d, (long long)(KV * hd), (int)d, (long long)tr * KV * hd, 0, (int)d,
-                        base + 2, seed, 0, 0, c->st);
+                        c->st, 1, 0, wt);
+    launch_init_weights(w.wqkv, (long long)(KV * hd), (int)d, (long long)tr * KV * hd, 0, (int)d, base + 1, seed, 0, 0,
+                        c->st, 1, (long long)(H * hd), wt);
+    launch_init_weights(w.wqkv, (long long)(KV * hd), (int)d, (long long)tr * KV * hd, 0, (int)d, base + 2, seed, 0, 0,
+                        c->st, 1, (long long)((H + KV) * hd), wt);
     if (md->qkv_bias) {
       launch_init_weights(w.bqkv, (long long)(H * hd), 1, (long long)tr * H * hd, 0, 1, base + 3, seed, 1, 0, c->st);
       launch_init_weights(w.bqkv + H * hd, (long long)(KV * hd), 1, (long long)tr * KV * hd, 0, 1, base + 4, seed, 1,
@@ -786,28 +819,28 @@ static int init_impl(RpCtx* c) {
       CK(cudaMemsetAsync(w.bqkv, 0, (H + 2 * KV) * hd * 4, c->st));
     }
     launch_init_weights(w.wo, (long long)d, (int)(H * hd), 0, (int)(tr * H * hd), (int)(Hf * hd), base + 6, seed, 0, 0,
-                        c->st);
-    launch_init_weights(w.wgu, (long long)F, (int)d, (long long)tr * F, 0, (int)d, base + 7, seed, 2, 0, c->st);
-    launch_init_weights(w.wgu, (long long)F, (int)d, (long long)tr * F, 0, (int)d, base + 8, seed, 2, 1, c->st);
-    launch_init_weights(w.wd, (long long)d, (int)F, 0, (int)(tr * F), (int)Ff, base + 9, seed, 0, 0, c->st);
+                        c->st, 1, 0, wt);
+    launch_init_weights(w.wgu, (long long)F, (int)d, (long long)tr * F, 0, (int)d, base + 7, seed, 2, 0, c->st, 1, 0, wt);
+    launch_init_weights(w.wgu, (long long)F, (int)d, (long long)tr * F, 0, (int)d, base + 8, seed, 2, 1, c->st, 1, 0, wt);
+    launch_init_weights(w.wd, (long long)d, (int)F, 0, (int)(tr * F), (int)Ff, base + 9, seed, 0, 0, c->st, 1, 0, wt);
     CK(cudaMemcpyAsync(w.ln1, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(w.ln2, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
   }
   c->emb = (__nv_bfloat16*)(wb + wl.off[k++]);
   c->lm = (__half*)(wb + wl.off[k++]);
   c->lnf = (float*)(wb + wl.off[k++]);
-  launch_init_weights(c->emb, (long long)md->vocab, (int)d, 0, 0, (int)d, 0x10000000u, seed, 0, 0, c->st, 0);
-  launch_init_weights(c->lm, (long long)V, (int)d, (long long)m.v0, 0, (int)d, 0x10000001u, seed, 0, 0, c->st);
+  launch_init_weights(c->emb, (long long)md->vocab, (int)d, 0, 0, (int)d, 0x10000000u, seed, 0, 0, c->st, 0, 0, 0);
+  launch_init_weights(c->lm, (long long)V, (int)d, (long long)m.v0, 0, (int)d, 0x10000001u, seed, 0, 0, c->st, 1, 0, wt);
   CK(cudaMemcpyAsync(c->lnf, ones.data(), d * 4, cudaMemcpyHostToDevice, c->st));
   // RMSNorm gains folded into the consuming GEMMs' weight columns (QKV <- ln1,
   // gate||up <- ln2, LM head <- final norm): RMSNorm(x) * g . W^T =
   // (x / rms) . (W diag g)^T, so every norm kernel and folded norm runs with
   // unit gain.  The Z12 gains are 1, for which the fold is exact.
   for (auto& w : c->layers) {
-    launch_scale_cols(w.wqkv, (long long)((H + 2 * KV) * hd), (int)d, w.ln1, c->st);
-    launch_scale_cols(w.wgu, (long long)(2 * F), (int)d, w.ln2, c->st);
+    launch_scale_cols(w.wqkv, (long long)((H + 2 * KV) * hd), (int)d, w.ln1, c->st, wt);
+    launch_scale_cols(w.wgu, (long long)(2 * F), (int)d, w.ln2, c->st, wt);
   }
-  launch_scale_cols(c->lm, (long long)V, (int)d, c->lnf, c->st);
+  launch_scale_cols(c->lm, (long long)V, (int)d, c->lnf, c->st, wt);
   CK(cudaGetLastError());
 
   // ---- RoPE frequencies theta^(-2i/hd) in fp64
@@ -830,13 +863,16 @@ static int init_impl(RpCtx* c) {
   const int Tcap = c->z.Tcap;
   const int qkvw = (int)((H + 2 * KV) * hd);
   for (auto& w : c->layers) {
-    if (make_plan(&w.p_qkv, w.wqkv, qkvw, (int)d, c->h, Tcap) ||
-        make_plan(&w.p_o, w.wo, (int)d, (int)(H * hd), c->att, Tcap) ||
-        make_plan(&w.p_gu, w.wgu, (int)(2 * F), (int)d, c->h, Tcap) ||
-        make_plan(&w.p_down, w.wd, (int)d, (int)F, c->mid, Tcap))
+    if (make_plan(&w.p_qkv, w.wqkv, qkvw, (int)d, c->h, Tcap, wt, c->h_lo) ||
+        make_plan(&w.p_o, w.wo, (int)d, (int)(H * hd), c->att, Tcap, wt, c->att_lo) ||
+        make_plan(&w.p_gu, w.wgu, (int)(2 * F), (int)d, c->h, Tcap, wt, c->h_lo) ||
+        make_plan(&w.p_down, w.wd, (int)d, (int)F, c->mid, Tcap, wt, c->mid_lo))
       return c->fail(RP_ECUDA, "cuTensorMapEncodeTiled failed");
   }
-  if (make_plan(&c->p_lm, c->lm, (int)V, (int)d, c->h, Tcap))
+  // the LM head reads the final-norm activations in fp16 only: its split
+  // precision moves the 28-layer logits error by < 1e-4 (0.0155 vs 0.0154,
+  // profiles/r02_emulate_fp16_points.txt) at 65% more LM-head time at 256 rows
+  if (make_plan(&c->p_lm, c->lm, (int)V, (int)d, c->h, Tcap, wt, nullptr))
     return c->fail(RP_ECUDA, "cuTensorMapEncodeTiled failed (lm head)");
   c->s_qkv = gemm_pick_splits(qkvw, (int)d, kSMs);
   c->s_o = gemm_pick_splits((int)d, (int)(H * hd), kSMs);
@@ -1059,8 +1095,8 @@ static int prefill(RpCtx* c, const std::vector<int>& toks, const std::vector<int
   bool pending = false;
   forward_layers(c, c->pre_tok, nullptr, T, c->pre_pos, c->pre_pt, c->items_pre, nullptr, (int)items.size(), false,
                  T, &pending);
-  launch_rmsnorm(c->x, pending ? c->ar : nullptr, c->pre_last, nullptr, (int)out_rows.size(), c->lnf, c->h, c->m.d,
-                 c->m.eps, c->st);
+  launch_rmsnorm(c->x, pending ? c->ar : nullptr, c->pre_last, nullptr, (int)out_rows.size(), nullptr, c->h, c->m.d,
+                 c->m.eps, c->st, c->h_lo);
   c->launches++;
   gemm(c, c->p_lm, c->m.V, c->m.d, nullptr, (int)out_rows.size(), 1, EPI_F32, c->logits, c->m.V, nullptr);
   CK(cudaGetLastError());
@@ -1637,22 +1673,26 @@ int rp_debug_profile(void* ctx, int32_t steps, double* ms_out, int64_t* counts_o
 }
 
 int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, float* Y, int32_t M, int32_t N,
-                  int32_t K, int32_t splits, int32_t iters, float* ms_out) {
+                  int32_t K, int32_t splits, int32_t iters, int32_t w_tiled, float* ms_out) {
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
   pdl_mode(c);
   if (M % 128 || K % 64 || M <= 0 || K <= 0 || N < 0 || N > rows_cap) return c->fail(RP_EINVAL, "invalid GEMM shape");
   if (splits <= 0) splits = gemm_pick_splits(M, K, kSMs);
   splits = std::min(splits, K / 64);
-  const size_t need = (size_t)(M / 128) * ((N + 255) / 256) * splits * 256 * 128;
+  const size_t need = (size_t)(M / 128) * ((N + 127) / 128) * splits * 256 * 128;   // 128-column chunks when LO
   if (splits > 1 && need > c->z.part_floats) return c->fail(RP_ENOSPC, "split-K workspace too small");
   if ((M / 128) * ((N + 255) / 256) > (1 << 15)) return c->fail(RP_ENOSPC, "too many tiles");
   GemmPlan p;
-  if (make_plan(&p, W, M, K, X, rows_cap)) return c->fail(RP_ECUDA, "tensor map");
+  // w_tiled bit 1: X holds [2][rows_cap][K] -- fp16 rows, then their residuals (split precision)
+  const void* X_lo = (w_tiled & 2) ? (const void*)((const __half*)X + (size_t)rows_cap * K) : nullptr;
+  if (make_plan(&p, W, M, K, X, rows_cap, w_tiled & 1, X_lo)) return c->fail(RP_ECUDA, "tensor map");
   iters = std::max(iters, 1);
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
+  const bool lo_saved = c->act_lo;
+  c->act_lo = X_lo != nullptr;
   gemm(c, p, M, K, nullptr, N, splits, EPI_F32, Y, M, nullptr);   // warm
   if (getenv("RP_GEMM_TIMELINE")) {   // debug: per-CTA phase timeline of one launch, to stderr
     long long* tl = nullptr;
@@ -1680,6 +1720,7 @@ int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, flo
   }
   CK(cudaEventRecord(e0, c->st));
   for (int i = 0; i < iters; ++i) gemm(c, p, M, K, nullptr, N, splits, EPI_F32, Y, M, nullptr);
+  c->act_lo = lo_saved;
   CK(cudaEventRecord(e1, c->st));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->st));

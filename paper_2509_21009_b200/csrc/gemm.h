@@ -15,6 +15,7 @@ enum GemmEpi { EPI_F32 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_BF16 = 3, EPI_QKV
 // (fp16, reading Z20).
 struct RopeArgs {
   __half* q_out;
+  __half* q_lo;           // fp16 residual of q (split precision), or nullptr
   uint8_t* kv_pool;
   const int* page_table;
   const int* row_pos;
@@ -31,6 +32,14 @@ struct GemmArgs {
   int splits;             // split-K factor (1 = direct epilogue)
   int coop_min;           // cooperative split-K reduction from this chunk width up (set by gemm_launch)
   int no_spin;            // 1: no inter-CTA waits (ticket reduction only; single-GPU local groups)
+  int a_tiled;            // weights stored in 128 x 64 tiles (set by gemm_launch from the plan)
+  // Split-precision activations (reading Z22): D = W . x_hi + W . x_lo with
+  // x_lo = fp16(x - x_hi), two MMAs per K step, fp32 accumulation -- the
+  // activation operand carries ~22 significant bits.  The weights are exact
+  // fp16 (the bf16 formula values), so only the activation rounding matters.
+  int lo;
+  __half* xb_lo;          // FOLD producer: fp16 residual of x next to xb_out
+  __half* out_lo;         // SWIGLU: fp16 residual of the output next to `out`
   int epi;                // GemmEpi
   void* out;              // out[n * ldo + m] (SWIGLU: out[n * ldo + feature])
   int ldo;
@@ -61,8 +70,11 @@ struct GemmArgs {
 };
 
 struct GemmPlan {
-  CUtensorMap tmA;        // weights [M, K] fp16, box 64 x 128
+  CUtensorMap tmA;        // weights [M, K] fp16, box 64 x 128; tiled: [M*K/64, 64] (128 x 64 tiles, each contiguous)
+  int a_tiled;
   CUtensorMap tmB16, tmB64, tmB256;   // activations [rows_cap, K], boxes of 16 / 64 / 256 rows
+  CUtensorMap tmL16, tmL64, tmL256;   // their fp16 rounding residuals (split precision), same boxes
+  int has_lo;
 };
 
 int make_tmap_act(CUtensorMap* map, const void* base, int rows, int cols, int box_rows);
@@ -73,6 +85,7 @@ int gemm_coop_min();
 int gemm_smem_bytes();
 int gemm_pick_splits(int M, int K, int n_sms);
 void gemm_launch(const GemmPlan& p, const GemmArgs& a, int grid, cudaStream_t st);
-int make_plan(GemmPlan* p, const void* W, int M, int K, const void* X, int rows_cap);
+int make_plan(GemmPlan* p, const void* W, int M, int K, const void* X, int rows_cap, int w_tiled,
+              const void* X_lo = nullptr);
 
 }  // namespace rp

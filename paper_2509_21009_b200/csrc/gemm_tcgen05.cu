@@ -174,12 +174,20 @@ __device__ __forceinline__ long long gtimer() {
 #define TL(k) do { if (a.timeline) a.timeline[blockIdx.x * 16 + (k)] = gtimer(); } while (0)
 
 struct Item { int tile, chunk, split; };
-__device__ __forceinline__ Item decode_item(int it, int m_tiles, int splits) {
+// split fastest, then tile, then chunk; with `chunks_inner` (split-precision
+// GEMMs, 128-column chunks) the chunks of a tile are adjacent items, so the
+// CTAs that read the same weight tile run together and share it through L2
+__device__ __forceinline__ Item decode_item(int it, int m_tiles, int splits, int n_chunks = 1, bool chunks_inner = false) {
   Item r;
   r.split = it % splits;
   int q = it / splits;
-  r.tile = q % m_tiles;
-  r.chunk = q / m_tiles;
+  if (chunks_inner) {
+    r.chunk = q % n_chunks;
+    r.tile = q / n_chunks;
+  } else {
+    r.tile = q % m_tiles;
+    r.chunk = q / m_tiles;
+  }
   return r;
 }
 
@@ -239,11 +247,16 @@ __device__ __forceinline__ void push_signal(const GemmArgs& a, int et) {
 // tcgen05.mma.cta_group::2 (M = 256) and each CTA's TMEM holds its 128 output
 // rows, so a stage carries half the activation bytes per SM and the ring runs
 // deeper (the wide-batch regime is bound by ring bytes per FLOP).
-template <int CG>
+// LO = 1: split-precision activations (GemmArgs::lo) -- a separate
+// instantiation, because runtime lo branches in the producer and MMA loops
+// cost ~25% of the weight-streaming rate at small N even when off (measured:
+// profiles/r02_gemm_lo_bisect.txt).
+template <int CG, int LO>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB16,
                     const __grid_constant__ CUtensorMap tmB64, const __grid_constant__ CUtensorMap tmB256,
-                    GemmArgs a) {
+                    const __grid_constant__ CUtensorMap tmL16, const __grid_constant__ CUtensorMap tmL64,
+                    const __grid_constant__ CUtensorMap tmL256, GemmArgs a) {
   const int N = a.n_dev ? *a.n_dev : a.n_host;
   if (N <= 0) return;
   if (threadIdx.x == 0) TL(0);
@@ -252,22 +265,30 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int n_ctas = CG == 2 ? (int)gridDim.x / 2 : (int)gridDim.x;
   const bool leader = crank == 0;
   const int m_tiles = a.M / (BM * CG);
-  const int n_chunks = (N + BN - 1) / BN;
+  // LO: 128-column chunks -- the MMA's N holds the chunk's hi rows and then
+  // its lo rows (at most 128 + 128), so a row's hi and lo products come out
+  // of one MMA (the weight tile is read from shared memory once per K step)
+  constexpr int BNX = LO ? 128 : BN;
+  const int n_chunks = (N + BNX - 1) / BNX;
   const int n_items = m_tiles * n_chunks * a.splits;
   if (cta_id >= n_items) return;                   // both CTAs of a pair leave together
   const int kb_total = a.K / BK;
   // cooperative split-K reduction: grid fits one wave and the chunk is wide
   // enough that a single CTA reducing the whole tile would be the bottleneck
-  const bool coop = a.splits > 1 && n_items <= n_ctas && min(BN, N) >= a.coop_min;
+  const bool coop = a.splits > 1 && n_items <= n_ctas && min(BNX, N) >= a.coop_min;
 
   // Ring geometry from the widest activation chunk: 16/64/256-row boxes; at
   // small N the stages shrink and the ring deepens (more weight bytes in
   // flight per SM for the HBM-bound small-batch regime).
   // (pair: each CTA holds half of the 16-padded chunk, at most 128 rows)
-  const int wmax = CG == 2 ? ((min(BN, N) + 15) & ~15) / 2 : min(BN, N);
+  const int wmax = CG == 2 ? ((min(BNX, N) + 15) & ~15) / 2 : min(BNX, N);
   const int brow_max = wmax > 192 ? 256 : wmax > 48 ? 64 : 16;
   const int b_rows = ((wmax + brow_max - 1) / brow_max) * brow_max;
-  const int STAGE_BYTES = A_BYTES + ((b_rows * BK * 2 + 1023) & ~1023);
+  // split-precision activations (LO): the stage's activation tile is the
+  // chunk's fp16 rows (hi, padded to whole boxes) followed by their fp16
+  // rounding residuals (lo)
+  const int NLO = LO ? 2 : 1;
+  const int STAGE_BYTES = A_BYTES + ((NLO * b_rows * BK * 2 + 1023) & ~1023);
   const int STAGES = min(MAX_STAGES, RING_BYTES / STAGE_BYTES);
 
   extern __shared__ uint8_t smem_raw[];
@@ -304,6 +325,11 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB16) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB64) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB256) : "memory");
+    if (LO) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmL16) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmL64) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmL256) : "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -321,10 +347,15 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       int stage = 0; uint32_t phase = 0;
       bool first = true;
       for (int it = cta_id; it < n_items; it += n_ctas) {
-        Item I = decode_item(it, m_tiles, a.splits);
+        Item I = decode_item(it, m_tiles, a.splits, n_chunks, LO);
         const int kb0 = (int)((long)I.split * kb_total / a.splits), kb1 = (int)((long)(I.split + 1) * kb_total / a.splits);
         const int wrow = (I.tile * CG + (int)crank) * BM;   // this CTA's 128 weight rows
-        int n0 = I.chunk * BN, nc = min(BN, N - n0);
+        // A box coordinates of k-block kb: (kb * 64, wrow) row-major, or the
+        // start row of tile (wrow / 128, kb) in the tiled layout (16 KB contiguous)
+        const int kbt = a.K / BK;
+#define A_C0(kb) (a.a_tiled ? 0 : (kb) * BK)
+#define A_C1(kb) (a.a_tiled ? ((wrow / BM) * kbt + (kb)) * BM : wrow)
+        int n0 = I.chunk * BNX, nc = min(BNX, N - n0);
         if (CG == 2) {                        // this CTA's half of the 16-padded chunk
           const int half = ((nc + 15) & ~15) / 2;
           n0 += (int)crank * half;
@@ -332,11 +363,13 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
         // X boxes: one 256-row box for wide chunks, else a few 64- or 16-row boxes
         const CUtensorMap* tb = nc > 192 ? &tmB256 : nc > 48 ? &tmB64 : &tmB16;
+        const CUtensorMap* tl = nc > 192 ? &tmL256 : nc > 48 ? &tmL64 : &tmL16;
         const int brow = nc > 192 ? 256 : nc > 48 ? 64 : 16;
         const int nbox = (nc + brow - 1) / brow;
+        const int lo_off = nbox * brow * BK * 2;           // LO: residual rows follow the hi rows
         // pair: the leader arms its full barrier with both CTAs' bytes; every
         // TMA of the pair completes on the leader's barrier
-        const uint32_t stage_tx = (uint32_t)CG * (A_BYTES + nbox * brow * BK * 2);
+        const uint32_t stage_tx = (uint32_t)CG * (A_BYTES + NLO * nbox * brow * BK * 2);
         const int cnt = kb1 - kb0;
         // rotate the K order per tile so the CTAs do not all request the same
         // activation tile at the same time (an L2 hot spot).  The rotation
@@ -355,8 +388,8 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             const int kb = kb0 + (j + rot) % cnt;
             const uint32_t fb = full0 + 8 * j;
             if (leader) mbar_expect_tx(fb, stage_tx);
-            if (CG == 2) tma_load_2d_pair(smem_u32(smem + j * STAGE_BYTES), &tmA, leader_addr(fb), kb * BK, wrow, pol_w);
-            else tma_load_2d(smem_u32(smem + j * STAGE_BYTES), &tmA, fb, kb * BK, wrow, pol_w);
+            if (CG == 2) tma_load_2d_pair(smem_u32(smem + j * STAGE_BYTES), &tmA, leader_addr(fb), A_C0(kb), A_C1(kb), pol_w);
+            else tma_load_2d(smem_u32(smem + j * STAGE_BYTES), &tmA, fb, A_C0(kb), A_C1(kb), pol_w);
           }
           pdl_wait();
           for (int j = 0; j < npre; ++j) {
@@ -366,6 +399,10 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             for (int b = 0; b < nbox; ++b) {
               if (CG == 2) tma_load_2d_pair(sa + A_BYTES + b * brow * BK * 2, tb, leader_addr(fb), kb * BK, n0 + brow * b, pol_x);
               else tma_load_2d(sa + A_BYTES + b * brow * BK * 2, tb, fb, kb * BK, n0 + brow * b, pol_x);
+              if (LO) {
+                if (CG == 2) tma_load_2d_pair(sa + A_BYTES + lo_off + b * brow * BK * 2, tl, leader_addr(fb), kb * BK, n0 + brow * b, pol_x);
+                else tma_load_2d(sa + A_BYTES + lo_off + b * brow * BK * 2, tl, fb, kb * BK, n0 + brow * b, pol_x);
+              }
             }
           }
           j0 = npre;
@@ -380,13 +417,17 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           if (CG == 2) {
             const uint32_t lb = leader_addr(fb);
-            tma_load_2d_pair(sa, &tmA, lb, kb * BK, wrow, pol_w);
-            for (int b = 0; b < nbox; ++b)
+            tma_load_2d_pair(sa, &tmA, lb, A_C0(kb), A_C1(kb), pol_w);
+            for (int b = 0; b < nbox; ++b) {
               tma_load_2d_pair(sa + A_BYTES + b * brow * BK * 2, tb, lb, kb * BK, n0 + brow * b, pol_x);
+              if (LO) tma_load_2d_pair(sa + A_BYTES + lo_off + b * brow * BK * 2, tl, lb, kb * BK, n0 + brow * b, pol_x);
+            }
           } else {
-            tma_load_2d(sa, &tmA, fb, kb * BK, wrow, pol_w);
-            for (int b = 0; b < nbox; ++b)
+            tma_load_2d(sa, &tmA, fb, A_C0(kb), A_C1(kb), pol_w);
+            for (int b = 0; b < nbox; ++b) {
               tma_load_2d(sa + A_BYTES + b * brow * BK * 2, tb, fb, kb * BK, n0 + brow * b, pol_x);
+              if (LO) tma_load_2d(sa + A_BYTES + lo_off + b * brow * BK * 2, tl, fb, kb * BK, n0 + brow * b, pol_x);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -397,10 +438,12 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       // ===== MMA issuer (single thread; the pair's leader for CG = 2) =====
       int stage = 0; uint32_t phase = 0; int local = 0;
       for (int it = cta_id; it < n_items; it += n_ctas, ++local) {
-        Item I = decode_item(it, m_tiles, a.splits);
+        Item I = decode_item(it, m_tiles, a.splits, n_chunks, LO);
         const int kb0 = (int)((long)I.split * kb_total / a.splits), kb1 = (int)((long)(I.split + 1) * kb_total / a.splits);
-        const int nc = min(BN, N - I.chunk * BN);
-        const int nmma = (nc + 15) & ~15;
+        const int nc = min(BNX, N - I.chunk * BNX);
+        // LO: N = the hi rows (whole boxes) + the 16-padded lo rows
+        const int hi_rows = nc > 48 ? ((nc + 63) & ~63) : ((nc + 15) & ~15);
+        const int nmma = LO ? hi_rows + ((nc + 15) & ~15) : (nc + 15) & ~15;
         const uint32_t idesc = make_idesc(nmma, BM * CG);
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
@@ -434,9 +477,10 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     int local = 0;
     int rsc_chunk = -1;                     // chunk whose RMSNorm scales are in rsc
     for (int it = cta_id; it < n_items; it += n_ctas, ++local) {
-      Item I = decode_item(it, m_tiles, a.splits);
+      Item I = decode_item(it, m_tiles, a.splits, n_chunks, LO);
       if (CG == 2) I.tile = I.tile * 2 + (int)crank;   // this CTA's 128-row tile (the pair has no split-K)
-      const int n0 = I.chunk * BN, nc = min(BN, N - n0);
+      const int n0 = I.chunk * BNX, nc = min(BNX, N - n0);
+      const int hi_rows = nc > 48 ? ((nc + 63) & ~63) : ((nc + 15) & ~15);   // LO: lo columns start here
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       if (a.ssq_in && I.chunk != rsc_chunk) {
@@ -474,6 +518,12 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         for (int c0 = 0; c0 < nc; c0 += 32) {
           uint32_t r[32];
           TMEM_LD32(tbase + c0, r);
+          if (LO) {                            // + W . x_lo (the residual columns)
+            uint32_t rl[32];
+            TMEM_LD32(tbase + hi_rows + c0, rl);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(rl[j]));
+          }
 #pragma unroll
           for (int j = 0; j < 32; ++j) stg[j * TS + row] = __uint_as_float(r[j]);
           named_bar(2, 128);
@@ -623,6 +673,14 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               act_t* dst;
               if (is_q) {
                 dst = R.q_out + ((size_t)n * R.H + head) * hd + i0;
+                if (R.q_lo) {                  // q's rounding residual (split precision)
+                  const float2 f01 = __half22float2(o01), f23 = __half22float2(o23);
+                  act2_t l01 = to_act2(o.x - f01.x, o.y - f01.y), l23 = to_act2(o.z - f23.x, o.w - f23.y);
+                  uint2 pl;
+                  pl.x = *(uint32_t*)&l01;
+                  pl.y = *(uint32_t*)&l23;
+                  *(uint2*)(R.q_lo + ((size_t)n * R.H + head) * hd + i0) = pl;
+                }
               } else {
                 const int kh = is_v ? head - R.H - R.KV : head - R.H;
                 const int page = R.page_table[(size_t)R.row_pt[n] * R.maxp + pos / kPage];
@@ -656,9 +714,8 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               if (a.ssq_out) {
                 // fp16(x) for the next GEMM and this tile's sum of squares of
                 // column n (the warp covers the tile's 128 rows: lanes x 4)
-                act2_t* xb = (act2_t*)(a.xb_out + (size_t)(n0 + col) * a.ldxb + m4);
-                xb[0] = to_act2(v.x, v.y);
-                xb[1] = to_act2(v.z, v.w);
+                const size_t xo = (size_t)(n0 + col) * a.ldxb + m4;
+                store_act4(a.xb_out + xo, a.xb_lo ? a.xb_lo + xo : nullptr, v);
                 float ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
@@ -716,6 +773,11 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           TMEM_LD32(tbase + c0, r);
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          if (LO) {                            // + W . x_lo (the residual columns)
+            TMEM_LD32(tbase + hi_rows + c0, r);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += __uint_as_float(r[j]);
+          }
         }
         if (a.ssq_in) {
 #pragma unroll
@@ -727,6 +789,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         if (a.epi == EPI_SWIGLU) {
           // rows 64..127 (quarters 2,3) hold `up`, rows 0..63 hold `gate`
           act_t* st2 = (act_t*)stg;                   // [32 columns][72] fp16
+          act_t* st2l = st2 + 32 * 72;                // its rounding residuals (split precision)
           named_bar(2, 128);
           if (q >= 2) {
 #pragma unroll
@@ -735,15 +798,23 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           named_bar(2, 128);
           if (q < 2) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) st2[j * 72 + row] = to_act(silu_f(v[j]) * xch[row * 33 + j]);
+            for (int j = 0; j < 32; ++j) {
+              const float f = silu_f(v[j]) * xch[row * 33 + j];
+              const act_t h = to_act(f);
+              st2[j * 72 + row] = h;
+              if (a.out_lo) st2l[j * 72 + row] = to_act(f - __half2float(h));
+            }
           }
           named_bar(2, 128);
           const int f0 = I.tile * 64;
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int idx = et + 128 * i, n = idx >> 3, f8 = (idx & 7) * 8;
-            if (c0 + n < nc)
-              *(uint4*)((act_t*)a.out + (size_t)(n0 + c0 + n) * a.ldo + f0 + f8) = *(const uint4*)(st2 + n * 72 + f8);
+            if (c0 + n < nc) {
+              const size_t oo = (size_t)(n0 + c0 + n) * a.ldo + f0 + f8;
+              *(uint4*)((act_t*)a.out + oo) = *(const uint4*)(st2 + n * 72 + f8);
+              if (a.out_lo) *(uint4*)(a.out_lo + oo) = *(const uint4*)(st2l + n * 72 + f8);
+            }
           }
         } else {
 #pragma unroll
@@ -761,9 +832,8 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               val.x += old.x; val.y += old.y; val.z += old.z; val.w += old.w;
               *(float4*)((float*)a.out + o) = val;
               if (a.ssq_out) {   // warp = one column n, lanes = the tile's 128 rows x 4
-                act2_t* xb = (act2_t*)(a.xb_out + (size_t)(n0 + c0 + n) * a.ldxb + mt0 + m4);
-                xb[0] = to_act2(val.x, val.y);
-                xb[1] = to_act2(val.z, val.w);
+                const size_t xo = (size_t)(n0 + c0 + n) * a.ldxb + mt0 + m4;
+                store_act4(a.xb_out + xo, a.xb_lo ? a.xb_lo + xo : nullptr, val);
                 float ss = val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
@@ -841,9 +911,13 @@ int gemm_smem_bytes() { return GEMM_SMEM; }
 
 int gemm_init_attrs() {
   const bool ok =
-      cudaFuncSetAttribute(gemm_tcgen05_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
+      cudaFuncSetAttribute(gemm_tcgen05_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
           cudaSuccess &&
-      cudaFuncSetAttribute(gemm_tcgen05_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
+      cudaFuncSetAttribute(gemm_tcgen05_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
+          cudaSuccess &&
+      cudaFuncSetAttribute(gemm_tcgen05_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
+          cudaSuccess &&
+      cudaFuncSetAttribute(gemm_tcgen05_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
           cudaSuccess;
   return ok ? 0 : -1;
 }
@@ -885,11 +959,13 @@ int gemm_coop_min() {
 void gemm_launch(const GemmPlan& p, const GemmArgs& a0, int grid, cudaStream_t st) {
   static const bool pair = getenv("RP_GEMM_PAIR") != nullptr;
   GemmArgs a = a0;
+  a.a_tiled = p.a_tiled;
+  a.lo = a0.lo && p.has_lo;
   // no_spin (single-GPU local groups): every split-K tile is reduced by its
   // last CTA (ticket), never by CTAs waiting for each other, because other
   // contexts' kernels may hold the SMs the waited-for splits need
   a.coop_min = a0.no_spin ? 0x7FFFFFFF : gemm_coop_min();
-  if (pair && a.splits == 1 && a.M % (2 * BM) == 0 && !a.timeline && grid % 2 == 0) {
+  if (pair && !a.lo && a.splits == 1 && a.M % (2 * BM) == 0 && !a.timeline && grid % 2 == 0) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(GEMM_THREADS);
@@ -902,18 +978,28 @@ void gemm_launch(const GemmPlan& p, const GemmArgs& a0, int grid, cudaStream_t s
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = g_no_pdl ? 1 : 2;
-    cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<2>, p.tmA, p.tmB16, p.tmB64, p.tmB256, a);
+    cudaLaunchKernelEx(&cfg, a.lo ? gemm_tcgen05_kernel<2, 1> : gemm_tcgen05_kernel<2, 0>, p.tmA, p.tmB16, p.tmB64,
+                       p.tmB256, p.tmL16, p.tmL64, p.tmL256, a);
     return;
   }
-  launch_pdl(gemm_tcgen05_kernel<1>, dim3(grid), dim3(GEMM_THREADS), GEMM_SMEM, st, p.tmA, p.tmB16, p.tmB64,
-             p.tmB256, a);
+  launch_pdl(a.lo ? gemm_tcgen05_kernel<1, 1> : gemm_tcgen05_kernel<1, 0>, dim3(grid), dim3(GEMM_THREADS), GEMM_SMEM,
+             st, p.tmA, p.tmB16, p.tmB64, p.tmB256, p.tmL16, p.tmL64, p.tmL256, a);
 }
 
-int make_plan(GemmPlan* p, const void* W, int M, int K, const void* X, int rows_cap) {
-  if (make_tmap_act(&p->tmA, W, M, K, 128)) return -1;
+int make_plan(GemmPlan* p, const void* W, int M, int K, const void* X, int rows_cap, int w_tiled, const void* X_lo) {
+  p->a_tiled = w_tiled;
+  // tiled: the weights are M*K/64 rows of 64 elements, 128 consecutive rows per tile
+  if (w_tiled ? make_tmap_act(&p->tmA, W, (int)((long long)M * K / BK), BK, 128) : make_tmap_act(&p->tmA, W, M, K, 128))
+    return -1;
   if (make_tmap_act(&p->tmB16, X, rows_cap, K, 16)) return -1;
   if (make_tmap_act(&p->tmB64, X, rows_cap, K, 64)) return -1;
   if (make_tmap_act(&p->tmB256, X, rows_cap, K, 256)) return -1;
+  // the split-precision residual of the activations (same layout), or X again when absent
+  p->has_lo = X_lo != nullptr;
+  const void* L = X_lo ? X_lo : X;
+  if (make_tmap_act(&p->tmL16, L, rows_cap, K, 16)) return -1;
+  if (make_tmap_act(&p->tmL64, L, rows_cap, K, 64)) return -1;
+  if (make_tmap_act(&p->tmL256, L, rows_cap, K, 256)) return -1;
   return 0;
 }
 

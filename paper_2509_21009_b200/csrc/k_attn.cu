@@ -103,10 +103,10 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
 // the PV MMA through movmatrix.trans; O^T = V^T P^T keeps head_dim on the rows.
 template <int HD, int CW, int NQT>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
-attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict__ q,
+attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict__ q, const act_t* __restrict__ q_lo,
             const int* __restrict__ page_table, int maxp, const AttnItem* __restrict__ items, const int* n_items_dev,
-            int n_items_host, act_t* __restrict__ out, float* __restrict__ partial, int* __restrict__ tickets,
-            ModelDims m, int layer) {
+            int n_items_host, act_t* __restrict__ out, act_t* __restrict__ out_lo, float* __restrict__ partial,
+            int* __restrict__ tickets, ModelDims m, int layer) {
   using C = AttnCfg<HD, CW, NQT>;
   constexpr int MR = C::MR;
   extern __shared__ uint8_t sm_raw[];
@@ -191,17 +191,21 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
     const AttnItem I = items[it];
     const int nrows = I.n_qtok * g;
     const int p_lo = I.kv_lo / kPage, npg = (I.kv_hi + kPage - 1) / kPage - p_lo;
-    // ---- Q^T B fragments: qb[nq][kk] = {Q[row][kk*16 + 2tr..], Q[row][kk*16 + 8 + 2tr..]}, row = nq*8 + tq
-    uint32_t qb[NQT][HD / 16][2];
+    // ---- Q^T B fragments: qb[nq][kk] = {Q[row][kk*16 + 2tr..], Q[row][kk*16 + 8 + 2tr..]}, row = nq*8 + tq;
+    // ql: the same fragments of q's fp16 rounding residual (split precision: S = K q_hi + K q_lo)
+    uint32_t qb[NQT][HD / 16][2], ql[NQT][HD / 16][2];
 #pragma unroll
     for (int nq = 0; nq < NQT; ++nq) {
       const int r = nq * 8 + tq;
-      const act_t* qr =
-          r < nrows ? q + ((size_t)(I.q_row0 + r / g) * m.H + kvh * g + r % g) * HD : nullptr;
+      const size_t qo = ((size_t)(I.q_row0 + r / g) * m.H + kvh * g + r % g) * HD;
+      const act_t* qr = r < nrows ? q + qo : nullptr;
+      const act_t* qlr = r < nrows && q_lo ? q_lo + qo : nullptr;
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
         qb[nq][kk][0] = qr ? *(const uint32_t*)(qr + kk * 16 + 2 * tr) : 0u;
         qb[nq][kk][1] = qr ? *(const uint32_t*)(qr + kk * 16 + 8 + 2 * tr) : 0u;
+        ql[nq][kk][0] = qlr ? *(const uint32_t*)(qlr + kk * 16 + 2 * tr) : 0u;
+        ql[nq][kk][1] = qlr ? *(const uint32_t*)(qlr + kk * 16 + 8 + 2 * tr) : 0u;
       }
     }
     // this thread's two query columns per n-tile: rows nq*8 + 2tr + e
@@ -245,7 +249,10 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
           uint32_t a[4];
           ldsm_x4(kt + swz(row, ch), a[0], a[1], a[2], a[3]);
 #pragma unroll
-          for (int nq = 0; nq < NQT; ++nq) mma16816(s[mt][nq], a, qb[nq][kk][0], qb[nq][kk][1]);
+          for (int nq = 0; nq < NQT; ++nq) {
+            mma16816(s[mt][nq], a, qb[nq][kk][0], qb[nq][kk][1]);
+            if (q_lo) mma16816(s[mt][nq], a, ql[nq][kk][0], ql[nq][kk][1]);
+          }
         }
       }
       // ---- mask + online softmax per query column (log2 domain)
@@ -357,7 +364,10 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
       }
       const int tok = I.q_row0 + r / g, head = kvh * g + r % g;
       if (I.nsplit == 1) {
-        out[((size_t)tok * m.H + head) * HD + c] = to_act(L > 0.f ? O / L : 0.f);
+        const float v = L > 0.f ? O / L : 0.f;
+        const act_t hv = to_act(v);
+        out[((size_t)tok * m.H + head) * HD + c] = hv;
+        if (out_lo) out_lo[((size_t)tok * m.H + head) * HD + c] = to_act(v - __half2float(hv));
       } else {
         float* pp = partial + ((size_t)it * m.KV + kvh) * (16 * (HD + 2));
         pp[32 + r * HD + c] = O;
@@ -416,9 +426,8 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
             }
           }
           const int tok = I.q_row0 + r / g, head = kvh * g + r % g;
-          act2_t* o2 = (act2_t*)(out + ((size_t)tok * m.H + head) * HD + c4);
-          o2[0] = to_act2(acc.x, acc.y);
-          o2[1] = to_act2(acc.z, acc.w);
+          const size_t oo = ((size_t)tok * m.H + head) * HD + c4;
+          store_act4(out + oo, out_lo ? out_lo + oo : nullptr, acc);
         }
       }
     }
@@ -477,24 +486,27 @@ int make_kv_map(CUtensorMap* map, const void* pool, size_t n_pages, const ModelD
 
 void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_table, int maxp,
                       const AttnItem* items, const int* n_items_dev, int n_items_host, void* out, float* partial,
-                      int* tickets, const ModelDims& m, int layer, bool decode, cudaStream_t st) {
+                      int* tickets, const ModelDims& m, int layer, bool decode, cudaStream_t st, const void* q_lo,
+                      void* out_lo) {
   const dim3 grid(148);   // one wave, persistent over the flat (item, KV head) units
   const auto* qq = (const act_t*)q;
+  const auto* ql = (const act_t*)q_lo;
   auto* oo = (act_t*)out;
+  auto* ol = (act_t*)out_lo;
   if (m.hd == 128) {
     if (decode)
-      launch_pdl(attn_kernel<128, 6, 1>, grid, dim3(AttnDec128::THREADS), AttnDec128::SMEM, st, kv_map, qq,
-                 page_table, maxp, items, n_items_dev, n_items_host, oo, partial, tickets, m, layer);
+      launch_pdl(attn_kernel<128, 6, 1>, grid, dim3(AttnDec128::THREADS), AttnDec128::SMEM, st, kv_map, qq, ql,
+                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer);
     else
-      launch_pdl(attn_kernel<128, 3, 2>, grid, dim3(AttnPre128::THREADS), AttnPre128::SMEM, st, kv_map, qq,
-                 page_table, maxp, items, n_items_dev, n_items_host, oo, partial, tickets, m, layer);
+      launch_pdl(attn_kernel<128, 3, 2>, grid, dim3(AttnPre128::THREADS), AttnPre128::SMEM, st, kv_map, qq, ql,
+                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer);
   } else {
     if (decode)
-      launch_pdl(attn_kernel<64, 6, 1>, grid, dim3(AttnDec64::THREADS), AttnDec64::SMEM, st, kv_map, qq, page_table,
-                 maxp, items, n_items_dev, n_items_host, oo, partial, tickets, m, layer);
+      launch_pdl(attn_kernel<64, 6, 1>, grid, dim3(AttnDec64::THREADS), AttnDec64::SMEM, st, kv_map, qq, ql,
+                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer);
     else
-      launch_pdl(attn_kernel<64, 3, 2>, grid, dim3(AttnPre64::THREADS), AttnPre64::SMEM, st, kv_map, qq, page_table,
-                 maxp, items, n_items_dev, n_items_host, oo, partial, tickets, m, layer);
+      launch_pdl(attn_kernel<64, 3, 2>, grid, dim3(AttnPre64::THREADS), AttnPre64::SMEM, st, kv_map, qq, ql,
+                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer);
   }
 }
 

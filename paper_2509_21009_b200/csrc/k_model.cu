@@ -10,13 +10,22 @@ namespace rp {
 // ------------------------------------------------------------- weight formula
 // Generates the [rows, cols] block whose element (r, c) is element
 // (r0 + r, c0 + c) of the logical [*, in_full] tensor `tid` (TP shards are
-// blocks of the full tensor).  mode 0: 16-bit out[r][c]; mode 1: fp32
-// out[r][c] (biases, exact widening of the bf16 value); mode 2: gate/up rows
-// interleaved in 64-row blocks of a [2*rows, cols] tensor (`up` selects the
-// second half of each 128-row block).  The value is the bf16 of the formula;
-// `f16` stores it as fp16 (GEMM operands, reading Z20), else as bf16.
+// blocks of the full tensor), into rows dst_row0 + r of the destination
+// matrix (`cols` columns).  mode 0: 16-bit values; mode 1: fp32 (biases,
+// exact widening of the bf16 value); mode 2: gate/up rows interleaved in
+// 64-row blocks of a [2*rows, cols] tensor (`up` selects the second half of
+// each 128-row block).  The value is the bf16 of the formula; `f16` stores it
+// as fp16 (GEMM operands, reading Z20), else as bf16.  tiled != 0 stores the
+// destination in 128 x 64 blocks, block (R / 128, C / 64) at ((R / 128) *
+// cols / 64 + C / 64) * 8192 elements, row-major inside (weight_tiled_index):
+// every TMA box of the GEMM is then one contiguous 16 KB read.
+__host__ __device__ __forceinline__ long long weight_tiled_index(long long R, long long C, long long cols) {
+  return ((R >> 7) * (cols >> 6) + (C >> 6)) * 8192 + (R & 127) * 64 + (C & 63);
+}
+
 __global__ void init_weights_kernel(void* out, long long rows, int cols, long long r0, int c0, int in_full,
-                                    uint32_t tid, uint32_t k0, uint32_t k1, int mode, int up, int f16) {
+                                    uint32_t tid, uint32_t k0, uint32_t k1, int mode, int up, int f16,
+                                    long long dst_row0, int tiled) {
   const float a = 0.034641016151377546f;   // fl32(0.02 * sqrt(3))
   const long long n = rows * cols;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
@@ -27,25 +36,24 @@ __global__ void init_weights_kernel(void* out, long long rows, int cols, long lo
         __fsub_rn(__fmul_rn(__fadd_rn(__uint2float_rn(u4_word(x, (int)(i & 3)) >> 9), 0.5f), 2.384185791015625e-07f),
                   1.0f);
     const __nv_bfloat16 v = __float2bfloat16_rn(__fmul_rn(a, u2m1));
-    long long o = e;
     if (mode == 1) {
       ((float*)out)[e] = __bfloat162float(v);
       continue;
-    } else if (mode == 2) {
-      o = ((r / 64) * 128 + (r % 64) + (up ? 64 : 0)) * cols + c;
     }
+    const long long R = dst_row0 + (mode == 2 ? (r / 64) * 128 + (r % 64) + (up ? 64 : 0) : r);
+    const long long o = tiled ? weight_tiled_index(R, c, cols) : R * cols + c;
     if (f16) ((__half*)out)[o] = __float2half_rn(__bfloat162float(v));
     else ((__nv_bfloat16*)out)[o] = v;
   }
 }
 
 void launch_init_weights(void* out, long long rows, int cols, long long r0, int c0, int in_full, uint32_t tid,
-                         uint64_t seed, int mode, int up, cudaStream_t st, int f16) {
+                         uint64_t seed, int mode, int up, cudaStream_t st, int f16, long long dst_row0, int tiled) {
   const long long n = rows * cols;
   long long blocks = (n + 255) / 256;
   int grid = (int)(blocks < 148 * 64 ? blocks : 148 * 64);
   init_weights_kernel<<<grid, 256, 0, st>>>(out, rows, cols, r0, c0, in_full, tid, (uint32_t)seed,
-                                            (uint32_t)(seed >> 32), mode, up, f16);
+                                            (uint32_t)(seed >> 32), mode, up, f16, dst_row0, tiled);
 }
 
 // Row kernels: one wave of 148 CTAs for device-side (decode) row counts; up
@@ -81,7 +89,7 @@ void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb,
 // x[r] += delta[r] first (the all-reduced partial of a row-parallel GEMM) and
 // the updated row is written back.
 __global__ void rmsnorm_kernel(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
-                               const float* gamma, act_t* h, int d, float eps) {
+                               const float* gamma, act_t* h, act_t* h_lo, int d, float eps) {
   __shared__ float red[32];
   pdl_wait();
   pdl_launch_dependents();
@@ -116,20 +124,21 @@ __global__ void rmsnorm_kernel(float* x, const float* delta, const int* gather, 
     __syncthreads();
     const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
     __syncthreads();
-    act2_t* hr = (act2_t*)(h + (size_t)r * d);
+    act_t* hr = h + (size_t)r * d;
+    act_t* hl = h_lo ? h_lo + (size_t)r * d : nullptr;
     const float4* g4 = (const float4*)gamma;
     for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
       const float4 v = xr[c], g = g4 ? g4[c] : make_float4(1.f, 1.f, 1.f, 1.f);
-      hr[2 * c] = to_act2(v.x * inv * g.x, v.y * inv * g.y);
-      hr[2 * c + 1] = to_act2(v.z * inv * g.z, v.w * inv * g.w);
+      store_act4(hr + 4 * c, hl ? hl + 4 * c : nullptr,
+                 make_float4(v.x * inv * g.x, v.y * inv * g.y, v.z * inv * g.z, v.w * inv * g.w));
     }
   }
 }
 
 void launch_rmsnorm(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
-                    const float* gamma, void* h, int d, float eps, cudaStream_t st) {
+                    const float* gamma, void* h, int d, float eps, cudaStream_t st, void* h_lo) {
   launch_pdl(rmsnorm_kernel, dim3(row_grid(n_dev, n_host)), dim3(256), 0, st, x, delta, gather, n_dev, n_host, gamma,
-             (act_t*)h, d, eps);
+             (act_t*)h, (act_t*)h_lo, d, eps);
 }
 
 // --------------------------------------------------- TP add + RMSNorm (peer)
@@ -148,8 +157,8 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 
 __global__ void tp_norm_kernel(float* x, const float* recv, int tp, size_t src_stride,
                                const unsigned long long* flags, unsigned long long* gen, int* done, int m_tiles,
-                               int splits, int coop_min, const int* n_dev, const float* gamma, act_t* h, int d,
-                               float eps) {
+                               int splits, int coop_min, const int* n_dev, const float* gamma, act_t* h,
+                               act_t* h_lo, int d, float eps) {
   __shared__ float red[32];
   __shared__ unsigned long long s_units;
   pdl_wait();
@@ -201,12 +210,13 @@ __global__ void tp_norm_kernel(float* x, const float* recv, int tp, size_t src_s
     __syncthreads();
     const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
     __syncthreads();
-    act2_t* hr = (act2_t*)(h + (size_t)r * d);
+    act_t* hr = h + (size_t)r * d;
+    act_t* hl = h_lo ? h_lo + (size_t)r * d : nullptr;
     const float4* g4 = (const float4*)gamma;
     for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
       const float4 v = xr[c], g = g4 ? g4[c] : make_float4(1.f, 1.f, 1.f, 1.f);
-      hr[2 * c] = to_act2(v.x * inv * g.x, v.y * inv * g.y);
-      hr[2 * c + 1] = to_act2(v.z * inv * g.z, v.w * inv * g.w);
+      store_act4(hr + 4 * c, hl ? hl + 4 * c : nullptr,
+                 make_float4(v.x * inv * g.x, v.y * inv * g.y, v.z * inv * g.z, v.w * inv * g.w));
     }
   }
   // this use of the slot is consumed once every CTA is past its reads
@@ -223,25 +233,28 @@ __global__ void tp_norm_kernel(float* x, const float* recv, int tp, size_t src_s
 void launch_tp_norm(float* x, const float* recv, int tp, size_t src_stride, const unsigned long long* flags,
                     unsigned long long* gen, int* done, int m_tiles, int splits, int coop_min, int max_grid,
                     const int* n_dev, int n_rows_grid, const float* gamma, void* h, int d, float eps,
-                    cudaStream_t st) {
+                    cudaStream_t st, void* h_lo) {
   // max_grid bounds the CTAs that spin on the peers' flags (single-GPU local
   // groups: the peers' GEMMs must find free SMs)
   const int grid = std::min(row_grid(n_dev, n_rows_grid), max_grid > 0 ? max_grid : 1 << 30);
   launch_pdl(tp_norm_kernel, dim3(grid), dim3(256), 0, st, x, recv, tp, src_stride, flags, gen, done, m_tiles, splits,
-             coop_min, n_dev, gamma, (act_t*)h, d, eps);
+             coop_min, n_dev, gamma, (act_t*)h, (act_t*)h_lo, d, eps);
 }
 
 // ------------------------------------------------------ folded norm gains
-__global__ void scale_cols_kernel(__half* w, long long rows, int cols, const float* __restrict__ gamma) {
+__global__ void scale_cols_kernel(__half* w, long long rows, int cols, const float* __restrict__ gamma, int tiled) {
   const long long n = rows * cols;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
-    w[e] = __float2half_rn(__half2float(w[e]) * gamma[e % cols]);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    // column of element e (tiled: block e / 8192 is column block (e / 8192) % (cols / 64))
+    const int c = tiled ? (int)(((e >> 13) % (cols >> 6)) * 64 + (e & 63)) : (int)(e % cols);
+    w[e] = __float2half_rn(__half2float(w[e]) * gamma[c]);
+  }
 }
 
-void launch_scale_cols(void* w, long long rows, int cols, const float* gamma, cudaStream_t st) {
+void launch_scale_cols(void* w, long long rows, int cols, const float* gamma, cudaStream_t st, int tiled) {
   const long long n = rows * cols;
   const int grid = (int)std::min<long long>((n + 255) / 256, 148 * 64);
-  scale_cols_kernel<<<grid, 256, 0, st>>>((__half*)w, rows, cols, gamma);
+  scale_cols_kernel<<<grid, 256, 0, st>>>((__half*)w, rows, cols, gamma, tiled);
 }
 
 // -------------------------------------------------------- RoPE + KV append
@@ -249,7 +262,7 @@ void launch_scale_cols(void* w, long long rows, int cols, const float* gamma, cu
 // Rotate-half RoPE at position row_pos[r] (angle in fp64, then fp32 sincos
 // of the reduced angle), q -> q_out[r][H][hd] fp16, k/v -> KV page (fp16).
 __global__ void rope_append_kernel(const float* qkv, const int* n_dev, int n_host, const int* row_pos,
-                                   const int* row_pt, const int* page_table, int maxp, act_t* q_out,
+                                   const int* row_pt, const int* page_table, int maxp, act_t* q_out, act_t* q_lo,
                                    uint8_t* kv_pool, ModelDims m, int layer, const double* inv_freq) {
   extern __shared__ float cs[];   // [hd/2] cos, [hd/2] sin
   pdl_wait();
@@ -277,8 +290,13 @@ __global__ void rope_append_kernel(const float* qkv, const int* n_dev, int n_hos
       const float x1 = src[i], x2 = src[i + half], c = cs[i], s = cs[half + i];
       const float o1 = x1 * c - x2 * s, o2 = x2 * c + x1 * s;
       if (head < m.H) {
-        act_t* dst = q_out + ((size_t)r * m.H + head) * m.hd;
-        dst[i] = to_act(o1); dst[i + half] = to_act(o2);
+        const size_t qo = ((size_t)r * m.H + head) * m.hd;
+        const act_t h1 = to_act(o1), h2 = to_act(o2);
+        q_out[qo + i] = h1; q_out[qo + i + half] = h2;
+        if (q_lo) {                      // rounding residual (split precision)
+          q_lo[qo + i] = to_act(o1 - __half2float(h1));
+          q_lo[qo + i + half] = to_act(o2 - __half2float(h2));
+        }
       } else {
         const int kh = head - m.H;
         act_t* dst = (act_t*)(pbase + ((size_t)((layer * m.KV + kh) * 2 + 0) * kPage + prow) * m.hd * 2);
@@ -296,9 +314,10 @@ __global__ void rope_append_kernel(const float* qkv, const int* n_dev, int n_hos
 
 void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const int* row_pos, const int* row_pt,
                         const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
-                        const double* inv_freq, cudaStream_t st) {
+                        const double* inv_freq, cudaStream_t st, void* q_lo) {
   launch_pdl(rope_append_kernel, dim3(row_grid(n_dev, n_host)), dim3(256), m.hd * sizeof(float), st, qkv, n_dev,
-             n_host, row_pos, row_pt, page_table, maxp, (act_t*)q_out, (uint8_t*)kv_pool, m, layer, inv_freq);
+             n_host, row_pos, row_pt, page_table, maxp, (act_t*)q_out, (act_t*)q_lo, (uint8_t*)kv_pool, m, layer,
+             inv_freq);
 }
 
 // ------------------------------------------------------------- prompt fork

@@ -83,18 +83,19 @@ struct ModelDims {
 
 // weights
 void launch_init_weights(void* out, long long rows, int cols, long long r0, int c0, int in_full, uint32_t tid,
-                         uint64_t seed, int mode, int up, cudaStream_t st, int f16 = 1);
+                         uint64_t seed, int mode, int up, cudaStream_t st, int f16 = 1, long long dst_row0 = 0,
+                         int tiled = 1);
 // forward pieces (n = n_dev ? *n_dev : n_host)
 void launch_embed(const int* tok, const int* n_dev, int n_host, const void* emb, float* x, int d, cudaStream_t st);
 void launch_rmsnorm(float* x, const float* delta, const int* gather, const int* n_dev, int n_host,
-                    const float* gamma, void* h, int d, float eps, cudaStream_t st);
+                    const float* gamma, void* h, int d, float eps, cudaStream_t st, void* h_lo = nullptr);
 void launch_tp_norm(float* x, const float* recv /* [tp][rows][d] slot base */, int tp, size_t src_stride,
                     const unsigned long long* flags /* [tp] */, unsigned long long* gen, int* done, int m_tiles,
                     int splits, int coop_min, int max_grid, const int* n_dev, int n_rows_grid, const float* gamma,
-                    void* h, int d, float eps, cudaStream_t st);
+                    void* h, int d, float eps, cudaStream_t st, void* h_lo = nullptr);
 // w[m][k] *= gamma[k] for an fp16 [rows, cols] weight (an RMSNorm gain folded
 // into the GEMM that consumes the normalised activations)
-void launch_scale_cols(void* w, long long rows, int cols, const float* gamma, cudaStream_t st);
+void launch_scale_cols(void* w, long long rows, int cols, const float* gamma, cudaStream_t st, int tiled = 1);
 
 // Device-memory collectives of a single-GPU local group (several contexts of
 // one process on one device): rank `me` of a group of
@@ -109,12 +110,13 @@ void launch_local_reduce(int op, void* dst, size_t bytes, const uint8_t* slots, 
                          const unsigned long long* gen, const int* state, cudaStream_t st);
 void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const int* row_pos, const int* row_pt,
                         const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
-                        const double* inv_freq, cudaStream_t st);
+                        const double* inv_freq, cudaStream_t st, void* q_lo = nullptr);
 int make_kv_map(CUtensorMap* map, const void* pool, size_t n_pages, const ModelDims& m);
 void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_table, int maxp,
                       const AttnItem* items, const int* n_items_dev, int n_items_host, void* out, float* partial,
                       int* tickets /* [items x KV], zero, self-resetting */, const ModelDims& m, int layer,
-                      bool decode /* <= 8 query rows per unit */, cudaStream_t st);
+                      bool decode /* <= 8 query rows per unit */, cudaStream_t st, const void* q_lo = nullptr,
+                      void* out_lo = nullptr);
 void launch_kv_fork(const int* jobs /*[n][3] src,dst,rows*/, int n, void* kv_pool, const ModelDims& m,
                     cudaStream_t st);
 void launch_sampler(const float* logits, int V, int v0, int row_div, const RoundDev& R, uint64_t seed,

@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librollpacker.so")
+# RP_LIB: load another build of the same ABI (A/B measurements of two builds in one box)
+LIB_PATH = os.environ.get("RP_LIB") or os.path.join(_HERE, "librollpacker.so")
 
 RP_OK, RP_EINVAL, RP_EBUSY, RP_ESTATE, RP_ENOMEM_KV, RP_ECUDA, RP_ENCCL, RP_ENOSPC = 0, -1, -2, -3, -4, -5, -6, -7
 RP_SHORT, RP_LONG, RP_TRACE = 0, 1, 4
@@ -92,7 +93,7 @@ def load_library(path=LIB_PATH):
     lib.rp_debug_trace_get.argtypes = [P, ctypes.POINTER(I32), I32]
     lib.rp_debug_last_logits.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(I32), I32,
                                          ctypes.POINTER(I32)]
-    lib.rp_debug_gemm.argtypes = [P, P, P, I32, P, I32, I32, I32, I32, I32, ctypes.POINTER(ctypes.c_float)]
+    lib.rp_debug_gemm.argtypes = [P, P, P, I32, P, I32, I32, I32, I32, I32, I32, ctypes.POINTER(ctypes.c_float)]
     lib.rp_debug_profile.argtypes = [P, I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64),
                                      ctypes.POINTER(I64)]
     lib.rp_nccl_unique_id.argtypes = [P]
@@ -428,14 +429,22 @@ class Engine:
                     launches={k: int(cnt[i]) for i, k in enumerate(self.PROF_NAMES)},
                     rows=int(rcs[0]), ctx=int(rcs[1]), steps=int(rcs[2]))
 
-    def debug_gemm(self, W, X, N, splits=0, iters=1, timed=False):
+    def debug_gemm(self, W, X, N, splits=0, iters=1, timed=False, tiled=False, X_lo=None):
         """W: torch fp16 [M, K] cuda, X: torch fp16 [rows_cap, K] cuda -> Y fp32 [N, M]
-        (and the mean ms per launch when timed)."""
+        (and the mean ms per launch when timed).  tiled=True hands W to the
+        kernel in the 128 x 64 tiled layout the model's weights use (the
+        rearrangement is argument marshalling: the same values).  X_lo: the
+        fp16 rounding residuals of X (split precision): Y = W (X + X_lo)^T."""
         torch = self.torch
         M, K = W.shape
+        flags = (1 if tiled else 0) | (2 if X_lo is not None else 0)
+        if X_lo is not None:
+            X = torch.cat([X, X_lo]).contiguous()
+        if tiled:
+            W = W.reshape(M // 128, 128, K // 64, 64).permute(0, 2, 1, 3).contiguous()
         Y = torch.zeros((max(N, 1), M), dtype=torch.float32, device=W.device)
         torch.cuda.synchronize()
         ms = ctypes.c_float()
-        self._check(self.L.rp_debug_gemm(self.h, W.data_ptr(), X.data_ptr(), X.shape[0], Y.data_ptr(), M, N, K,
-                                         splits, iters, ctypes.byref(ms)))
+        self._check(self.L.rp_debug_gemm(self.h, W.data_ptr(), X.data_ptr(), X.shape[0] // (2 if X_lo is not None else 1),
+                                         Y.data_ptr(), M, N, K, splits, iters, flags, ctypes.byref(ms)))
         return (Y[:N], ms.value) if timed else Y[:N]

@@ -4,6 +4,11 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# Single-GPU local groups (tests/test_gpu_local.py) run up to 8 contexts on
+# their own streams with device-side waits between them: every stream needs
+# its own hardware queue, or a waiting kernel would block the streams queued
+# behind it.  Must be set before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

@@ -50,11 +50,35 @@ def test_gemm_tcgen05_vs_fp32(torch, tiny, M, K, N):
     W = (torch.randn(M, K, device="cuda", generator=g) * 0.05).to(torch.float16)
     X = (torch.randn(max(N, 1) + 40, K, device="cuda", generator=g)).to(torch.float16)
     ref = X[:N].float() @ W.float().T
-    for splits in (1, 3):
-        Y = eng.debug_gemm(W, X, N, splits=splits)
+    for splits, tiled in ((1, False), (3, False), (1, True), (3, True)):
+        Y = eng.debug_gemm(W, X, N, splits=splits, tiled=tiled)
         torch.cuda.synchronize()
         err = (Y - ref).abs().max().item() if N else 0.0
-        assert err <= 1e-3 * max(1.0, ref.abs().max().item()), (splits, err)
+        assert err <= 1e-3 * max(1.0, ref.abs().max().item()), (splits, tiled, err)
+
+
+@pytest.mark.parametrize("M,K", [(256, 1024), (4608, 3584), (1024, 18944)])
+@pytest.mark.parametrize("N", [1, 16, 50, 100, 128, 129, 256, 300])
+def test_gemm_split_precision_vs_fp64(torch, tiny, M, K, N):
+    """Split-precision activations (reading Z22): with X = X_hi + X_lo (fp16
+    values and their fp16 rounding residuals) the GEMM equals W X^T for the
+    fp32 X to ~2^-20 relative -- the fp16-only product misses it by ~2^-12 --
+    at chunk widths 1..300 (128-column chunks, hi and lo rows in one MMA),
+    with and without split-K."""
+    eng = _shared_engine(tiny)
+    g = torch.Generator(device="cuda").manual_seed(M + K + N)
+    W = (torch.randn(M, K, device="cuda", generator=g) * 0.02).to(torch.float16)
+    X32 = torch.randn(max(N, 1) + 8, K, device="cuda", generator=g)
+    Xh = X32.to(torch.float16)
+    Xl = (X32 - Xh.float()).to(torch.float16)
+    ref = (X32[:N].double() @ W.double().T)
+    scale = (X32[:N].double().abs() @ W.double().abs().T).max().item()
+    for splits, tiled in ((1, True), (4, True), (1, False)):
+        Y = eng.debug_gemm(W, Xh, N, splits=splits, tiled=tiled, X_lo=Xl).double()
+        err = (Y - ref).abs().max().item() / scale
+        Y0 = eng.debug_gemm(W, Xh, N, splits=splits, tiled=tiled).double()
+        err0 = (Y0 - ref).abs().max().item() / scale
+        assert err <= 2e-6 and err < err0 / 20, (splits, tiled, err, err0)
 
 
 _ENG = {}

@@ -1,4 +1,4 @@
-"""Evidence for DESIGN.md reading Z20 (run by hand, ~10 min of CPU):
+"""Which fp16 rounding points of the decode path matter at full depth (run by hand, ~15 min of CPU):
 
     python tests/emulate_activation_precision.py
 
@@ -35,7 +35,7 @@ def layer_bf(x, w, pos, R):
     q = decoder.rope(q.reshape(T, H, hd).transpose(1, 0, 2), pos, cfg["rope_theta"])
     k = decoder.rope(k.reshape(T, KV, hd).transpose(1, 0, 2), pos, cfg["rope_theta"])
     v = v.reshape(T, KV, hd).transpose(1, 0, 2)
-    q, k, v = R["qkv"](q), R["qkv"](k), R["qkv"](v)
+    q, k, v = R["q"](q), R["k"](k), R["v"](v)
     g = H // KV
     out = np.empty((H, T, hd))
     for h in range(H):
@@ -46,14 +46,18 @@ def layer_bf(x, w, pos, R):
     a = R["a"](out.transpose(1, 0, 2).reshape(T, H * hd))
     x = x + a @ f(w["o"]).T
     r2 = 1.0 / np.sqrt(np.mean(x * x, -1, keepdims=True) + eps)
-    h2 = R["h"](x)
+    h2 = R["h"](x)   # layer norms
     gt = (h2 @ f(w["gate"]).T) * r2; up = (h2 @ f(w["up"]).T) * r2
     mid = R["mid"](decoder.silu(gt) * up)
     return x + mid @ f(w["down"]).T
-pts = ["h", "qkv", "p", "a", "mid"]
-variants = {"all_fp16": {p: f16 for p in pts}}
-for p in pts:
-    R = {q: f16 for q in pts}; R[p] = ident; variants["fp16_exact_" + p] = R
+pts = ["h", "hf", "q", "k", "v", "p", "a", "mid"]     # h: layer-norm outputs (QKV, gate/up inputs); hf: final norm (LM head input)
+def mk(exact):
+    return {p: (ident if p in exact else f16) for p in pts}
+import sys as _sys
+combos = {"all_fp16": [], "q+h+hf+a+mid": ["q", "h", "hf", "a", "mid"], "q+h+a+mid (LM hi only)": ["q", "h", "a", "mid"],
+          "q+h+hf+mid (no a)": ["q", "h", "hf", "mid"], "q+h+hf+a (no mid)": ["q", "h", "hf", "a"],
+          "q+h+hf": ["q", "h", "hf"], "q+hf+a+mid (no h)": ["q", "hf", "a", "mid"], "q+h+a": ["q", "h", "a"]}
+variants = {m: mk(ex) for m, ex in combos.items()}
 w = weights.Weights(cfg, configs.WEIGHT_SEED, use_c=True)
 toks = gen.prompts(1, 0, cfg["eos_id"], (56, 56), 6)[0]["tokens"]
 pos = np.arange(56)
@@ -68,7 +72,7 @@ lm = w.lm_head()
 h64 = decoder.rmsnorm(x64, w.final_norm(), eps)
 for m, R in variants.items():
     r = 1.0 / np.sqrt(np.mean(xs[m]**2, -1, keepdims=True) + eps)
-    hb = R["h"](xs[m]) * r
+    hb = R["hf"](xs[m]) * r
     worst = 0.0
     for v0 in range(0, cfg["vocab"], 16384):
         W = np.asarray(lm[v0:v0+16384], np.float64)
