@@ -55,6 +55,7 @@ extern "C" {
 #define RP_SHORT 0       /* speculative short round: stop at `target` accepted   */
 #define RP_LONG 1        /* long round: target must equal n_prompts, no aborts   */
 #define RP_TRACE 4       /* trace mode: EOS masked before and forced at L (Z15)  */
+#define RP_PREEMPT 8     /* KV pressure: recompute preemption instead of RP_ENOMEM_KV (Z26) */
 
 /* ------------------------------------------------- finish codes (rp_response) */
 #define RP_FINISH_EOS 1  /* ended with EOS (natural or trace-forced)             */
@@ -142,6 +143,7 @@ typedef struct {
   int64_t decoded_tokens;    /* tokens decoded on this rank this round (incl. aborted) */
   int64_t kv_tokens_read;    /* sum over decode steps and decoded rows of the attention context
                                 (KV tokens read per layer and KV head); measurement only   */
+  int32_t preemptions;       /* prompts preempted by KV pressure this round on this rank */
 } rp_status;
 
 typedef struct {
@@ -187,7 +189,17 @@ int rp_plan_round(void* ctx, int32_t P0, float eta, int32_t drain, int32_t* kind
  * ones are collected.  RP_LONG requires keep == G (speculation disabled,
  * P:124).  cap: length cap of every response (>= 1).
  * target: prompts to accept (P0), 1 <= target <= n_prompts; RP_LONG requires
- * target == n_prompts.  flags: RP_SHORT|RP_LONG [|RP_TRACE].  round_id seeds
+ * target == n_prompts.  flags: RP_SHORT|RP_LONG [|RP_TRACE] [|RP_PREEMPT].
+ * RP_PREEMPT (reading Z26): when the next
+ * step's KV pages exceed the free pages, the most recently admitted prompt
+ * with a live response (never the last one) is preempted -- its responses'
+ * private pages freed -- and waits in a FIFO; a step that preempts nothing
+ * re-admits waiting prompts while they fit, and the library recomputes
+ * their KV (prefill kernels over the response's own tokens) before the next
+ * step, which continues them at their next token.  The schedule is exact
+ * (oracle sched.kv_step_loop); rp_status.preemptions counts the victims.
+ * Not combinable with continuous issuance.  Without it, exhaustion is
+ * RP_ENOMEM_KV.  round_id seeds
  * the sampler counter (reading Z5: re-rolls draw fresh noise).  Runs the
  * prefill and decode step 1 (the token sampled from the prefill logits).
  * Errors: RP_EINVAL, RP_EBUSY (round active), RP_ENOMEM_KV, RP_ENOSPC. */

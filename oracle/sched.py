@@ -500,3 +500,227 @@ def simulate(trace, n_rounds, P0, eta, G, short_cap, long_cap, tail_batching=Tru
             queue.extend(ids[i] for i in r.deferred)
         out.append(dict(kind=kind, ids=ids, round=r, queue_after=list(queue)))
     return out
+
+
+# ------------------------------------------ KV pressure (NEXT-2)
+#
+# short rounds raise memory pressure and serving engines "alleviate
+# memory pressure by preempting ongoing requests"; the planner
+# "keeps track of the preemption counts and adapts the TP sizes ... a sudden
+# rise in preemptions (e.g., >1.05x) triggers an increase in TP (doubling the
+# size), while sustained zero preemptions across four steps trigger a
+# decrease (halving the size)".  Readings (Z26):
+#   * the KV pool holds n_pages pages of PAGE tokens; a prompt of plen tokens
+#     holds ceil(plen / PAGE) prompt pages for the whole round (its G
+#     responses share the floor(plen / PAGE) full ones) and each response a
+#     private copy of the partial last prompt page, then private pages for
+#     its generated tokens; a response that generated g tokens has written
+#     kv = plen + g - 1 positions (token g is its next input) and holds
+#     ceil(kv / PAGE) - floor(plen / PAGE) private pages;
+#   * after the step's endings free their pages, the survivors need one page
+#     each whose kv is a multiple of PAGE; while that exceeds the free pages
+#     the most recently admitted prompt with a live response is preempted
+#     (LIFO, whole prompt: all its live responses, their private pages
+#     freed) and joins the back of a FIFO wait queue -- never the last live
+#     prompt: if it alone does not fit, the pool is exhausted;
+#   * preemption is by recompute: a step that preempts nothing re-admits
+#     wait-queue prompts from the head while their pages fit --
+#     sum over their preempted responses of ceil((plen + g) / PAGE) -
+#     floor(plen / PAGE) (the recomputed prefix and the next append) -- after
+#     the survivors' needs; a re-admitted response continues at token g + 1
+#     in the next step (its KV for positions plen .. plen + g - 2 recomputed
+#     between the two steps) and its prompt becomes the most recent admission;
+#   * the next step's rows: the survivors in their order, then the
+#     re-admitted responses (re-admission order, j ascending);
+#   * a round whose live set is empty ends (plain rule) unless re-admission
+#     refills it; no live row and a wait-queue head that does not fit, or a
+#     single live prompt that does not fit, is KV exhaustion.
+
+PAGE = 64
+PREEMPTED = 5
+
+
+class KVExhausted(Exception):
+    pass
+
+
+def _pages(x):
+    return -(-int(x) // PAGE)
+
+
+class KVRank:
+    """One rank's round state under KV pressure (the per-rank part of
+    `kv_step_loop`; the DP cutoff couples ranks only through `done`)."""
+
+    def __init__(self, L, plen, cap, kind, n_pages, keep, first_prompt=0):
+        self.L = np.asarray(L, np.int64)
+        self.n, self.G = self.L.shape
+        self.plen = [int(x) for x in plen]
+        self.cap, self.kind, self.keep = cap, kind, keep
+        self.own0 = [p // PAGE for p in self.plen]
+        used = sum(_pages(p) for p in self.plen) + sum(self.G * (p % PAGE != 0) for p in self.plen)
+        if used > n_pages:
+            raise KVExhausted("prompt pages do not fit at submit")
+        self.free = n_pages - used
+        self.g = np.zeros((self.n, self.G), np.int64)
+        self.kv = np.array([[p] * self.G for p in self.plen], np.int64)
+        self.status = np.zeros((self.n, self.G), np.int32)           # 0 live / FINISHED / CAPPED / ABORTED / PREEMPTED
+        self.kept = np.zeros((self.n, self.G), bool)
+        self.cnt = [0] * self.n
+        self.done_p = [False] * self.n
+        self.adm = list(range(self.n))                                # admission order (oldest first)
+        self.wait = []                                                # FIFO of preempted prompts
+        self.live = [i * self.G + j for i in range(self.n) for j in range(self.G)]
+        self.preemptions = 0
+        self.first = first_prompt
+
+    def step(self, t):
+        """Decode step t on this rank.  Returns (decoded slots, prompts
+        completed at t (local indices, ascending))."""
+        G = self.G
+        decoded = list(self.live)
+        ending, completed = [], []
+        for s in decoded:
+            i, j = divmod(s, G)
+            self.g[i, j] += 1
+            if t >= 2:
+                self.kv[i, j] += 1                     # the input token's KV was appended
+            k = self.g[i, j]
+            if k == self.L[i, j]:
+                self.status[i, j] = FINISHED
+                ending.append(s)
+                if not self.done_p[i] and self.cnt[i] < self.keep:
+                    self.cnt[i] += 1
+                    self.kept[i, j] = True
+                    if self.cnt[i] == self.keep:
+                        completed.append(i)
+            elif k == self.cap:
+                self.status[i, j] = CAPPED
+                ending.append(s)
+                if self.kind == LONG:
+                    self.cnt[i] += 1
+                    self.kept[i, j] = True
+                    if self.cnt[i] == G:
+                        completed.append(i)
+        for i in completed:
+            self.done_p[i] = True
+        ended = set(ending)
+        for s in decoded:
+            if s not in ended and self.done_p[s // G]:
+                self.status[s // G, s % G] = ABORTED
+                ended.add(s)
+        for s in ended:
+            i, j = divmod(s, G)
+            self.free += _pages(self.kv[i, j]) - self.own0[i]
+        self.survivors = [s for s in decoded if s not in ended]
+        return decoded, sorted(completed)
+
+    def pressure(self):
+        """Preemption (LIFO whole prompts) until the survivors' next-step
+        pages fit, then (if nothing was preempted) re-admission from the head
+        of the wait queue.  Sets the next step's live list."""
+        G = self.G
+        need = lambda rows: sum(1 for s in rows if self.kv[s // G, s % G] % PAGE == 0)
+        rows = list(self.survivors)
+        preempted = False
+        while need(rows) > self.free:
+            live_p = set(s // G for s in rows)
+            if len(live_p) <= 1:
+                raise KVExhausted("the last live prompt does not fit")
+            v = max(live_p, key=lambda i: self.adm.index(i))
+            for s in [s for s in rows if s // G == v]:
+                j = s % G
+                self.free += _pages(self.kv[v, j]) - self.own0[v]
+                self.status[v, j] = PREEMPTED
+            rows = [s for s in rows if s // G != v]
+            self.wait.append(v)
+            self.preemptions += 1
+            preempted = True
+        avail = self.free - need(rows)
+        self.free = avail
+        if not preempted:
+            while self.wait:
+                v = self.wait[0]
+                js = [j for j in range(G) if self.status[v, j] == PREEMPTED]
+                req = sum(_pages(self.plen[v] + self.g[v, j]) - self.own0[v] for j in js)
+                if req > self.free:
+                    break
+                self.wait.pop(0)
+                self.free -= req
+                for j in js:
+                    self.status[v, j] = 0
+                    self.kv[v, j] = self.plen[v] + self.g[v, j] - 1
+                    rows.append(v * G + j)
+                self.adm.remove(v)
+                self.adm.append(v)
+        if not rows and self.wait:
+            v = self.wait[0]
+            req = sum(_pages(self.plen[v] + self.g[v, j]) - self.own0[v] for j in range(G)
+                      if self.status[v, j] == PREEMPTED)
+            if req > self.free:
+                raise KVExhausted("the wait-queue head can never fit")
+        self.live = rows
+
+
+def kv_step_loop(L, plen, cap, target, kind, n_pages, world=1, with_steps=False, keep=None):
+    """Literal step loop of a round under KV pressure (readings above),
+    sharded over `world` DP ranks (contiguous prompt ranges, `n_pages` pages
+    per rank) with the per-step cutoff exchange of `dp_protocol`.  With
+    enough pages it is `step_loop` / `dp_protocol` (a test).  Returns a Round
+    whose steps carry each rank's decoded slots (local), plus `preemptions`
+    (per rank) and `order` (each rank's final admission order)."""
+    L = np.asarray(L, np.int64)
+    n, G = L.shape
+    keep = G if (keep is None or kind == LONG) else keep
+    if kind == LONG:
+        target = n
+    parts = partition(n, world)
+    ranks = [KVRank(L[lo:hi], plen[lo:hi], cap, kind, n_pages, keep, lo) for lo, hi in parts]
+    accepted, steps = [], []
+    t = 0
+    while True:
+        t += 1
+        dec, comps = [], []
+        for r in ranks:
+            d, c = r.step(t)
+            dec.append(d)
+            comps.append(c)
+        before = len(accepted)
+        for (lo, hi), c in zip(parts, comps):          # rank order = prompt-index order
+            take = min(len(c), max(0, target - len(accepted)))
+            accepted.extend(lo + i for i in c[:take])
+        for r in ranks:
+            r.pressure()
+        done = len(accepted) >= target or all(not r.live for r in ranks)
+        if with_steps:
+            steps.append(dict(t=t, live=[np.array(d, np.int32) for d in dec], accepted=len(accepted),
+                              done=int(done)))
+        if done:
+            break
+    outcome = np.zeros((n, G), np.int32)
+    retained = np.zeros((n, G), np.int64)
+    acc = set(accepted)
+    for (lo, hi), r in zip(parts, ranks):
+        st = r.status.copy()
+        st[(st == 0) | (st == PREEMPTED)] = ABORTED
+        outcome[lo:hi] = st
+        for i in range(lo, hi):
+            if i in acc:
+                retained[i] = np.where(r.kept[i - lo], np.minimum(L[i], cap), 0)
+    deferred = [i for i in range(n) if i not in accepted]
+    rnd = Round(kind, t, accepted, deferred, len(accepted) < target, outcome, retained, steps)
+    rnd.preemptions = [r.preemptions for r in ranks]
+    return rnd
+
+
+def plan_tp(tp, tp_max, prev_preemptions, preemptions, zero_streak):
+    """The parallelism planner's heuristic: a sudden rise in
+    preemptions (> 1.05x the previous round of the same kind) doubles the TP
+    size (up to the GPUs of one server, tp_max); four consecutive rounds with
+    zero preemptions halve it.  Returns (next tp, next zero streak)."""
+    streak = zero_streak + 1 if preemptions == 0 else 0
+    if preemptions > 0 and preemptions > 1.05 * prev_preemptions:
+        return min(2 * tp, tp_max), 0
+    if streak >= 4:
+        return max(tp // 2, 1), 0
+    return tp, streak

@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <climits>
 #include <condition_variable>
 #include <chrono>
@@ -182,6 +183,7 @@ struct RpCtx {
   int coop_min = 16;          // cooperative split-K from this chunk width (no_spin: never)
   int* memb = nullptr;        // [P + 1] local membership, then [world][P + 1] gathered (rp_collect)
   int* memb_h = nullptr;      // pinned host staging of memb
+  int* rejobs_h = nullptr;    // pinned host copy of the recompute jobs (KV pressure)
 
   // round state (host)
   bool active = false, collected = true;
@@ -283,7 +285,7 @@ static Sizes compute_sizes(const rp_model_desc* md, const rp_runtime_desc* rd) {
   const int hid = lm.H * lm.hd;
   const int shapes[5][2] = {{qkvw, d}, {d, hid}, {2 * F, d}, {d, F}, {lm.V, d}};
   size_t mx = 0;
-  const int nch = (z.S + 127) / 128;   // 128-column chunks of the split-precision GEMMs
+  const int nch = z.S <= 128 ? 1 : (z.S + 255) / 256;   // narrow split-precision chunks: N <= 128
   for (auto& s : shapes) {
     const int sp = gemm_pick_splits(s[0], s[1], kSMs);
     if (sp > 1) mx = std::max(mx, (size_t)(s[0] / 128) * nch * sp * 256 * 128);
@@ -386,6 +388,15 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto best = cv.take<unsigned long long>(std::max(z.S, 1));
   auto ks_local = cv.take<int>(4);
   auto ks = cv.take<int>((size_t)4 * std::max(1, rd->world));
+  // KV pressure (NEXT-2): per-prompt admission / wait state, scratch sums, the wait FIFO, recompute jobs
+  auto p_plen = cv.take<int>(z.P);
+  auto p_adm = cv.take<int>(z.P);
+  auto p_wait = cv.take<int>(z.P);
+  auto p_live = cv.take<int>(z.P);
+  auto p_pfree = cv.take<int>(z.P);
+  auto p_pneed = cv.take<int>(z.P);
+  auto wait_q = cv.take<int>(z.P);
+  auto rejobs = cv.take<int>((size_t)5 * z.S);
   auto memb = cv.take<int>((size_t)(z.P + 1) * (1 + std::max(1, rd->world)));
   auto ctl = cv.take<CtlBlock>(1);
   const size_t page_bytes = lm.page_bytes;
@@ -411,6 +422,8 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
     R.p_state = p_state; R.p_gid = p_gid; R.comp_list = comp_list; R.accept_order = accept_order;
     R.live = live; R.live_next = live_next; R.tok_in = tok_in; R.row_pos = row_pos; R.row_pt = row_pt;
     R.max_items = z.max_items_dec;
+    R.p_plen = p_plen; R.p_adm = p_adm; R.p_wait = p_wait; R.p_live = p_live; R.p_pfree = p_pfree;
+    R.p_pneed = p_pneed; R.wait_q = wait_q; R.rejobs = rejobs;
     R.best = best; R.items = items_dec; R.rows_hist = rows_hist; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
     R.ctl = ctl; R.cap = rd->max_cap;
   }
@@ -676,7 +689,7 @@ static void decode_step(RpCtx* c, int bucket) {
     launch_ctl(R, 1, 0, c->st); c->launches++;
   } else {
     { ProfScope ps(c, RP_PROF_CTL); launch_ctl(R, 1, 1, c->st); c->launches++; }
-    { ProfScope ps(c, RP_PROF_NCCL); coll_allgather_i32(c, c->dp, R.ks_local, R.ks, 3); }
+    { ProfScope ps(c, RP_PROF_NCCL); coll_allgather_i32(c, c->dp, R.ks_local, R.ks, 4); }
     { ProfScope ps(c, RP_PROF_CTL); launch_ctl(R, 1, 2, c->st); c->launches++; }
   }
 }
@@ -892,6 +905,7 @@ static int init_impl(RpCtx* c) {
   }
   CK(cudaMallocHost(&c->h_ctl, sizeof(CtlBlock)));
   if (rd->world > 1) CK(cudaMallocHost(&c->memb_h, (size_t)(c->z.P + 1) * (rd->world + 1) * 4));
+  CK(cudaMallocHost(&c->rejobs_h, (size_t)5 * c->z.S * 4));
   memset(c->h_ctl, 0, sizeof(CtlBlock));
   c->h_ctl->done = 1;
   CK(cudaMemcpyAsync(c->R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
@@ -1014,6 +1028,7 @@ void rp_free(void* ctx) {
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->gate_h) cudaFreeHost((void*)c->gate_h);
   if (c->memb_h) cudaFreeHost(c->memb_h);
+  if (c->rejobs_h) cudaFreeHost(c->rejobs_h);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->trace_dev) cudaFree(c->trace_dev);
   if (c->dp.nccl) ncclCommDestroy(c->dp.nccl);
@@ -1111,6 +1126,9 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   if (c->active) return c->fail(RP_EBUSY, "a round is active (collect it first)");
   const int kind = flags & RP_LONG ? 1 : 0;
   const int trace = flags & RP_TRACE ? 1 : 0;
+  const int preempt = flags & RP_PREEMPT ? 1 : 0;
+  if (preempt && c->issue_cap > 0)
+    return c->fail(RP_EINVAL, "invalid field: flags (RP_PREEMPT with continuous issuance is not supported)");
   if (G < 1) return c->fail(RP_EINVAL, "invalid field: G (>= 1)");
   if (keep == 0) keep = G;
   if (keep < 1 || keep > G) return c->fail(RP_EINVAL, "invalid field: keep (1..G, 0 = G)");
@@ -1185,6 +1203,7 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   RoundDev& R = c->R;
   R.cap = cap; R.G = G; R.keep = keep; R.target = target; R.kind = kind; R.trace = trace; R.n_prompts = n_loc;
   R.max_active = A;
+  R.preempt = preempt;
   const int n_first = A > 0 ? A : n_loc;   // prompts live at step 1
   R.trace_buf = c->trace_dev; R.trace_steps = c->trace_steps;
 
@@ -1237,6 +1256,9 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   }
   if (n_loc > 0) {
     CK(up(R.p_gid, gid, n_loc)); CK(up(R.p_cnt, zeros, n_loc)); CK(up(R.p_state, zeros, n_loc));
+    std::vector<int> ident(n_loc);
+    for (int p = 0; p < n_loc; ++p) ident[p] = p;                  // admission stamps: index order
+    CK(up(R.p_plen, plen, n_loc)); CK(up(R.p_adm, ident, n_loc)); CK(up(R.p_wait, zeros, n_loc));
     CK(up(R.p_last_tok, last_tok, n_loc)); CK(up(R.p_stamp, zeros, n_loc));
   }
   if (!jobs.empty()) {
@@ -1248,6 +1270,7 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   CK(cudaMemsetAsync(R.rows_hist, 0, ((size_t)c->z.S + 1) * sizeof(unsigned long long), c->st));
   CtlBlock cb{};
   cb.n_live = n_first * G; cb.t = 1; cb.free_top = top; cb.n_issued = n_first;
+  cb.adm_ctr = n_loc - 1;
   *c->h_ctl = cb;
   CK(cudaMemcpyAsync(R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
   if (c->trace_dev) CK(cudaMemsetAsync(c->trace_dev, 0, (size_t)c->trace_steps * (2 + S) * 4, c->st));
@@ -1260,7 +1283,7 @@ int rp_submit_round(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
     launch_ctl(R, 0, 0, c->st); c->launches++;
   } else {
     launch_ctl(R, 0, 1, c->st); c->launches++;
-    coll_allgather_i32(c, c->dp, R.ks_local, R.ks, 3);
+    coll_allgather_i32(c, c->dp, R.ks_local, R.ks, 4);
     launch_ctl(R, 0, 2, c->st); c->launches++;
   }
   CK(cudaGetLastError());
@@ -1287,6 +1310,102 @@ static void fill_status(RpCtx* c, rp_status* st) {
   st->accepted = b.acc; st->accepted_local = b.acc_local; st->done = b.done; st->underfilled = b.underfilled;
   st->n_prompts_local = c->n_loc; st->decoded_tokens = b.decoded;
   st->kv_tokens_read = b.kv_read;
+  st->preemptions = b.preemptions;
+}
+
+// Recompute of re-admitted responses (KV pressure, reading Z26), between
+// two decode steps while the round is paused: copy the prompt's partial page
+// into each response's first private page, then run the decoder over the
+// response's tokens 1 .. g-1 at positions plen .. plen + g - 2 (prefill
+// kernels; keys from the response's own page table), writing their KV; no LM
+// head.  Pieces bounded by the prefill buffers.  Then resume the step.
+static int recompute_paused(RpCtx* c) {
+  CtlBlock& b = *c->h_ctl;
+  const int nj = b.n_rejobs;
+  if (nj > 0) {
+    CK(cudaMemcpyAsync(c->rejobs_h, c->R.rejobs, (size_t)5 * nj * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    std::vector<int> jobs;
+    for (int j = 0; j < nj; ++j) {
+      const int* J = c->rejobs_h + 5 * j;
+      if (J[4] > 0) { jobs.push_back(J[2]); jobs.push_back(J[3]); jobs.push_back(J[4]); }
+    }
+    if (!jobs.empty()) {
+      CK(idle(c));
+      CK(cudaMemcpyAsync(c->fork_jobs, jobs.data(), jobs.size() * 4, cudaMemcpyHostToDevice, c->st));
+      launch_kv_fork(c->fork_jobs, (int)jobs.size() / 3, c->rd.kv_pool, c->m, c->st);
+      c->launches++;
+    }
+    // continuation segments (slot, first token index, end) in job order
+    struct Seg { int s, plen, k0, k1; };
+    std::vector<Seg> segs;
+    for (int j = 0; j < nj; ++j) {
+      const int* J = c->rejobs_h + 5 * j;
+      const int s = J[0], g = J[1], plen = (int)c->round_prompts[s / c->G].tokens.size();
+      if (g >= 2) segs.push_back({s, plen, 0, g - 1});
+    }
+    const int g_heads = c->m.H / c->m.KV, tpb = 16 / g_heads;
+    const int tok_cap = c->rd.max_prompt_tokens;
+    size_t si = 0;
+    while (si < segs.size()) {
+      // one piece: whole or partial segments within the token and item capacities
+      std::vector<int> pos, pt;
+      std::vector<AttnItem> items;
+      std::vector<std::array<int, 4>> copies;   // dst offset, slot, k0, count
+      int T = 0;
+      while (si < segs.size() && T < tok_cap) {
+        Seg& sg = segs[si];
+        int take = std::min(sg.k1 - sg.k0, tok_cap - T);
+        // items of these tokens: ceil(nq / tpb) blocks x ceil(keys / chunk) splits each
+        auto n_items_for = [&](int k0, int cnt) {
+          int it = 0;
+          for (int b0 = 0; b0 < cnt; b0 += tpb) {
+            const int hi = sg.plen + k0 + std::min(b0 + tpb, cnt);
+            it += (hi + kAttnChunk - 1) / kAttnChunk;
+          }
+          return it;
+        };
+        while (take > 0 && (int)items.size() + n_items_for(sg.k0, take) > c->z.max_items_pre) take /= 2;
+        if (take <= 0) break;
+        const int off = T;
+        for (int k = 0; k < take; ++k) { pos.push_back(sg.plen + sg.k0 + k); pt.push_back(sg.s); }
+        for (int b0 = 0; b0 < take; b0 += tpb) {
+          const int nq = std::min(tpb, take - b0);
+          const int p0 = sg.plen + sg.k0 + b0, hi = p0 + nq;
+          const int ns = (hi + kAttnChunk - 1) / kAttnChunk, item0 = (int)items.size();
+          for (int sp = 0; sp < ns; ++sp) {
+            AttnItem I;
+            I.q_row0 = off + b0; I.n_qtok = nq; I.pos0 = p0; I.pt_row = sg.s;
+            I.kv_lo = sp * kAttnChunk; I.kv_hi = std::min(hi, (sp + 1) * kAttnChunk);
+            I.nsplit = ns; I.item0 = item0;
+            items.push_back(I);
+          }
+        }
+        copies.push_back({off, sg.s, sg.k0, take});
+        T += take;
+        sg.k0 += take;
+        if (sg.k0 >= sg.k1) ++si;
+      }
+      if (T == 0) return c->fail(RP_ENOSPC, "recompute: prefill buffers too small for one token");
+      CK(idle(c));
+      for (auto& cp : copies)
+        CK(cudaMemcpyAsync(c->pre_tok + cp[0], c->R.tok_out + (size_t)cp[1] * c->rd.max_cap + cp[2],
+                           (size_t)cp[3] * 4, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(c->pre_pos, pos.data(), T * 4, cudaMemcpyHostToDevice, c->st));
+      CK(cudaMemcpyAsync(c->pre_pt, pt.data(), T * 4, cudaMemcpyHostToDevice, c->st));
+      CK(cudaMemcpyAsync(c->items_pre, items.data(), items.size() * sizeof(AttnItem), cudaMemcpyHostToDevice, c->st));
+      bool pending = false;
+      forward_layers(c, c->pre_tok, nullptr, T, c->pre_pos, c->pre_pt, c->items_pre, nullptr, (int)items.size(), false,
+                     T, &pending);
+      CK(cudaGetLastError());
+    }
+  }
+  // resume the held step
+  b.pause = 0;
+  b.n_live = b.n_live_saved;
+  b.n_items = b.n_items_saved;
+  CK(cudaMemcpyAsync(c->R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
+  return RP_OK;
 }
 
 int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
@@ -1298,6 +1417,10 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
   if (rc) return rc;
   int steps = 0;
   while (!c->h_ctl->done && steps < max_steps) {
+    if (c->h_ctl->pause) {                 // re-admitted responses wait for their KV
+      if ((rc = recompute_paused(c))) return rc;
+      continue;
+    }
     // rows can grow inside a graph of graph_steps steps when prompts are issued
     const int grow = c->max_active ? std::min(c->max_active * c->G, c->h_ctl->n_live +
                                               (c->n_loc - c->h_ctl->n_issued) * c->G) : 0;
@@ -1680,7 +1803,8 @@ int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, flo
   if (M % 128 || K % 64 || M <= 0 || K <= 0 || N < 0 || N > rows_cap) return c->fail(RP_EINVAL, "invalid GEMM shape");
   if (splits <= 0) splits = gemm_pick_splits(M, K, kSMs);
   splits = std::min(splits, K / 64);
-  const size_t need = (size_t)(M / 128) * ((N + 127) / 128) * splits * 256 * 128;   // 128-column chunks when LO
+  const int chunk = (w_tiled & 2) && N <= 128 ? 128 : 256;   // narrow split-precision chunks are 128 wide
+  const size_t need = (size_t)(M / 128) * ((N + chunk - 1) / chunk) * splits * 256 * 128;
   if (splits > 1 && need > c->z.part_floats) return c->fail(RP_ENOSPC, "split-K workspace too small");
   if ((M / 128) * ((N + 255) / 256) > (1 << 15)) return c->fail(RP_ENOSPC, "too many tiles");
   GemmPlan p;

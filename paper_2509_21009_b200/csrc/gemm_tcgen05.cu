@@ -265,10 +265,15 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int n_ctas = CG == 2 ? (int)gridDim.x / 2 : (int)gridDim.x;
   const bool leader = crank == 0;
   const int m_tiles = a.M / (BM * CG);
-  // LO: 128-column chunks -- the MMA's N holds the chunk's hi rows and then
-  // its lo rows (at most 128 + 128), so a row's hi and lo products come out
-  // of one MMA (the weight tile is read from shared memory once per K step)
-  constexpr int BNX = LO ? 128 : BN;
+  // LO, N <= 128 (narrow): one chunk whose hi rows and then lo rows form the
+  // MMA's N, so a row's hi and lo products come out of one MMA (the weight
+  // tile is read from shared memory once per K step).  LO, N > 128 (wide):
+  // 256-column chunks, the hi rows and the lo rows multiplied by two MMAs into
+  // two TMEM accumulators (columns [0, 256) and [256, 512): no double
+  // buffering) -- per element the same two fp32 sums as the narrow form, so
+  // the result does not depend on the batch size.
+  const bool wide = LO && N > 128;
+  const int BNX = (LO && !wide) ? 128 : BN;
   const int n_chunks = (N + BNX - 1) / BNX;
   const int n_items = m_tiles * n_chunks * a.splits;
   if (cta_id >= n_items) return;                   // both CTAs of a pair leave together
@@ -347,7 +352,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       int stage = 0; uint32_t phase = 0;
       bool first = true;
       for (int it = cta_id; it < n_items; it += n_ctas) {
-        Item I = decode_item(it, m_tiles, a.splits, n_chunks, LO);
+        Item I = decode_item(it, m_tiles, a.splits, n_chunks, LO && !wide);
         const int kb0 = (int)((long)I.split * kb_total / a.splits), kb1 = (int)((long)(I.split + 1) * kb_total / a.splits);
         const int wrow = (I.tile * CG + (int)crank) * BM;   // this CTA's 128 weight rows
         // A box coordinates of k-block kb: (kb * 64, wrow) row-major, or the
@@ -438,32 +443,51 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       // ===== MMA issuer (single thread; the pair's leader for CG = 2) =====
       int stage = 0; uint32_t phase = 0; int local = 0;
       for (int it = cta_id; it < n_items; it += n_ctas, ++local) {
-        Item I = decode_item(it, m_tiles, a.splits, n_chunks, LO);
+        Item I = decode_item(it, m_tiles, a.splits, n_chunks, LO && !wide);
         const int kb0 = (int)((long)I.split * kb_total / a.splits), kb1 = (int)((long)(I.split + 1) * kb_total / a.splits);
         const int nc = min(BNX, N - I.chunk * BNX);
-        // LO: N = the hi rows (whole boxes) + the 16-padded lo rows
-        const int hi_rows = nc > 48 ? ((nc + 63) & ~63) : ((nc + 15) & ~15);
-        const int nmma = LO ? hi_rows + ((nc + 15) & ~15) : (nc + 15) & ~15;
+        // narrow LO: N = the hi rows (whole boxes) + the 16-padded lo rows
+        const int hi_rows = nc > 192 ? 256 : nc > 48 ? ((nc + 63) & ~63) : ((nc + 15) & ~15);
+        const int nmma = (LO && !wide) ? hi_rows + ((nc + 15) & ~15) : (nc + 15) & ~15;
         const uint32_t idesc = make_idesc(nmma, BM * CG);
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
+        // wide LO: one accumulator pair (all 512 columns), phases alternate per item
+        const int acc = wide ? 0 : (local & 1);
+        const uint32_t acc_phase = wide ? (local & 1) : ((local >> 1) & 1);
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(full0 + 8 * stage, phase);
-          if (kb == kb0 && local < 3) TL(2 + 2 * local);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-          const uint64_t da = make_sdesc(sa), db = make_sdesc(sa + A_BYTES);
+        if (!wide) {
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(full0 + 8 * stage, phase);
+            if (kb == kb0 && local < 3) TL(2 + 2 * local);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+            const uint64_t da = make_sdesc(sa), db = make_sdesc(sa + A_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {  // +32 B along K per UMMA_K=16 step
-            if (CG == 2) umma_f16_pair(tmem_d, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-            else umma_f16(tmem_d, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {  // +32 B along K per UMMA_K=16 step
+              if (CG == 2) umma_f16_pair(tmem_d, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              else umma_f16(tmem_d, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
+            if (CG == 2) umma_commit_pair(empty0 + 8 * stage);
+            else umma_commit(empty0 + 8 * stage);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          if (CG == 2) umma_commit_pair(empty0 + 8 * stage);
-          else umma_commit(empty0 + 8 * stage);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        } else {
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(full0 + 8 * stage, phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+            const uint64_t da = make_sdesc(sa), db = make_sdesc(sa + A_BYTES),
+                           dl = make_sdesc(sa + A_BYTES + hi_rows * BK * 2);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
+              umma_f16(tmem_d, da + 2 * k, db + 2 * k, idesc, accum);          // W . x_hi
+              umma_f16(tmem_d + BN, da + 2 * k, dl + 2 * k, idesc, accum);     // W . x_lo
+            }
+            umma_commit(empty0 + 8 * stage);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
         }
         if (CG == 2) umma_commit_pair(tfull0 + 8 * acc);
         else umma_commit(tfull0 + 8 * acc);
@@ -477,12 +501,13 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     int local = 0;
     int rsc_chunk = -1;                     // chunk whose RMSNorm scales are in rsc
     for (int it = cta_id; it < n_items; it += n_ctas, ++local) {
-      Item I = decode_item(it, m_tiles, a.splits, n_chunks, LO);
+      Item I = decode_item(it, m_tiles, a.splits, n_chunks, LO && !wide);
       if (CG == 2) I.tile = I.tile * 2 + (int)crank;   // this CTA's 128-row tile (the pair has no split-K)
       const int n0 = I.chunk * BNX, nc = min(BNX, N - n0);
-      const int hi_rows = nc > 48 ? ((nc + 63) & ~63) : ((nc + 15) & ~15);   // LO: lo columns start here
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
+      // LO: the lo columns start after the hi rows (narrow) or at column 256 (wide)
+      const int hi_rows = wide ? BN : nc > 48 ? ((nc + 63) & ~63) : ((nc + 15) & ~15);
+      const int acc = wide ? 0 : (local & 1);
+      const uint32_t acc_phase = wide ? (local & 1) : ((local >> 1) & 1);
       if (a.ssq_in && I.chunk != rsc_chunk) {
         // folded RMSNorm: column scales of this chunk (once per chunk; every
         // decode item shares chunk 0), computed while the item's MMAs run.

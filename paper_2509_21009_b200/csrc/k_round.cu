@@ -89,8 +89,127 @@ constexpr int CTL_THREADS = 1024;
 // detection, prompts completed at step t (index order), page frees of ended
 // sequences, and the counts exchanged between DP ranks: {k, rows still live,
 // error}.
+__device__ __forceinline__ int pages_of(int tokens) { return (tokens + kPage - 1) / kPage; }
+
+// KV pressure (NEXT-2, reading Z26; oracle sched.kv_step_loop): while the
+// survivors' next-step pages exceed the free pages, preempt the most recently
+// admitted prompt with a live response (never the last one), freeing its
+// responses' private pages; a step that preempts nothing re-admits waiting
+// prompts from the head of the FIFO while their pages fit.  Updates the
+// phase-A tallies in place.  Called by every thread.
+__device__ void ctl_kv_pressure(const RoundDev& R, int* scan_sm, int& s_top, int& s_keep, int& s_need, int& s_err,
+                                long long& s_ctx, int& s_pause) {
+  __shared__ int v_need, v_top, v_preempted;
+  CtlBlock* C = R.ctl;
+  const int n = C->n_live;
+  const int tid = threadIdx.x;
+  __syncthreads();
+  if (tid == 0) { v_need = s_need; v_top = s_top; v_preempted = 0; }
+  __syncthreads();
+  if (v_need > v_top && !s_err) {
+    for (int p = tid; p < R.n_prompts; p += CTL_THREADS) { R.p_live[p] = 0; R.p_pfree[p] = 0; R.p_pneed[p] = 0; }
+    __syncthreads();
+    for (int i = tid; i < n; i += CTL_THREADS) {
+      const int s = R.live[i];
+      if (R.status[s] != ST_LIVE) continue;
+      const int p = R.slot_prompt[s];
+      atomicAdd(&R.p_live[p], 1);
+      atomicAdd(&R.p_pfree[p], pages_of(R.kv_len[s]) - R.own0[s]);
+      atomicAdd(&R.p_pneed[p], R.kv_len[s] % kPage == 0 ? 1 : 0);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      // LIFO whole-prompt victims until the survivors' pages fit
+      while (v_need > v_top) {
+        int live_p = 0, v = -1;
+        for (int p = 0; p < R.n_prompts; ++p)
+          if (R.p_live[p] > 0) { ++live_p; if (v < 0 || R.p_adm[p] > R.p_adm[v]) v = p; }
+        if (live_p <= 1) { s_err = 1; break; }     // the last live prompt does not fit: exhausted
+        v_top += R.p_pfree[v];
+        v_need -= R.p_pneed[v];
+        R.p_live[v] = 0;
+        R.p_wait[v] = PW_VICTIM;
+        R.wait_q[C->wait_tail % R.P] = v;
+        C->wait_tail += 1;
+        C->preemptions += 1;
+        v_preempted = 1;
+      }
+    }
+    __syncthreads();
+    // free the victims' private pages; recount the survivors
+    if (tid == 0) { s_keep = 0; s_need = 0; s_ctx = 0; }
+    __syncthreads();
+    for (int base = 0; base < n; base += CTL_THREADS) {
+      const int i = base + tid;
+      int cnt = 0, keep = 0, need = 0, s = -1;
+      if (i < n) {
+        s = R.live[i];
+        if (R.status[s] == ST_LIVE) {
+          if (R.p_wait[R.slot_prompt[s]] == PW_VICTIM) {
+            R.status[s] = ST_PREEMPTED;
+            cnt = pages_of(R.kv_len[s]) - R.own0[s];
+          } else {
+            keep = 1;
+            need = R.kv_len[s] % kPage == 0 ? 1 : 0;
+          }
+        }
+      }
+      int tot, tk, tn, tc;
+      const int off = block_exscan(cnt, &tot, scan_sm);
+      block_exscan(keep, &tk, scan_sm);
+      block_exscan(need, &tn, scan_sm);
+      block_exscan(keep ? R.kv_len[s] + 1 : 0, &tc, scan_sm);
+      for (int c = 0; c < cnt; ++c)
+        R.free_stack[s_top + off + c] = R.page_table[(size_t)s * R.maxp + R.own0[s] + c];
+      __syncthreads();
+      if (tid == 0) { s_top += tot; s_keep += tk; s_need += tn; s_ctx += tc; }
+      __syncthreads();
+    }
+    for (int p = tid; p < R.n_prompts; p += CTL_THREADS)
+      if (R.p_wait[p] == PW_VICTIM) R.p_wait[p] = PW_WAITING;
+    __syncthreads();
+  }
+  // re-admission (a step that preempted nothing): FIFO head first, while the
+  // recomputed prefix + the next append of every preempted response fit
+  if (tid == 0) {
+    C->readmit_n = 0; C->readmit_rows = 0; C->readmit_pages = 0;
+    if (!v_preempted && !s_err && C->wait_head < C->wait_tail) {
+      int avail = s_top - s_need, rows = 0, pages = 0, nre = 0;
+      long long ctx = 0;
+      for (int q = C->wait_head; q < C->wait_tail; ++q) {
+        const int v = R.wait_q[q % R.P];
+        int req = 0, cnt = 0;
+        for (int j = 0; j < R.G; ++j) {
+          const int s = v * R.G + j;
+          if (R.status[s] == ST_PREEMPTED) { req += pages_of(R.p_plen[v] + R.gen[s]) - R.own0[s]; ++cnt; }
+        }
+        if (req > avail) break;
+        avail -= req;
+        for (int j = 0; j < R.G; ++j) {
+          const int s = v * R.G + j;
+          if (R.status[s] != ST_PREEMPTED) continue;
+          int* J = R.rejobs + 5 * (rows++);
+          J[0] = s; J[1] = R.gen[s];
+          J[2] = R.page_table[(size_t)(R.S + v) * R.maxp + R.own0[s]];   // the prompt's partial page
+          J[3] = -1;
+          J[4] = R.p_plen[v] % kPage;
+          ctx += R.p_plen[v] + R.gen[s];
+        }
+        pages += req;
+        R.p_wait[v] = PW_READMIT;
+        ++nre;
+      }
+      C->readmit_n = nre; C->readmit_rows = rows; C->readmit_pages = pages;
+      s_keep += rows; s_need += pages; s_ctx += ctx;
+      s_pause = nre > 0;
+    }
+    if (!s_err && s_keep == 0 && C->wait_head < C->wait_tail && C->readmit_n == 0) s_err = 1;   // head never fits
+  }
+  __syncthreads();
+}
+
 __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
-  __shared__ int s_k, s_top, s_keep, s_need, s_err;
+  __shared__ int s_k, s_top, s_keep, s_need, s_err, s_pause;
   __shared__ long long s_ctx, s_rd;
   CtlBlock* C = R.ctl;
   const int n = C->n_live;
@@ -114,7 +233,7 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     if (fin || (capped && R.kind == 1)) atomicAdd(&R.p_cnt[R.slot_prompt[s]], 1);
   }
   if (tid == 0) {
-    s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; s_ctx = 0; s_rd = 0;
+    s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; s_ctx = 0; s_rd = 0; s_pause = 0;
     if (appended && R.rows_hist) R.rows_hist[n] += 1;   // one decode step over n rows
   }
   __syncthreads();
@@ -181,6 +300,7 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     if (tid == 0) { s_top += tot; s_keep += tk; s_need += tn; s_ctx += tc; s_rd += trd; }
     __syncthreads();
   }
+  if (R.preempt) ctl_kv_pressure(R, scan_sm, s_top, s_keep, s_need, s_err, s_ctx, s_pause);
   // Continuous issuance (NEXT-4; oracle sched.issue_step_loop): after
   // step t the lowest-index unissued prompts of this rank are issued while
   // fewer than max_active prompts have a live response.  An issued prompt's G
@@ -225,8 +345,8 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     C->need_pages = s_need;
     C->ctx_sum = s_ctx;
     C->kv_read += s_rd;
-    R.ks_local[0] = s_k; R.ks_local[1] = s_keep; R.ks_local[2] = s_err;
-    if (R.world == 1) { R.ks[0] = s_k; R.ks[1] = s_keep; R.ks[2] = s_err; }
+    R.ks_local[0] = s_k; R.ks_local[1] = s_keep; R.ks_local[2] = s_err; R.ks_local[3] = s_pause;
+    if (R.world == 1) { R.ks[0] = s_k; R.ks[1] = s_keep; R.ks[2] = s_err; R.ks[3] = s_pause; }
   }
 }
 
@@ -235,23 +355,24 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
 // lowest index first; then stable compaction, page allocation, next-step
 // inputs and attention items, and the (globally identical) done decision.
 __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
-  __shared__ int s_take, s_acc_new, s_next_global, s_err;
+  __shared__ int s_take, s_acc_new, s_next_global, s_err, s_pause;
   CtlBlock* C = R.ctl;
   const int n = C->n_live;
   const int t = C->t;
   const int tid = threadIdx.x;
   if (tid == 0) {
     const int acc = C->acc;
-    int take = 0, total = 0, nextg = 0, err = 0;
+    int take = 0, total = 0, nextg = 0, err = 0, pause = 0;
     for (int r = 0; r < R.world; ++r) {
-      const int kr = R.ks[3 * r];
+      const int kr = R.ks[4 * r];
       const int tr = min(kr, max(0, R.target - acc - total));
       if (r == R.rank) take = tr;
       total += tr;
-      nextg += R.ks[3 * r + 1];
-      err = max(err, R.ks[3 * r + 2]);
+      nextg += R.ks[4 * r + 1];
+      err = max(err, R.ks[4 * r + 2]);
+      pause |= R.ks[4 * r + 3];
     }
-    s_take = take; s_acc_new = acc + total; s_next_global = nextg; s_err = err;
+    s_take = take; s_acc_new = acc + total; s_next_global = nextg; s_err = err; s_pause = pause;
   }
   __syncthreads();
   for (int r = tid; r < s_take; r += CTL_THREADS) {
@@ -270,6 +391,18 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
   // the target is reached: the round ends here)
   const int n_is0 = C->n_issued;
   const int nis = s_acc_new >= R.target ? 0 : C->issue_n * R.G;
+  // ... or (KV pressure, exclusive with issuance) the responses re-admitted
+  // after this step, in re-admission order: their KV restarts at the
+  // recomputed prefix plen + g - 1 and they decode token g + 1 next
+  const int nrd = s_acc_new >= R.target || s_err ? 0 : C->readmit_rows;
+  for (int e = tid; e < nrd; e += CTL_THREADS) {
+    const int sl = R.rejobs[5 * e];
+    R.kv_len[sl] = R.p_plen[R.slot_prompt[sl]] + R.gen[sl] - 1;
+    R.status[sl] = ST_LIVE;
+  }
+  __syncthreads();
+  const int nx = nis + nrd;
+#define EXTRA_SLOT(e) (nrd ? R.rejobs[5 * (e)] : n_is0 * R.G + (e))   // (#undef at the end of phase B)
   // Full waves: with k = ceil(rows / U1) in {2, 3} (between one and three
   // waves' worth of rows per head) budget k whole waves so the flat list
   // does not end in a partial wave; the splits left over by the floors go one
@@ -283,11 +416,11 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
   if (R.attn_waves && !s_err && kw >= 2 && kw <= 3) {
     U = U1 * kw;
     int sum = 0;
-    for (int base = 0; base < n + nis; base += CTL_THREADS) {
+    for (int base = 0; base < n + nx; base += CTL_THREADS) {
       const int i = base + tid;
       int b = 0;
-      if (i < n + nis) {
-        const int s = i < n ? R.live[i] : n_is0 * R.G + (i - n);
+      if (i < n + nx) {
+        const int s = i < n ? R.live[i] : EXTRA_SLOT(i - n);
         if (i >= n || R.status[s] == ST_LIVE) b = (int)((long long)(R.kv_len[s] + 1) * U / ctx_total);
       }
       int tot;
@@ -298,15 +431,16 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
   }
   int kept = 0, alloc = 0, items = 0;
   if (!s_err) {
-    for (int base = 0; base < n + nis; base += CTL_THREADS) {
+    for (int base = 0; base < n + nx; base += CTL_THREADS) {
       const int i = base + tid;
       int keep = 0, need = 0, ns = 0, chunk = 0, s = -1;
-      if (i < n + nis) {
-        s = i < n ? R.live[i] : n_is0 * R.G + (i - n);
+      if (i < n + nx) {
+        s = i < n ? R.live[i] : EXTRA_SLOT(i - n);
         keep = i >= n || R.status[s] == ST_LIVE;
         if (keep) {
           const int ctx = R.kv_len[s] + 1;
-          need = (R.kv_len[s] % kPage) == 0;
+          // a re-admitted response takes the pages of its recomputed prefix and the next append
+          need = (i >= n && nrd) ? pages_of(ctx) - R.own0[s] : (R.kv_len[s] % kPage) == 0;
           const int want = (int)max(1LL, (long long)ctx * U / ctx_total);
           chunk = ((ctx + want - 1) / want + kPage - 1) / kPage * kPage;   // whole pages per split
           ns = (ctx + chunk - 1) / chunk;
@@ -328,13 +462,21 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
         R.live_next[pos] = s;
         if (i < n) {
           R.tok_in[pos] = R.tok_out[(size_t)s * R.cap + (t - R.t0[s]) - 1];
+        } else if (nrd) {
+          R.tok_in[pos] = R.tok_out[(size_t)s * R.cap + R.gen[s] - 1];   // its last token (index g)
         } else {
           R.tok_in[pos] = R.p_last_tok[R.slot_prompt[s]];
           R.t0[s] = t;
         }
         R.row_pos[pos] = kv;
         R.row_pt[pos] = s;
-        if (need) R.page_table[(size_t)s * R.maxp + kv / kPage] = R.free_stack[top - 1 - (alloc + oa)];
+        if (i >= n && nrd) {
+          for (int k = 0; k < need; ++k)
+            R.page_table[(size_t)s * R.maxp + R.own0[s] + k] = R.free_stack[top - 1 - (alloc + oa + k)];
+          R.rejobs[5 * (i - n) + 3] = R.page_table[(size_t)s * R.maxp + R.own0[s]];   // fork destination
+        } else if (need) {
+          R.page_table[(size_t)s * R.maxp + kv / kPage] = R.free_stack[top - 1 - (alloc + oa)];
+        }
         const int it0 = items + oi;
         for (int sp = 0; sp < ns; ++sp) {
           AttnItem I;
@@ -358,6 +500,15 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     C->n_items = min(items, R.max_items);
     C->n_issued = n_is0 + nis / R.G;
     C->issue_n = 0;
+    // commit the re-admissions: popped from the FIFO, newest admissions
+    C->n_rejobs = nrd;
+    if (nrd)
+      for (int q = 0; q < C->readmit_n; ++q) {
+        const int v = R.wait_q[(C->wait_head + q) % R.P];
+        R.p_wait[v] = PW_NONE;
+        R.p_adm[v] = ++C->adm_ctr;
+      }
+    if (nrd) C->wait_head += C->readmit_n;
     if (items > R.max_items) s_err = 3;    // unreachable by the bound S + 3 * U1; fail loudly if not
     const bool done = s_acc_new >= R.target || s_next_global == 0 || s_err;
     if (R.trace_buf && t <= R.trace_steps) {
@@ -368,17 +519,24 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     if (done) {
       C->done = 1; C->t_end = t; C->n_final = kept; C->n_live = 0;
       C->underfilled = s_acc_new < R.target;
+    } else if (s_pause) {
+      // some rank re-admitted responses: every rank holds the next step
+      // until the host recomputed their KV (rp_step, between steps)
+      C->pause = 1; C->n_live_saved = kept; C->n_items_saved = min(items, R.max_items);
+      C->n_live = 0; C->n_items = 0; C->t = t + 1;
     } else {
       C->n_live = kept; C->t = t + 1;
     }
   }
 }
 
+#undef EXTRA_SLOT
+
 __global__ void __launch_bounds__(CTL_THREADS) ctl_kernel(RoundDev R, int appended, int mode) {
   __shared__ int scan_sm[40];
   pdl_wait();
   pdl_launch_dependents();
-  if (R.ctl->done) return;
+  if (R.ctl->done || R.ctl->pause) return;
   if (mode != 2) ctl_phase_a(R, appended, scan_sm);
   if (mode == 0) { __threadfence_block(); __syncthreads(); }
   if (mode != 1) ctl_phase_b(R, scan_sm);

@@ -8,8 +8,12 @@ namespace rp {
 
 // ST_DROPPED: finished (EOS) at the step its prompt completed but beyond the
 // first `keep` (response-level speculation, ties to the lower j).
-enum SeqStatus { ST_LIVE = 0, ST_FINISHED = 1, ST_CAPPED = 2, ST_ABORTED = 3, ST_DROPPED = 4 };
+// ST_PREEMPTED: KV pressure (NEXT-2, reading Z26): the response's private
+// pages were freed and its prompt waits for re-admission (recompute).
+enum SeqStatus { ST_LIVE = 0, ST_FINISHED = 1, ST_CAPPED = 2, ST_ABORTED = 3, ST_DROPPED = 4, ST_PREEMPTED = 5 };
 enum PromptState { PS_RUNNING = 0, PS_ACCEPTED = 1, PS_COMPLETE = 2 };
+// per-prompt wait state (KV pressure): none / waiting / re-admitted at this step
+enum WaitState { PW_NONE = 0, PW_WAITING = 1, PW_READMIT = 2, PW_VICTIM = 3 };
 
 // One unit of attention work: a block of query tokens (decode: 1 token; the
 // g query heads of a KV head form the MMA rows) against a key range.
@@ -43,12 +47,31 @@ struct CtlBlock {
   long long kv_read;  // sum over decode steps so far of the decoded rows' attention context
   int n_issued;     // continuous issuance: prompts of this rank issued so far (committed)
   int issue_n;      // prompts phase A issues after this step (committed by phase B unless done)
+  // KV pressure (NEXT-2, reading Z26)
+  int preemptions;  // prompts preempted this round on this rank
+  int wait_head, wait_tail;   // FIFO of waiting prompts in wait_q[head .. tail)
+  int adm_ctr;      // last admission stamp
+  int readmit_n;    // prompts phase A re-admits after this step
+  int readmit_rows; // their responses (rows appended by phase B)
+  int readmit_pages;  // pages they take
+  int pause;        // 1: re-admitted responses await their KV recompute (the host runs it between steps)
+  int n_live_saved, n_items_saved;  // the next step's rows / attention items while paused
+  int n_rejobs;     // recompute jobs written by phase B
 };
 
 struct RoundDev {
   int S, P, maxp, cap, G, target, kind /*0 short 1 long*/, trace, eos, n_prompts, kv_heads;
   int keep;           // responses retained per prompt (R0 <= G; == G in long rounds)
   int max_active;     // continuous issuance (NEXT-4): max prompts with a live response; 0 = off
+  int preempt;        // KV-pressure preemption with recompute (NEXT-2); 0 = exhaustion is an error
+  int* p_plen;        // [P] prompt lengths (the KV a response starts from)
+  int* p_adm;         // [P] admission stamps (LIFO victims: the largest)
+  int* p_wait;        // [P] WaitState
+  int* p_live;        // [P] scratch: live responses this step
+  int* p_pfree;       // [P] scratch: their private pages
+  int* p_pneed;       // [P] scratch: their next-step page needs
+  int* wait_q;        // [P] FIFO ring of waiting prompts
+  int* rejobs;        // [S][5] recompute jobs: slot, g, fork src page, fork dst page, fork rows
   int attn_units;     // decode-attention split budget per KV head (0: 148 / KV)
   int attn_waves;     // 1: budget whole waves of attention units (k-wave fill), 0: one-wave floor
   int world, rank;
@@ -66,8 +89,8 @@ struct RoundDev {
   AttnItem* items;
   unsigned long long* rows_hist;  // [S + 1] decode steps of this round by live rows (measurement)
   int* free_stack;
-  int* ks_local;      // [3]: prompts completed at this step, rows still live, error
-  int* ks;            // [3 * world] all-gathered ks_local (== ks_local when world == 1)
+  int* ks_local;      // [4]: prompts completed at this step, rows still live, error, re-admission pause
+  int* ks;            // [4 * world] all-gathered ks_local (== ks_local when world == 1)
   CtlBlock* ctl;
   int* trace_buf; int trace_steps;   // debug: [steps][2 + S] (n, acc|done<<30, live...)
 };

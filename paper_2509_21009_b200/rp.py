@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RP_LIB") or os.path.join(_HERE, "librollpacker.so")
 
 RP_OK, RP_EINVAL, RP_EBUSY, RP_ESTATE, RP_ENOMEM_KV, RP_ECUDA, RP_ENCCL, RP_ENOSPC = 0, -1, -2, -3, -4, -5, -6, -7
-RP_SHORT, RP_LONG, RP_TRACE = 0, 1, 4
+RP_SHORT, RP_LONG, RP_TRACE, RP_PREEMPT = 0, 1, 4, 8
 RP_FINISH_EOS, RP_FINISH_CAP = 1, 2
 RP_IPC_HANDLE_BYTES = 64
 
@@ -54,7 +54,8 @@ class Status(ctypes.Structure):
     _fields_ = [("round_id", ctypes.c_int64), ("kind", ctypes.c_int32), ("t", ctypes.c_int32),
                 ("n_live", ctypes.c_int32), ("accepted", ctypes.c_int32), ("accepted_local", ctypes.c_int32),
                 ("done", ctypes.c_int32), ("underfilled", ctypes.c_int32), ("n_prompts_local", ctypes.c_int32),
-                ("decoded_tokens", ctypes.c_int64), ("kv_tokens_read", ctypes.c_int64)]
+                ("decoded_tokens", ctypes.c_int64), ("kv_tokens_read", ctypes.c_int64),
+                ("preemptions", ctypes.c_int32)]
 
 
 class Response(ctypes.Structure):
@@ -269,7 +270,7 @@ class Engine:
 
     # --------------------------------------------------------------- the ABI
     def submit(self, prompts, G, cap, target, long_round=False, trace=None, round_id=0, keep=0, trace_retry=None,
-               trace_mode=None):
+               trace_mode=None, preempt=False):
         """prompts: list of dicts {prompt_id, tokens} (None -> pop `target`
         prompts off the long-prompt queue; pass trace_mode=True for a trace-mode
         round over queued prompts); trace: None or int array [n, G] of response
@@ -277,7 +278,7 @@ class Engine:
         a prompt is deferred (reading Z5); keep: responses retained per prompt
         (R0 < G: response-level speculation; 0 -> G)."""
         tm = trace is not None if trace_mode is None else trace_mode
-        flags = (RP_LONG if long_round else RP_SHORT) | (RP_TRACE if tm else 0)
+        flags = (RP_LONG if long_round else RP_SHORT) | (RP_TRACE if tm else 0) | (RP_PREEMPT if preempt else 0)
         if prompts is None:
             n = target
             rc = self.L.rp_submit_round(self.h, None, n, G, keep, cap, target, flags, round_id)
