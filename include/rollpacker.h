@@ -277,6 +277,18 @@ int rp_long_queue(void* ctx, int32_t* ids_out, int32_t max, int32_t* n_out);
  * Errors: RP_EINVAL (n < 0 or n > queue length). */
 int rp_long_queue_pop(void* ctx, int32_t n);
 
+/* The parallelism planner's adaptation rule (SURVEY
+ * NEXT-2): "a sudden rise in preemptions (e.g., >1.05x) triggers an increase
+ * in TP (doubling the size), while sustained zero preemptions across four
+ * steps trigger a decrease (halving the size)".  Given the current TP size of
+ * a round kind, the largest allowed (the GPUs of one server), the previous
+ * and the latest round's preemption counts (rp_status.preemptions summed
+ * over the replica) and the count of consecutive zero-preemption rounds so
+ * far, writes the next TP size and streak.  Host only, no context.
+ * Errors: RP_EINVAL. */
+int rp_plan_tp(int32_t tp, int32_t tp_max, int64_t prev_preemptions, int64_t preemptions, int32_t zero_streak,
+               int32_t* tp_next, int32_t* zero_streak_next);
+
 /* Single-GPU local group: a host object shared by the
  * world x tp contexts of one process on one device, holding the exchange
  * buffers of the device-memory collectives (k_comm.cu) and the TP peer

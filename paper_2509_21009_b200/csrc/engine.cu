@@ -154,6 +154,7 @@ struct RpCtx {
   // producers write them and the consumers read them only while act_lo is set
   __half *h_lo = nullptr, *q_lo = nullptr, *att_lo = nullptr, *mid_lo = nullptr;
   bool act_lo = true;
+  int lo_mask = 0;
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
   int* gctr = nullptr;
   int* atickets = nullptr;
@@ -226,6 +227,10 @@ struct RpCtx {
 };
 
 static std::string g_init_err;
+
+// split-precision operands (reading Z22)
+enum { LO_QKV = 1, LO_O = 2, LO_GU = 4, LO_DOWN = 8, LO_Q = 16 };
+static const int kDefaultLoMask = LO_QKV | LO_O | LO_GU | LO_DOWN | LO_Q;
 
 // Programmatic dependent launch is off while a local-group context issues
 // work from this thread (common.cuh g_no_pdl).
@@ -795,7 +800,17 @@ static int init_impl(RpCtx* c) {
     for (int i = 0; i < RP_PROF_N; ++i)
       if (i != RP_PROF_CTL && i != RP_PROF_NCCL && strstr(sk, names[i])) c->skip_mask |= 1u << i;
   }
-  if (!c->act_lo) c->h_lo = c->q_lo = c->att_lo = c->mid_lo = nullptr;   // producers skip, plans map hi only
+  // which operands carry their residual: bit 0 QKV input, 1 O input (attention
+  // output), 2 gate/up input, 3 down input (SwiGLU output), 4 the attention
+  // query; RP_LO_MASK overrides, RP_ACT_LO=0 clears it (A/B)
+  c->lo_mask = getenv("RP_LO_MASK") ? (int)strtol(getenv("RP_LO_MASK"), nullptr, 0) : kDefaultLoMask;
+  if (!c->act_lo) c->lo_mask = 0;
+  c->act_lo = c->lo_mask != 0;
+  // producers skip the residuals nobody reads; plans without one map hi only
+  if (!(c->lo_mask & (LO_QKV | LO_GU))) c->h_lo = nullptr;
+  if (!(c->lo_mask & LO_O)) c->att_lo = nullptr;
+  if (!(c->lo_mask & LO_DOWN)) c->mid_lo = nullptr;
+  if (!(c->lo_mask & LO_Q)) c->q_lo = nullptr;
   // GEMM weights in 128 x 64 tiles: every weight TMA box is one contiguous
   // 16 KB read (RP_W_ROWMAJOR=1: plain row-major, an A/B switch)
   const int wt = getenv("RP_W_ROWMAJOR") ? 0 : 1;
@@ -876,9 +891,9 @@ static int init_impl(RpCtx* c) {
   const int Tcap = c->z.Tcap;
   const int qkvw = (int)((H + 2 * KV) * hd);
   for (auto& w : c->layers) {
-    if (make_plan(&w.p_qkv, w.wqkv, qkvw, (int)d, c->h, Tcap, wt, c->h_lo) ||
+    if (make_plan(&w.p_qkv, w.wqkv, qkvw, (int)d, c->h, Tcap, wt, (c->lo_mask & LO_QKV) ? c->h_lo : nullptr) ||
         make_plan(&w.p_o, w.wo, (int)d, (int)(H * hd), c->att, Tcap, wt, c->att_lo) ||
-        make_plan(&w.p_gu, w.wgu, (int)(2 * F), (int)d, c->h, Tcap, wt, c->h_lo) ||
+        make_plan(&w.p_gu, w.wgu, (int)(2 * F), (int)d, c->h, Tcap, wt, (c->lo_mask & LO_GU) ? c->h_lo : nullptr) ||
         make_plan(&w.p_down, w.wd, (int)d, (int)F, c->mid, Tcap, wt, c->mid_lo))
       return c->fail(RP_ECUDA, "cuTensorMapEncodeTiled failed");
   }
@@ -1389,7 +1404,7 @@ static int recompute_paused(RpCtx* c) {
       if (T == 0) return c->fail(RP_ENOSPC, "recompute: prefill buffers too small for one token");
       CK(idle(c));
       for (auto& cp : copies)
-        CK(cudaMemcpyAsync(c->pre_tok + cp[0], c->R.tok_out + (size_t)cp[1] * c->rd.max_cap + cp[2],
+        CK(cudaMemcpyAsync(c->pre_tok + cp[0], c->R.tok_out + (size_t)cp[1] * c->R.cap + cp[2],   // row stride: the round's cap
                            (size_t)cp[3] * 4, cudaMemcpyDeviceToDevice, c->st));
       CK(cudaMemcpyAsync(c->pre_pos, pos.data(), T * 4, cudaMemcpyHostToDevice, c->st));
       CK(cudaMemcpyAsync(c->pre_pt, pt.data(), T * 4, cudaMemcpyHostToDevice, c->st));
@@ -1685,6 +1700,29 @@ int rp_plan_round(void* ctx, int32_t P0, float eta, int32_t drain, int32_t* kind
     // ceil in exact arithmetic: eta is a float (1.25 exactly); the tiny
     // margin keeps a product that lands on an integer from rounding up
     *n_prompts = (int)std::ceil((double)eta * (double)P0 - 1e-9);
+  }
+  return RP_OK;
+}
+
+// The parallelism planner's heuristic (oracle sched.plan_tp).
+int rp_plan_tp(int32_t tp, int32_t tp_max, int64_t prev_preemptions, int64_t preemptions, int32_t zero_streak,
+               int32_t* tp_next, int32_t* zero_streak_next) {
+  if (!tp_next || !zero_streak_next || tp < 1 || tp_max < tp || preemptions < 0 || prev_preemptions < 0 ||
+      zero_streak < 0) {
+    g_init_err = "invalid field: rp_plan_tp arguments";
+    return RP_EINVAL;
+  }
+  const int streak = preemptions == 0 ? zero_streak + 1 : 0;
+  // a sudden rise (> 1.05x the previous round of this kind) doubles the TP size
+  if (preemptions > 0 && (double)preemptions > 1.05 * (double)prev_preemptions) {
+    *tp_next = std::min(2 * tp, tp_max);
+    *zero_streak_next = 0;
+  } else if (streak >= 4) {          // four rounds without preemption halve it
+    *tp_next = std::max(tp / 2, 1);
+    *zero_streak_next = 0;
+  } else {
+    *tp_next = tp;
+    *zero_streak_next = streak;
   }
   return RP_OK;
 }

@@ -31,13 +31,17 @@ namespace rp {
 constexpr int BM = 128, BK = 64, BN = 256;
 constexpr int A_BYTES = BM * BK * 2;         // 16 KB
 constexpr int B_BYTES = BN * BK * 2;         // 32 KB (widest activation tile)
-constexpr int RING_BYTES = 4 * (A_BYTES + B_BYTES);   // 192 KB of stages
+// 200 KB of stages: everything the 227 KB opt-in leaves beside the epilogue
+// buffers.  Bytes in flight per SM set the weight-streaming rate at small N
+// (Little's law: ~6 us of loaded HBM latency), so the ring takes the rest.
+constexpr int RING_BYTES = 200 * 1024;
 constexpr int MAX_STAGES = 12;               // ring depth at small N (18 KB stages)
 constexpr int XCH_BYTES = 64 * 33 * 4;       // swiglu exchange
 constexpr int TS = BM + 4;                   // fp32 row stride of the epilogue staging tile
 constexpr int STG_BYTES = 32 * TS * 4;       // [32 columns][128 rows] fp32 staging for 16-byte stores
 constexpr int RSC_BYTES = BN * 4;             // per-column RMSNorm scales of the current item
 constexpr int GEMM_SMEM = RING_BYTES + XCH_BYTES + STG_BYTES + RSC_BYTES + 1024 /*align*/ + 8 * (2 * MAX_STAGES + 4) + 16;
+static_assert(GEMM_SMEM <= 232448, "GEMM shared memory above the sm_100 opt-in limit");
 constexpr int GEMM_THREADS = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

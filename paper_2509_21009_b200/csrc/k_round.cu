@@ -399,6 +399,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     const int sl = R.rejobs[5 * e];
     R.kv_len[sl] = R.p_plen[R.slot_prompt[sl]] + R.gen[sl] - 1;
     R.status[sl] = ST_LIVE;
+    R.t0[sl] = t - R.gen[sl];        // its token index at step t + 1 is g + 1 (the counter of its next token)
   }
   __syncthreads();
   const int nx = nis + nrd;

@@ -68,7 +68,7 @@ EXPORTS = ["rp_query_sizes", "rp_init_model", "rp_submit_round", "rp_step", "rp_
            "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm", "rp_debug_profile", "rp_nccl_unique_id",
            "rp_tp_ipc_handle", "rp_tp_ipc_open", "rp_collect_ready", "rp_round_rows_histogram",
            "rp_round_issue_cap", "rp_round_unissued", "rp_plan_round", "rp_long_queue_pop",
-           "rp_local_group_create", "rp_local_group_free"]
+           "rp_local_group_create", "rp_local_group_free", "rp_plan_tp"]
 
 
 def load_library(path=LIB_PATH):
@@ -110,6 +110,7 @@ def load_library(path=LIB_PATH):
     lib.rp_local_group_create.argtypes = [I32, I32, ctypes.POINTER(P)]
     lib.rp_local_group_free.argtypes = [P]
     lib.rp_local_group_free.restype = None
+    lib.rp_plan_tp.argtypes = [I32, I32, I64, I64, I32, ctypes.POINTER(I32), ctypes.POINTER(I32)]
     for name in EXPORTS:
         if name not in ("rp_free", "rp_last_error", "rp_launch_count", "rp_local_group_free"):
             getattr(lib, name).restype = I32
@@ -138,6 +139,16 @@ class RPError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__("rollpacker error %d: %s" % (code, msg))
         self.code = code
+
+
+def plan_tp(tp, tp_max, prev_preemptions, preemptions, zero_streak):
+    """rp_plan_tp: the planner's TP adaptation -> (tp, streak)."""
+    a, b = ctypes.c_int32(), ctypes.c_int32()
+    rc = lib().rp_plan_tp(int(tp), int(tp_max), int(prev_preemptions), int(preemptions), int(zero_streak),
+                          ctypes.byref(a), ctypes.byref(b))
+    if rc != RP_OK:
+        raise RPError(rc, "rp_plan_tp")
+    return a.value, b.value
 
 
 class LocalGroup:

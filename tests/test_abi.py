@@ -75,3 +75,15 @@ def test_sass_uses_tcgen05_and_tma(lib):
     assert "UTCHMMA" in out or "UTCQMMA" in out      # tcgen05.mma
     assert "UTMALDG" in out                           # TMA tensor loads
     assert "LDTM" in out                              # tcgen05.ld
+
+
+def test_plan_tp_matches_oracle():
+    """rp_plan_tp (host-only C ABI) equals the oracle heuristic
+    on every small input."""
+    from oracle import sched
+    from paper_2509_21009_b200 import rp
+    for tp in (1, 2, 4, 8):
+        for prev in (0, 1, 20, 100):
+            for cur in (0, 1, 19, 21, 105, 106, 300):
+                for z in range(5):
+                    assert rp.plan_tp(tp, 8, prev, cur, z) == sched.plan_tp(tp, 8, prev, cur, z), (tp, prev, cur, z)

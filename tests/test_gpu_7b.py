@@ -65,7 +65,7 @@ def test_7b_teacher_forced_logits(bench_engine):
     * decode-step logits of the bench engine's timed path (CUDA graph of 16
       steps, split-K / cooperative GEMMs with the fused RoPE epilogue, the
       folded norm over 28 partials, decode attention) for 2 responses at step
-      17 of a 16-row round, teacher-forced on the GPU's own tokens;
+      17 of a 16-row round, teacher-forced on the GPU's own tokens (6 rows);
     * the sampled tokens of steps 1-17 of those responses (gap rule)."""
     from oracle import decoder, sampler, weights
     from synth import configs, gen
@@ -83,7 +83,7 @@ def test_7b_teacher_forced_logits(bench_engine):
     assert st.t == 17 and len(slots) == 16
     eng.run()
     res = {(r["prompt_id"], r["j"]): r["tokens"] for r in eng.collect()}
-    pick = [(0, 2), (1, 7)]                                    # (prompt, j)
+    pick = [(0, 2), (0, 5), (0, 7), (1, 0), (1, 3), (1, 7)]    # (prompt, j)
     seqs = [np.asarray(toks)] + [np.concatenate([ps[p]["tokens"], res[(ps[p]["prompt_id"], j)][:16]])
                                  for p, j in pick]
     weights.build_c()
@@ -117,7 +117,7 @@ def test_7b_teacher_forced_logits(bench_engine):
                 assert gap <= 1e-2, (p, j, t, gap)
                 mism += 1
         o += 17
-    print("7b decode-step (graph, step 17, 16 rows) logits max-abs vs fp64 oracle: %.4g; %d in-gap token "
-          "mismatches of 34" % (dworst, mism))
+    print("7b decode-step (graph, step 17, 16 rows) logits max-abs vs fp64 oracle: %.4g over %d rows; %d in-gap "
+          "token mismatches of %d" % (dworst, len(pick), mism, 17 * len(pick)))
     assert dworst <= 2e-2, dworst
-    assert mism <= 1
+    assert mism <= 2

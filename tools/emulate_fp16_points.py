@@ -46,17 +46,15 @@ def layer_bf(x, w, pos, R):
     a = R["a"](out.transpose(1, 0, 2).reshape(T, H * hd))
     x = x + a @ f(w["o"]).T
     r2 = 1.0 / np.sqrt(np.mean(x * x, -1, keepdims=True) + eps)
-    h2 = R["h"](x)   # layer norms
+    h2 = R["h2"](x)   # second layer norm (gate/up input)
     gt = (h2 @ f(w["gate"]).T) * r2; up = (h2 @ f(w["up"]).T) * r2
     mid = R["mid"](decoder.silu(gt) * up)
     return x + mid @ f(w["down"]).T
-pts = ["h", "hf", "q", "k", "v", "p", "a", "mid"]     # h: layer-norm outputs (QKV, gate/up inputs); hf: final norm (LM head input)
+pts = ["h", "h2", "hf", "q", "k", "v", "p", "a", "mid"]   # h: first norm (QKV input), h2: second norm (gate/up), hf: final
 def mk(exact):
     return {p: (ident if p in exact else f16) for p in pts}
-import sys as _sys
-combos = {"all_fp16": [], "q+h+hf+a+mid": ["q", "h", "hf", "a", "mid"], "q+h+a+mid (LM hi only)": ["q", "h", "a", "mid"],
-          "q+h+hf+mid (no a)": ["q", "h", "hf", "mid"], "q+h+hf+a (no mid)": ["q", "h", "hf", "a"],
-          "q+h+hf": ["q", "h", "hf"], "q+hf+a+mid (no h)": ["q", "hf", "a", "mid"], "q+h+a": ["q", "h", "a"]}
+combos = {"all_fp16": [], "q+a+mid": ["q", "a", "mid"], "q+h+a+mid": ["q", "h", "a", "mid"],
+          "q+h2+a+mid": ["q", "h2", "a", "mid"], "q+h2+mid": ["q", "h2", "mid"]}
 variants = {m: mk(ex) for m, ex in combos.items()}
 w = weights.Weights(cfg, configs.WEIGHT_SEED, use_c=True)
 toks = gen.prompts(1, 0, cfg["eos_id"], (56, 56), 6)[0]["tokens"]
