@@ -290,13 +290,17 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   // small N the stages shrink and the ring deepens (more weight bytes in
   // flight per SM for the HBM-bound small-batch regime).
   // (pair: each CTA holds half of the 16-padded chunk, at most 128 rows)
-  const int wmax = CG == 2 ? ((min(BNX, N) + 15) & ~15) / 2 : min(BNX, N);
+  // (pair, narrow LO: CTA 0 holds the chunk's hi rows and CTA 1 its lo rows,
+  // so the pair MMA's N is [hi | lo] and each CTA stages as many bytes as
+  // without split precision)
+  const bool pair_narrow = CG == 2 && LO && !wide;
+  const int wmax = (CG == 2 && !pair_narrow) ? ((min(BNX, N) + 15) & ~15) / 2 : min(BNX, N);
   const int brow_max = wmax > 192 ? 256 : wmax > 48 ? 64 : 16;
   const int b_rows = ((wmax + brow_max - 1) / brow_max) * brow_max;
   // split-precision activations (LO): the stage's activation tile is the
   // chunk's fp16 rows (hi, padded to whole boxes) followed by their fp16
-  // rounding residuals (lo)
-  const int NLO = LO ? 2 : 1;
+  // rounding residuals (lo) -- except a narrow pair, where each CTA holds one
+  const int NLO = (LO && !pair_narrow) ? 2 : 1;
   const int STAGE_BYTES = A_BYTES + ((NLO * b_rows * BK * 2 + 1023) & ~1023);
   const int STAGES = min(MAX_STAGES, RING_BYTES / STAGE_BYTES);
 
@@ -365,7 +369,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #define A_C0(kb) (a.a_tiled ? 0 : (kb) * BK)
 #define A_C1(kb) (a.a_tiled ? ((wrow / BM) * kbt + (kb)) * BM : wrow)
         int n0 = I.chunk * BNX, nc = min(BNX, N - n0);
-        if (CG == 2) {                        // this CTA's half of the 16-padded chunk
+        if (CG == 2 && !pair_narrow) {        // this CTA's half of the 16-padded chunk
           const int half = ((nc + 15) & ~15) / 2;
           n0 += (int)crank * half;
           nc = half;
@@ -373,6 +377,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         // X boxes: one 256-row box for wide chunks, else a few 64- or 16-row boxes
         const CUtensorMap* tb = nc > 192 ? &tmB256 : nc > 48 ? &tmB64 : &tmB16;
         const CUtensorMap* tl = nc > 192 ? &tmL256 : nc > 48 ? &tmL64 : &tmL16;
+        if (pair_narrow && crank == 1) tb = tl;   // CTA 1 of a narrow pair stages the lo rows
         const int brow = nc > 192 ? 256 : nc > 48 ? 64 : 16;
         const int nbox = (nc + brow - 1) / brow;
         const int lo_off = nbox * brow * BK * 2;           // LO: residual rows follow the hi rows
@@ -408,7 +413,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             for (int b = 0; b < nbox; ++b) {
               if (CG == 2) tma_load_2d_pair(sa + A_BYTES + b * brow * BK * 2, tb, leader_addr(fb), kb * BK, n0 + brow * b, pol_x);
               else tma_load_2d(sa + A_BYTES + b * brow * BK * 2, tb, fb, kb * BK, n0 + brow * b, pol_x);
-              if (LO) {
+              if (LO && NLO == 2) {
                 if (CG == 2) tma_load_2d_pair(sa + A_BYTES + lo_off + b * brow * BK * 2, tl, leader_addr(fb), kb * BK, n0 + brow * b, pol_x);
                 else tma_load_2d(sa + A_BYTES + lo_off + b * brow * BK * 2, tl, fb, kb * BK, n0 + brow * b, pol_x);
               }
@@ -429,7 +434,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             tma_load_2d_pair(sa, &tmA, lb, A_C0(kb), A_C1(kb), pol_w);
             for (int b = 0; b < nbox; ++b) {
               tma_load_2d_pair(sa + A_BYTES + b * brow * BK * 2, tb, lb, kb * BK, n0 + brow * b, pol_x);
-              if (LO) tma_load_2d_pair(sa + A_BYTES + lo_off + b * brow * BK * 2, tl, lb, kb * BK, n0 + brow * b, pol_x);
+              if (LO && NLO == 2) tma_load_2d_pair(sa + A_BYTES + lo_off + b * brow * BK * 2, tl, lb, kb * BK, n0 + brow * b, pol_x);
             }
           } else {
             tma_load_2d(sa, &tmA, fb, A_C0(kb), A_C1(kb), pol_w);
@@ -452,7 +457,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         const int nc = min(BNX, N - I.chunk * BNX);
         // narrow LO: N = the hi rows (whole boxes) + the 16-padded lo rows
         const int hi_rows = nc > 192 ? 256 : nc > 48 ? ((nc + 63) & ~63) : ((nc + 15) & ~15);
-        const int nmma = (LO && !wide) ? hi_rows + ((nc + 15) & ~15) : (nc + 15) & ~15;
+        const int nmma = pair_narrow ? 2 * hi_rows : (LO && !wide) ? hi_rows + ((nc + 15) & ~15) : (nc + 15) & ~15;
         const uint32_t idesc = make_idesc(nmma, BM * CG);
         // wide LO: one accumulator pair (all 512 columns), phases alternate per item
         const int acc = wide ? 0 : (local & 1);
@@ -481,15 +486,25 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             mbar_wait(full0 + 8 * stage, phase);
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+            // the lo rows follow this CTA's hi rows (the pair: each CTA's half)
+            const int cta_rows = CG == 2 ? ((((nc + 15) & ~15) / 2 > 48) ? ((((nc + 15) & ~15) / 2 + 63) & ~63)
+                                                                          : ((((nc + 15) & ~15) / 2 + 15) & ~15))
+                                         : hi_rows;
             const uint64_t da = make_sdesc(sa), db = make_sdesc(sa + A_BYTES),
-                           dl = make_sdesc(sa + A_BYTES + hi_rows * BK * 2);
+                           dl = make_sdesc(sa + A_BYTES + cta_rows * BK * 2);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
-              umma_f16(tmem_d, da + 2 * k, db + 2 * k, idesc, accum);          // W . x_hi
-              umma_f16(tmem_d + BN, da + 2 * k, dl + 2 * k, idesc, accum);     // W . x_lo
+              if (CG == 2) {
+                umma_f16_pair(tmem_d, da + 2 * k, db + 2 * k, idesc, accum);
+                umma_f16_pair(tmem_d + BN, da + 2 * k, dl + 2 * k, idesc, accum);
+              } else {
+                umma_f16(tmem_d, da + 2 * k, db + 2 * k, idesc, accum);          // W . x_hi
+                umma_f16(tmem_d + BN, da + 2 * k, dl + 2 * k, idesc, accum);     // W . x_lo
+              }
             }
-            umma_commit(empty0 + 8 * stage);
+            if (CG == 2) umma_commit_pair(empty0 + 8 * stage);
+            else umma_commit(empty0 + 8 * stage);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
         }
@@ -994,7 +1009,10 @@ void gemm_launch(const GemmPlan& p, const GemmArgs& a0, int grid, cudaStream_t s
   // last CTA (ticket), never by CTAs waiting for each other, because other
   // contexts' kernels may hold the SMs the waited-for splits need
   a.coop_min = a0.no_spin ? 0x7FFFFFFF : gemm_coop_min();
-  if (pair && !a.lo && a.splits == 1 && a.M % (2 * BM) == 0 && !a.timeline && grid % 2 == 0) {
+  // CTA pairs: with RP_GEMM_PAIR=1, and always for split-precision GEMMs
+  // without split-K (gate/up: the pair stages the hi and the lo rows in
+  // different CTAs, so the ring keeps the depth of the plain GEMM)
+  if ((pair || a.lo) && a.splits == 1 && a.M % (2 * BM) == 0 && !a.timeline && grid % 2 == 0) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(GEMM_THREADS);
