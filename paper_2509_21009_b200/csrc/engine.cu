@@ -155,6 +155,7 @@ struct RpCtx {
   __half *h_lo = nullptr, *q_lo = nullptr, *att_lo = nullptr, *mid_lo = nullptr;
   bool act_lo = true;
   int lo_mask = 0;
+  bool fuse_qkv = true;       // decode attention sums the QKV split partials (RP_FUSE_QKV=0: GEMM epilogue, A/B)
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
   int* gctr = nullptr;
   int* atickets = nullptr;
@@ -608,7 +609,20 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
       ProfScope ps(c, RP_PROF_RMSNORM);
       if (!skipped(c)) launch_rmsnorm(c->x, delta, nullptr, n_dev, n_host, nullptr, c->h, m.d, m.eps, c->st, c->h_lo); c->launches++;
     }
-    if (decode && sp_qkv > 1 && m.hd % 64 == 0) {
+    QkvFuse fz{};
+    const bool fuse = decode && sp_qkv > 1 && m.hd % 64 == 0 && c->fuse_qkv;
+    if (fuse) {
+      // the QKV GEMM writes its split-K partials; the decode attention sums
+      // them per row, applies the folded norm, bias and RoPE, and appends k / v
+      ProfScope ps(c, RP_PROF_GEMM_QKV);
+      gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_PARTIAL, c->qkv, qkvw, w.bqkv, nullptr, f_in);
+      fz.part = c->gpart; fz.splits = sp_qkv; fz.m_tiles = qkvw / 128;
+      fz.gemm_lo = c->act_lo && (c->lo_mask & LO_QKV) ? 1 : 0;
+      fz.n_rows = n_dev; fz.bias = w.bqkv;
+      fz.ssq = f_in == FOLD_CONSUME ? c->ssq : nullptr; fz.ssq_parts = m.d / 128; fz.ssq_stride = m.d / 128;
+      fz.inv_d = 1.0f / (float)m.d; fz.eps = m.eps;
+      fz.cs = c->rope_cs; fz.kv_pool = (uint8_t*)c->rd.kv_pool; fz.page_bytes = m.page_bytes;
+    } else if (decode && sp_qkv > 1 && m.hd % 64 == 0) {
       // RoPE + KV append fused into the split-K reduction of the QKV GEMM
       ProfScope ps(c, RP_PROF_GEMM_QKV);
       RopeArgs ra{c->q, c->q_lo, (uint8_t*)c->rd.kv_pool, c->R.page_table, row_pos, row_pt, c->rope_cs, m.page_bytes,
@@ -623,7 +637,8 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
     }
     { ProfScope ps(c, RP_PROF_ATTN);
       if (!skipped(c)) launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
-                       c->apart, c->atickets, m, l, decode, c->st, c->q_lo, c->att_lo); c->launches++; }
+                       c->apart, c->atickets, m, l, decode, c->st, c->q_lo, c->att_lo, fuse ? &fz : nullptr);
+      c->launches++; }
     { ProfScope ps(c, RP_PROF_GEMM_O);
       gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
            nullptr, nullptr, f_prod, peer ? 0 : -1); }
@@ -806,6 +821,7 @@ static int init_impl(RpCtx* c) {
   c->lo_mask = getenv("RP_LO_MASK") ? (int)strtol(getenv("RP_LO_MASK"), nullptr, 0) : kDefaultLoMask;
   if (!c->act_lo) c->lo_mask = 0;
   c->act_lo = c->lo_mask != 0;
+  c->fuse_qkv = !(getenv("RP_FUSE_QKV") && atoi(getenv("RP_FUSE_QKV")) == 0);
   // producers skip the residuals nobody reads; plans without one map hi only
   if (!(c->lo_mask & (LO_QKV | LO_GU))) c->h_lo = nullptr;
   if (!(c->lo_mask & LO_O)) c->att_lo = nullptr;

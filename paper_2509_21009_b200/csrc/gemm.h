@@ -8,7 +8,9 @@
 
 namespace rp {
 
-enum GemmEpi { EPI_F32 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_BF16 = 3, EPI_QKV_ROPE = 4 };
+// EPI_PARTIAL (split-K only): write the fp32 split partials and stop -- the
+// decode QKV GEMM, whose splits the attention kernel sums (k_attn.cu QkvFuse).
+enum GemmEpi { EPI_F32 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_BF16 = 3, EPI_QKV_ROPE = 4, EPI_PARTIAL = 5 };
 
 // Fused QKV epilogue (decode, split-K path): bias, rotate-half RoPE from a
 // per-position cos/sin table, q -> q_out fp16 [n][H][hd], k/v -> KV page

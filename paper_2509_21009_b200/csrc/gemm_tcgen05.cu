@@ -582,6 +582,13 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       bool last = true;
       int col_lo = 0, col_hi = nc;
       if (split && et == 0 && local == 0) TL(11);   // partials written
+      if (split && a.epi == EPI_PARTIAL) {
+        // the consumer kernel reduces the splits (decode attention sums the
+        // QKV partials of its rows): no ticket, no wait, no epilogue here
+        tc_fence_before();
+        mbar_arrive(tempty0 + 8 * acc);
+        continue;
+      }
       if (split) {
         tc_fence_before();
         mbar_arrive(tempty0 + 8 * acc);     // TMEM stage free for the next item

@@ -88,7 +88,7 @@ struct AttnCfg {
   static constexpr int MR = 8 * NQT;                 // query rows per work unit (<= 8: decode, <= 16: prefill)
   static constexpr int MERGE_FLOATS = CW * MR * (HD + 2);
   static constexpr int THREADS = (CW + 1) * 32;
-  static constexpr int SMEM = AT_STAGES * STAGE_BYTES + MERGE_FLOATS * 4 + 1024 + 256;
+  static constexpr int SMEM = AT_STAGES * STAGE_BYTES + MERGE_FLOATS * 4 + 1024 + 256;   // bars: full, empty, kvready
   static_assert(AT_STAGES % CW == 0, "stage ownership");
 };
 
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
 attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict__ q, const act_t* __restrict__ q_lo,
             const int* __restrict__ page_table, int maxp, const AttnItem* __restrict__ items, const int* n_items_dev,
             int n_items_host, act_t* __restrict__ out, act_t* __restrict__ out_lo, float* __restrict__ partial,
-            int* __restrict__ tickets, ModelDims m, int layer) {
+            int* __restrict__ tickets, ModelDims m, int layer, QkvFuse fz) {
   using C = AttnCfg<HD, CW, NQT>;
   constexpr int MR = C::MR;
   extern __shared__ uint8_t sm_raw[];
@@ -116,6 +116,10 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
   const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(bars);
   const uint32_t empty0 = full0 + 8 * AT_STAGES;
+  // fused QKV reduction (decode): the consumers append the current token's
+  // k / v to its page, then release the producer's load of that page
+  const uint32_t kvready = full0 + 16 * AT_STAGES;
+  const bool fused = NQT == 1 && fz.part != nullptr;
 
   // Decode (NQT == 1): the work list, page tables and every KV page except
   // the one holding a row's current position come from kernels that finished
@@ -134,6 +138,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < AT_STAGES; ++i) { bar_init(full0 + 8 * i, 1); bar_init(empty0 + 8 * i, 1); }
+    bar_init(kvready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -144,18 +149,25 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&kv_map) : "memory");
     bool waited = !kEarly;
     long long gpage = 0;
+    int kvn = 0;                                      // fused: KV-append units so far (kvready parity)
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int it = u / m.KV, kvh = u % m.KV;
       const AttnItem I = items[it];
       const int p_lo = I.kv_lo / kPage, npg = (I.kv_hi + kPage - 1) / kPage - p_lo;
       const int* ptab = page_table + (size_t)I.pt_row * maxp + p_lo;
+      const bool kvu = fused && I.kv_hi == I.pos0 + 1;   // this unit holds the current token
       for (int j0 = 0; j0 < npg; j0 += 32) {
         const int mine = j0 + lane < npg ? ptab[j0 + lane] : 0;   // coalesced page-id batch
         const int cnt = min(32, npg - j0);
         for (int jj = 0; jj < cnt; ++jj) {
           const int page = __shfl_sync(0xffffffffu, mine, jj);
           if (lane == 0) {
-            if (!waited && (p_lo + j0 + jj + 1) * kPage > I.pos0) {
+            if (fused) {
+              if (kvu && (p_lo + j0 + jj) == I.pos0 / kPage) {   // wait for the consumers' append
+                mbar_wait_wd(kvready, (uint32_t)(kvn & 1), 300, it, I.pos0);
+                ++kvn;
+              }
+            } else if (!waited && (p_lo + j0 + jj + 1) * kPage > I.pos0) {
               pdl_wait();
               waited = true;
               if (u == (int)blockIdx.x) ATL(1);
@@ -194,18 +206,92 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
     // ---- Q^T B fragments: qb[nq][kk] = {Q[row][kk*16 + 2tr..], Q[row][kk*16 + 8 + 2tr..]}, row = nq*8 + tq;
     // ql: the same fragments of q's fp16 rounding residual (split precision: S = K q_hi + K q_lo)
     uint32_t qb[NQT][HD / 16][2], ql[NQT][HD / 16][2];
-#pragma unroll
-    for (int nq = 0; nq < NQT; ++nq) {
-      const int r = nq * 8 + tq;
-      const size_t qo = ((size_t)(I.q_row0 + r / g) * m.H + kvh * g + r % g) * HD;
-      const act_t* qr = r < nrows ? q + qo : nullptr;
-      const act_t* qlr = r < nrows && q_lo ? q_lo + qo : nullptr;
+    if (fused) {
+      // the QKV GEMM's split partials of this row, summed in split order,
+      // times the folded-RMSNorm scale, + bias, rotate-half RoPE at pos0
+      float* xs = mrg;                            // [g + 2][HD] pre-RoPE q heads, k, v
+      float* xr = mrg + (size_t)(g + 2) * HD;     // [g + 1][HD] rotated q heads, k
+      __shared__ float s_rsc;
+      const bool kvu = I.kv_hi == I.pos0 + 1;
+      const int nrow = I.q_row0;
+      const int bnx = (fz.gemm_lo && *fz.n_rows <= 128) ? 128 : 256;
+      const int chunk = nrow / bnx, col = nrow % bnx;
+      if (threadIdx.x == 0) {
+        float sc = 1.f;
+        if (fz.ssq) {
+          const float* sp = fz.ssq + (size_t)nrow * fz.ssq_stride;
+          float ss = 0.f;
+          for (int pp = 0; pp < fz.ssq_parts; ++pp) ss += __ldcg(sp + pp);
+          sc = 1.0f / sqrtf(ss * fz.inv_d + fz.eps);
+        }
+        s_rsc = sc;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
+      const float sc = s_rsc;
+      const int ne = (g + (kvu ? 2 : 0)) * HD;
+      for (int e = threadIdx.x; e < ne; e += CW * 32) {
+        const int which = e / HD, d = e % HD;
+        const int mrow = which < g ? (kvh * g + which) * HD + d
+                                   : (which == g ? (m.H + kvh) * HD + d : (m.H + m.KV + kvh) * HD + d);
+        const float* pp = fz.part + ((size_t)((chunk * fz.m_tiles + (mrow >> 7)) * fz.splits) * 256 + col) * 128 +
+                          (mrow & 127);
+        float v = 0.f;
+        for (int sp = 0; sp < fz.splits; ++sp) v += __ldcg(pp + (size_t)sp * 256 * 128);
+        xs[e] = v * sc + fz.bias[mrow];
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
+      const int half = HD / 2;
+      const float2* csp = fz.cs + (size_t)I.pos0 * half;
+      for (int e = threadIdx.x; e < (g + (kvu ? 1 : 0)) * HD; e += CW * 32) {
+        const int base = e - e % HD, d = e % HD;
+        const float2 cs = csp[d % half];
+        xr[e] = d < half ? xs[e] * cs.x - xs[base + d + half] * cs.y : xs[e] * cs.x + xs[base + d - half] * cs.y;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
+      if (kvu) {
+        // append k (rotated) and v to the current token's page slot; the
+        // producer loads that page only after this (kvready)
+        const int page = page_table[(size_t)I.pt_row * maxp + I.pos0 / kPage];
+        act_t* kd = (act_t*)(fz.kv_pool + (size_t)page * fz.page_bytes +
+                             ((size_t)((layer * m.KV + kvh) * 2 + 0) * kPage + I.pos0 % kPage) * HD * 2);
+        act_t* vd = (act_t*)(fz.kv_pool + (size_t)page * fz.page_bytes +
+                             ((size_t)((layer * m.KV + kvh) * 2 + 1) * kPage + I.pos0 % kPage) * HD * 2);
+        for (int d = threadIdx.x; d < HD; d += CW * 32) {
+          kd[d] = to_act(xr[g * HD + d]);
+          vd[d] = to_act(xs[(g + 1) * HD + d]);
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence_block();
+        asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
+        if (threadIdx.x == 0) bar_arrive(kvready);
+      }
+      const float* qr = tq < nrows ? xr + (size_t)tq * HD : nullptr;   // decode: row tq = head tq of this KV head
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
-        qb[nq][kk][0] = qr ? *(const uint32_t*)(qr + kk * 16 + 2 * tr) : 0u;
-        qb[nq][kk][1] = qr ? *(const uint32_t*)(qr + kk * 16 + 8 + 2 * tr) : 0u;
-        ql[nq][kk][0] = qlr ? *(const uint32_t*)(qlr + kk * 16 + 2 * tr) : 0u;
-        ql[nq][kk][1] = qlr ? *(const uint32_t*)(qlr + kk * 16 + 8 + 2 * tr) : 0u;
+        float2 a0 = qr ? make_float2(qr[kk * 16 + 2 * tr], qr[kk * 16 + 2 * tr + 1]) : make_float2(0.f, 0.f);
+        float2 a1 = qr ? make_float2(qr[kk * 16 + 8 + 2 * tr], qr[kk * 16 + 9 + 2 * tr]) : make_float2(0.f, 0.f);
+        const act2_t h0 = to_act2(a0.x, a0.y), h1 = to_act2(a1.x, a1.y);
+        qb[0][kk][0] = *(const uint32_t*)&h0;
+        qb[0][kk][1] = *(const uint32_t*)&h1;
+        const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+        const act2_t l0 = to_act2(a0.x - f0.x, a0.y - f0.y), l1 = to_act2(a1.x - f1.x, a1.y - f1.y);
+        ql[0][kk][0] = q_lo ? *(const uint32_t*)&l0 : 0u;
+        ql[0][kk][1] = q_lo ? *(const uint32_t*)&l1 : 0u;
+      }
+    } else {
+#pragma unroll
+      for (int nq = 0; nq < NQT; ++nq) {
+        const int r = nq * 8 + tq;
+        const size_t qo = ((size_t)(I.q_row0 + r / g) * m.H + kvh * g + r % g) * HD;
+        const act_t* qr = r < nrows ? q + qo : nullptr;
+        const act_t* qlr = r < nrows && q_lo ? q_lo + qo : nullptr;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          qb[nq][kk][0] = qr ? *(const uint32_t*)(qr + kk * 16 + 2 * tr) : 0u;
+          qb[nq][kk][1] = qr ? *(const uint32_t*)(qr + kk * 16 + 8 + 2 * tr) : 0u;
+          ql[nq][kk][0] = qlr ? *(const uint32_t*)(qlr + kk * 16 + 2 * tr) : 0u;
+          ql[nq][kk][1] = qlr ? *(const uint32_t*)(qlr + kk * 16 + 8 + 2 * tr) : 0u;
+        }
       }
     }
     // this thread's two query columns per n-tile: rows nq*8 + 2tr + e
@@ -487,8 +573,10 @@ int make_kv_map(CUtensorMap* map, const void* pool, size_t n_pages, const ModelD
 void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_table, int maxp,
                       const AttnItem* items, const int* n_items_dev, int n_items_host, void* out, float* partial,
                       int* tickets, const ModelDims& m, int layer, bool decode, cudaStream_t st, const void* q_lo,
-                      void* out_lo) {
+                      void* out_lo, const QkvFuse* fuse) {
   const dim3 grid(148);   // one wave, persistent over the flat (item, KV head) units
+  QkvFuse fz{};
+  if (fuse && decode) fz = *fuse;
   const auto* qq = (const act_t*)q;
   const auto* ql = (const act_t*)q_lo;
   auto* oo = (act_t*)out;
@@ -496,17 +584,17 @@ void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_
   if (m.hd == 128) {
     if (decode)
       launch_pdl(attn_kernel<128, 6, 1>, grid, dim3(AttnDec128::THREADS), AttnDec128::SMEM, st, kv_map, qq, ql,
-                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer);
+                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer, fz);
     else
       launch_pdl(attn_kernel<128, 3, 2>, grid, dim3(AttnPre128::THREADS), AttnPre128::SMEM, st, kv_map, qq, ql,
-                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer);
+                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer, fz);
   } else {
     if (decode)
       launch_pdl(attn_kernel<64, 6, 1>, grid, dim3(AttnDec64::THREADS), AttnDec64::SMEM, st, kv_map, qq, ql,
-                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer);
+                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer, fz);
     else
       launch_pdl(attn_kernel<64, 3, 2>, grid, dim3(AttnPre64::THREADS), AttnPre64::SMEM, st, kv_map, qq, ql,
-                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer);
+                 page_table, maxp, items, n_items_dev, n_items_host, oo, ol, partial, tickets, m, layer, fz);
   }
 }
 

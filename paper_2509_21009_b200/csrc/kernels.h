@@ -135,11 +135,26 @@ void launch_rope_append(const float* qkv, const int* n_dev, int n_host, const in
                         const int* page_table, int maxp, void* q_out, void* kv_pool, const ModelDims& m, int layer,
                         const double* inv_freq, cudaStream_t st, void* q_lo = nullptr);
 int make_kv_map(CUtensorMap* map, const void* pool, size_t n_pages, const ModelDims& m);
+// Decode attention fused with the QKV GEMM's split-K reduction (EPI_PARTIAL):
+// each work unit sums its row's q partials (and, for the unit holding the
+// current token, k and v) in split order, applies the folded RMSNorm scale,
+// the bias and RoPE, appends k / v to the KV page and uses q directly.
+struct QkvFuse {
+  const float* part;      // split partials [(chunk * m_tiles + tile) * splits + split][256][128]; nullptr = off
+  int splits, m_tiles;
+  int gemm_lo;            // the QKV GEMM ran split precision: 128-column chunks while the live count <= 128
+  const int* n_rows;      // live rows of the step (device)
+  const float* bias;      // bqkv [M]
+  const float* ssq; int ssq_parts, ssq_stride; float inv_d, eps;   // folded RMSNorm (ssq == nullptr: none)
+  const float2* cs;       // RoPE (cos, sin) [pos][hd / 2]
+  uint8_t* kv_pool; size_t page_bytes;
+};
+
 void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_table, int maxp,
                       const AttnItem* items, const int* n_items_dev, int n_items_host, void* out, float* partial,
                       int* tickets /* [items x KV], zero, self-resetting */, const ModelDims& m, int layer,
                       bool decode /* <= 8 query rows per unit */, cudaStream_t st, const void* q_lo = nullptr,
-                      void* out_lo = nullptr);
+                      void* out_lo = nullptr, const QkvFuse* fuse = nullptr);
 void launch_kv_fork(const int* jobs /*[n][3] src,dst,rows*/, int n, void* kv_pool, const ModelDims& m,
                     cudaStream_t st);
 void launch_sampler(const float* logits, int V, int v0, int row_div, const RoundDev& R, uint64_t seed,

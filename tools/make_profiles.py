@@ -17,6 +17,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__sass_inst_executed_op_utcmma.sum", "lts__t_bytes.sum",
         "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
         "launch__shared_mem_per_block_dynamic"]
 SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0}
@@ -82,10 +85,13 @@ def main():
         for r in recs:
             t = r.get("gpu__time_duration.sum", 0)
             rd, wr = r.get("dram__bytes_read.sum", 0), r.get("dram__bytes_write.sum", 0)
-            lines.append("%-28s %8.1f us  DRAM %7.1f MB (%5.1f%% of peak)  SM %5.1f%%  issue %5.1f%%  regs %s  grid %s" % (
+            lines.append("%-28s %8.1f us  DRAM %7.1f MB (%5.1f%% of peak)  SM %5.1f%%  tcgen05 pipe %5.1f%%  "
+                         "UTCMMA %8s  issue %5.1f%%  regs %s  grid %s" % (
                 r["kernel"][:28], t * 1e6, (rd + wr) / 1e6,
                 r.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 0),
                 r.get("sm__throughput.avg.pct_of_peak_sustained_elapsed", 0),
+                r.get("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active", 0) or 0,
+                r.get("smsp__sass_inst_executed_op_utcmma.sum", "?"),
                 r.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0),
                 r.get("launch__registers_per_thread", "?"), r.get("launch__grid_size", "?")))
     if lfile:
@@ -101,7 +107,8 @@ def main():
     for label, recs in summary["reports"].items():
         shape = os.environ.get("SHAPE_" + label, label)
         traffic["%s_%s" % (tag, label)] = {
-            "shape": shape, "source": "profiles/%s_ncu_summary.json (ncu --set full, one decode step)" % tag,
+            "shape": shape, "rows": int(os.environ.get("ROWS_" + label, "0")),
+            "source": "profiles/%s_ncu_summary.json (ncu --set full, one decode step)" % tag,
             "dram_bytes_per_launch": {k: r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0)
                                       for k, r in zip(order, recs)},
             "ncu_duration_us": {k: 1e6 * r.get("gpu__time_duration.sum", 0) for k, r in zip(order, recs)}}
