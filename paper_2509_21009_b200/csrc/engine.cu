@@ -155,7 +155,9 @@ struct RpCtx {
   __half *h_lo = nullptr, *q_lo = nullptr, *att_lo = nullptr, *mid_lo = nullptr;
   bool act_lo = true;
   int lo_mask = 0;
-  bool fuse_qkv = true;       // decode attention sums the QKV split partials (RP_FUSE_QKV=0: GEMM epilogue, A/B)
+  // decode attention sums the QKV split partials (RP_FUSE_QKV=1; off by
+  // default: measured slower, profiles/r02_fused_qkv_ab.txt)
+  bool fuse_qkv = false;
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
   int* gctr = nullptr;
   int* atickets = nullptr;
@@ -821,7 +823,7 @@ static int init_impl(RpCtx* c) {
   c->lo_mask = getenv("RP_LO_MASK") ? (int)strtol(getenv("RP_LO_MASK"), nullptr, 0) : kDefaultLoMask;
   if (!c->act_lo) c->lo_mask = 0;
   c->act_lo = c->lo_mask != 0;
-  c->fuse_qkv = !(getenv("RP_FUSE_QKV") && atoi(getenv("RP_FUSE_QKV")) == 0);
+  c->fuse_qkv = getenv("RP_FUSE_QKV") && atoi(getenv("RP_FUSE_QKV")) != 0;
   // producers skip the residuals nobody reads; plans without one map hi only
   if (!(c->lo_mask & (LO_QKV | LO_GU))) c->h_lo = nullptr;
   if (!(c->lo_mask & LO_O)) c->att_lo = nullptr;

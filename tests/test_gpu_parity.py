@@ -434,6 +434,15 @@ def test_decode_step_logits(tiny, oracle_w):
     eng.close()
 
 
+def test_decode_step_logits_fused_qkv(tiny, oracle_w, monkeypatch):
+    """The optional fused path (RP_FUSE_QKV=1, profiles/r02_fused_qkv_ab.txt):
+    the decode attention sums the QKV GEMM's split partials, applies the
+    folded norm, bias and RoPE and appends k / v itself."""
+    monkeypatch.setenv("RP_FUSE_QKV", "1")
+    test_decode_step_logits(tiny, oracle_w)
+    test_sampled_tokens_trace_mode(tiny, oracle_w)
+
+
 def test_invalid_arguments(tiny):
     from paper_2509_21009_b200 import rp
     eng = make_engine(tiny, graph_steps=0)
