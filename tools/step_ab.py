@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--ctx", type=int, default=1024)
     ap.add_argument("--tag", default="")
     ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--G", type=int, default=8, help="responses per prompt (1: no sibling sharing)")
     a = ap.parse_args()
     import torch
     from paper_2509_21009_b200 import rp
@@ -32,7 +33,7 @@ def main():
     torch.cuda.set_device(0)
     cfg = configs.model_config(a.model, n_layers=a.layers or None)
     batches = [int(x) for x in a.batches.split(",")]
-    G, cap = 8, 64
+    G, cap = a.G, 64
     maxb = max(batches)
     eng = rp.Engine(cfg, max_seqs=maxb, max_prompts=maxb // G, max_prompt_len=a.ctx,
                     max_prompt_tokens=maxb // G * a.ctx, max_cap=cap, graph_steps=16, kv_fraction=0.5)
@@ -55,7 +56,7 @@ def main():
         eng.run()
         eng.collect()
         tot = sum(p["ms"].values())
-        row = dict(tag=a.tag, B=B, ctx=a.ctx, graph_step_ms=round(graph_ms, 4), eager_step_ms=round(tot / p["steps"], 4),
+        row = dict(tag=a.tag, B=B, G=G, ctx=a.ctx, graph_step_ms=round(graph_ms, 4), eager_step_ms=round(tot / p["steps"], 4),
                    cls={k: round(v / p["steps"] * 1e3 / max(1, p["launches"][k] / p["steps"]), 2)
                         for k, v in p["ms"].items() if v > 0})
         print(json.dumps(row), flush=True)
