@@ -158,6 +158,7 @@ struct RpCtx {
   // decode attention sums the QKV split partials (RP_FUSE_QKV=1; off by
   // default: measured slower, profiles/r02_fused_qkv_ab.txt)
   bool fuse_qkv = false;
+  int ag_dbg = 0;                         // RP_AG_DBG: group-attention measurement knobs (k_attn_group.cu)
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
   int* gctr = nullptr;
   int* atickets = nullptr;
@@ -300,7 +301,11 @@ static Sizes compute_sizes(const rp_model_desc* md, const rp_runtime_desc* rd) {
   }
   // rp_debug_gemm may request splits of an arbitrary shape: keep >= 16M floats
   z.part_floats = std::max(mx, (size_t)1 << 24);
-  z.apart_floats = (size_t)std::max(z.max_items_dec, z.max_items_pre) * lm.KV * 16 * (lm.hd + 2);
+  // attention split partials: per-row items (16 rows of (m, l, O)) or
+  // sibling-group items (8 members x 8 rows)
+  z.apart_floats = std::max((size_t)z.max_items_dec * lm.KV * std::max((size_t)16 * (lm.hd + 2),
+                                                                       attn_group_partial_floats(lm.hd)),
+                            (size_t)z.max_items_pre * lm.KV * 16 * (lm.hd + 2));
   return z;
 }
 
@@ -360,7 +365,9 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto atick = cv.take<int>((size_t)std::max(z.max_items_dec, z.max_items_pre) * KV);
   auto invf = cv.take<double>(hd / 2);
   auto rope_cs = cv.take<float2>((size_t)(rd->max_prompt_len + rd->max_cap + 2) * (hd / 2));
-  auto items_dec = cv.take<AttnItem>(z.max_items_dec);
+  auto items_dec = cv.take<AttnGroupItem>(z.max_items_dec);   // AttnItem or AttnGroupItem (RoundDev.attn_group)
+  auto grp_key = cv.take<int>(z.S);
+  auto grp_start = cv.take<int>((size_t)z.S + 1);
   auto rows_hist = cv.take<unsigned long long>((size_t)z.S + 1);
   auto items_pre = cv.take<AttnItem>(z.max_items_pre);
   auto pre_tok = cv.take<int>(rd->max_prompt_tokens);
@@ -432,7 +439,8 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
     R.max_items = z.max_items_dec;
     R.p_plen = p_plen; R.p_adm = p_adm; R.p_wait = p_wait; R.p_live = p_live; R.p_pfree = p_pfree;
     R.p_pneed = p_pneed; R.wait_q = wait_q; R.rejobs = rejobs;
-    R.best = best; R.items = items_dec; R.rows_hist = rows_hist; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
+    R.grp_key = grp_key; R.grp_start = grp_start;
+    R.best = best; R.items = reinterpret_cast<AttnItem*>(items_dec); R.rows_hist = rows_hist; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
     R.ctl = ctl; R.cap = rd->max_cap;
   }
   return align_up(cv.off);
@@ -638,8 +646,17 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
                            c->rd.kv_pool, m, l, c->inv_freq, c->st, c->q_lo); c->launches++; }
     }
     { ProfScope ps(c, RP_PROF_ATTN);
-      if (!skipped(c)) launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
-                       c->apart, c->atickets, m, l, decode, c->st, c->q_lo, c->att_lo, fuse ? &fz : nullptr);
+      if (skipped(c)) {
+      } else if (decode && c->R.attn_group) {
+        launch_attention_group(c->kv_map, c->q, c->q_lo, c->R.page_table, c->R.maxp,
+                               reinterpret_cast<const AttnGroupItem*>(items), n_items_dev, c->att, c->att_lo, c->apart,
+                               c->atickets, m, l, c->st, c->ag_dbg, c->lg ? 0 : 1);
+      } else {
+        fz.dbg = c->ag_dbg;
+        launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
+                         c->apart, c->atickets, m, l, decode, c->st, c->q_lo, c->att_lo,
+                         fuse || c->ag_dbg ? &fz : nullptr);
+      }
       c->launches++; }
     { ProfScope ps(c, RP_PROF_GEMM_O);
       gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
@@ -801,7 +818,7 @@ static int init_impl(RpCtx* c) {
   CK(cudaMemsetAsync(rd->kv_pool, 0, (size_t)c->n_pages * m.page_bytes, c->st));
   workspace_bytes(md, rd, c);
   if (gemm_init_attrs()) return c->fail(RP_ECUDA, "gemm smem attribute");
-  if (attn_init_attrs()) return c->fail(RP_ECUDA, "attention smem attribute");
+  if (attn_init_attrs() || attn_group_init_attrs()) return c->fail(RP_ECUDA, "attention smem attribute");
 
   // ---- weights (formula Z12), layout per layer
   uint8_t* wb = (uint8_t*)rd->weights;
@@ -824,6 +841,10 @@ static int init_impl(RpCtx* c) {
   if (!c->act_lo) c->lo_mask = 0;
   c->act_lo = c->lo_mask != 0;
   c->fuse_qkv = getenv("RP_FUSE_QKV") && atoi(getenv("RP_FUSE_QKV")) != 0;
+  // decode attention over sibling groups (g <= 8 query heads per KV head fit
+  // one n-tile per member); RP_ATTN_GROUP=0 keeps the per-row kernel, 2 / 3 force sibling groups / single rows (A/B)
+  c->ag_dbg = getenv("RP_AG_DBG") ? atoi(getenv("RP_AG_DBG")) : 0;
+  c->R.attn_group = c->fuse_qkv || m.H / m.KV > 8 ? 0 : (getenv("RP_ATTN_GROUP") ? atoi(getenv("RP_ATTN_GROUP")) : 1);
   // producers skip the residuals nobody reads; plans without one map hi only
   if (!(c->lo_mask & (LO_QKV | LO_GU))) c->h_lo = nullptr;
   if (!(c->lo_mask & LO_O)) c->att_lo = nullptr;

@@ -10,7 +10,7 @@ namespace rp {
 
 // EPI_PARTIAL (split-K only): write the fp32 split partials and stop -- the
 // decode QKV GEMM, whose splits the attention kernel sums (k_attn.cu QkvFuse).
-enum GemmEpi { EPI_F32 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_BF16 = 3, EPI_QKV_ROPE = 4, EPI_PARTIAL = 5 };
+enum GemmEpi { EPI_F32 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_ACT = 3, EPI_QKV_ROPE = 4, EPI_PARTIAL = 5 };
 
 // Fused QKV epilogue (decode, split-K path): bias, rotate-half RoPE from a
 // per-position cos/sin table, q -> q_out fp16 [n][H][hd], k/v -> KV page
@@ -45,7 +45,7 @@ struct GemmArgs {
   int epi;                // GemmEpi
   void* out;              // out[n * ldo + m] (SWIGLU: out[n * ldo + feature])
   int ldo;
-  const float* bias;      // [M] or nullptr (EPI_F32 / EPI_BF16)
+  const float* bias;      // [M] or nullptr (EPI_F32 / EPI_ACT)
   float* partial;         // split-K partials (splits > 1)
   int* counters;          // split-K tickets, zero-initialised, self-resetting
   long long* timeline;    // debug: per-CTA %globaltimer stamps [grid][16] (nullptr = off)

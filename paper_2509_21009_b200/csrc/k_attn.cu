@@ -20,53 +20,13 @@
 #include <cuda.h>
 #include "common.cuh"
 #include "kernels.h"
+#include "attn_mma.cuh"
 
 namespace rp {
 
 constexpr int AT_STAGES = 6;   // 64-token stages.  Stage s is always consumed by warp s % CW (CW divides
                                // AT_STAGES): mbarrier parity only tells adjacent phases apart, so every
                                // waiter must consume its stage's uses in order.
-
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
-}
-__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t movtrans(uint32_t x) {
-  uint32_t y;
-  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
-  return y;
-}
-__device__ __forceinline__ uint32_t pack_act(float lo, float hi) {
-  act2_t v = to_act2(lo, hi);
-  return *(uint32_t*)&v;
-}
-__device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void bar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void bar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          dst),
-      "l"(map), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
 
 // debug timeline (RP_ATTN_TIMELINE): per CTA, %globaltimer marks of its first
 // unit -- [0] start, [1] producer past the dependency wait, [2] first page
@@ -92,12 +52,6 @@ struct AttnCfg {
   static_assert(AT_STAGES % CW == 0, "stage ownership");
 };
 
-// byte offset of (row, 16-byte chunk) in a [64][HD] tile stored as HD/64
-// SWIZZLE_128B boxes of [64][64]
-__device__ __forceinline__ uint32_t swz(int row, int chunk) {
-  return (uint32_t)((chunk >> 3) * 8192 + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
-}
-
 // S^T = K Q^T: the key tokens are the MMA rows (m16) and the <= 8 query rows
 // of a work unit are the n8 columns, so no MMA lane is padding; P^T reaches
 // the PV MMA through movmatrix.trans; O^T = V^T P^T keeps head_dim on the rows.
@@ -120,6 +74,8 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
   // k / v to its page, then release the producer's load of that page
   const uint32_t kvready = full0 + 16 * AT_STAGES;
   const bool fused = NQT == 1 && fz.part != nullptr;
+  const bool skip_mma = fz.dbg & 1;
+  if (fz.dbg & 2) q_lo = nullptr;
 
   // Decode (NQT == 1): the work list, page tables and every KV page except
   // the one holding a row's current position come from kernels that finished
@@ -318,6 +274,11 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
       const int st = (int)(gp % AT_STAGES);
       mbar_wait_wd(full0 + 8 * st, (uint32_t)((gp / AT_STAGES) & 1), 200 + st, gp, (long long)it * 1000 + npg);
       if (threadIdx.x == 0 && j == 0 && u == (int)blockIdx.x) ATL(2);
+      if (skip_mma) {
+        __syncwarp();
+        if (lane == 0) bar_arrive(empty0 + 8 * st);
+        continue;
+      }
       const uint32_t kt = sbase + st * C::STAGE_BYTES, vt = kt + C::TILE_BYTES;
       const int tok0 = (p_lo + j) * kPage;
       // ---- S^T = K Q^T (64 tokens x query rows): 4 token tiles of 16
@@ -577,6 +538,7 @@ void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_
   const dim3 grid(148);   // one wave, persistent over the flat (item, KV head) units
   QkvFuse fz{};
   if (fuse && decode) fz = *fuse;
+  if (fuse) fz.dbg = fuse->dbg;
   const auto* qq = (const act_t*)q;
   const auto* ql = (const act_t*)q_lo;
   auto* oo = (act_t*)out;

@@ -478,8 +478,9 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
         } else if (need) {
           R.page_table[(size_t)s * R.maxp + kv / kPage] = R.free_stack[top - 1 - (alloc + oa)];
         }
+        if (R.attn_group) R.grp_key[pos] = R.slot_prompt[s] * ((R.G + 7) / 8) + R.slot_j[s] / 8;
         const int it0 = items + oi;
-        for (int sp = 0; sp < ns; ++sp) {
+        for (int sp = 0; sp < ns && !R.attn_group; ++sp) {
           AttnItem I;
           I.q_row0 = pos; I.n_qtok = 1; I.pos0 = kv; I.pt_row = s;
           I.kv_lo = sp * chunk; I.kv_hi = min(kv + 1, (sp + 1) * chunk);
@@ -491,6 +492,86 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     }
   }
   __syncthreads();
+  if (R.attn_group && !s_err) {
+    // Sibling groups (k_attn_group.cu): maximal runs of next-step rows with
+    // the same (prompt, j / 8) -- siblings are adjacent in the live list (slot
+    // order, order-preserving compaction).  A group's work is its longest
+    // member's pages over the warps a member pair gets (rep); splits as for
+    // rows: ns_g = max(1, floor(c_g * U / sum c)) with U <= 3 * U1 whole
+    // waves, so items <= groups + U <= S + 3 * U1 (the work-list capacity).
+    int ng = 0;
+    for (int base = 0; base < kept; base += CTL_THREADS) {
+      const int pos = base + tid;
+      const int st = pos < kept && (pos == 0 || R.grp_key[pos] != R.grp_key[pos - 1]);
+      int tot;
+      const int o = block_exscan(st, &tot, scan_sm);
+      if (st) R.grp_start[ng + o] = pos;
+      ng += tot;
+    }
+    // Few sibling groups (ng < U1 / 6, e.g. 16 rows of 2 prompts) would need
+    // ~U1 / ng page splits per group to fill the wave, and the partials and
+    // merges of so many splits cost more than the shared fills save: every row
+    // becomes its own group (8 warps split its pages, as the per-row list did).
+    // Measured crossover: profiles/r02_attn_group_ab.txt.  attn_group 2 / 3
+    // force sibling groups / single rows (A/B).
+    if (R.attn_group == 3 || (R.attn_group == 1 && ng * 6 < U1)) {
+      for (int pos = tid; pos < kept; pos += CTL_THREADS) R.grp_start[pos] = pos;
+      ng = kept;
+    }
+    if (tid == 0) R.grp_start[ng] = kept;
+    __syncthreads();
+    auto gcost = [&](int gi, int& w, int& nm, int& rep) {
+      const int p0 = R.grp_start[gi];
+      nm = min(8, R.grp_start[gi + 1] - p0);
+      w = 0;
+      for (int x = 0; x < nm; ++x) w = max(w, pages_of(R.row_pos[p0 + x] + 1));
+      rep = nm > 4 ? 1 : (nm > 2 ? 2 : (nm > 1 ? 4 : 8));   // warps per member of the 8 (k_attn_group.cu)
+      return (w + rep - 1) / rep;
+    };
+    long long csum = 0;
+    for (int base = 0; base < ng; base += CTL_THREADS) {
+      const int gi = base + tid;
+      int w, nm, rep, c = 0, tot;
+      if (gi < ng) c = gcost(gi, w, nm, rep);
+      block_exscan(c, &tot, scan_sm);
+      csum += tot;
+    }
+    csum = max(1LL, csum);
+    const int Ug = U1 * min(3, max(1, (ng + U1 - 1) / U1));
+    AttnGroupItem* gitems = reinterpret_cast<AttnGroupItem*>(R.items);
+    items = 0;
+    for (int base = 0; base < ng; base += CTL_THREADS) {
+      const int gi = base + tid;
+      int w = 0, nm = 0, rep = 1, ns = 0, chunk = 1;
+      if (gi < ng) {
+        const int c = gcost(gi, w, nm, rep);
+        const int want = (int)max(1LL, min(32LL, (long long)c * Ug / csum));   // <= 32: the merge's smem
+        chunk = (w + want - 1) / want;
+        ns = (w + chunk - 1) / chunk;
+      }
+      int tot;
+      const int o = block_exscan(ns, &tot, scan_sm);
+      if (gi < ng) {
+        const int p0 = R.grp_start[gi], it0 = items + o;
+        AttnGroupItem I;
+        I.n_mem = nm; I.nsplit = ns; I.item0 = it0; I.rep = rep; I.pad = 0;
+        int snp = 1 << 30;
+        for (int x = 0; x < 8; ++x) {
+          const int s = x < nm ? R.live_next[p0 + x] : 0;
+          I.q_row[x] = x < nm ? p0 + x : 0;
+          I.pt_row[x] = s;
+          I.pos0[x] = x < nm ? R.row_pos[p0 + x] : -1;
+          if (x < nm) snp = min(snp, min(R.own0[s], R.row_pos[p0 + x] / kPage));
+        }
+        I.shared_np = snp;
+        for (int sp = 0; sp < ns; ++sp) {
+          I.pg_lo = sp * chunk; I.pg_hi = min(w, (sp + 1) * chunk);
+          if (it0 + sp < R.max_items) gitems[it0 + sp] = I;
+        }
+      }
+      items += tot;
+    }
+  }
   for (int i = tid; i < n; i += CTL_THREADS) R.best[i] = 0ull;
   for (int i = tid; i < kept; i += CTL_THREADS) R.live[i] = R.live_next[i];
   if (tid == 0) {

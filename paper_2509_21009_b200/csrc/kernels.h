@@ -27,6 +27,21 @@ struct AttnItem {
   int item0;    // index of the block's first item (partials of split s at item0+s)
 };
 
+// Decode attention over a group of <= 8 live siblings of one prompt
+// (k_attn_group.cu): the shared prompt pages are read once for every member.
+struct AttnGroupItem {
+  int n_mem;        // members (live rows), <= 8
+  int shared_np;    // leading pages shared by every member (identical page ids)
+  int pg_lo, pg_hi; // page-index range of this split
+  int nsplit;       // splits of the group (1 -> outputs written directly)
+  int item0;        // the group's first item (split s: partials at item0 + s)
+  int rep;          // consumer warps per member: 1 (5-8 members), 2 (3-4), 4 (2), 8 (1)
+  int pad;
+  int q_row[8];     // members' rows in q / attn_out (next-step live positions)
+  int pt_row[8];    // members' page-table rows (slots)
+  int pos0[8];      // members' current positions (keys <= pos0 visible)
+};
+
 struct CtlBlock {
   int n_live;       // rows decoded by the next step on this rank (0 => idle)
   int t;            // step index the next decode step produces
@@ -74,6 +89,10 @@ struct RoundDev {
   int* rejobs;        // [S][5] recompute jobs: slot, g, fork src page, fork dst page, fork rows
   int attn_units;     // decode-attention split budget per KV head (0: 148 / KV)
   int attn_waves;     // 1: budget whole waves of attention units (k-wave fill), 0: one-wave floor
+  int attn_group;     // decode work list: 0 per-row AttnItem (k_attn.cu); AttnGroupItem (k_attn_group.cu) of
+                      // 1 sibling groups unless too few (then single rows), 2 always sibling groups, 3 always single rows
+  int* grp_key;       // [S] scratch: (prompt, j / 8) of each next-step row
+  int* grp_start;     // [S + 1] scratch: first row of each group
   int world, rank;
   int max_items;      // capacity of `items` (ctl flags err 3 rather than overflow it)
   int* slot_prompt; int* slot_j; int* kv_len; int* gen; int* trace_L; int* status; int* own0;
@@ -148,6 +167,7 @@ struct QkvFuse {
   const float* ssq; int ssq_parts, ssq_stride; float inv_d, eps;   // folded RMSNorm (ssq == nullptr: none)
   const float2* cs;       // RoPE (cos, sin) [pos][hd / 2]
   uint8_t* kv_pool; size_t page_bytes;
+  int dbg;                // RP_AG_DBG measurement knobs (also without the fusion): 1 no MMAs, 2 no q_lo MMAs
 };
 
 void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_table, int maxp,
@@ -155,6 +175,13 @@ void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_
                       int* tickets /* [items x KV], zero, self-resetting */, const ModelDims& m, int layer,
                       bool decode /* <= 8 query rows per unit */, cudaStream_t st, const void* q_lo = nullptr,
                       void* out_lo = nullptr, const QkvFuse* fuse = nullptr);
+// sibling-group decode attention (RoundDev.attn_group; g = H / KV <= 8)
+void launch_attention_group(const CUtensorMap& kv_map, const void* q, const void* q_lo, const int* page_table,
+                            int maxp, const AttnGroupItem* items, const int* n_items_dev, void* out, void* out_lo,
+                            float* partial, int* tickets, const ModelDims& m, int layer, cudaStream_t st,
+                            int dbg = 0, int may_spin = 1 /* 0 in single-GPU local groups */);
+int attn_group_init_attrs();
+size_t attn_group_partial_floats(int hd);   // per (item, KV head)
 void launch_kv_fork(const int* jobs /*[n][3] src,dst,rows*/, int n, void* kv_pool, const ModelDims& m,
                     cudaStream_t st);
 void launch_sampler(const float* logits, int V, int v0, int row_div, const RoundDev& R, uint64_t seed,

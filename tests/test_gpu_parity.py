@@ -495,3 +495,48 @@ def test_decode_long_context_split_kv(tiny, oracle_w):
         worst = max(worst, float(np.max(np.abs(lg[row] - want))))
     assert len(seq) > 600 and worst <= LOGIT_TOL, (len(seq), worst)
     eng.close()
+
+
+@pytest.mark.parametrize("model", ["tiny", "tiny-kv8"])
+@pytest.mark.parametrize("G", [1, 3, 8, 10])
+@pytest.mark.parametrize("mode", ["auto", "group", "single", "rows"])
+def test_decode_attention_sibling_groups(model, G, mode, monkeypatch):
+    """Decode attention over sibling groups (k_attn_group.cu: the default
+    'auto', forced sibling groups, forced single rows) and the per-row kernel
+    (RP_ATTN_GROUP=0, k_attn.cu): logits of eager decode steps vs
+    the oracle teacher-forced on the GPU's own history, for groups of 1-8
+    members (rep 4 / 2 / 1 warps per member pair), a G = 10 prompt split into
+    groups of 8 and 2, siblings dying mid-round (groups shrink), head_dim 64
+    (g = 2) and 128 (g = 5), and ~650-token contexts cut into many page
+    splits merged per member."""
+    monkeypatch.setenv("RP_ATTN_GROUP", {"auto": "1", "group": "2", "single": "3", "rows": "0"}[mode])
+    cfg = configs.model_config(model)
+    w = weights.Weights(cfg, configs.WEIGHT_SEED)
+    eng = make_engine(cfg, graph_steps=0, max_cap=640, max_seqs=32, max_prompt_len=160, kv_pool_bytes=256 << 20)
+    n = 2
+    ps = gen.prompts(n, 0, cfg["eos_id"], (100, 130), 91 + G)
+    L = np.full((n, G), 600, np.int32)
+    L[:, : G // 2] = 40 + 7 * np.arange(G // 2)          # the first half of the siblings end early
+    eng.debug_trace_enable(700)
+    eng.submit(ps, G, 640, n, long_round=True, trace=L, round_id=5)
+    caps, cur = {}, 1                                     # rp_submit_round decodes step 1
+    for t_stop in (3, 45, 560):
+        st = eng.step(t_stop - cur)
+        cur = st.t
+        lg, slots = eng.debug_last_logits()
+        caps[st.t] = (lg.copy(), slots.copy())
+    eng.run()
+    res = eng.collect()
+    eng.close()
+    toks = {(r["prompt_id"] - ps[0]["prompt_id"], r["j"]): r["tokens"] for r in res}
+    worst, rows = 0.0, 0
+    for t, (lg, slots) in caps.items():
+        for row, s in enumerate(slots):
+            p, j = divmod(int(s), G)
+            if j % 3 and row % 2:                         # a sample of the rows keeps the oracle cheap
+                continue
+            seq = np.concatenate([ps[p]["tokens"], toks[(p, j)][:t - 1]])
+            want = decoder.logits(w, seq, rows=[len(seq) - 1])[0]
+            worst = max(worst, float(np.max(np.abs(lg[row] - want))))
+            rows += 1
+    assert max(caps) >= 560 and rows >= 4 and worst <= LOGIT_TOL, (caps.keys(), rows, worst)
