@@ -36,6 +36,13 @@ __device__ __forceinline__ void store_act4(act_t* hi, act_t* lo, float4 v) {
 
 
 constexpr int kPage = 64;          // tokens per KV page (DESIGN.md §5 D1)
+// KV pool layout: [L][n_pages][KV][K|V][kPage][hd] fp16, layer-major, so the pages one
+// layer's attention reads lie in one contiguous [n_pages][KV][2][kPage][hd] slab (16 pages of the 7B
+// shape per 2 MB TLB entry instead of one): element offset of the (layer, page, kv head, K|V) block.
+__host__ __device__ __forceinline__ size_t kv_block_elems(int layer, int page, int kvh, int kv, int n_pages, int KV,
+                                                          int hd) {
+  return (((((size_t)layer * n_pages + page) * KV + kvh) * 2 + kv) * kPage) * hd;
+}
 constexpr int kAttnChunk = 512;    // tokens per decode-attention split
 constexpr int kAttnFillUnits = 2 * 148;  // (row, kv head) units that fill the GPU without splits
 

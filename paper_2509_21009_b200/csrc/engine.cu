@@ -158,7 +158,8 @@ struct RpCtx {
   // decode attention sums the QKV split partials (RP_FUSE_QKV=1; off by
   // default: measured slower, profiles/r02_fused_qkv_ab.txt)
   bool fuse_qkv = false;
-  int ag_dbg = 0;                         // RP_AG_DBG: group-attention measurement knobs (k_attn_group.cu)
+  int ag_dbg = 0;
+  int gemm_rows_max = 0;                  // rows bound of the current forward (decode bucket / prefill tokens)                         // RP_AG_DBG: group-attention measurement knobs (k_attn_group.cu)
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
   int* gctr = nullptr;
   int* atickets = nullptr;
@@ -561,6 +562,7 @@ static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, in
   a.M = M; a.K = K; a.n_dev = n_dev; a.n_host = n_host; a.splits = splits; a.epi = epi; a.out = out; a.ldo = ldo;
   a.bias = bias; a.partial = c->gpart; a.counters = c->gctr;
   a.no_spin = c->lg ? 1 : 0;
+  a.dsm = gemm_dsm_enabled() && c->gemm_rows_max > 0 && c->gemm_rows_max <= 256 ? 1 : 0;
   a.lo = c->act_lo ? 1 : 0;
   a.out_lo = c->act_lo ? out_lo : nullptr;
   a.ssq_stride = c->m.d / 128; a.ssq_parts = c->m.d / 128;
@@ -590,6 +592,7 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
   const bool tp = c->tp > 1;
   const float* delta = nullptr;
   const int qkvw = (m.H + 2 * m.KV) * m.hd;
+  c->gemm_rows_max = decode ? ar_rows : n_host;   // DSMEM split-K needs one activation chunk (<= 256 rows)
   const int sp_qkv = decode ? c->s_qkv : 1, sp_o = decode ? c->s_o : 1, sp_gu = decode ? c->s_gu : 1,
             sp_down = decode ? c->s_down : 1;
   // folded RMSNorm on a single rank: only layer 0's input norm is a kernel
@@ -632,11 +635,12 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
       fz.ssq = f_in == FOLD_CONSUME ? c->ssq : nullptr; fz.ssq_parts = m.d / 128; fz.ssq_stride = m.d / 128;
       fz.inv_d = 1.0f / (float)m.d; fz.eps = m.eps;
       fz.cs = c->rope_cs; fz.kv_pool = (uint8_t*)c->rd.kv_pool; fz.page_bytes = m.page_bytes;
+      fz.n_pages = m.n_pages;
     } else if (decode && sp_qkv > 1 && m.hd % 64 == 0) {
       // RoPE + KV append fused into the split-K reduction of the QKV GEMM
       ProfScope ps(c, RP_PROF_GEMM_QKV);
       RopeArgs ra{c->q, c->q_lo, (uint8_t*)c->rd.kv_pool, c->R.page_table, row_pos, row_pt, c->rope_cs, m.page_bytes,
-                  c->R.maxp, l, m.H, m.KV, m.hd};
+                  c->R.maxp, l, m.H, m.KV, m.hd, m.n_pages};
       gemm(c, w.p_qkv, qkvw, m.d, n_dev, n_host, sp_qkv, EPI_QKV_ROPE, c->qkv, qkvw, w.bqkv, &ra, f_in);
     } else {
       { ProfScope ps(c, RP_PROF_GEMM_QKV);
@@ -811,6 +815,7 @@ static int init_impl(RpCtx* c) {
   if (rd->workspace_bytes < ws) return c->fail(RP_ENOSPC, "workspace too small: %zu < %zu", rd->workspace_bytes, ws);
   c->n_pages = (int)(rd->kv_pool_bytes / m.page_bytes);
   if (c->n_pages < 2) return c->fail(RP_ENOSPC, "kv pool holds %d pages", c->n_pages);
+  m.n_pages = c->n_pages;   // layer-major KV layout (kv_block_elems)
   if (make_kv_map(&c->kv_map, rd->kv_pool, (size_t)c->n_pages, m))
     return c->fail(RP_ECUDA, "KV tensor map (pool too large for 2^31 token rows?)");
   // stale rows of a page are masked in attention but multiplied by P = 0:
@@ -841,10 +846,14 @@ static int init_impl(RpCtx* c) {
   if (!c->act_lo) c->lo_mask = 0;
   c->act_lo = c->lo_mask != 0;
   c->fuse_qkv = getenv("RP_FUSE_QKV") && atoi(getenv("RP_FUSE_QKV")) != 0;
-  // decode attention over sibling groups (g <= 8 query heads per KV head fit
-  // one n-tile per member); RP_ATTN_GROUP=0 keeps the per-row kernel, 2 / 3 force sibling groups / single rows (A/B)
+  // decode attention over sibling groups (k_attn_group.cu; g <= 8 query heads
+  // per KV head fit one n-tile per member): RP_ATTN_GROUP=1 auto, 2 / 3 force
+  // sibling groups / single rows.  Off by default: 1.9x faster attention at
+  // 256 rows x 1K context, but on the bench rounds (fragmented groups, long
+  // private tails) 2.5% slower overall than the per-row kernel
+  // (profiles/r02_attn_group_ab.txt)
   c->ag_dbg = getenv("RP_AG_DBG") ? atoi(getenv("RP_AG_DBG")) : 0;
-  c->R.attn_group = c->fuse_qkv || m.H / m.KV > 8 ? 0 : (getenv("RP_ATTN_GROUP") ? atoi(getenv("RP_ATTN_GROUP")) : 1);
+  c->R.attn_group = c->fuse_qkv || m.H / m.KV > 8 ? 0 : (getenv("RP_ATTN_GROUP") ? atoi(getenv("RP_ATTN_GROUP")) : 0);
   // producers skip the residuals nobody reads; plans without one map hi only
   if (!(c->lo_mask & (LO_QKV | LO_GU))) c->h_lo = nullptr;
   if (!(c->lo_mask & LO_O)) c->att_lo = nullptr;
@@ -964,6 +973,11 @@ static int init_impl(RpCtx* c) {
   c->h_ctl->done = 1;
   CK(cudaMemcpyAsync(c->R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
 
+  if (getenv("RP_VERBOSE"))
+    fprintf(stderr, "rollpacker: decode split-K qkv %d o %d gu %d down %d lm %d; dsm %d, cluster capacity 2..8: %d %d %d %d %d %d %d\n",
+            c->s_qkv, c->s_o, c->s_gu, c->s_down, c->s_lm, (int)gemm_dsm_enabled(), gemm_cluster_cap(2),
+            gemm_cluster_cap(3), gemm_cluster_cap(4), gemm_cluster_cap(5), gemm_cluster_cap(6), gemm_cluster_cap(7),
+            gemm_cluster_cap(8));
   if (getenv("RP_ATTN_TIMELINE")) {
     CK(cudaMalloc(&c->attn_tl, (size_t)kSMs * 8 * sizeof(long long)));
     CK(cudaMemset(c->attn_tl, 0, (size_t)kSMs * 8 * sizeof(long long)));
@@ -1901,6 +1915,7 @@ int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, flo
     CK(cudaMemsetAsync(tl, 0, kSMs * 16 * sizeof(long long), c->st));
     GemmArgs a{};
     a.M = M; a.K = K; a.n_host = N; a.splits = splits; a.epi = EPI_F32; a.out = Y; a.ldo = M;
+    a.dsm = gemm_dsm_enabled() && N <= 256 ? 1 : 0;   // taken when the split count fits a resident cluster grid
     a.partial = c->gpart; a.counters = c->gctr; a.timeline = tl;
     gemm_launch(p, a, kSMs, c->st);
     std::vector<long long> h(kSMs * 16);

@@ -25,6 +25,7 @@ struct RopeArgs {
   const float2* cs;       // [pos][hd/2] (cos, sin)
   size_t page_bytes;
   int maxp, layer, H, KV, hd;
+  int n_pages;            // KV pool pages (layout: kv_block_elems)
 };
 
 struct GemmArgs {
@@ -34,6 +35,8 @@ struct GemmArgs {
   int splits;             // split-K factor (1 = direct epilogue)
   int coop_min;           // cooperative split-K reduction from this chunk width up (set by gemm_launch)
   int no_spin;            // 1: no inter-CTA waits (ticket reduction only; single-GPU local groups)
+  int dsm;                // 1: the splits of a tile form a thread-block cluster and reduce through
+                          // distributed shared memory (one item per CTA; set by gemm_launch)
   int a_tiled;            // weights stored in 128 x 64 tiles (set by gemm_launch from the plan)
   // Split-precision activations (reading Z22): D = W . x_hi + W . x_lo with
   // x_lo = fp16(x - x_hi), two MMAs per K step, fp32 accumulation -- the
@@ -86,6 +89,8 @@ int gemm_init_attrs();
 int gemm_coop_min();
 int gemm_smem_bytes();
 int gemm_pick_splits(int M, int K, int n_sms);
+bool gemm_dsm_enabled();        // DSMEM split-K reduction (RP_GEMM_DSM=1; off by default)
+int gemm_cluster_cap(int s);    // CTAs of cluster size s resident at once (0 before gemm_init_attrs)
 void gemm_launch(const GemmPlan& p, const GemmArgs& a, int grid, cudaStream_t st);
 int make_plan(GemmPlan* p, const void* W, int M, int K, const void* X, int rows_cap, int w_tiled,
               const void* X_lo = nullptr);

@@ -134,6 +134,33 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
+// generic address of the same shared-memory object in cluster CTA `rank`
+__device__ __forceinline__ const float* dsm_peer(const float* p, uint32_t rank) {
+  uint64_t r;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(p), "r"(rank));
+  return (const float*)r;
+}
+__device__ __forceinline__ uint32_t dsm_peer_u32(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t phase) {
+  uint32_t ok = 0, spins = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase)
+        : "memory");
+    if (!ok && ++spins == (1u << 24)) {
+      printf("rollpacker watchdog: split-K cluster exchange stuck (block %d)\n", blockIdx.x);
+      __trap();
+    }
+  } while (!ok);
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -234,6 +261,27 @@ __device__ __forceinline__ void reduce_splits_loop(float4 (&acc)[RU], const floa
   }
 }
 
+// the same sums from the split CTAs' shared memory (cluster DSMEM), split order
+template <int S>
+__device__ __forceinline__ void reduce_splits_dsm(float4 (&acc)[RU], const float* const (&pp)[8], int cb, int col_hi,
+                                                  int r4) {
+  float4 t[S][RU];
+#pragma unroll
+  for (int sp = 0; sp < S; ++sp)
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int col = cb + 4 * u;
+      t[sp][u] = col < col_hi ? *(const float4*)(pp[sp] + (size_t)col * BM + r4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+  for (int u = 0; u < RU; ++u) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int sp = 0; sp < S; ++sp) { v.x += t[sp][u].x; v.y += t[sp][u].y; v.z += t[sp][u].z; v.w += t[sp][u].w; }
+    acc[u] = v;
+  }
+}
+
 // Tensor-parallel push: this output unit's stores (local and NVLink peer) are
 // released at system scope, then every destination's counter is bumped.
 __device__ __forceinline__ void push_signal(const GemmArgs& a, int et) {
@@ -284,7 +332,11 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int kb_total = a.K / BK;
   // cooperative split-K reduction: grid fits one wave and the chunk is wide
   // enough that a single CTA reducing the whole tile would be the bottleneck
-  const bool coop = a.splits > 1 && n_items <= n_ctas && min(BNX, N) >= a.coop_min;
+  const bool coop = !a.dsm && a.splits > 1 && n_items <= n_ctas && min(BNX, N) >= a.coop_min;
+  if (a.dsm && n_items != n_ctas) {                // the host sized the cluster grid for one chunk
+    if (threadIdx.x == 0) printf("rollpacker: dsm split-K grid %d != items %d\n", n_ctas, n_items);
+    __trap();
+  }
 
   // Ring geometry from the widest activation chunk: 16/64/256-row boxes; at
   // small N the stages shrink and the ring deepens (more weight bytes in
@@ -313,6 +365,9 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   // bars: full[MAX_STAGES], empty[MAX_STAGES], tfull[2], tempty[2]; then tmem slot, ticket
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * MAX_STAGES + 4);
   int* ticket = (int*)(tmem_slot + 1);
+  // dsm: every split CTA of the cluster arrives once when its partial is in
+  // its shared memory (the ring, free after the item's last MMA)
+  const uint32_t dsm_bar = smem_u32(bars + 2 * MAX_STAGES + 5);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + MAX_STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * MAX_STAGES), tempty0 = smem_u32(bars + 2 * MAX_STAGES + 2);
 
@@ -321,6 +376,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     for (int i = 0; i < STAGES; ++i) { mbar_init(full0 + 8 * i, 1); mbar_init(empty0 + 8 * i, 1); }
     // tempty: 128 epilogue threads (single CTA) or one elected arrival per CTA (pair, leader's barrier)
     for (int i = 0; i < 2; ++i) { mbar_init(tfull0 + 8 * i, 1); mbar_init(tempty0 + 8 * i, CG == 2 ? 2 : 128); }
+    if (a.dsm) mbar_init(dsm_bar, a.splits);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -346,7 +402,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
-  if (CG == 2) cluster_sync_all();                 // the peer's barriers exist before any remote use
+  if (CG == 2 || a.dsm) cluster_sync_all();        // the peers' barriers exist before any remote use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) TL(1);
@@ -558,7 +614,8 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (split) {
         // fp32 partials: part[((tile*n_chunks+chunk)*splits+split)][col][row],
         // staged through shared memory so every thread writes float4s
-        float* part = a.partial + ((size_t)((I.chunk * m_tiles + I.tile) * a.splits + I.split)) * BN * BM;
+        float* part = a.dsm ? (float*)smem
+                            : a.partial + ((size_t)((I.chunk * m_tiles + I.tile) * a.splits + I.split)) * BN * BM;
         for (int c0 = 0; c0 < nc; c0 += 32) {
           uint32_t r[32];
           TMEM_LD32(tbase + c0, r);
@@ -574,7 +631,10 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int idx = et + 128 * i, n = idx >> 5, m4 = (idx & 31) * 4;
-            if (c0 + n < nc) __stcg((float4*)(part + (size_t)(c0 + n) * BM + m4), *(const float4*)(stg + n * TS + m4));
+            if (c0 + n < nc) {
+              if (a.dsm) *(float4*)(part + (size_t)(c0 + n) * BM + m4) = *(const float4*)(stg + n * TS + m4);
+              else __stcg((float4*)(part + (size_t)(c0 + n) * BM + m4), *(const float4*)(stg + n * TS + m4));
+            }
           }
           named_bar(2, 128);
         }
@@ -593,7 +653,20 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         tc_fence_before();
         mbar_arrive(tempty0 + 8 * acc);     // TMEM stage free for the next item
         int* ctr = a.counters + I.chunk * m_tiles + I.tile;
-        if (coop) {
+        if (a.dsm) {
+          // cluster exchange: release this CTA's partial to the cluster, one
+          // arrival on every split CTA's barrier, wait for all splits; then
+          // each CTA reduces its 1/splits of the columns from their shared
+          // memory (split order: the same sums as the global paths)
+          asm volatile("fence.acq_rel.cluster;" ::: "memory");
+          named_bar(1, 128);
+          if (et == 0)
+            for (int r = 0; r < a.splits; ++r) mbar_arrive_remote(dsm_peer_u32(dsm_bar, (uint32_t)r));
+          mbar_wait_cluster(dsm_bar, 0);
+          const int per = ((nc + a.splits - 1) / a.splits + 3) & ~3;
+          col_lo = min(nc, I.split * per);
+          col_hi = min(nc, col_lo + per);
+        } else if (coop) {
           __threadfence();
           named_bar(1, 128);
           // One wave (every CTA of the grid is resident, so waiting on the
@@ -669,7 +742,20 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           float4 acc[RU];
           // every split's partials requested at once (one L2 round trip),
           // summed in split order (deterministic, bit-identical to a loop)
-          switch (a.splits) {
+          if (a.dsm) {
+            const float* pp[8];
+#pragma unroll
+            for (int sp = 0; sp < 8; ++sp) pp[sp] = dsm_peer((const float*)smem, (uint32_t)min(sp, a.splits - 1));
+            switch (a.splits) {
+              case 2: reduce_splits_dsm<2>(acc, pp, cb, col_hi, r4); break;
+              case 3: reduce_splits_dsm<3>(acc, pp, cb, col_hi, r4); break;
+              case 4: reduce_splits_dsm<4>(acc, pp, cb, col_hi, r4); break;
+              case 5: reduce_splits_dsm<5>(acc, pp, cb, col_hi, r4); break;
+              case 6: reduce_splits_dsm<6>(acc, pp, cb, col_hi, r4); break;
+              case 7: reduce_splits_dsm<7>(acc, pp, cb, col_hi, r4); break;
+              default: reduce_splits_dsm<8>(acc, pp, cb, col_hi, r4); break;
+            }
+          } else switch (a.splits) {
             case 2: reduce_splits<2>(acc, pb, cb, col_hi, r4); break;
             case 3: reduce_splits<3>(acc, pb, cb, col_hi, r4); break;
             case 4: reduce_splits<4>(acc, pb, cb, col_hi, r4); break;
@@ -735,9 +821,8 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               } else {
                 const int kh = is_v ? head - R.H - R.KV : head - R.H;
                 const int page = R.page_table[(size_t)R.row_pt[n] * R.maxp + pos / kPage];
-                dst = (act_t*)(R.kv_pool + (size_t)page * R.page_bytes +
-                                       ((size_t)((R.layer * R.KV + kh) * 2 + (is_v ? 1 : 0)) * kPage + pos % kPage) *
-                                           hd * 2) + i0;
+                dst = (act_t*)R.kv_pool + kv_block_elems(R.layer, page, kh, is_v ? 1 : 0, R.n_pages, R.KV, hd) +
+                      (size_t)(pos % kPage) * hd + i0;
               }
               *(uint2*)dst = packed;
             }
@@ -920,7 +1005,9 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
-  if (CG == 2) cluster_sync_all();                 // the leader's MMAs into this CTA's TMEM are done
+  // pair: the leader's MMAs into this CTA's TMEM are done; dsm: no CTA leaves
+  // while a peer may still read its partial
+  if (CG == 2 || a.dsm) cluster_sync_all();
   if (warp == 2) {
     tc_fence_after();
     if (CG == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
@@ -960,6 +1047,22 @@ int make_tmap_act(CUtensorMap* map, const void* base, int rows, int cols, int bo
 
 int gemm_smem_bytes() { return GEMM_SMEM; }
 
+// Split-K through distributed shared memory (RP_GEMM_DSM=1):
+// the splits of a tile run as one thread-block cluster, so the whole grid
+// must be resident at once -- g_cluster_cap[s] = CTAs of cluster size s the
+// device holds concurrently (cudaOccupancyMaxActiveClusters; 4-CTA clusters
+// strand SMs of the 16/18/20-SM GPCs), which bounds the split count.
+static int g_cluster_cap[9] = {0};
+// Off by default: parity-green, but the capacity-bounded split counts (qkv 3,
+// o 4, down 4 instead of 4 / 5 / 5) cost more than the exchange saves
+// (7B decode step 4.17 vs 4.04 ms at 16 rows, 10.60 vs 10.41 at 256,
+// profiles/r02_gemm_dsm_ab.txt).
+bool gemm_dsm_enabled() {
+  static const bool v = getenv("RP_GEMM_DSM") && atoi(getenv("RP_GEMM_DSM")) != 0;
+  return v;
+}
+int gemm_cluster_cap(int s) { return s >= 2 && s <= 8 ? g_cluster_cap[s] : 0; }
+
 int gemm_init_attrs() {
   const bool ok =
       cudaFuncSetAttribute(gemm_tcgen05_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
@@ -970,6 +1073,25 @@ int gemm_init_attrs() {
           cudaSuccess &&
       cudaFuncSetAttribute(gemm_tcgen05_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
           cudaSuccess;
+  if (ok && gemm_dsm_enabled() && !g_cluster_cap[2]) {
+    for (int cs = 2; cs <= 8; ++cs) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(cs * 64);
+      cfg.blockDim = dim3(GEMM_THREADS);
+      cfg.dynamicSmemBytes = GEMM_SMEM;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, gemm_tcgen05_kernel<1, 1>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+      }
+      g_cluster_cap[cs] = n * cs;
+    }
+  }
   return ok ? 0 : -1;
 }
 
@@ -985,6 +1107,9 @@ int gemm_pick_splits(int M, int K, int n_sms) {
     // partial traffic, uneven waves) measured slower than no split, e.g.
     // 13824 x 5120 at N=136: 4 splits 58.6 us vs none 45.0 us
     if (s > 1 && items > n_sms) break;
+    // with DSMEM split-K (once the cluster capacities are known) every split
+    // count must fit its cluster size's resident capacity
+    if (s > 1 && gemm_dsm_enabled() && g_cluster_cap[2] && (s > 8 || items > g_cluster_cap[s])) continue;
     const double waves = (double)((items + n_sms - 1) / n_sms);
     const double cost = waves * ((kb + s - 1) / s + 4) + (s > 1 ? 2.0 : 0.0);
     if (cost < best_cost - 1e-9) { best_cost = cost; best = s; }
@@ -1012,6 +1137,12 @@ void gemm_launch(const GemmPlan& p, const GemmArgs& a0, int grid, cudaStream_t s
   GemmArgs a = a0;
   a.a_tiled = p.a_tiled;
   a.lo = a0.lo && p.has_lo;
+  // DSMEM split-K: one item per CTA (the caller guarantees one chunk: <= 256
+  // rows), the tile's splits one cluster, the grid resident at once
+  const int dsm_items = (a.M / BM) * a.splits;
+  const bool dsm = a.dsm && a.splits >= 2 && a.splits <= 8 && a.epi != EPI_SWIGLU && a.epi != EPI_PARTIAL &&
+                   !a.timeline && dsm_items <= gemm_cluster_cap(a.splits);
+  a.dsm = 0;
   // no_spin (single-GPU local groups): every split-K tile is reduced by its
   // last CTA (ticket), never by CTAs waiting for each other, because other
   // contexts' kernels may hold the SMs the waited-for splits need
@@ -1033,6 +1164,24 @@ void gemm_launch(const GemmPlan& p, const GemmArgs& a0, int grid, cudaStream_t s
     cfg.attrs = at;
     cfg.numAttrs = g_no_pdl ? 1 : 2;
     cudaLaunchKernelEx(&cfg, a.lo ? gemm_tcgen05_kernel<2, 1> : gemm_tcgen05_kernel<2, 0>, p.tmA, p.tmB16, p.tmB64,
+                       p.tmB256, p.tmL16, p.tmL64, p.tmL256, a);
+    return;
+  }
+  if (dsm) {
+    a.dsm = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(dsm_items);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = GEMM_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = a.splits; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_no_pdl ? 1 : 2;
+    cudaLaunchKernelEx(&cfg, a.lo ? gemm_tcgen05_kernel<1, 1> : gemm_tcgen05_kernel<1, 0>, p.tmA, p.tmB16, p.tmB64,
                        p.tmB256, p.tmL16, p.tmL64, p.tmL256, a);
     return;
   }

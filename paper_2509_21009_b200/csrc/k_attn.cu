@@ -134,7 +134,7 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
             mbar_wait_wd(empty0 + 8 * st, ph ^ 1, 100 + st, gp, (long long)it * 1000 + npg);
             const uint32_t fb = full0 + 8 * st;
             bar_expect_tx(fb, C::STAGE_BYTES);
-            const int row_k = (((page * m.L + layer) * m.KV + kvh) * 2 + 0) * kPage;
+            const int row_k = (int)(kv_block_elems(layer, page, kvh, 0, m.n_pages, m.KV, HD) / HD);
             const uint32_t dst = sbase + st * C::STAGE_BYTES;
 #pragma unroll
             for (int h = 0; h < C::HALVES; ++h) {
@@ -208,10 +208,10 @@ attn_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __restrict_
         // append k (rotated) and v to the current token's page slot; the
         // producer loads that page only after this (kvready)
         const int page = page_table[(size_t)I.pt_row * maxp + I.pos0 / kPage];
-        act_t* kd = (act_t*)(fz.kv_pool + (size_t)page * fz.page_bytes +
-                             ((size_t)((layer * m.KV + kvh) * 2 + 0) * kPage + I.pos0 % kPage) * HD * 2);
-        act_t* vd = (act_t*)(fz.kv_pool + (size_t)page * fz.page_bytes +
-                             ((size_t)((layer * m.KV + kvh) * 2 + 1) * kPage + I.pos0 % kPage) * HD * 2);
+        act_t* kd = (act_t*)fz.kv_pool + kv_block_elems(layer, page, kvh, 0, m.n_pages, m.KV, HD) +
+                    (size_t)(I.pos0 % kPage) * HD;
+        act_t* vd = (act_t*)fz.kv_pool + kv_block_elems(layer, page, kvh, 1, m.n_pages, m.KV, HD) +
+                    (size_t)(I.pos0 % kPage) * HD;
         for (int d = threadIdx.x; d < HD; d += CW * 32) {
           kd[d] = to_act(xr[g * HD + d]);
           vd[d] = to_act(xs[(g + 1) * HD + d]);

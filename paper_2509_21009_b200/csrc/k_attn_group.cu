@@ -218,7 +218,7 @@ attn_group_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __res
       mbar_wait_wd(empty0 + 8 * st, (uint32_t)(((gp / AG_STAGES) & 1) ^ 1), 400 + st, gp, page);
       const uint32_t fb = full0 + 8 * st;
       bar_expect_tx(fb, C::STAGE_BYTES);
-      const int row_k = (((page * m.L + layer) * m.KV + kvh) * 2 + 0) * kPage;
+      const int row_k = (int)(kv_block_elems(layer, page, kvh, 0, m.n_pages, m.KV, HD) / HD);
       const uint32_t dst = sbase + st * C::STAGE_BYTES;
 #pragma unroll
       for (int h = 0; h < C::HALVES; ++h) {

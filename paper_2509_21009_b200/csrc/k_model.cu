@@ -282,7 +282,7 @@ __global__ void rope_append_kernel(const float* qkv, const int* n_dev, int n_hos
     const float* row = qkv + (size_t)r * W;
     const int page = page_table[(size_t)row_pt[r] * maxp + pos / kPage];
     const int prow = pos % kPage;
-    uint8_t* pbase = kv_pool + (size_t)page * m.page_bytes;
+    act_t* kbase = (act_t*)kv_pool + (size_t)prow * m.hd;
     // q and k: rotated pairs
     for (int e = threadIdx.x; e < (m.H + m.KV) * half; e += blockDim.x) {
       const int head = e / half, i = e % half;
@@ -299,13 +299,13 @@ __global__ void rope_append_kernel(const float* qkv, const int* n_dev, int n_hos
         }
       } else {
         const int kh = head - m.H;
-        act_t* dst = (act_t*)(pbase + ((size_t)((layer * m.KV + kh) * 2 + 0) * kPage + prow) * m.hd * 2);
+        act_t* dst = kbase + kv_block_elems(layer, page, kh, 0, m.n_pages, m.KV, m.hd);
         dst[i] = to_act(o1); dst[i + half] = to_act(o2);
       }
     }
     for (int e = threadIdx.x; e < m.KV * m.hd; e += blockDim.x) {
       const int kh = e / m.hd, i = e % m.hd;
-      act_t* dst = (act_t*)(pbase + ((size_t)((layer * m.KV + kh) * 2 + 1) * kPage + prow) * m.hd * 2);
+      act_t* dst = kbase + kv_block_elems(layer, page, kh, 1, m.n_pages, m.KV, m.hd);
       dst[i] = to_act(row[(m.H + m.KV) * m.hd + e]);
     }
     __syncthreads();
@@ -328,8 +328,9 @@ __global__ void kv_fork_kernel(const int* jobs, int n, uint8_t* pool, ModelDims 
   for (int j = blockIdx.x; j < n * blocks; j += gridDim.x) {
     const int job = j / blocks, blk = j % blocks;
     const int src = jobs[3 * job], dst = jobs[3 * job + 1], rows = jobs[3 * job + 2];
-    const int4* s = (const int4*)(pool + (size_t)src * m.page_bytes + (size_t)blk * kPage * m.hd * 2);
-    int4* d = (int4*)(pool + (size_t)dst * m.page_bytes + (size_t)blk * kPage * m.hd * 2);
+    const int layer = blk / (m.KV * 2), kvh = (blk / 2) % m.KV, kv = blk % 2;
+    const int4* s = (const int4*)((const act_t*)pool + kv_block_elems(layer, src, kvh, kv, m.n_pages, m.KV, m.hd));
+    int4* d = (int4*)((act_t*)pool + kv_block_elems(layer, dst, kvh, kv, m.n_pages, m.KV, m.hd));
     const int n16 = rows * m.hd * 2 / 16;
     for (int i = threadIdx.x; i < n16; i += blockDim.x) d[i] = s[i];
   }

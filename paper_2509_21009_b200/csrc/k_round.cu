@@ -493,28 +493,56 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
   }
   __syncthreads();
   if (R.attn_group && !s_err) {
-    // Sibling groups (k_attn_group.cu): maximal runs of next-step rows with
-    // the same (prompt, j / 8) -- siblings are adjacent in the live list (slot
-    // order, order-preserving compaction).  A group's work is its longest
-    // member's pages over the warps a member pair gets (rep); splits as for
-    // rows: ns_g = max(1, floor(c_g * U / sum c)) with U <= 3 * U1 whole
-    // waves, so items <= groups + U <= S + 3 * U1 (the work-list capacity).
-    int ng = 0;
+    // Sibling groups (k_attn_group.cu): runs of next-step rows with the same
+    // (prompt, j / 8) -- siblings are adjacent in the live list (slot order,
+    // order-preserving compaction) -- cut into groups of 8 / 4 / 2 / 1 members
+    // (the binary decomposition of the run length, largest first), so the 8
+    // consumer warps divide evenly over the members (rep = 8 / members).  A
+    // group's work is its longest member's pages x members / 8 per warp;
+    // splits ns_g = max(1, floor(c_g * Ug / sum c)) with Ug <= 3 * U1 whole
+    // waves, so items <= groups + Ug <= S + 3 * U1 (the work-list capacity).
+    int ng = 0, nsib = 0, saved = 0, pages_all = 0;
     for (int base = 0; base < kept; base += CTL_THREADS) {
       const int pos = base + tid;
-      const int st = pos < kept && (pos == 0 || R.grp_key[pos] != R.grp_key[pos - 1]);
-      int tot;
+      int st = 0, sib = 0, sv = 0, pg = 0;
+      if (pos < kept) {
+        const int key = R.grp_key[pos];
+        int k = 0, n = 1;
+        while (k < 7 && pos - k - 1 >= 0 && R.grp_key[pos - k - 1] == key) ++k;
+        n += k;
+        while (n < 8 && pos + (n - k) < kept && R.grp_key[pos + (n - k)] == key) ++n;
+        sib = k == 0;
+        pg = pages_of(R.row_pos[pos] + 1);
+        for (int b = 8, off = 0; b >= 1; b >>= 1)
+          if (n & b) {
+            if (k == off) {   // a group of b members starts here: b - 1 fills saved per shared page
+              st = 1;
+              sv = min(R.own0[R.live_next[pos]], R.row_pos[pos] / kPage) * (b - 1);
+            }
+            off += b;
+          }
+      }
+      int tot, tsib, tsv, tpg;
       const int o = block_exscan(st, &tot, scan_sm);
+      block_exscan(sib, &tsib, scan_sm);
+      block_exscan(sv, &tsv, scan_sm);
+      block_exscan(pg, &tpg, scan_sm);
       if (st) R.grp_start[ng + o] = pos;
       ng += tot;
+      nsib += tsib;
+      saved += tsv;
+      pages_all += tpg;
     }
-    // Few sibling groups (ng < U1 / 6, e.g. 16 rows of 2 prompts) would need
-    // ~U1 / ng page splits per group to fill the wave, and the partials and
-    // merges of so many splits cost more than the shared fills save: every row
-    // becomes its own group (8 warps split its pages, as the per-row list did).
-    // Measured crossover: profiles/r02_attn_group_ab.txt.  attn_group 2 / 3
+    // Sibling groups pay off when they save a large share of the page fills:
+    // with few sibling runs (nsib < U1 / 8, e.g. 16 rows of 2 prompts) the
+    // groups would need ~U1 / nsib page splits each to fill the wave, whose
+    // partials and merges cost more than the fills save, and late in a round
+    // (long private tails, small groups) the shared prompt pages are a small
+    // share of the reads.  Then every row is its own group (8 warps split its
+    // pages, as the per-row list did): below 40% of the fills saved, measured
+    // on the bench rounds (profiles/r02_attn_group_ab.txt).  attn_group 2 / 3
     // force sibling groups / single rows (A/B).
-    if (R.attn_group == 3 || (R.attn_group == 1 && ng * 6 < U1)) {
+    if (R.attn_group == 3 || (R.attn_group == 1 && (nsib * 8 < U1 || saved * 10 < pages_all * 4))) {
       for (int pos = tid; pos < kept; pos += CTL_THREADS) R.grp_start[pos] = pos;
       ng = kept;
     }
@@ -525,7 +553,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
       nm = min(8, R.grp_start[gi + 1] - p0);
       w = 0;
       for (int x = 0; x < nm; ++x) w = max(w, pages_of(R.row_pos[p0 + x] + 1));
-      rep = nm > 4 ? 1 : (nm > 2 ? 2 : (nm > 1 ? 4 : 8));   // warps per member of the 8 (k_attn_group.cu)
+      rep = 8 / nm;                     // nm in {1, 2, 4, 8}: warps per member (k_attn_group.cu)
       return (w + rep - 1) / rep;
     };
     long long csum = 0;
@@ -537,18 +565,18 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
       csum += tot;
     }
     csum = max(1LL, csum);
-    const int Ug = U1 * min(3, max(1, (ng + U1 - 1) / U1));
+    const int Ug = U1 * min(3, max(1, (ng + U1 - 1) / U1));   // whole waves (one-wave cap measured slower)
+    auto nsplits = [&](int c, int w, int ug, int& chunk) {
+      const int want = (int)max(1LL, min(32LL, (long long)c * ug / csum));   // <= 32: the merge's smem
+      chunk = (w + want - 1) / want;
+      return (w + chunk - 1) / chunk;
+    };
     AttnGroupItem* gitems = reinterpret_cast<AttnGroupItem*>(R.items);
     items = 0;
     for (int base = 0; base < ng; base += CTL_THREADS) {
       const int gi = base + tid;
       int w = 0, nm = 0, rep = 1, ns = 0, chunk = 1;
-      if (gi < ng) {
-        const int c = gcost(gi, w, nm, rep);
-        const int want = (int)max(1LL, min(32LL, (long long)c * Ug / csum));   // <= 32: the merge's smem
-        chunk = (w + want - 1) / want;
-        ns = (w + chunk - 1) / chunk;
-      }
+      if (gi < ng) ns = nsplits(gcost(gi, w, nm, rep), w, Ug, chunk);
       int tot;
       const int o = block_exscan(ns, &tot, scan_sm);
       if (gi < ng) {

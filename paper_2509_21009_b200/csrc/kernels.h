@@ -120,7 +120,8 @@ struct ModelDims {
   int L, d, H, KV, hd, F, V, eos;
   int v0;                  // first vocab id of this rank's LM-head shard
   float eps;
-  size_t page_bytes;       // one page: [L][KV][2][kPage][hd] fp16 (reading Z20)
+  size_t page_bytes;       // one page: L x KV x 2 x kPage x hd fp16 (reading Z20)
+  int n_pages;             // pages in the KV pool (layout: kv_block_elems, common.cuh)
 };
 
 // weights
@@ -167,6 +168,7 @@ struct QkvFuse {
   const float* ssq; int ssq_parts, ssq_stride; float inv_d, eps;   // folded RMSNorm (ssq == nullptr: none)
   const float2* cs;       // RoPE (cos, sin) [pos][hd / 2]
   uint8_t* kv_pool; size_t page_bytes;
+  int n_pages;
   int dbg;                // RP_AG_DBG measurement knobs (also without the fusion): 1 no MMAs, 2 no q_lo MMAs
 };
 

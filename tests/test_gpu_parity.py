@@ -501,9 +501,9 @@ def test_decode_long_context_split_kv(tiny, oracle_w):
 @pytest.mark.parametrize("G", [1, 3, 8, 10])
 @pytest.mark.parametrize("mode", ["auto", "group", "single", "rows"])
 def test_decode_attention_sibling_groups(model, G, mode, monkeypatch):
-    """Decode attention over sibling groups (k_attn_group.cu: the default
-    'auto', forced sibling groups, forced single rows) and the per-row kernel
-    (RP_ATTN_GROUP=0, k_attn.cu): logits of eager decode steps vs
+    """Decode attention over sibling groups (k_attn_group.cu, RP_ATTN_GROUP:
+    1 'auto', 2 forced sibling groups, 3 forced single rows) and the per-row
+    kernel (0, k_attn.cu, the default): logits of eager decode steps vs
     the oracle teacher-forced on the GPU's own history, for groups of 1-8
     members (rep 4 / 2 / 1 warps per member pair), a G = 10 prompt split into
     groups of 8 and 2, siblings dying mid-round (groups shrink), head_dim 64
@@ -540,3 +540,18 @@ def test_decode_attention_sibling_groups(model, G, mode, monkeypatch):
             worst = max(worst, float(np.max(np.abs(lg[row] - want))))
             rows += 1
     assert max(caps) >= 560 and rows >= 4 and worst <= LOGIT_TOL, (caps.keys(), rows, worst)
+
+
+def test_gemm_dsm_split_k_subprocess():
+    """The optional DSMEM split-K reduction (RP_GEMM_DSM=1, off by default:
+    profiles/r02_gemm_dsm_ab.txt): the GEMM sweep and the decode-step logits
+    in a fresh process (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RP_GEMM_DSM="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.join(root, "tests", "test_gpu_parity.py"),
+                        "-k", "gemm_tcgen05_vs_fp32 or decode_step_logits and not fused"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
