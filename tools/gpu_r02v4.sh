@@ -10,3 +10,9 @@ import json
 s=open('gpurun_out/r02v4_bench_n4.json').read(); d=json.loads(s[s.index('{'):]); print('N=4', d['value'], d['decoded_tokens_per_s'], d['s_per_rl_step'], d.get('clocks'))
 "
 tail -3 gpurun_out/r02v4_bench_n4.err
+timeout 1500 python -m torch.distributed.run --nnodes 1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29522 \
+   bench.py --gpus 2 --steps 6 --warmup 5 > gpurun_out/r02v4_bench_n2.json 2> gpurun_out/r02v4_bench_n2.err
+python -c "
+import json
+s=open('gpurun_out/r02v4_bench_n2.json').read(); d=json.loads(s[s.index('{'):]); print('N=2', d['value'], d['decoded_tokens_per_s'], d['s_per_rl_step'], d.get('clocks'))
+"
