@@ -1930,8 +1930,8 @@ int rp_debug_gemm(void* ctx, const void* W, const void* X, int32_t rows_cap, flo
         if (h[b * 16 + k]) { acc[k] += (h[b * 16 + k] - t0) / 1e3; cnt[k]++; tend = std::max(tend, h[b * 16 + k]); }
     fprintf(stderr, "gemm timeline M=%d N=%d K=%d splits=%d (us from first CTA start, mean over CTAs):", M, N, K, splits);
     const char* nm[16] = {"start", "setup", "it0_first", "it0_lastmma", "it1_first", "it1_lastmma", "it2_first",
-                          "it2_lastmma", "it0_epi", "it1_epi", "it2_epi", "sk_partials", "sk_ticket", "sk_reduced", "", ""};
-    for (int k = 0; k < 14; ++k) if (cnt[k]) fprintf(stderr, " %s=%.2f(%d)", nm[k], acc[k] / cnt[k], cnt[k]);
+                          "it2_lastmma", "it0_epi", "it1_epi", "it2_epi", "sk_partials", "sk_ticket", "sk_reduced", "sk_loaded", ""};
+    for (int k = 0; k < 15; ++k) if (cnt[k]) fprintf(stderr, " %s=%.2f(%d)", nm[k], acc[k] / cnt[k], cnt[k]);
     fprintf(stderr, " end=%.2f\n", (tend - t0) / 1e3);
   }
   CK(cudaEventRecord(e0, c->st));

@@ -763,6 +763,10 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             case 6: reduce_splits<6>(acc, pb, cb, col_hi, r4); break;
             default: reduce_splits_loop(acc, pb, cb, col_hi, r4, a.splits); break;
           }
+          if (a.timeline && et == 0 && local == 0 && cb == col_lo) {   // debug: the partials have arrived
+            asm volatile("" ::"f"(acc[0].x), "f"(acc[RU - 1].w));
+            TL(14);
+          }
           if (a.ssq_in) {
 #pragma unroll
             for (int u = 0; u < RU; ++u) {
