@@ -159,7 +159,11 @@ struct RpCtx {
   // default: measured slower, profiles/r02_fused_qkv_ab.txt)
   bool fuse_qkv = false;
   int ag_dbg = 0;
-  int gemm_rows_max = 0;                  // rows bound of the current forward (decode bucket / prefill tokens)                         // RP_AG_DBG: group-attention measurement knobs (k_attn_group.cu)
+  int gemm_rows_max = 0;                  // rows bound of the current forward (decode bucket / prefill tokens)
+  bool cur_gmode = false;                 // the decode step being captured / launched uses the group attention
+  int* gmode_dev = nullptr;               // RoundDev.gmode
+  int* gmode_h = nullptr;                 // pinned staging of it
+  int gmode_last = -1;                         // RP_AG_DBG: group-attention measurement knobs (k_attn_group.cu)
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
   int* gctr = nullptr;
   int* atickets = nullptr;
@@ -174,7 +178,7 @@ struct RpCtx {
   CUtensorMap kv_map{};        // the KV pool as [token rows, head_dim] for TMA
 
   // graphs
-  struct Graph { int bucket; cudaGraphExec_t exec; int nodes; };
+  struct Graph { int bucket; bool gmode; cudaGraphExec_t exec; int nodes; };
   std::vector<Graph> graphs;    // per live-row bucket, valid for the current round
   cudaGraphExec_t gexec = nullptr;
   int graph_nodes = 0;
@@ -366,7 +370,9 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto atick = cv.take<int>((size_t)std::max(z.max_items_dec, z.max_items_pre) * KV);
   auto invf = cv.take<double>(hd / 2);
   auto rope_cs = cv.take<float2>((size_t)(rd->max_prompt_len + rd->max_cap + 2) * (hd / 2));
-  auto items_dec = cv.take<AttnGroupItem>(z.max_items_dec);   // AttnItem or AttnGroupItem (RoundDev.attn_group)
+  auto items_dec = cv.take<AttnItem>(z.max_items_dec);
+  auto gitems_dec = cv.take<AttnGroupItem>(z.max_items_dec);   // sibling-group list (RoundDev.attn_group)
+  auto gmode = cv.take<int>(1);
   auto grp_key = cv.take<int>(z.S);
   auto grp_start = cv.take<int>((size_t)z.S + 1);
   auto rows_hist = cv.take<unsigned long long>((size_t)z.S + 1);
@@ -441,7 +447,7 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
     R.p_plen = p_plen; R.p_adm = p_adm; R.p_wait = p_wait; R.p_live = p_live; R.p_pfree = p_pfree;
     R.p_pneed = p_pneed; R.wait_q = wait_q; R.rejobs = rejobs;
     R.grp_key = grp_key; R.grp_start = grp_start;
-    R.best = best; R.items = reinterpret_cast<AttnItem*>(items_dec); R.rows_hist = rows_hist; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
+    R.best = best; R.items = items_dec; R.gitems = gitems_dec; R.gmode = gmode; c->gmode_dev = gmode; R.rows_hist = rows_hist; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
     R.ctl = ctl; R.cap = rd->max_cap;
   }
   return align_up(cv.off);
@@ -651,10 +657,10 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
     }
     { ProfScope ps(c, RP_PROF_ATTN);
       if (skipped(c)) {
-      } else if (decode && c->R.attn_group) {
-        launch_attention_group(c->kv_map, c->q, c->q_lo, c->R.page_table, c->R.maxp,
-                               reinterpret_cast<const AttnGroupItem*>(items), n_items_dev, c->att, c->att_lo, c->apart,
-                               c->atickets, m, l, c->st, c->ag_dbg, c->lg ? 0 : 1);
+      } else if (decode && c->cur_gmode) {
+        launch_attention_group(c->kv_map, c->q, c->q_lo, c->R.page_table, c->R.maxp, c->R.gitems,
+                               &c->R.ctl->n_gitems, c->att, c->att_lo, c->apart, c->atickets, m, l, c->st, c->ag_dbg,
+                               c->lg ? 0 : 1);
       } else {
         fz.dbg = c->ag_dbg;
         launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
@@ -750,6 +756,22 @@ static int bucket_for(const RpCtx* c, int n) {
   return std::min(b, c->z.S);
 }
 
+// Decode attention of the next steps: the sibling-group kernel while the
+// live batch exceeds group_rows_min (wide steps: siblings mostly alive, the
+// shared prompt pages dominate the reads; 49 vs 94 us per layer at 256 rows),
+// the per-row kernel below (profiles/r02_attn_group_ab.txt).  The device flag
+// tells ctl to keep building the group list while a group-mode graph runs.
+static int set_gmode(RpCtx* c) {
+  const bool mode = c->R.attn_group && c->h_ctl->n_live > c->R.group_rows_min;
+  if ((int)mode != c->gmode_last) {
+    *c->gmode_h = mode ? 1 : 0;
+    CK(cudaMemcpyAsync(c->gmode_dev, c->gmode_h, sizeof(int), cudaMemcpyHostToDevice, c->st));
+    c->gmode_last = mode;
+  }
+  c->cur_gmode = mode;
+  return RP_OK;
+}
+
 static int ensure_graph(RpCtx* c, int bucket) {
   if (c->graph_dirty) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
@@ -757,7 +779,7 @@ static int ensure_graph(RpCtx* c, int bucket) {
     c->graph_dirty = false;
   }
   for (auto& g : c->graphs)
-    if (g.bucket == bucket) { c->gexec = g.exec; c->graph_nodes = g.nodes; return RP_OK; }
+    if (g.bucket == bucket && g.gmode == c->cur_gmode) { c->gexec = g.exec; c->graph_nodes = g.nodes; return RP_OK; }
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
   const long long before = c->launches;
@@ -766,7 +788,7 @@ static int ensure_graph(RpCtx* c, int bucket) {
   c->capturing = false;
   cudaError_t e = cudaStreamEndCapture(c->st, &g);
   if (e != cudaSuccess) return c->fail(RP_ECUDA, "graph capture: %s", cudaGetErrorString(e));
-  RpCtx::Graph entry{bucket, nullptr, (int)(c->launches - before)};
+  RpCtx::Graph entry{bucket, c->cur_gmode, nullptr, (int)(c->launches - before)};
   c->launches = before;
   CK(cudaGraphInstantiate(&entry.exec, g, 0));
   CK(cudaGraphDestroy(g));
@@ -853,7 +875,8 @@ static int init_impl(RpCtx* c) {
   // private tails) 2.5% slower overall than the per-row kernel
   // (profiles/r02_attn_group_ab.txt)
   c->ag_dbg = getenv("RP_AG_DBG") ? atoi(getenv("RP_AG_DBG")) : 0;
-  c->R.attn_group = c->fuse_qkv || m.H / m.KV > 8 ? 0 : (getenv("RP_ATTN_GROUP") ? atoi(getenv("RP_ATTN_GROUP")) : 0);
+  c->R.attn_group = c->fuse_qkv || m.H / m.KV > 8 ? 0 : (getenv("RP_ATTN_GROUP") ? atoi(getenv("RP_ATTN_GROUP")) : 1);
+  c->R.group_rows_min = getenv("RP_ATTN_GROUP_MIN") ? atoi(getenv("RP_ATTN_GROUP_MIN")) : 128;
   // producers skip the residuals nobody reads; plans without one map hi only
   if (!(c->lo_mask & (LO_QKV | LO_GU))) c->h_lo = nullptr;
   if (!(c->lo_mask & LO_O)) c->att_lo = nullptr;
@@ -967,6 +990,10 @@ static int init_impl(RpCtx* c) {
     CK(cudaStreamSynchronize(c->st));
   }
   CK(cudaMallocHost(&c->h_ctl, sizeof(CtlBlock)));
+  CK(cudaMallocHost(&c->gmode_h, sizeof(int)));
+  *c->gmode_h = 0;
+  CK(cudaMemcpyAsync(c->gmode_dev, c->gmode_h, sizeof(int), cudaMemcpyHostToDevice, c->st));
+  c->gmode_last = 0;
   if (rd->world > 1) CK(cudaMallocHost(&c->memb_h, (size_t)(c->z.P + 1) * (rd->world + 1) * 4));
   CK(cudaMallocHost(&c->rejobs_h, (size_t)5 * c->z.S * 4));
   memset(c->h_ctl, 0, sizeof(CtlBlock));
@@ -1098,6 +1125,7 @@ void rp_free(void* ctx) {
   if (c->memb_h) cudaFreeHost(c->memb_h);
   if (c->rejobs_h) cudaFreeHost(c->rejobs_h);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
+  if (c->gmode_h) cudaFreeHost(c->gmode_h);
   if (c->trace_dev) cudaFree(c->trace_dev);
   if (c->dp.nccl) ncclCommDestroy(c->dp.nccl);
   if (c->tpc.nccl) ncclCommDestroy(c->tpc.nccl);
@@ -1472,6 +1500,7 @@ static int recompute_paused(RpCtx* c) {
   b.pause = 0;
   b.n_live = b.n_live_saved;
   b.n_items = b.n_items_saved;
+  b.n_gitems = b.n_gitems_saved;
   CK(cudaMemcpyAsync(c->R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
   return RP_OK;
 }
@@ -1493,6 +1522,7 @@ int rp_step(void* ctx, int32_t max_steps, rp_status* st) {
     const int grow = c->max_active ? std::min(c->max_active * c->G, c->h_ctl->n_live +
                                               (c->n_loc - c->h_ctl->n_issued) * c->G) : 0;
     const int bucket = bucket_for(c, std::max(c->h_ctl->n_live, grow));
+    if ((rc = set_gmode(c))) return rc;
     if (c->prof_steps_left > 0) {
       const int rows = c->h_ctl->n_live;
       const long long ctx = c->h_ctl->ctx_sum;

@@ -480,7 +480,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
         }
         if (R.attn_group) R.grp_key[pos] = R.slot_prompt[s] * ((R.G + 7) / 8) + R.slot_j[s] / 8;
         const int it0 = items + oi;
-        for (int sp = 0; sp < ns && !R.attn_group; ++sp) {
+        for (int sp = 0; sp < ns; ++sp) {
           AttnItem I;
           I.q_row0 = pos; I.n_qtok = 1; I.pos0 = kv; I.pt_row = s;
           I.kv_lo = sp * chunk; I.kv_hi = min(kv + 1, (sp + 1) * chunk);
@@ -492,7 +492,12 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     }
   }
   __syncthreads();
-  if (R.attn_group && !s_err) {
+  // sibling-group work list for the group kernel, when the host may run the
+  // next step with it (more than group_rows_min rows, or a group-mode graph
+  // is running); the per-row list above is always built
+  int gcnt = 0;
+  if (R.attn_group && !s_err && (kept > R.group_rows_min || *R.gmode)) {
+    int items = 0;   // shadows the per-row count in this block
     // Sibling groups (k_attn_group.cu): runs of next-step rows with the same
     // (prompt, j / 8) -- siblings are adjacent in the live list (slot order,
     // order-preserving compaction) -- cut into groups of 8 / 4 / 2 / 1 members
@@ -571,8 +576,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
       chunk = (w + want - 1) / want;
       return (w + chunk - 1) / chunk;
     };
-    AttnGroupItem* gitems = reinterpret_cast<AttnGroupItem*>(R.items);
-    items = 0;
+    AttnGroupItem* gitems = R.gitems;
     for (int base = 0; base < ng; base += CTL_THREADS) {
       const int gi = base + tid;
       int w = 0, nm = 0, rep = 1, ns = 0, chunk = 1;
@@ -599,6 +603,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
       }
       items += tot;
     }
+    gcnt = items;
   }
   for (int i = tid; i < n; i += CTL_THREADS) R.best[i] = 0ull;
   for (int i = tid; i < kept; i += CTL_THREADS) R.live[i] = R.live_next[i];
@@ -608,6 +613,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     C->decoded += n;
     C->free_top = top - alloc;
     C->n_items = min(items, R.max_items);
+    C->n_gitems = min(gcnt, R.max_items);
     C->n_issued = n_is0 + nis / R.G;
     C->issue_n = 0;
     // commit the re-admissions: popped from the FIFO, newest admissions
@@ -619,7 +625,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
         R.p_adm[v] = ++C->adm_ctr;
       }
     if (nrd) C->wait_head += C->readmit_n;
-    if (items > R.max_items) s_err = 3;    // unreachable by the bound S + 3 * U1; fail loudly if not
+    if (items > R.max_items || gcnt > R.max_items) s_err = 3;    // unreachable by the bound S + 3 * U1; fail loudly if not
     const bool done = s_acc_new >= R.target || s_next_global == 0 || s_err;
     if (R.trace_buf && t <= R.trace_steps) {
       int* tb = R.trace_buf + (size_t)(t - 1) * (2 + R.S);
@@ -633,7 +639,8 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
       // some rank re-admitted responses: every rank holds the next step
       // until the host recomputed their KV (rp_step, between steps)
       C->pause = 1; C->n_live_saved = kept; C->n_items_saved = min(items, R.max_items);
-      C->n_live = 0; C->n_items = 0; C->t = t + 1;
+      C->n_gitems_saved = min(gcnt, R.max_items);
+      C->n_live = 0; C->n_items = 0; C->n_gitems = 0; C->t = t + 1;
     } else {
       C->n_live = kept; C->t = t + 1;
     }

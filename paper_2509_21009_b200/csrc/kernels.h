@@ -71,6 +71,8 @@ struct CtlBlock {
   int readmit_pages;  // pages they take
   int pause;        // 1: re-admitted responses await their KV recompute (the host runs it between steps)
   int n_live_saved, n_items_saved;  // the next step's rows / attention items while paused
+  int n_gitems;     // sibling-group attention items of the next step (RoundDev.gitems)
+  int n_gitems_saved;
   int n_rejobs;     // recompute jobs written by phase B
 };
 
@@ -89,8 +91,11 @@ struct RoundDev {
   int* rejobs;        // [S][5] recompute jobs: slot, g, fork src page, fork dst page, fork rows
   int attn_units;     // decode-attention split budget per KV head (0: 148 / KV)
   int attn_waves;     // 1: budget whole waves of attention units (k-wave fill), 0: one-wave floor
-  int attn_group;     // decode work list: 0 per-row AttnItem (k_attn.cu); AttnGroupItem (k_attn_group.cu) of
+  int attn_group;     // sibling-group work list (gitems, k_attn_group.cu) besides the per-row one: 0 off;
                       // 1 sibling groups unless too few (then single rows), 2 always sibling groups, 3 always single rows
+  int group_rows_min; // build gitems when the next step has more rows (or *gmode: the running graph uses them)
+  const int* gmode;   // [1] 1 while the host runs decode steps with the group kernel
+  AttnGroupItem* gitems;
   int* grp_key;       // [S] scratch: (prompt, j / 8) of each next-step row
   int* grp_start;     // [S + 1] scratch: first row of each group
   int world, rank;

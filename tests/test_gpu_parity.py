@@ -502,14 +502,16 @@ def test_decode_long_context_split_kv(tiny, oracle_w):
 @pytest.mark.parametrize("mode", ["auto", "group", "single", "rows"])
 def test_decode_attention_sibling_groups(model, G, mode, monkeypatch):
     """Decode attention over sibling groups (k_attn_group.cu, RP_ATTN_GROUP:
-    1 'auto', 2 forced sibling groups, 3 forced single rows) and the per-row
-    kernel (0, k_attn.cu, the default): logits of eager decode steps vs
+    1 'auto', 2 forced sibling groups, 3 forced single rows; by default it
+    runs only above 128 live rows) and the per-row kernel (0, k_attn.cu):
+    logits of eager decode steps vs
     the oracle teacher-forced on the GPU's own history, for groups of 1-8
     members (rep 4 / 2 / 1 warps per member pair), a G = 10 prompt split into
     groups of 8 and 2, siblings dying mid-round (groups shrink), head_dim 64
     (g = 2) and 128 (g = 5), and ~650-token contexts cut into many page
     splits merged per member."""
     monkeypatch.setenv("RP_ATTN_GROUP", {"auto": "1", "group": "2", "single": "3", "rows": "0"}[mode])
+    monkeypatch.setenv("RP_ATTN_GROUP_MIN", "0")          # the group kernel at every live batch
     cfg = configs.model_config(model)
     w = weights.Weights(cfg, configs.WEIGHT_SEED)
     eng = make_engine(cfg, graph_steps=0, max_cap=640, max_seqs=32, max_prompt_len=160, kv_pool_bytes=256 << 20)
