@@ -242,6 +242,32 @@ int rp_collect_ready(void* ctx, int32_t first, rp_response* out, int32_t max_out
  * Lets the caller compute the per-round roofline of SURVEY §8(d). */
 int rp_round_rows_histogram(void* ctx, int64_t* out, int32_t n);
 
+/* Migration of an in-flight round by recompute (PAPER.md
+ * when rollout GPUs are handed to training, their
+ * unfinished responses move to the remaining instances and their KV is
+ * recomputed there; reading Z27).  Between two rp_step calls,
+ * rp_round_export writes the round's step state -- control block, live list
+ * and next-step inputs, attention work lists, per-response lengths, status,
+ * tokens and issue offsets, per-prompt counters, acceptance order -- into a
+ * caller buffer of rp_round_state_bytes bytes (host memory; the KV cache is
+ * not exported).  rp_round_import, on an idle context created with the same
+ * model and runtime sizes (on this or another GPU), takes the round's
+ * ORIGINAL rp_submit_round arguments plus that buffer: it re-submits the round
+ * (prefill and step 1 are deterministic), installs the exported state, sizes
+ * the live responses' page tables and recomputes the KV of their generated
+ * tokens with the prefill kernels, so rp_step continues at the exported step
+ * with the same schedule (live lists, acceptance, cutoff) and the same
+ * sampling counters.  Single-rank contexts (world 1, tp 1), no continuous
+ * issuance, no prompts waiting for re-admission; the exporting context keeps
+ * its round (collect or drop it).  Errors: RP_ESTATE (no active round / done
+ * / waiting prompts), RP_ENOSPC (buffer too small), RP_EINVAL (size or header
+ * mismatch, unsupported mode), RP_ENOMEM_KV (the pool cannot hold the live
+ * contexts), RP_ECUDA. */
+int rp_round_state_bytes(void* ctx, int64_t* bytes);
+int rp_round_export(void* ctx, void* buf, int64_t bytes);
+int rp_round_import(void* ctx, const rp_prompt* prompts, int32_t n_prompts, int32_t G, int32_t keep, int32_t cap,
+                    int32_t target, int32_t flags, int64_t round_id, const void* buf, int64_t bytes);
+
 /* Continuous issuance (DAPO integration:
  * "set a maximum number of active requests for each LLM instance and
  * continuously issue new requests"; readings Z21).  Applies to the rounds

@@ -159,6 +159,7 @@ struct RpCtx {
   // default: measured slower, profiles/r02_fused_qkv_ab.txt)
   bool fuse_qkv = false;
   int ag_dbg = 0;
+  bool o_dsm = false;                     // O projection split-K through DSMEM
   int gemm_rows_max = 0;                  // rows bound of the current forward (decode bucket / prefill tokens)
   bool cur_gmode = false;                 // the decode step being captured / launched uses the group attention
   int* gmode_dev = nullptr;               // RoundDev.gmode
@@ -553,7 +554,7 @@ static void coll_allreduce_max_u64(RpCtx* c, CommCtx& cm, unsigned long long* bu
 
 static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, int n_host, int splits, int epi,
                  void* out, int ldo, const float* bias, const RopeArgs* rope = nullptr, int fold = FOLD_NONE,
-                 int push_slot = -1, __half* out_lo = nullptr) {
+                 int push_slot = -1, __half* out_lo = nullptr, bool dsm = false) {
   if (skipped(c)) return;
   GemmArgs a{};
   if (push_slot >= 0) {
@@ -568,7 +569,7 @@ static void gemm(RpCtx* c, const GemmPlan& p, int M, int K, const int* n_dev, in
   a.M = M; a.K = K; a.n_dev = n_dev; a.n_host = n_host; a.splits = splits; a.epi = epi; a.out = out; a.ldo = ldo;
   a.bias = bias; a.partial = c->gpart; a.counters = c->gctr;
   a.no_spin = c->lg ? 1 : 0;
-  a.dsm = gemm_dsm_enabled() && c->gemm_rows_max > 0 && c->gemm_rows_max <= 256 ? 1 : 0;
+  a.dsm = (gemm_dsm_enabled() || dsm) && c->gemm_rows_max > 0 && c->gemm_rows_max <= 256 ? 1 : 0;
   a.lo = c->act_lo ? 1 : 0;
   a.out_lo = c->act_lo ? out_lo : nullptr;
   a.ssq_stride = c->m.d / 128; a.ssq_parts = c->m.d / 128;
@@ -670,7 +671,7 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
       c->launches++; }
     { ProfScope ps(c, RP_PROF_GEMM_O);
       gemm(c, w.p_o, m.d, m.H * m.hd, n_dev, n_host, sp_o, tp ? EPI_F32 : EPI_RESID, tp ? c->ar : c->x, m.d,
-           nullptr, nullptr, f_prod, peer ? 0 : -1); }
+           nullptr, nullptr, f_prod, peer ? 0 : -1, nullptr, decode && c->o_dsm && !tp); }
     if (peer) {
       tp_norm(0, nullptr, sp_o);
     } else if (tp) {
@@ -974,7 +975,13 @@ static int init_impl(RpCtx* c) {
   if (make_plan(&c->p_lm, c->lm, (int)V, (int)d, c->h, Tcap, wt, nullptr))
     return c->fail(RP_ECUDA, "cuTensorMapEncodeTiled failed (lm head)");
   c->s_qkv = gemm_pick_splits(qkvw, (int)d, kSMs);
-  c->s_o = gemm_pick_splits((int)d, (int)(H * hd), kSMs);
+  // the O projection reduces its split-K through DSMEM (4 splits in clusters
+  // of 4 beat 5 splits over global memory: profiles/r02_gemm_dsm_ab.txt);
+  // RP_GEMM_DSM_O=0 keeps the global paths
+  // (single rank only: under TP the O partials are pushed to the peers and
+  // tp_norm counts the split CTAs' signals by the global-path rules)
+  c->o_dsm = c->tp <= 1 && !(getenv("RP_GEMM_DSM_O") && atoi(getenv("RP_GEMM_DSM_O")) == 0);
+  c->s_o = c->o_dsm ? gemm_pick_splits_dsm((int)d, (int)(H * hd), kSMs) : gemm_pick_splits((int)d, (int)(H * hd), kSMs);
   c->s_gu = gemm_pick_splits((int)(2 * F), (int)d, kSMs);
   c->s_down = gemm_pick_splits((int)d, (int)F, kSMs);
   c->s_lm = gemm_pick_splits((int)V, (int)d, kSMs);
@@ -1409,6 +1416,71 @@ static void fill_status(RpCtx* c, rp_status* st) {
   st->preemptions = b.preemptions;
 }
 
+// KV recompute of response tokens (re-admission after preemption, Z26;
+// migration of an in-flight round, Z27): for each segment the decoder runs
+// the prefill kernels over tokens k0 .. k1-1 of slot s's response (positions
+// plen + k), reading their keys from the slot's own page table and writing
+// their KV; no LM head.  Pieces bounded by the prefill buffers.
+struct RecomputeSeg { int s, plen, k0, k1; };
+static int recompute_segments(RpCtx* c, std::vector<RecomputeSeg>& segs) {
+  const int g_heads = c->m.H / c->m.KV, tpb = 16 / g_heads;
+  const int tok_cap = c->rd.max_prompt_tokens;
+  size_t si = 0;
+  while (si < segs.size()) {
+    // one piece: whole or partial segments within the token and item capacities
+    std::vector<int> pos, pt;
+    std::vector<AttnItem> items;
+    std::vector<std::array<int, 4>> copies;   // dst offset, slot, k0, count
+    int T = 0;
+    while (si < segs.size() && T < tok_cap) {
+      RecomputeSeg& sg = segs[si];
+      int take = std::min(sg.k1 - sg.k0, tok_cap - T);
+      // items of these tokens: ceil(nq / tpb) blocks x ceil(keys / chunk) splits each
+      auto n_items_for = [&](int k0, int cnt) {
+        int it = 0;
+        for (int b0 = 0; b0 < cnt; b0 += tpb) {
+          const int hi = sg.plen + k0 + std::min(b0 + tpb, cnt);
+          it += (hi + kAttnChunk - 1) / kAttnChunk;
+        }
+        return it;
+      };
+      while (take > 0 && (int)items.size() + n_items_for(sg.k0, take) > c->z.max_items_pre) take /= 2;
+      if (take <= 0) break;
+      const int off = T;
+      for (int k = 0; k < take; ++k) { pos.push_back(sg.plen + sg.k0 + k); pt.push_back(sg.s); }
+      for (int b0 = 0; b0 < take; b0 += tpb) {
+        const int nq = std::min(tpb, take - b0);
+        const int p0 = sg.plen + sg.k0 + b0, hi = p0 + nq;
+        const int ns = (hi + kAttnChunk - 1) / kAttnChunk, item0 = (int)items.size();
+        for (int sp = 0; sp < ns; ++sp) {
+          AttnItem I;
+          I.q_row0 = off + b0; I.n_qtok = nq; I.pos0 = p0; I.pt_row = sg.s;
+          I.kv_lo = sp * kAttnChunk; I.kv_hi = std::min(hi, (sp + 1) * kAttnChunk);
+          I.nsplit = ns; I.item0 = item0;
+          items.push_back(I);
+        }
+      }
+      copies.push_back({off, sg.s, sg.k0, take});
+      T += take;
+      sg.k0 += take;
+      if (sg.k0 >= sg.k1) ++si;
+    }
+    if (T == 0) return c->fail(RP_ENOSPC, "recompute: prefill buffers too small for one token");
+    CK(idle(c));
+    for (auto& cp : copies)
+      CK(cudaMemcpyAsync(c->pre_tok + cp[0], c->R.tok_out + (size_t)cp[1] * c->R.cap + cp[2],   // row stride: the round's cap
+                         (size_t)cp[3] * 4, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(c->pre_pos, pos.data(), T * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->pre_pt, pt.data(), T * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->items_pre, items.data(), items.size() * sizeof(AttnItem), cudaMemcpyHostToDevice, c->st));
+    bool pending = false;
+    forward_layers(c, c->pre_tok, nullptr, T, c->pre_pos, c->pre_pt, c->items_pre, nullptr, (int)items.size(), false,
+                   T, &pending);
+    CK(cudaGetLastError());
+  }
+  return RP_OK;
+}
+
 // Recompute of re-admitted responses (KV pressure, reading Z26), between
 // two decode steps while the round is paused: copy the prompt's partial page
 // into each response's first private page, then run the decoder over the
@@ -1433,68 +1505,14 @@ static int recompute_paused(RpCtx* c) {
       c->launches++;
     }
     // continuation segments (slot, first token index, end) in job order
-    struct Seg { int s, plen, k0, k1; };
-    std::vector<Seg> segs;
+    std::vector<RecomputeSeg> segs;
     for (int j = 0; j < nj; ++j) {
       const int* J = c->rejobs_h + 5 * j;
       const int s = J[0], g = J[1], plen = (int)c->round_prompts[s / c->G].tokens.size();
       if (g >= 2) segs.push_back({s, plen, 0, g - 1});
     }
-    const int g_heads = c->m.H / c->m.KV, tpb = 16 / g_heads;
-    const int tok_cap = c->rd.max_prompt_tokens;
-    size_t si = 0;
-    while (si < segs.size()) {
-      // one piece: whole or partial segments within the token and item capacities
-      std::vector<int> pos, pt;
-      std::vector<AttnItem> items;
-      std::vector<std::array<int, 4>> copies;   // dst offset, slot, k0, count
-      int T = 0;
-      while (si < segs.size() && T < tok_cap) {
-        Seg& sg = segs[si];
-        int take = std::min(sg.k1 - sg.k0, tok_cap - T);
-        // items of these tokens: ceil(nq / tpb) blocks x ceil(keys / chunk) splits each
-        auto n_items_for = [&](int k0, int cnt) {
-          int it = 0;
-          for (int b0 = 0; b0 < cnt; b0 += tpb) {
-            const int hi = sg.plen + k0 + std::min(b0 + tpb, cnt);
-            it += (hi + kAttnChunk - 1) / kAttnChunk;
-          }
-          return it;
-        };
-        while (take > 0 && (int)items.size() + n_items_for(sg.k0, take) > c->z.max_items_pre) take /= 2;
-        if (take <= 0) break;
-        const int off = T;
-        for (int k = 0; k < take; ++k) { pos.push_back(sg.plen + sg.k0 + k); pt.push_back(sg.s); }
-        for (int b0 = 0; b0 < take; b0 += tpb) {
-          const int nq = std::min(tpb, take - b0);
-          const int p0 = sg.plen + sg.k0 + b0, hi = p0 + nq;
-          const int ns = (hi + kAttnChunk - 1) / kAttnChunk, item0 = (int)items.size();
-          for (int sp = 0; sp < ns; ++sp) {
-            AttnItem I;
-            I.q_row0 = off + b0; I.n_qtok = nq; I.pos0 = p0; I.pt_row = sg.s;
-            I.kv_lo = sp * kAttnChunk; I.kv_hi = std::min(hi, (sp + 1) * kAttnChunk);
-            I.nsplit = ns; I.item0 = item0;
-            items.push_back(I);
-          }
-        }
-        copies.push_back({off, sg.s, sg.k0, take});
-        T += take;
-        sg.k0 += take;
-        if (sg.k0 >= sg.k1) ++si;
-      }
-      if (T == 0) return c->fail(RP_ENOSPC, "recompute: prefill buffers too small for one token");
-      CK(idle(c));
-      for (auto& cp : copies)
-        CK(cudaMemcpyAsync(c->pre_tok + cp[0], c->R.tok_out + (size_t)cp[1] * c->R.cap + cp[2],   // row stride: the round's cap
-                           (size_t)cp[3] * 4, cudaMemcpyDeviceToDevice, c->st));
-      CK(cudaMemcpyAsync(c->pre_pos, pos.data(), T * 4, cudaMemcpyHostToDevice, c->st));
-      CK(cudaMemcpyAsync(c->pre_pt, pt.data(), T * 4, cudaMemcpyHostToDevice, c->st));
-      CK(cudaMemcpyAsync(c->items_pre, items.data(), items.size() * sizeof(AttnItem), cudaMemcpyHostToDevice, c->st));
-      bool pending = false;
-      forward_layers(c, c->pre_tok, nullptr, T, c->pre_pos, c->pre_pt, c->items_pre, nullptr, (int)items.size(), false,
-                     T, &pending);
-      CK(cudaGetLastError());
-    }
+    const int rc = recompute_segments(c, segs);
+    if (rc) return rc;
   }
   // resume the held step
   b.pause = 0;
@@ -1717,6 +1735,150 @@ int rp_round_rows_histogram(void* ctx, int64_t* out, int32_t n) {
   CK(cudaMemcpyAsync(h.data(), c->R.rows_hist, (size_t)m * 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   for (int i = 0; i < n; ++i) out[i] = i < m ? (int64_t)h[i] : 0;
+  return RP_OK;
+}
+
+// ---- migration of an in-flight round (reading Z27) --------
+// The device state a round carries from one decode step to the next, in a
+// fixed order; the KV cache is not part of it (recomputed on import).
+struct StateSec { void* dev; size_t bytes; };
+static std::vector<StateSec> round_sections(RpCtx* c) {
+  RoundDev& R = c->R;
+  const size_t S = c->z.S, P = c->z.P, MI = c->z.max_items_dec;
+  return {{R.ctl, sizeof(CtlBlock)},       {R.live, S * 4},           {R.tok_in, S * 4},
+          {R.row_pos, S * 4},              {R.row_pt, S * 4},         {R.items, MI * sizeof(AttnItem)},
+          {R.gitems, MI * sizeof(AttnGroupItem)}, {R.kv_len, S * 4}, {R.gen, S * 4},
+          {R.status, S * 4},               {R.t0, S * 4},             {R.tok_out, S * (size_t)R.cap * 4},
+          {R.p_state, P * 4},              {R.p_cnt, P * 4},          {R.accept_order, P * 4},
+          {R.rows_hist, (S + 1) * 8}};
+}
+constexpr int64_t kStateMagic = 0x3153525052LL;   // "RPRS1"
+constexpr int kStateHdr = 12;                      // int64 header words
+static void state_header(RpCtx* c, int64_t* h) {
+  const int64_t v[kStateHdr] = {kStateMagic, c->z.S, c->z.P, c->R.cap, c->z.max_items_dec, (int64_t)sizeof(CtlBlock),
+                                c->G, c->n_loc, c->kind, c->keep, c->rd.world, c->tp};
+  for (int i = 0; i < kStateHdr; ++i) h[i] = v[i];
+}
+
+int rp_round_state_bytes(void* ctx, int64_t* bytes) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c || !bytes) return RP_EINVAL;
+  size_t b = kStateHdr * 8;
+  for (auto& sec : round_sections(c)) b += sec.bytes;
+  *bytes = (int64_t)b;
+  return RP_OK;
+}
+
+int rp_round_export(void* ctx, void* buf, int64_t bytes) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (!buf) return c->fail(RP_EINVAL, "invalid field: buf");
+  if (!c->active) return c->fail(RP_ESTATE, "no active round");
+  if (c->rd.world != 1 || c->tp != 1 || c->lg)
+    return c->fail(RP_EINVAL, "round export: single-rank contexts only (world 1, tp 1)");
+  if (c->max_active) return c->fail(RP_EINVAL, "round export: continuous issuance is not supported");
+  int64_t need = 0;
+  rp_round_state_bytes(ctx, &need);
+  if (bytes < need) return c->fail(RP_ENOSPC, "round export: buffer of %lld bytes < %lld", (long long)bytes, (long long)need);
+  int rc = read_ctl(c);
+  if (rc) return rc;
+  const CtlBlock& b = *c->h_ctl;
+  if (b.done) return c->fail(RP_ESTATE, "round export: the round is done (collect it)");
+  if (b.pause || b.wait_head != b.wait_tail)
+    return c->fail(RP_ESTATE, "round export: preempted prompts are waiting (export between re-admissions)");
+  uint8_t* out = (uint8_t*)buf;
+  state_header(c, (int64_t*)out);
+  size_t off = kStateHdr * 8;
+  for (auto& sec : round_sections(c)) {
+    CK(cudaMemcpyAsync(out + off, sec.dev, sec.bytes, cudaMemcpyDeviceToHost, c->st));
+    off += sec.bytes;
+  }
+  CK(cudaStreamSynchronize(c->st));
+  return RP_OK;
+}
+
+// Import: the round is submitted again with the caller's original arguments
+// (prompts, G, keep, cap, target, flags, round_id: prefill, page tables and
+// step 1 are deterministic), then the exported step state replaces the
+// device state, the page tables are grown / shrunk to the live responses'
+// contexts, and the KV of every live response's generated tokens 1 .. g-1 is
+// recomputed (prefill kernels), so the next decode step continues the round
+// exactly where the exporting engine left it.
+int rp_round_import(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, int32_t keep, int32_t cap,
+                    int32_t target, int32_t flags, int64_t round_id, const void* buf, int64_t bytes) {
+  RpCtx* c = (RpCtx*)ctx;
+  if (!c) return RP_EINVAL;
+  if (!buf || !prompts) return c->fail(RP_EINVAL, "invalid field: buf / prompts");
+  if (c->rd.world != 1 || c->tp != 1 || c->lg)
+    return c->fail(RP_EINVAL, "round import: single-rank contexts only (world 1, tp 1)");
+  if (c->issue_cap > 0) return c->fail(RP_EINVAL, "round import: continuous issuance is not supported");
+  if (bytes < kStateHdr * 8) return c->fail(RP_EINVAL, "round import: state of %lld bytes", (long long)bytes);
+  const int64_t* hdr = (const int64_t*)buf;
+  int64_t mine[kStateHdr];
+  int rc = rp_submit_round(ctx, prompts, n, G, keep, cap, target, flags, round_id);
+  if (rc) return rc;
+  int64_t need = 0;
+  rp_round_state_bytes(ctx, &need);   // the token rows follow this round's cap
+  if (bytes != need) {
+    c->active = false;
+    return c->fail(RP_EINVAL, "round import: state of %lld bytes, this round needs %lld", (long long)bytes,
+                   (long long)need);
+  }
+  state_header(c, mine);
+  for (int i = 0; i < kStateHdr; ++i)
+    if (hdr[i] != mine[i]) {
+      c->active = false;
+      return c->fail(RP_EINVAL, "round import: state header word %d is %lld, this round has %lld", i,
+                     (long long)hdr[i], (long long)mine[i]);
+    }
+  const std::vector<StateSec> secs = round_sections(c);
+  std::vector<const uint8_t*> src(secs.size());
+  size_t off = kStateHdr * 8;
+  for (size_t i = 0; i < secs.size(); ++i) { src[i] = (const uint8_t*)buf + off; off += secs[i].bytes; }
+  const CtlBlock& ex = *(const CtlBlock*)src[0];
+  const int* ex_kv = (const int*)src[7];
+  const int* ex_gen = (const int*)src[8];
+  const int* ex_status = (const int*)src[9];
+  if (ex.done || ex.pause || ex.wait_head != ex.wait_tail)
+    return c->fail(RP_EINVAL, "round import: the exported round is done or has waiting prompts");
+  // after submit: step 1 decoded, private pages for positions <= plen of the live responses
+  if ((rc = read_ctl(c))) return rc;
+  const int S = c->z.S, maxp = c->z.maxp, nS = c->n_loc * c->G;
+  std::vector<int> st_now(S), kv_now(S), ptab((size_t)S * maxp), fstack(c->n_pages);
+  CK(cudaMemcpyAsync(st_now.data(), c->R.status, (size_t)S * 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(kv_now.data(), c->R.kv_len, (size_t)S * 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(ptab.data(), c->R.page_table, ptab.size() * 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(fstack.data(), c->R.free_stack, fstack.size() * 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  int top = c->h_ctl->free_top;
+  auto pages_of = [](int tokens) { return (tokens + kPage - 1) / kPage; };
+  std::vector<RecomputeSeg> segs;
+  for (int s = 0; s < nS; ++s) {
+    const int plen = (int)c->round_prompts[s / c->G].tokens.size(), own0 = plen / kPage;
+    const int cur = st_now[s] == ST_LIVE ? pages_of(kv_now[s] + 1) - own0 : 0;
+    const int want = ex_status[s] == ST_LIVE ? pages_of(ex_kv[s] + 1) - own0 : 0;
+    for (int k = cur; k < want; ++k) {
+      if (top <= 0) { c->active = false; return c->fail(RP_ENOMEM_KV, "round import: KV pool exhausted"); }
+      ptab[(size_t)s * maxp + own0 + k] = fstack[--top];
+    }
+    for (int k = want; k < cur; ++k) fstack[top++] = ptab[(size_t)s * maxp + own0 + k];
+    if (ex_status[s] == ST_LIVE && ex_gen[s] >= 2) segs.push_back({s, plen, 0, ex_gen[s] - 1});
+  }
+  CK(idle(c));
+  CK(cudaMemcpyAsync(c->R.page_table, ptab.data(), ptab.size() * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->R.free_stack, fstack.data(), (size_t)top * 4, cudaMemcpyHostToDevice, c->st));
+  for (size_t i = 1; i < secs.size(); ++i)
+    CK(cudaMemcpyAsync(secs[i].dev, src[i], secs[i].bytes, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(c->R.best, 0, (size_t)S * 8, c->st));
+  // the KV of the generated tokens (the next step appends token g itself)
+  if ((rc = recompute_segments(c, segs))) { c->active = false; return rc; }
+  *c->h_ctl = ex;
+  c->h_ctl->free_top = top;
+  c->h_ctl->err = 0;
+  CK(cudaMemcpyAsync(c->R.ctl, c->h_ctl, sizeof(CtlBlock), cudaMemcpyHostToDevice, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->step_logits_valid = false;
+  c->graph_dirty = true;
   return RP_OK;
 }
 

@@ -91,6 +91,7 @@ int gemm_smem_bytes();
 int gemm_pick_splits(int M, int K, int n_sms);
 bool gemm_dsm_enabled();        // DSMEM split-K reduction (RP_GEMM_DSM=1; off by default)
 int gemm_cluster_cap(int s);    // CTAs of cluster size s resident at once (0 before gemm_init_attrs)
+int gemm_pick_splits_dsm(int M, int K, int n_sms);
 void gemm_launch(const GemmPlan& p, const GemmArgs& a, int grid, cudaStream_t st);
 int make_plan(GemmPlan* p, const void* W, int M, int K, const void* X, int rows_cap, int w_tiled,
               const void* X_lo = nullptr);

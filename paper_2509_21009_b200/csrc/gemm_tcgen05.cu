@@ -1077,7 +1077,7 @@ int gemm_init_attrs() {
           cudaSuccess &&
       cudaFuncSetAttribute(gemm_tcgen05_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) ==
           cudaSuccess;
-  if (ok && gemm_dsm_enabled() && !g_cluster_cap[2]) {
+  if (ok && !g_cluster_cap[2]) {
     for (int cs = 2; cs <= 8; ++cs) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(cs * 64);
@@ -1099,7 +1099,13 @@ int gemm_init_attrs() {
   return ok ? 0 : -1;
 }
 
-int gemm_pick_splits(int M, int K, int n_sms) {
+static int pick_splits(int M, int K, int n_sms, bool dsm);
+int gemm_pick_splits(int M, int K, int n_sms) { return pick_splits(M, K, n_sms, gemm_dsm_enabled()); }
+// the split count of a GEMM reduced through DSMEM (bounded by the resident
+// cluster capacity; the plain rule until gemm_init_attrs measured it)
+int gemm_pick_splits_dsm(int M, int K, int n_sms) { return pick_splits(M, K, n_sms, true); }
+
+static int pick_splits(int M, int K, int n_sms, bool dsm) {
   // Fill the SMs for a single 256-column chunk: minimise the critical path
   // ceil(items / n_sms) * ceil(kb / splits) (+ a small per-split cost).
   const int tiles = M / BM, kb = K / BK;
@@ -1113,7 +1119,7 @@ int gemm_pick_splits(int M, int K, int n_sms) {
     if (s > 1 && items > n_sms) break;
     // with DSMEM split-K (once the cluster capacities are known) every split
     // count must fit its cluster size's resident capacity
-    if (s > 1 && gemm_dsm_enabled() && g_cluster_cap[2] && (s > 8 || items > g_cluster_cap[s])) continue;
+    if (s > 1 && dsm && g_cluster_cap[2] && (s > 8 || items > g_cluster_cap[s])) continue;
     const double waves = (double)((items + n_sms - 1) / n_sms);
     const double cost = waves * ((kb + s - 1) / s + 4) + (s > 1 ? 2.0 : 0.0);
     if (cost < best_cost - 1e-9) { best_cost = cost; best = s; }

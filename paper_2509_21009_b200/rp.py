@@ -68,7 +68,7 @@ EXPORTS = ["rp_query_sizes", "rp_init_model", "rp_submit_round", "rp_step", "rp_
            "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm", "rp_debug_profile", "rp_nccl_unique_id",
            "rp_tp_ipc_handle", "rp_tp_ipc_open", "rp_collect_ready", "rp_round_rows_histogram",
            "rp_round_issue_cap", "rp_round_unissued", "rp_plan_round", "rp_long_queue_pop",
-           "rp_local_group_create", "rp_local_group_free", "rp_plan_tp"]
+           "rp_local_group_create", "rp_local_group_free", "rp_plan_tp", "rp_round_state_bytes", "rp_round_export", "rp_round_import"]
 
 
 def load_library(path=LIB_PATH):
@@ -101,6 +101,9 @@ def load_library(path=LIB_PATH):
     lib.rp_tp_ipc_handle.argtypes = [P, P]
     lib.rp_tp_ipc_open.argtypes = [P, P]
     lib.rp_round_rows_histogram.argtypes = [P, ctypes.POINTER(I64), I32]
+    lib.rp_round_state_bytes.argtypes = [P, ctypes.POINTER(I64)]
+    lib.rp_round_export.argtypes = [P, P, I64]
+    lib.rp_round_import.argtypes = [P, ctypes.POINTER(Prompt), I32, I32, I32, I32, I32, I32, I64, P, I64]
     lib.rp_round_issue_cap.argtypes = [P, I32]
     lib.rp_round_unissued.argtypes = [P, ctypes.POINTER(I32), I32, ctypes.POINTER(I32)]
     lib.rp_collect_ready.argtypes = [P, I32, ctypes.POINTER(Response), I32, ctypes.POINTER(I32), I64,
@@ -295,6 +298,10 @@ class Engine:
             rc = self.L.rp_submit_round(self.h, None, n, G, keep, cap, target, flags, round_id)
             self._check(rc)
             return
+        arr, n = self._prompt_array(prompts, trace, trace_retry)
+        self._check(self.L.rp_submit_round(self.h, arr, n, G, keep, cap, target, flags, round_id))
+
+    def _prompt_array(self, prompts, trace, trace_retry=None):
         n = len(prompts)
         arr = (Prompt * n)()
         self._keep = []
@@ -312,7 +319,28 @@ class Engine:
                 tr = np.ascontiguousarray(trace_retry[i], dtype=np.int32)
                 self._keep.append(tr)
                 arr[i].trace_lens_retry = _i32p(tr)
-        self._check(self.L.rp_submit_round(self.h, arr, n, G, keep, cap, target, flags, round_id))
+        return arr, n
+
+    def export_round(self):
+        """The in-flight round's step state (bytes; NEXT-3 migration, see
+        rp_round_export).  The KV cache is not part of it."""
+        nb = ctypes.c_int64()
+        self._check(self.L.rp_round_state_bytes(self.h, ctypes.byref(nb)))
+        buf = ctypes.create_string_buffer(nb.value)
+        self._check(self.L.rp_round_export(self.h, ctypes.cast(buf, ctypes.c_void_p), nb.value))
+        return buf.raw
+
+    def import_round(self, state, prompts, G, cap, target, long_round=False, trace=None, round_id=0, keep=0,
+                     trace_retry=None, preempt=False):
+        """Continue a round exported by export_round on this (idle) engine:
+        the original submit arguments plus the state; the live responses' KV
+        is recomputed (rp_round_import)."""
+        flags = (RP_LONG if long_round else RP_SHORT) | (RP_TRACE if trace is not None else 0) | \
+            (RP_PREEMPT if preempt else 0)
+        arr, n = self._prompt_array(prompts, trace, trace_retry)
+        buf = ctypes.create_string_buffer(bytes(state), len(state))
+        self._check(self.L.rp_round_import(self.h, arr, n, G, keep, cap, target, flags, round_id,
+                                           ctypes.cast(buf, ctypes.c_void_p), len(state)))
 
     def step(self, max_steps=1 << 30):
         st = Status()
@@ -404,12 +432,14 @@ class Engine:
         self._check(self.L.rp_debug_trace_enable(self.h, steps))
         self._trace_steps = steps
 
-    def debug_trace(self, steps=None):
+    def debug_trace(self, steps=None, start=1):
+        """Per-step records from step `start` (1-based) up to the first step
+        without live rows (an imported round records from its import step)."""
         steps = steps or self._trace_steps
         buf = np.zeros((steps, 2 + self.max_seqs), dtype=np.int32)
         self._check(self.L.rp_debug_trace_get(self.h, _i32p(buf), steps))
         out = []
-        for t in range(steps):
+        for t in range(start - 1, steps):
             n = int(buf[t, 0])
             if n == 0:
                 break

@@ -1,0 +1,134 @@
+"""Migration of an in-flight round by recompute (PAPER P:921-925,
+P:965-972; reading Z27), through the C ABI (rp_round_export / rp_round_import):
+
+* a round stepped to some step t on one engine, exported, and imported into a
+  fresh engine (on the same GPU, or on a second GPU) continues with the
+  oracle's schedule: the per-step live lists, acceptance counts and done flags
+  of every step after t and t_end are bit-exact (sched.closed_form), SHORT and
+  LONG rounds, CUDA graphs and eager;
+* the collected responses are the oracle's (accepted prompts in order,
+  lengths = the trace) and every token -- sampled before the migration on the
+  first engine or after it on the second, whose KV was recomputed -- equals
+  the oracle's Gumbel argmax teacher-forced on the GPU's history (gap rule);
+* unsupported or mismatched imports fail with RP_EINVAL, exports without an
+  active round with RP_ESTATE.
+"""
+import numpy as np
+import pytest
+
+from oracle import decoder, sampler, sched, weights
+from synth import configs, gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return configs.model_config("tiny")
+
+
+def engine(cfg, graph_steps, **kw):
+    from paper_2509_21009_b200 import rp
+    return rp.Engine(cfg, max_seqs=64, max_prompts=16, max_prompt_len=128, max_prompt_tokens=1024, max_cap=512,
+                     kv_pool_bytes=64 << 20, graph_steps=graph_steps, sample_seed=configs.SAMPLE_SEED, **kw)
+
+
+def _trace(n, G, seed, lo=20, hi=300):
+    return np.random.default_rng(seed).integers(lo, hi, size=(n, G)).astype(np.int64)
+
+
+def _check_tokens(cfg, res, ps, L, G, round_id):
+    w = weights.Weights(cfg, configs.WEIGHT_SEED)
+    checked = mism = 0
+    for r in res:
+        p = ps[r["prompt_id"] - ps[0]["prompt_id"]]["tokens"]
+        seq = np.concatenate([p, r["tokens"]])
+        lg = decoder.logits(w, seq[:-1], rows=np.arange(len(p) - 1, len(seq) - 1))
+        i = r["prompt_id"] - ps[0]["prompt_id"]
+        for t in range(1, r["len"] + 1):
+            tok, gap = sampler.sample(lg[t - 1], t, r["prompt_id"] * G + r["j"], round_id, configs.SAMPLE_SEED,
+                                      eos_id=cfg["eos_id"], trace_len=L[i, r["j"]])
+            checked += 1
+            if tok != r["tokens"][t - 1]:
+                assert gap <= 1e-2, (r["prompt_id"], r["j"], t, gap)
+                mism += 1
+    return checked, mism
+
+
+def _migrate(cfg, kind, graph_steps, t_cut, dev_b=0, n=8, G=3, seed=21):
+    import torch
+    ps = gen.prompts(n, 0, cfg["eos_id"], (5, 100), 61 + seed)
+    L = _trace(n, G, seed)
+    long_round = kind == "long"
+    cap, target = (400, n) if long_round else (250, 6)
+    ref = sched.closed_form(L, cap, target, sched.LONG if long_round else sched.SHORT, with_steps=True)
+    assert ref.t_end > t_cut + 10
+    round_id = 9
+    torch.cuda.set_device(0)
+    a = engine(cfg, graph_steps)
+    a.submit(ps, G, cap, target, long_round=long_round, trace=L, round_id=round_id)
+    st = a.step(t_cut - 1)
+    t_exp = st.t                       # graphs step in whole graphs: the actual cut
+    state = a.export_round()
+    a.close()
+    torch.cuda.set_device(dev_b)
+    b = engine(cfg, graph_steps)
+    b.debug_trace_enable(ref.t_end + 8)
+    b.import_round(state, ps, G, cap, target, long_round=long_round, trace=L, round_id=round_id)
+    st2 = b.run()
+    got = b.debug_trace(ref.t_end + 8, start=t_exp + 1)
+    res = b.collect()
+    b.close()
+    torch.cuda.set_device(0)
+    assert st2.t == ref.t_end and st2.accepted == len(ref.accepted)
+    assert len(got) == ref.t_end - t_exp
+    for g in got:
+        want = ref.steps[g["t"] - 1]
+        assert np.array_equal(g["live"], want["live"]), g["t"]
+        assert g["accepted"] == want["accepted"] and g["done"] == want["done"], g["t"]
+    assert list(dict.fromkeys(r["prompt_id"] for r in res)) == [ps[i]["prompt_id"] for i in ref.accepted]
+    for r in res:
+        i = r["prompt_id"] - ps[0]["prompt_id"]
+        assert r["len"] == min(L[i, r["j"]], cap)
+    checked, mism = _check_tokens(cfg, res, ps, L, G, round_id)
+    assert checked > 500 and mism <= checked // 50
+    return t_exp
+
+
+@pytest.mark.parametrize("kind,graph_steps,t_cut", [("short", 4, 37), ("short", 0, 90), ("long", 0, 61),
+                                                    ("long", 4, 150)])
+def test_migrate_round_bit_exact(tiny, kind, graph_steps, t_cut):
+    _migrate(tiny, kind, graph_steps, t_cut)
+
+
+def test_migrate_round_to_second_gpu(tiny):
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    _migrate(tiny, "long", 4, 101, dev_b=1)
+
+
+def test_migrate_errors(tiny):
+    from paper_2509_21009_b200 import rp
+    ps = gen.prompts(3, 0, tiny["eos_id"], (5, 40), 3)
+    L = _trace(3, 2, 4)
+    a = engine(tiny, 0)
+    with pytest.raises(rp.RPError) as e:
+        a.export_round()                               # no active round
+    assert e.value.code == rp.RP_ESTATE
+    a.submit(ps, 2, 300, 3, long_round=True, trace=L, round_id=1)
+    a.step(5)
+    state = a.export_round()
+    a.close()
+    b = engine(tiny, 0)
+    with pytest.raises(rp.RPError) as e:
+        b.import_round(state, ps, 3, 300, 3, long_round=True, trace=np.repeat(L, 2, axis=1)[:, :3], round_id=1)
+    assert e.value.code == rp.RP_EINVAL               # G differs from the exported round
+    with pytest.raises(rp.RPError) as e:
+        b.import_round(state[:-8], ps, 2, 300, 3, long_round=True, trace=L, round_id=1)
+    assert e.value.code == rp.RP_EINVAL               # truncated state
+    b.import_round(state, ps, 2, 300, 3, long_round=True, trace=L, round_id=1)
+    st = b.run()
+    assert st.done
+    b.collect()
+    b.close()
