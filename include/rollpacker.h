@@ -257,8 +257,10 @@ int rp_round_rows_histogram(void* ctx, int64_t* out, int32_t n);
  * the live responses' page tables and recomputes the KV of their generated
  * tokens with the prefill kernels, so rp_step continues at the exported step
  * with the same schedule (live lists, acceptance, cutoff) and the same
- * sampling counters.  Single-rank contexts (world 1, tp 1), no continuous
- * issuance, no prompts waiting for re-admission; the exporting context keeps
+ * sampling counters.  DP jobs migrate rank by rank into contexts of the
+ * same world and rank (every rank imports at the same step: the re-submit
+ * runs step 1's cutoff exchange); no TP contexts, no continuous issuance,
+ * no prompts waiting for re-admission; the exporting context keeps
  * its round (collect or drop it).  Errors: RP_ESTATE (no active round / done
  * / waiting prompts), RP_ENOSPC (buffer too small), RP_EINVAL (size or header
  * mismatch, unsupported mode), RP_ENOMEM_KV (the pool cannot hold the live

@@ -1753,10 +1753,10 @@ static std::vector<StateSec> round_sections(RpCtx* c) {
           {R.rows_hist, (S + 1) * 8}};
 }
 constexpr int64_t kStateMagic = 0x3153525052LL;   // "RPRS1"
-constexpr int kStateHdr = 12;                      // int64 header words
+constexpr int kStateHdr = 13;                      // int64 header words
 static void state_header(RpCtx* c, int64_t* h) {
   const int64_t v[kStateHdr] = {kStateMagic, c->z.S, c->z.P, c->R.cap, c->z.max_items_dec, (int64_t)sizeof(CtlBlock),
-                                c->G, c->n_loc, c->kind, c->keep, c->rd.world, c->tp};
+                                c->G, c->n_loc, c->kind, c->keep, c->rd.world, c->tp, c->rd.rank};
   for (int i = 0; i < kStateHdr; ++i) h[i] = v[i];
 }
 
@@ -1774,8 +1774,7 @@ int rp_round_export(void* ctx, void* buf, int64_t bytes) {
   if (!c) return RP_EINVAL;
   if (!buf) return c->fail(RP_EINVAL, "invalid field: buf");
   if (!c->active) return c->fail(RP_ESTATE, "no active round");
-  if (c->rd.world != 1 || c->tp != 1 || c->lg)
-    return c->fail(RP_EINVAL, "round export: single-rank contexts only (world 1, tp 1)");
+  if (c->tp != 1) return c->fail(RP_EINVAL, "round export: tensor-parallel contexts are not supported");
   if (c->max_active) return c->fail(RP_EINVAL, "round export: continuous issuance is not supported");
   int64_t need = 0;
   rp_round_state_bytes(ctx, &need);
@@ -1809,8 +1808,7 @@ int rp_round_import(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
   if (!buf || !prompts) return c->fail(RP_EINVAL, "invalid field: buf / prompts");
-  if (c->rd.world != 1 || c->tp != 1 || c->lg)
-    return c->fail(RP_EINVAL, "round import: single-rank contexts only (world 1, tp 1)");
+  if (c->tp != 1) return c->fail(RP_EINVAL, "round import: tensor-parallel contexts are not supported");
   if (c->issue_cap > 0) return c->fail(RP_EINVAL, "round import: continuous issuance is not supported");
   if (bytes < kStateHdr * 8) return c->fail(RP_EINVAL, "round import: state of %lld bytes", (long long)bytes);
   const int64_t* hdr = (const int64_t*)buf;

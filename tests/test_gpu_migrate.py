@@ -132,3 +132,73 @@ def test_migrate_errors(tiny):
     assert st.done
     b.collect()
     b.close()
+
+
+def test_migrate_dp_round_local_group(tiny):
+    """DP = 2 in a single-GPU local group: both ranks export their slices at the
+    same step and a second local group of two fresh contexts imports them; the
+    per-rank live counts of every later step, t_end and the acceptance follow
+    the oracle's DP protocol (sched.dp_protocol)."""
+    import threading
+    from paper_2509_21009_b200 import rp
+    n, G, cap, target, rid = 8, 3, 250, 6, 4
+    ps = gen.prompts(n, 0, tiny["eos_id"], (5, 100), 71)
+    L = _trace(n, G, 33)
+    t_end, accepted, live_counts = sched.dp_protocol(L, cap, target, sched.SHORT, 2)
+    states, cut, errs = [None, None], [0, 0], []
+    out = [None, None]
+
+    def run_group(fn):
+        g = rp.LocalGroup(2, 1)
+        bar = threading.Barrier(2)
+
+        def th(r):
+            import torch
+            torch.cuda.set_device(0)
+            e = None
+            try:
+                e = engine(tiny, 4, rank=r, world=2, local_group=g)
+                bar.wait(300)
+                fn(e, r)
+                bar.wait(300)
+            except BaseException as ex:
+                errs.append(repr(ex))
+                bar.abort()
+            finally:
+                if e is not None:
+                    e.close()
+
+        ts = [threading.Thread(target=th, args=(r,), daemon=True) for r in range(2)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(600)
+        g.close()
+        assert not errs, errs
+
+    def first(e, r):
+        e.submit(ps, G, cap, target, trace=L, round_id=rid)
+        st = e.step(40)
+        cut[r] = st.t
+        states[r] = e.export_round()
+
+    def second(e, r):
+        e.debug_trace_enable(t_end + 8)
+        e.import_round(states[r], ps, G, cap, target, trace=L, round_id=rid)
+        st = e.run()
+        out[r] = (st.t, st.accepted, e.debug_trace(t_end + 8, start=cut[r] + 1), e.collect())
+
+    run_group(first)
+    assert cut[0] == cut[1] and cut[0] < t_end - 10
+    run_group(second)
+    res_all = []
+    for r in range(2):
+        t2, acc, got, res = out[r]
+        assert t2 == t_end and acc == len(accepted)
+        for x in got:
+            assert len(x["live"]) == live_counts[x["t"] - 1][r], (r, x["t"])
+        res_all += res
+        for x in res:
+            i = x["prompt_id"] - ps[0]["prompt_id"]
+            assert x["len"] == L[i, x["j"]]
+    assert sorted(set(x["prompt_id"] - ps[0]["prompt_id"] for x in res_all)) == sorted(accepted)
