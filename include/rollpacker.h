@@ -270,6 +270,18 @@ int rp_round_export(void* ctx, void* buf, int64_t bytes);
 int rp_round_import(void* ctx, const rp_prompt* prompts, int32_t n_prompts, int32_t G, int32_t keep, int32_t cap,
                     int32_t target, int32_t flags, int64_t round_id, const void* buf, int64_t bytes);
 
+/* Re-shard the exported states of all W ranks of a DP job (rank order) to
+ * new_world ranks, for rp_round_import into contexts of that world: the
+ * rollout GPU set shrinks (or grows) mid-round (NEXT-3; Z27).
+ * Host only (no context).  Prompts are re-split contiguously by global
+ * index, each prompt's state moves whole; the next step's inputs are rebuilt
+ * from the live responses in slot order (one attention item per row); the
+ * local acceptance order is (completion step, index).  out == NULL returns
+ * the state size in *need.  RP_EINVAL: mismatched / unsupported states
+ * (done, paused, preempted), slice too large for the engine sizes. */
+int rp_round_reshard(const void* const* states, const int64_t* bytes, int32_t n_states, int32_t n_prompts,
+                     int32_t new_world, int32_t new_rank, void* out, int64_t out_bytes, int64_t* need);
+
 /* Continuous issuance (DAPO integration:
  * "set a maximum number of active requests for each LLM instance and
  * continuously issue new requests"; readings Z21).  Applies to the rounds

@@ -763,7 +763,8 @@ static int bucket_for(const RpCtx* c, int n) {
 // the per-row kernel below (profiles/r02_attn_group_ab.txt).  The device flag
 // tells ctl to keep building the group list while a group-mode graph runs.
 static int set_gmode(RpCtx* c) {
-  const bool mode = c->R.attn_group && c->h_ctl->n_live > c->R.group_rows_min;
+  // (an imported / re-sharded step carries no group list: n_gitems == 0)
+  const bool mode = c->R.attn_group && c->h_ctl->n_live > c->R.group_rows_min && c->h_ctl->n_gitems > 0;
   if ((int)mode != c->gmode_last) {
     *c->gmode_h = mode ? 1 : 0;
     CK(cudaMemcpyAsync(c->gmode_dev, c->gmode_h, sizeof(int), cudaMemcpyHostToDevice, c->st));
@@ -1877,6 +1878,144 @@ int rp_round_import(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   CK(cudaStreamSynchronize(c->st));
   c->step_logits_valid = false;
   c->graph_dirty = true;
+  return RP_OK;
+}
+
+// Re-shard exported DP rank states to another world size (the rollout GPU
+// set shrinks or grows mid-round, Z27).  The prompts are split contiguously by
+// global index on both sides (as rp_submit_round does), so every prompt's
+// per-response and per-prompt state moves whole; the next step's inputs are
+// rebuilt from the live responses in slot order with one attention item per
+// row (ctl re-balances the splits from the step after), the local acceptance
+// order is the accepted prompts ordered by (completion step, index) -- the
+// order the cutoff admitted them in -- and the measurement counters land on
+// the new rank 0.
+static std::vector<size_t> state_sizes(int64_t S, int64_t P, int64_t cap, int64_t MI) {
+  return {sizeof(CtlBlock), (size_t)S * 4, (size_t)S * 4, (size_t)S * 4, (size_t)S * 4, (size_t)MI * sizeof(AttnItem),
+          (size_t)MI * sizeof(AttnGroupItem), (size_t)S * 4, (size_t)S * 4, (size_t)S * 4, (size_t)S * 4,
+          (size_t)S * cap * 4, (size_t)P * 4, (size_t)P * 4, (size_t)P * 4, (size_t)(S + 1) * 8};
+}
+
+int rp_round_reshard(const void* const* states, const int64_t* bytes, int32_t n_states, int32_t n_prompts,
+                     int32_t new_world, int32_t new_rank, void* out, int64_t out_bytes, int64_t* need) {
+  auto bad = [](const char* m) { g_init_err = m; return RP_EINVAL; };
+  if (!states || !bytes || n_states < 1 || new_world < 1 || new_rank < 0 || new_rank >= new_world || n_prompts < 1)
+    return bad("round reshard: invalid arguments");
+  const int64_t* h0 = (const int64_t*)states[0];
+  if (bytes[0] < kStateHdr * 8 || h0[0] != kStateMagic) return bad("round reshard: not a round state");
+  const int64_t S = h0[1], P = h0[2], cap = h0[3], MI = h0[4], G = h0[6], kind = h0[8], keep = h0[9];
+  if (h0[5] != (int64_t)sizeof(CtlBlock)) return bad("round reshard: state from another library version");
+  const std::vector<size_t> sz = state_sizes(S, P, cap, MI);
+  size_t total = kStateHdr * 8;
+  for (size_t x : sz) total += x;
+  if (need) *need = (int64_t)total;
+  if (!out) return RP_OK;
+  if (out_bytes < (int64_t)total) return bad("round reshard: output buffer too small");
+  if (h0[10] != n_states) return bad("round reshard: need one state per old rank");
+  auto part = [&](int world, int r, int& lo, int& nl) {
+    const int base = n_prompts / world, extra = n_prompts % world;
+    lo = r * base + std::min(r, extra);
+    nl = base + (r < extra ? 1 : 0);
+  };
+  // section pointers of every old rank
+  std::vector<std::vector<const uint8_t*>> sec(n_states);
+  for (int r = 0; r < n_states; ++r) {
+    const int64_t* h = (const int64_t*)states[r];
+    if (bytes[r] != (int64_t)total || h[0] != kStateMagic || h[1] != S || h[2] != P || h[3] != cap || h[4] != MI ||
+        h[6] != G || h[10] != n_states || h[11] != 1 || h[12] != r)
+      return bad("round reshard: states of different shapes or ranks");
+    int lo, nl;
+    part(n_states, r, lo, nl);
+    if (h[7] != nl) return bad("round reshard: state slice does not match n_prompts");
+    const CtlBlock& cb = *(const CtlBlock*)((const uint8_t*)states[r] + kStateHdr * 8);
+    if (cb.done || cb.pause || cb.wait_head != cb.wait_tail || cb.preemptions)
+      return bad("round reshard: done, paused or preempted rounds are not supported");
+    size_t off = kStateHdr * 8;
+    for (size_t x : sz) { sec[r].push_back((const uint8_t*)states[r] + off); off += x; }
+  }
+  int nlo, nn;
+  part(new_world, new_rank, nlo, nn);
+  if ((int64_t)nn > P || (int64_t)nn * G > S) return bad("round reshard: the new slice exceeds max_prompts / max_seqs");
+  std::vector<uint8_t> buf(total, 0);
+  int64_t* ho = (int64_t*)buf.data();
+  const int64_t hv[kStateHdr] = {kStateMagic, S, P, cap, MI, (int64_t)sizeof(CtlBlock), G, nn, kind, keep,
+                                 new_world, 1, new_rank};
+  for (int i = 0; i < kStateHdr; ++i) ho[i] = hv[i];
+  std::vector<uint8_t*> o;
+  {
+    size_t off = kStateHdr * 8;
+    for (size_t x : sz) { o.push_back(buf.data() + off); off += x; }
+  }
+  auto I32 = [](const uint8_t* p) { return (const int*)p; };
+  auto O32 = [](uint8_t* p) { return (int*)p; };
+  struct Acc { int step, gidx, nli; };
+  std::vector<Acc> acc;
+  for (int nli = 0; nli < nn; ++nli) {
+    const int gi = nlo + nli;
+    int r = 0, lo = 0, nl = 0;
+    for (r = 0; r < n_states; ++r) {
+      part(n_states, r, lo, nl);
+      if (gi < lo + nl) break;
+    }
+    const int li = gi - lo;
+    O32(o[12])[nli] = I32(sec[r][12])[li];
+    O32(o[13])[nli] = I32(sec[r][13])[li];
+    std::vector<int> fin;
+    int t0 = 0;
+    for (int j = 0; j < G; ++j) {
+      const int os = li * (int)G + j, ns = nli * (int)G + j;
+      for (int k : {7, 8, 9, 10}) O32(o[k])[ns] = I32(sec[r][k])[os];
+      memcpy(o[11] + (size_t)ns * cap * 4, sec[r][11] + (size_t)os * cap * 4, (size_t)cap * 4);
+      const int st = I32(sec[r][9])[os];
+      t0 = I32(sec[r][10])[os];
+      if (st == ST_FINISHED || st == ST_CAPPED || st == ST_DROPPED) fin.push_back(I32(sec[r][8])[os]);
+    }
+    if (O32(o[12])[nli] == PS_ACCEPTED) {
+      std::sort(fin.begin(), fin.end());
+      const int k = (int)std::min<int64_t>(keep, (int64_t)fin.size());
+      acc.push_back({t0 + (k > 0 ? fin[k - 1] : 0), gi, nli});
+    }
+  }
+  std::sort(acc.begin(), acc.end(), [](const Acc& a, const Acc& b) {
+    return a.step != b.step ? a.step < b.step : a.gidx < b.gidx;
+  });
+  for (size_t k = 0; k < acc.size(); ++k) O32(o[14])[k] = acc[k].nli;
+  // next-step inputs: the live responses in slot order
+  int n_live = 0;
+  long long ctx_sum = 0;
+  AttnItem* items = (AttnItem*)o[5];
+  for (int ns = 0; ns < nn * (int)G; ++ns) {
+    if (O32(o[9])[ns] != ST_LIVE) continue;
+    const int kv = O32(o[7])[ns], g = O32(o[8])[ns];
+    O32(o[1])[n_live] = ns;
+    O32(o[2])[n_live] = I32(o[11] + (size_t)ns * cap * 4)[g - 1];
+    O32(o[3])[n_live] = kv;
+    O32(o[4])[n_live] = ns;
+    AttnItem I;
+    I.q_row0 = n_live; I.n_qtok = 1; I.pos0 = kv; I.pt_row = ns;
+    I.kv_lo = 0; I.kv_hi = kv + 1; I.nsplit = 1; I.item0 = n_live;
+    items[n_live] = I;
+    ctx_sum += kv + 1;
+    ++n_live;
+  }
+  CtlBlock cb = *(const CtlBlock*)sec[0][0];     // global fields: t, acc, ...
+  long long decoded = 0, kv_read = 0;
+  std::vector<unsigned long long> hist(S + 1, 0);
+  for (int r = 0; r < n_states; ++r) {
+    const CtlBlock& x = *(const CtlBlock*)sec[r][0];
+    decoded += x.decoded;
+    kv_read += x.kv_read;
+    const unsigned long long* hx = (const unsigned long long*)sec[r][15];
+    for (int64_t i = 0; i <= S; ++i) hist[i] += hx[i];
+  }
+  cb.n_live = n_live; cb.n_next = n_live; cb.n_items = n_live; cb.n_gitems = 0; cb.ctx_sum = ctx_sum;
+  cb.acc_local = (int)acc.size(); cb.n_issued = nn; cb.issue_n = 0; cb.k_step = 0; cb.need_pages = 0;
+  cb.decoded = new_rank == 0 ? decoded : 0;
+  cb.kv_read = new_rank == 0 ? kv_read : 0;
+  cb.err = 0; cb.underfilled = 0; cb.n_rejobs = 0; cb.readmit_n = cb.readmit_rows = cb.readmit_pages = 0;
+  memcpy(o[0], &cb, sizeof(CtlBlock));
+  if (new_rank == 0) memcpy(o[15], hist.data(), (size_t)(S + 1) * 8);
+  memcpy(out, buf.data(), total);
   return RP_OK;
 }
 

@@ -68,7 +68,8 @@ EXPORTS = ["rp_query_sizes", "rp_init_model", "rp_submit_round", "rp_step", "rp_
            "rp_debug_trace_get", "rp_debug_last_logits", "rp_debug_gemm", "rp_debug_profile", "rp_nccl_unique_id",
            "rp_tp_ipc_handle", "rp_tp_ipc_open", "rp_collect_ready", "rp_round_rows_histogram",
            "rp_round_issue_cap", "rp_round_unissued", "rp_plan_round", "rp_long_queue_pop",
-           "rp_local_group_create", "rp_local_group_free", "rp_plan_tp", "rp_round_state_bytes", "rp_round_export", "rp_round_import"]
+           "rp_local_group_create", "rp_local_group_free", "rp_plan_tp", "rp_round_state_bytes", "rp_round_export", "rp_round_import",
+           "rp_round_reshard"]
 
 
 def load_library(path=LIB_PATH):
@@ -104,6 +105,8 @@ def load_library(path=LIB_PATH):
     lib.rp_round_state_bytes.argtypes = [P, ctypes.POINTER(I64)]
     lib.rp_round_export.argtypes = [P, P, I64]
     lib.rp_round_import.argtypes = [P, ctypes.POINTER(Prompt), I32, I32, I32, I32, I32, I32, I64, P, I64]
+    lib.rp_round_reshard.argtypes = [ctypes.POINTER(P), ctypes.POINTER(I64), I32, I32, I32, I32, P, I64,
+                                     ctypes.POINTER(I64)]
     lib.rp_round_issue_cap.argtypes = [P, I32]
     lib.rp_round_unissued.argtypes = [P, ctypes.POINTER(I32), I32, ctypes.POINTER(I32)]
     lib.rp_collect_ready.argtypes = [P, I32, ctypes.POINTER(Response), I32, ctypes.POINTER(I32), I64,
@@ -182,6 +185,29 @@ def model_desc(cfg, weight_seed=0):
     return ModelDesc(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"],
                      cfg["d_ff"], cfg["vocab"], cfg["eos_id"], cfg.get("qkv_bias", 1), cfg["rope_theta"],
                      cfg["rms_eps"], weight_seed)
+
+
+def reshard_round_states(states, n_prompts, new_world):
+    """Exported states of every rank of a DP job (rank order) -> the states of
+    new_world ranks (rp_round_reshard), for Engine.import_round."""
+    L = lib()
+    n = len(states)
+    bufs = [ctypes.create_string_buffer(bytes(s), len(s)) for s in states]
+    ptrs = (ctypes.c_void_p * n)(*[ctypes.cast(b, ctypes.c_void_p) for b in bufs])
+    sizes = (ctypes.c_int64 * n)(*[len(s) for s in states])
+    need = ctypes.c_int64()
+    rc = L.rp_round_reshard(ptrs, sizes, n, n_prompts, new_world, 0, None, 0, ctypes.byref(need))
+    if rc != RP_OK:
+        raise RPError(rc, L.rp_last_error(None).decode())
+    out = []
+    for r in range(new_world):
+        buf = ctypes.create_string_buffer(need.value)
+        rc = L.rp_round_reshard(ptrs, sizes, n, n_prompts, new_world, r, ctypes.cast(buf, ctypes.c_void_p),
+                                need.value, ctypes.byref(need))
+        if rc != RP_OK:
+            raise RPError(rc, L.rp_last_error(None).decode())
+        out.append(buf.raw)
+    return out
 
 
 class Engine:

@@ -202,3 +202,91 @@ def test_migrate_dp_round_local_group(tiny):
             i = x["prompt_id"] - ps[0]["prompt_id"]
             assert x["len"] == L[i, x["j"]]
     assert sorted(set(x["prompt_id"] - ps[0]["prompt_id"] for x in res_all)) == sorted(accepted)
+
+
+@pytest.mark.parametrize("w_from,w_to", [(2, 1), (1, 2)])
+def test_migrate_dp_reshard(tiny, w_from, w_to):
+    """The rollout GPU set shrinks (DP 2 -> 1) or grows (1 -> 2) mid-round: the
+    ranks' exported states are re-sharded (rp_round_reshard) and imported into
+    contexts of the new world (single-GPU local groups); the schedule after
+    the cut is the oracle's (world-invariant, Z1): per-rank live counts from
+    sched.dp_protocol at the new world, t_end, the accepted set, lengths, and
+    the tokens vs the oracle's Gumbel argmax (gap rule)."""
+    import threading
+    from paper_2509_21009_b200 import rp
+    n, G, cap, target, rid = 8, 3, 250, 6, 5
+    ps = gen.prompts(n, 0, tiny["eos_id"], (5, 100), 81)
+    L = _trace(n, G, 44)
+    t_end, accepted, live_new = sched.dp_protocol(L, cap, target, sched.SHORT, w_to)
+    ref = sched.closed_form(L, cap, target, sched.SHORT, with_steps=True)
+    assert ref.t_end == t_end and sorted(ref.accepted) == sorted(accepted)
+    errs = []
+
+    def run_group(world, fn):
+        g = rp.LocalGroup(world, 1) if world > 1 else None
+        bar = threading.Barrier(world)
+
+        def th(r):
+            import torch
+            torch.cuda.set_device(0)
+            e = None
+            try:
+                kw = dict(rank=r, world=world, local_group=g) if world > 1 else {}
+                e = engine(tiny, 4, **kw)
+                bar.wait(300)
+                fn(e, r)
+                bar.wait(300)
+            except BaseException as ex:
+                errs.append(repr(ex))
+                bar.abort()
+            finally:
+                if e is not None:
+                    e.close()
+
+        ts = [threading.Thread(target=th, args=(r,), daemon=True) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(600)
+        if g is not None:
+            g.close()
+        assert not errs, errs
+
+    states, cut = [None] * w_from, [0] * w_from
+
+    def first(e, r):
+        e.submit(ps, G, cap, target, trace=L, round_id=rid)
+        cut[r] = e.step(40).t
+        states[r] = e.export_round()
+
+    run_group(w_from, first)
+    assert len(set(cut)) == 1 and cut[0] < t_end - 10
+    new_states = rp.reshard_round_states(states, n, w_to)
+    out = [None] * w_to
+
+    def second(e, r):
+        e.debug_trace_enable(t_end + 8)
+        e.import_round(new_states[r], ps, G, cap, target, trace=L, round_id=rid)
+        st = e.run()
+        out[r] = (st.t, st.accepted, e.debug_trace(t_end + 8, start=cut[0] + 1), e.collect())
+
+    run_group(w_to, second)
+    res_all = []
+    for r in range(w_to):
+        t2, acc, got, res = out[r]
+        assert t2 == t_end and acc == len(accepted)
+        assert len(got) == t_end - cut[0]
+        for x in got:
+            assert len(x["live"]) == live_new[x["t"] - 1][r], (r, x["t"])
+            if w_to == 1:
+                assert np.array_equal(x["live"], ref.steps[x["t"] - 1]["live"]), x["t"]
+        res_all += res
+        for x in res:
+            i = x["prompt_id"] - ps[0]["prompt_id"]
+            assert x["len"] == L[i, x["j"]]
+    got_acc = [x["prompt_id"] - ps[0]["prompt_id"] for x in res_all]
+    assert sorted(set(got_acc)) == sorted(accepted)
+    if w_to == 1:
+        assert list(dict.fromkeys(got_acc)) == ref.accepted       # acceptance order restored
+    checked, mism = _check_tokens(tiny, res_all, ps, L, G, rid)
+    assert checked > 300 and mism <= max(1, checked // 50)
