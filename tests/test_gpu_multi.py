@@ -31,7 +31,8 @@ def _port():
 
 @pytest.mark.parametrize("script,marker,ngpu", [("test_gpu_dp.py", "DP PARITY PASS", 2),
                                                ("test_gpu_tp.py", "TP PARITY PASS", 2),
-                                               ("test_gpu_dpxtp.py", "DPxTP PARITY PASS", 4)])
+                                               ("test_gpu_dpxtp.py", "DPxTP PARITY PASS", 4),
+                                               ("test_gpu_migrate_nccl.py", "MIGRATE NCCL PASS", 2)])
 def test_multi_gpu_parity(script, marker, ngpu):
     if _ngpus() < ngpu:
         pytest.skip("needs %d GPUs" % ngpu)
