@@ -759,8 +759,8 @@ static int bucket_for(const RpCtx* c, int n) {
 
 // Decode attention of the next steps: the sibling-group kernel while the
 // live batch exceeds group_rows_min (wide steps: siblings mostly alive, the
-// shared prompt pages dominate the reads; 49 vs 94 us per layer at 256 rows),
-// the per-row kernel below (profiles/r02_attn_group_ab.txt).  The device flag
+// shared prompt pages dominate the reads; 45 vs 67 us per layer at the
+// bench's 255-row steps), the per-row kernel below (profiles/r02_attn_group_ab.txt).  The device flag
 // tells ctl to keep building the group list while a group-mode graph runs.
 static int set_gmode(RpCtx* c) {
   // (an imported / re-sharded step carries no group list: n_gitems == 0)
@@ -878,7 +878,10 @@ static int init_impl(RpCtx* c) {
   // (profiles/r02_attn_group_ab.txt)
   c->ag_dbg = getenv("RP_AG_DBG") ? atoi(getenv("RP_AG_DBG")) : 0;
   c->R.attn_group = c->fuse_qkv || m.H / m.KV > 8 ? 0 : (getenv("RP_ATTN_GROUP") ? atoi(getenv("RP_ATTN_GROUP")) : 1);
-  c->R.group_rows_min = getenv("RP_ATTN_GROUP_MIN") ? atoi(getenv("RP_ATTN_GROUP_MIN")) : 128;
+  // the group kernel wins on the bench's own live sets only while nearly
+  // every sibling is alive and the private tails are short (above ~200 of
+  // 256 rows; tools/attn_window_ab.py, profiles/r02_attn_group_ab.txt)
+  c->R.group_rows_min = getenv("RP_ATTN_GROUP_MIN") ? atoi(getenv("RP_ATTN_GROUP_MIN")) : 200;
   // producers skip the residuals nobody reads; plans without one map hi only
   if (!(c->lo_mask & (LO_QKV | LO_GU))) c->h_lo = nullptr;
   if (!(c->lo_mask & LO_O)) c->att_lo = nullptr;

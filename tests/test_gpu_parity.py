@@ -503,7 +503,7 @@ def test_decode_long_context_split_kv(tiny, oracle_w):
 def test_decode_attention_sibling_groups(model, G, mode, monkeypatch):
     """Decode attention over sibling groups (k_attn_group.cu, RP_ATTN_GROUP:
     1 'auto', 2 forced sibling groups, 3 forced single rows; by default it
-    runs only above 128 live rows) and the per-row kernel (0, k_attn.cu):
+    runs only above 200 live rows) and the per-row kernel (0, k_attn.cu):
     logits of eager decode steps vs
     the oracle teacher-forced on the GPU's own history, for groups of 1-8
     members (rep 4 / 2 / 1 warps per member pair), a G = 10 prompt split into
