@@ -64,7 +64,7 @@ struct QueuedPrompt {
 };
 
 struct Sizes {
-  int S, P, maxp, Tcap, max_items_dec, max_items_pre, pt_rows;
+  int S, P, maxp, Tcap, max_items_dec, max_items_pre, pt_rows, max_items_g;
   size_t part_floats, apart_floats;
 };
 
@@ -168,6 +168,8 @@ struct RpCtx {
   float *qkv = nullptr, *logits = nullptr, *gpart = nullptr, *apart = nullptr;
   int* gctr = nullptr;
   int* atickets = nullptr;
+  float* rowpart = nullptr;   // group attention: member-row split partials (attn_group 4)
+  int* rtickets = nullptr;
   double* inv_freq = nullptr;
   float2* rope_cs = nullptr;    // [pos][hd/2] (cos, sin) of pos * theta^(-2i/hd), from fp64
   AttnItem *items_pre = nullptr;
@@ -293,6 +295,8 @@ static Sizes compute_sizes(const rp_model_desc* md, const rp_runtime_desc* rd) {
   const int units_env = getenv("RP_ATTN_UNITS") ? atoi(getenv("RP_ATTN_UNITS")) : 0;
   const int U1max = std::max(std::max(1, 148 / std::max(1, kv_loc)), units_env);
   z.max_items_dec = z.S + 3 * U1max;
+  // sibling-group list: group units + per-row private units (attn_group 4) + splits
+  z.max_items_g = 2 * z.S + 3 * U1max;
   z.max_items_pre = rd->max_prompt_tokens * ((rd->max_prompt_len + kAttnChunk - 1) / kAttnChunk) + z.P;
   // split-K partials: worst GEMM at the decode sizes
   const ModelDims lm = local_dims(md, rd);
@@ -372,7 +376,9 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
   auto invf = cv.take<double>(hd / 2);
   auto rope_cs = cv.take<float2>((size_t)(rd->max_prompt_len + rd->max_cap + 2) * (hd / 2));
   auto items_dec = cv.take<AttnItem>(z.max_items_dec);
-  auto gitems_dec = cv.take<AttnGroupItem>(z.max_items_dec);   // sibling-group list (RoundDev.attn_group)
+  auto gitems_dec = cv.take<AttnGroupItem>(z.max_items_g);   // sibling-group list (RoundDev.attn_group)
+  auto rowpart = cv.take<float>((size_t)z.S * KV * kRowSplits * (attn_group_partial_floats(hd) / 8));
+  auto rtick = cv.take<int>((size_t)z.S * KV);
   auto gmode = cv.take<int>(1);
   auto grp_key = cv.take<int>(z.S);
   auto grp_start = cv.take<int>((size_t)z.S + 1);
@@ -448,7 +454,8 @@ static size_t workspace_bytes(const rp_model_desc* md, const rp_runtime_desc* rd
     R.p_plen = p_plen; R.p_adm = p_adm; R.p_wait = p_wait; R.p_live = p_live; R.p_pfree = p_pfree;
     R.p_pneed = p_pneed; R.wait_q = wait_q; R.rejobs = rejobs;
     R.grp_key = grp_key; R.grp_start = grp_start;
-    R.best = best; R.items = items_dec; R.gitems = gitems_dec; R.gmode = gmode; c->gmode_dev = gmode; R.rows_hist = rows_hist; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
+    R.best = best; R.items = items_dec; R.gitems = gitems_dec; R.gmode = gmode; c->gmode_dev = gmode;
+    R.max_items_g = z.max_items_g; c->rowpart = rowpart; c->rtickets = rtick; R.rows_hist = rows_hist; R.free_stack = free_stack; R.ks_local = ks_local; R.ks = ks;
     R.ctl = ctl; R.cap = rd->max_cap;
   }
   return align_up(cv.off);
@@ -661,7 +668,7 @@ static void forward_layers(RpCtx* c, const int* tok, const int* n_dev, int n_hos
       } else if (decode && c->cur_gmode) {
         launch_attention_group(c->kv_map, c->q, c->q_lo, c->R.page_table, c->R.maxp, c->R.gitems,
                                &c->R.ctl->n_gitems, c->att, c->att_lo, c->apart, c->atickets, m, l, c->st, c->ag_dbg,
-                               c->lg ? 0 : 1);
+                               c->lg ? 0 : 1, c->rowpart, c->rtickets);
       } else {
         fz.dbg = c->ag_dbg;
         launch_attention(c->kv_map, c->q, c->R.page_table, c->R.maxp, items, n_items_dev, n_items_host, c->att,
@@ -992,6 +999,7 @@ static int init_impl(RpCtx* c) {
   CK(cudaMemsetAsync(c->gctr, 0, (1 << 16) * sizeof(int), c->st));
   CK(cudaMemsetAsync(c->atickets, 0, (size_t)std::max(c->z.max_items_dec, c->z.max_items_pre) * KV * sizeof(int),
                      c->st));
+  CK(cudaMemsetAsync(c->rtickets, 0, (size_t)c->z.S * KV * sizeof(int), c->st));
 
   // ---- identity free list (page ids 0..n_pages-1)
   {
@@ -1751,7 +1759,7 @@ static std::vector<StateSec> round_sections(RpCtx* c) {
   const size_t S = c->z.S, P = c->z.P, MI = c->z.max_items_dec;
   return {{R.ctl, sizeof(CtlBlock)},       {R.live, S * 4},           {R.tok_in, S * 4},
           {R.row_pos, S * 4},              {R.row_pt, S * 4},         {R.items, MI * sizeof(AttnItem)},
-          {R.gitems, MI * sizeof(AttnGroupItem)}, {R.kv_len, S * 4}, {R.gen, S * 4},
+          {R.gitems, (size_t)c->z.max_items_g * sizeof(AttnGroupItem)}, {R.kv_len, S * 4}, {R.gen, S * 4},
           {R.status, S * 4},               {R.t0, S * 4},             {R.tok_out, S * (size_t)R.cap * 4},
           {R.p_state, P * 4},              {R.p_cnt, P * 4},          {R.accept_order, P * 4},
           {R.rows_hist, (S + 1) * 8}};
@@ -1895,7 +1903,8 @@ int rp_round_import(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
 // the new rank 0.
 static std::vector<size_t> state_sizes(int64_t S, int64_t P, int64_t cap, int64_t MI) {
   return {sizeof(CtlBlock), (size_t)S * 4, (size_t)S * 4, (size_t)S * 4, (size_t)S * 4, (size_t)MI * sizeof(AttnItem),
-          (size_t)MI * sizeof(AttnGroupItem), (size_t)S * 4, (size_t)S * 4, (size_t)S * 4, (size_t)S * 4,
+          (size_t)(S + MI) * sizeof(AttnGroupItem),   // max_items_g = 2 S + 3 U1 = S + max_items_dec
+          (size_t)S * 4, (size_t)S * 4, (size_t)S * 4, (size_t)S * 4,
           (size_t)S * cap * 4, (size_t)P * 4, (size_t)P * 4, (size_t)P * 4, (size_t)(S + 1) * 8};
 }
 

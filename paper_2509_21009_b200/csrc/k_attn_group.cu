@@ -182,7 +182,8 @@ attn_group_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __res
                   const act_t* __restrict__ q_lo, const int* __restrict__ page_table, int maxp,
                   const AttnGroupItem* __restrict__ items, const int* __restrict__ n_items_dev,
                   act_t* __restrict__ out, act_t* __restrict__ out_lo, float* __restrict__ partial,
-                  int* __restrict__ tickets, ModelDims m, int layer, int dbg, int may_spin) {
+                  int* __restrict__ tickets, ModelDims m, int layer, int dbg, int may_spin,
+                  float* __restrict__ rowpart, int* __restrict__ rtickets) {
   using C = AgCfg<HD>;
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
@@ -367,7 +368,18 @@ attn_group_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __res
         const float* orow = wk + 16 + r * C::OST + d4;
         acc.x += orow[0] * f; acc.y += orow[1] * f; acc.z += orow[2] * f; acc.w += orow[3] * f;
       }
-      if (nsplit == 1) {
+      if (I->rowmerge) {
+        if (I->nspl[xe] == 1) {
+          const float inv = L > 0.f ? 1.f / L : 0.f;
+          acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+          const size_t oo = ((size_t)I->q_row[xe] * m.H + kvh * g + r) * HD + d4;
+          store_act4(out + oo, out_lo ? out_lo + oo : nullptr, acc);
+        } else {
+          float* pm = rowpart + (((size_t)I->q_row[xe] * m.KV + kvh) * kRowSplits + I->sidx[xe]) * C::MB;
+          if (d4 == 0) { pm[r] = M; pm[8 + r] = L; }
+          *(float4*)(pm + 16 + r * HD + d4) = acc;
+        }
+      } else if (nsplit == 1) {
         const float inv = L > 0.f ? 1.f / L : 0.f;
         acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
         const size_t oo = ((size_t)I->q_row[xe] * m.H + kvh * g + r) * HD + d4;
@@ -378,7 +390,32 @@ attn_group_kernel(const __grid_constant__ CUtensorMap kv_map, const act_t* __res
         *(float4*)(pm + 16 + r * HD + d4) = acc;
       }
     }
-    if (nsplit > 1) {
+    if (I->rowmerge) {
+      // per member row: the last of its units to finish merges its partials
+      // (split order; the row's ticket resets itself)
+      __shared__ int s_lastr[8];
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"r"(AG_CW * 32) : "memory");
+      if (threadIdx.x < n_mem) {
+        const int x = threadIdx.x, ns = I->nspl[x];
+        int last = 0;
+        if (ns > 1) {
+          int* tk = rtickets + (size_t)I->q_row[x] * m.KV + kvh;
+          last = atomicAdd(tk, 1) == ns - 1;
+          if (last) *tk = 0;
+        }
+        s_lastr[x] = last;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(AG_CW * 32) : "memory");
+      for (int x = 0; x < n_mem; ++x) {
+        if (!s_lastr[x]) continue;
+        __threadfence();
+        const float* rb = rowpart + ((size_t)I->q_row[x] * m.KV + kvh) * kRowSplits * C::MB;
+        ag_merge_rows<HD>(rb - (size_t)x * C::MB, C::MB, I->nspl[x], x * g, (x + 1) * g, g, I, kvh, m, out, out_lo,
+                          wst);
+        asm volatile("bar.sync 1, %0;" ::"r"(AG_CW * 32) : "memory");
+      }
+    } else if (nsplit > 1) {
       __shared__ int s_last;
       const float* __restrict__ p0 = partial + (size_t)item0 * m.KV * 8 * C::MB + (size_t)kvh * 8 * C::MB;
       const size_t sstride = (size_t)m.KV * 8 * C::MB;
@@ -440,7 +477,7 @@ size_t attn_group_partial_floats(int hd) { return (size_t)8 * (16 + 8 * hd); }
 void launch_attention_group(const CUtensorMap& kv_map, const void* q, const void* q_lo, const int* page_table,
                             int maxp, const AttnGroupItem* items, const int* n_items_dev, void* out, void* out_lo,
                             float* partial, int* tickets, const ModelDims& m, int layer, cudaStream_t st,
-                            int dbg, int may_spin) {
+                            int dbg, int may_spin, float* rowpart, int* rtickets) {
   const dim3 grid(148);   // one wave, persistent over the flat (group item, KV head) units
   const auto* qq = (const act_t*)q;
   const auto* ql = (const act_t*)q_lo;
@@ -448,10 +485,10 @@ void launch_attention_group(const CUtensorMap& kv_map, const void* q, const void
   auto* ol = (act_t*)out_lo;
   if (m.hd == 128)
     launch_pdl(attn_group_kernel<128>, grid, dim3(AgCfg<128>::THREADS), AgCfg<128>::SMEM, st, kv_map, qq, ql,
-               page_table, maxp, items, n_items_dev, oo, ol, partial, tickets, m, layer, dbg, may_spin);
+               page_table, maxp, items, n_items_dev, oo, ol, partial, tickets, m, layer, dbg, may_spin, rowpart, rtickets);
   else
     launch_pdl(attn_group_kernel<64>, grid, dim3(AgCfg<64>::THREADS), AgCfg<64>::SMEM, st, kv_map, qq, ql,
-               page_table, maxp, items, n_items_dev, oo, ol, partial, tickets, m, layer, dbg, may_spin);
+               page_table, maxp, items, n_items_dev, oo, ol, partial, tickets, m, layer, dbg, may_spin, rowpart, rtickets);
 }
 
 }  // namespace rp

@@ -553,6 +553,109 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     }
     if (tid == 0) R.grp_start[ng] = kept;
     __syncthreads();
+    if (R.attn_group == 4) {
+      // Shared pages in group units (every member's columns, one fill per
+      // page), private pages in per-row units (8 warps page-parallel); each
+      // member row's partials (kRowSplits slots) are merged by the last of
+      // its units.  Cost in warp-pages: shared pages x members / 8, private
+      // pages / 8; splits ns = clamp(floor(c * Ug / sum c), 1, 16) per part.
+      struct GInfo { int p0, nm, snp, w[8]; };
+      auto ginfo = [&](int gi) {
+        GInfo q;
+        q.p0 = R.grp_start[gi];
+        q.nm = min(8, R.grp_start[gi + 1] - q.p0);
+        q.snp = 1 << 30;
+        for (int x = 0; x < q.nm; ++x) {
+          const int sl = R.live_next[q.p0 + x], pos = R.row_pos[q.p0 + x];
+          q.w[x] = pages_of(pos + 1);
+          q.snp = min(q.snp, min(R.own0[sl], pos / kPage));
+        }
+        return q;
+      };
+      auto parts = [&](const GInfo& q, int ug, long long csum, int& ns_s, int& ch_s, int* ns_p, int* ch_p) {
+        const int c_s = (q.snp * q.nm + 7) / 8;
+        int want = ug > 0 ? (int)max(1LL, min(16LL, (long long)c_s * ug / csum)) : 1;
+        ns_s = 0; ch_s = 1;
+        if (q.snp > 0) { ch_s = (q.snp + want - 1) / want; ns_s = (q.snp + ch_s - 1) / ch_s; }
+        int units = ns_s;
+        for (int x = 0; x < q.nm; ++x) {
+          const int pp = q.w[x] - q.snp;
+          ns_p[x] = 0; ch_p[x] = 1;
+          if (pp > 0) {
+            want = ug > 0 ? (int)max(1LL, min(16LL, (long long)((pp + 7) / 8) * ug / csum)) : 1;
+            ch_p[x] = (pp + want - 1) / want;
+            ns_p[x] = (pp + ch_p[x] - 1) / ch_p[x];
+          }
+          units += ns_p[x];
+        }
+        return units;
+      };
+      long long csum = 0;
+      int nbase = 0;
+      for (int base = 0; base < ng; base += CTL_THREADS) {
+        const int gi = base + tid;
+        int c = 0, nb = 0, tot;
+        if (gi < ng) {
+          const GInfo q = ginfo(gi);
+          c = (q.snp * q.nm + 7) / 8;
+          nb = q.snp > 0 ? 1 : 0;
+          for (int x = 0; x < q.nm; ++x)
+            if (q.w[x] > q.snp) { c += (q.w[x] - q.snp + 7) / 8; ++nb; }
+        }
+        block_exscan(c, &tot, scan_sm);
+        csum += tot;
+        block_exscan(nb, &tot, scan_sm);
+        nbase += tot;
+      }
+      csum = max(1LL, csum);
+      const int Ug = U1 * min(3, max(1, (nbase + U1 - 1) / U1));
+      AttnGroupItem* gitems = R.gitems;
+      int items = 0;
+      for (int base = 0; base < ng; base += CTL_THREADS) {
+        const int gi = base + tid;
+        int units = 0, ns_s = 0, ch_s = 1, ns_p[8], ch_p[8];
+        GInfo q;
+        if (gi < ng) {
+          q = ginfo(gi);
+          units = parts(q, Ug, csum, ns_s, ch_s, ns_p, ch_p);
+        }
+        int tot;
+        const int o = block_exscan(units, &tot, scan_sm);
+        if (gi < ng) {
+          int it = items + o;
+          AttnGroupItem I;
+          I.nsplit = 1; I.item0 = 0; I.rowmerge = 1; I.shared_np = q.snp;
+          for (int x = 0; x < 8; ++x) {
+            const bool m = x < q.nm;
+            I.q_row[x] = m ? q.p0 + x : 0;
+            I.pt_row[x] = m ? R.live_next[q.p0 + x] : 0;
+            I.pos0[x] = m ? R.row_pos[q.p0 + x] : -1;
+            I.nspl[x] = m ? ns_s + ns_p[x] : 1;
+          }
+          // shared units: every member
+          I.n_mem = q.nm; I.rep = 8 / q.nm;
+          for (int k = 0; k < ns_s; ++k, ++it) {
+            I.pg_lo = k * ch_s; I.pg_hi = min(q.snp, (k + 1) * ch_s);
+            for (int x = 0; x < 8; ++x) I.sidx[x] = k;
+            if (it < R.max_items_g) gitems[it] = I;
+          }
+          // private units: one member each
+          for (int x = 0; x < q.nm; ++x) {
+            AttnGroupItem J = I;
+            J.n_mem = 1; J.rep = 8;
+            J.q_row[0] = I.q_row[x]; J.pt_row[0] = I.pt_row[x]; J.pos0[0] = I.pos0[x]; J.nspl[0] = I.nspl[x];
+            for (int y = 1; y < 8; ++y) { J.q_row[y] = 0; J.pt_row[y] = 0; J.pos0[y] = -1; J.nspl[y] = 1; J.sidx[y] = 0; }
+            for (int k = 0; k < ns_p[x]; ++k, ++it) {
+              J.pg_lo = q.snp + k * ch_p[x]; J.pg_hi = min(q.w[x], q.snp + (k + 1) * ch_p[x]);
+              J.sidx[0] = ns_s + k;
+              if (it < R.max_items_g) gitems[it] = J;
+            }
+          }
+        }
+        items += tot;
+      }
+      gcnt = items;
+    } else {
     auto gcost = [&](int gi, int& w, int& nm, int& rep) {
       const int p0 = R.grp_start[gi];
       nm = min(8, R.grp_start[gi + 1] - p0);
@@ -586,7 +689,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
       if (gi < ng) {
         const int p0 = R.grp_start[gi], it0 = items + o;
         AttnGroupItem I;
-        I.n_mem = nm; I.nsplit = ns; I.item0 = it0; I.rep = rep; I.pad = 0;
+        I.n_mem = nm; I.nsplit = ns; I.item0 = it0; I.rep = rep; I.rowmerge = 0;
         int snp = 1 << 30;
         for (int x = 0; x < 8; ++x) {
           const int s = x < nm ? R.live_next[p0 + x] : 0;
@@ -598,12 +701,13 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
         I.shared_np = snp;
         for (int sp = 0; sp < ns; ++sp) {
           I.pg_lo = sp * chunk; I.pg_hi = min(w, (sp + 1) * chunk);
-          if (it0 + sp < R.max_items) gitems[it0 + sp] = I;
+          if (it0 + sp < R.max_items_g) gitems[it0 + sp] = I;
         }
       }
       items += tot;
     }
     gcnt = items;
+    }   // attn_group 1-3
   }
   for (int i = tid; i < n; i += CTL_THREADS) R.best[i] = 0ull;
   for (int i = tid; i < kept; i += CTL_THREADS) R.live[i] = R.live_next[i];
@@ -613,7 +717,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
     C->decoded += n;
     C->free_top = top - alloc;
     C->n_items = min(items, R.max_items);
-    C->n_gitems = min(gcnt, R.max_items);
+    C->n_gitems = min(gcnt, R.max_items_g);
     C->n_issued = n_is0 + nis / R.G;
     C->issue_n = 0;
     // commit the re-admissions: popped from the FIFO, newest admissions
@@ -625,7 +729,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
         R.p_adm[v] = ++C->adm_ctr;
       }
     if (nrd) C->wait_head += C->readmit_n;
-    if (items > R.max_items || gcnt > R.max_items) s_err = 3;    // unreachable by the bound S + 3 * U1; fail loudly if not
+    if (items > R.max_items || gcnt > R.max_items_g) s_err = 3;    // unreachable by the bound S + 3 * U1; fail loudly if not
     const bool done = s_acc_new >= R.target || s_next_global == 0 || s_err;
     if (R.trace_buf && t <= R.trace_steps) {
       int* tb = R.trace_buf + (size_t)(t - 1) * (2 + R.S);
@@ -639,7 +743,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
       // some rank re-admitted responses: every rank holds the next step
       // until the host recomputed their KV (rp_step, between steps)
       C->pause = 1; C->n_live_saved = kept; C->n_items_saved = min(items, R.max_items);
-      C->n_gitems_saved = min(gcnt, R.max_items);
+      C->n_gitems_saved = min(gcnt, R.max_items_g);
       C->n_live = 0; C->n_items = 0; C->n_gitems = 0; C->t = t + 1;
     } else {
       C->n_live = kept; C->t = t + 1;

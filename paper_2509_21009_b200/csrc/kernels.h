@@ -36,11 +36,14 @@ struct AttnGroupItem {
   int nsplit;       // splits of the group (1 -> outputs written directly)
   int item0;        // the group's first item (split s: partials at item0 + s)
   int rep;          // consumer warps per member: 1 (5-8 members), 2 (3-4), 4 (2), 8 (1)
-  int pad;
+  int rowmerge;     // 1: partials per member row (sidx / nspl below), merged per row (attn_group 4)
   int q_row[8];     // members' rows in q / attn_out (next-step live positions)
   int pt_row[8];    // members' page-table rows (slots)
   int pos0[8];      // members' current positions (keys <= pos0 visible)
+  int sidx[8];      // rowmerge: this unit's split index in each member row's partial list
+  int nspl[8];      // rowmerge: each member row's number of partials (1 -> written directly)
 };
+constexpr int kRowSplits = 32;   // rowmerge: partials per (row, KV head)
 
 struct CtlBlock {
   int n_live;       // rows decoded by the next step on this rank (0 => idle)
@@ -100,6 +103,7 @@ struct RoundDev {
   int* grp_start;     // [S + 1] scratch: first row of each group
   int world, rank;
   int max_items;      // capacity of `items` (ctl flags err 3 rather than overflow it)
+  int max_items_g;    // capacity of `gitems`
   int* slot_prompt; int* slot_j; int* kv_len; int* gen; int* trace_L; int* status; int* own0;
   int* t0;            // [S] step before the sequence's first token: local token index = t - t0 (0 unless issued late)
   int* p_last_tok;    // [P] last prompt token (a late-issued prompt decodes it as its first step)
@@ -186,7 +190,9 @@ void launch_attention(const CUtensorMap& kv_map, const void* q, const int* page_
 void launch_attention_group(const CUtensorMap& kv_map, const void* q, const void* q_lo, const int* page_table,
                             int maxp, const AttnGroupItem* items, const int* n_items_dev, void* out, void* out_lo,
                             float* partial, int* tickets, const ModelDims& m, int layer, cudaStream_t st,
-                            int dbg = 0, int may_spin = 1 /* 0 in single-GPU local groups */);
+                            int dbg = 0, int may_spin = 1 /* 0 in single-GPU local groups */,
+                            float* rowpart = nullptr /* [S][KV][kRowSplits] member-row partials */,
+                            int* rtickets = nullptr /* [S][KV], zero, self-resetting */);
 int attn_group_init_attrs();
 size_t attn_group_partial_floats(int hd);   // per (item, KV head)
 void launch_kv_fork(const int* jobs /*[n][3] src,dst,rows*/, int n, void* kv_pool, const ModelDims& m,

@@ -499,10 +499,11 @@ def test_decode_long_context_split_kv(tiny, oracle_w):
 
 @pytest.mark.parametrize("model", ["tiny", "tiny-kv8"])
 @pytest.mark.parametrize("G", [1, 3, 8, 10])
-@pytest.mark.parametrize("mode", ["auto", "group", "single", "rows"])
+@pytest.mark.parametrize("mode", ["auto", "group", "single", "split", "rows"])
 def test_decode_attention_sibling_groups(model, G, mode, monkeypatch):
     """Decode attention over sibling groups (k_attn_group.cu, RP_ATTN_GROUP:
-    1 'auto', 2 forced sibling groups, 3 forced single rows; by default it
+    1 'auto', 2 forced sibling groups, 3 forced single rows, 4 shared pages
+    in group units and private pages in per-row units merged per row; by default it
     runs only above 200 live rows) and the per-row kernel (0, k_attn.cu):
     logits of eager decode steps vs
     the oracle teacher-forced on the GPU's own history, for groups of 1-8
@@ -510,7 +511,7 @@ def test_decode_attention_sibling_groups(model, G, mode, monkeypatch):
     groups of 8 and 2, siblings dying mid-round (groups shrink), head_dim 64
     (g = 2) and 128 (g = 5), and ~650-token contexts cut into many page
     splits merged per member."""
-    monkeypatch.setenv("RP_ATTN_GROUP", {"auto": "1", "group": "2", "single": "3", "rows": "0"}[mode])
+    monkeypatch.setenv("RP_ATTN_GROUP", {"auto": "1", "group": "2", "single": "3", "split": "4", "rows": "0"}[mode])
     monkeypatch.setenv("RP_ATTN_GROUP_MIN", "0")          # the group kernel at every live batch
     cfg = configs.model_config(model)
     w = weights.Weights(cfg, configs.WEIGHT_SEED)
