@@ -889,6 +889,7 @@ static int init_impl(RpCtx* c) {
   // every sibling is alive and the private tails are short (above ~200 of
   // 256 rows; tools/attn_window_ab.py, profiles/r02_attn_group_ab.txt)
   c->R.group_rows_min = getenv("RP_ATTN_GROUP_MIN") ? atoi(getenv("RP_ATTN_GROUP_MIN")) : 200;
+  c->R.group_waves = getenv("RP_ATTN_GROUP_WAVES") ? std::max(1, atoi(getenv("RP_ATTN_GROUP_WAVES"))) : 1;
   // producers skip the residuals nobody reads; plans without one map hi only
   if (!(c->lo_mask & (LO_QKV | LO_GU))) c->h_lo = nullptr;
   if (!(c->lo_mask & LO_O)) c->att_lo = nullptr;

@@ -673,7 +673,7 @@ __device__ void ctl_phase_b(const RoundDev& R, int* scan_sm) {
       csum += tot;
     }
     csum = max(1LL, csum);
-    const int Ug = U1 * min(3, max(1, (ng + U1 - 1) / U1));   // whole waves (one-wave cap measured slower)
+    const int Ug = U1 * min(3, max(R.group_waves, (ng + U1 - 1) / U1));   // whole waves (one-wave cap measured slower)
     auto nsplits = [&](int c, int w, int ug, int& chunk) {
       const int want = (int)max(1LL, min(32LL, (long long)c * ug / csum));   // <= 32: the merge's smem
       chunk = (w + want - 1) / want;

@@ -97,6 +97,7 @@ struct RoundDev {
   int attn_group;     // sibling-group work list (gitems, k_attn_group.cu) besides the per-row one: 0 off;
                       // 1 sibling groups unless too few (then single rows), 2 always sibling groups, 3 always single rows
   int group_rows_min; // build gitems when the next step has more rows (or *gmode: the running graph uses them)
+  int group_waves;    // split budget of the group list: at least this many waves of units (A/B)
   const int* gmode;   // [1] 1 while the host runs decode steps with the group kernel
   AttnGroupItem* gitems;
   int* grp_key;       // [S] scratch: (prompt, j / 8) of each next-step row
