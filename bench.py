@@ -263,7 +263,10 @@ def run_ours(a):
         if profile:
             prof = e.debug_profile_read()
             e.debug_profile_arm(-1)
-            prof.update(kind=kind, hist=hist.tolist(), kv_tokens=st.kv_tokens_read, tp=e.tp)
+            # bytes: each prompt's shared pages once per step (what HBM must deliver);
+            # FLOPs: every row's full context
+            prof.update(kind=kind, hist=hist.tolist(), kv_tokens=st.kv_tokens_unique,
+                        kv_tokens_per_row=st.kv_tokens_read, tp=e.tp)
         res = e.collect()
         if W.schedule == "issue" and kind == "short":
             W.returned = allgather_ids(e.unissued()) + W.returned
@@ -271,8 +274,8 @@ def run_ours(a):
         retained = sum(r["len"] for r in res)
         decoded = st.decoded_tokens
         # algorithmic HBM bytes of this rank's decode steps (step 1 comes from the prefill)
-        hbm = step_bytes(cfg, e.tp, max(0, st.t - 1), st.decoded_tokens, st.kv_tokens_read)
-        t_roof = round_t_roof(cfg, e.tp, hist, st.decoded_tokens, st.kv_tokens_read)
+        hbm = step_bytes(cfg, e.tp, max(0, st.t - 1), st.decoded_tokens, st.kv_tokens_unique)
+        t_roof = round_t_roof(cfg, e.tp, hist, st.decoded_tokens, st.kv_tokens_unique)
         if e is not eng and rank != 0:
             # TP ranks decode the same tokens: count them once (on rank 0)
             decoded, retained, h2d, d2h = 0, 0, 0, 0
@@ -573,8 +576,9 @@ def roofline(profs, cfg):
     """Per-kernel-class roofline over whole profiled rounds (the first short
     and the first long round of the run, every decode step): algorithmic
     bytes and FLOPs summed over every launch at its live batch (device
-    histogram of rows per step) and the attention context actually read
-    (kv_tokens_read), divided by the class's summed CUDA-event time.  The
+    histogram of rows per step) and the attention context (bytes: each
+    prompt's shared pages once per step, kv_tokens_unique; FLOPs: every row's
+    context, kv_tokens_read), divided by the class's summed CUDA-event time.  The
     `roofline` object is the dominant class (largest share of the profiled
     time): bound = hbm if its launches' byte time exceeds their FLOP time at
     the peaks, achieved = algorithmic bytes (FLOPs) / time."""
@@ -587,7 +591,8 @@ def roofline(profs, cfg):
         hist = p["hist"]
         steps += sum(hist)
         rows_sum += sum(B * n for B, n in enumerate(hist))
-        ctx_sum += p["kv_tokens"]
+        kv_rows = p.get("kv_tokens_per_row", p["kv_tokens"])
+        ctx_sum += kv_rows
         for k, v in p["ms"].items():
             tot_ms[k] = tot_ms.get(k, 0.0) + v
             tot_cnt[k] = tot_cnt.get(k, 0) + p["launches"][k]
@@ -601,7 +606,7 @@ def roofline(profs, cfg):
                     t_roof[cls] = t_roof.get(cls, 0) + n * nl * max(b / (hbm * 1e9), f / (tf_sus * 1e12))
         ab = p["kv_tokens"] * L * KV * hd * 2 * 2 + sum(B * n for B, n in enumerate(hist)) * L * H * hd * 2 * 2
         by["attention"] = by.get("attention", 0) + ab
-        fl["attention"] = fl.get("attention", 0) + 4.0 * p["kv_tokens"] * L * H * hd
+        fl["attention"] = fl.get("attention", 0) + 4.0 * kv_rows * L * H * hd
         t_roof["attention"] = t_roof.get("attention", 0) + ab / (hbm * 1e9)
     total = sum(tot_ms.values())
     detail = {}

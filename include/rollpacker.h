@@ -144,6 +144,8 @@ typedef struct {
   int64_t kv_tokens_read;    /* sum over decode steps and decoded rows of the attention context
                                 (KV tokens read per layer and KV head); measurement only   */
   int32_t preemptions;       /* prompts preempted by KV pressure this round on this rank */
+  int64_t kv_tokens_unique;  /* kv_tokens_read with each prompt's shared full prompt pages counted
+                                once per step (the bytes HBM must deliver); measurement only */
 } rp_status;
 
 typedef struct {

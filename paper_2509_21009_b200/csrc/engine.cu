@@ -1426,6 +1426,7 @@ static void fill_status(RpCtx* c, rp_status* st) {
   st->accepted = b.acc; st->accepted_local = b.acc_local; st->done = b.done; st->underfilled = b.underfilled;
   st->n_prompts_local = c->n_loc; st->decoded_tokens = b.decoded;
   st->kv_tokens_read = b.kv_read;
+  st->kv_tokens_unique = b.kv_read_unique;
   st->preemptions = b.preemptions;
 }
 
@@ -2012,12 +2013,13 @@ int rp_round_reshard(const void* const* states, const int64_t* bytes, int32_t n_
     ++n_live;
   }
   CtlBlock cb = *(const CtlBlock*)sec[0][0];     // global fields: t, acc, ...
-  long long decoded = 0, kv_read = 0;
+  long long decoded = 0, kv_read = 0, kv_unique = 0;
   std::vector<unsigned long long> hist(S + 1, 0);
   for (int r = 0; r < n_states; ++r) {
     const CtlBlock& x = *(const CtlBlock*)sec[r][0];
     decoded += x.decoded;
     kv_read += x.kv_read;
+    kv_unique += x.kv_read_unique;
     const unsigned long long* hx = (const unsigned long long*)sec[r][15];
     for (int64_t i = 0; i <= S; ++i) hist[i] += hx[i];
   }
@@ -2025,6 +2027,7 @@ int rp_round_reshard(const void* const* states, const int64_t* bytes, int32_t n_
   cb.acc_local = (int)acc.size(); cb.n_issued = nn; cb.issue_n = 0; cb.k_step = 0; cb.need_pages = 0;
   cb.decoded = new_rank == 0 ? decoded : 0;
   cb.kv_read = new_rank == 0 ? kv_read : 0;
+  cb.kv_read_unique = new_rank == 0 ? kv_unique : 0;
   cb.err = 0; cb.underfilled = 0; cb.n_rejobs = 0; cb.readmit_n = cb.readmit_rows = cb.readmit_pages = 0;
   memcpy(o[0], &cb, sizeof(CtlBlock));
   if (new_rank == 0) memcpy(o[15], hist.data(), (size_t)(S + 1) * 8);

@@ -210,7 +210,7 @@ __device__ void ctl_kv_pressure(const RoundDev& R, int* scan_sm, int& s_top, int
 
 __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
   __shared__ int s_k, s_top, s_keep, s_need, s_err, s_pause;
-  __shared__ long long s_ctx, s_rd;
+  __shared__ long long s_ctx, s_rd, s_ru;
   CtlBlock* C = R.ctl;
   const int n = C->n_live;
   const int t = C->t;
@@ -233,7 +233,7 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     if (fin || (capped && R.kind == 1)) atomicAdd(&R.p_cnt[R.slot_prompt[s]], 1);
   }
   if (tid == 0) {
-    s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; s_ctx = 0; s_rd = 0; s_pause = 0;
+    s_k = 0; s_top = C->free_top; s_keep = 0; s_need = 0; s_err = 0; s_ctx = 0; s_rd = 0; s_ru = 0; s_pause = 0;
     if (appended && R.rows_hist) R.rows_hist[n] += 1;   // one decode step over n rows
   }
   __syncthreads();
@@ -287,9 +287,18 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
         }
       }
     }
-    int tot, tk, tn, tc, trd;
-    // KV tokens the attention of this step read for row i: its context incl. the appended token
+    int tot, tk, tn, tc, trd, tru;
+    // KV tokens the attention of this step read for row i: its context incl. the appended token;
+    // unique: the prompt's shared full pages once per prompt (its first live row; siblings are
+    // adjacent in the live list) + every row's private tokens
     block_exscan(i < n && appended ? R.kv_len[s] : 0, &trd, scan_sm);
+    int ru = 0;
+    if (i < n && appended) {
+      const int sh = R.own0[s] * kPage;
+      ru = R.kv_len[s] - sh;
+      if (i == 0 || R.slot_prompt[R.live[i - 1]] != R.slot_prompt[s]) ru += sh;
+    }
+    block_exscan(ru, &tru, scan_sm);
     const int off = block_exscan(cnt, &tot, scan_sm);
     block_exscan(keep, &tk, scan_sm);
     block_exscan(need, &tn, scan_sm);
@@ -297,7 +306,7 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     for (int c = 0; c < cnt; ++c)
       R.free_stack[s_top + off + c] = R.page_table[(size_t)s * R.maxp + R.own0[s] + c];
     __syncthreads();
-    if (tid == 0) { s_top += tot; s_keep += tk; s_need += tn; s_ctx += tc; s_rd += trd; }
+    if (tid == 0) { s_top += tot; s_keep += tk; s_need += tn; s_ctx += tc; s_rd += trd; s_ru += tru; }
     __syncthreads();
   }
   if (R.preempt) ctl_kv_pressure(R, scan_sm, s_top, s_keep, s_need, s_err, s_ctx, s_pause);
@@ -345,6 +354,7 @@ __device__ void ctl_phase_a(const RoundDev& R, int appended, int* scan_sm) {
     C->need_pages = s_need;
     C->ctx_sum = s_ctx;
     C->kv_read += s_rd;
+    C->kv_read_unique += s_ru;
     R.ks_local[0] = s_k; R.ks_local[1] = s_keep; R.ks_local[2] = s_err; R.ks_local[3] = s_pause;
     if (R.world == 1) { R.ks[0] = s_k; R.ks[1] = s_keep; R.ks[2] = s_err; R.ks[3] = s_pause; }
   }

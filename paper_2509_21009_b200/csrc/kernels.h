@@ -77,6 +77,7 @@ struct CtlBlock {
   int n_gitems;     // sibling-group attention items of the next step (RoundDev.gitems)
   int n_gitems_saved;
   int n_rejobs;     // recompute jobs written by phase B
+  long long kv_read_unique;  // as kv_read with each prompt's shared full pages counted once per step
 };
 
 struct RoundDev {

@@ -55,7 +55,7 @@ class Status(ctypes.Structure):
                 ("n_live", ctypes.c_int32), ("accepted", ctypes.c_int32), ("accepted_local", ctypes.c_int32),
                 ("done", ctypes.c_int32), ("underfilled", ctypes.c_int32), ("n_prompts_local", ctypes.c_int32),
                 ("decoded_tokens", ctypes.c_int64), ("kv_tokens_read", ctypes.c_int64),
-                ("preemptions", ctypes.c_int32)]
+                ("preemptions", ctypes.c_int32), ("kv_tokens_unique", ctypes.c_int64)]
 
 
 class Response(ctypes.Structure):

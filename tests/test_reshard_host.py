@@ -26,7 +26,8 @@ class Ctl(ctypes.Structure):          # kernels.h CtlBlock
                [("decoded", ctypes.c_longlong), ("ctx_sum", ctypes.c_longlong), ("kv_read", ctypes.c_longlong)] + \
                [(n, ctypes.c_int) for n in ("n_issued", "issue_n", "preemptions", "wait_head", "wait_tail", "adm_ctr",
                                              "readmit_n", "readmit_rows", "readmit_pages", "pause", "n_live_saved",
-                                             "n_items_saved", "n_gitems", "n_gitems_saved", "n_rejobs")]
+                                             "n_items_saved", "n_gitems", "n_gitems_saved", "n_rejobs")] + \
+               [("kv_read_unique", ctypes.c_longlong)]
 
 
 ITEM, GITEM = 32, 192                 # sizeof(AttnItem), sizeof(AttnGroupItem)
