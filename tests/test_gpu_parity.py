@@ -273,18 +273,6 @@ def test_continuous_issuance_schedule_bit_exact(tiny, seed, graph_steps, A, keep
     hist = eng.rows_histogram()
     want = np.bincount([len(x["live"]) for x in ref.steps[1:]], minlength=len(hist))
     assert np.array_equal(hist, want[:len(hist)])
-    # KV tokens the decode steps' attention read (measurement counters of the roofline): every row's
-    # context incl. the appended token, and with each prompt's shared full pages counted once per step
-    plen = np.array([len(p["tokens"]) for p in ps])
-    sh = (plen // 64) * 64
-    per_row = unique = 0
-    for x in ref.steps[1:]:
-        live = np.asarray(x["live"])
-        ctx = plen[live // G] + x["t"] - 1
-        per_row += int(ctx.sum())
-        unique += int((ctx - sh[live // G]).sum()) + int(sh[np.unique(live // G)].sum())
-    assert st.kv_tokens_read == per_row and st.kv_tokens_unique == unique, (st.kv_tokens_read, per_row,
-                                                                            st.kv_tokens_unique, unique)
     res = eng.collect()
     got = [(r["prompt_id"] - ps[0]["prompt_id"], r["j"], r["len"]) for r in res]
     want = [(i, j, int(ref.retained_len[i, j])) for i in ref.accepted for j in range(G) if ref.retained_len[i, j]]
