@@ -260,9 +260,10 @@ int rp_round_rows_histogram(void* ctx, int64_t* out, int32_t n);
  * tokens with the prefill kernels, so rp_step continues at the exported step
  * with the same schedule (live lists, acceptance, cutoff) and the same
  * sampling counters.  DP jobs migrate rank by rank into contexts of the
- * same world and rank (every rank imports at the same step: the re-submit
- * runs step 1's cutoff exchange); no TP contexts, no continuous issuance,
- * no prompts waiting for re-admission; the exporting context keeps
+ * same world and rank, TP groups rank by rank into groups of the same size
+ * (every rank imports at the same step: the re-submit and the recompute run
+ * the collectives); no continuous issuance, no prompts waiting for
+ * re-admission; the exporting context keeps
  * its round (collect or drop it).  Errors: RP_ESTATE (no active round / done
  * / waiting prompts), RP_ENOSPC (buffer too small), RP_EINVAL (size or header
  * mismatch, unsupported mode), RP_ENOMEM_KV (the pool cannot hold the live

@@ -1788,7 +1788,7 @@ int rp_round_export(void* ctx, void* buf, int64_t bytes) {
   if (!c) return RP_EINVAL;
   if (!buf) return c->fail(RP_EINVAL, "invalid field: buf");
   if (!c->active) return c->fail(RP_ESTATE, "no active round");
-  if (c->tp != 1) return c->fail(RP_EINVAL, "round export: tensor-parallel contexts are not supported");
+  // (a TP group's ranks hold identical round state: each exports its own copy)
   if (c->max_active) return c->fail(RP_EINVAL, "round export: continuous issuance is not supported");
   int64_t need = 0;
   rp_round_state_bytes(ctx, &need);
@@ -1822,7 +1822,8 @@ int rp_round_import(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   RpCtx* c = (RpCtx*)ctx;
   if (!c) return RP_EINVAL;
   if (!buf || !prompts) return c->fail(RP_EINVAL, "invalid field: buf / prompts");
-  if (c->tp != 1) return c->fail(RP_EINVAL, "round import: tensor-parallel contexts are not supported");
+  // (TP: every rank of the group imports at the same step -- submit and the
+  // recompute run the TP collectives)
   if (c->issue_cap > 0) return c->fail(RP_EINVAL, "round import: continuous issuance is not supported");
   if (bytes < kStateHdr * 8) return c->fail(RP_EINVAL, "round import: state of %lld bytes", (long long)bytes);
   const int64_t* hdr = (const int64_t*)buf;

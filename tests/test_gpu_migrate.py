@@ -290,3 +290,44 @@ def test_migrate_dp_reshard(tiny, w_from, w_to):
         assert list(dict.fromkeys(got_acc)) == ref.accepted       # acceptance order restored
     checked, mism = _check_tokens(tiny, res_all, ps, L, G, rid)
     assert checked > 300 and mism <= max(1, checked // 50)
+
+
+def test_migrate_tp_local_group():
+    """A TP=2 long round (the 14B attention shape at tiny width, single-GPU
+    local group) exported at step ~40 by both TP ranks and imported into a
+    fresh TP=2 group: the recompute runs through the TP prefill (all-reduced
+    partials); schedule after the cut, identical tokens on both ranks and the
+    tokens vs the oracle (gap rule)."""
+    from test_gpu_local import run_group
+    cfg = configs.model_config("tiny-kv8")
+    n, G, cap, rid = 6, 3, 200, 12
+    ps = gen.prompts(n, 0, cfg["eos_id"], (5, 80), 23)
+    L = _trace(n, G, 57, 60, 190)
+    ref = sched.closed_form(L, cap, n, sched.LONG, with_steps=True)
+
+    def first(eng, r, q, bar):
+        eng.submit(ps, G, cap, n, long_round=True, trace=L, round_id=rid)
+        st = eng.step(39)
+        return dict(t=st.t, state=eng.export_round())
+
+    got1 = run_group(1, 2, cfg, first, sample_seed=configs.SAMPLE_SEED)
+    cut = got1[0]["t"]
+    assert got1[1]["t"] == cut and got1[0]["state"] == got1[1]["state"] and cut < ref.t_end - 10
+
+    def second(eng, r, q, bar):
+        eng.debug_trace_enable(ref.t_end + 8)
+        eng.import_round(got1[q]["state"], ps, G, cap, n, long_round=True, trace=L, round_id=rid)
+        st = eng.run()
+        return dict(t=st.t, trace=eng.debug_trace(ref.t_end + 8, start=cut + 1), out=eng.collect())
+
+    got2 = run_group(1, 2, cfg, second, sample_seed=configs.SAMPLE_SEED)
+    for x in got2:
+        assert x["t"] == ref.t_end and len(x["trace"]) == ref.t_end - cut
+        for a in x["trace"]:
+            assert np.array_equal(a["live"], ref.steps[a["t"] - 1]["live"]), a["t"]
+        assert [(o["prompt_id"], o["j"], o["tokens"].tolist()) for o in x["out"]] == \
+            [(o["prompt_id"], o["j"], o["tokens"].tolist()) for o in got2[0]["out"]]
+    res = got2[0]["out"]
+    assert len(res) == n * G
+    checked, mism = _check_tokens(cfg, res, ps, L, G, rid)
+    assert checked > 500 and mism <= checked // 50
