@@ -262,8 +262,9 @@ int rp_round_rows_histogram(void* ctx, int64_t* out, int32_t n);
  * sampling counters.  DP jobs migrate rank by rank into contexts of the
  * same world and rank, TP groups rank by rank into groups of the same size
  * (every rank imports at the same step: the re-submit and the recompute run
- * the collectives); no continuous issuance, no prompts waiting for
- * re-admission; the exporting context keeps
+ * the collectives); prompts preempted by KV pressure move with their
+ * admission stamps and wait queue (re-admitted and recomputed there); not
+ * at a step a re-admission paused, no continuous issuance; the exporting context keeps
  * its round (collect or drop it).  Errors: RP_ESTATE (no active round / done
  * / waiting prompts), RP_ENOSPC (buffer too small), RP_EINVAL (size or header
  * mismatch, unsupported mode), RP_ENOMEM_KV (the pool cannot hold the live

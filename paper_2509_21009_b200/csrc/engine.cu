@@ -1764,7 +1764,8 @@ static std::vector<StateSec> round_sections(RpCtx* c) {
           {R.gitems, (size_t)c->z.max_items_g * sizeof(AttnGroupItem)}, {R.kv_len, S * 4}, {R.gen, S * 4},
           {R.status, S * 4},               {R.t0, S * 4},             {R.tok_out, S * (size_t)R.cap * 4},
           {R.p_state, P * 4},              {R.p_cnt, P * 4},          {R.accept_order, P * 4},
-          {R.rows_hist, (S + 1) * 8}};
+          {R.rows_hist, (S + 1) * 8},      {R.p_adm, P * 4},          {R.p_wait, P * 4},
+          {R.wait_q, P * 4}};
 }
 constexpr int64_t kStateMagic = 0x3153525052LL;   // "RPRS1"
 constexpr int kStateHdr = 13;                      // int64 header words
@@ -1797,8 +1798,7 @@ int rp_round_export(void* ctx, void* buf, int64_t bytes) {
   if (rc) return rc;
   const CtlBlock& b = *c->h_ctl;
   if (b.done) return c->fail(RP_ESTATE, "round export: the round is done (collect it)");
-  if (b.pause || b.wait_head != b.wait_tail)
-    return c->fail(RP_ESTATE, "round export: preempted prompts are waiting (export between re-admissions)");
+  if (b.pause) return c->fail(RP_ESTATE, "round export: a re-admission is pausing the round (step once more)");
   uint8_t* out = (uint8_t*)buf;
   state_header(c, (int64_t*)out);
   size_t off = kStateHdr * 8;
@@ -1852,8 +1852,7 @@ int rp_round_import(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   const int* ex_kv = (const int*)src[7];
   const int* ex_gen = (const int*)src[8];
   const int* ex_status = (const int*)src[9];
-  if (ex.done || ex.pause || ex.wait_head != ex.wait_tail)
-    return c->fail(RP_EINVAL, "round import: the exported round is done or has waiting prompts");
+  if (ex.done || ex.pause) return c->fail(RP_EINVAL, "round import: the exported round is done or paused");
   // after submit: step 1 decoded, private pages for positions <= plen of the live responses
   if ((rc = read_ctl(c))) return rc;
   const int S = c->z.S, maxp = c->z.maxp, nS = c->n_loc * c->G;
@@ -1866,17 +1865,24 @@ int rp_round_import(void* ctx, const rp_prompt* prompts, int32_t n, int32_t G, i
   int top = c->h_ctl->free_top;
   auto pages_of = [](int tokens) { return (tokens + kPage - 1) / kPage; };
   std::vector<RecomputeSeg> segs;
-  for (int s = 0; s < nS; ++s) {
-    const int plen = (int)c->round_prompts[s / c->G].tokens.size(), own0 = plen / kPage;
-    const int cur = st_now[s] == ST_LIVE ? pages_of(kv_now[s] + 1) - own0 : 0;
-    const int want = ex_status[s] == ST_LIVE ? pages_of(ex_kv[s] + 1) - own0 : 0;
-    for (int k = cur; k < want; ++k) {
-      if (top <= 0) { c->active = false; return c->fail(RP_ENOMEM_KV, "round import: KV pool exhausted"); }
-      ptab[(size_t)s * maxp + own0 + k] = fstack[--top];
+  // private pages: release those of responses that are no longer live (all
+  // slots first, so a tight pool is not exhausted by the order), then grow
+  // the live ones to their exported contexts
+  for (int pass = 0; pass < 2; ++pass)
+    for (int s = 0; s < nS; ++s) {
+      const int plen = (int)c->round_prompts[s / c->G].tokens.size(), own0 = plen / kPage;
+      const int cur = st_now[s] == ST_LIVE ? pages_of(kv_now[s] + 1) - own0 : 0;
+      const int want = ex_status[s] == ST_LIVE ? pages_of(ex_kv[s] + 1) - own0 : 0;
+      if (pass == 0) {
+        for (int k = want; k < cur; ++k) fstack[top++] = ptab[(size_t)s * maxp + own0 + k];
+        continue;
+      }
+      for (int k = cur; k < want; ++k) {
+        if (top <= 0) { c->active = false; return c->fail(RP_ENOMEM_KV, "round import: KV pool exhausted"); }
+        ptab[(size_t)s * maxp + own0 + k] = fstack[--top];
+      }
+      if (ex_status[s] == ST_LIVE && ex_gen[s] >= 2) segs.push_back({s, plen, 0, ex_gen[s] - 1});
     }
-    for (int k = want; k < cur; ++k) fstack[top++] = ptab[(size_t)s * maxp + own0 + k];
-    if (ex_status[s] == ST_LIVE && ex_gen[s] >= 2) segs.push_back({s, plen, 0, ex_gen[s] - 1});
-  }
   CK(idle(c));
   CK(cudaMemcpyAsync(c->R.page_table, ptab.data(), ptab.size() * 4, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->R.free_stack, fstack.data(), (size_t)top * 4, cudaMemcpyHostToDevice, c->st));
@@ -1908,7 +1914,8 @@ static std::vector<size_t> state_sizes(int64_t S, int64_t P, int64_t cap, int64_
   return {sizeof(CtlBlock), (size_t)S * 4, (size_t)S * 4, (size_t)S * 4, (size_t)S * 4, (size_t)MI * sizeof(AttnItem),
           (size_t)(S + MI) * sizeof(AttnGroupItem),   // max_items_g = 2 S + 3 U1 = S + max_items_dec
           (size_t)S * 4, (size_t)S * 4, (size_t)S * 4, (size_t)S * 4,
-          (size_t)S * cap * 4, (size_t)P * 4, (size_t)P * 4, (size_t)P * 4, (size_t)(S + 1) * 8};
+          (size_t)S * cap * 4, (size_t)P * 4, (size_t)P * 4, (size_t)P * 4, (size_t)(S + 1) * 8,
+          (size_t)P * 4, (size_t)P * 4, (size_t)P * 4};
 }
 
 int rp_round_reshard(const void* const* states, const int64_t* bytes, int32_t n_states, int32_t n_prompts,
@@ -2032,6 +2039,9 @@ int rp_round_reshard(const void* const* states, const int64_t* bytes, int32_t n_
   cb.err = 0; cb.underfilled = 0; cb.n_rejobs = 0; cb.readmit_n = cb.readmit_rows = cb.readmit_pages = 0;
   memcpy(o[0], &cb, sizeof(CtlBlock));
   if (new_rank == 0) memcpy(o[15], hist.data(), (size_t)(S + 1) * 8);
+  for (int nli = 0; nli < nn; ++nli) O32(o[16])[nli] = nli;   // admission stamps: index order (as submit)
+  cb.adm_ctr = nn - 1;
+  memcpy(o[0], &cb, sizeof(CtlBlock));
   memcpy(out, buf.data(), total);
   return RP_OK;
 }

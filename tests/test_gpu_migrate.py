@@ -331,3 +331,57 @@ def test_migrate_tp_local_group():
     assert len(res) == n * G
     checked, mism = _check_tokens(cfg, res, ps, L, G, rid)
     assert checked > 500 and mism <= checked // 50
+
+
+def test_migrate_with_waiting_preempted_prompts(tiny):
+    """KV pressure (RP_PREEMPT, NEXT-2) and migration together: a LONG round on
+    a pool too small for its contexts is exported at a step where preempted
+    prompts wait for re-admission; the importing engine (same pool size)
+    re-admits and recomputes them itself.  Live lists after the cut, t_end and
+    the preemption count follow the oracle's kv_step_loop; every response keeps
+    its trace length; tokens vs the oracle (gap rule)."""
+    import ctypes
+    from paper_2509_21009_b200 import rp
+    from test_gpu_preempt import tight_pool, page_bytes
+    from test_reshard_host import Ctl
+    n, G, cap = 6, 3, 400
+    ps = gen.prompts(n, 0, tiny["eos_id"], (5, 80), 31)
+    plen = np.array([len(p["tokens"]) for p in ps])
+    L = np.random.default_rng(5).integers(60, 260, size=(n, G)).astype(np.int64)
+    pool, ref = tight_pool(L, plen, cap, n, sched.LONG)
+    mk = lambda: rp.Engine(tiny, max_seqs=64, max_prompts=16, max_prompt_len=128, max_prompt_tokens=1024,
+                           max_cap=512, kv_pool_bytes=pool * page_bytes(tiny), graph_steps=0,
+                           sample_seed=configs.SAMPLE_SEED)
+    a = mk()
+    a.submit(ps, G, cap, n, long_round=True, trace=L, round_id=7, preempt=True)
+    state, cut = None, 0
+    while True:
+        st = a.step(1)
+        assert not st.done, "no step with waiting prompts"
+        try:
+            s = a.export_round()
+        except rp.RPError:
+            continue                                   # a re-admission paused this step
+        c = Ctl.from_buffer_copy(s[13 * 8:13 * 8 + ctypes.sizeof(Ctl)])
+        if c.wait_tail > c.wait_head:
+            state, cut = s, st.t
+            break
+    a.close()
+    b = mk()
+    b.debug_trace_enable(ref.t_end + 8)
+    b.import_round(state, ps, G, cap, n, long_round=True, trace=L, round_id=7, preempt=True)
+    st = b.run()
+    got = b.debug_trace(ref.t_end + 8, start=cut + 1)
+    res = b.collect()
+    b.close()
+    assert st.t == ref.t_end and st.preemptions == ref.preemptions[0] > 0
+    steps = [x for x in ref.steps if x["t"] > cut and len(x["live"][0])]
+    assert len(got) == len(steps)
+    for g_, w_ in zip(got, steps):
+        assert g_["t"] == w_["t"] and np.array_equal(g_["live"], w_["live"][0]), w_["t"]
+        assert g_["accepted"] == w_["accepted"] and g_["done"] == w_["done"]
+    assert len(res) == n * G
+    for r in res:
+        assert r["len"] == L[r["prompt_id"] - ps[0]["prompt_id"], r["j"]]
+    checked, mism = _check_tokens(tiny, res, ps, L, G, 7)
+    assert checked > 1000 and mism <= checked // 50

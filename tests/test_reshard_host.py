@@ -37,7 +37,7 @@ MI = S + U                            # max_items_dec; the group list holds S + 
 
 def sizes():
     return [ctypes.sizeof(Ctl), S * 4, S * 4, S * 4, S * 4, MI * ITEM, (S + MI) * GITEM, S * 4, S * 4, S * 4, S * 4,
-            S * CAP * 4, P * 4, P * 4, P * 4, (S + 1) * 8]
+            S * CAP * 4, P * 4, P * 4, P * 4, (S + 1) * 8, P * 4, P * 4, P * 4]
 
 
 def part(n, world, r):
